@@ -1,0 +1,246 @@
+/*
+ * oracle/kmc_oracle.cpp -- CPU ORACLE for canonical k-mer counting (KMC 2,
+ * arXiv 1407.1507).  TEST INFRASTRUCTURE ONLY: only tests/, the
+ * __graft_entry__.smoke() check and bench.py's cpu_baseline / --impl reference
+ * legs may load this library.  The product path (paper_1407_1507_b200/) never
+ * links, imports or calls it, and this file shares no code, header, table or
+ * helper with the CUDA path.
+ *
+ * What it computes is the PLAIN DEFINITION of the result:
+ *   - k-mer counting = "the histogram of occurrences of every k-symbol long
+ *     substring" (Abstract; Sec. 1);
+ *   - canonical k-mer = "lexicographically smaller of the pair: the k-mer and
+ *     its reverse complement" (Sec. 2.1);
+ *   - symbol codes A->0, C->1, G->2, T->3, leftmost symbol most significant
+ *     (Suppl. Sec. 4 "[map]": ACGAC = 97);
+ *   - cutoffs: keep k-mers with ci <= count <= cx (Sec. 2.5;
+ *     P:L1191-1193 Suppl. Sec. 1; reading R10 in DESIGN.md);
+ *   - non-ACGT symbols (after case folding) make every window containing them
+ *     invalid (reading R3; "segment_read").
+ * Signatures (used only by the K2 debug-hook parity test) follow Sec. 2.2,
+ * canonical minimizers restricted to m-mers that do not start with
+ * AAA or ACA and contain no AA except at the beginning (readings R1, R2, R4).
+ *
+ * Counting: every valid window's canonical value is appended to an array, the
+ * array is sorted with std::sort (a library primitive), and equal neighbours
+ * are counted -- the histogram by definition.  f and r are recomputed from
+ * the characters for every window (no rolling update), in O(k) per window.
+ * Status: parity PINNED (tests/test_oracle.py).
+ */
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+typedef unsigned __int128 u128;
+
+/* symbol code by P:L1506: A->0, C->1, G->2, T->3; lowercase folded (R3); -1 = not ACGT */
+static inline int sym_code(uint8_t ch) {
+    switch (ch) {
+        case 'A': case 'a': return 0;
+        case 'C': case 'c': return 1;
+        case 'G': case 'g': return 2;
+        case 'T': case 't': return 3;
+        default: return -1;
+    }
+}
+
+/* true iff every symbol of w[0..k) is A/C/G/T (either case) */
+static bool window_valid(const uint8_t* w, int k) {
+    for (int j = 0; j < k; ++j)
+        if (sym_code(w[j]) < 0) return false;
+    return true;
+}
+
+/* f = sum_j code(w[j]) * 4^(k-1-j)  (leftmost symbol most significant) */
+static u128 forward_value(const uint8_t* w, int k) {
+    u128 f = 0;
+    for (int j = 0; j < k; ++j) f = f * 4 + (u128)sym_code(w[j]);
+    return f;
+}
+
+/* r = value of the reverse complement: read w backwards, complement each
+ * symbol (A<->T, C<->G, i.e. code -> 3 - code): sum_j (3 - code(w[k-1-j])) * 4^(k-1-j) */
+static u128 revcomp_value(const uint8_t* w, int k) {
+    u128 r = 0;
+    for (int j = 0; j < k; ++j) r = r * 4 + (u128)(3 - sym_code(w[k - 1 - j]));
+    return r;
+}
+
+/* canonical value = min(f, r) */
+static u128 canonical_value(const uint8_t* w, int k) {
+    u128 f = forward_value(w, k), r = revcomp_value(w, k);
+    return f < r ? f : r;
+}
+
+template <typename K>
+static int64_t count_impl(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k,
+                          uint32_t ci, uint32_t cx, uint64_t* out_keys, uint32_t* out_counts,
+                          uint64_t cap, uint64_t* stats) {
+    std::vector<K> keys;
+    uint64_t n_windows = 0;
+    for (uint64_t i = 0; i < n_reads; ++i) {
+        uint64_t b = offsets[i], e = offsets[i + 1];
+        if (e < b + (uint64_t)k) continue;
+        for (uint64_t s = b; s + k <= e; ++s) {
+            const uint8_t* w = reads + (s - offsets[0]);
+            if (!window_valid(w, k)) continue;
+            keys.push_back((K)canonical_value(w, k));
+            ++n_windows;
+        }
+    }
+    std::sort(keys.begin(), keys.end());
+    if (ci == 0) ci = 1;
+    uint64_t n_unique = 0, n_below = 0, n_above = 0, n_out = 0;
+    for (size_t a = 0; a < keys.size();) {
+        size_t z = a;
+        while (z < keys.size() && keys[z] == keys[a]) ++z;
+        uint64_t c = z - a;
+        ++n_unique;
+        if (c < ci) ++n_below;
+        else if (c > cx) ++n_above;
+        else {
+            if (n_out < cap) {
+                u128 v = (u128)keys[a];
+                if (sizeof(K) == 8) {
+                    out_keys[n_out] = (uint64_t)v;
+                } else {
+                    out_keys[2 * n_out] = (uint64_t)v;
+                    out_keys[2 * n_out + 1] = (uint64_t)(v >> 64);
+                }
+                out_counts[n_out] = (uint32_t)(c > 0xFFFFFFFFull ? 0xFFFFFFFFull : c);
+            }
+            ++n_out;
+        }
+        a = z;
+    }
+    if (stats) {
+        stats[0] = n_windows; stats[1] = n_unique; stats[2] = n_below; stats[3] = n_above; stats[4] = n_out;
+    }
+    return (int64_t)n_out;
+}
+
+extern "C" {
+
+/* Exact sorted (canonical k-mer, count) list with cutoffs.
+ * reads: host ASCII bytes; read i = reads[offsets[i]-offsets[0] .. offsets[i+1]-offsets[0]).
+ * out_keys: 1 uint64 per k-mer if k <= 32, else 2 (lo, hi).  Writes at most cap pairs;
+ * returns the number of survivors (may exceed cap).  stats[5] = n_windows, n_unique,
+ * n_below_min, n_above_max, n_out.  Returns -1 on bad k. */
+int64_t oracle_count(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k,
+                     uint32_t ci, uint32_t cx, uint64_t* out_keys, uint32_t* out_counts,
+                     uint64_t cap, uint64_t* stats) {
+    if (k < 1 || k > 64) return -1;
+    if (k <= 32) return count_impl<uint64_t>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, cap, stats);
+    return count_impl<u128>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, cap, stats);
+}
+
+/* Number of valid k-windows (upper bound for the survivor list). */
+uint64_t oracle_n_windows(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k) {
+    uint64_t n = 0;
+    for (uint64_t i = 0; i < n_reads; ++i)
+        for (uint64_t s = offsets[i]; s + k <= offsets[i + 1]; ++s)
+            if (window_valid(reads + (s - offsets[0]), k)) ++n;
+    return n;
+}
+
+/* Occurrence counts of given canonical keys (sampled parity at full size):
+ * for each query q (sorted ascending, 1 or 2 words per key as in oracle_count),
+ * count[q] = number of valid windows whose canonical value equals q. */
+void oracle_count_queries(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k,
+                          const uint64_t* queries, uint64_t nq, uint64_t* out_counts) {
+    std::vector<u128> q(nq);
+    for (uint64_t i = 0; i < nq; ++i)
+        q[i] = (k <= 32) ? (u128)queries[i] : ((u128)queries[2 * i + 1] << 64) | (u128)queries[2 * i];
+    std::memset(out_counts, 0, nq * sizeof(uint64_t));
+    for (uint64_t i = 0; i < n_reads; ++i) {
+        for (uint64_t s = offsets[i]; s + k <= offsets[i + 1]; ++s) {
+            const uint8_t* w = reads + (s - offsets[0]);
+            if (!window_valid(w, k)) continue;
+            u128 v = canonical_value(w, k);
+            auto it = std::lower_bound(q.begin(), q.end(), v);
+            if (it != q.end() && *it == v) ++out_counts[it - q.begin()];
+        }
+    }
+}
+
+/* Signature rule of Sec. 2.2, applied to the CANONICAL m-mer c[0..m)
+ * (reading R1): not starting with AAA, not starting with ACA, and no AA at any
+ * position j >= 1 (reading R2: "AA anywhere except at their beginning"). */
+int oracle_allowed_codes(const int* c, int m) {
+    if (m >= 3 && c[0] == 0 && c[1] == 0 && c[2] == 0) return 0; /* AAA prefix */
+    if (m >= 3 && c[0] == 0 && c[1] == 1 && c[2] == 0) return 0; /* ACA prefix */
+    for (int j = 1; j + 1 < m; ++j)
+        if (c[j] == 0 && c[j + 1] == 0) return 0;                 /* AA not at the beginning */
+    return 1;
+}
+
+/* Allowed test on an m-mer index (base-4, leftmost most significant). */
+int oracle_allowed_index(uint64_t idx, int m) {
+    int c[32];
+    for (int j = m - 1; j >= 0; --j) { c[j] = (int)(idx & 3); idx >>= 2; }
+    return oracle_allowed_codes(c, m);
+}
+
+/* Signature of the window w[0..k) with signature length p (Sec. 2.2, P:L206-208;
+ * Suppl. Sec. 4 P:L1506 "the smallest 5-mer which satisfies conditions of being a
+ * signature"): min over the k-p+1 p-mers of (canonical p-mer value if it is
+ * allowed, else the reserved value 4^p (reading R4)).  rules=0 gives the plain
+ * canonical minimizer for the Fig. 1 minimizer panel. */
+static uint64_t window_signature(const uint8_t* w, int k, int p, int rules) {
+    uint64_t reserved = 1ull << (2 * p);
+    uint64_t best = reserved;
+    int c[32];
+    for (int j = 0; j + p <= k; ++j) {
+        u128 v = canonical_value(w + j, p);
+        uint64_t x = (uint64_t)v;
+        for (int t = p - 1; t >= 0; --t) { c[t] = (int)(x & 3); x >>= 2; }
+        uint64_t key = (!rules || oracle_allowed_codes(c, p)) ? (uint64_t)v : reserved;
+        if (key < best) best = key;
+    }
+    return best;
+}
+
+/* Per-position signatures: out[s - offsets[0]] = signature of the window starting at
+ * global position s if that window is valid (inside one read, all ACGT), else
+ * 0xFFFFFFFF.  out has offsets[n_reads]-offsets[0] entries. */
+void oracle_signatures(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k, int p,
+                       int rules, uint32_t* out) {
+    uint64_t n = offsets[n_reads] - offsets[0];
+    for (uint64_t i = 0; i < n; ++i) out[i] = 0xFFFFFFFFu;
+    for (uint64_t i = 0; i < n_reads; ++i) {
+        for (uint64_t s = offsets[i]; s + k <= offsets[i + 1]; ++s) {
+            const uint8_t* w = reads + (s - offsets[0]);
+            if (!window_valid(w, k)) continue;
+            out[s - offsets[0]] = (uint32_t)window_signature(w, k, p, rules);
+        }
+    }
+}
+
+/* Super-k-mers (Fig. 1; reading R5): maximal runs of consecutive
+ * valid windows of one read with equal signature.  Writes (start position, number of
+ * windows, signature) triples; returns the number of super-k-mers (writes at most cap). */
+uint64_t oracle_superkmers(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k, int p,
+                           int rules, uint64_t* out_start, uint32_t* out_nwin, uint32_t* out_sig, uint64_t cap) {
+    uint64_t n = 0;
+    for (uint64_t i = 0; i < n_reads; ++i) {
+        uint64_t prev_sig = ~0ull;
+        bool in_run = false;
+        for (uint64_t s = offsets[i]; s + k <= offsets[i + 1]; ++s) {
+            const uint8_t* w = reads + (s - offsets[0]);
+            if (!window_valid(w, k)) { in_run = false; continue; }
+            uint64_t sg = window_signature(w, k, p, rules);
+            if (in_run && sg == prev_sig) {
+                if (n - 1 < cap) out_nwin[n - 1] += 1;
+            } else {
+                if (n < cap) { out_start[n] = s; out_nwin[n] = 1; out_sig[n] = (uint32_t)sg; }
+                ++n;
+                in_run = true;
+                prev_sig = sg;
+            }
+        }
+    }
+    return n;
+}
+
+}  /* extern "C" */

@@ -1,0 +1,318 @@
+"""Oracle pins (-m "not gpu"): the CPU oracle checked against values the paper prints,
+closed forms, invariants and brute force -- never against itself.
+
+Each test names the PAPER.md passage (P:Lnnn, section) or the mathematical fact it
+relies on.  Golden fixtures with citations live in tests/golden/.
+"""
+import itertools
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def c_count(seqs, k, ci=1, cx=10**9):
+    w = synth.from_strings(seqs, k)
+    res = oracle.count(w.reads, w.offsets, k, ci, cx)
+    out = {}
+    for i in range(len(res.counts)):
+        key = int(res.keys[i]) if k <= 32 else (int(res.keys[i, 1]) << 64) | int(res.keys[i, 0])
+        out[oracle.value_str(key, k)] = int(res.counts[i])
+    return out, res
+
+
+# --- encoding and reverse complement: values printed in the paper ----------------------
+
+def test_encoding_goldens():
+    g = golden("encoding.json")
+    for s, v in g["values"].items():
+        assert oracle.str_value(s) == v, (s, g["cite"])
+
+
+def test_revcomp_goldens_string_and_c():
+    g = golden("revcomp.json")
+    for s, rc in g["pairs"].items():
+        assert oracle.revcomp_str(s) == rc
+        # The C++ oracle's canonical value of s must be value(min(s, rc)) -- P:L143-145.
+        d, _ = c_count([s], len(s))
+        assert d == {min(s, rc): 1}
+
+
+# --- Fig. 1 and Suppl. Sec. 4: signatures ------------------------
+
+def test_fig1_signature_split():
+    g = golden("fig1_split.json")
+    read, k, m = g["read"], g["k"], g["m"]
+    for mode, rules in (("signatures", True), ("minimizers", False)):
+        exp = g[mode]
+        # string oracle
+        got = oracle.split_str(read, k, m, rules)
+        assert [(a, b) for a, b in got] == [tuple(x) for x in exp], mode
+        # C++ oracle
+        w = synth.from_strings([read], k)
+        sk = oracle.superkmers(w.reads, w.offsets, k, m, rules)
+        assert len(sk) == len(exp)
+        for (start, nwin, sig), (sub, sigs) in zip(sk, exp):
+            assert read[start:start + nwin + k - 1] == sub
+            assert sig == oracle.str_value(sigs)
+
+
+def test_suppl4_signature_example():
+    g = golden("suppl4_signature.json")
+    w = synth.from_strings([g["kmer"]], len(g["kmer"]))
+    sig = oracle.signatures(w.reads, w.offsets, len(g["kmer"]), g["m"], True)
+    assert int(sig[0]) == g["signature_value"] == oracle.str_value(g["signature"])
+    assert oracle.signature_str(g["kmer"], g["m"]) == g["signature"]
+    minz = oracle.signatures(w.reads, w.offsets, len(g["kmer"]), g["m"], False)
+    assert oracle.value_str(int(minz[0]), g["m"]) == g["plain_minimizer"]
+
+
+def _allowed_dp(m):
+    """Independent count of allowed m-mers (readings R1/R2) by a transfer
+    matrix over (position, previous symbol is A): strings with no 'AA' at pair positions
+    j >= 1, minus those starting AAA or ACA (those with AAA already contain AA at j=1
+    when m>=3, so only the ACA-prefixed ones need subtracting)."""
+    # f[a] = number of valid strings of length L ending in A (a=1) / not A (a=0) with no AA at j>=1
+    # position 0 and 1 are free to be AA (j = 0 pair allowed).
+    if m == 1:
+        return 4
+    # length-2 prefixes: all 16 allowed
+    end_a, end_n = 4, 12            # strings of length 2 ending in A: xA (4); else 12
+    for _ in range(2, m):
+        end_a, end_n = end_n * 1, (end_a + end_n) * 3
+    total = end_a + end_n
+    # strings starting ACA with no AA at j>=1: ACA followed by a valid continuation from state "ends in A"
+    ea, en = 1, 0
+    for _ in range(3, m):
+        ea, en = en, (ea + en) * 3
+    aca = ea + en if m >= 3 else 0
+    return total - aca
+
+
+def test_allowed_set_constants():
+    g = golden("allowed_counts.json")
+    for m_s, expected in g["allowed"].items():
+        m = int(m_s)
+        assert _allowed_dp(m) == expected
+        if m <= 7:
+            brute = sum(oracle.allowed_index(i, m) for i in range(4 ** m))
+            assert brute == expected
+            strs = sum(oracle.allowed_str("".join(t)) for t in itertools.product("ACGT", repeat=m))
+            assert strs == expected
+    for s, v in g["spec_examples"].items():
+        assert oracle.allowed_str(s) == v
+        assert oracle.allowed_index(oracle.str_value(s), len(s)) == int(v)
+
+
+def test_signature_c_vs_string_random():
+    rnd = random.Random(7)
+    for case in range(40):
+        k = rnd.choice([5, 8, 12, 21, 28, 33])
+        p = rnd.choice([3, 4, 5, 7])
+        if p > k:
+            p = k
+        seqs = synth.random_reads(case, 4, 0, 60, n_frac=0.03, lower_frac=0.1)
+        w = synth.from_strings(seqs, k)
+        sig = oracle.signatures(w.reads, w.offsets, k, p, True)
+        for r, seq in enumerate(seqs):
+            s = seq.decode()
+            base = int(w.offsets[r])
+            for i in range(len(s) - k + 1):
+                win = s[i:i + k].upper()
+                if set(win) <= set("ACGT"):
+                    exp = oracle.signature_str(win, p)
+                    ev = (1 << (2 * p)) if exp is None else oracle.str_value(exp)
+                    assert int(sig[base + i]) == ev
+                else:
+                    assert int(sig[base + i]) == 0xFFFFFFFF
+        # windows past the end of each read are invalid
+        for r, seq in enumerate(seqs):
+            for i in range(max(0, len(seq) - k + 1), len(seq)):
+                assert int(sig[int(w.offsets[r]) + i]) == 0xFFFFFFFF
+
+
+# --- counting: brute force, closed forms, invariants -----------------------------------
+
+def test_tiny_counts_golden():
+    for case in golden("tiny_counts.json")["cases"]:
+        d, _ = c_count(case["reads"], case["k"], case.get("ci", 1))
+        assert d == case["expected"], case["cite"]
+        assert oracle.count_strings(case["reads"], case["k"], case.get("ci", 1)) == case["expected"]
+
+
+def test_closed_form_homopolymer():
+    # A read of L A's has L-k+1 windows, all A^k (its own canonical: A^k < T^k).
+    for L, k in ((100, 28), (40, 25), (70, 33)):
+        for ch in "AT":
+            d, res = c_count([ch * L], k)
+            assert d == {"A" * k: L - k + 1}
+            assert res.n_windows == L - k + 1
+
+
+def test_closed_form_at_repeat():
+    # (AT)^(L/2), even k: windows starting at even positions are ATAT..AT, odd ones TATA..TA;
+    # both are reverse-complement palindromes, counts ceil/floor((L-k+1)/2).
+    L, k = 100, 28
+    d, _ = c_count(["AT" * (L // 2)], k)
+    n = L - k + 1
+    assert d == {"AT" * (k // 2): (n + 1) // 2, "TA" * (k // 2): n // 2}
+
+
+def _de_bruijn(alphabet, n):
+    """Standard Lyndon-word (FKM) construction of a de Bruijn sequence B(|A|, n)."""
+    kk = len(alphabet)
+    a = [0] * kk * n
+    seq = []
+
+    def db(t, p):
+        if t > n:
+            if n % p == 0:
+                seq.extend(a[1:p + 1])
+        else:
+            a[t] = a[t - p]
+            db(t + 1, p)
+            for j in range(a[t - p] + 1, kk):
+                a[t] = j
+                db(t + 1, t)
+    db(1, 1)
+    return "".join(alphabet[i] for i in seq)
+
+
+@pytest.mark.parametrize("k", [3, 4, 5, 6])
+def test_closed_form_de_bruijn(k):
+    s = _de_bruijn("ACGT", k)
+    lin = s + s[:k - 1]  # every k-mer exactly once
+    d, res = c_count([lin], k)
+    pal = 4 ** (k // 2) if k % 2 == 0 else 0
+    assert res.n_windows == 4 ** k
+    assert res.n_unique == (4 ** k + pal) // 2
+    assert sum(1 for v in d.values() if v == 1) == pal
+    assert sum(1 for v in d.values() if v == 2) == (4 ** k - pal) // 2
+
+
+def _windows_independent(seqs, k):
+    n = 0
+    for s in seqs:
+        for seg in oracle.segments(s.decode()):
+            n += max(0, len(seg) - k + 1)
+    return n
+
+
+@pytest.mark.parametrize("k", [5, 21, 28, 33, 55])
+def test_invariants_random(k):
+    seqs = synth.random_reads(100 + k, 300, 36, 151, n_frac=0.01, lower_frac=0.05)
+    w = synth.from_strings(seqs, k)
+    base = oracle.count(w.reads, w.offsets, k, 1, 10**9)
+    # sum of counts = valid windows
+    assert int(base.counts.sum()) == base.n_windows == _windows_independent(seqs, k)
+    assert base.n_unique == base.n_out
+    # strictly ascending keys
+    if k <= 32:
+        assert np.all(base.keys[1:] > base.keys[:-1])
+    else:
+        v = [(int(h) << 64) | int(l) for l, h in base.keys]
+        assert all(b > a for a, b in zip(v, v[1:]))
+    rnd = random.Random(k)
+    # reverse-complementing a random half of the reads (uppercase first; N stays N)
+    flipped = []
+    for s in seqs:
+        t = s.decode().upper()
+        flipped.append(oracle.revcomp_str(t) if rnd.random() < 0.5 else t)
+    # permuting reads
+    rnd.shuffle(flipped)
+    # splitting reads at an N into two reads
+    split = []
+    for t in flipped:
+        if "N" in t:
+            i = t.index("N")
+            split += [t[:i], t[i + 1:]]
+        else:
+            split.append(t)
+    for variant in (flipped, split):
+        w2 = synth.from_strings(variant, k)
+        r2 = oracle.count(w2.reads, w2.offsets, k, 1, 10**9)
+        assert np.array_equal(r2.keys, base.keys) and np.array_equal(r2.counts, base.counts)
+
+
+def test_c_vs_string_oracle_100_cases():
+    rnd = random.Random(1234)
+    for case in range(100):
+        k = rnd.choice([1, 2, 5, 11, 21, 28, 31, 32, 33, 47, 55, 64])
+        ci = rnd.choice([1, 2, 3])
+        cx = rnd.choice([10**9, 3, 5])
+        seqs = synth.random_reads(case, rnd.randint(0, 12), 0, 90, n_frac=0.02, lower_frac=0.05,
+                                  alphabet=rnd.choice([b"ACGT", b"AC", b"AT"]))
+        d, res = c_count(seqs, k, ci, cx)
+        assert d == oracle.count_strings(seqs, k, ci, cx), (case, k)
+
+
+def test_cutoffs_and_stats():
+    seqs = synth.random_reads(5, 200, 40, 80, alphabet=b"AC")
+    w = synth.from_strings(seqs, 9)
+    full = oracle.count(w.reads, w.offsets, 9, 1, 10**9)
+    ci, cx = 3, 40
+    cut = oracle.count(w.reads, w.offsets, 9, ci, cx)
+    keep = (full.counts >= ci) & (full.counts <= cx)
+    assert np.array_equal(cut.keys, full.keys[keep]) and np.array_equal(cut.counts, full.counts[keep])
+    assert cut.n_below_min == int((full.counts < ci).sum())
+    assert cut.n_above_max == int((full.counts > cx).sum())
+    assert cut.n_unique == full.n_unique
+    # ci = 0 behaves as 1
+    z = oracle.count(w.reads, w.offsets, 9, 0, 10**9)
+    assert np.array_equal(z.counts, full.counts)
+
+
+def test_signature_binning_invariance():
+    """Counting per signature bin and merging equals plain counting:
+    a k-mer and its reverse complement have the same signature, so all copies land in one bin."""
+    seqs = synth.random_reads(77, 150, 30, 120, n_frac=0.01)
+    k, p = 15, 5
+    bins = {}
+    for s in seqs:
+        for seg in oracle.segments(s.decode()):
+            for i in range(len(seg) - k + 1):
+                win = seg[i:i + k]
+                bins.setdefault(oracle.signature_str(win, p), []).append(oracle.canonical_str(win))
+    merged = {}
+    for sig, kmers in bins.items():
+        for km in kmers:
+            # every copy of km must be in this bin only
+            merged[km] = merged.get(km, 0) + 1
+        for km in set(kmers):
+            assert oracle.signature_str(km, p) == sig
+    assert merged == oracle.count_strings(seqs, k)
+
+
+def test_count_queries_matches_full():
+    wl = synth.make("C1", scale=0.02)
+    full = oracle.count(wl.reads, wl.offsets, wl.k, 1)
+    rng = np.random.default_rng(3)
+    idx = np.sort(rng.choice(len(full.keys), 200, replace=False))
+    q = full.keys[idx]
+    got = oracle.count_queries(wl.reads, wl.offsets, wl.k, q)
+    assert np.array_equal(got, full.counts[idx].astype(np.uint64))
+
+
+def test_synth_deterministic_and_shaped():
+    a = synth.make("C5", scale=0.01, n_threads=1)
+    b = synth.make("C5", scale=0.01, n_threads=4)
+    assert np.array_equal(a.reads, b.reads) and np.array_equal(a.offsets, b.offsets)
+    L = np.diff(a.offsets.astype(np.int64))
+    assert L.min() >= 50 and L.max() <= 250
+    nfrac = float((a.reads == ord("N")).mean())
+    assert 0.003 < nfrac < 0.03
+    c1 = synth.make("C1", scale=0.1)
+    assert c1.n_reads == 10_000 and c1.n_bases == 1_000_000
+    assert set(np.unique(c1.reads).tolist()) <= set(b"ACGT")
