@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py -- canonical k-mer counting (KMC 2 hot path) on B200.
+
+Default workload: BASELINE.json configs[3] ("C4": 100 Mbp x 40x, 40M x 100 bp reads,
+k=28, p=9, ci=2, cx=1e9), the configuration the metric is quoted on.  One "step" is one
+full kmc_count call (S1-S9) over the whole read set, inputs resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kmcgpu|reference] [--config C4]
+
+N > 1 runs under torchrun; every rank counts its own copy of the workload (independent
+problems, no data-path collective: weak scaling); the time is the max over ranks.
+``--impl reference`` times the CPU oracle (oracle/) on the host cores, rank 0 only.
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "input bases/s (k-mers counted/s and HBM-roofline fraction alongside)"
+
+# Algorithmic HBM bytes per stage.  Each entry: (bytes per launch, launches)
+# computed from the per-call statistics.
+
+
+def stage_bytes(st: dict, n_reads: int, k: int) -> dict:
+    ksz = 8 if k <= 32 else 16
+    rw = 16 if k <= 32 else 32
+    nb = st["n_bases"]
+    off = 8 * (n_reads + 1)
+    rec = st["n_records"] * rw
+    lw = st["large_windows"]
+    nout = st["n_out"]
+    small_rec = rec * (1 - (lw / st["n_windows"] if st["n_windows"] else 0))
+    return {
+        "signature": nb + off,                       # ASCII + offsets read (histogram is noise)
+        "scatter": nb + off + rec,                   # ASCII + offsets read, records written
+        "small_bins": small_rec + nout * (ksz + 4),  # records read, survivors written (upper bound share)
+        "large_expand": rec - small_rec + lw * ksz,  # records read, keys written
+        "large_sort": 2 * lw * ksz,                  # keys read + written once (per full sort)
+        "large_compact": lw * ksz,                   # sorted keys read once
+        "order": 2 * nout * (ksz + 4),               # survivors read + written once
+        "output": 2 * nout * (ksz + 4),
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_oracle_sample(w, n_reads_sample: int):
+    import oracle
+    n = min(n_reads_sample, w.n_reads)
+    offs = w.offsets[: n + 1]
+    reads = w.reads[: int(offs[-1])]
+    t0 = time.perf_counter()
+    r = oracle.count(reads, offs, w.k, w.cutoff_min, w.cutoff_max)
+    dt = time.perf_counter() - t0
+    return dt, int(offs[-1] - offs[0]), r.n_windows, n
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kmcgpu", choices=["kmcgpu", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-reads", type=int, default=400_000)
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    cfg = synth.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return reference_arm(args, world, rank, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1407_1507_b200 as kmc
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    kmc.load()
+    kmc.use_torch_allocator(True)
+
+    gen_threads = max(1, (os.cpu_count() or 8) // max(1, world))
+    w = synth.make(args.config, scale=args.scale, n_threads=gen_threads)
+    n_bases = w.n_bases
+    reads_d = torch.from_numpy(w.reads).cuda()
+    offs_d = torch.from_numpy(w.offsets.view(np.uint64)).cuda()
+    k, p, ci, cx = w.k, w.p, w.cutoff_min, w.cutoff_max
+    stream = torch.cuda.current_stream()
+
+    def step(profile=True):
+        return kmc.count(reads_d, offs_d, k, p, ci, cx, profile=profile)
+
+    for _ in range(max(3, args.warmup)):
+        res = step()
+        del res
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    stage_ms = {}
+    stage_launches = {}
+    n_launches = 0
+    last = None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+        for s_, v in res.stats["stage_ms"].items():
+            stage_ms[s_] = stage_ms.get(s_, 0.0) + v
+        for s_, v in res.stats["stage_launches"].items():
+            stage_launches[s_] = stage_launches.get(s_, 0) + v
+        n_launches += res.stats["n_launches"]
+        last = res.stats
+        del res
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- e2e: same call with pinned HOST buffers (H2D of inputs and D2H of outputs inside)
+    e2e = None
+    if not args.no_e2e:
+        reads_h = torch.from_numpy(w.reads).pin_memory()
+        offs_h = torch.from_numpy(w.offsets.view(np.uint64)).pin_memory()
+        r = kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu")
+        n_out = r.stats["n_out"]
+        del r
+        e_steps = max(1, min(args.steps, 3))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            r = kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu")
+            del r
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * n_bases / (e_ms / 1e3), "unit": "bases/s",
+               "ms_per_step": e_ms, "h2d_bytes_per_step": int(w.reads.nbytes + w.offsets.nbytes),
+               "d2h_bytes_per_step": int(n_out * ((8 if k <= 32 else 16) + 4))}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant stage
+    peaks = measured_peaks()
+    sb = stage_bytes(last, w.n_reads, k)
+    per_stage = {}
+    for s_, tot in stage_ms.items():
+        if tot <= 0:
+            continue
+        per_step = tot / args.steps
+        bytes_ = sb.get(s_, 0.0)
+        per_stage[s_] = {"ms": round(per_step, 3), "share": round(per_step / ms, 4),
+                         "launches": stage_launches.get(s_, 0) // args.steps,
+                         "alg_bytes": int(bytes_),
+                         "gbs": round(bytes_ / (per_step / 1e3) / 1e9, 1) if bytes_ else None}
+    dom = max(per_stage, key=lambda s_: per_stage[s_]["ms"])
+    dom_ms = per_stage[dom]["ms"]
+    achieved = sb.get(dom, 0.0) / (dom_ms / 1e3) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+            "peak_source": peaks["source"],
+            "whole_step": {"alg_bytes": int(sum(v for s_, v in sb.items() if s_ in ("signature", "scatter"))),
+                           "note": "see DESIGN.md 6 for B_alg of the full pipeline"}}
+    b_alg = n_bases + 8 * (w.n_reads + 1) + 2 * last["n_records"] * (16 if k <= 32 else 32) + \
+        last["n_out"] * ((8 if k <= 32 else 16) + 4)
+    roof["pipeline"] = {"B_alg": int(b_alg), "frac_of_step": round(b_alg / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        dt, nb_s, nw_s, nr_s = run_oracle_sample(w, args.cpu_sample_reads)
+        cpu = {"value": nb_s / dt, "unit": "bases/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {nr_s} reads of {args.config} ({nb_s} bases, {nw_s} windows), single thread",
+               "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+
+    out = {
+        "metric": METRIC,
+        "value": world * n_bases / (ms / 1e3),
+        "unit": "bases/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": round(ms, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64" if k <= 32 else "u128",
+        "data": "synthetic (seeded; BASELINE.json configs, SURVEY 8(d) recipe)",
+        "config": {"workload": f"{args.config}: {cfg.desc}", "scale": args.scale, "n_reads": w.n_reads,
+                   "n_bases": n_bases, "k": k, "p": p, "cutoff_min": ci, "cutoff_max": cx,
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs (4 GB) larger than L2 (126 MB); no flush needed"},
+        "kmers_per_s": world * last["n_windows"] / (ms / 1e3),
+        "stats": {x: last[x] for x in ("n_windows", "n_superkmers", "n_records", "n_bins", "n_large_bins",
+                                      "max_bin_windows", "large_windows", "n_unique", "n_out")},
+        "stages": per_stage,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": n_launches,
+        "clocks": clk,
+    }
+    print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def reference_arm(args, world, rank, cfg):
+    """The CPU oracle, as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    w = synth.make(args.config, scale=args.scale)
+    n_sample = 200_000
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm state worth excluding; warm-up steps are not run
+    t_tot, nb_tot, nw_tot = 0.0, 0, 0
+    for s in range(args.steps):
+        dt, nb_s, nw_s, nr_s = run_oracle_sample(w, n_sample)
+        t_tot += dt
+        nb_tot += nb_s
+        nw_tot += nw_s
+    v = nb_tot / t_tot
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "bases/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_tot / args.steps, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64" if cfg.k <= 32 else "u128",
+           "data": "synthetic", "config": {"workload": f"{args.config}: {cfg.desc}", "scale": args.scale},
+           "kmers_per_s": nw_tot / t_tot,
+           "cpu_baseline": {"value": v, "unit": "bases/s", "cores": 1, "kind": "oracle",
+                            "sample": f"first {n_sample} reads of {args.config} per step, single thread",
+                            "cpu_model": cpu_model()},
+           "e2e": {"value": v, "unit": "bases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

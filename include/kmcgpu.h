@@ -1,0 +1,170 @@
+/*
+ * kmcgpu.h -- C ABI of the B200 (sm_100a) canonical k-mer counter: the
+ * data-parallel hot path of KMC 2 (Deorowicz, Kokot, Grabowski,
+ * Debudaj-Grabysz, arXiv 1407.1507).  Citations "P:Lnnn" are lines of the
+ * paper text with its section.
+ *
+ * Operation (kmc_count): "Building the histogram of occurrences of every
+ * k-symbol long substring of nucleotide data" (Abstract; P:L46-48,
+ * Sec. 1), over canonical k-mers -- "lexicographically smaller of the pair:
+ * the k-mer and its reverse complement" (Sec. 2.1) -- keeping the
+ * k-mers whose count c satisfies cutoff_min <= c <= cutoff_max (P:L523-525,
+ * Sec. 2.5, Suppl. Sec. 1 "-ci", "-cx").  The path follows the
+ * paper's two phases (Sec. 2.4): reads are 2-bit packed, each
+ * k-mer window gets its signature (restricted canonical minimizer of length p,
+ * P:L206-208, Sec. 2.2), reads are cut into super-k-mers that are
+ * binned by signature in HBM; each bin is expanded into canonical k-mers,
+ * radix sorted and run-length compacted into (k-mer, count)
+ * pairs with the cutoffs applied (appendix "Sorter").
+ *
+ * Symbols and keys.  A->0, C->1, G->2, T->3 (Suppl. Sec. 4).  A
+ * k-mer's key is its 2k-bit value with the leftmost symbol most significant,
+ * so unsigned order = A<C<G<T lexicographic order.  Lowercase a/c/g/t are
+ * folded to upper case; any other byte (N, IUPAC codes, newline, ...)
+ * invalidates every k-mer window containing it (reading R3).
+ * Windows never cross read boundaries.
+ *
+ * Output.  out_kmers is sorted strictly ascending by key (DESIGN.md reading
+ * R8).  k <= 32: one uint64 per k-mer; 33 <= k <= 64: two uint64 per k-mer,
+ * [lo, hi] (little-endian unsigned __int128 layout).  out_counts holds the
+ * exact uint32 count (saturating at 2^32-1; reading R9).
+ *
+ * Memory.  All pointers may be device or host memory (the library asks the
+ * CUDA driver which); host inputs are copied to the device inside the call,
+ * host outputs are written by a device-to-host copy.  The caller owns every
+ * buffer passed in; the library never frees caller memory.  Scratch comes from
+ * the allocator set by kmc_set_allocator (default: cudaMallocAsync on a pool
+ * that keeps its memory between calls) and is released before return.
+ *
+ * Streams and blocking.  All work is enqueued on `stream` (cudaStream_t passed
+ * as void*, 0 = legacy default stream).  kmc_count_begin synchronizes the
+ * stream a few times (to size scratch from the data: input extent, bin plan,
+ * survivor count) and returns once the survivor count is known;
+ * kmc_count_finish returns after the outputs are complete.
+ *
+ * Errors.  Every entry point returns a kmc_status; on a non-OK status
+ * kmc_last_error() returns a thread-local message.  No partial-output
+ * guarantee on error.  Invalid arguments are rejected before any device work.
+ *
+ * Determinism.  Output bytes are identical across runs and launch
+ * configurations; atomics only decide internal placement.
+ */
+#ifndef KMCGPU_H
+#define KMCGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KMCGPU_VERSION 100
+
+typedef enum {
+    KMC_OK = 0,
+    KMC_ERR_INVALID_ARG = 1,   /* argument outside the documented range */
+    KMC_ERR_OUT_CAPACITY = 2,  /* out_capacity < n_out; stats->n_out holds the required count */
+    KMC_ERR_ALLOC = 3,         /* scratch allocation failed */
+    KMC_ERR_CUDA = 4,          /* a CUDA runtime call or kernel failed */
+    KMC_ERR_INTERNAL = 5       /* internal consistency check failed (a bug) */
+} kmc_status;
+
+/* Pipeline stages timed with CUDA events when kmc_options.profile != 0. */
+enum {
+    KMC_STAGE_INPUT = 0,      /* host->device copy of host inputs */
+    KMC_STAGE_SIGNATURE = 1,  /* S1-S3: encode + signatures + super-k-mer histogram (pass 1) */
+    KMC_STAGE_PLAN = 2,       /* S4: signature->bin map, bin offsets (scans) */
+    KMC_STAGE_SCATTER = 3,    /* S1-S3 again + S5: super-k-mer records into HBM bins (pass 2) */
+    KMC_STAGE_SMALL_BINS = 4, /* S6-S8 for bins that fit one CTA: expand + SMEM radix sort + compact */
+    KMC_STAGE_LARGE_EXPAND = 5, /* S6 for large bins: expand into HBM keys */
+    KMC_STAGE_LARGE_SORT = 6,   /* S7 for large bins: multi-CTA radix sort */
+    KMC_STAGE_LARGE_COMPACT = 7,/* S8 for large bins */
+    KMC_STAGE_ORDER = 8,      /* S9: global ascending order of survivors */
+    KMC_STAGE_OUTPUT = 9,     /* copy of the sorted survivors into the caller's buffers */
+    KMC_N_STAGES = 10
+};
+
+typedef struct {
+    uint64_t n_reads;
+    uint64_t n_bases;          /* offsets[n_reads] - offsets[0] */
+    uint64_t n_invalid_bases;  /* bytes that are not A/C/G/T/a/c/g/t */
+    uint64_t n_windows;        /* valid k-mer windows = sum of all counts before cutoffs */
+    uint64_t n_superkmers;     /* maximal equal-signature runs of valid windows */
+    uint64_t n_records;        /* bin records (super-k-mer pieces) written to HBM bins */
+    uint64_t n_signatures_used;/* distinct signature values seen (incl. the reserved 4^p) */
+    uint64_t n_bins;           /* bins in the plan */
+    uint64_t n_large_bins;     /* bins sorted by the multi-CTA path */
+    uint64_t max_bin_windows;  /* windows in the largest bin */
+    uint64_t large_windows;    /* windows in large bins */
+    uint64_t n_unique;         /* distinct canonical k-mers before cutoffs */
+    uint64_t n_below_min;      /* distinct k-mers removed by cutoff_min */
+    uint64_t n_above_max;      /* distinct k-mers removed by cutoff_max */
+    uint64_t n_out;            /* pairs written; or required, on KMC_ERR_OUT_CAPACITY */
+    uint64_t n_launches;       /* kernels this library launched for the call */
+    float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
+    uint32_t stage_launches[KMC_N_STAGES];
+} kmc_stats;
+
+typedef struct {
+    uint32_t profile;          /* 1: record CUDA events around every stage (stats.stage_ms) */
+    uint32_t small_bin_capacity; /* 0 = default; max windows of a bin sorted by one CTA
+                                    (clamped to the kernel maximum); smaller values force
+                                    more bins down the large path (testing) */
+    uint32_t force_large;      /* 1: every bin takes the large (multi-CTA) path (testing) */
+    uint32_t reserved[5];
+} kmc_options;
+
+/* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).
+ * Passing NULL restores the default (cudaMallocAsync / cudaFreeAsync on a retained pool). */
+typedef void* (*kmc_alloc_fn)(uint64_t bytes, void* stream, void* ctx);
+typedef void (*kmc_free_fn)(void* ptr, void* stream, void* ctx);
+void kmc_set_allocator(kmc_alloc_fn alloc_fn, kmc_free_fn free_fn, void* ctx);
+
+/* One-call form.  reads: n_bases bytes, read i = reads[offsets[i]-offsets[0] ..
+ * offsets[i+1]-offsets[0]); read_offsets: n_reads+1 nondecreasing uint64 (offsets[0] may
+ * be any value).  Requires 1 <= k <= 64, 3 <= p <= min(k, 12) (p = signature length,
+ * P:L1188 "-p"), cutoff_max >= max(cutoff_min, 1) (cutoff_min 0 is treated as 1).
+ * Writes n_out pairs if out_capacity >= n_out, else returns KMC_ERR_OUT_CAPACITY with
+ * stats->n_out = required.  A capacity that is always enough is
+ * floor(n_windows / max(cutoff_min, 1)).  stats may be NULL; opt may be NULL. */
+kmc_status kmc_count(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads,
+                     int k, int p, uint32_t cutoff_min, uint32_t cutoff_max,
+                     uint64_t* out_kmers, uint32_t* out_counts, uint64_t out_capacity,
+                     kmc_stats* stats, void* stream);
+
+kmc_status kmc_count_ex(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads,
+                        int k, int p, uint32_t cutoff_min, uint32_t cutoff_max,
+                        uint64_t* out_kmers, uint32_t* out_counts, uint64_t out_capacity,
+                        kmc_stats* stats, void* stream, const kmc_options* opt);
+
+/* Two-call form, so the caller can allocate outputs of exactly n_out pairs.
+ * kmc_count_begin runs phases S1-S8 and returns the survivor count in *n_out and an
+ * opaque job; kmc_count_finish runs S9 into the caller's buffers (capacity as above)
+ * and frees the job (also on error).  kmc_job_free releases a job without finishing.
+ * Input buffers must stay valid until kmc_count_finish returns. */
+typedef struct kmc_job kmc_job;
+kmc_status kmc_count_begin(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads,
+                           int k, int p, uint32_t cutoff_min, uint32_t cutoff_max,
+                           void* stream, const kmc_options* opt, kmc_job** job, uint64_t* n_out);
+kmc_status kmc_count_finish(kmc_job* job, uint64_t* out_kmers, uint32_t* out_counts,
+                            uint64_t out_capacity, kmc_stats* stats);
+void kmc_job_free(kmc_job* job);
+
+/* Test hook for S2 parity: out_sig[j] (n_bases uint32, device or host) = signature of
+ * the window starting at base j (the minimum over its k-p+1 p-mers of the canonical
+ * p-mer value if allowed by P:L206-208, else the reserved value 4^p), or 0xFFFFFFFF if
+ * no valid window starts at j. */
+kmc_status kmc_debug_signatures(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads,
+                                int k, int p, uint32_t* out_sig, void* stream);
+
+/* Signature-rule test hook: out[i] = 1 if the p-mer with value i (i < 4^p) is an allowed
+ * signature -- evaluated by the same device function the kernels use. */
+kmc_status kmc_debug_allowed(int p, uint8_t* out_allowed, void* stream);
+
+const char* kmc_last_error(void);
+int kmc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KMCGPU_H */

@@ -45,7 +45,7 @@ def build(force: bool = False) -> str:
     src = os.path.join(_HERE, "kmc_oracle.cpp")
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", tmp, src])
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-o", tmp, src])
         os.replace(tmp, _SO)
     return _SO
 
@@ -59,6 +59,8 @@ def _load():
             lib.oracle_count.restype = ctypes.c_int64
             lib.oracle_n_windows.argtypes = [_P, _P, _U64, ctypes.c_int]
             lib.oracle_n_windows.restype = _U64
+            lib.oracle_n_windows_par.argtypes = [_P, _P, _U64, ctypes.c_int]
+            lib.oracle_n_windows_par.restype = _U64
             lib.oracle_count_queries.argtypes = [_P, _P, _U64, ctypes.c_int, _P, _U64, _P]
             lib.oracle_count_queries.restype = None
             lib.oracle_allowed_index.argtypes = [_U64, ctypes.c_int]
@@ -110,6 +112,12 @@ def n_windows(reads, offsets, k: int) -> int:
     lib = _load()
     reads, offsets = _arrays(reads, offsets)
     return int(lib.oracle_n_windows(reads.ctypes.data, offsets.ctypes.data, offsets.shape[0] - 1, k))
+
+
+def n_windows_parallel(reads, offsets, k: int) -> int:
+    lib = _load()
+    reads, offsets = _arrays(reads, offsets)
+    return int(lib.oracle_n_windows_par(reads.ctypes.data, offsets.ctypes.data, offsets.shape[0] - 1, k))
 
 
 def count_queries(reads, offsets, k: int, queries) -> np.ndarray:

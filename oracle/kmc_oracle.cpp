@@ -153,15 +153,33 @@ void oracle_count_queries(const uint8_t* reads, const uint64_t* offsets, uint64_
     for (uint64_t i = 0; i < nq; ++i)
         q[i] = (k <= 32) ? (u128)queries[i] : ((u128)queries[2 * i + 1] << 64) | (u128)queries[2 * i];
     std::memset(out_counts, 0, nq * sizeof(uint64_t));
-    for (uint64_t i = 0; i < n_reads; ++i) {
-        for (uint64_t s = offsets[i]; s + k <= offsets[i + 1]; ++s) {
-            const uint8_t* w = reads + (s - offsets[0]);
-            if (!window_valid(w, k)) continue;
-            u128 v = canonical_value(w, k);
-            auto it = std::lower_bound(q.begin(), q.end(), v);
-            if (it != q.end() && *it == v) ++out_counts[it - q.begin()];
+    /* reads are independent; threads own disjoint read ranges and private counters */
+#pragma omp parallel
+    {
+        std::vector<uint64_t> local(nq, 0);
+#pragma omp for schedule(dynamic, 4096)
+        for (int64_t i = 0; i < (int64_t)n_reads; ++i) {
+            for (uint64_t s = offsets[i]; s + k <= offsets[i + 1]; ++s) {
+                const uint8_t* w = reads + (s - offsets[0]);
+                if (!window_valid(w, k)) continue;
+                u128 v = canonical_value(w, k);
+                auto it = std::lower_bound(q.begin(), q.end(), v);
+                if (it != q.end() && *it == v) ++local[it - q.begin()];
+            }
         }
+#pragma omp critical
+        for (uint64_t j = 0; j < nq; ++j) out_counts[j] += local[j];
     }
+}
+
+/* Number of valid windows, in parallel over reads (a checker for full-size runs). */
+uint64_t oracle_n_windows_par(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k) {
+    uint64_t n = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : n)
+    for (int64_t i = 0; i < (int64_t)n_reads; ++i)
+        for (uint64_t s = offsets[i]; s + k <= offsets[i + 1]; ++s)
+            if (window_valid(reads + (s - offsets[0]), k)) ++n;
+    return n;
 }
 
 /* Signature rule of Sec. 2.2, applied to the CANONICAL m-mer c[0..m)

@@ -1,0 +1,223 @@
+"""kmcgpu: B200-native (sm_100a) canonical k-mer counting -- the data-parallel hot path of
+KMC 2 (Deorowicz et al., arXiv 1407.1507) behind the C ABI in include/kmcgpu.h.
+
+This module is argument marshalling only: every step of the path runs in the CUDA
+kernels of ``libkmcgpu.so`` (built in-tree by ``paper_1407_1507_b200.build``).  There
+is no CPU fallback; if the library is missing or no GPU is present the calls raise.
+PyTorch provides device memory (inputs, outputs and, through the allocator hook, the
+library's scratch) and the CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkmcgpu.so")
+
+KMC_OK, KMC_ERR_INVALID_ARG, KMC_ERR_OUT_CAPACITY, KMC_ERR_ALLOC, KMC_ERR_CUDA, KMC_ERR_INTERNAL = range(6)
+STAGES = ["input", "signature", "plan", "scatter", "small_bins", "large_expand", "large_sort",
+          "large_compact", "order", "output"]
+
+
+class KmcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"kmcgpu status {status}: {msg}")
+        self.status = status
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "n_reads", "n_bases", "n_invalid_bases", "n_windows", "n_superkmers", "n_records",
+        "n_signatures_used", "n_bins", "n_large_bins", "max_bin_windows", "large_windows", "n_unique",
+        "n_below_min", "n_above_max", "n_out", "n_launches")] + [
+        ("stage_ms", ctypes.c_float * len(STAGES)), ("stage_launches", ctypes.c_uint32 * len(STAGES))]
+
+    def to_dict(self) -> dict:
+        d = {n: int(getattr(self, n)) for n, _ in self._fields_[:-2]}
+        d["stage_ms"] = {s: float(self.stage_ms[i]) for i, s in enumerate(STAGES)}
+        d["stage_launches"] = {s: int(self.stage_launches[i]) for i, s in enumerate(STAGES)}
+        return d
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("profile", ctypes.c_uint32), ("small_bin_capacity", ctypes.c_uint32),
+                ("force_large", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 5)]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+_lock = threading.Lock()
+_lib = None
+_cb_refs = []
+
+
+def load():
+    """Load libkmcgpu.so (raises if it is missing -- no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_1407_1507_b200.build`")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, U64, U32, I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+        lib.kmc_count_begin.argtypes = [P, P, U64, I, I, U32, U32, P, ctypes.POINTER(_Options),
+                                        ctypes.POINTER(P), ctypes.POINTER(U64)]
+        lib.kmc_count_begin.restype = I
+        lib.kmc_count_finish.argtypes = [P, P, P, U64, ctypes.POINTER(_Stats)]
+        lib.kmc_count_finish.restype = I
+        lib.kmc_job_free.argtypes = [P]
+        lib.kmc_job_free.restype = None
+        lib.kmc_count.argtypes = [P, P, U64, I, I, U32, U32, P, P, U64, ctypes.POINTER(_Stats), P]
+        lib.kmc_count.restype = I
+        lib.kmc_count_ex.argtypes = [P, P, U64, I, I, U32, U32, P, P, U64, ctypes.POINTER(_Stats), P,
+                                     ctypes.POINTER(_Options)]
+        lib.kmc_count_ex.restype = I
+        lib.kmc_debug_signatures.argtypes = [P, P, U64, I, I, P, P]
+        lib.kmc_debug_signatures.restype = I
+        lib.kmc_debug_allowed.argtypes = [I, P, P]
+        lib.kmc_debug_allowed.restype = I
+        lib.kmc_last_error.argtypes = []
+        lib.kmc_last_error.restype = ctypes.c_char_p
+        lib.kmc_version.restype = I
+        lib.kmc_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, P]
+        lib.kmc_set_allocator.restype = None
+        _lib = lib
+        return lib
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route the library's scratch allocations through torch's caching allocator."""
+    import torch
+    lib = load()
+    if not enable:
+        lib.kmc_set_allocator(_ALLOC_FN(0), _FREE_FN(0), None)
+        return
+
+    def _alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream or 0)
+        except Exception:  # noqa: BLE001 -- reported to the library as NULL -> KMC_ERR_ALLOC
+            return None
+
+    def _free(ptr, stream, ctx):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    a, f = _ALLOC_FN(_alloc), _FREE_FN(_free)
+    _cb_refs[:] = [a, f]
+    lib.kmc_set_allocator(a, f, None)
+
+
+def _check(st: int):
+    if st != KMC_OK:
+        raise KmcError(st, load().kmc_last_error().decode(errors="replace"))
+
+
+def _ptr(x) -> int:
+    if x is None:
+        return 0
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _stream_handle(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+@dataclasses.dataclass
+class Result:
+    kmers: object   # uint64 [n] (k <= 32) or [n, 2] (lo, hi); torch tensor (device or host) or numpy
+    counts: object  # uint32 [n]
+    stats: dict
+
+
+def _options(profile, small_bin_capacity, force_large):
+    o = _Options()
+    o.profile = int(bool(profile))
+    o.small_bin_capacity = int(small_bin_capacity)
+    o.force_large = int(bool(force_large))
+    return o
+
+
+def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *, stream=None,
+          profile: bool = False, small_bin_capacity: int = 0, force_large: bool = False,
+          out_device: str | None = None) -> Result:
+    """Count canonical k-mers (KMC 2 hot path on the GPU).
+
+    reads: uint8 tensor (cuda, or pinned/pageable cpu -- copied inside the call), n_bases bytes.
+    offsets: uint64/int64 tensor, n_reads+1 read boundaries (same device rules).
+    Returns sorted unique canonical k-mers and exact counts with
+    cutoff_min <= count <= cutoff_max.  Outputs land on ``out_device`` (default: the
+    device of ``reads``).
+    """
+    import torch
+    lib = load()
+    n_reads = int(offsets.shape[0]) - 1
+    if n_reads < 0:
+        raise ValueError("offsets must have n_reads + 1 entries")
+    opt = _options(profile, small_bin_capacity, force_large)
+    job = ctypes.c_void_p()
+    n_out = ctypes.c_uint64()
+    sh = _stream_handle(stream)
+    _check(lib.kmc_count_begin(_ptr(reads), _ptr(offsets), n_reads, k, p, cutoff_min, cutoff_max, sh,
+                               ctypes.byref(opt), ctypes.byref(job), ctypes.byref(n_out)))
+    n = int(n_out.value)
+    dev = out_device or (reads.device if hasattr(reads, "device") else "cpu")
+    shape = (n,) if k <= 32 else (n, 2)
+    pin = str(dev) == "cpu" and torch.cuda.is_available()
+    try:
+        kmers = torch.empty(shape, dtype=torch.uint64, device=dev, pin_memory=pin)
+        counts = torch.empty((n,), dtype=torch.uint32, device=dev, pin_memory=pin)
+    except Exception:
+        lib.kmc_job_free(job)
+        raise
+    st = _Stats()
+    _check(lib.kmc_count_finish(job, _ptr(kmers), _ptr(counts), n, ctypes.byref(st)))
+    return Result(kmers, counts, st.to_dict())
+
+
+def count_into(reads, offsets, k: int, p: int, cutoff_min: int, cutoff_max: int, out_kmers, out_counts, *,
+               stream=None, profile: bool = False) -> dict:
+    """One-call form (kmc_count_ex) into caller buffers (device or host); returns stats."""
+    lib = load()
+    n_reads = int(offsets.shape[0]) - 1
+    opt = _options(profile, 0, False)
+    st = _Stats()
+    cap = int(out_counts.shape[0])
+    _check(lib.kmc_count_ex(_ptr(reads), _ptr(offsets), n_reads, k, p, cutoff_min, cutoff_max, _ptr(out_kmers),
+                            _ptr(out_counts), cap, ctypes.byref(st), _stream_handle(stream), ctypes.byref(opt)))
+    return st.to_dict()
+
+
+def debug_signatures(reads, offsets, k: int, p: int, stream=None):
+    """Per-position window signature (S2 test hook): uint32 [n_bases], 0xFFFFFFFF = no window."""
+    import torch
+    lib = load()
+    n_reads = int(offsets.shape[0]) - 1
+    n_bases = int(reads.shape[0])
+    out = torch.empty((max(n_bases, 1),), dtype=torch.uint32, device=reads.device)
+    _check(lib.kmc_debug_signatures(_ptr(reads), _ptr(offsets), n_reads, k, p, _ptr(out), _stream_handle(stream)))
+    return out[:n_bases]
+
+
+def debug_allowed(p: int) -> np.ndarray:
+    """Device evaluation of the signature rule for every p-mer value (uint8 [4^p])."""
+    lib = load()
+    out = np.zeros(4 ** p, dtype=np.uint8)
+    import torch
+    _check(lib.kmc_debug_allowed(p, out.ctypes.data, _stream_handle(torch.cuda.current_stream())))
+    return out
+
+
+def version() -> int:
+    return int(load().kmc_version())

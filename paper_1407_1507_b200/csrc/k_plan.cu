@@ -1,0 +1,189 @@
+// k_plan.cu -- S4: device exclusive scans and the signature -> bin plan.
+//
+// The paper samples a fraction of the input, builds a signature histogram and merges
+// the least frequent signatures until at most 512 bins remain (Sec. 2.4).
+// On the B200 the histogram is exact (pass 1 counts every window and record) and bins
+// are sized to on-chip capacity instead of a file count (reading R6): runs of
+// consecutive small signatures are merged while their summed cost stays below half the
+// single-CTA capacity; a signature above that threshold forms a bin of its own.  A bin
+// never splits a signature, so every copy of a canonical k-mer lands in one bin
+// (a k-mer and its reverse complement share the signature).
+#include "kmc_device.cuh"
+#include "kmc_internal.h"
+
+namespace kmc {
+
+namespace {
+
+constexpr int SCAN_NT = 512;
+constexpr int SCAN_IPT = 8;
+constexpr uint64_t SCAN_TILE = SCAN_NT * SCAN_IPT;  // 4096
+
+template <class T> struct ArrayIn {
+    const T* a;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return (uint64_t)a[i]; }
+};
+
+// Cost of a signature in key units: max(windows, records * recw).
+struct CostIn {
+    const unsigned long long* hw;
+    const uint32_t* hr;
+    uint32_t recw;
+    uint64_t half;
+    __device__ __forceinline__ uint64_t cost(uint64_t i) const {
+        uint64_t w = hw[i], r = (uint64_t)hr[i] * recw;
+        return w > r ? w : r;
+    }
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        uint64_t c = cost(i);
+        return c > half ? 0 : c;  // big signatures get their own bin
+    }
+};
+
+// 1 where a new bin starts at signature i.
+struct BoundaryIn {
+    CostIn c;
+    const uint64_t* P;  // exclusive scan of small costs
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        if (i == 0) return 1;
+        const bool big = c.cost(i) > c.half, big_prev = c.cost(i - 1) > c.half;
+        if (big || big_prev) return 1;
+        return (P[i] / c.half) != (P[i - 1] / c.half) ? 1 : 0;
+    }
+};
+
+template <class F, class TO>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_reduce(F f, uint64_t n, TO* sums) {
+    __shared__ TO ws[SCAN_NT / 32 + 1];
+    const uint64_t base = blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_IPT;
+    TO s = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_IPT; ++j)
+        if (base + j < n) s += (TO)f(base + j);
+    TO t = block_sum<SCAN_NT, TO>(s, ws);
+    if (threadIdx.x == 0) sums[blockIdx.x] = t;
+}
+
+// out[i] = block_off[b] + exclusive prefix within block; out[n] written by the last element.
+template <class F, class TO>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_down(F f, uint64_t n, const TO* block_off, TO* out) {
+    __shared__ TO ws[SCAN_NT / 32 + 1];
+    const uint64_t base = blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_IPT;
+    TO v[SCAN_IPT];
+    TO s = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_IPT; ++j) {
+        v[j] = (base + j < n) ? (TO)f(base + j) : (TO)0;
+        s += v[j];
+    }
+    TO ex = block_excl_sum<SCAN_NT, TO>(s, ws, (TO*)nullptr) + (block_off ? block_off[blockIdx.x] : (TO)0);
+#pragma unroll
+    for (int j = 0; j < SCAN_IPT; ++j) {
+        if (base + j < n) out[base + j] = ex;
+        if (base + j == n - 1) out[n] = ex + v[j];
+        ex += v[j];
+    }
+}
+
+template <class TO> size_t scan_temp_elems(uint64_t n) {
+    size_t tot = 0;
+    while (n > 1) {
+        uint64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+        tot += 2 * (nb + 1);
+        n = nb;
+    }
+    return tot + 2;
+}
+
+// Generic recursive exclusive scan: out has n+1 entries.
+template <class TO, class F>
+cudaError_t scan_generic(F f, uint64_t n, TO* out, TO* temp, cudaStream_t s, int* launches) {
+    if (n == 0) {
+        cudaError_t e = cudaMemsetAsync(out, 0, sizeof(TO), s);
+        return e;
+    }
+    const uint64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (nb == 1) {
+        k_scan_down<F, TO><<<1, SCAN_NT, 0, s>>>(f, n, (const TO*)nullptr, out);
+        if (launches) *launches += 1;
+        return cudaGetLastError();
+    }
+    TO* sums = temp;
+    TO* offs = temp + nb;  // nb + 1 entries
+    TO* rest = temp + 2 * (nb + 1);
+    k_scan_reduce<F, TO><<<(unsigned)nb, SCAN_NT, 0, s>>>(f, n, sums);
+    if (launches) *launches += 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = scan_generic<TO>(ArrayIn<TO>{sums}, nb, offs, rest, s, launches);
+    if (e != cudaSuccess) return e;
+    k_scan_down<F, TO><<<(unsigned)nb, SCAN_NT, 0, s>>>(f, n, offs, out);
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+}
+
+__global__ void k_sig2bin(BoundaryIn bf, uint64_t ns, const uint64_t* B, uint32_t* sig2bin, uint64_t* bin_first,
+                          const unsigned long long* hw, unsigned long long* gstats) {
+    __shared__ uint32_t ws[9];
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t used = 0;
+    if (i < ns) {
+        const uint64_t bnd = bf(i);
+        const uint64_t incl = B[i] + bnd;
+        sig2bin[i] = (uint32_t)(incl - 1);
+        if (bnd) bin_first[incl - 1] = i;
+        if (i == ns - 1) bin_first[B[ns]] = ns;
+        used = hw[i] != 0;
+    }
+    uint32_t t = block_sum<256, uint32_t>(used, ws);
+    if (threadIdx.x == 0 && t) atomicAdd(&gstats[GS_SIGS_USED], (unsigned long long)t);
+}
+
+__global__ void k_bins(uint64_t ns, const uint64_t* B, const uint64_t* bin_first, const uint64_t* Wp,
+                       const uint64_t* Rp, uint64_t* bin_w, uint64_t* bin_nrec, uint64_t* bin_rec_off) {
+    const uint64_t n_bins = B[ns];
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n_bins;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t fs = bin_first[b], fe = bin_first[b + 1];
+        bin_w[b] = Wp[fe] - Wp[fs];
+        bin_nrec[b] = Rp[fe] - Rp[fs];
+        bin_rec_off[b] = Rp[fs];
+    }
+}
+
+}  // namespace
+
+size_t scan_temp_bytes(uint64_t n) { return scan_temp_elems<uint64_t>(n) * sizeof(uint64_t); }
+
+cudaError_t scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, void* temp, cudaStream_t s) {
+    return scan_generic<uint64_t>(ArrayIn<uint64_t>{in}, n, out, (uint64_t*)temp, s, nullptr);
+}
+
+cudaError_t scan_u32_to_u32(const uint32_t* in, uint32_t* out, uint64_t n, void* temp, cudaStream_t s) {
+    return scan_generic<uint32_t>(ArrayIn<uint32_t>{in}, n, out, (uint32_t*)temp, s, nullptr);
+}
+
+size_t plan_temp_bytes(uint64_t ns) { return scan_temp_bytes(ns); }
+
+cudaError_t launch_plan(const PlanArgs& a, cudaStream_t s, int* n_launches) {
+    cudaError_t e;
+    CostIn ci{a.hist_w, a.hist_r, a.recw, a.half_cap};
+    uint64_t* tmp = (uint64_t*)a.temp;
+    if ((e = scan_generic<uint64_t>(ci, a.ns, a.cost_scan, tmp, s, n_launches)) != cudaSuccess) return e;
+    BoundaryIn bf{ci, a.cost_scan};
+    if ((e = scan_generic<uint64_t>(bf, a.ns, a.bnd_scan, tmp, s, n_launches)) != cudaSuccess) return e;
+    if ((e = scan_generic<uint64_t>(ArrayIn<unsigned long long>{a.hist_w}, a.ns, a.win_scan, tmp, s, n_launches)) !=
+        cudaSuccess)
+        return e;
+    if ((e = scan_generic<uint64_t>(ArrayIn<uint32_t>{a.hist_r}, a.ns, a.rec_scan, tmp, s, n_launches)) != cudaSuccess)
+        return e;
+    k_sig2bin<<<(unsigned)((a.ns + 255) / 256), 256, 0, s>>>(bf, a.ns, a.bnd_scan, a.sig2bin, a.bin_first, a.hist_w,
+                                                             a.gstats);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k_bins<<<(unsigned)std::min<uint64_t>((a.ns + 255) / 256, 4096), 256, 0, s>>>(
+        a.ns, a.bnd_scan, a.bin_first, a.win_scan, a.rec_scan, a.bin_w, a.bin_nrec, a.bin_rec_off);
+    if (n_launches) *n_launches += 2;
+    return cudaGetLastError();
+}
+
+}  // namespace kmc

@@ -1,0 +1,452 @@
+// k_sort.cu -- phase 2 of KMC 2 on the B200 (Sec. 2.4 "sorting"; appendix
+// "Sorter": uncompact super-k-mers, sort, merge identical k-mers with the
+// cutoffs) and S9 (global ascending order of the survivors, reading R8).
+//
+//   k_small_bins  one CTA per bin that fits shared memory: records -> canonical keys
+//                 (S6) -> LSD radix sort in SMEM (S7) -> run-length compaction with
+//                 ci <= count <= cx (S8) -> survivors appended to the survivor buffer.
+//   k_large_expand  S6 for bins above CTA capacity: keys into HBM.
+//   k_upsweep / k_downsweep  device-wide LSD radix sort (8-bit digits, constant digits
+//                 skipped) -- S7 for large bins and S9 for the survivors.
+//   k_rle         S8 over a globally sorted HBM key array.
+#include <algorithm>
+#include <vector>
+
+#include "kmc_device.cuh"
+#include "kmc_internal.h"
+
+namespace kmc {
+
+namespace {
+
+constexpr int SB_NT = 512;
+constexpr int SB_NW = SB_NT / 32;
+constexpr int SB_CAP64 = 6144;  // keys per small bin (u64); 2 CTAs per SM
+constexpr int SB_CAP128 = 3072;
+
+template <class K> struct SmallCap;
+template <> struct SmallCap<uint64_t> { static constexpr int v = SB_CAP64; };
+template <> struct SmallCap<K128> { static constexpr int v = SB_CAP128; };
+
+template <class K> __host__ __device__ constexpr size_t small_smem_bytes() {
+    return 2 * (size_t)SmallCap<K>::v * sizeof(K) + RADIX * SB_NW * 4 + 128 + 64;
+}
+
+// Expand one record into n canonical keys at dst[0..n) (min(fwd, rc)).
+template <class K>
+__device__ __forceinline__ void expand_record(const uint32_t* rec, int k, K* dst) {
+    typename RollFor<K>::T roll(k);
+    const int n = (int)rec_nwin(rec);
+    for (int j = 0; j < k - 1; ++j) roll.push(rec_sym(rec, j));
+    for (int w = 0; w < n; ++w) {
+        roll.push(rec_sym(rec, k - 1 + w));
+        dst[w] = roll.canon();
+    }
+}
+
+// Run-length compaction of the sorted keys S[0..n) with the cutoffs (S8); cnt is a free
+// uint32 scratch of n entries.  Survivors are appended at a CTA-reserved range.
+template <class K, int NT>
+__device__ __forceinline__ void block_rle_emit(const K* S, int n, uint32_t* cnt, uint32_t ci, uint32_t cx,
+                                               K* out_keys, uint32_t* out_counts, unsigned long long* gstats,
+                                               uint32_t* wsum, unsigned long long* bcast) {
+    const int seg = (n + NT - 1) / NT;
+    const int b0 = threadIdx.x * seg, b1 = min(n, b0 + seg);
+    uint32_t uniq = 0, below = 0, above = 0, keep = 0;
+    for (int i = b0; i < b1; ++i) {
+        uint32_t c = 0;
+        if (i == 0 || !key_eq(S[i], S[i - 1])) {
+            int j = i + 1;
+            while (j < n && key_eq(S[j], S[i])) ++j;
+            const uint32_t run = (uint32_t)(j - i);
+            ++uniq;
+            if (run < ci) ++below;
+            else if (run > cx) ++above;
+            else {
+                c = run;
+                ++keep;
+            }
+        }
+        cnt[i] = c;
+    }
+    uint32_t total;
+    uint32_t ex = block_excl_sum<NT, uint32_t>(keep, wsum, &total);
+    const uint32_t tu = block_sum<NT, uint32_t>(uniq, wsum);
+    const uint32_t tb = block_sum<NT, uint32_t>(below, wsum);
+    const uint32_t ta = block_sum<NT, uint32_t>(above, wsum);
+    if (threadIdx.x == 0) {
+        *bcast = total ? atomicAdd(&gstats[GS_SURV], (unsigned long long)total) : 0ull;
+        if (tu) atomicAdd(&gstats[GS_UNIQUE], (unsigned long long)tu);
+        if (tb) atomicAdd(&gstats[GS_BELOW], (unsigned long long)tb);
+        if (ta) atomicAdd(&gstats[GS_ABOVE], (unsigned long long)ta);
+    }
+    __syncthreads();
+    const uint64_t base = *bcast + ex;
+    uint64_t o = 0;
+    for (int i = b0; i < b1; ++i) {
+        const uint32_t c = cnt[i];
+        if (c) {
+            out_keys[base + o] = S[i];
+            out_counts[base + o] = c;
+            ++o;
+        }
+    }
+}
+
+template <class K>
+__global__ void __launch_bounds__(SB_NT) k_small_bins(SmallArgs a) {
+    constexpr int CAP = SmallCap<K>::v;
+    extern __shared__ __align__(16) uint8_t smem[];
+    K* A = reinterpret_cast<K*>(smem);
+    K* B = A + CAP;
+    uint32_t* whist = reinterpret_cast<uint32_t*>(B + CAP);
+    uint32_t* wsum = whist + RADIX * SB_NW;                                      // 17 used
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(wsum + 24);  // 4
+    unsigned long long* bcast = red + 4;
+
+    const uint32_t bin = a.small_list[blockIdx.x];
+    const uint64_t rec0 = a.bin_rec_off[bin];
+    const int nrec = (int)a.bin_nrec[bin];
+    const int n = (int)a.bin_w[bin];
+    const int k = a.k;
+    const int RW = record_words(k);
+
+    // ---- load the bin's records (16-byte vectors) into B
+    uint32_t* R = reinterpret_cast<uint32_t*>(B);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.bins + rec0 * RW);
+        uint4* dst = reinterpret_cast<uint4*>(R);
+        const int nv = nrec * RW / 4;
+        for (int v = threadIdx.x; v < nv; v += SB_NT) dst[v] = src[v];
+    }
+    __syncthreads();
+    // ---- S6: expand records into canonical keys in A (record prefix sums by block scan)
+    {
+        const int rpt = (nrec + SB_NT - 1) / SB_NT;
+        const int r0 = threadIdx.x * rpt, r1 = min(nrec, r0 + rpt);
+        uint32_t s = 0;
+        for (int r = r0; r < r1; ++r) s += rec_nwin(R + r * RW);
+        uint32_t pos = block_excl_sum<SB_NT, uint32_t>(s, wsum, nullptr);
+        for (int r = r0; r < r1; ++r) {
+            const uint32_t* rec = R + r * RW;
+            expand_record<K>(rec, k, A + pos);
+            pos += rec_nwin(rec);
+        }
+    }
+    __syncthreads();
+    // ---- S7: LSD radix sort in shared memory
+    const int cur = block_radix_sort<K, SB_NT, false>(A, B, nullptr, nullptr, n, 2 * k, whist, wsum, red);
+    K* S = cur ? B : A;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(cur ? A : B);
+    // ---- S8: run-length compaction + cutoffs
+    block_rle_emit<K, SB_NT>(S, n, cnt, a.ci, a.cx, reinterpret_cast<K*>(a.surv_keys), a.surv_counts, a.gstats, wsum,
+                             bcast);
+}
+
+// ---------------------------------------------------------------- large-bin expansion
+constexpr int LE_NT = 256;
+
+template <class K>
+__global__ void __launch_bounds__(LE_NT) k_large_expand(const uint32_t* __restrict__ bins,
+                                                        const Piece* __restrict__ pieces, int k, K* keys,
+                                                        unsigned long long* gstats) {
+    __shared__ __align__(16) uint32_t R[PIECE_RECORDS * 8];
+    __shared__ uint32_t wsum[LE_NT / 32 + 1];
+    __shared__ unsigned long long bcast;
+    const Piece pc = pieces[blockIdx.x];
+    const int RW = record_words(k);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(bins + pc.rec_begin * RW);
+        uint4* dst = reinterpret_cast<uint4*>(R);
+        const int nv = (int)pc.nrec * RW / 4;
+        for (int v = threadIdx.x; v < nv; v += LE_NT) dst[v] = src[v];
+    }
+    __syncthreads();
+    const int nrec = (int)pc.nrec;
+    const int rpt = (nrec + LE_NT - 1) / LE_NT;
+    const int r0 = threadIdx.x * rpt, r1 = min(nrec, r0 + rpt);
+    uint32_t s = 0;
+    for (int r = r0; r < r1; ++r) s += rec_nwin(R + r * RW);
+    uint32_t total;
+    uint32_t pos = block_excl_sum<LE_NT, uint32_t>(s, wsum, &total);
+    if (threadIdx.x == 0) bcast = atomicAdd(&gstats[GS_LARGE_KEYS], (unsigned long long)total);
+    __syncthreads();
+    K* out = keys + bcast;
+    for (int r = r0; r < r1; ++r) {
+        const uint32_t* rec = R + r * RW;
+        expand_record<K>(rec, k, out + pos);
+        pos += rec_nwin(rec);
+    }
+}
+
+// ---------------------------------------------------------------- device radix sort
+template <class K> struct RadixTile;
+template <> struct RadixTile<uint64_t> { static constexpr int NT = 256, TI = 4096; };
+template <> struct RadixTile<K128> { static constexpr int NT = 256, TI = 2048; };
+
+template <class K>
+__global__ void k_orand(const K* __restrict__ keys, uint64_t n, unsigned long long* red) {
+    uint64_t o = 0, an = ~0ull, oh = 0, ah = ~0ull;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        key_or_and_accum(keys[i], o, an, oh, ah);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, s);
+        an &= __shfl_xor_sync(0xffffffffu, an, s);
+        oh |= __shfl_xor_sync(0xffffffffu, oh, s);
+        ah &= __shfl_xor_sync(0xffffffffu, ah, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(&red[0], (unsigned long long)o);
+        atomicAnd(&red[1], (unsigned long long)an);
+        atomicOr(&red[2], (unsigned long long)oh);
+        atomicAnd(&red[3], (unsigned long long)ah);
+    }
+}
+
+template <class K>
+__global__ void k_upsweep(const K* __restrict__ keys, uint64_t n, int shift, uint32_t* __restrict__ tile_hist,
+                          uint64_t ntiles) {
+    constexpr int NT = RadixTile<K>::NT, TI = RadixTile<K>::TI;
+    __shared__ uint32_t h[RADIX];
+    for (int d = threadIdx.x; d < RADIX; d += NT) h[d] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * TI;
+    for (int j = threadIdx.x; j < TI; j += NT) {
+        const uint64_t i = base + j;
+        if (i < n) atomicAdd(&h[key_digit(keys[i], shift)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < RADIX; d += NT) tile_hist[(uint64_t)d * ntiles + blockIdx.x] = h[d];
+}
+
+template <class K, bool VALS>
+__global__ void __launch_bounds__(RadixTile<K>::NT) k_downsweep(const K* __restrict__ kin,
+                                                                const uint32_t* __restrict__ vin, K* __restrict__ kout,
+                                                                uint32_t* __restrict__ vout, uint64_t n, int shift,
+                                                                const uint32_t* __restrict__ tile_off, uint64_t ntiles) {
+    constexpr int NT = RadixTile<K>::NT, TI = RadixTile<K>::TI, NW = NT / 32;
+    extern __shared__ __align__(16) uint8_t smem[];
+    K* A = reinterpret_cast<K*>(smem);
+    K* B = A + TI;
+    uint32_t* VA = reinterpret_cast<uint32_t*>(B + TI);
+    uint32_t* VB = VA + (VALS ? TI : 0);
+    uint32_t* whist = VB + (VALS ? TI : 0);
+    uint32_t* wsum = whist + RADIX * NW;
+    uint32_t* dstart = wsum + NW + 1;  // RADIX + 1
+    uint32_t* goff = dstart + RADIX + 1;
+    const uint64_t base = (uint64_t)blockIdx.x * TI;
+    const int cnt = (int)((n - base) < (uint64_t)TI ? (n - base) : (uint64_t)TI);
+    for (int j = threadIdx.x; j < cnt; j += NT) {
+        A[j] = kin[base + j];
+        if (VALS) VA[j] = vin[base + j];
+    }
+    for (int d = threadIdx.x; d < RADIX; d += NT) goff[d] = tile_off[(uint64_t)d * ntiles + blockIdx.x];
+    __syncthreads();
+    block_digit_pass<K, NT, VALS>(A, B, VA, VB, cnt, shift, whist, wsum, dstart);
+    for (int j = threadIdx.x; j < cnt; j += NT) {
+        const K key = B[j];
+        const uint32_t d = key_digit(key, shift);
+        const uint64_t pos = (uint64_t)goff[d] + (uint32_t)(j - dstart[d]);
+        kout[pos] = key;
+        if (VALS) vout[pos] = VB[j];
+    }
+}
+
+template <class K, bool VALS> constexpr size_t downsweep_smem() {
+    constexpr int NT = RadixTile<K>::NT, TI = RadixTile<K>::TI, NW = NT / 32;
+    return 2 * (size_t)TI * sizeof(K) + (VALS ? 2 * (size_t)TI * 4 : 0) + (RADIX * NW + NW + 1 + 2 * RADIX + 1) * 4 + 16;
+}
+
+template <class K>
+cudaError_t radix_sort_t(K* keys, uint32_t* vals, uint64_t n, int nbits, const RadixScratch& rs, cudaStream_t s,
+                         void** res_keys, uint32_t** res_vals, int* launches) {
+    constexpr int NT = RadixTile<K>::NT, TI = RadixTile<K>::TI;
+    *res_keys = keys;
+    *res_vals = vals;
+    if (n <= 1) return cudaSuccess;
+    if (n >= (1ull << 32)) return cudaErrorInvalidValue;
+    cudaError_t e;
+    // constant digits are skipped: bitwise OR / AND over all keys
+    if ((e = cudaMemsetAsync(rs.red, 0, 4 * sizeof(unsigned long long), s)) != cudaSuccess) return e;
+    {
+        unsigned long long init[4] = {0ull, ~0ull, 0ull, ~0ull};
+        if ((e = cudaMemcpyAsync(rs.red, init, sizeof(init), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+    }
+    const unsigned og = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+    k_orand<K><<<og, 256, 0, s>>>(keys, n, rs.red);
+    *launches += 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(rs.red_host, rs.red, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s)) !=
+        cudaSuccess)
+        return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    const uint64_t vlo = rs.red_host[0] ^ rs.red_host[1], vhi = rs.red_host[2] ^ rs.red_host[3];
+    const uint64_t ntiles = (n + TI - 1) / TI;
+    K* src = keys;
+    K* dst = reinterpret_cast<K*>(rs.keys_alt);
+    uint32_t* vsrc = vals;
+    uint32_t* vdst = rs.vals_alt;
+    const bool has_vals = vals != nullptr;
+    const size_t sm = has_vals ? downsweep_smem<K, true>() : downsweep_smem<K, false>();
+    if (has_vals) {
+        if ((e = cudaFuncSetAttribute(k_downsweep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) !=
+            cudaSuccess)
+            return e;
+    } else {
+        if ((e = cudaFuncSetAttribute(k_downsweep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) !=
+            cudaSuccess)
+            return e;
+    }
+    for (int shift = 0; shift < nbits; shift += RADIX_BITS) {
+        const bool varies = shift < 64 ? ((vlo >> shift) & 0xFF) != 0 : ((vhi >> (shift - 64)) & 0xFF) != 0;
+        if (!varies) continue;
+        k_upsweep<K><<<(unsigned)ntiles, NT, 0, s>>>(src, n, shift, rs.tile_hist, ntiles);
+        *launches += 1;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = scan_u32_to_u32(rs.tile_hist, rs.tile_off, RADIX * ntiles, rs.scan_temp, s)) != cudaSuccess) return e;
+        *launches += 2;
+        if (has_vals)
+            k_downsweep<K, true><<<(unsigned)ntiles, NT, sm, s>>>(src, vsrc, dst, vdst, n, shift, rs.tile_off, ntiles);
+        else
+            k_downsweep<K, false><<<(unsigned)ntiles, NT, sm, s>>>(src, nullptr, dst, nullptr, n, shift, rs.tile_off,
+                                                                   ntiles);
+        *launches += 1;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        std::swap(src, dst);
+        std::swap(vsrc, vdst);
+    }
+    *res_keys = src;
+    *res_vals = has_vals ? vsrc : nullptr;
+    return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- RLE over HBM keys
+constexpr int RLE_NT = 256, RLE_IPT = 8;
+
+template <class K>
+__global__ void __launch_bounds__(RLE_NT) k_rle(const K* __restrict__ keys, uint64_t n, uint32_t ci, uint32_t cx,
+                                                K* __restrict__ sk, uint32_t* __restrict__ sc,
+                                                unsigned long long* gstats) {
+    __shared__ uint32_t wsum[RLE_NT / 32 + 1];
+    __shared__ unsigned long long bcast;
+    const uint64_t base = (uint64_t)blockIdx.x * (RLE_NT * RLE_IPT);
+    uint32_t cnts[RLE_IPT];
+    uint32_t uniq = 0, below = 0, above = 0, keep = 0;
+#pragma unroll
+    for (int j = 0; j < RLE_IPT; ++j) {
+        const uint64_t i = base + (uint64_t)j * RLE_NT + threadIdx.x;
+        cnts[j] = 0;
+        if (i >= n) continue;
+        const K key = keys[i];
+        if (i > 0 && key_eq(keys[i - 1], key)) continue;
+        // galloping search for the end of the run
+        uint64_t lo = i, hi, step = 1;
+        for (;;) {
+            const uint64_t pr = lo + step;
+            if (pr >= n || !key_eq(keys[pr], key)) {
+                hi = pr < n ? pr : n;
+                break;
+            }
+            lo = pr;
+            step <<= 1;
+        }
+        while (hi - lo > 1) {
+            const uint64_t mid = lo + ((hi - lo) >> 1);
+            if (key_eq(keys[mid], key)) lo = mid;
+            else hi = mid;
+        }
+        const uint64_t run = hi - i;
+        ++uniq;
+        if (run < ci) ++below;
+        else if (run > cx) ++above;
+        else {
+            cnts[j] = (uint32_t)(run > 0xFFFFFFFFull ? 0xFFFFFFFFull : run);
+            ++keep;
+        }
+    }
+    uint32_t total;
+    uint32_t ex = block_excl_sum<RLE_NT, uint32_t>(keep, wsum, &total);
+    const uint32_t tu = block_sum<RLE_NT, uint32_t>(uniq, wsum);
+    const uint32_t tb = block_sum<RLE_NT, uint32_t>(below, wsum);
+    const uint32_t ta = block_sum<RLE_NT, uint32_t>(above, wsum);
+    if (threadIdx.x == 0) {
+        bcast = total ? atomicAdd(&gstats[GS_SURV], (unsigned long long)total) : 0ull;
+        if (tu) atomicAdd(&gstats[GS_UNIQUE], (unsigned long long)tu);
+        if (tb) atomicAdd(&gstats[GS_BELOW], (unsigned long long)tb);
+        if (ta) atomicAdd(&gstats[GS_ABOVE], (unsigned long long)ta);
+    }
+    __syncthreads();
+    uint64_t o = bcast + ex;
+#pragma unroll
+    for (int j = 0; j < RLE_IPT; ++j) {
+        if (cnts[j]) {
+            const uint64_t i = base + (uint64_t)j * RLE_NT + threadIdx.x;
+            sk[o] = keys[i];
+            sc[o] = cnts[j];
+            ++o;
+        }
+    }
+}
+
+}  // namespace
+
+int small_capacity(int k) { return k <= 32 ? SB_CAP64 : SB_CAP128; }
+
+cudaError_t launch_small_bins(const SmallArgs& a, uint64_t n_small, cudaStream_t s) {
+    if (n_small == 0) return cudaSuccess;
+    cudaError_t e;
+    if (a.k <= 32) {
+        const size_t sm = small_smem_bytes<uint64_t>();
+        if ((e = cudaFuncSetAttribute(k_small_bins<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) !=
+            cudaSuccess)
+            return e;
+        k_small_bins<uint64_t><<<(unsigned)n_small, SB_NT, sm, s>>>(a);
+    } else {
+        const size_t sm = small_smem_bytes<K128>();
+        if ((e = cudaFuncSetAttribute(k_small_bins<K128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) !=
+            cudaSuccess)
+            return e;
+        k_small_bins<K128><<<(unsigned)n_small, SB_NT, sm, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, void* keys,
+                                unsigned long long* gstats, cudaStream_t s) {
+    if (n_pieces == 0) return cudaSuccess;
+    if (k <= 32)
+        k_large_expand<uint64_t><<<(unsigned)n_pieces, LE_NT, 0, s>>>(bins, pieces, k, (uint64_t*)keys, gstats);
+    else
+        k_large_expand<K128><<<(unsigned)n_pieces, LE_NT, 0, s>>>(bins, pieces, k, (K128*)keys, gstats);
+    return cudaGetLastError();
+}
+
+uint64_t radix_tile_items(int key_words) { return key_words == 1 ? RadixTile<uint64_t>::TI : RadixTile<K128>::TI; }
+
+size_t radix_scan_temp_bytes(uint64_t n, int key_words) {
+    const uint64_t ntiles = (n + radix_tile_items(key_words) - 1) / radix_tile_items(key_words);
+    return scan_temp_bytes(RADIX * ntiles + 1);
+}
+
+cudaError_t device_radix_sort(int key_words, void* keys, uint32_t* vals, uint64_t n, int nbits,
+                              const RadixScratch& rs, cudaStream_t s, void** res_keys, uint32_t** res_vals,
+                              int* n_launches) {
+    if (key_words == 1)
+        return radix_sort_t<uint64_t>((uint64_t*)keys, vals, n, nbits, rs, s, res_keys, res_vals, n_launches);
+    return radix_sort_t<K128>((K128*)keys, vals, n, nbits, rs, s, res_keys, res_vals, n_launches);
+}
+
+cudaError_t launch_rle(int key_words, const void* keys, uint64_t n, uint32_t ci, uint32_t cx, void* surv_keys,
+                       uint32_t* surv_counts, unsigned long long* gstats, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((n + RLE_NT * RLE_IPT - 1) / (RLE_NT * RLE_IPT));
+    if (key_words == 1)
+        k_rle<uint64_t><<<grid, RLE_NT, 0, s>>>((const uint64_t*)keys, n, ci, cx, (uint64_t*)surv_keys, surv_counts,
+                                                gstats);
+    else
+        k_rle<K128><<<grid, RLE_NT, 0, s>>>((const K128*)keys, n, ci, cx, (K128*)surv_keys, surv_counts, gstats);
+    return cudaGetLastError();
+}
+
+}  // namespace kmc

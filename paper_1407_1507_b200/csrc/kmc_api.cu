@@ -1,0 +1,683 @@
+// kmc_api.cu -- C ABI (include/kmcgpu.h) and host orchestration of the KMC 2 hot path.
+//
+// Stream-ordered sequence per call:
+//   [input H2D] -> tile/read index -> pass 1 (S1-S3 + histogram) -> plan (S4)
+//   -> sync: bin table -> pass 2 (S1-S3 + scatter, S5) -> small bins (S6-S8)
+//   -> large bins: expand (S6) + device radix sort (S7) + RLE (S8)
+//   -> sync: survivor count -> [finish] global order (S9) -> output copy.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/kmcgpu.h"
+#include "kmc_device.cuh"
+#include "kmc_internal.h"
+
+using namespace kmc;
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_alloc_mu;
+kmc_alloc_fn g_alloc = nullptr;
+kmc_free_fn g_free = nullptr;
+void* g_ctx = nullptr;
+std::once_flag g_pool_once;
+
+void set_err(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+struct Fail {
+    kmc_status st;
+};
+
+#define CK(call)                                                                                       \
+    do {                                                                                               \
+        cudaError_t _e = (call);                                                                       \
+        if (_e != cudaSuccess) {                                                                       \
+            set_err("%s:%d: %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e));               \
+            throw Fail{KMC_ERR_CUDA};                                                                  \
+        }                                                                                              \
+    } while (0)
+
+void init_pool() {
+    std::call_once(g_pool_once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+struct Arena {
+    cudaStream_t s = 0;
+    std::vector<void*> ptrs;
+    kmc_alloc_fn af = nullptr;
+    kmc_free_fn ff = nullptr;
+    void* ctx = nullptr;
+    void bind(cudaStream_t st) {
+        s = st;
+        std::lock_guard<std::mutex> g(g_alloc_mu);
+        af = g_alloc;
+        ff = g_free;
+        ctx = g_ctx;
+        if (!af) init_pool();
+    }
+    void* alloc(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        bytes = (bytes + 255) & ~(size_t)255;
+        void* p = nullptr;
+        if (af) {
+            p = af(bytes, (void*)s, ctx);
+        } else {
+            if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) p = nullptr;
+        }
+        if (!p) {
+            cudaGetLastError();
+            set_err("scratch allocation of %zu bytes failed", bytes);
+            throw Fail{KMC_ERR_ALLOC};
+        }
+        ptrs.push_back(p);
+        return p;
+    }
+    template <class T> T* get(size_t n) { return reinterpret_cast<T*>(alloc(n * sizeof(T))); }
+    void release(void* p) {
+        if (!p) return;
+        auto it = std::find(ptrs.begin(), ptrs.end(), p);
+        if (it == ptrs.end()) return;
+        ptrs.erase(it);
+        if (ff) ff(p, (void*)s, ctx);
+        else cudaFreeAsync(p, s);
+    }
+    void release_all() {
+        for (void* p : ptrs) {
+            if (ff) ff(p, (void*)s, ctx);
+            else cudaFreeAsync(p, s);
+        }
+        ptrs.clear();
+    }
+};
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+struct StageEv {
+    int stage;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct kmc_job {
+    cudaStream_t s = 0;
+    int k = 0, p = 0, key_words = 1;
+    uint32_t ci = 1, cx = 0;
+    kmc_options opt{};
+    Arena arena;
+    void* surv_keys = nullptr;
+    uint32_t* surv_counts = nullptr;
+    uint64_t n_surv = 0;
+    kmc_stats st{};
+    int launches = 0;
+    std::vector<StageEv> evs;
+    int cur_stage = -1;
+    cudaEvent_t cur_a = nullptr;
+    unsigned long long* host_small = nullptr;  // pinned readback area
+
+    void stage_begin(int stage) {
+        cur_stage = stage;
+        if (!opt.profile) return;
+        CK(cudaEventCreate(&cur_a));
+        CK(cudaEventRecord(cur_a, s));
+    }
+    void stage_end(int launches_in_stage) {
+        if (cur_stage >= 0) st.stage_launches[cur_stage] += launches_in_stage;
+        if (opt.profile && cur_a) {
+            cudaEvent_t b;
+            CK(cudaEventCreate(&b));
+            CK(cudaEventRecord(b, s));
+            evs.push_back({cur_stage, cur_a, b});
+        }
+        cur_stage = -1;
+        cur_a = nullptr;
+    }
+    void collect_profile() {
+        for (auto& e : evs) {
+            float ms = 0;
+            if (cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess) st.stage_ms[e.stage] += ms;
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        evs.clear();
+    }
+    ~kmc_job() {
+        for (auto& e : evs) {
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        if (cur_a) cudaEventDestroy(cur_a);
+        arena.release_all();
+        if (host_small) cudaFreeHost(host_small);
+    }
+};
+
+namespace {
+
+kmc_status validate(int k, int p, uint32_t ci, uint32_t cx) {
+    if (k < 1 || k > 64) {
+        set_err("k=%d outside [1, 64]", k);
+        return KMC_ERR_INVALID_ARG;
+    }
+    if (p < 1 || p > 12 || p > k) {
+        set_err("p=%d outside [1, min(k, 12)] (k=%d)", p, k);
+        return KMC_ERR_INVALID_ARG;
+    }
+    if (ci == 0) ci = 1;
+    if (cx < ci) {
+        set_err("cutoff_max=%u < cutoff_min=%u", cx, ci);
+        return KMC_ERR_INVALID_ARG;
+    }
+    return KMC_OK;
+}
+
+// Reads offsets[0] and offsets[n_reads] (device or host).
+void read_extent(kmc_job* j, const uint64_t* offsets, uint64_t n_reads, uint64_t* off0, uint64_t* offN) {
+    if (is_device_ptr(offsets)) {
+        CK(cudaMemcpyAsync(&j->host_small[0], offsets, 8, cudaMemcpyDeviceToHost, j->s));
+        CK(cudaMemcpyAsync(&j->host_small[1], offsets + n_reads, 8, cudaMemcpyDeviceToHost, j->s));
+        CK(cudaStreamSynchronize(j->s));
+        *off0 = j->host_small[0];
+        *offN = j->host_small[1];
+    } else {
+        *off0 = offsets[0];
+        *offN = offsets[n_reads];
+    }
+}
+
+void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads) {
+    const int k = j->k, p = j->p, kw = j->key_words;
+    const size_t ksz = kw == 1 ? 8 : 16;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    CK(cudaMallocHost(&j->host_small, 64 * sizeof(unsigned long long)));
+    j->st.n_reads = n_reads;
+    uint64_t off0 = 0, offN = 0;
+    if (n_reads > 0) read_extent(j, offsets, n_reads, &off0, &offN);
+    if (offN < off0) {
+        set_err("read_offsets decreasing: offsets[0]=%llu > offsets[n]=%llu", (unsigned long long)off0,
+                (unsigned long long)offN);
+        throw Fail{KMC_ERR_INVALID_ARG};
+    }
+    const uint64_t n_bases = offN - off0;
+    j->st.n_bases = n_bases;
+    if (n_bases == 0 || (uint64_t)k > n_bases) {
+        j->n_surv = 0;
+        return;
+    }
+    if (n_bases >= (1ull << 36)) {
+        set_err("n_bases=%llu exceeds the per-call limit 2^36", (unsigned long long)n_bases);
+        throw Fail{KMC_ERR_INVALID_ARG};
+    }
+    // ---- inputs on the device
+    const uint8_t* d_reads = reads;
+    const uint64_t* d_off = offsets;
+    j->stage_begin(KMC_STAGE_INPUT);
+    if (!is_device_ptr(reads)) {
+        uint8_t* r = ar.get<uint8_t>(n_bases);
+        CK(cudaMemcpyAsync(r, reads, n_bases, cudaMemcpyHostToDevice, s));
+        d_reads = r;
+    }
+    if (!is_device_ptr(offsets)) {
+        uint64_t* o = ar.get<uint64_t>(n_reads + 1);
+        CK(cudaMemcpyAsync(o, offsets, (n_reads + 1) * 8, cudaMemcpyHostToDevice, s));
+        d_off = o;
+    }
+    j->stage_end(0);
+
+    // ---- pass 1: S1-S3 + per-signature histogram
+    const uint64_t ns = (1ull << (2 * p)) + 1;
+    unsigned long long* hist_w = ar.get<unsigned long long>(ns);
+    uint32_t* hist_r = ar.get<uint32_t>(ns);
+    unsigned long long* gstats = ar.get<unsigned long long>(GS_N);
+    const uint64_t n_tiles = p1_num_tiles(n_bases);
+    uint64_t* tile_r_lo = ar.get<uint64_t>(n_tiles);
+    j->stage_begin(KMC_STAGE_SIGNATURE);
+    CK(cudaMemsetAsync(hist_w, 0, ns * 8, s));
+    CK(cudaMemsetAsync(hist_r, 0, ns * 4, s));
+    CK(cudaMemsetAsync(gstats, 0, GS_N * 8, s));
+    CK(launch_tile_reads(d_off, n_reads, off0, n_tiles, tile_r_lo, s));
+    P1Args a{};
+    a.reads = d_reads;
+    a.offsets = d_off;
+    a.n_reads = n_reads;
+    a.off0 = off0;
+    a.n_bases = n_bases;
+    a.k = k;
+    a.p = p;
+    a.reads_aligned16 = ((uintptr_t)d_reads & 15) == 0;
+    a.tile_r_lo = tile_r_lo;
+    a.hist_w = hist_w;
+    a.hist_r = hist_r;
+    a.gstats = gstats;
+    CK(launch_p1(P1_MODE_HIST, a, n_tiles, s));
+    j->launches += 2;
+    j->stage_end(2);
+
+    // ---- S4: plan
+    const int RW = record_words(k);
+    int cap = small_capacity(k);
+    if (j->opt.small_bin_capacity) cap = std::min<int>(cap, (int)j->opt.small_bin_capacity);
+    if (j->opt.force_large) cap = 0;
+    PlanArgs pa{};
+    pa.hist_w = hist_w;
+    pa.hist_r = hist_r;
+    pa.ns = ns;
+    pa.half_cap = std::max<uint64_t>(1, (uint64_t)cap / 2);
+    pa.recw = (uint32_t)(RW * 4 / ksz);
+    pa.cost_scan = ar.get<uint64_t>(ns + 1);
+    pa.bnd_scan = ar.get<uint64_t>(ns + 1);
+    pa.win_scan = ar.get<uint64_t>(ns + 1);
+    pa.rec_scan = ar.get<uint64_t>(ns + 1);
+    pa.sig2bin = ar.get<uint32_t>(ns);
+    pa.bin_first = ar.get<uint64_t>(ns + 1);
+    pa.bin_w = ar.get<uint64_t>(ns);
+    pa.bin_nrec = ar.get<uint64_t>(ns);
+    pa.bin_rec_off = ar.get<uint64_t>(ns);
+    pa.gstats = gstats;
+    pa.temp = ar.alloc(plan_temp_bytes(ns));
+    j->stage_begin(KMC_STAGE_PLAN);
+    int pl = 0;
+    CK(launch_plan(pa, s, &pl));
+    j->launches += pl;
+    j->stage_end(pl);
+    unsigned long long* hs = j->host_small;
+    CK(cudaMemcpyAsync(&hs[0], pa.bnd_scan + ns, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs[1], pa.win_scan + ns, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs[2], pa.rec_scan + ns, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t n_bins = hs[0], n_windows = hs[1], n_records = hs[2];
+    j->st.n_windows = n_windows;
+    j->st.n_superkmers = hs[16 + GS_SUPERKMERS];
+    j->st.n_records = n_records;
+    j->st.n_invalid_bases = hs[16 + GS_INVALID];
+    j->st.n_signatures_used = hs[16 + GS_SIGS_USED];
+    j->st.n_bins = n_bins;
+    if (hs[16 + GS_WINDOWS] != n_windows || hs[16 + GS_RECORDS] != n_records) {
+        set_err("histogram totals disagree with pass-1 counters (%llu/%llu windows, %llu/%llu records)",
+                (unsigned long long)n_windows, (unsigned long long)hs[16 + GS_WINDOWS], (unsigned long long)n_records,
+                (unsigned long long)hs[16 + GS_RECORDS]);
+        throw Fail{KMC_ERR_INTERNAL};
+    }
+    if (n_windows == 0) {
+        j->n_surv = 0;
+        return;
+    }
+    std::vector<uint64_t> bw(n_bins), bn(n_bins), bo(n_bins);
+    CK(cudaMemcpyAsync(bw.data(), pa.bin_w, n_bins * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(bn.data(), pa.bin_nrec, n_bins * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(bo.data(), pa.bin_rec_off, n_bins * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    // ---- host: classify bins (small: one CTA in SMEM; large: multi-CTA path)
+    std::vector<uint32_t> small;
+    std::vector<Piece> pieces;
+    uint64_t large_windows = 0, n_large = 0, max_bin = 0;
+    for (uint64_t b = 0; b < n_bins; ++b) {
+        if (bw[b] == 0) continue;
+        max_bin = std::max(max_bin, bw[b]);
+        const uint64_t cost = std::max<uint64_t>(bw[b], bn[b] * pa.recw);
+        if (cost <= (uint64_t)cap && !j->opt.force_large) {
+            small.push_back((uint32_t)b);
+        } else {
+            ++n_large;
+            large_windows += bw[b];
+            for (uint64_t r = 0; r < bn[b]; r += PIECE_RECORDS)
+                pieces.push_back(Piece{bo[b] + r, (uint32_t)std::min<uint64_t>(PIECE_RECORDS, bn[b] - r), 0});
+        }
+    }
+    std::sort(small.begin(), small.end(), [&](uint32_t x, uint32_t y) { return bw[x] > bw[y] || (bw[x] == bw[y] && x < y); });
+    j->st.n_large_bins = n_large;
+    j->st.large_windows = large_windows;
+    j->st.max_bin_windows = max_bin;
+
+    // ---- pass 2: S1-S3 again + S5 scatter of records into bins
+    uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4));
+    uint32_t* bin_fill = ar.get<uint32_t>(n_bins);
+    j->stage_begin(KMC_STAGE_SCATTER);
+    CK(cudaMemsetAsync(bin_fill, 0, n_bins * 4, s));
+    a.sig2bin = pa.sig2bin;
+    a.bin_rec_off = pa.bin_rec_off;
+    a.bin_fill = bin_fill;
+    a.bins = bins;
+    CK(launch_p1(P1_MODE_SCATTER, a, n_tiles, s));
+    j->launches += 1;
+    j->stage_end(1);
+    ar.release(hist_w);
+    ar.release(hist_r);
+    ar.release(pa.cost_scan);
+    ar.release(pa.bnd_scan);
+    ar.release(pa.win_scan);
+    ar.release(pa.rec_scan);
+    ar.release(pa.bin_first);
+    ar.release(pa.temp);
+
+    // ---- survivors buffer: every survivor has count >= ci, counts sum to n_windows
+    const uint64_t surv_cap = n_windows / j->ci + 1;
+    j->surv_keys = ar.alloc(surv_cap * ksz);
+    j->surv_counts = ar.get<uint32_t>(surv_cap);
+
+    // ---- S6-S8 small bins
+    if (!small.empty()) {
+        uint32_t* d_small = ar.get<uint32_t>(small.size());
+        CK(cudaMemcpyAsync(d_small, small.data(), small.size() * 4, cudaMemcpyHostToDevice, s));
+        SmallArgs sa{};
+        sa.bins = bins;
+        sa.small_list = d_small;
+        sa.bin_rec_off = pa.bin_rec_off;
+        sa.bin_nrec = pa.bin_nrec;
+        sa.bin_w = pa.bin_w;
+        sa.k = k;
+        sa.ci = j->ci;
+        sa.cx = j->cx;
+        sa.surv_keys = j->surv_keys;
+        sa.surv_counts = j->surv_counts;
+        sa.gstats = gstats;
+        j->stage_begin(KMC_STAGE_SMALL_BINS);
+        CK(launch_small_bins(sa, small.size(), s));
+        j->launches += 1;
+        j->stage_end(1);
+    }
+    // ---- S6-S8 large bins
+    if (large_windows > 0) {
+        Piece* d_pieces = ar.get<Piece>(pieces.size());
+        CK(cudaMemcpyAsync(d_pieces, pieces.data(), pieces.size() * sizeof(Piece), cudaMemcpyHostToDevice, s));
+        void* lkeys = ar.alloc(large_windows * ksz);
+        j->stage_begin(KMC_STAGE_LARGE_EXPAND);
+        CK(launch_large_expand(bins, d_pieces, pieces.size(), k, lkeys, gstats, s));
+        j->launches += 1;
+        j->stage_end(1);
+        RadixScratch rs{};
+        rs.keys_alt = ar.alloc(large_windows * ksz);
+        rs.vals_alt = nullptr;
+        const uint64_t nt = (large_windows + radix_tile_items(kw) - 1) / radix_tile_items(kw);
+        rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
+        rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+        rs.scan_temp = ar.alloc(radix_scan_temp_bytes(large_windows, kw));
+        rs.red = ar.get<unsigned long long>(4);
+        rs.red_host = hs + 40;
+        void* sorted = nullptr;
+        uint32_t* dummy = nullptr;
+        int sl = 0;
+        j->stage_begin(KMC_STAGE_LARGE_SORT);
+        CK(device_radix_sort(kw, lkeys, nullptr, large_windows, 2 * k, rs, s, &sorted, &dummy, &sl));
+        j->launches += sl;
+        j->stage_end(sl);
+        j->stage_begin(KMC_STAGE_LARGE_COMPACT);
+        CK(launch_rle(kw, sorted, large_windows, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+        j->launches += 1;
+        j->stage_end(1);
+        ar.release(lkeys);
+        ar.release(rs.keys_alt);
+        ar.release(rs.tile_hist);
+        ar.release(rs.tile_off);
+        ar.release(rs.scan_temp);
+    }
+    CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    j->n_surv = hs[16 + GS_SURV];
+    j->st.n_unique = hs[16 + GS_UNIQUE];
+    j->st.n_below_min = hs[16 + GS_BELOW];
+    j->st.n_above_max = hs[16 + GS_ABOVE];
+    if (hs[16 + GS_LARGE_KEYS] != large_windows) {
+        set_err("large-bin expansion produced %llu keys, plan says %llu", (unsigned long long)hs[16 + GS_LARGE_KEYS],
+                (unsigned long long)large_windows);
+        throw Fail{KMC_ERR_INTERNAL};
+    }
+    if (j->n_surv > surv_cap) {
+        set_err("survivor overflow");
+        throw Fail{KMC_ERR_INTERNAL};
+    }
+    ar.release(bins);
+}
+
+void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
+    const int kw = j->key_words;
+    const size_t ksz = kw == 1 ? 8 : 16;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    const uint64_t n = j->n_surv;
+    if (n == 0) return;
+    void* keys = j->surv_keys;
+    uint32_t* vals = j->surv_counts;
+    if (n > 1) {
+        RadixScratch rs{};
+        rs.keys_alt = ar.alloc(n * ksz);
+        rs.vals_alt = ar.get<uint32_t>(n);
+        const uint64_t nt = (n + radix_tile_items(kw) - 1) / radix_tile_items(kw);
+        rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
+        rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+        rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n, kw));
+        rs.red = ar.get<unsigned long long>(4);
+        rs.red_host = j->host_small + 40;
+        int sl = 0;
+        j->stage_begin(KMC_STAGE_ORDER);
+        CK(device_radix_sort(kw, keys, vals, n, 2 * j->k, rs, s, &keys, &vals, &sl));
+        j->launches += sl;
+        j->stage_end(sl);
+    }
+    j->stage_begin(KMC_STAGE_OUTPUT);
+    CK(cudaMemcpyAsync(out_kmers, keys, n * ksz, cudaMemcpyDefault, s));
+    CK(cudaMemcpyAsync(out_counts, vals, n * 4, cudaMemcpyDefault, s));
+    j->stage_end(0);
+}
+
+}  // namespace
+
+extern "C" {
+
+void kmc_set_allocator(kmc_alloc_fn alloc_fn, kmc_free_fn free_fn, void* ctx) {
+    std::lock_guard<std::mutex> g(g_alloc_mu);
+    if (alloc_fn && free_fn) {
+        g_alloc = alloc_fn;
+        g_free = free_fn;
+        g_ctx = ctx;
+    } else {
+        g_alloc = nullptr;
+        g_free = nullptr;
+        g_ctx = nullptr;
+    }
+}
+
+const char* kmc_last_error(void) { return g_err.c_str(); }
+int kmc_version(void) { return KMCGPU_VERSION; }
+
+kmc_status kmc_count_begin(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads, int k, int p,
+                           uint32_t cutoff_min, uint32_t cutoff_max, void* stream, const kmc_options* opt,
+                           kmc_job** job, uint64_t* n_out) {
+    if (!job || !n_out) {
+        set_err("job and n_out must be non-NULL");
+        return KMC_ERR_INVALID_ARG;
+    }
+    *job = nullptr;
+    *n_out = 0;
+    kmc_status v = validate(k, p, cutoff_min, cutoff_max);
+    if (v != KMC_OK) return v;
+    if (n_reads > 0 && (!reads || !read_offsets)) {
+        set_err("reads and read_offsets must be non-NULL when n_reads > 0");
+        return KMC_ERR_INVALID_ARG;
+    }
+    kmc_job* j = new kmc_job();
+    j->s = (cudaStream_t)stream;
+    j->k = k;
+    j->p = p;
+    j->key_words = k <= 32 ? 1 : 2;
+    j->ci = cutoff_min ? cutoff_min : 1;
+    j->cx = cutoff_max;
+    if (opt) j->opt = *opt;
+    j->arena.bind(j->s);
+    try {
+        run_begin(j, reads, read_offsets, n_reads);
+    } catch (const Fail& f) {
+        cudaStreamSynchronize(j->s);
+        delete j;
+        return f.st;
+    }
+    *n_out = j->n_surv;
+    *job = j;
+    return KMC_OK;
+}
+
+kmc_status kmc_count_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts, uint64_t out_capacity,
+                            kmc_stats* stats) {
+    if (!j) {
+        set_err("NULL job");
+        return KMC_ERR_INVALID_ARG;
+    }
+    kmc_status st = KMC_OK;
+    if (out_capacity < j->n_surv) {
+        set_err("out_capacity=%llu < n_out=%llu", (unsigned long long)out_capacity, (unsigned long long)j->n_surv);
+        st = KMC_ERR_OUT_CAPACITY;
+    } else if (j->n_surv > 0 && (!out_kmers || !out_counts)) {
+        set_err("NULL output buffers");
+        st = KMC_ERR_INVALID_ARG;
+    } else {
+        try {
+            run_finish(j, out_kmers, out_counts);
+            CK(cudaStreamSynchronize(j->s));
+        } catch (const Fail& f) {
+            st = f.st;
+        }
+    }
+    cudaStreamSynchronize(j->s);
+    j->collect_profile();
+    j->st.n_out = j->n_surv;
+    j->st.n_launches = (uint64_t)j->launches;
+    if (stats) *stats = j->st;
+    delete j;
+    return st;
+}
+
+void kmc_job_free(kmc_job* j) {
+    if (!j) return;
+    cudaStreamSynchronize(j->s);
+    delete j;
+}
+
+kmc_status kmc_count_ex(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads, int k, int p,
+                        uint32_t cutoff_min, uint32_t cutoff_max, uint64_t* out_kmers, uint32_t* out_counts,
+                        uint64_t out_capacity, kmc_stats* stats, void* stream, const kmc_options* opt) {
+    kmc_job* j = nullptr;
+    uint64_t n = 0;
+    kmc_status st = kmc_count_begin(reads, read_offsets, n_reads, k, p, cutoff_min, cutoff_max, stream, opt, &j, &n);
+    if (st != KMC_OK) return st;
+    return kmc_count_finish(j, out_kmers, out_counts, out_capacity, stats);
+}
+
+kmc_status kmc_count(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads, int k, int p,
+                     uint32_t cutoff_min, uint32_t cutoff_max, uint64_t* out_kmers, uint32_t* out_counts,
+                     uint64_t out_capacity, kmc_stats* stats, void* stream) {
+    return kmc_count_ex(reads, read_offsets, n_reads, k, p, cutoff_min, cutoff_max, out_kmers, out_counts,
+                        out_capacity, stats, stream, nullptr);
+}
+
+kmc_status kmc_debug_signatures(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads, int k, int p,
+                                uint32_t* out_sig, void* stream) {
+    kmc_status v = validate(k, p, 1, 1);
+    if (v != KMC_OK) return v;
+    kmc_job j;
+    j.s = (cudaStream_t)stream;
+    j.k = k;
+    j.p = p;
+    j.arena.bind(j.s);
+    try {
+        CK(cudaMallocHost(&j.host_small, 64 * sizeof(unsigned long long)));
+        if (n_reads == 0) return KMC_OK;
+        uint64_t off0, offN;
+        read_extent(&j, read_offsets, n_reads, &off0, &offN);
+        const uint64_t n_bases = offN - off0;
+        if (n_bases == 0) return KMC_OK;
+        const uint8_t* d_reads = reads;
+        const uint64_t* d_off = read_offsets;
+        if (!is_device_ptr(reads)) {
+            uint8_t* r = j.arena.get<uint8_t>(n_bases);
+            CK(cudaMemcpyAsync(r, reads, n_bases, cudaMemcpyHostToDevice, j.s));
+            d_reads = r;
+        }
+        if (!is_device_ptr(read_offsets)) {
+            uint64_t* o = j.arena.get<uint64_t>(n_reads + 1);
+            CK(cudaMemcpyAsync(o, read_offsets, (n_reads + 1) * 8, cudaMemcpyHostToDevice, j.s));
+            d_off = o;
+        }
+        uint32_t* d_out = out_sig;
+        const bool host_out = !is_device_ptr(out_sig);
+        if (host_out) d_out = j.arena.get<uint32_t>(n_bases);
+        const uint64_t n_tiles = p1_num_tiles(n_bases);
+        uint64_t* tile_r_lo = j.arena.get<uint64_t>(n_tiles);
+        CK(launch_tile_reads(d_off, n_reads, off0, n_tiles, tile_r_lo, j.s));
+        P1Args a{};
+        a.reads = d_reads;
+        a.offsets = d_off;
+        a.n_reads = n_reads;
+        a.off0 = off0;
+        a.n_bases = n_bases;
+        a.k = k;
+        a.p = p;
+        a.reads_aligned16 = ((uintptr_t)d_reads & 15) == 0;
+        a.tile_r_lo = tile_r_lo;
+        a.dbg_sig = d_out;
+        CK(launch_p1(P1_MODE_DEBUG, a, n_tiles, j.s));
+        if (host_out) CK(cudaMemcpyAsync(out_sig, d_out, n_bases * 4, cudaMemcpyDeviceToHost, j.s));
+        CK(cudaStreamSynchronize(j.s));
+    } catch (const Fail& f) {
+        cudaStreamSynchronize(j.s);
+        return f.st;
+    }
+    return KMC_OK;
+}
+
+kmc_status kmc_debug_allowed(int p, uint8_t* out_allowed, void* stream) {
+    if (p < 1 || p > 12) {
+        set_err("p=%d outside [1, 12]", p);
+        return KMC_ERR_INVALID_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena ar;
+    ar.bind(s);
+    try {
+        const uint64_t n = 1ull << (2 * p);
+        uint8_t* d = out_allowed;
+        const bool host_out = !is_device_ptr(out_allowed);
+        if (host_out) d = ar.get<uint8_t>(n);
+        CK(launch_debug_allowed(p, d, s));
+        if (host_out) CK(cudaMemcpyAsync(out_allowed, d, n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    } catch (const Fail& f) {
+        ar.release_all();
+        return f.st;
+    }
+    ar.release_all();
+    return KMC_OK;
+}
+
+}  // extern "C"

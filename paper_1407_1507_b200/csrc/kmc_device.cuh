@@ -1,0 +1,282 @@
+// kmc_device.cuh -- device building blocks shared by the kmcgpu kernels (sm_100a).
+//
+// Keys: canonical k-mer values, 2 bits per symbol, leftmost symbol most significant
+// (Suppl. Sec. 4).  k <= 32 -> uint64_t; 33 <= k <= 64 -> K128 {lo, hi}.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kmc {
+
+constexpr int RADIX_BITS = 8;
+constexpr int RADIX = 1 << RADIX_BITS;
+
+struct __align__(16) K128 {
+    uint64_t lo, hi;
+};
+
+// ---------------------------------------------------------------- key operations
+__device__ __forceinline__ bool key_lt(uint64_t a, uint64_t b) { return a < b; }
+__device__ __forceinline__ bool key_lt(const K128& a, const K128& b) {
+    return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
+}
+__device__ __forceinline__ bool key_eq(uint64_t a, uint64_t b) { return a == b; }
+__device__ __forceinline__ bool key_eq(const K128& a, const K128& b) { return a.hi == b.hi && a.lo == b.lo; }
+__device__ __forceinline__ uint32_t key_digit(uint64_t a, int shift) { return (uint32_t)(a >> shift) & (RADIX - 1); }
+__device__ __forceinline__ uint32_t key_digit(const K128& a, int shift) {
+    return shift < 64 ? (uint32_t)(a.lo >> shift) & (RADIX - 1) : (uint32_t)(a.hi >> (shift - 64)) & (RADIX - 1);
+}
+__device__ __forceinline__ uint64_t key_min(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ K128 key_min(const K128& a, const K128& b) { return key_lt(b, a) ? b : a; }
+
+// Rolling forward / reverse-complement values of a k-mer: pushing symbol c
+// (0..3) at the right end: fwd = fwd*4 + c (mod 4^k); the reverse complement gains the
+// complement 3-c at its most significant position: rc = rc/4 + (3-c)*4^(k-1).
+struct Roll64 {
+    uint64_t fwd = 0, rc = 0, mask;
+    int top;  // 2k-2
+    __device__ __forceinline__ explicit Roll64(int k) {
+        mask = (k >= 32) ? ~0ull : ((1ull << (2 * k)) - 1);
+        top = 2 * k - 2;
+    }
+    __device__ __forceinline__ void push(uint32_t c) {
+        fwd = ((fwd << 2) | c) & mask;
+        rc = (rc >> 2) | ((uint64_t)(3u - c) << top);
+    }
+    __device__ __forceinline__ uint64_t canon() const { return fwd < rc ? fwd : rc; }
+};
+
+struct Roll128 {  // 33 <= k <= 64
+    uint64_t flo = 0, fhi = 0, rlo = 0, rhi = 0, hmask;
+    int htop;  // 2k-2-64
+    __device__ __forceinline__ explicit Roll128(int k) {
+        int hb = 2 * k - 64;
+        hmask = (hb >= 64) ? ~0ull : ((1ull << hb) - 1);
+        htop = 2 * k - 2 - 64;
+    }
+    __device__ __forceinline__ void push(uint32_t c) {
+        fhi = ((fhi << 2) | (flo >> 62)) & hmask;
+        flo = (flo << 2) | c;
+        rlo = (rlo >> 2) | (rhi << 62);
+        rhi = (rhi >> 2) | ((uint64_t)(3u - c) << htop);
+    }
+    __device__ __forceinline__ K128 canon() const {
+        K128 f{flo, fhi}, r{rlo, rhi};
+        return key_lt(r, f) ? r : f;
+    }
+};
+
+template <class K> struct RollFor;
+template <> struct RollFor<uint64_t> { using T = Roll64; };
+template <> struct RollFor<K128> { using T = Roll128; };
+
+// ---------------------------------------------------------------- signature rule
+// P:L206-208 (Sec. 2.2): canonical minimizers that "do not start with AAA, neither start
+// with ACA, neither contain AA anywhere except at their beginning" -- applied to the
+// canonical p-mer x (2p bits, leftmost symbol most significant).  isA marks the low bit
+// of every 2-bit group equal to 00; aa marks adjacent A pairs, the pair at positions
+// (0,1) removed.
+__device__ __forceinline__ bool sig_allowed(uint32_t x, int p) {
+    if (p < 3) return true;  // no 3-symbol prefix and no AA pair after position 0 exist
+    uint32_t m2 = (p >= 16) ? 0xFFFFFFFFu : ((1u << (2 * p)) - 1);
+    uint32_t isA = ~(x | (x >> 1)) & 0x55555555u & m2;
+    uint32_t aa = isA & (isA >> 2) & ~(1u << (2 * (p - 2)));
+    uint32_t pre3 = x >> (2 * (p - 3));
+    return aa == 0 && pre3 != 0u && pre3 != 4u;
+}
+
+// ---------------------------------------------------------------- record format (bins)
+// A bin record holds a piece of one super-k-mer: RW 32-bit words, big-endian bit string:
+// bits [0,8) = number of windows n (1..255); bits [8+2j, 10+2j) = symbol j.
+// RW = 4 (60 symbols) for k <= 32, RW = 8 (124 symbols) for k >= 33.
+__host__ __device__ __forceinline__ int record_words(int k) { return k <= 32 ? 4 : 8; }
+__host__ __device__ __forceinline__ int record_max_windows(int k) { return 16 * record_words(k) - 4 - k + 1; }
+
+__device__ __forceinline__ uint32_t rec_nwin(const uint32_t* rec) { return rec[0] >> 24; }
+__device__ __forceinline__ uint32_t rec_sym(const uint32_t* rec, int j) {
+    int g = 8 + 2 * j;
+    return (rec[g >> 5] >> (30 - (g & 31))) & 3u;
+}
+
+// ---------------------------------------------------------------- warp / block helpers
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <class T> __device__ __forceinline__ T warp_incl_sum(T v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+    }
+    return v;
+}
+
+// Exclusive block-wide sum; wsum needs NT/32 + 1 entries of T.  All threads must call.
+template <int NT, class T> __device__ __forceinline__ T block_excl_sum(T v, T* wsum, T* total) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T inc = warp_incl_sum(v);
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        T w = (lane < NW) ? wsum[lane] : T(0);
+        T wi = warp_incl_sum(w);
+        if (lane < NW) wsum[lane] = wi - w;
+        if (lane == NW - 1) wsum[NW] = wi;
+    }
+    __syncthreads();
+    T r = wsum[warp] + inc - v;
+    if (total) *total = wsum[NW];
+    __syncthreads();
+    return r;
+}
+
+template <int NT, class T> __device__ __forceinline__ T block_sum(T v, T* wsum) {
+    T tot;
+    block_excl_sum<NT, T>(v, wsum, &tot);
+    return tot;
+}
+
+// ---------------------------------------------------------------- block radix pass
+// One stable counting-sort pass of n (<= 65535*NW) keys (and optional uint32 values)
+// from src to dst in shared memory, by the 8-bit digit at `shift`.  Warp w owns the
+// contiguous segment [w*seg, (w+1)*seg); within a round of 32 keys, ranks come from
+// __match_any_sync peers, so the pass is stable.  whist: RADIX*NW uint32 (digit-major),
+// wsum: NT/32+1 uint32.  If dstart != nullptr it receives the start of every digit
+// (RADIX+1 entries).
+template <class K, int NT, bool VALS>
+__device__ __forceinline__ void block_digit_pass(const K* src, K* dst, const uint32_t* vsrc, uint32_t* vdst,
+                                                 int n, int shift, uint32_t* whist, uint32_t* wsum,
+                                                 uint32_t* dstart) {
+    constexpr int NW = NT / 32;
+    constexpr int IPT = RADIX * NW / NT;  // 8
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < RADIX * NW; i += NT) whist[i] = 0;
+    __syncthreads();
+    int seg = (n + NW - 1) / NW;
+    seg = (seg + 31) & ~31;
+    const int beg = warp * seg, end = min(n, beg + seg);
+    for (int base = beg; base < end; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < end;
+        const uint32_t d = ok ? key_digit(src[i], shift) : (uint32_t)(RADIX + lane);
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (ok && lane == __ffs(peers) - 1) whist[d * NW + warp] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    uint32_t loc[IPT];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        loc[j] = whist[threadIdx.x * IPT + j];
+        s += loc[j];
+    }
+    uint32_t ex = block_excl_sum<NT, uint32_t>(s, wsum, nullptr);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        whist[threadIdx.x * IPT + j] = ex;
+        ex += loc[j];
+    }
+    __syncthreads();
+    if (dstart) {
+        for (int d = threadIdx.x; d < RADIX; d += NT) dstart[d] = whist[d * NW];
+        if (threadIdx.x == 0) dstart[RADIX] = n;
+    }
+    const uint32_t ltm = lanemask_lt();
+    for (int base = beg; base < end; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < end;
+        K key;
+        uint32_t d = (uint32_t)(RADIX + lane);
+        if (ok) {
+            key = src[i];
+            d = key_digit(key, shift);
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (ok) {
+            const uint32_t off = whist[d * NW + warp] + __popc(peers & ltm);
+            dst[off] = key;
+            if (VALS) vdst[off] = vsrc[i];
+        }
+        __syncwarp();
+        if (ok && lane == __ffs(peers) - 1) whist[d * NW + warp] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+}
+
+// Bitwise OR and AND over n keys in shared memory (to skip constant digits).
+__device__ __forceinline__ void key_or_and_accum(uint64_t k, uint64_t& o, uint64_t& a, uint64_t&, uint64_t&) {
+    o |= k;
+    a &= k;
+}
+__device__ __forceinline__ void key_or_and_accum(const K128& k, uint64_t& o, uint64_t& a, uint64_t& oh, uint64_t& ah) {
+    o |= k.lo;
+    a &= k.lo;
+    oh |= k.hi;
+    ah &= k.hi;
+}
+
+// Varying-bit mask of the keys (lo word, hi word); red needs 4 uint64 of shared memory.
+template <class K, int NT>
+__device__ __forceinline__ void block_varying_bits(const K* keys, int n, unsigned long long* red, uint64_t& vlo,
+                                                   uint64_t& vhi) {
+    if (threadIdx.x == 0) {
+        red[0] = 0;
+        red[1] = ~0ull;
+        red[2] = 0;
+        red[3] = ~0ull;
+    }
+    __syncthreads();
+    uint64_t o = 0, a = ~0ull, oh = 0, ah = ~0ull;
+    for (int i = threadIdx.x; i < n; i += NT) key_or_and_accum(keys[i], o, a, oh, ah);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, s);
+        a &= __shfl_xor_sync(0xffffffffu, a, s);
+        oh |= __shfl_xor_sync(0xffffffffu, oh, s);
+        ah &= __shfl_xor_sync(0xffffffffu, ah, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(&red[0], (unsigned long long)o);
+        atomicAnd(&red[1], (unsigned long long)a);
+        atomicOr(&red[2], (unsigned long long)oh);
+        atomicAnd(&red[3], (unsigned long long)ah);
+    }
+    __syncthreads();
+    vlo = red[0] ^ red[1];
+    vhi = red[2] ^ red[3];
+    if (n == 0) vlo = vhi = 0;
+    __syncthreads();
+}
+
+__device__ __forceinline__ bool digit_varies(uint64_t vlo, uint64_t vhi, int shift) {
+    return shift < 64 ? ((vlo >> shift) & (RADIX - 1)) != 0 : ((vhi >> (shift - 64)) & (RADIX - 1)) != 0;
+}
+
+// LSD radix sort of n keys (+ optional values) in shared memory over bits [0, nbits),
+// skipping digits that are constant across the keys.  Returns 0 if the result is in
+// (a, va), 1 if in (b, vb).
+template <class K, int NT, bool VALS>
+__device__ __forceinline__ int block_radix_sort(K* a, K* b, uint32_t* va, uint32_t* vb, int n, int nbits,
+                                                uint32_t* whist, uint32_t* wsum, unsigned long long* red) {
+    uint64_t vlo, vhi;
+    block_varying_bits<K, NT>(a, n, red, vlo, vhi);
+    int cur = 0;
+    for (int shift = 0; shift < nbits; shift += RADIX_BITS) {
+        if (!digit_varies(vlo, vhi, shift)) continue;
+        if (cur == 0)
+            block_digit_pass<K, NT, VALS>(a, b, va, vb, n, shift, whist, wsum, nullptr);
+        else
+            block_digit_pass<K, NT, VALS>(b, a, vb, va, n, shift, whist, wsum, nullptr);
+        cur ^= 1;
+    }
+    return cur;
+}
+
+}  // namespace kmc

@@ -1,0 +1,130 @@
+// kmc_internal.h -- host-side declarations shared by the kmcgpu translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kmc {
+
+// global statistics slots (device unsigned long long[GS_N])
+enum {
+    GS_WINDOWS = 0,
+    GS_SUPERKMERS = 1,
+    GS_RECORDS = 2,
+    GS_INVALID = 3,
+    GS_UNIQUE = 4,
+    GS_BELOW = 5,
+    GS_ABOVE = 6,
+    GS_SURV = 7,        // survivor cursor
+    GS_LARGE_KEYS = 8,  // large-bin key cursor
+    GS_SIGS_USED = 9,
+    GS_N = 16
+};
+
+// ------------------------------------------------------------ phase 1 (distribution)
+constexpr int P1_TILE = 4096;  // window starts per CTA
+constexpr int P1_NT = 256;
+
+struct P1Args {
+    const uint8_t* reads;
+    const uint64_t* offsets;
+    uint64_t n_reads;
+    uint64_t off0;
+    uint64_t n_bases;
+    int k, p;
+    int reads_aligned16;
+    const uint64_t* tile_r_lo;  // first read index whose start lies after each tile's left edge
+    // pass 1
+    unsigned long long* hist_w;  // [4^p + 1]
+    uint32_t* hist_r;            // [4^p + 1]
+    unsigned long long* gstats;
+    // pass 2
+    const uint32_t* sig2bin;
+    const uint64_t* bin_rec_off;
+    uint32_t* bin_fill;
+    uint32_t* bins;
+    // debug
+    uint32_t* dbg_sig;
+};
+
+enum { P1_MODE_HIST = 0, P1_MODE_SCATTER = 1, P1_MODE_DEBUG = 2 };
+
+uint64_t p1_num_tiles(uint64_t n_bases);
+cudaError_t launch_tile_reads(const uint64_t* offsets, uint64_t n_reads, uint64_t off0, uint64_t n_tiles,
+                              uint64_t* tile_r_lo, cudaStream_t s);
+cudaError_t launch_p1(int mode, const P1Args& a, uint64_t n_tiles, cudaStream_t s);
+cudaError_t launch_debug_allowed(int p, uint8_t* out, cudaStream_t s);
+
+// ------------------------------------------------------------ scans / plan
+// out[0..n] exclusive prefix sums (out[n] = total) of in[0..n) (uint64).
+size_t scan_temp_bytes(uint64_t n);
+cudaError_t scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, void* temp, cudaStream_t s);
+cudaError_t scan_u32_to_u32(const uint32_t* in, uint32_t* out, uint64_t n, void* temp, cudaStream_t s);
+
+struct PlanArgs {
+    const unsigned long long* hist_w;
+    const uint32_t* hist_r;
+    uint64_t ns;          // 4^p + 1
+    uint64_t half_cap;    // small-bin cost grouping threshold (capacity / 2)
+    uint32_t recw;        // record cost in key units
+    // outputs / temps (ns + 1 entries each unless noted)
+    uint64_t* cost_scan;  // P
+    uint64_t* bnd_scan;   // B
+    uint64_t* win_scan;   // Wp
+    uint64_t* rec_scan;   // Rp
+    uint32_t* sig2bin;    // [ns]
+    uint64_t* bin_first;  // [ns + 1]
+    uint64_t* bin_w;      // [ns]
+    uint64_t* bin_nrec;   // [ns]
+    uint64_t* bin_rec_off;// [ns]
+    unsigned long long* gstats;
+    void* temp;
+};
+size_t plan_temp_bytes(uint64_t ns);
+cudaError_t launch_plan(const PlanArgs& a, cudaStream_t s, int* n_launches);
+
+// ------------------------------------------------------------ phase 2 (sorting)
+struct SmallArgs {
+    const uint32_t* bins;
+    const uint32_t* small_list;   // bin ids
+    const uint64_t* bin_rec_off;
+    const uint64_t* bin_nrec;
+    const uint64_t* bin_w;
+    int k;
+    uint32_t ci, cx;
+    void* surv_keys;              // K*
+    uint32_t* surv_counts;
+    unsigned long long* gstats;
+};
+int small_capacity(int k);  // max windows per small bin for this key width
+cudaError_t launch_small_bins(const SmallArgs& a, uint64_t n_small, cudaStream_t s);
+
+struct Piece {
+    uint64_t rec_begin;
+    uint32_t nrec;
+    uint32_t pad;
+};
+constexpr int PIECE_RECORDS = 1024;
+cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, void* keys,
+                                unsigned long long* gstats, cudaStream_t s);
+
+// Device-wide LSD radix sort of n keys (+ optional uint32 values).  Result lands in
+// (*res_keys, *res_vals) which is either the input or the alternate buffers.
+struct RadixScratch {
+    void* keys_alt;
+    uint32_t* vals_alt;
+    uint32_t* tile_hist;   // RADIX * ntiles
+    uint32_t* tile_off;    // RADIX * ntiles
+    void* scan_temp;
+    unsigned long long* red;  // 4 entries
+    unsigned long long* red_host;  // pinned 4 entries
+};
+uint64_t radix_tile_items(int key_words);
+size_t radix_scan_temp_bytes(uint64_t n, int key_words);
+cudaError_t device_radix_sort(int key_words, void* keys, uint32_t* vals, uint64_t n, int nbits,
+                              const RadixScratch& rs, cudaStream_t s, void** res_keys, uint32_t** res_vals,
+                              int* n_launches);
+
+cudaError_t launch_rle(int key_words, const void* keys, uint64_t n, uint32_t ci, uint32_t cx, void* surv_keys,
+                       uint32_t* surv_counts, unsigned long long* gstats, cudaStream_t s);
+
+}  // namespace kmc

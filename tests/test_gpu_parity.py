@@ -1,0 +1,245 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI vs the CPU oracle, element by element.
+
+Bit-exact is the bar everywhere (integer keys and counts).  Small and reduced configs are
+compared in full; BASELINE.json's full-size configs are compared on sampled outputs that
+the oracle counts one by one, plus properties that hold at any size.
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev(w):
+    r = torch.from_numpy(w.reads).cuda() if w.reads.size else torch.zeros(0, dtype=torch.uint8, device="cuda")
+    o = torch.from_numpy(w.offsets.view(np.uint64)).cuda()
+    return r, o
+
+
+def gpu_count(kmc, w, k=None, p=None, ci=None, cx=None, **kw):
+    r, o = to_dev(w)
+    res = kmc.count(r, o, k or w.k, p or w.p, w.cutoff_min if ci is None else ci,
+                    w.cutoff_max if cx is None else cx, **kw)
+    keys = res.kmers.cpu().numpy()
+    counts = res.counts.cpu().numpy()
+    return keys, counts, res.stats
+
+
+def assert_same(kmc, w, k=None, p=None, ci=None, cx=None, **kw):
+    k = k or w.k
+    ci = w.cutoff_min if ci is None else ci
+    cx = w.cutoff_max if cx is None else cx
+    keys, counts, st = gpu_count(kmc, w, k, p, ci, cx, **kw)
+    ref = oracle.count(w.reads, w.offsets, k, ci, cx)
+    assert keys.shape[0] == ref.keys.shape[0], (keys.shape, ref.keys.shape)
+    assert np.array_equal(keys, ref.keys)
+    assert np.array_equal(counts, ref.counts)
+    assert st["n_windows"] == ref.n_windows
+    assert st["n_unique"] == ref.n_unique
+    assert st["n_below_min"] == ref.n_below_min
+    assert st["n_above_max"] == ref.n_above_max
+    assert st["n_out"] == ref.n_out
+    return st
+
+
+# ---------------------------------------------------------------- S2: signatures
+
+def test_allowed_rule_matches_oracle(gpu):
+    for p in range(1, 9):
+        dev = gpu.debug_allowed(p)
+        ref = np.array([oracle.allowed_index(i, p) for i in range(4 ** p)], dtype=np.uint8)
+        assert np.array_equal(dev, ref), p
+
+
+def _sig_case(gpu, w, k, p):
+    r, o = to_dev(w)
+    got = gpu.debug_signatures(r, o, k, p).cpu().numpy()
+    ref = oracle.signatures(w.reads, w.offsets, k, p, True)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, (k, p, bad[:10], got[bad[:10]], ref[bad[:10]])
+
+
+def test_signature_fig1_golden(gpu):
+    w = synth.from_strings(["CGTTGATCAATTTG"], 8)
+    r, o = to_dev(w)
+    got = gpu.debug_signatures(r, o, 8, 4).cpu().numpy()
+    sig = [oracle.str_value(s) for s in ("AACG", "ATCA", "ATCA", "ATCA", "AATT", "AATT", "AATT")]
+    assert got[:7].tolist() == sig and all(x == 0xFFFFFFFF for x in got[7:])
+
+
+@pytest.mark.parametrize("k,p", [(25, 7), (28, 9), (31, 9), (55, 11), (64, 12), (8, 8), (12, 3), (5, 1), (33, 5)])
+def test_signature_parity_random(gpu, k, p):
+    seqs = synth.random_reads(k * 100 + p, 400, 0, 300, n_frac=0.01, lower_frac=0.02)
+    _sig_case(gpu, synth.from_strings(seqs, k), k, p)
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 0.02), ("C5", 0.002), ("C4", 0.0002), ("C3", 0.002)])
+def test_signature_parity_configs(gpu, name, scale):
+    w = synth.make(name, scale=scale)
+    _sig_case(gpu, w, w.k, w.p)
+
+
+def test_superkmer_count(gpu):
+    w = synth.make("C5", scale=0.002)
+    _, _, st = gpu_count(gpu, w)
+    assert st["n_superkmers"] == len(oracle.superkmers(w.reads, w.offsets, w.k, w.p))
+
+
+# ---------------------------------------------------------------- end-to-end parity
+
+@pytest.mark.parametrize("name,scale", [("C1", 1.0), ("C2", 0.02), ("C3", 0.02), ("C4", 0.001), ("C5", 0.02)])
+def test_count_parity_configs(gpu, name, scale):
+    st = assert_same(gpu, synth.make(name, scale=scale))
+    assert st["n_superkmers"] > 0 and st["n_bins"] > 0
+
+
+@pytest.mark.parametrize("opts", [dict(force_large=True), dict(small_bin_capacity=64), dict(small_bin_capacity=1024)])
+def test_forced_paths(gpu, opts):
+    w = synth.make("C5", scale=0.005)
+    st = assert_same(gpu, w, **opts)
+    if opts.get("force_large"):
+        assert st["large_windows"] == st["n_windows"]
+
+
+def test_p_invariance(gpu):
+    w = synth.make("C2", scale=0.005)
+    outs = []
+    for p in (3, 5, 7, 9, 11, 12):
+        keys, counts, _ = gpu_count(gpu, w, p=p)
+        outs.append((keys, counts))
+    for keys, counts in outs[1:]:
+        assert np.array_equal(keys, outs[0][0]) and np.array_equal(counts, outs[0][1])
+
+
+def test_revcomp_and_permutation_invariance(gpu):
+    w = synth.make("C1", scale=0.05)
+    seqs = [bytes(w.reads[w.offsets[i]:w.offsets[i + 1]]).decode() for i in range(w.n_reads)]
+    rnd = random.Random(3)
+    flipped = [oracle.revcomp_str(s) if rnd.random() < 0.5 else s for s in seqs]
+    rnd.shuffle(flipped)
+    w2 = synth.from_strings(flipped, w.k, w.p, 1)
+    a = gpu_count(gpu, w, ci=1)
+    b = gpu_count(gpu, w2, ci=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 15, 16, 17, 31, 32, 33, 47, 63, 64])
+def test_k_boundaries(gpu, k):
+    p = min(k, 5)
+    seqs = synth.random_reads(k, 600, 0, 200, n_frac=0.01, lower_frac=0.01, alphabet=b"ACGT")
+    assert_same(gpu, synth.from_strings(seqs, k, p, 1))
+
+
+def test_low_complexity_and_skew(gpu):
+    seqs = ["A" * 300, "T" * 250, "AT" * 120, "ACGT" * 60, "N" * 50, "", "ACG", "CA" * 100] * 50
+    seqs += [s.decode() for s in synth.random_reads(9, 200, 50, 250)]
+    for k, p in ((31, 9), (28, 7), (55, 11), (21, 3)):
+        assert_same(gpu, synth.from_strings(seqs, k, p, 2))
+
+
+def test_edge_cases(gpu):
+    # empty input
+    keys, counts, st = gpu_count(gpu, synth.from_strings([], 25, 7, 1))
+    assert keys.shape[0] == 0 and st["n_windows"] == 0
+    # all reads shorter than k; all-N
+    for seqs in (["ACGT", "ACG", ""], ["N" * 100, "n" * 40]):
+        keys, counts, st = gpu_count(gpu, synth.from_strings(seqs, 25, 7, 1))
+        assert keys.shape[0] == 0 and st["n_windows"] == 0
+    # cutoffs that remove everything
+    w = synth.make("C1", scale=0.01)
+    keys, counts, st = gpu_count(gpu, w, ci=10**6, cx=10**9)
+    assert keys.shape[0] == 0 and st["n_below_min"] == st["n_unique"]
+    # cutoff_max removes the frequent ones; ci = 0 treated as 1
+    assert_same(gpu, w, ci=0, cx=1)
+    # lowercase + non-ACGT bytes
+    seqs = synth.random_reads(11, 300, 20, 200, n_frac=0.05, lower_frac=0.3, alphabet=b"ACGTRYacgt")
+    assert_same(gpu, synth.from_strings(seqs, 21, 7, 1))
+
+
+def test_offsets_base_and_misaligned_pointer(gpu):
+    w = synth.make("C1", scale=0.01)
+    pad = 5
+    reads = np.concatenate([np.frombuffer(b"NNNNN", dtype=np.uint8), w.reads])
+    r = torch.from_numpy(reads).cuda()[pad:]                      # misaligned device pointer
+    o = torch.from_numpy((w.offsets + np.uint64(1000)).view(np.uint64)).cuda()  # offsets[0] != 0
+    res = gpu.count(r, o, w.k, w.p, 1, 10**9)
+    ref = oracle.count(w.reads, w.offsets, w.k, 1, 10**9)
+    assert np.array_equal(res.kmers.cpu().numpy(), ref.keys) and np.array_equal(res.counts.cpu().numpy(), ref.counts)
+
+
+def test_host_buffers_and_capacity(gpu):
+    w = synth.make("C5", scale=0.002)
+    rh = torch.from_numpy(w.reads).pin_memory()
+    oh = torch.from_numpy(w.offsets.view(np.uint64))
+    res = gpu.count(rh, oh, w.k, w.p, 2, 10**9, out_device="cpu")
+    ref = oracle.count(w.reads, w.offsets, w.k, 2, 10**9)
+    assert np.array_equal(res.kmers.numpy(), ref.keys) and np.array_equal(res.counts.numpy(), ref.counts)
+    # one-call form: too small capacity -> KMC_ERR_OUT_CAPACITY with the required count
+    r, o = to_dev(w)
+    small_k = torch.empty(1, dtype=torch.uint64, device="cuda")
+    small_c = torch.empty(1, dtype=torch.uint32, device="cuda")
+    with pytest.raises(gpu.KmcError) as ei:
+        gpu.count_into(r, o, w.k, w.p, 2, 10**9, small_k, small_c)
+    assert ei.value.status == gpu.KMC_ERR_OUT_CAPACITY
+    ok_k = torch.empty(ref.n_out, dtype=torch.uint64, device="cuda")
+    ok_c = torch.empty(ref.n_out, dtype=torch.uint32, device="cuda")
+    st = gpu.count_into(r, o, w.k, w.p, 2, 10**9, ok_k, ok_c)
+    assert st["n_out"] == ref.n_out and np.array_equal(ok_k.cpu().numpy(), ref.keys)
+
+
+def test_invalid_args(gpu):
+    w = synth.make("C1", scale=0.001)
+    r, o = to_dev(w)
+    for k, p, ci, cx in ((0, 1, 1, 10), (65, 9, 1, 10), (25, 13, 1, 10), (5, 7, 1, 10), (25, 7, 5, 4)):
+        with pytest.raises(gpu.KmcError) as ei:
+            gpu.count(r, o, k, p, ci, cx)
+        assert ei.value.status == gpu.KMC_ERR_INVALID_ARG
+
+
+def test_deterministic(gpu):
+    w = synth.make("C5", scale=0.005)
+    a = gpu_count(gpu, w)
+    b = gpu_count(gpu, w, small_bin_capacity=512)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ---------------------------------------------------------------- full-size configs (sampled)
+
+def _sampled_full(gpu, name, n_sample=400):
+    w = synth.make(name)
+    keys, counts, st = gpu_count(gpu, w)
+    ci, cx = w.cutoff_min, w.cutoff_max
+    # properties at any size: strictly ascending keys, counts within cutoffs, window total
+    if keys.ndim == 1:
+        assert np.all(keys[1:] > keys[:-1])
+    else:
+        hi, lo = keys[:, 1], keys[:, 0]
+        assert np.all((hi[1:] > hi[:-1]) | ((hi[1:] == hi[:-1]) & (lo[1:] > lo[:-1])))
+    assert counts.min() >= ci and counts.max() <= cx
+    assert st["n_windows"] == oracle.n_windows_parallel(w.reads, w.offsets, w.k)
+    assert st["n_unique"] == st["n_out"] + st["n_below_min"] + st["n_above_max"]
+    assert int(counts.sum(dtype=np.uint64)) <= st["n_windows"]
+    # sampled survivors: exact counts from the oracle, one key at a time
+    rng = np.random.default_rng(17)
+    idx = np.sort(rng.choice(keys.shape[0], min(n_sample, keys.shape[0]), replace=False))
+    q = keys[idx]
+    ref = oracle.count_queries(w.reads, w.offsets, w.k, q)
+    assert np.array_equal(ref, counts[idx].astype(np.uint64))
+    return st
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_full_config_sampled(gpu, name):
+    _sampled_full(gpu, name)
+
+
+@pytest.mark.slow
+def test_full_c4_sampled(gpu):
+    st = _sampled_full(gpu, "C4", n_sample=200)
+    assert st["n_windows"] > 2_500_000_000
