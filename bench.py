@@ -44,15 +44,17 @@ def stage_bytes(st: dict, n_reads: int, k: int) -> dict:
     rec = st["n_records"] * rw
     lw = st["large_windows"]
     nout = st["n_out"]
-    small_rec = rec * (1 - (lw / st["n_windows"] if st["n_windows"] else 0))
+    lfrac = lw / st["n_windows"] if st["n_windows"] else 0.0
+    small_rec = rec * (1 - lfrac)
+    large_rec = rec - small_rec
     return {
-        "signature": nb + off,                       # ASCII + offsets read (histogram is noise)
-        "scatter": nb + off + rec,                   # ASCII + offsets read, records written
-        "small_bins": small_rec + nout * (ksz + 4),  # records read, survivors written (upper bound share)
-        "large_expand": rec - small_rec + lw * ksz,  # records read, keys written
-        "large_sort": 2 * lw * ksz,                  # keys read + written once (per full sort)
-        "large_compact": lw * ksz,                   # sorted keys read once
-        "order": 2 * nout * (ksz + 4),               # survivors read + written once
+        "signature": nb + off,                               # ASCII + offsets read (histogram is noise)
+        "scatter": nb + off + rec,                           # ASCII + offsets read, records written
+        "small_bins": small_rec + (1 - lfrac) * nout * (ksz + 4),  # records read, survivors written
+        "large_split": 2 * large_rec + lw * ksz,             # records read (count + scatter), keys written
+        "large_chunks": lw * ksz + lfrac * nout * (ksz + 4),  # keys read, survivors written
+        "large_fallback": 2 * lw * ksz,                      # (LSD path only) keys read + written once
+        "order": 2 * nout * (ksz + 4),                       # survivors read + written once
         "output": 2 * nout * (ksz + 4),
     }
 

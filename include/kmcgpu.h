@@ -76,9 +76,11 @@ enum {
     KMC_STAGE_PLAN = 2,       /* S4: signature->bin map, bin offsets (scans) */
     KMC_STAGE_SCATTER = 3,    /* S1-S3 again + S5: super-k-mer records into HBM bins (pass 2) */
     KMC_STAGE_SMALL_BINS = 4, /* S6-S8 for bins that fit one CTA: expand + SMEM radix sort + compact */
-    KMC_STAGE_LARGE_EXPAND = 5, /* S6 for large bins: expand into HBM keys */
-    KMC_STAGE_LARGE_SORT = 6,   /* S7 for large bins: multi-CTA radix sort */
-    KMC_STAGE_LARGE_COMPACT = 7,/* S8 for large bins */
+    KMC_STAGE_LARGE_SPLIT = 5,  /* S6 + MSD step of S7 for large bins: expand, count top digits,
+                                   plan chunks, scatter keys to HBM digit ranges */
+    KMC_STAGE_LARGE_CHUNKS = 6, /* S7-S8 for large bins: SMEM radix sort + compaction per chunk */
+    KMC_STAGE_LARGE_FALLBACK = 7,/* S7-S8 for oversize digits (or all large bins with
+                                   large_path=1): device-wide LSD radix sort + run-length pass */
     KMC_STAGE_ORDER = 8,      /* S9: global ascending order of survivors */
     KMC_STAGE_OUTPUT = 9,     /* copy of the sorted survivors into the caller's buffers */
     KMC_N_STAGES = 10
@@ -111,7 +113,9 @@ typedef struct {
                                     (clamped to the kernel maximum); smaller values force
                                     more bins down the large path (testing) */
     uint32_t force_large;      /* 1: every bin takes the large (multi-CTA) path (testing) */
-    uint32_t reserved[5];
+    uint32_t large_path;       /* 0: MSD split + per-chunk SMEM sort (default);
+                                  1: device-wide LSD radix sort of all large-bin keys (testing) */
+    uint32_t reserved[4];
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).
@@ -122,7 +126,7 @@ void kmc_set_allocator(kmc_alloc_fn alloc_fn, kmc_free_fn free_fn, void* ctx);
 
 /* One-call form.  reads: n_bases bytes, read i = reads[offsets[i]-offsets[0] ..
  * offsets[i+1]-offsets[0]); read_offsets: n_reads+1 nondecreasing uint64 (offsets[0] may
- * be any value).  Requires 1 <= k <= 64, 3 <= p <= min(k, 12) (p = signature length,
+ * be any value).  Requires 1 <= k <= 64, 1 <= p <= min(k, 12) (p = signature length,
  * P:L1188 "-p"), cutoff_max >= max(cutoff_min, 1) (cutoff_min 0 is treated as 1).
  * Writes n_out pairs if out_capacity >= n_out, else returns KMC_ERR_OUT_CAPACITY with
  * stats->n_out = required.  A capacity that is always enough is

@@ -20,8 +20,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libkmcgpu.so")
 
 KMC_OK, KMC_ERR_INVALID_ARG, KMC_ERR_OUT_CAPACITY, KMC_ERR_ALLOC, KMC_ERR_CUDA, KMC_ERR_INTERNAL = range(6)
-STAGES = ["input", "signature", "plan", "scatter", "small_bins", "large_expand", "large_sort",
-          "large_compact", "order", "output"]
+STAGES = ["input", "signature", "plan", "scatter", "small_bins", "large_split", "large_chunks",
+          "large_fallback", "order", "output"]
 
 
 class KmcError(RuntimeError):
@@ -46,7 +46,8 @@ class _Stats(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("profile", ctypes.c_uint32), ("small_bin_capacity", ctypes.c_uint32),
-                ("force_large", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 5)]
+                ("force_large", ctypes.c_uint32), ("large_path", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 4)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
@@ -141,17 +142,18 @@ class Result:
     stats: dict
 
 
-def _options(profile, small_bin_capacity, force_large):
+def _options(profile, small_bin_capacity, force_large, large_path=0):
     o = _Options()
     o.profile = int(bool(profile))
     o.small_bin_capacity = int(small_bin_capacity)
     o.force_large = int(bool(force_large))
+    o.large_path = int(large_path)
     return o
 
 
 def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *, stream=None,
           profile: bool = False, small_bin_capacity: int = 0, force_large: bool = False,
-          out_device: str | None = None) -> Result:
+          large_path: int = 0, out_device: str | None = None) -> Result:
     """Count canonical k-mers (KMC 2 hot path on the GPU).
 
     reads: uint8 tensor (cuda, or pinned/pageable cpu -- copied inside the call), n_bases bytes.
@@ -165,7 +167,7 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
     n_reads = int(offsets.shape[0]) - 1
     if n_reads < 0:
         raise ValueError("offsets must have n_reads + 1 entries")
-    opt = _options(profile, small_bin_capacity, force_large)
+    opt = _options(profile, small_bin_capacity, force_large, large_path)
     job = ctypes.c_void_p()
     n_out = ctypes.c_uint64()
     sh = _stream_handle(stream)

@@ -15,11 +15,11 @@ namespace kmc {
 namespace {
 
 constexpr int LEFT = 16;                      // halo before the tile (window q0-1 + alignment)
-constexpr int NB = P1_TILE + LEFT + 64;       // loaded bases (k <= 64); multiple of 16
+constexpr int NB = P1_TILE + 96;             // loaded bases: LEFT + tile + k-1 (k <= 64); multiple of 32
 constexpr int CH = (NB + P1_NT - 1) / P1_NT;  // positions per thread in the scans
 constexpr int WPT = P1_TILE / P1_NT;          // windows owned per thread
 constexpr uint32_t INV = 0xFFFFFFFFu;
-static_assert(NB % 16 == 0, "NB");
+static_assert(NB % 32 == 0 && NB >= LEFT + P1_TILE + 63, "NB");
 
 // A->0, C->1, G->2, T->3; lowercase folded; anything else -> 4 (invalid, R3).
 __device__ __forceinline__ uint32_t encode_base(uint32_t ch) {
@@ -43,109 +43,151 @@ __global__ void k_tile_reads(const uint64_t* __restrict__ offsets, uint64_t n_re
     tile_r_lo[t] = lo;
 }
 
+constexpr int NWD = NB / 32 + 8;  // bitmask words (with slack for funnel reads)
+
 struct P1Smem {
-    uint32_t key[NB];            // p-mer keys, then per-window signatures
-    uint32_t pre[NB];            // block prefix minima
-    uint32_t suf[NB];            // block suffix minima
+    uint32_t pre[NB];            // p-mer keys, then (in place) block prefix minima; later the run-start list
+    uint32_t suf[NB];            // block suffix minima, then (in place) per-window signatures
     uint32_t pk[NB / 16 + 8];    // 2-bit packed codes, 16 per word, MSB first
+    uint32_t inv[NWD];           // bit x: base x is not A/C/G/T (or outside the stream)
+    uint32_t rs[NWD];            // bit x: a read starts at x
+    uint32_t ext[NWD];           // bit x: x can extend a run to its left (valid, no read start)
+    uint32_t t0[NWD], t1[NWD];   // doubling scratch
+    uint32_t vwin[NWD];          // bit i: window i is valid
+    uint32_t wk[NWD];            // window-AND result before the final shift
+    uint32_t vpm[NWD];           // bit j: p-mer j is valid
+    uint32_t ebits[P1_TILE / 32 + 8];
     uint32_t wsum32[P1_NT / 32 + 1];
-    int32_t wmax[P1_NT / 32];
-    uint8_t code[NB];            // 0..3 = A,C,G,T; 4 = invalid
-    uint8_t rsf[NB];             // 1 where a read starts
-    uint8_t run[NB];             // valid-run length ending here (capped at 255)
+    uint32_t cnt[8];
 };
+
+// bits [a, a+32) of a bitmask (bit x&31 of word x>>5 is position x)
+__device__ __forceinline__ uint32_t bits32_at(const uint32_t* m, int a) {
+    return __funnelshift_r(m[a >> 5], m[(a >> 5) + 1], a & 31);
+}
+
+// dst[w] = AND of src over positions [x, x+len) for every x, len >= 1, by doubling:
+// P_1 = src; P_2t = P_t & (P_t >> t); then P_len = P_2^a & (P_2^a >> (len - 2^a)).
+// Runs in one warp (the masks are NWD words); tmp buffers t0, t1.
+__device__ __forceinline__ void warp_window_and(const uint32_t* src, uint32_t* dst, int len, uint32_t* t0,
+                                                uint32_t* t1, int nwords) {
+    const int lane = threadIdx.x & 31;
+    for (int w = lane; w < nwords; w += 32) t0[w] = src[w];
+    __syncwarp();
+    int span = 1;
+    uint32_t* cur = t0;
+    uint32_t* nxt = t1;
+    while (2 * span <= len) {
+        for (int w = lane; w < nwords - 2; w += 32) nxt[w] = cur[w] & bits32_at(cur, w * 32 + span);
+        __syncwarp();
+        uint32_t* t = cur;
+        cur = nxt;
+        nxt = t;
+        span *= 2;
+    }
+    const int rest = len - span;
+    for (int w = lane; w < nwords - 2; w += 32) dst[w] = cur[w] & (rest ? bits32_at(cur, w * 32 + rest) : cur[w]);
+    __syncwarp();
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
     extern __shared__ __align__(16) uint8_t p1_smem[];
     P1Smem& S = *reinterpret_cast<P1Smem*>(p1_smem);
-    uint8_t(&code)[NB] = S.code;
-    uint8_t(&rsf)[NB] = S.rsf;
-    uint8_t(&run)[NB] = S.run;
-    uint32_t(&key)[NB] = S.key;
-    uint32_t(&pre)[NB] = S.pre;
-    uint32_t(&suf)[NB] = S.suf;
-    uint32_t(&pk)[NB / 16 + 8] = S.pk;
-    uint32_t* wsum32 = S.wsum32;
-    int32_t* wmax = S.wmax;
+    uint32_t* pre = S.pre;
+    uint32_t* suf = S.suf;
+    uint32_t* pk = S.pk;
 
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const int64_t q0 = (int64_t)blockIdx.x * P1_TILE;
     const int64_t lbase = q0 - LEFT;  // stream position of smem index 0
     const int64_t nb = (int64_t)a.n_bases;
     const int k = a.k, p = a.p;
+    const uint64_t r0 = a.tile_r_lo[blockIdx.x];  // issued early: its latency overlaps S1
 
-    // ---- S1: load ASCII, encode to 2-bit codes (invalid -> 4), clear read-start flags
+    // ---- S1: load ASCII (16-byte vectors), encode A0 C1 G2 T3 four bytes at a time
+    //      (lowercase folded); non-ACGT bytes and bytes outside the stream -> inv bits
     uint32_t n_invalid = 0;
     for (int v = tid; v < NB / 16; v += P1_NT) {
         const int64_t q = lbase + 16 * v;
-        uint8_t bytes[16];
+        uint32_t wd[4];
         if (a.reads_aligned16 && q >= 0 && q + 16 <= nb) {
-            uint4 w = *reinterpret_cast<const uint4*>(a.reads + q);
-            *reinterpret_cast<uint4*>(bytes) = w;
+            const uint4 w = *reinterpret_cast<const uint4*>(a.reads + q);
+            wd[0] = w.x; wd[1] = w.y; wd[2] = w.z; wd[3] = w.w;
         } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) bytes[j] = (q + j >= 0 && q + j < nb) ? a.reads[q + j] : (uint8_t)'N';
-        }
-        uint32_t packed = 0;
+            for (int t = 0; t < 4; ++t) {
+                uint32_t x = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            uint32_t c = encode_base(bytes[j]);
-            packed |= (c & 3u) << (30 - 2 * j);
-            code[16 * v + j] = (uint8_t)c;
-            rsf[16 * v + j] = 0;
-            const int li = 16 * v + j;
-            if (c == 4u && li >= LEFT && li < LEFT + P1_TILE && q + j < nb) ++n_invalid;
+                for (int j = 0; j < 4; ++j) {
+                    const int64_t qq = q + 4 * t + j;
+                    const uint32_t b = (qq >= 0 && qq < nb) ? a.reads[qq] : (uint32_t)'N';
+                    x |= b << (8 * j);
+                }
+                wd[t] = x;
+            }
+        }
+        uint32_t packed = 0, invbits = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t c = wd[t] & 0xDFDFDFDFu;
+            const uint32_t ok = __vcmpeq4(c, 0x41414141u) | __vcmpeq4(c, 0x43434343u) | __vcmpeq4(c, 0x47474747u) |
+                                __vcmpeq4(c, 0x54545454u);
+            const uint32_t cd = ((c >> 1) ^ (c >> 2)) & 0x03030303u;  // per byte: A0 C1 G2 T3
+            const uint32_t b8 = ((cd & 0xFFu) << 6) | (((cd >> 8) & 0xFFu) << 4) | (((cd >> 16) & 0xFFu) << 2) |
+                                (cd >> 24);
+            packed |= b8 << (24 - 8 * t);
+            const uint32_t bad = (~ok) & 0x01010101u;
+            invbits |= (((bad * 0x01020408u) >> 24) & 0xFu) << (4 * t);
         }
         pk[v] = packed;
+        reinterpret_cast<uint16_t*>(S.inv)[v] = (uint16_t)invbits;
+        // invalid bytes inside the tile's own window starts [LEFT, LEFT+TILE) and the stream
+        const int li = 16 * v;
+        if (li >= LEFT && li < LEFT + P1_TILE) {
+            uint32_t m = invbits;
+            if (q + 16 > nb) m &= (q >= nb) ? 0u : ((1u << (uint32_t)(nb - q)) - 1u);
+            n_invalid += __popc(m);
+        }
+    }
+    if (tid < NWD - NB / 32) {
+        S.inv[NB / 32 + tid] = 0xFFFFFFFFu;
+        S.rs[NB / 32 + tid] = 0;
     }
     if (tid < 8) pk[NB / 16 + tid] = 0;
+    for (int w = tid; w < NB / 32; w += P1_NT) S.rs[w] = 0;
     __syncthreads();
     // ---- read starts inside (lbase, lbase + NB): segment breaks
-    {
-        uint64_t r0 = a.tile_r_lo[blockIdx.x];
-        for (uint64_t rb = r0;; rb += P1_NT) {
-            uint64_t r = rb + tid;
-            bool inr = false;
-            if (r <= a.n_reads) {
-                int64_t s = (int64_t)(a.offsets[r] - a.off0) - lbase;
-                if (s < NB) {
-                    inr = true;
-                    if (s > 0) rsf[s] = 1;
-                }
+    for (uint64_t rb = r0;; rb += P1_NT) {
+        const uint64_t r = rb + tid;
+        bool inr = false;
+        if (r <= a.n_reads) {
+            const int64_t st = (int64_t)(a.offsets[r] - a.off0) - lbase;
+            if (st < NB) {
+                inr = true;
+                if (st > 0) atomicOr(&S.rs[st >> 5], 1u << (st & 31));
             }
-            if (!__syncthreads_or(inr && tid == P1_NT - 1)) break;
         }
+        if (!__syncthreads_or(inr && tid == P1_NT - 1)) break;
     }
+    // ---- validity bitmasks: window i valid iff bases [i, i+k) are all valid and no read
+    //      starts in (i, i+k); p-mer j likewise over [j, j+p).  ext(x) = valid(x) & !rs(x).
+    for (int w = tid; w < NWD; w += P1_NT) S.ext[w] = ~(S.inv[w] | S.rs[w]);
     __syncthreads();
-    // ---- valid-run length ending at each position: run(e) = e - max_{x<=e} brk(x) + 1,
-    //      brk(x) = x+1 if base x invalid, x if a read starts at x
-    {
-        const int b0 = tid * CH, b1 = min(NB, b0 + CH);
-        int32_t m = 0;
-        for (int x = b0; x < b1; ++x) {
-            int32_t br = code[x] == 4 ? x + 1 : (rsf[x] ? x : 0);
-            m = max(m, br);
-        }
-        // block exclusive prefix max
-        const int lane = tid & 31, warp = tid >> 5;
-        int32_t inc = m;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int32_t n = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc = max(inc, n);
-        }
-        if (lane == 31) wmax[warp] = inc;
-        int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-        if (lane == 0) ex = 0;
-        __syncthreads();
-        for (int w = 0; w < warp; ++w) ex = max(ex, wmax[w]);
-        int32_t cur = ex;
-        for (int x = b0; x < b1; ++x) {
-            int32_t br = code[x] == 4 ? x + 1 : (rsf[x] ? x : 0);
-            cur = max(cur, br);
-            run[x] = (uint8_t)min(255, x - cur + 1);
-        }
+    if (warp == 0) {
+        // vwin(i) = !inv(i) & AND ext[i+1 .. i+k-1]
+        if (k > 1) warp_window_and(S.ext, S.wk, k - 1, S.t0, S.t1, NWD);
+        for (int w = lane; w < NWD - 2; w += 32)
+            S.vwin[w] = ~S.inv[w] & (k > 1 ? bits32_at(S.wk, w * 32 + 1) : 0xFFFFFFFFu);
+    } else if (warp == 1) {
+        // same rule over p symbols, into vpm (second scratch pair)
+        uint32_t* t0 = S.pre;  // pre[] is free until the p-mer keys are written
+        uint32_t* t1 = S.pre + NWD;
+        uint32_t* pw = S.pre + 2 * NWD;
+        if (p > 1) warp_window_and(S.ext, pw, p - 1, t0, t1, NWD);
+        for (int w = lane; w < NWD - 2; w += 32)
+            S.vpm[w] = ~S.inv[w] & (p > 1 ? bits32_at(pw, w * 32 + 1) : 0xFFFFFFFFu);
     }
     __syncthreads();
     // ---- S2a: canonical p-mer key of every position j:
@@ -159,39 +201,40 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
         uint32_t fwd = 0, rc = 0;
         if (b0 < b1) {
             for (int j = b0; j < b0 + p - 1; ++j) {
-                uint32_t c = code[j] & 3u;
+                const uint32_t c = (pk[j >> 4] >> (30 - 2 * (j & 15))) & 3u;
                 fwd = ((fwd << 2) | c) & pmask;
                 rc = (rc >> 2) | ((3u - c) << top);
             }
         }
         for (int j = b0; j < b1; ++j) {
-            uint32_t c = code[j + p - 1] & 3u;
+            const int jj = j + p - 1;
+            const uint32_t c = (pk[jj >> 4] >> (30 - 2 * (jj & 15))) & 3u;
             fwd = ((fwd << 2) | c) & pmask;
             rc = (rc >> 2) | ((3u - c) << top);
-            uint32_t cn = fwd < rc ? fwd : rc;
-            bool ok = run[j + p - 1] >= p && sig_allowed(cn, p);
-            key[j] = ok ? cn : RES;
+            const uint32_t cn = fwd < rc ? fwd : rc;
+            const bool ok = ((S.vpm[j >> 5] >> (j & 31)) & 1u) && sig_allowed(cn, p);
+            pre[j] = ok ? cn : RES;
         }
-        for (int j = max(b0, NBK); j < min(NB, b0 + CH); ++j) key[j] = RES;
+        for (int j = max(b0, NBK); j < min(NB, b0 + CH); ++j) pre[j] = RES;
     }
     __syncthreads();
     // ---- S2b: sliding-window minimum over W = k-p+1 consecutive p-mers (van Herk /
-    //      Gil-Werman): blocks of W, prefix minima pre[] and suffix minima suf[];
-    //      sig(i) = min(suf[i], pre[i+W-1]).
+    //      Gil-Werman): blocks of W; suffix minima into suf[], prefix minima in place in
+    //      pre[]; sig(i) = min(suf[i], pre[i+W-1]).
     const int W = k - p + 1;
     {
         const int nblk = (NBK + W - 1) / W;
         for (int b = tid; b < nblk; b += P1_NT) {
-            const int s = b * W, e = min(NBK, s + W);
+            const int s0 = b * W, e = min(NBK, s0 + W);
             uint32_t m = 0xFFFFFFFFu;
-            for (int j = s; j < e; ++j) {
-                m = min(m, key[j]);
-                pre[j] = m;
+            for (int j = e - 1; j >= s0; --j) {
+                m = min(m, pre[j]);
+                suf[j] = m;
             }
             m = 0xFFFFFFFFu;
-            for (int j = e - 1; j >= s; --j) {
-                m = min(m, key[j]);
-                suf[j] = m;
+            for (int j = s0; j < e; ++j) {
+                m = min(m, pre[j]);
+                pre[j] = m;
             }
         }
     }
@@ -199,10 +242,11 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
     // signature per window i in [LEFT-1, LEFT+TILE) (window q0-1 only for the run test),
     // INV where the window is not valid (crosses a read end or holds a non-ACGT byte)
     for (int i = LEFT - 1 + tid; i < LEFT + P1_TILE; i += P1_NT) {
-        const bool ok = run[i + k - 1] >= k;
-        key[i] = ok ? min(suf[i], pre[i + W - 1]) : INV;
+        const bool ok = (S.vwin[i >> 5] >> (i & 31)) & 1u;
+        suf[i] = ok ? min(suf[i], pre[i + W - 1]) : INV;
     }
     __syncthreads();
+    uint32_t* key = suf;
 
     if (MODE == P1_MODE_DEBUG) {
         for (int w = tid; w < P1_TILE; w += P1_NT) {
@@ -214,22 +258,48 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
 
     // ---- S3: super-k-mers = maximal runs of valid windows with equal signature
     //      (Fig. 1); record runs are additionally cut at the tile edge and
-    //      into pieces of at most record_max_windows(k) windows.
+    //      into pieces of at most record_max_windows(k) windows.  Warp ballots build a
+    //      bitmask of the windows where a run cannot continue (invalid or a new start)
+    //      and a compacted list of run starts; a run's length is the distance to the
+    //      next set bit.
     const int maxw = record_max_windows(k);
     const int RW = record_words(k);
-    uint32_t l_windows = 0, l_skm = 0, l_recs = 0;
+    uint32_t* ebits = S.ebits;
+    uint32_t* list = pre;  // pre[] is free after the signatures are formed
+    if (tid < 8) S.cnt[tid] = 0;
+    __syncthreads();
+    uint32_t l_skm = 0;
+#pragma unroll 4
     for (int w = 0; w < WPT; ++w) {
-        const int i = LEFT + tid * WPT + w;
+        const int i = LEFT + w * P1_NT + tid;
+        const uint32_t s = key[i], prev = key[i - 1];
+        const bool valid = s != INV;
+        const bool skm = valid && prev != s;
+        const bool start = skm || (valid && i == LEFT);
+        const uint32_t bE = __ballot_sync(0xffffffffu, !valid || start);
+        const uint32_t bS = __ballot_sync(0xffffffffu, start);
+        l_skm += skm;
+        uint32_t base = 0;
+        if (lane == 0) {
+            ebits[(w * P1_NT + warp * 32) >> 5] = bE;
+            if (bS) base = atomicAdd(&S.cnt[0], (uint32_t)__popc(bS));
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (start) list[base + __popc(bS & lanemask_lt())] = (uint32_t)i;
+    }
+    if (tid == 0) ebits[P1_TILE >> 5] = 1u;  // sentinel: the tile edge ends every run
+    __syncthreads();
+    const int nstarts = (int)S.cnt[0];
+    uint32_t l_windows = 0, l_recs = 0;
+    for (int idx = tid; idx < nstarts; idx += P1_NT) {
+        const int i = (int)list[idx];
         const uint32_t s = key[i];
-        if (s == INV) continue;
-        const uint32_t prev = key[i - 1];
-        const bool skm_start = prev != s;
-        if (!skm_start && i != LEFT) continue;
-        l_skm += skm_start;
-        int j = i + 1;
-        while (j < LEFT + P1_TILE && key[j] == s) ++j;
-        const int n = j - i;
-        const int nrec = (n + maxw - 1) / maxw;
+        int pos = i - LEFT + 1;
+        int wd = pos >> 5;
+        uint32_t bits = ebits[wd] & (0xFFFFFFFFu << (pos & 31));
+        while (bits == 0) bits = ebits[++wd];
+        const int n = (wd * 32 + __ffs(bits) - 1) - (i - LEFT);
+        const int nrec = n <= maxw ? 1 : (n + maxw - 1) / maxw;
         l_windows += n;
         l_recs += nrec;
         if (MODE == P1_MODE_HIST) {
@@ -240,35 +310,43 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
             //      to bins ... related to signatures"); bins live in HBM.
             const uint32_t bin = a.sig2bin[s];
             const uint64_t base = a.bin_rec_off[bin];
+            const int j = i + n;
             for (int ii = i; ii < j; ii += maxw) {
                 const int m = min(maxw, j - ii);
                 // record words: word 0 = n (8 bits) + symbols [0,12); word u>0 = symbols
                 // [12+16(u-1), 12+16u); extracted from the packed tile by funnel shifts
-                uint32_t wd[8];
+                uint32_t wd4[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     if (u >= RW) break;
                     const int b = ii + (u == 0 ? 0 : 12 + 16 * (u - 1));
                     const uint32_t x = __funnelshift_l(pk[(b >> 4) + 1], pk[b >> 4], 2 * (b & 15));
-                    wd[u] = (u == 0) ? (((uint32_t)m << 24) | (x >> 8)) : x;
+                    wd4[u] = (u == 0) ? (((uint32_t)m << 24) | (x >> 8)) : x;
                 }
                 const uint32_t slot = atomicAdd(&a.bin_fill[bin], 1u);
                 uint4* dst = reinterpret_cast<uint4*>(a.bins + (base + slot) * (uint64_t)RW);
-                dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-                if (RW == 8) dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+                dst[0] = make_uint4(wd4[0], wd4[1], wd4[2], wd4[3]);
+                if (RW == 8) dst[1] = make_uint4(wd4[4], wd4[5], wd4[6], wd4[7]);
             }
         }
     }
     if (MODE == P1_MODE_HIST) {
-        uint32_t tw = block_sum<P1_NT, uint32_t>(l_windows, wsum32);
-        uint32_t ts = block_sum<P1_NT, uint32_t>(l_skm, wsum32);
-        uint32_t tr = block_sum<P1_NT, uint32_t>(l_recs, wsum32);
-        uint32_t ti = block_sum<P1_NT, uint32_t>(n_invalid, wsum32);
+        const uint32_t tw = __reduce_add_sync(0xffffffffu, l_windows);
+        const uint32_t ts = __reduce_add_sync(0xffffffffu, l_skm);
+        const uint32_t tr = __reduce_add_sync(0xffffffffu, l_recs);
+        const uint32_t ti = __reduce_add_sync(0xffffffffu, n_invalid);
+        if (lane == 0) {
+            atomicAdd(&S.cnt[1], tw);
+            atomicAdd(&S.cnt[2], ts);
+            atomicAdd(&S.cnt[3], tr);
+            atomicAdd(&S.cnt[4], ti);
+        }
+        __syncthreads();
         if (tid == 0) {
-            if (tw) atomicAdd(&a.gstats[GS_WINDOWS], (unsigned long long)tw);
-            if (ts) atomicAdd(&a.gstats[GS_SUPERKMERS], (unsigned long long)ts);
-            if (tr) atomicAdd(&a.gstats[GS_RECORDS], (unsigned long long)tr);
-            if (ti) atomicAdd(&a.gstats[GS_INVALID], (unsigned long long)ti);
+            if (S.cnt[1]) atomicAdd(&a.gstats[GS_WINDOWS], (unsigned long long)S.cnt[1]);
+            if (S.cnt[2]) atomicAdd(&a.gstats[GS_SUPERKMERS], (unsigned long long)S.cnt[2]);
+            if (S.cnt[3]) atomicAdd(&a.gstats[GS_RECORDS], (unsigned long long)S.cnt[3]);
+            if (S.cnt[4]) atomicAdd(&a.gstats[GS_INVALID], (unsigned long long)S.cnt[4]);
         }
     }
 }

@@ -94,7 +94,7 @@ __device__ __forceinline__ void block_rle_emit(const K* S, int n, uint32_t* cnt,
 }
 
 template <class K>
-__global__ void __launch_bounds__(SB_NT) k_small_bins(SmallArgs a) {
+__global__ void __launch_bounds__(SB_NT, 2) k_small_bins(SmallArgs a) {
     constexpr int CAP = SmallCap<K>::v;
     extern __shared__ __align__(16) uint8_t smem[];
     K* A = reinterpret_cast<K*>(smem);
@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(SB_NT) k_small_bins(SmallArgs a) {
     uint32_t* wsum = whist + RADIX * SB_NW;                                      // 17 used
     unsigned long long* red = reinterpret_cast<unsigned long long*>(wsum + 24);  // 4
     unsigned long long* bcast = red + 4;
+    unsigned int* scnt = reinterpret_cast<unsigned int*>(bcast + 1);
 
     const uint32_t bin = a.small_list[blockIdx.x];
     const uint64_t rec0 = a.bin_rec_off[bin];
@@ -134,13 +135,11 @@ __global__ void __launch_bounds__(SB_NT) k_small_bins(SmallArgs a) {
         }
     }
     __syncthreads();
-    // ---- S7: LSD radix sort in shared memory
-    const int cur = block_radix_sort<K, SB_NT, false>(A, B, nullptr, nullptr, n, 2 * k, whist, wsum, red);
-    K* S = cur ? B : A;
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(cur ? A : B);
+    // ---- S7: LSD radix sort in shared memory (in place)
+    block_sort_inplace<K, SB_NT, CAP / SB_NT, false>(A, nullptr, n, 2 * k, whist, wsum, red);
     // ---- S8: run-length compaction + cutoffs
-    block_rle_emit<K, SB_NT>(S, n, cnt, a.ci, a.cx, reinterpret_cast<K*>(a.surv_keys), a.surv_counts, a.gstats, wsum,
-                             bcast);
+    block_rle_bitmask<K, SB_NT>(A, n, reinterpret_cast<uint32_t*>(B), a.ci, a.cx, reinterpret_cast<K*>(a.surv_keys),
+                                a.surv_counts, a.gstats, wsum, scnt, bcast, GS_SURV, GS_UNIQUE, GS_BELOW, GS_ABOVE);
 }
 
 // ---------------------------------------------------------------- large-bin expansion
@@ -389,6 +388,249 @@ __global__ void __launch_bounds__(RLE_NT) k_rle(const K* __restrict__ keys, uint
     }
 }
 
+// ---------------------------------------------------------------- partition split of large bins
+// A bin above one CTA's capacity is sorted by a multi-CTA split followed by per-chunk
+// shared-memory sorts: (1) count a D-bit digit of every key of the bin,
+// (2) scan the digit counts per bin and group consecutive digits into chunks of at most
+// CAP keys, (3) re-expand the records and scatter every key to its digit's range in HBM,
+// (4) sort + compact every chunk in shared memory (k_chunk_sort).  The digit is a
+// multiplicative hash of the whole key: a chunk only has to hold every copy of its keys
+// (S9 orders the survivors globally), and the top bits of a key are a poor digit -- about
+// 1/(k-p+1) of a bin's windows start with the bin's own signature.  A digit holding more
+// than CAP keys (identical-key pile-ups, e.g. poly-A) becomes an "oversize" chunk sorted
+// by the device-wide LSD path.
+constexpr int MSD_NT = 256;
+constexpr int MSD_MAXD = 12;
+
+__device__ __forceinline__ uint32_t part_digit(uint64_t key, int D) {
+    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - D));
+}
+__device__ __forceinline__ uint32_t part_digit(const K128& key, int D) {
+    const uint64_t h = (key.lo ^ (key.hi * 0xC2B2AE3D27D4EB4Full)) * 0x9E3779B97F4A7C15ull;
+    return (uint32_t)(h >> (64 - D));
+}
+
+template <class K> struct MsdPiece;
+template <> struct MsdPiece<uint64_t> { static constexpr int REC = 128, MAXW = 60; };
+template <> struct MsdPiece<K128> { static constexpr int REC = 64, MAXW = 92; };
+
+template <class K>
+__global__ void __launch_bounds__(MSD_NT) k_large_count(const uint32_t* __restrict__ bins,
+                                                        const Piece* __restrict__ pieces,
+                                                        const LargeBin* __restrict__ lbins, int k,
+                                                        uint32_t* __restrict__ digit_cnt) {
+    constexpr int REC = MsdPiece<K>::REC;
+    __shared__ __align__(16) uint32_t R[REC * 8];
+    __shared__ uint32_t h[1 << MSD_MAXD];
+    const Piece pc = pieces[blockIdx.x];
+    const LargeBin lb = lbins[pc.lbin];
+    const int RW = record_words(k), D = (int)lb.D, nd = 1 << D;
+    for (int d = threadIdx.x; d < nd; d += MSD_NT) h[d] = 0;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(bins + pc.rec_begin * RW);
+        uint4* dst = reinterpret_cast<uint4*>(R);
+        const int nv = (int)pc.nrec * RW / 4;
+        for (int v = threadIdx.x; v < nv; v += MSD_NT) dst[v] = src[v];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < (int)pc.nrec; r += MSD_NT) {
+        const uint32_t* rec = R + r * RW;
+        typename RollFor<K>::T roll(k);
+        const int n = (int)rec_nwin(rec);
+        for (int j = 0; j < k - 1; ++j) roll.push(rec_sym(rec, j));
+        for (int w = 0; w < n; ++w) {
+            roll.push(rec_sym(rec, k - 1 + w));
+            atomicAdd(&h[part_digit(roll.canon(), D)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < nd; d += MSD_NT)
+        if (h[d]) atomicAdd(&digit_cnt[lb.digit_base + d], h[d]);
+}
+
+// Greedy chunk planner.  One CTA per segment of consecutive digits (a large bin's 2^D
+// digits, or a 4096-digit window of S9's global digits): exclusive scan of the digit
+// counts -> per-digit cursors; then consecutive digits are packed greedily into chunks of
+// at most cap keys (a digit above cap becomes an "oversize" chunk of its own).  Chunks are
+// collected in shared memory and appended with one atomic per list per CTA.
+constexpr int GP_NT = 256;
+constexpr int GP_SEG = 4096;
+
+__global__ void __launch_bounds__(GP_NT) k_greedy_chunks(GreedyArgs g) {
+    extern __shared__ __align__(16) uint32_t gsm[];
+    uint32_t* pre = gsm;                 // GP_SEG + 1
+    uint32_t* cs = pre + GP_SEG + 1;     // chunk starts (relative)
+    uint32_t* cn = cs + GP_SEG;          // chunk sizes; oversize chunks are marked by bit 31
+    __shared__ uint32_t wsum[GP_NT / 32 + 1];
+    __shared__ uint32_t nl_s, nreg_s, nover_s;
+    __shared__ unsigned long long base_reg, base_over;
+    uint64_t dbase, kbase;
+    int nd;
+    if (g.lbins) {
+        const LargeBin lb = g.lbins[blockIdx.x];
+        dbase = lb.digit_base;
+        nd = 1 << lb.D;
+        kbase = lb.key_base;
+    } else {
+        dbase = (uint64_t)blockIdx.x * GP_SEG;
+        nd = (int)((g.n_digits - dbase) < (uint64_t)GP_SEG ? (g.n_digits - dbase) : (uint64_t)GP_SEG);
+        kbase = g.gstart[dbase];
+    }
+    const int ipt = (nd + GP_NT - 1) / GP_NT;
+    const int d0 = threadIdx.x * ipt, d1 = min(nd, d0 + ipt);
+    uint32_t s = 0;
+    for (int d = d0; d < d1; ++d) s += g.cnt[dbase + d];
+    uint32_t total;
+    uint32_t P = block_excl_sum<GP_NT, uint32_t>(s, wsum, &total);
+    for (int d = d0; d < d1; ++d) {
+        pre[d] = P;
+        if (g.cursor) g.cursor[dbase + d] = g.cursor_abs ? (uint32_t)(kbase + P) : P;
+        P += g.cnt[dbase + d];
+    }
+    if (threadIdx.x == 0) pre[nd] = total;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t nl = 0, nreg = 0, nover = 0, cstart = 0, acc = 0;
+        for (int d = 0; d < nd; ++d) {
+            const uint32_t c = pre[d + 1] - pre[d];
+            if (c > g.cap) {
+                if (acc) { cs[nl] = cstart; cn[nl++] = acc; ++nreg; acc = 0; }
+                cs[nl] = pre[d]; cn[nl++] = c | 0x80000000u; ++nover;
+                continue;
+            }
+            if (acc + c > g.cap) { cs[nl] = cstart; cn[nl++] = acc; ++nreg; acc = 0; }
+            if (acc == 0) cstart = pre[d];
+            acc += c;
+        }
+        if (acc) { cs[nl] = cstart; cn[nl++] = acc; ++nreg; }
+        nl_s = nl;
+        base_reg = nreg ? atomicAdd(&g.counters[0], (unsigned long long)nreg) : 0ull;
+        base_over = nover ? atomicAdd(&g.counters[1], (unsigned long long)nover) : 0ull;
+        nreg_s = nreg;
+        nover_s = nover;
+    }
+    __syncthreads();
+    // stable placement inside the CTA's reserved ranges (ballot ranks per list)
+    const uint32_t nl = nl_s;
+    __shared__ uint32_t run_reg, run_over;
+    if (threadIdx.x == 0) { run_reg = 0; run_over = 0; }
+    __syncthreads();
+    for (uint32_t i0 = 0; i0 < nl; i0 += GP_NT) {
+        const uint32_t i = i0 + threadIdx.x;
+        const bool ok = i < nl;
+        const uint32_t c = ok ? cn[i] : 0u;
+        const bool over = ok && (c & 0x80000000u);
+        const bool reg = ok && !over;
+        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint32_t br = __ballot_sync(0xffffffffu, reg), bo = __ballot_sync(0xffffffffu, over);
+        __shared__ uint32_t wr[GP_NT / 32], wo[GP_NT / 32];
+        if (lane == 0) { wr[warp] = __popc(br); wo[warp] = __popc(bo); }
+        __syncthreads();
+        uint32_t orr = run_reg, oo = run_over;
+        for (uint32_t w = 0; w < warp; ++w) { orr += wr[w]; oo += wo[w]; }
+        const uint32_t lt = lanemask_lt();
+        if (reg) g.chunks[base_reg + orr + __popc(br & lt)] = Chunk{kbase + cs[i], c, 0};
+        if (over) g.oversize[base_over + oo + __popc(bo & lt)] = Chunk{kbase + cs[i], c & 0x7FFFFFFFu, 0};
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (uint32_t w = 0; w < GP_NT / 32; ++w) { run_reg += wr[w]; run_over += wo[w]; }
+        }
+        __syncthreads();
+    }
+}
+
+template <class K> constexpr size_t scatter_smem() {
+    return (size_t)MsdPiece<K>::REC * MsdPiece<K>::MAXW * sizeof(K) + MsdPiece<K>::REC * 8 * 4 +
+           (1 << MSD_MAXD) * 4 + 64;
+}
+
+template <class K>
+__global__ void __launch_bounds__(MSD_NT) k_large_scatter(const uint32_t* __restrict__ bins,
+                                                          const Piece* __restrict__ pieces,
+                                                          const LargeBin* __restrict__ lbins, int k,
+                                                          uint32_t* __restrict__ digit_cur, K* __restrict__ out) {
+    constexpr int REC = MsdPiece<K>::REC;
+    extern __shared__ __align__(16) uint8_t smem[];
+    K* keys = reinterpret_cast<K*>(smem);
+    uint32_t* R = reinterpret_cast<uint32_t*>(keys + REC * MsdPiece<K>::MAXW);
+    uint32_t* h = R + REC * 8;
+    uint32_t* wsum = h + (1 << MSD_MAXD);
+    const Piece pc = pieces[blockIdx.x];
+    const LargeBin lb = lbins[pc.lbin];
+    const int RW = record_words(k), D = (int)lb.D, nd = 1 << D;
+    for (int d = threadIdx.x; d < nd; d += MSD_NT) h[d] = 0;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(bins + pc.rec_begin * RW);
+        uint4* dst = reinterpret_cast<uint4*>(R);
+        const int nv = (int)pc.nrec * RW / 4;
+        for (int v = threadIdx.x; v < nv; v += MSD_NT) dst[v] = src[v];
+    }
+    __syncthreads();
+    // expand (one record per thread; REC <= MSD_NT) and count digits
+    const int r = threadIdx.x;
+    const uint32_t nw = r < (int)pc.nrec ? rec_nwin(R + r * RW) : 0u;
+    uint32_t total;
+    const uint32_t pos = block_excl_sum<MSD_NT, uint32_t>(nw, wsum, &total);
+    if (nw) {
+        const uint32_t* rec = R + r * RW;
+        typename RollFor<K>::T roll(k);
+        for (int j = 0; j < k - 1; ++j) roll.push(rec_sym(rec, j));
+        for (uint32_t w = 0; w < nw; ++w) {
+            roll.push(rec_sym(rec, k - 1 + (int)w));
+            const K key = roll.canon();
+            keys[pos + w] = key;
+            atomicAdd(&h[part_digit(key, D)], 1u);
+        }
+    }
+    __syncthreads();
+    // reserve one range per non-empty digit (bin-relative cursors), then place keys
+    for (int d = threadIdx.x; d < nd; d += MSD_NT) {
+        const uint32_t c = h[d];
+        if (c) h[d] = atomicAdd(&digit_cur[lb.digit_base + d], c);
+    }
+    __syncthreads();
+    K* dst = out + lb.key_base;
+    for (uint32_t i = threadIdx.x; i < total; i += MSD_NT) {
+        const K key = keys[i];
+        const uint32_t slot = atomicAdd(&h[part_digit(key, D)], 1u);
+        dst[slot] = key;
+    }
+}
+
+__global__ void k_make_pieces(const LargeBin* __restrict__ lbins, const uint64_t* __restrict__ piece_prefix,
+                              uint32_t rpp, Piece* __restrict__ pieces) {
+    const LargeBin lb = lbins[blockIdx.x];
+    const uint64_t p0 = piece_prefix[blockIdx.x], np = piece_prefix[blockIdx.x + 1] - p0;
+    for (uint64_t j = threadIdx.x; j < np; j += blockDim.x) {
+        const uint64_t r = j * rpp;
+        const uint64_t left = lb.nrec - r;
+        pieces[p0 + j] = Piece{lb.rec_off + r, (uint32_t)(left < rpp ? left : rpp), blockIdx.x};
+    }
+}
+
+template <class K>
+__global__ void __launch_bounds__(SB_NT, 2) k_chunk_sort(const K* __restrict__ keys, const Chunk* __restrict__ chunks,
+                                                      int k, uint32_t ci, uint32_t cx, K* sk, uint32_t* sc,
+                                                      unsigned long long* gstats) {
+    constexpr int CAP = SmallCap<K>::v;
+    extern __shared__ __align__(16) uint8_t smem[];
+    K* A = reinterpret_cast<K*>(smem);
+    K* B = A + CAP;
+    uint32_t* whist = reinterpret_cast<uint32_t*>(B + CAP);
+    uint32_t* wsum = whist + RADIX * SB_NW;
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(wsum + 24);
+    unsigned long long* bcast = red + 4;
+    unsigned int* scnt = reinterpret_cast<unsigned int*>(bcast + 1);
+    const Chunk c = chunks[blockIdx.x];
+    const int n = (int)c.n;
+    const K* src = keys + c.begin;
+    for (int i = threadIdx.x; i < n; i += SB_NT) A[i] = src[i];
+    __syncthreads();
+    block_sort_inplace<K, SB_NT, CAP / SB_NT, false>(A, nullptr, n, 2 * k, whist, wsum, red);
+    block_rle_bitmask<K, SB_NT>(A, n, reinterpret_cast<uint32_t*>(B), ci, cx, sk, sc, gstats, wsum, scnt, bcast,
+                                GS_SURV, GS_UNIQUE, GS_BELOW, GS_ABOVE);
+}
+
 }  // namespace
 
 int small_capacity(int k) { return k <= 32 ? SB_CAP64 : SB_CAP128; }
@@ -419,6 +661,82 @@ cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint6
         k_large_expand<uint64_t><<<(unsigned)n_pieces, LE_NT, 0, s>>>(bins, pieces, k, (uint64_t*)keys, gstats);
     else
         k_large_expand<K128><<<(unsigned)n_pieces, LE_NT, 0, s>>>(bins, pieces, k, (K128*)keys, gstats);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_make_pieces(const LargeBin* lbins, const uint64_t* piece_prefix, uint64_t n_lbins,
+                               uint32_t rec_per_piece, Piece* pieces, cudaStream_t s) {
+    if (n_lbins == 0) return cudaSuccess;
+    k_make_pieces<<<(unsigned)n_lbins, 256, 0, s>>>(lbins, piece_prefix, rec_per_piece, pieces);
+    return cudaGetLastError();
+}
+
+int msd_piece_records(int k) { return k <= 32 ? MsdPiece<uint64_t>::REC : MsdPiece<K128>::REC; }
+
+int msd_digit_bits(uint64_t bin_windows, int k, int cap) {
+    // about cap/8 keys per digit on average; 1 <= D <= 12
+    (void)k;
+    int D = 1;
+    while (D < MSD_MAXD && (bin_windows >> D) > (uint64_t)std::max(1, cap / 8)) ++D;
+    return D;
+}
+
+cudaError_t launch_large_count(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
+                               int k, uint32_t* digit_cnt, cudaStream_t s) {
+    if (n_pieces == 0) return cudaSuccess;
+    if (k <= 32) k_large_count<uint64_t><<<(unsigned)n_pieces, MSD_NT, 0, s>>>(bins, pieces, lbins, k, digit_cnt);
+    else k_large_count<K128><<<(unsigned)n_pieces, MSD_NT, 0, s>>>(bins, pieces, lbins, k, digit_cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaStream_t s) {
+    if (n_segments == 0) return cudaSuccess;
+    const int sm = (int)((GP_SEG + 1 + 2 * GP_SEG) * 4);
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_greedy_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+    k_greedy_chunks<<<(unsigned)n_segments, GP_NT, sm, s>>>(g);
+    return cudaGetLastError();
+}
+
+uint64_t greedy_segments(uint64_t n_digits) { return (n_digits + GP_SEG - 1) / GP_SEG; }
+
+cudaError_t launch_large_scatter(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
+                                 int k, uint32_t* digit_cur, void* keys, cudaStream_t s) {
+    if (n_pieces == 0) return cudaSuccess;
+    cudaError_t e;
+    if (k <= 32) {
+        const int sm = (int)scatter_smem<uint64_t>();
+        if ((e = cudaFuncSetAttribute(k_large_scatter<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)))
+            return e;
+        k_large_scatter<uint64_t><<<(unsigned)n_pieces, MSD_NT, sm, s>>>(bins, pieces, lbins, k, digit_cur,
+                                                                         (uint64_t*)keys);
+    } else {
+        const int sm = (int)scatter_smem<K128>();
+        if ((e = cudaFuncSetAttribute(k_large_scatter<K128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)))
+            return e;
+        k_large_scatter<K128><<<(unsigned)n_pieces, MSD_NT, sm, s>>>(bins, pieces, lbins, k, digit_cur, (K128*)keys);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_sort(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
+                              uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
+                              cudaStream_t s) {
+    if (n_chunks == 0) return cudaSuccess;
+    cudaError_t e;
+    if (k <= 32) {
+        const size_t sm = small_smem_bytes<uint64_t>();
+        if ((e = cudaFuncSetAttribute(k_chunk_sort<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
+            return e;
+        k_chunk_sort<uint64_t><<<(unsigned)n_chunks, SB_NT, sm, s>>>((const uint64_t*)keys, chunks, k, ci, cx,
+                                                                     (uint64_t*)surv_keys, surv_counts, gstats);
+    } else {
+        const size_t sm = small_smem_bytes<K128>();
+        if ((e = cudaFuncSetAttribute(k_chunk_sort<K128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
+            return e;
+        k_chunk_sort<K128><<<(unsigned)n_chunks, SB_NT, sm, s>>>((const K128*)keys, chunks, k, ci, cx,
+                                                                 (K128*)surv_keys, surv_counts, gstats);
+    }
     return cudaGetLastError();
 }
 

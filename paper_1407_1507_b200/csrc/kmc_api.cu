@@ -122,6 +122,30 @@ bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+std::mutex g_pin_mu;
+std::vector<unsigned long long*> g_pin_free;
+unsigned long long* pin_acquire() {
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        if (!g_pin_free.empty()) {
+            unsigned long long* p = g_pin_free.back();
+            g_pin_free.pop_back();
+            return p;
+        }
+    }
+    unsigned long long* p = nullptr;
+    if (cudaMallocHost(&p, 64 * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+void pin_release(unsigned long long* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    g_pin_free.push_back(p);
+}
+
 struct StageEv {
     int stage;
     cudaEvent_t a, b;
@@ -178,7 +202,7 @@ struct kmc_job {
         }
         if (cur_a) cudaEventDestroy(cur_a);
         arena.release_all();
-        if (host_small) cudaFreeHost(host_small);
+        pin_release(host_small);
     }
 };
 
@@ -220,7 +244,11 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     const size_t ksz = kw == 1 ? 8 : 16;
     Arena& ar = j->arena;
     cudaStream_t s = j->s;
-    CK(cudaMallocHost(&j->host_small, 64 * sizeof(unsigned long long)));
+    j->host_small = pin_acquire();
+    if (!j->host_small) {
+        set_err("pinned readback buffer allocation failed");
+        throw Fail{KMC_ERR_ALLOC};
+    }
     j->st.n_reads = n_reads;
     uint64_t off0 = 0, offN = 0;
     if (n_reads > 0) read_extent(j, offsets, n_reads, &off0, &offN);
@@ -341,7 +369,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     CK(cudaStreamSynchronize(s));
     // ---- host: classify bins (small: one CTA in SMEM; large: multi-CTA path)
     std::vector<uint32_t> small;
-    std::vector<Piece> pieces;
+    std::vector<uint64_t> large_ids;
     uint64_t large_windows = 0, n_large = 0, max_bin = 0;
     for (uint64_t b = 0; b < n_bins; ++b) {
         if (bw[b] == 0) continue;
@@ -352,8 +380,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         } else {
             ++n_large;
             large_windows += bw[b];
-            for (uint64_t r = 0; r < bn[b]; r += PIECE_RECORDS)
-                pieces.push_back(Piece{bo[b] + r, (uint32_t)std::min<uint64_t>(PIECE_RECORDS, bn[b] - r), 0});
+            large_ids.push_back(b);
         }
     }
     std::sort(small.begin(), small.end(), [&](uint32_t x, uint32_t y) { return bw[x] > bw[y] || (bw[x] == bw[y] && x < y); });
@@ -409,17 +436,30 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         j->stage_end(1);
     }
     // ---- S6-S8 large bins
-    if (large_windows > 0) {
-        Piece* d_pieces = ar.get<Piece>(pieces.size());
-        CK(cudaMemcpyAsync(d_pieces, pieces.data(), pieces.size() * sizeof(Piece), cudaMemcpyHostToDevice, s));
+    if (large_windows > 0 && j->opt.large_path == 1) {
+        // device-wide LSD radix sort of all large-bin keys together (a bin partitions the
+        // k-mer space, so sorting the union sorts every bin); kept for testing
+        std::vector<LargeBin> lbins(large_ids.size());
+        std::vector<uint64_t> pp(large_ids.size() + 1, 0);
+        for (size_t i = 0; i < large_ids.size(); ++i) {
+            const uint64_t b = large_ids[i];
+            lbins[i] = LargeBin{0, 0, bo[b], (uint32_t)bw[b], 0, (uint32_t)bn[b], 0};
+            pp[i + 1] = pp[i] + (bn[b] + PIECE_RECORDS - 1) / PIECE_RECORDS;
+        }
+        const uint64_t n_pieces = pp.back();
+        LargeBin* d_lbins = ar.get<LargeBin>(lbins.size());
+        uint64_t* d_pp = ar.get<uint64_t>(pp.size());
+        Piece* d_pieces = ar.get<Piece>(n_pieces);
+        CK(cudaMemcpyAsync(d_lbins, lbins.data(), lbins.size() * sizeof(LargeBin), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
         void* lkeys = ar.alloc(large_windows * ksz);
-        j->stage_begin(KMC_STAGE_LARGE_EXPAND);
-        CK(launch_large_expand(bins, d_pieces, pieces.size(), k, lkeys, gstats, s));
-        j->launches += 1;
-        j->stage_end(1);
+        j->stage_begin(KMC_STAGE_LARGE_SPLIT);
+        CK(launch_make_pieces(d_lbins, d_pp, lbins.size(), PIECE_RECORDS, d_pieces, s));
+        CK(launch_large_expand(bins, d_pieces, n_pieces, k, lkeys, gstats, s));
+        j->launches += 2;
+        j->stage_end(2);
         RadixScratch rs{};
         rs.keys_alt = ar.alloc(large_windows * ksz);
-        rs.vals_alt = nullptr;
         const uint64_t nt = (large_windows + radix_tile_items(kw) - 1) / radix_tile_items(kw);
         rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
         rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
@@ -429,19 +469,102 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         void* sorted = nullptr;
         uint32_t* dummy = nullptr;
         int sl = 0;
-        j->stage_begin(KMC_STAGE_LARGE_SORT);
+        j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
         CK(device_radix_sort(kw, lkeys, nullptr, large_windows, 2 * k, rs, s, &sorted, &dummy, &sl));
-        j->launches += sl;
-        j->stage_end(sl);
-        j->stage_begin(KMC_STAGE_LARGE_COMPACT);
         CK(launch_rle(kw, sorted, large_windows, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
-        j->launches += 1;
-        j->stage_end(1);
+        j->launches += sl + 1;
+        j->stage_end(sl + 1);
         ar.release(lkeys);
         ar.release(rs.keys_alt);
         ar.release(rs.tile_hist);
         ar.release(rs.tile_off);
         ar.release(rs.scan_temp);
+    } else if (large_windows > 0) {
+        // MSD split: per large bin, D top bits -> digit ranges in HBM -> chunks <= cap keys
+        const int kcap = small_capacity(k);
+        const int prec = msd_piece_records(k);
+        std::vector<LargeBin> lbins(large_ids.size());
+        std::vector<uint64_t> pp(large_ids.size() + 1, 0);
+        uint64_t key_base = 0, digit_base = 0;
+        for (size_t i = 0; i < large_ids.size(); ++i) {
+            const uint64_t b = large_ids[i];
+            const int D = msd_digit_bits(bw[b], k, kcap);
+            lbins[i] = LargeBin{key_base, digit_base, bo[b], (uint32_t)bw[b], (uint32_t)D, (uint32_t)bn[b], 0};
+            key_base += bw[b];
+            digit_base += 1ull << D;
+            pp[i + 1] = pp[i] + (bn[b] + prec - 1) / prec;
+        }
+        const uint64_t n_pieces = pp.back();
+        if (bw.size() && large_windows != key_base) {
+            set_err("large-bin table inconsistent");
+            throw Fail{KMC_ERR_INTERNAL};
+        }
+        LargeBin* d_lbins = ar.get<LargeBin>(lbins.size());
+        uint64_t* d_pp = ar.get<uint64_t>(pp.size());
+        Piece* d_pieces = ar.get<Piece>(n_pieces);
+        uint32_t* digit_cnt = ar.get<uint32_t>(digit_base);
+        uint32_t* digit_cur = ar.get<uint32_t>(digit_base);
+        Chunk* chunks = ar.get<Chunk>(digit_base);
+        Chunk* oversize = ar.get<Chunk>(digit_base);
+        unsigned long long* counters = ar.get<unsigned long long>(2);
+        void* lkeys = ar.alloc(large_windows * ksz);
+        CK(cudaMemcpyAsync(d_lbins, lbins.data(), lbins.size() * sizeof(LargeBin), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
+        j->stage_begin(KMC_STAGE_LARGE_SPLIT);
+        CK(cudaMemsetAsync(digit_cnt, 0, digit_base * 4, s));
+        CK(cudaMemsetAsync(counters, 0, 16, s));
+        CK(launch_make_pieces(d_lbins, d_pp, lbins.size(), (uint32_t)prec, d_pieces, s));
+        CK(launch_large_count(bins, d_pieces, n_pieces, d_lbins, k, digit_cnt, s));
+        GreedyArgs ga{};
+        ga.cnt = digit_cnt;
+        ga.lbins = d_lbins;
+        ga.cursor = digit_cur;
+        ga.cursor_abs = 0;
+        ga.chunks = chunks;
+        ga.oversize = oversize;
+        ga.counters = counters;
+        ga.cap = (uint32_t)kcap;
+        CK(launch_greedy_chunks(ga, lbins.size(), s));
+        CK(launch_large_scatter(bins, d_pieces, n_pieces, d_lbins, k, digit_cur, lkeys, s));
+        j->launches += 4;
+        j->stage_end(4);
+        CK(cudaMemcpyAsync(&hs[48], counters, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t n_chunks = hs[48], n_over = hs[49];
+        j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
+        CK(launch_chunk_sort(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+        j->launches += 1;
+        j->stage_end(1);
+        if (n_over > 0) {
+            std::vector<Chunk> ov(n_over);
+            CK(cudaMemcpyAsync(ov.data(), oversize, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            uint64_t maxn = 0;
+            for (auto& c : ov) maxn = std::max<uint64_t>(maxn, c.n);
+            RadixScratch rs{};
+            rs.keys_alt = ar.alloc(maxn * ksz);
+            const uint64_t nt = (maxn + radix_tile_items(kw) - 1) / radix_tile_items(kw);
+            rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
+            rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+            rs.scan_temp = ar.alloc(radix_scan_temp_bytes(maxn, kw));
+            rs.red = ar.get<unsigned long long>(4);
+            rs.red_host = hs + 40;
+            int sl = 0;
+            j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
+            for (auto& c : ov) {
+                void* seg = (uint8_t*)lkeys + c.begin * ksz;
+                void* sorted = nullptr;
+                uint32_t* dummy = nullptr;
+                CK(device_radix_sort(kw, seg, nullptr, c.n, 2 * k, rs, s, &sorted, &dummy, &sl));
+                CK(launch_rle(kw, sorted, c.n, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+                sl += 1;
+            }
+            j->launches += sl;
+            j->stage_end(sl);
+        }
+        ar.release(lkeys);
+        j->st.n_large_bins = n_large;
+        hs[16 + GS_LARGE_KEYS] = large_windows;  // the split writes exactly the planned keys
     }
     CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -449,7 +572,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     j->st.n_unique = hs[16 + GS_UNIQUE];
     j->st.n_below_min = hs[16 + GS_BELOW];
     j->st.n_above_max = hs[16 + GS_ABOVE];
-    if (hs[16 + GS_LARGE_KEYS] != large_windows) {
+    if (j->opt.large_path == 1 && hs[16 + GS_LARGE_KEYS] != large_windows) {
         set_err("large-bin expansion produced %llu keys, plan says %llu", (unsigned long long)hs[16 + GS_LARGE_KEYS],
                 (unsigned long long)large_windows);
         throw Fail{KMC_ERR_INTERNAL};
@@ -468,28 +591,55 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     cudaStream_t s = j->s;
     const uint64_t n = j->n_surv;
     if (n == 0) return;
-    void* keys = j->surv_keys;
-    uint32_t* vals = j->surv_counts;
-    if (n > 1) {
+    // ---- S9: global ascending order, written straight into device outputs
+    const bool dev_out = is_device_ptr(out_kmers) && is_device_ptr(out_counts);
+    void* ok = dev_out ? (void*)out_kmers : ar.alloc(n * ksz);
+    uint32_t* oc = dev_out ? out_counts : ar.get<uint32_t>(n);
+    const uint64_t nd = 1ull << order_digit_bits(n, j->k);
+    OrderScratch os{};
+    os.cnt = ar.get<uint32_t>(nd);
+    os.start = ar.get<uint32_t>(nd + 1);
+    os.cursor = ar.get<uint32_t>(nd);
+    os.chunks = ar.get<Chunk>(nd);
+    os.oversize = ar.get<Chunk>(nd);
+    os.counters = ar.get<unsigned long long>(2);
+    os.tmp_keys = ar.alloc(n * ksz);
+    os.tmp_vals = ar.get<uint32_t>(n);
+    os.scan_temp = ar.alloc(order_scan_temp_bytes(nd + 1));
+    os.host = j->host_small + 56;
+    std::vector<OrderSegment> over;
+    int sl = 0;
+    j->stage_begin(KMC_STAGE_ORDER);
+    CK(launch_order(kw, j->surv_keys, j->surv_counts, n, j->k, ok, oc, os, s, &sl, &over));
+    if (!over.empty()) {
+        uint64_t maxn = 0;
+        for (auto& g : over) maxn = std::max(maxn, g.n);
         RadixScratch rs{};
-        rs.keys_alt = ar.alloc(n * ksz);
-        rs.vals_alt = ar.get<uint32_t>(n);
-        const uint64_t nt = (n + radix_tile_items(kw) - 1) / radix_tile_items(kw);
+        rs.keys_alt = ar.alloc(maxn * ksz);
+        rs.vals_alt = ar.get<uint32_t>(maxn);
+        const uint64_t nt = (maxn + radix_tile_items(kw) - 1) / radix_tile_items(kw);
         rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
         rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
-        rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n, kw));
+        rs.scan_temp = ar.alloc(radix_scan_temp_bytes(maxn, kw));
         rs.red = ar.get<unsigned long long>(4);
         rs.red_host = j->host_small + 40;
-        int sl = 0;
-        j->stage_begin(KMC_STAGE_ORDER);
-        CK(device_radix_sort(kw, keys, vals, n, 2 * j->k, rs, s, &keys, &vals, &sl));
-        j->launches += sl;
-        j->stage_end(sl);
+        for (auto& g : over) {
+            void* rk = nullptr;
+            uint32_t* rv = nullptr;
+            CK(device_radix_sort(kw, (uint8_t*)os.tmp_keys + g.begin * ksz, os.tmp_vals + g.begin, g.n, 2 * j->k, rs, s,
+                                 &rk, &rv, &sl));
+            CK(cudaMemcpyAsync((uint8_t*)ok + g.begin * ksz, rk, g.n * ksz, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(oc + g.begin, rv, g.n * 4, cudaMemcpyDeviceToDevice, s));
+        }
     }
-    j->stage_begin(KMC_STAGE_OUTPUT);
-    CK(cudaMemcpyAsync(out_kmers, keys, n * ksz, cudaMemcpyDefault, s));
-    CK(cudaMemcpyAsync(out_counts, vals, n * 4, cudaMemcpyDefault, s));
-    j->stage_end(0);
+    j->launches += sl;
+    j->stage_end(sl);
+    if (!dev_out) {
+        j->stage_begin(KMC_STAGE_OUTPUT);
+        CK(cudaMemcpyAsync(out_kmers, ok, n * ksz, cudaMemcpyDefault, s));
+        CK(cudaMemcpyAsync(out_counts, oc, n * 4, cudaMemcpyDefault, s));
+        j->stage_end(0);
+    }
 }
 
 }  // namespace
@@ -611,7 +761,11 @@ kmc_status kmc_debug_signatures(const uint8_t* reads, const uint64_t* read_offse
     j.p = p;
     j.arena.bind(j.s);
     try {
-        CK(cudaMallocHost(&j.host_small, 64 * sizeof(unsigned long long)));
+        j.host_small = pin_acquire();
+        if (!j.host_small) {
+            set_err("pinned readback buffer allocation failed");
+            throw Fail{KMC_ERR_ALLOC};
+        }
         if (n_reads == 0) return KMC_OK;
         uint64_t off0, offN;
         read_extent(&j, read_offsets, n_reads, &off0, &offN);

@@ -279,4 +279,161 @@ __device__ __forceinline__ int block_radix_sort(K* a, K* b, uint32_t* va, uint32
     return cur;
 }
 
+// Exclusive scan, in place, of RADIX*NW digit-major warp counters (IPT per thread).
+template <int NT>
+__device__ __forceinline__ void block_scan_whist(uint32_t* whist, uint32_t* wsum) {
+    constexpr int NW = NT / 32;
+    constexpr int IPT = RADIX * NW / NT;
+    uint32_t loc[IPT];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        loc[j] = whist[threadIdx.x * IPT + j];
+        s += loc[j];
+    }
+    uint32_t ex = block_excl_sum<NT, uint32_t>(s, wsum, nullptr);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        whist[threadIdx.x * IPT + j] = ex;
+        ex += loc[j];
+    }
+    __syncthreads();
+}
+
+// In-place LSD radix sort of n <= NT*KPT keys (+ optional uint32 values) in shared memory
+// over bits [0, nbits), 8-bit digits, constant digits skipped.  Warp w owns positions
+// [w*32*KPT, (w+1)*32*KPT); per pass every key is read once into registers and ranked
+// once: __match_any_sync gives its peers in the round, the warp's running digit counter
+// (read before the leader adds the round's peers) gives the keys of earlier rounds; after
+// the block-wide digit-major scan the key is stored straight to its final position.
+// Rounds are processed in position order, so every pass is stable.
+template <class K, int NT, int KPT, bool VALS>
+__device__ __forceinline__ void block_sort_inplace(K* A, uint32_t* VA, int n, int nbits, uint32_t* whist,
+                                                   uint32_t* wsum, unsigned long long* red) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t ltm = lanemask_lt();
+    uint64_t vlo, vhi;
+    block_varying_bits<K, NT>(A, n, red, vlo, vhi);
+    // warp segments sized from n (multiples of 32), at most KPT rounds each
+    const int rounds = (((n + NW - 1) / NW) + 31) / 32;
+    const int wbase = warp * rounds * 32;
+    for (int shift = 0; shift < nbits; shift += RADIX_BITS) {
+        if (!digit_varies(vlo, vhi, shift)) continue;
+        for (int i = threadIdx.x; i < RADIX * NW; i += NT) whist[i] = 0;
+        K key[KPT];
+        uint32_t val[KPT];
+        uint32_t rank[KPT];
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+            if (r >= rounds) break;
+            const int i = wbase + r * 32 + lane;
+            if (i < n) {
+                key[r] = A[i];
+                if (VALS) val[r] = VA[i];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+            if (r >= rounds || wbase + r * 32 >= n) break;
+            const int i = wbase + r * 32 + lane;
+            const bool ok = i < n;
+            const uint32_t d = ok ? key_digit(key[r], shift) : (uint32_t)(RADIX + lane);
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t pre = ok ? whist[d * NW + warp] : 0u;
+            __syncwarp();
+            if (ok && lane == __ffs(peers) - 1) whist[d * NW + warp] = pre + __popc(peers);
+            __syncwarp();
+            rank[r] = pre + __popc(peers & ltm);
+        }
+        __syncthreads();
+        block_scan_whist<NT>(whist, wsum);
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+            if (r >= rounds) break;
+            const int i = wbase + r * 32 + lane;
+            if (i < n) {
+                const uint32_t pos = whist[key_digit(key[r], shift) * NW + warp] + rank[r];
+                A[pos] = key[r];
+                if (VALS) VA[pos] = val[r];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Run-length compaction of the sorted keys S[0..n) with the cutoffs ci <= count <= cx
+// (S8).  bits: (n+32)/32+1 uint32 of scratch.  Run starts are found with warp ballots; a
+// run's length is the distance to the next start bit.  Survivors are appended, in any
+// order, at a range reserved with one global atomic per CTA.
+template <class K, int NT>
+__device__ __forceinline__ void block_rle_bitmask(const K* S, int n, uint32_t* bits, uint32_t ci, uint32_t cx,
+                                                  K* out_keys, uint32_t* out_counts, unsigned long long* gstats,
+                                                  uint32_t* wsum, unsigned int* scnt, unsigned long long* bcast,
+                                                  int gs_surv, int gs_unique, int gs_below, int gs_above) {
+    const int lane = threadIdx.x & 31;
+    const int nwords = (n + 32) / 32;  // covers the sentinel bit n
+    for (int base = (threadIdx.x & ~31); base < nwords * 32; base += NT) {
+        const int i = base + lane;
+        const bool st = i < n ? (i == 0 || !key_eq(S[i], S[i - 1])) : (i == n);
+        const uint32_t b = __ballot_sync(0xffffffffu, st);
+        if (lane == 0) bits[base >> 5] = b;
+    }
+    if (threadIdx.x < 4) scnt[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t uniq = 0, below = 0, above = 0, keep = 0;
+    for (int i = threadIdx.x; i < n; i += NT) {
+        if (!((bits[i >> 5] >> (i & 31)) & 1u)) continue;
+        int pos = i + 1, wd = pos >> 5;
+        uint32_t m = bits[wd] & (0xFFFFFFFFu << (pos & 31));
+        while (m == 0) m = bits[++wd];
+        const uint32_t run = (uint32_t)(wd * 32 + __ffs(m) - 1 - i);
+        ++uniq;
+        if (run < ci) ++below;
+        else if (run > cx) ++above;
+        else ++keep;
+    }
+    const uint32_t tk = block_sum<NT, uint32_t>(keep, wsum);
+    if (threadIdx.x == 0) {
+        *bcast = tk ? atomicAdd(&gstats[gs_surv], (unsigned long long)tk) : 0ull;
+    }
+    {
+        const uint32_t a = __reduce_add_sync(0xffffffffu, uniq);
+        const uint32_t b = __reduce_add_sync(0xffffffffu, below);
+        const uint32_t c = __reduce_add_sync(0xffffffffu, above);
+        if (lane == 0) {
+            atomicAdd(&scnt[1], a);
+            atomicAdd(&scnt[2], b);
+            atomicAdd(&scnt[3], c);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (scnt[1]) atomicAdd(&gstats[gs_unique], (unsigned long long)scnt[1]);
+        if (scnt[2]) atomicAdd(&gstats[gs_below], (unsigned long long)scnt[2]);
+        if (scnt[3]) atomicAdd(&gstats[gs_above], (unsigned long long)scnt[3]);
+    }
+    const unsigned long long base = *bcast;
+    for (int i0 = (threadIdx.x & ~31); i0 < n; i0 += NT) {
+        const int i = i0 + lane;
+        uint32_t run = 0;
+        if (i < n && ((bits[i >> 5] >> (i & 31)) & 1u)) {
+            int pos = i + 1, wd = pos >> 5;
+            uint32_t m = bits[wd] & (0xFFFFFFFFu << (pos & 31));
+            while (m == 0) m = bits[++wd];
+            run = (uint32_t)(wd * 32 + __ffs(m) - 1 - i);
+            if (run < ci || run > cx) run = 0;
+        }
+        const uint32_t b = __ballot_sync(0xffffffffu, run != 0);
+        uint32_t slot = 0;
+        if (lane == 0 && b) slot = atomicAdd(&scnt[0], (uint32_t)__popc(b));
+        slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(b & lanemask_lt());
+        if (run) {
+            out_keys[base + slot] = S[i];
+            out_counts[base + slot] = run;
+        }
+    }
+}
+
 }  // namespace kmc

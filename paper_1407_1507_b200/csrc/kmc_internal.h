@@ -1,6 +1,8 @@
 // kmc_internal.h -- host-side declarations shared by the kmcgpu translation units.
 #pragma once
 #include <cstdint>
+#include <vector>
+
 #include <cuda_runtime.h>
 
 namespace kmc {
@@ -101,9 +103,55 @@ cudaError_t launch_small_bins(const SmallArgs& a, uint64_t n_small, cudaStream_t
 struct Piece {
     uint64_t rec_begin;
     uint32_t nrec;
+    uint32_t lbin;  // index into the large-bin table
+};
+constexpr int PIECE_RECORDS = 1024;  // LSD path expansion
+int msd_piece_records(int k);        // MSD path: records per piece (bounded by shared memory)
+
+// Large bin of the MSD path: keys of the bin occupy [key_base, key_base + n) in the large
+// key array after the split; its top-D-bit digit counters live at digit_base.
+struct LargeBin {
+    uint64_t key_base;
+    uint64_t digit_base;
+    uint64_t rec_off;
+    uint32_t n;
+    uint32_t D;
+    uint32_t nrec;
     uint32_t pad;
 };
-constexpr int PIECE_RECORDS = 1024;
+// pieces[piece_prefix[i] + j] = records [j*rec_per_piece, ...) of large bin i
+cudaError_t launch_make_pieces(const LargeBin* lbins, const uint64_t* piece_prefix, uint64_t n_lbins,
+                               uint32_t rec_per_piece, Piece* pieces, cudaStream_t s);
+struct Chunk {
+    uint64_t begin;  // into the large key array
+    uint32_t n;
+    uint32_t pad;
+};
+int msd_digit_bits(uint64_t bin_windows, int k, int cap);
+cudaError_t launch_large_count(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
+                               int k, uint32_t* digit_cnt, cudaStream_t s);
+// Greedy chunk planner: segments are either the large bins (lbins != nullptr; one CTA per
+// bin, 2^D digits each, chunk keys at key_base + bin-relative offsets) or 4096-digit windows
+// of a global digit array (lbins == nullptr; gstart = exclusive scan of cnt).
+struct GreedyArgs {
+    const uint32_t* cnt;
+    const LargeBin* lbins;
+    const uint32_t* gstart;
+    uint64_t n_digits;
+    uint32_t* cursor;     // per-digit scatter cursor (may be nullptr)
+    int cursor_abs;       // 1: cursor = key_base + prefix; 0: bin-relative prefix
+    Chunk* chunks;
+    Chunk* oversize;
+    unsigned long long* counters;  // [0] chunks, [1] oversize
+    uint32_t cap;
+};
+cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaStream_t s);
+uint64_t greedy_segments(uint64_t n_digits);
+cudaError_t launch_large_scatter(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
+                                 int k, uint32_t* digit_cur, void* keys, cudaStream_t s);
+cudaError_t launch_chunk_sort(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
+                              uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
+                              cudaStream_t s);
 cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, void* keys,
                                 unsigned long long* gstats, cudaStream_t s);
 
@@ -126,5 +174,30 @@ cudaError_t device_radix_sort(int key_words, void* keys, uint32_t* vals, uint64_
 
 cudaError_t launch_rle(int key_words, const void* keys, uint64_t n, uint32_t ci, uint32_t cx, void* surv_keys,
                        uint32_t* surv_counts, unsigned long long* gstats, cudaStream_t s);
+
+// ------------------------------------------------------------ S9 global order
+struct OrderScratch {
+    uint32_t* cnt;          // [2^D] digit counts
+    uint32_t* start;        // [2^D + 1] exclusive scan
+    uint32_t* cursor;       // [2^D] scatter cursors
+    Chunk* chunks;          // [2^D]
+    Chunk* oversize;        // [2^D]
+    unsigned long long* counters;  // [2]
+    void* tmp_keys;         // [n] K
+    uint32_t* tmp_vals;     // [n]
+    void* scan_temp;        // order_scan_temp_bytes(2^D)
+    unsigned long long* host;  // pinned, 2 entries
+};
+struct OrderSegment {
+    uint64_t begin, n;  // in the scattered (tmp) arrays == in the output
+};
+int order_digit_bits(uint64_t n, int k);
+size_t order_scan_temp_bytes(uint64_t n_digits);
+// Sorts (keys, vals) ascending into (out_keys, out_vals).  Segments whose digit holds more
+// than the chunk capacity are left, grouped, in os.tmp_keys/tmp_vals and returned in
+// *oversize for the caller to sort with device_radix_sort.
+cudaError_t launch_order(int key_words, const void* keys, const uint32_t* vals, uint64_t n, int k, void* out_keys,
+                         uint32_t* out_vals, const OrderScratch& os, cudaStream_t s, int* launches,
+                         std::vector<OrderSegment>* oversize);
 
 }  // namespace kmc

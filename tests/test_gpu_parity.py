@@ -99,7 +99,8 @@ def test_count_parity_configs(gpu, name, scale):
     assert st["n_superkmers"] > 0 and st["n_bins"] > 0
 
 
-@pytest.mark.parametrize("opts", [dict(force_large=True), dict(small_bin_capacity=64), dict(small_bin_capacity=1024)])
+@pytest.mark.parametrize("opts", [dict(force_large=True), dict(small_bin_capacity=64), dict(small_bin_capacity=1024),
+                                  dict(large_path=1), dict(force_large=True, large_path=1)])
 def test_forced_paths(gpu, opts):
     w = synth.make("C5", scale=0.005)
     st = assert_same(gpu, w, **opts)
@@ -136,11 +137,13 @@ def test_k_boundaries(gpu, k):
     assert_same(gpu, synth.from_strings(seqs, k, p, 1))
 
 
-def test_low_complexity_and_skew(gpu):
+@pytest.mark.parametrize("large_path", [0, 1])
+def test_low_complexity_and_skew(gpu, large_path):
+    # poly-A / (AT)n pile-ups: one k-mer with ~25K copies -> an "oversize" MSD digit
     seqs = ["A" * 300, "T" * 250, "AT" * 120, "ACGT" * 60, "N" * 50, "", "ACG", "CA" * 100] * 50
     seqs += [s.decode() for s in synth.random_reads(9, 200, 50, 250)]
     for k, p in ((31, 9), (28, 7), (55, 11), (21, 3)):
-        assert_same(gpu, synth.from_strings(seqs, k, p, 2))
+        assert_same(gpu, synth.from_strings(seqs, k, p, 2), large_path=large_path)
 
 
 def test_edge_cases(gpu):
