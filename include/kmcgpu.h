@@ -74,7 +74,8 @@ enum {
     KMC_STAGE_INPUT = 0,      /* host->device copy of host inputs */
     KMC_STAGE_SIGNATURE = 1,  /* S1-S3: encode + signatures + super-k-mer histogram (pass 1) */
     KMC_STAGE_PLAN = 2,       /* S4: signature->bin map, bin offsets (scans) */
-    KMC_STAGE_SCATTER = 3,    /* S1-S3 again + S5: super-k-mer records into HBM bins (pass 2) */
+    KMC_STAGE_SCATTER = 3,    /* S5: super-k-mer records into HBM bins (copy of pass 1's record
+                                 stream, or S1-S3 recomputed as pass 2) */
     KMC_STAGE_SMALL_BINS = 4, /* S6-S8 for bins that fit one CTA: expand + SMEM radix sort + compact */
     KMC_STAGE_LARGE_SPLIT = 5,  /* S6 + MSD step of S7 for large bins: expand, count top digits,
                                    plan chunks, scatter keys to HBM digit ranges */
@@ -113,9 +114,11 @@ typedef struct {
                                     (clamped to the kernel maximum); smaller values force
                                     more bins down the large path (testing) */
     uint32_t force_large;      /* 1: every bin takes the large (multi-CTA) path (testing) */
-    uint32_t large_path;       /* 0: MSD split + per-chunk SMEM sort (default);
+    uint32_t large_path;       /* 0: hashed split + per-chunk SMEM sort (default);
                                   1: device-wide LSD radix sort of all large-bin keys (testing) */
-    uint32_t reserved[4];
+    uint32_t distribute_path;  /* 0: pass 1 streams its records, S5 copies them into bins (default);
+                                  1: S5 recomputes pass 1 from the reads (testing) */
+    uint32_t reserved[3];
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).

@@ -47,7 +47,7 @@ class _Stats(ctypes.Structure):
 class _Options(ctypes.Structure):
     _fields_ = [("profile", ctypes.c_uint32), ("small_bin_capacity", ctypes.c_uint32),
                 ("force_large", ctypes.c_uint32), ("large_path", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32 * 4)]
+                ("distribute_path", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 3)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
@@ -142,8 +142,9 @@ class Result:
     stats: dict
 
 
-def _options(profile, small_bin_capacity, force_large, large_path=0):
+def _options(profile, small_bin_capacity, force_large, large_path=0, distribute_path=0):
     o = _Options()
+    o.distribute_path = int(distribute_path)
     o.profile = int(bool(profile))
     o.small_bin_capacity = int(small_bin_capacity)
     o.force_large = int(bool(force_large))
@@ -153,7 +154,7 @@ def _options(profile, small_bin_capacity, force_large, large_path=0):
 
 def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *, stream=None,
           profile: bool = False, small_bin_capacity: int = 0, force_large: bool = False,
-          large_path: int = 0, out_device: str | None = None) -> Result:
+          large_path: int = 0, distribute_path: int = 0, out_device: str | None = None) -> Result:
     """Count canonical k-mers (KMC 2 hot path on the GPU).
 
     reads: uint8 tensor (cuda, or pinned/pageable cpu -- copied inside the call), n_bases bytes.
@@ -167,7 +168,7 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
     n_reads = int(offsets.shape[0]) - 1
     if n_reads < 0:
         raise ValueError("offsets must have n_reads + 1 entries")
-    opt = _options(profile, small_bin_capacity, force_large, large_path)
+    opt = _options(profile, small_bin_capacity, force_large, large_path, distribute_path)
     job = ctypes.c_void_p()
     n_out = ctypes.c_uint64()
     sh = _stream_handle(stream)

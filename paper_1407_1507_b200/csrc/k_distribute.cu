@@ -7,6 +7,8 @@
 // Everything between the ASCII load and the histogram / bin write stays in shared
 // memory: codes, valid-run lengths, the canonical p-mer key of every position, the
 // van Herk / Gil-Werman block prefix/suffix minima, and the per-window signature.
+#include <algorithm>
+
 #include "kmc_device.cuh"
 #include "kmc_internal.h"
 
@@ -52,42 +54,17 @@ struct P1Smem {
     uint32_t inv[NWD];           // bit x: base x is not A/C/G/T (or outside the stream)
     uint32_t rs[NWD];            // bit x: a read starts at x
     uint32_t ext[NWD];           // bit x: x can extend a run to its left (valid, no read start)
-    uint32_t t0[NWD], t1[NWD];   // doubling scratch
     uint32_t vwin[NWD];          // bit i: window i is valid
-    uint32_t wk[NWD];            // window-AND result before the final shift
     uint32_t vpm[NWD];           // bit j: p-mer j is valid
     uint32_t ebits[P1_TILE / 32 + 8];
     uint32_t wsum32[P1_NT / 32 + 1];
     uint32_t cnt[8];
+    unsigned long long tmp_base;
 };
 
 // bits [a, a+32) of a bitmask (bit x&31 of word x>>5 is position x)
 __device__ __forceinline__ uint32_t bits32_at(const uint32_t* m, int a) {
     return __funnelshift_r(m[a >> 5], m[(a >> 5) + 1], a & 31);
-}
-
-// dst[w] = AND of src over positions [x, x+len) for every x, len >= 1, by doubling:
-// P_1 = src; P_2t = P_t & (P_t >> t); then P_len = P_2^a & (P_2^a >> (len - 2^a)).
-// Runs in one warp (the masks are NWD words); tmp buffers t0, t1.
-__device__ __forceinline__ void warp_window_and(const uint32_t* src, uint32_t* dst, int len, uint32_t* t0,
-                                                uint32_t* t1, int nwords) {
-    const int lane = threadIdx.x & 31;
-    for (int w = lane; w < nwords; w += 32) t0[w] = src[w];
-    __syncwarp();
-    int span = 1;
-    uint32_t* cur = t0;
-    uint32_t* nxt = t1;
-    while (2 * span <= len) {
-        for (int w = lane; w < nwords - 2; w += 32) nxt[w] = cur[w] & bits32_at(cur, w * 32 + span);
-        __syncwarp();
-        uint32_t* t = cur;
-        cur = nxt;
-        nxt = t;
-        span *= 2;
-    }
-    const int rest = len - span;
-    for (int w = lane; w < nwords - 2; w += 32) dst[w] = cur[w] & (rest ? bits32_at(cur, w * 32 + rest) : cur[w]);
-    __syncwarp();
 }
 
 template <int MODE>
@@ -175,19 +152,21 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
     //      starts in (i, i+k); p-mer j likewise over [j, j+p).  ext(x) = valid(x) & !rs(x).
     for (int w = tid; w < NWD; w += P1_NT) S.ext[w] = ~(S.inv[w] | S.rs[w]);
     __syncthreads();
-    if (warp == 0) {
-        // vwin(i) = !inv(i) & AND ext[i+1 .. i+k-1]
-        if (k > 1) warp_window_and(S.ext, S.wk, k - 1, S.t0, S.t1, NWD);
-        for (int w = lane; w < NWD - 2; w += 32)
-            S.vwin[w] = ~S.inv[w] & (k > 1 ? bits32_at(S.wk, w * 32 + 1) : 0xFFFFFFFFu);
-    } else if (warp == 1) {
-        // same rule over p symbols, into vpm (second scratch pair)
-        uint32_t* t0 = S.pre;  // pre[] is free until the p-mer keys are written
-        uint32_t* t1 = S.pre + NWD;
-        uint32_t* pw = S.pre + 2 * NWD;
-        if (p > 1) warp_window_and(S.ext, pw, p - 1, t0, t1, NWD);
-        for (int w = lane; w < NWD - 2; w += 32)
-            S.vpm[w] = ~S.inv[w] & (p > 1 ? bits32_at(pw, w * 32 + 1) : 0xFFFFFFFFu);
+    // one thread per mask word: AND of ext over the next L positions from three register-
+    // held words (window: L = k-1 -> vwin; p-mer: L = p-1 -> vpm), then AND with !inv(i)
+    {
+        constexpr int NWU = NB / 32 + 1;  // words covering every window / p-mer start we use
+        for (int t = tid; t < 2 * NWU; t += P1_NT) {
+            const int w = t < NWU ? t : t - NWU;
+            const int L = t < NWU ? k - 1 : p - 1;
+            const uint32_t x0 = S.ext[w], x1 = S.ext[w + 1], x2 = S.ext[w + 2];
+            uint32_t acc = 0xFFFFFFFFu;
+            for (int o = 1; o <= L; ++o)
+                acc &= o < 32 ? __funnelshift_r(x0, x1, o) : (o == 32 ? x1 : __funnelshift_r(x1, x2, o - 32));
+            const uint32_t v = ~S.inv[w] & acc;
+            if (t < NWU) S.vwin[w] = v;
+            else S.vpm[w] = v;
+        }
     }
     __syncthreads();
     // ---- S2a: canonical p-mer key of every position j:
@@ -290,15 +269,30 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
     if (tid == 0) ebits[P1_TILE >> 5] = 1u;  // sentinel: the tile edge ends every run
     __syncthreads();
     const int nstarts = (int)S.cnt[0];
+    // record words of the run piece starting at smem index ii with m windows: word 0 =
+    // m (8 bits) + symbols [0,12); word u>0 = symbols [12+16(u-1), 12+16u); extracted from
+    // the packed tile by funnel shifts
+    auto pack = [&](int ii, int m, uint32_t (&wd4)[8]) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (u >= RW) break;
+            const int b = ii + (u == 0 ? 0 : 12 + 16 * (u - 1));
+            const uint32_t x = __funnelshift_l(pk[(b >> 4) + 1], pk[b >> 4], 2 * (b & 15));
+            wd4[u] = (u == 0) ? (((uint32_t)m << 24) | (x >> 8)) : x;
+        }
+    };
+    auto run_len = [&](int i) {
+        const int pos = i - LEFT + 1;
+        int wd = pos >> 5;
+        uint32_t bits = ebits[wd] & (0xFFFFFFFFu << (pos & 31));
+        while (bits == 0) bits = ebits[++wd];
+        return (wd * 32 + __ffs(bits) - 1) - (i - LEFT);
+    };
     uint32_t l_windows = 0, l_recs = 0;
     for (int idx = tid; idx < nstarts; idx += P1_NT) {
         const int i = (int)list[idx];
         const uint32_t s = key[i];
-        int pos = i - LEFT + 1;
-        int wd = pos >> 5;
-        uint32_t bits = ebits[wd] & (0xFFFFFFFFu << (pos & 31));
-        while (bits == 0) bits = ebits[++wd];
-        const int n = (wd * 32 + __ffs(bits) - 1) - (i - LEFT);
+        const int n = run_len(i);
         const int nrec = n <= maxw ? 1 : (n + maxw - 1) / maxw;
         l_windows += n;
         l_recs += nrec;
@@ -306,23 +300,16 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
             atomicAdd(&a.hist_w[s], (unsigned long long)n);
             atomicAdd(&a.hist_r[s], (uint32_t)nrec);
         } else {
-            // ---- S5: write each piece as a bin record (super-k-mers "are sent
-            //      to bins ... related to signatures"); bins live in HBM.
+            // ---- S5 (recompute path): write each piece as a bin record (P:L258-259:
+            //      super-k-mers "are sent to bins ... related to signatures"); bins live in
+            //      HBM.
             const uint32_t bin = a.sig2bin[s];
             const uint64_t base = a.bin_rec_off[bin];
             const int j = i + n;
             for (int ii = i; ii < j; ii += maxw) {
                 const int m = min(maxw, j - ii);
-                // record words: word 0 = n (8 bits) + symbols [0,12); word u>0 = symbols
-                // [12+16(u-1), 12+16u); extracted from the packed tile by funnel shifts
                 uint32_t wd4[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (u >= RW) break;
-                    const int b = ii + (u == 0 ? 0 : 12 + 16 * (u - 1));
-                    const uint32_t x = __funnelshift_l(pk[(b >> 4) + 1], pk[b >> 4], 2 * (b & 15));
-                    wd4[u] = (u == 0) ? (((uint32_t)m << 24) | (x >> 8)) : x;
-                }
+                pack(ii, m, wd4);
                 const uint32_t slot = atomicAdd(&a.bin_fill[bin], 1u);
                 uint4* dst = reinterpret_cast<uint4*>(a.bins + (base + slot) * (uint64_t)RW);
                 dst[0] = make_uint4(wd4[0], wd4[1], wd4[2], wd4[3]);
@@ -331,6 +318,31 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
         }
     }
     if (MODE == P1_MODE_HIST) {
+        // ---- the tile's records are also appended, unbinned and tagged with their
+        //      signature, to a temporary stream; S5 then only copies them into their bins
+        if (a.tmp_recs) {
+            uint32_t tot;
+            uint32_t rpos = block_excl_sum<P1_NT, uint32_t>(l_recs, S.wsum32, &tot);
+            if (tid == 0) S.tmp_base = tot ? atomicAdd(&a.gstats[GS_TMP_RECS], (unsigned long long)tot) : 0ull;
+            __syncthreads();
+            const unsigned long long base = S.tmp_base;
+            if (base + tot <= a.tmp_cap) {
+                for (int idx = tid; idx < nstarts; idx += P1_NT) {
+                    const int i = (int)list[idx];
+                    const uint32_t s = key[i];
+                    const int j = i + run_len(i);
+                    for (int ii = i; ii < j; ii += maxw) {
+                        uint32_t wd4[8];
+                        pack(ii, min(maxw, j - ii), wd4);
+                        const uint64_t slot = base + rpos++;
+                        uint4* dst = reinterpret_cast<uint4*>(a.tmp_recs + slot * (uint64_t)RW);
+                        dst[0] = make_uint4(wd4[0], wd4[1], wd4[2], wd4[3]);
+                        if (RW == 8) dst[1] = make_uint4(wd4[4], wd4[5], wd4[6], wd4[7]);
+                        a.tmp_sig[slot] = s;
+                    }
+                }
+            }
+        }
         const uint32_t tw = __reduce_add_sync(0xffffffffu, l_windows);
         const uint32_t ts = __reduce_add_sync(0xffffffffu, l_skm);
         const uint32_t tr = __reduce_add_sync(0xffffffffu, l_recs);
@@ -347,6 +359,34 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
             if (S.cnt[2]) atomicAdd(&a.gstats[GS_SUPERKMERS], (unsigned long long)S.cnt[2]);
             if (S.cnt[3]) atomicAdd(&a.gstats[GS_RECORDS], (unsigned long long)S.cnt[3]);
             if (S.cnt[4]) atomicAdd(&a.gstats[GS_INVALID], (unsigned long long)S.cnt[4]);
+        }
+    }
+}
+
+// S5 from the temporary stream: every record is copied into its bin (signature -> bin
+// map of the plan); one atomic per (warp, bin) reserves the slots.
+__global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ tmp_recs,
+                                                     const uint32_t* __restrict__ tmp_sig, uint64_t n, int RW,
+                                                     const uint32_t* __restrict__ sig2bin,
+                                                     const uint64_t* __restrict__ bin_rec_off,
+                                                     uint32_t* __restrict__ bin_fill, uint32_t* __restrict__ bins) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t ltm = lanemask_lt();
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = base + threadIdx.x;
+        const bool ok = i < n;
+        const uint32_t bin = ok ? sig2bin[tmp_sig[i]] : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+        const uint32_t leader = __ffs(peers) - 1;
+        uint32_t b = 0;
+        if (ok && lane == leader) b = atomicAdd(&bin_fill[bin], (uint32_t)__popc(peers));
+        b = __shfl_sync(0xffffffffu, b, leader);
+        if (ok) {
+            const uint64_t slot = bin_rec_off[bin] + b + __popc(peers & ltm);
+            const uint4* src = reinterpret_cast<const uint4*>(tmp_recs + i * (uint64_t)RW);
+            uint4* dst = reinterpret_cast<uint4*>(bins + slot * (uint64_t)RW);
+            dst[0] = src[0];
+            if (RW == 8) dst[1] = src[1];
         }
     }
 }
@@ -383,6 +423,15 @@ cudaError_t launch_p1(int mode, const P1Args& a, uint64_t n_tiles, cudaStream_t 
         if ((e = cudaFuncSetAttribute(k_pass<P1_MODE_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
         k_pass<P1_MODE_DEBUG><<<grid, P1_NT, sm, s>>>(a);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bin_scatter(const uint32_t* tmp_recs, const uint32_t* tmp_sig, uint64_t n, int k,
+                               const uint32_t* sig2bin, const uint64_t* bin_rec_off, uint32_t* bin_fill,
+                               uint32_t* bins, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k_bin_scatter<<<grid, 256, 0, s>>>(tmp_recs, tmp_sig, n, record_words(k), sig2bin, bin_rec_off, bin_fill, bins);
     return cudaGetLastError();
 }
 

@@ -31,7 +31,9 @@ template <class K> constexpr size_t order_smem() {
     return 2 * (size_t)OrderCap<K>::v * (sizeof(K) + 4) + RADIX * OC_NW * 4 + 192;
 }
 
-__device__ __forceinline__ uint32_t hi_digit(uint64_t key, int twok, int D) { return (uint32_t)(key >> (twok - D)); }
+__device__ __forceinline__ uint32_t hi_digit(uint64_t key, int twok, int D) {
+    return (uint32_t)(key >> (twok - D)) & ((1u << D) - 1);
+}
 __device__ __forceinline__ uint32_t hi_digit(const K128& key, int twok, int D) {
     const int sh = twok - D;
     uint64_t v;

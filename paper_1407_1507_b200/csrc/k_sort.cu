@@ -35,13 +35,10 @@ template <class K> __host__ __device__ constexpr size_t small_smem_bytes() {
 // Expand one record into n canonical keys at dst[0..n) (min(fwd, rc)).
 template <class K>
 __device__ __forceinline__ void expand_record(const uint32_t* rec, int k, K* dst) {
-    typename RollFor<K>::T roll(k);
-    const int n = (int)rec_nwin(rec);
-    for (int j = 0; j < k - 1; ++j) roll.push(rec_sym(rec, j));
-    for (int w = 0; w < n; ++w) {
-        roll.push(rec_sym(rec, k - 1 + w));
-        dst[w] = roll.canon();
-    }
+    constexpr int RW = RecWords<K>::v;
+    uint32_t wd[RW];
+    load_record<RW>(rec, wd);
+    for_each_window<K, RW>(wd, k, [&](int w, const K& key) { dst[w] = key; });
 }
 
 // Run-length compaction of the sorted keys S[0..n) with the cutoffs (S8); cnt is a free
@@ -402,14 +399,6 @@ __global__ void __launch_bounds__(RLE_NT) k_rle(const K* __restrict__ keys, uint
 constexpr int MSD_NT = 256;
 constexpr int MSD_MAXD = 12;
 
-__device__ __forceinline__ uint32_t part_digit(uint64_t key, int D) {
-    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - D));
-}
-__device__ __forceinline__ uint32_t part_digit(const K128& key, int D) {
-    const uint64_t h = (key.lo ^ (key.hi * 0xC2B2AE3D27D4EB4Full)) * 0x9E3779B97F4A7C15ull;
-    return (uint32_t)(h >> (64 - D));
-}
-
 template <class K> struct MsdPiece;
 template <> struct MsdPiece<uint64_t> { static constexpr int REC = 128, MAXW = 60; };
 template <> struct MsdPiece<K128> { static constexpr int REC = 64, MAXW = 92; };
@@ -434,14 +423,9 @@ __global__ void __launch_bounds__(MSD_NT) k_large_count(const uint32_t* __restri
     }
     __syncthreads();
     for (int r = threadIdx.x; r < (int)pc.nrec; r += MSD_NT) {
-        const uint32_t* rec = R + r * RW;
-        typename RollFor<K>::T roll(k);
-        const int n = (int)rec_nwin(rec);
-        for (int j = 0; j < k - 1; ++j) roll.push(rec_sym(rec, j));
-        for (int w = 0; w < n; ++w) {
-            roll.push(rec_sym(rec, k - 1 + w));
-            atomicAdd(&h[part_digit(roll.canon(), D)], 1u);
-        }
+        uint32_t wd[RecWords<K>::v];
+        load_record<RecWords<K>::v>(R + r * RW, wd);
+        for_each_window<K, RecWords<K>::v>(wd, k, [&](int, const K& key) { atomicAdd(&h[part_digit(key, D)], 1u); });
     }
     __syncthreads();
     for (int d = threadIdx.x; d < nd; d += MSD_NT)
@@ -539,22 +523,23 @@ __global__ void __launch_bounds__(GP_NT) k_greedy_chunks(GreedyArgs g) {
     }
 }
 
-template <class K> constexpr size_t scatter_smem() {
-    return (size_t)MsdPiece<K>::REC * MsdPiece<K>::MAXW * sizeof(K) + MsdPiece<K>::REC * 8 * 4 +
-           (1 << MSD_MAXD) * 4 + 64;
+template <class K> size_t scatter_smem(int k, int dmax) {
+    return (size_t)MsdPiece<K>::REC * record_max_windows(k) * sizeof(K) + MsdPiece<K>::REC * 8 * 4 +
+           ((size_t)1 << dmax) * 4 + 64;
 }
 
 template <class K>
 __global__ void __launch_bounds__(MSD_NT) k_large_scatter(const uint32_t* __restrict__ bins,
                                                           const Piece* __restrict__ pieces,
-                                                          const LargeBin* __restrict__ lbins, int k,
+                                                          const LargeBin* __restrict__ lbins, int k, int dmax,
                                                           uint32_t* __restrict__ digit_cur, K* __restrict__ out) {
     constexpr int REC = MsdPiece<K>::REC;
+    constexpr int RWK = RecWords<K>::v;
     extern __shared__ __align__(16) uint8_t smem[];
     K* keys = reinterpret_cast<K*>(smem);
-    uint32_t* R = reinterpret_cast<uint32_t*>(keys + REC * MsdPiece<K>::MAXW);
+    uint32_t* R = reinterpret_cast<uint32_t*>(keys + REC * record_max_windows(k));
     uint32_t* h = R + REC * 8;
-    uint32_t* wsum = h + (1 << MSD_MAXD);
+    uint32_t* wsum = h + (1 << dmax);
     const Piece pc = pieces[blockIdx.x];
     const LargeBin lb = lbins[pc.lbin];
     const int RW = record_words(k), D = (int)lb.D, nd = 1 << D;
@@ -568,19 +553,19 @@ __global__ void __launch_bounds__(MSD_NT) k_large_scatter(const uint32_t* __rest
     __syncthreads();
     // expand (one record per thread; REC <= MSD_NT) and count digits
     const int r = threadIdx.x;
-    const uint32_t nw = r < (int)pc.nrec ? rec_nwin(R + r * RW) : 0u;
+    uint32_t wd[RWK];
+    uint32_t nw = 0;
+    if (r < (int)pc.nrec) {
+        load_record<RWK>(R + r * RW, wd);
+        nw = wd[0] >> 24;
+    }
     uint32_t total;
     const uint32_t pos = block_excl_sum<MSD_NT, uint32_t>(nw, wsum, &total);
     if (nw) {
-        const uint32_t* rec = R + r * RW;
-        typename RollFor<K>::T roll(k);
-        for (int j = 0; j < k - 1; ++j) roll.push(rec_sym(rec, j));
-        for (uint32_t w = 0; w < nw; ++w) {
-            roll.push(rec_sym(rec, k - 1 + (int)w));
-            const K key = roll.canon();
+        for_each_window<K, RWK>(wd, k, [&](int w, const K& key) {
             keys[pos + w] = key;
             atomicAdd(&h[part_digit(key, D)], 1u);
-        }
+        });
     }
     __syncthreads();
     // reserve one range per non-empty digit (bin-relative cursors), then place keys
@@ -674,10 +659,11 @@ cudaError_t launch_make_pieces(const LargeBin* lbins, const uint64_t* piece_pref
 int msd_piece_records(int k) { return k <= 32 ? MsdPiece<uint64_t>::REC : MsdPiece<K128>::REC; }
 
 int msd_digit_bits(uint64_t bin_windows, int k, int cap) {
-    // about cap/8 keys per digit on average; 1 <= D <= 12
+    // about cap/4 keys per digit on average (hashed digits are near-uniform, so chunks of
+    // 3-4 digits fill a CTA); 1 <= D <= 12
     (void)k;
     int D = 1;
-    while (D < MSD_MAXD && (bin_windows >> D) > (uint64_t)std::max(1, cap / 8)) ++D;
+    while (D < MSD_MAXD && (bin_windows >> D) > (uint64_t)std::max(1, cap / 4)) ++D;
     return D;
 }
 
@@ -701,20 +687,21 @@ cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaS
 uint64_t greedy_segments(uint64_t n_digits) { return (n_digits + GP_SEG - 1) / GP_SEG; }
 
 cudaError_t launch_large_scatter(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
-                                 int k, uint32_t* digit_cur, void* keys, cudaStream_t s) {
+                                 int k, int dmax, uint32_t* digit_cur, void* keys, cudaStream_t s) {
     if (n_pieces == 0) return cudaSuccess;
     cudaError_t e;
     if (k <= 32) {
-        const int sm = (int)scatter_smem<uint64_t>();
+        const int sm = (int)scatter_smem<uint64_t>(k, dmax);
         if ((e = cudaFuncSetAttribute(k_large_scatter<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)))
             return e;
-        k_large_scatter<uint64_t><<<(unsigned)n_pieces, MSD_NT, sm, s>>>(bins, pieces, lbins, k, digit_cur,
+        k_large_scatter<uint64_t><<<(unsigned)n_pieces, MSD_NT, sm, s>>>(bins, pieces, lbins, k, dmax, digit_cur,
                                                                          (uint64_t*)keys);
     } else {
-        const int sm = (int)scatter_smem<K128>();
+        const int sm = (int)scatter_smem<K128>(k, dmax);
         if ((e = cudaFuncSetAttribute(k_large_scatter<K128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)))
             return e;
-        k_large_scatter<K128><<<(unsigned)n_pieces, MSD_NT, sm, s>>>(bins, pieces, lbins, k, digit_cur, (K128*)keys);
+        k_large_scatter<K128><<<(unsigned)n_pieces, MSD_NT, sm, s>>>(bins, pieces, lbins, k, dmax, digit_cur,
+                                                                     (K128*)keys);
     }
     return cudaGetLastError();
 }

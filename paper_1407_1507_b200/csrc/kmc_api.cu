@@ -308,6 +308,20 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     a.hist_w = hist_w;
     a.hist_r = hist_r;
     a.gstats = gstats;
+    // temporary record stream: pass 1 appends its records so S5 is a copy, not a recompute
+    // (estimate n_bases/8 records; on overflow S5 falls back to recomputing pass 1)
+    const int RWt = record_words(k);
+    uint32_t* tmp_recs = nullptr;
+    uint32_t* tmp_sig = nullptr;
+    uint64_t tmp_cap = 0;
+    if (j->opt.distribute_path != 1) {
+        tmp_cap = std::max<uint64_t>(n_bases / 8, 4096);
+        tmp_recs = reinterpret_cast<uint32_t*>(ar.alloc(tmp_cap * RWt * 4));
+        tmp_sig = ar.get<uint32_t>(tmp_cap);
+    }
+    a.tmp_recs = tmp_recs;
+    a.tmp_sig = tmp_sig;
+    a.tmp_cap = tmp_cap;
     CK(launch_p1(P1_MODE_HIST, a, n_tiles, s));
     j->launches += 2;
     j->stage_end(2);
@@ -388,18 +402,31 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     j->st.large_windows = large_windows;
     j->st.max_bin_windows = max_bin;
 
-    // ---- pass 2: S1-S3 again + S5 scatter of records into bins
+    // ---- S5: records into bins -- a copy from pass 1's temporary stream, or (if the stream
+    //      overflowed its estimate) pass 2 = S1-S3 recomputed + scatter
     uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4));
     uint32_t* bin_fill = ar.get<uint32_t>(n_bins);
+    const uint64_t tmp_n = hs[16 + GS_TMP_RECS];
     j->stage_begin(KMC_STAGE_SCATTER);
     CK(cudaMemsetAsync(bin_fill, 0, n_bins * 4, s));
-    a.sig2bin = pa.sig2bin;
-    a.bin_rec_off = pa.bin_rec_off;
-    a.bin_fill = bin_fill;
-    a.bins = bins;
-    CK(launch_p1(P1_MODE_SCATTER, a, n_tiles, s));
+    if (tmp_recs && tmp_n <= tmp_cap) {
+        if (tmp_n != n_records) {
+            set_err("temporary record stream holds %llu records, histogram %llu", (unsigned long long)tmp_n,
+                    (unsigned long long)n_records);
+            throw Fail{KMC_ERR_INTERNAL};
+        }
+        CK(launch_bin_scatter(tmp_recs, tmp_sig, tmp_n, k, pa.sig2bin, pa.bin_rec_off, bin_fill, bins, s));
+    } else {
+        a.sig2bin = pa.sig2bin;
+        a.bin_rec_off = pa.bin_rec_off;
+        a.bin_fill = bin_fill;
+        a.bins = bins;
+        CK(launch_p1(P1_MODE_SCATTER, a, n_tiles, s));
+    }
     j->launches += 1;
     j->stage_end(1);
+    ar.release(tmp_recs);
+    ar.release(tmp_sig);
     ar.release(hist_w);
     ar.release(hist_r);
     ar.release(pa.cost_scan);
@@ -486,9 +513,11 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         std::vector<LargeBin> lbins(large_ids.size());
         std::vector<uint64_t> pp(large_ids.size() + 1, 0);
         uint64_t key_base = 0, digit_base = 0;
+        int dmax = 1;
         for (size_t i = 0; i < large_ids.size(); ++i) {
             const uint64_t b = large_ids[i];
             const int D = msd_digit_bits(bw[b], k, kcap);
+            dmax = std::max(dmax, D);
             lbins[i] = LargeBin{key_base, digit_base, bo[b], (uint32_t)bw[b], (uint32_t)D, (uint32_t)bn[b], 0};
             key_base += bw[b];
             digit_base += 1ull << D;
@@ -525,7 +554,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         ga.counters = counters;
         ga.cap = (uint32_t)kcap;
         CK(launch_greedy_chunks(ga, lbins.size(), s));
-        CK(launch_large_scatter(bins, d_pieces, n_pieces, d_lbins, k, digit_cur, lkeys, s));
+        CK(launch_large_scatter(bins, d_pieces, n_pieces, d_lbins, k, dmax, digit_cur, lkeys, s));
         j->launches += 4;
         j->stage_end(4);
         CK(cudaMemcpyAsync(&hs[48], counters, 16, cudaMemcpyDeviceToHost, s));

@@ -93,6 +93,52 @@ __host__ __device__ __forceinline__ int record_words(int k) { return k <= 32 ? 4
 __host__ __device__ __forceinline__ int record_max_windows(int k) { return 16 * record_words(k) - 4 - k + 1; }
 
 __device__ __forceinline__ uint32_t rec_nwin(const uint32_t* rec) { return rec[0] >> 24; }
+
+template <class K> struct RecWords;
+template <> struct RecWords<uint64_t> { static constexpr int v = 4; };
+template <> struct RecWords<K128> { static constexpr int v = 8; };
+
+// Calls emit(w, key) for the windows w = 0..n-1 of a record held in registers: the
+// canonical key min(fwd, rc) of every window.  The symbol loop is fully
+// unrolled so every symbol's word and shift are compile-time constants.
+template <class K, int RW, class F>
+__device__ __forceinline__ void for_each_window(const uint32_t (&wd)[RW], int k, F&& emit) {
+    typename RollFor<K>::T roll(k);
+    const int nb = (int)(wd[0] >> 24) + k - 1;
+#pragma unroll
+    for (int j = 0; j < 16 * RW - 4; ++j) {
+        if (j >= nb) break;
+        const int g = 8 + 2 * j;
+        roll.push((wd[g >> 5] >> (30 - (g & 31))) & 3u);
+        if (j >= k - 1) emit(j - (k - 1), roll.canon());
+    }
+}
+
+// Digit of the large-bin split: a multiplicative hash of the whole key (equal keys share
+// a digit; the top bits of a key are a poor digit, see k_sort.cu).  1 <= D <= 12.
+__device__ __forceinline__ uint32_t part_digit(uint64_t key, int D) {
+    const uint32_t h = (((uint32_t)(key >> 32) * 0x85EBCA6Bu) ^ (uint32_t)key) * 0x9E3779B1u;
+    return h >> (32 - D);
+}
+__device__ __forceinline__ uint32_t part_digit(const K128& key, int D) {
+    const uint32_t h = (((uint32_t)(key.hi >> 32) * 0x27D4EB2Fu) ^ ((uint32_t)key.hi * 0xC2B2AE35u) ^
+                        ((uint32_t)(key.lo >> 32) * 0x85EBCA6Bu) ^ (uint32_t)key.lo) *
+                       0x9E3779B1u;
+    return h >> (32 - D);
+}
+
+// Loads a record (16-byte aligned, RW words) into registers.
+template <int RW>
+__device__ __forceinline__ void load_record(const uint32_t* rec, uint32_t (&wd)[RW]) {
+#pragma unroll
+    for (int q = 0; q < RW / 4; ++q) {
+        const uint4 v = reinterpret_cast<const uint4*>(rec)[q];
+        wd[4 * q] = v.x;
+        wd[4 * q + 1] = v.y;
+        wd[4 * q + 2] = v.z;
+        wd[4 * q + 3] = v.w;
+    }
+}
 __device__ __forceinline__ uint32_t rec_sym(const uint32_t* rec, int j) {
     int g = 8 + 2 * j;
     return (rec[g >> 5] >> (30 - (g & 31))) & 3u;
@@ -300,64 +346,101 @@ __device__ __forceinline__ void block_scan_whist(uint32_t* whist, uint32_t* wsum
     __syncthreads();
 }
 
+// Largest value of a key with nbits bits (sorts after every real key in every digit).
+template <class K> __device__ __forceinline__ K key_sentinel(int nbits);
+template <> __device__ __forceinline__ uint64_t key_sentinel<uint64_t>(int nbits) {
+    return nbits >= 64 ? ~0ull : ((1ull << nbits) - 1);
+}
+template <> __device__ __forceinline__ K128 key_sentinel<K128>(int nbits) {
+    K128 s;
+    s.lo = nbits >= 64 ? ~0ull : ((1ull << nbits) - 1);
+    s.hi = nbits >= 128 ? ~0ull : (nbits > 64 ? ((1ull << (nbits - 64)) - 1) : 0ull);
+    return s;
+}
+
 // In-place LSD radix sort of n <= NT*KPT keys (+ optional uint32 values) in shared memory
-// over bits [0, nbits), 8-bit digits, constant digits skipped.  Warp w owns positions
-// [w*32*KPT, (w+1)*32*KPT); per pass every key is read once into registers and ranked
-// once: __match_any_sync gives its peers in the round, the warp's running digit counter
-// (read before the leader adds the round's peers) gives the keys of earlier rounds; after
-// the block-wide digit-major scan the key is stored straight to its final position.
-// Rounds are processed in position order, so every pass is stable.
+// over bits [0, nbits), 8-bit digits, constant digits skipped.  The keys are padded with
+// sentinels to rounds*NT (A needs that capacity); warp w owns positions
+// [w*32*rounds, (w+1)*32*rounds).  Per pass every key is read once into registers and
+// ranked once: __match_any_sync gives its peers in the round (the peer with no lower peer
+// is the leader), the warp's running digit counter -- read before the leader adds the
+// round's peers -- gives the keys of earlier rounds; after the block-wide scan of the
+// warp-major counters the key is stored straight to its final position.  Rounds are
+// processed in position order, so every pass is stable and the sentinels stay last.
 template <class K, int NT, int KPT, bool VALS>
 __device__ __forceinline__ void block_sort_inplace(K* A, uint32_t* VA, int n, int nbits, uint32_t* whist,
                                                    uint32_t* wsum, unsigned long long* red) {
     constexpr int NW = NT / 32;
+    static_assert(NT >= RADIX, "one thread per digit in the scan");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ltm = lanemask_lt();
     uint64_t vlo, vhi;
     block_varying_bits<K, NT>(A, n, red, vlo, vhi);
-    // warp segments sized from n (multiples of 32), at most KPT rounds each
-    const int rounds = (((n + NW - 1) / NW) + 31) / 32;
+    const int rounds = (n + NT - 1) / NT;
+    const int m = rounds * NT;
+    {
+        const K sent = key_sentinel<K>(nbits);
+        for (int i = n + threadIdx.x; i < m; i += NT) {
+            A[i] = sent;
+            if (VALS) VA[i] = 0;
+        }
+    }
+    __syncthreads();  // the padding is read by the owners of the warp segments
     const int wbase = warp * rounds * 32;
+    uint32_t* wh = whist + warp * RADIX;
     for (int shift = 0; shift < nbits; shift += RADIX_BITS) {
         if (!digit_varies(vlo, vhi, shift)) continue;
-        for (int i = threadIdx.x; i < RADIX * NW; i += NT) whist[i] = 0;
+        for (int i = threadIdx.x; i < RADIX * NW / 4; i += NT) reinterpret_cast<uint4*>(whist)[i] = make_uint4(0, 0, 0, 0);
         K key[KPT];
         uint32_t val[KPT];
         uint32_t rank[KPT];
 #pragma unroll
         for (int r = 0; r < KPT; ++r) {
             if (r >= rounds) break;
-            const int i = wbase + r * 32 + lane;
-            if (i < n) {
-                key[r] = A[i];
-                if (VALS) val[r] = VA[i];
-            }
+            key[r] = A[wbase + r * 32 + lane];
+            if (VALS) val[r] = VA[wbase + r * 32 + lane];
         }
         __syncthreads();
-#pragma unroll
-        for (int r = 0; r < KPT; ++r) {
-            if (r >= rounds || wbase + r * 32 >= n) break;
-            const int i = wbase + r * 32 + lane;
-            const bool ok = i < n;
-            const uint32_t d = ok ? key_digit(key[r], shift) : (uint32_t)(RADIX + lane);
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const uint32_t pre = ok ? whist[d * NW + warp] : 0u;
-            __syncwarp();
-            if (ok && lane == __ffs(peers) - 1) whist[d * NW + warp] = pre + __popc(peers);
-            __syncwarp();
-            rank[r] = pre + __popc(peers & ltm);
-        }
-        __syncthreads();
-        block_scan_whist<NT>(whist, wsum);
 #pragma unroll
         for (int r = 0; r < KPT; ++r) {
             if (r >= rounds) break;
-            const int i = wbase + r * 32 + lane;
-            if (i < n) {
-                const uint32_t pos = whist[key_digit(key[r], shift) * NW + warp] + rank[r];
-                A[pos] = key[r];
-                if (VALS) VA[pos] = val[r];
+            const uint32_t d = key_digit(key[r], shift);
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t below = __popc(peers & ltm);
+            const uint32_t pre = wh[d];
+            __syncwarp();
+            if (below == 0) wh[d] = pre + __popc(peers);
+            __syncwarp();
+            rank[r] = pre + below;
+        }
+        __syncthreads();
+        // digit-major exclusive offsets from the warp-major counters (thread t < RADIX owns digit t)
+        {
+            uint32_t c[NW];
+            uint32_t tot = 0;
+            if (threadIdx.x < RADIX) {
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    c[w] = whist[w * RADIX + threadIdx.x];
+                    tot += c[w];
+                }
             }
+            uint32_t run = block_excl_sum<NT, uint32_t>(threadIdx.x < RADIX ? tot : 0u, wsum, nullptr);
+            if (threadIdx.x < RADIX) {
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    whist[w * RADIX + threadIdx.x] = run;
+                    run += c[w];
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+            if (r >= rounds) break;
+            const uint32_t pos = wh[key_digit(key[r], shift)] + rank[r];
+            A[pos] = key[r];
+            if (VALS) VA[pos] = val[r];
         }
         __syncthreads();
     }

@@ -19,6 +19,7 @@ enum {
     GS_SURV = 7,        // survivor cursor
     GS_LARGE_KEYS = 8,  // large-bin key cursor
     GS_SIGS_USED = 9,
+    GS_TMP_RECS = 10,   // records appended to the temporary stream by pass 1
     GS_N = 16
 };
 
@@ -44,6 +45,10 @@ struct P1Args {
     const uint64_t* bin_rec_off;
     uint32_t* bin_fill;
     uint32_t* bins;
+    // pass 1: temporary record stream (nullptr = not used)
+    uint32_t* tmp_recs;
+    uint32_t* tmp_sig;
+    uint64_t tmp_cap;  // records
     // debug
     uint32_t* dbg_sig;
 };
@@ -55,6 +60,9 @@ cudaError_t launch_tile_reads(const uint64_t* offsets, uint64_t n_reads, uint64_
                               uint64_t* tile_r_lo, cudaStream_t s);
 cudaError_t launch_p1(int mode, const P1Args& a, uint64_t n_tiles, cudaStream_t s);
 cudaError_t launch_debug_allowed(int p, uint8_t* out, cudaStream_t s);
+cudaError_t launch_bin_scatter(const uint32_t* tmp_recs, const uint32_t* tmp_sig, uint64_t n, int k,
+                               const uint32_t* sig2bin, const uint64_t* bin_rec_off, uint32_t* bin_fill,
+                               uint32_t* bins, cudaStream_t s);
 
 // ------------------------------------------------------------ scans / plan
 // out[0..n] exclusive prefix sums (out[n] = total) of in[0..n) (uint64).
@@ -148,7 +156,7 @@ struct GreedyArgs {
 cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaStream_t s);
 uint64_t greedy_segments(uint64_t n_digits);
 cudaError_t launch_large_scatter(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
-                                 int k, uint32_t* digit_cur, void* keys, cudaStream_t s);
+                                 int k, int dmax, uint32_t* digit_cur, void* keys, cudaStream_t s);
 cudaError_t launch_chunk_sort(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
                               uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
                               cudaStream_t s);

@@ -100,7 +100,8 @@ def test_count_parity_configs(gpu, name, scale):
 
 
 @pytest.mark.parametrize("opts", [dict(force_large=True), dict(small_bin_capacity=64), dict(small_bin_capacity=1024),
-                                  dict(large_path=1), dict(force_large=True, large_path=1)])
+                                  dict(large_path=1), dict(force_large=True, large_path=1),
+                                  dict(distribute_path=1)])
 def test_forced_paths(gpu, opts):
     w = synth.make("C5", scale=0.005)
     st = assert_same(gpu, w, **opts)
