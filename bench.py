@@ -132,6 +132,17 @@ def run_oracle_sample(w, n_reads_sample: int):
     return dt, int(offs[-1] - offs[0]), r.n_windows, n
 
 
+def reduce_max(value: float, world: int, device=None) -> float:
+    """Max over ranks (the timing rule: a multi-GPU step takes as long as its slowest rank)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -209,11 +220,7 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = reduce_max(ev0.elapsed_time(ev1) / args.steps, world, "cuda")
 
     # ---- e2e: same call with pinned HOST buffers (H2D of inputs and D2H of outputs inside)
     e2e = None
@@ -236,11 +243,7 @@ def main():
             del r
         e1.record(stream)
         torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1) / e_steps
-        if world > 1:
-            t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+        e_ms = reduce_max(e0.elapsed_time(e1) / e_steps, world, "cuda")
         e2e = {"value": world * n_bases / (e_ms / 1e3), "unit": "bases/s",
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(w.reads.nbytes + w.offsets.nbytes),
                "d2h_bytes_per_step": int(n_out * ((8 if k <= 32 else 16) + 4))}

@@ -26,6 +26,12 @@ __device__ __forceinline__ uint32_t key_digit(uint64_t a, int shift) { return (u
 __device__ __forceinline__ uint32_t key_digit(const K128& a, int shift) {
     return shift < 64 ? (uint32_t)(a.lo >> shift) & (RADIX - 1) : (uint32_t)(a.hi >> (shift - 64)) & (RADIX - 1);
 }
+// 32-bit word w (0 = least significant) of a key
+__device__ __forceinline__ uint32_t key_word(uint64_t a, int w) { return w ? (uint32_t)(a >> 32) : (uint32_t)a; }
+__device__ __forceinline__ uint32_t key_word(const K128& a, int w) {
+    const uint64_t x = (w & 2) ? a.hi : a.lo;
+    return (w & 1) ? (uint32_t)(x >> 32) : (uint32_t)x;
+}
 __device__ __forceinline__ uint64_t key_min(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ K128 key_min(const K128& a, const K128& b) { return key_lt(b, a) ? b : a; }
 
@@ -281,12 +287,12 @@ __device__ __forceinline__ void block_varying_bits(const K* keys, int n, unsigne
     __syncthreads();
     uint64_t o = 0, a = ~0ull, oh = 0, ah = ~0ull;
     for (int i = threadIdx.x; i < n; i += NT) key_or_and_accum(keys[i], o, a, oh, ah);
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-        o |= __shfl_xor_sync(0xffffffffu, o, s);
-        a &= __shfl_xor_sync(0xffffffffu, a, s);
-        oh |= __shfl_xor_sync(0xffffffffu, oh, s);
-        ah &= __shfl_xor_sync(0xffffffffu, ah, s);
+    {
+        const unsigned FULL = 0xffffffffu;
+        o = ((uint64_t)__reduce_or_sync(FULL, (unsigned)(o >> 32)) << 32) | __reduce_or_sync(FULL, (unsigned)o);
+        a = ((uint64_t)__reduce_and_sync(FULL, (unsigned)(a >> 32)) << 32) | __reduce_and_sync(FULL, (unsigned)a);
+        oh = ((uint64_t)__reduce_or_sync(FULL, (unsigned)(oh >> 32)) << 32) | __reduce_or_sync(FULL, (unsigned)oh);
+        ah = ((uint64_t)__reduce_and_sync(FULL, (unsigned)(ah >> 32)) << 32) | __reduce_and_sync(FULL, (unsigned)ah);
     }
     if ((threadIdx.x & 31) == 0) {
         atomicOr(&red[0], (unsigned long long)o);
@@ -390,6 +396,8 @@ __device__ __forceinline__ void block_sort_inplace(K* A, uint32_t* VA, int n, in
     uint32_t* wh = whist + warp * RADIX;
     for (int shift = 0; shift < nbits; shift += RADIX_BITS) {
         if (!digit_varies(vlo, vhi, shift)) continue;
+        // the digit lives in one 32-bit word of the key: word index and in-word shift
+        const int wsel = shift >> 5, wsh = shift & 31;
         for (int i = threadIdx.x; i < RADIX * NW / 4; i += NT) reinterpret_cast<uint4*>(whist)[i] = make_uint4(0, 0, 0, 0);
         K key[KPT];
         uint32_t val[KPT];
@@ -401,17 +409,20 @@ __device__ __forceinline__ void block_sort_inplace(K* A, uint32_t* VA, int n, in
             if (VALS) val[r] = VA[wbase + r * 32 + lane];
         }
         __syncthreads();
+        // rank: peers of the round from __match_any_sync; the warp's running counter (read
+        // by all peers before the round's leader -- the peer with no lower peer -- adds the
+        // round's count) gives the keys of earlier rounds.  Rounds in order => stable.
 #pragma unroll
         for (int r = 0; r < KPT; ++r) {
             if (r >= rounds) break;
-            const uint32_t d = key_digit(key[r], shift);
+            const uint32_t d = (key_word(key[r], wsel) >> wsh) & (RADIX - 1);
             const uint32_t peers = __match_any_sync(0xffffffffu, d);
             const uint32_t below = __popc(peers & ltm);
             const uint32_t pre = wh[d];
             __syncwarp();
             if (below == 0) wh[d] = pre + __popc(peers);
             __syncwarp();
-            rank[r] = pre + below;
+            rank[r] = ((pre + below) << 8) | d;  // rank < 2^16 (n <= NT*KPT), digit < 2^8
         }
         __syncthreads();
         // digit-major exclusive offsets from the warp-major counters (thread t < RADIX owns digit t)
@@ -438,7 +449,7 @@ __device__ __forceinline__ void block_sort_inplace(K* A, uint32_t* VA, int n, in
 #pragma unroll
         for (int r = 0; r < KPT; ++r) {
             if (r >= rounds) break;
-            const uint32_t pos = wh[key_digit(key[r], shift)] + rank[r];
+            const uint32_t pos = wh[rank[r] & (RADIX - 1)] + (rank[r] >> 8);
             A[pos] = key[r];
             if (VALS) VA[pos] = val[r];
         }
@@ -449,12 +460,14 @@ __device__ __forceinline__ void block_sort_inplace(K* A, uint32_t* VA, int n, in
 // Run-length compaction of the sorted keys S[0..n) with the cutoffs ci <= count <= cx
 // (S8).  bits: (n+32)/32+1 uint32 of scratch.  Run starts are found with warp ballots; a
 // run's length is the distance to the next start bit.  Survivors are appended, in any
-// order, at a range reserved with one global atomic per CTA.
+// order, at ranges reserved with one global atomic per warp and round.
 template <class K, int NT>
 __device__ __forceinline__ void block_rle_bitmask(const K* S, int n, uint32_t* bits, uint32_t ci, uint32_t cx,
                                                   K* out_keys, uint32_t* out_counts, unsigned long long* gstats,
                                                   uint32_t* wsum, unsigned int* scnt, unsigned long long* bcast,
                                                   int gs_surv, int gs_unique, int gs_below, int gs_above) {
+    (void)wsum;
+    (void)bcast;
     const int lane = threadIdx.x & 31;
     const int nwords = (n + 32) / 32;  // covers the sentinel bit n
     for (int base = (threadIdx.x & ~31); base < nwords * 32; base += NT) {
@@ -465,30 +478,45 @@ __device__ __forceinline__ void block_rle_bitmask(const K* S, int n, uint32_t* b
     }
     if (threadIdx.x < 4) scnt[threadIdx.x] = 0;
     __syncthreads();
-    uint32_t uniq = 0, below = 0, above = 0, keep = 0;
-    for (int i = threadIdx.x; i < n; i += NT) {
-        if (!((bits[i >> 5] >> (i & 31)) & 1u)) continue;
-        int pos = i + 1, wd = pos >> 5;
-        uint32_t m = bits[wd] & (0xFFFFFFFFu << (pos & 31));
-        while (m == 0) m = bits[++wd];
-        const uint32_t run = (uint32_t)(wd * 32 + __ffs(m) - 1 - i);
-        ++uniq;
-        if (run < ci) ++below;
-        else if (run > cx) ++above;
-        else ++keep;
-    }
-    const uint32_t tk = block_sum<NT, uint32_t>(keep, wsum);
-    if (threadIdx.x == 0) {
-        *bcast = tk ? atomicAdd(&gstats[gs_surv], (unsigned long long)tk) : 0ull;
+    uint32_t uniq = 0, below = 0, above = 0;
+    const uint32_t ltm = lanemask_lt();
+    for (int i0 = (threadIdx.x & ~31); i0 < n; i0 += NT) {
+        const int i = i0 + lane;
+        uint32_t run = 0;
+        const uint32_t w0 = bits[i0 >> 5];
+        if (i < n && ((w0 >> lane) & 1u)) {
+            int pos = i + 1, wd = pos >> 5;
+            uint32_t m = bits[wd] & (0xFFFFFFFFu << (pos & 31));
+            while (m == 0) m = bits[++wd];
+            run = (uint32_t)(wd * 32 + __ffs(m) - 1 - i);
+            ++uniq;
+            if (run < ci) {
+                ++below;
+                run = 0;
+            } else if (run > cx) {
+                ++above;
+                run = 0;
+            }
+        }
+        const uint32_t b = __ballot_sync(0xffffffffu, run != 0);
+        if (b) {
+            unsigned long long slot = 0;
+            if (lane == 0) slot = atomicAdd(&gstats[gs_surv], (unsigned long long)__popc(b));
+            slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(b & ltm);
+            if (run) {
+                out_keys[slot] = S[i];
+                out_counts[slot] = run;
+            }
+        }
     }
     {
         const uint32_t a = __reduce_add_sync(0xffffffffu, uniq);
         const uint32_t b = __reduce_add_sync(0xffffffffu, below);
         const uint32_t c = __reduce_add_sync(0xffffffffu, above);
         if (lane == 0) {
-            atomicAdd(&scnt[1], a);
-            atomicAdd(&scnt[2], b);
-            atomicAdd(&scnt[3], c);
+            if (a) atomicAdd(&scnt[1], a);
+            if (b) atomicAdd(&scnt[2], b);
+            if (c) atomicAdd(&scnt[3], c);
         }
     }
     __syncthreads();
@@ -496,26 +524,6 @@ __device__ __forceinline__ void block_rle_bitmask(const K* S, int n, uint32_t* b
         if (scnt[1]) atomicAdd(&gstats[gs_unique], (unsigned long long)scnt[1]);
         if (scnt[2]) atomicAdd(&gstats[gs_below], (unsigned long long)scnt[2]);
         if (scnt[3]) atomicAdd(&gstats[gs_above], (unsigned long long)scnt[3]);
-    }
-    const unsigned long long base = *bcast;
-    for (int i0 = (threadIdx.x & ~31); i0 < n; i0 += NT) {
-        const int i = i0 + lane;
-        uint32_t run = 0;
-        if (i < n && ((bits[i >> 5] >> (i & 31)) & 1u)) {
-            int pos = i + 1, wd = pos >> 5;
-            uint32_t m = bits[wd] & (0xFFFFFFFFu << (pos & 31));
-            while (m == 0) m = bits[++wd];
-            run = (uint32_t)(wd * 32 + __ffs(m) - 1 - i);
-            if (run < ci || run > cx) run = 0;
-        }
-        const uint32_t b = __ballot_sync(0xffffffffu, run != 0);
-        uint32_t slot = 0;
-        if (lane == 0 && b) slot = atomicAdd(&scnt[0], (uint32_t)__popc(b));
-        slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(b & lanemask_lt());
-        if (run) {
-            out_keys[base + slot] = S[i];
-            out_counts[base + slot] = run;
-        }
     }
 }
 
