@@ -270,8 +270,16 @@ def main():
     dom = max(per_stage, key=lambda s_: per_stage[s_]["ms"])
     dom_ms = per_stage[dom]["ms"]
     achieved = sb.get(dom, 0.0) / (dom_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        if tj.get("workload") == args.config and float(tj.get("scale", 0)) == args.scale and dom in tj["stages"]:
+            e = tj["stages"][dom]
+            traffic = int(e["dram_bytes_read"] + e["dram_bytes_write"])
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
-            "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+            "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+            "alg_bytes_per_launch": int(sb.get(dom, 0.0)), "ms_per_launch": dom_ms,
             "peak_source": peaks["source"],
             "whole_step": {"alg_bytes": int(sum(v for s_, v in sb.items() if s_ in ("signature", "scatter"))),
                            "note": "see DESIGN.md 6 for B_alg of the full pipeline"}}

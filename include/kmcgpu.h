@@ -104,6 +104,8 @@ typedef struct {
     uint64_t n_above_max;      /* distinct k-mers removed by cutoff_max */
     uint64_t n_out;            /* pairs written; or required, on KMC_ERR_OUT_CAPACITY */
     uint64_t n_launches;       /* kernels this library launched for the call */
+    uint64_t n_input_batches;  /* pass-1 batches of host-resident reads (0: reads were on the device) */
+    uint64_t n_large_groups;   /* memory-bounded groups the large bins were processed in */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;
@@ -118,7 +120,12 @@ typedef struct {
                                   1: device-wide LSD radix sort of all large-bin keys (testing) */
     uint32_t distribute_path;  /* 0: pass 1 streams its records, S5 copies them into bins (default);
                                   1: S5 recomputes pass 1 from the reads (testing) */
-    uint32_t reserved[3];
+    uint32_t input_batch_mb;   /* host-resident reads are streamed through pass 1 in read-aligned
+                                  batches of this many MiB (0 = default 1024), double-buffered so
+                                  the H2D copy of batch i+1 overlaps pass 1 on batch i */
+    uint32_t large_group_mkeys;/* large bins are split/sorted in groups of at most this many Mi
+                                  keys (0 = auto: as many as fit in free device memory) */
+    uint32_t reserved[1];
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).

@@ -94,6 +94,20 @@ struct Arena {
         return p;
     }
     template <class T> T* get(size_t n) { return reinterpret_cast<T*>(alloc(n * sizeof(T))); }
+    // nullptr instead of an error when the allocator is out of memory
+    void* try_alloc(size_t bytes) {
+        bytes = (bytes + 255) & ~(size_t)255;
+        if (bytes == 0) bytes = 256;
+        void* p = nullptr;
+        if (af) p = af(bytes, (void*)s, ctx);
+        else if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) p = nullptr;
+        if (!p) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        ptrs.push_back(p);
+        return p;
+    }
     void release(void* p) {
         if (!p) return;
         auto it = std::find(ptrs.begin(), ptrs.end(), p);
@@ -168,6 +182,18 @@ struct kmc_job {
     int cur_stage = -1;
     cudaEvent_t cur_a = nullptr;
     unsigned long long* host_small = nullptr;  // pinned readback area
+    cudaStream_t cs = nullptr;                 // copy stream for streamed input batches
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+
+    void make_copy_stream() {
+        if (cs) return;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int t = 0; t < 2; ++t) {
+            CK(cudaEventCreateWithFlags(&ev_copy[t], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_done[t], cudaEventDisableTiming));
+            CK(cudaEventRecord(ev_done[t], s));
+        }
+    }
 
     void stage_begin(int stage) {
         cur_stage = stage;
@@ -201,6 +227,14 @@ struct kmc_job {
             cudaEventDestroy(e.b);
         }
         if (cur_a) cudaEventDestroy(cur_a);
+        if (cs) {
+            cudaStreamSynchronize(cs);
+            for (int t = 0; t < 2; ++t) {
+                cudaEventDestroy(ev_copy[t]);
+                cudaEventDestroy(ev_done[t]);
+            }
+            cudaStreamDestroy(cs);
+        }
         arena.release_all();
         pin_release(host_small);
     }
@@ -267,16 +301,24 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         set_err("n_bases=%llu exceeds the per-call limit 2^36", (unsigned long long)n_bases);
         throw Fail{KMC_ERR_INVALID_ARG};
     }
-    // ---- inputs on the device
+    // ---- inputs: device-resident reads are used in place; host-resident reads are streamed
+    //      through pass 1 in read-aligned batches (f2: "pinned host memory only when the
+    //      input exceeds HBM"), so the reads never need to fit in device memory.
+    const bool host_reads = !is_device_ptr(reads);
     const uint8_t* d_reads = reads;
     const uint64_t* d_off = offsets;
+    std::vector<uint64_t> h_off_copy;
+    const uint64_t* h_off = nullptr;
     j->stage_begin(KMC_STAGE_INPUT);
-    if (!is_device_ptr(reads)) {
-        uint8_t* r = ar.get<uint8_t>(n_bases);
-        CK(cudaMemcpyAsync(r, reads, n_bases, cudaMemcpyHostToDevice, s));
-        d_reads = r;
-    }
-    if (!is_device_ptr(offsets)) {
+    if (host_reads) {
+        if (is_device_ptr(offsets)) {
+            h_off_copy.resize(n_reads + 1);
+            CK(cudaMemcpy(h_off_copy.data(), offsets, (n_reads + 1) * 8, cudaMemcpyDeviceToHost));
+            h_off = h_off_copy.data();
+        } else {
+            h_off = offsets;
+        }
+    } else if (!is_device_ptr(offsets)) {
         uint64_t* o = ar.get<uint64_t>(n_reads + 1);
         CK(cudaMemcpyAsync(o, offsets, (n_reads + 1) * 8, cudaMemcpyHostToDevice, s));
         d_off = o;
@@ -288,13 +330,12 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     unsigned long long* hist_w = ar.get<unsigned long long>(ns);
     uint32_t* hist_r = ar.get<uint32_t>(ns);
     unsigned long long* gstats = ar.get<unsigned long long>(GS_N);
-    const uint64_t n_tiles = p1_num_tiles(n_bases);
-    uint64_t* tile_r_lo = ar.get<uint64_t>(n_tiles);
+    const uint64_t n_tiles = host_reads ? 0 : p1_num_tiles(n_bases);
+    uint64_t* tile_r_lo = host_reads ? nullptr : ar.get<uint64_t>(n_tiles);
     j->stage_begin(KMC_STAGE_SIGNATURE);
     CK(cudaMemsetAsync(hist_w, 0, ns * 8, s));
     CK(cudaMemsetAsync(hist_r, 0, ns * 4, s));
     CK(cudaMemsetAsync(gstats, 0, GS_N * 8, s));
-    CK(launch_tile_reads(d_off, n_reads, off0, n_tiles, tile_r_lo, s));
     P1Args a{};
     a.reads = d_reads;
     a.offsets = d_off;
@@ -322,9 +363,67 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     a.tmp_recs = tmp_recs;
     a.tmp_sig = tmp_sig;
     a.tmp_cap = tmp_cap;
-    CK(launch_p1(P1_MODE_HIST, a, n_tiles, s));
-    j->launches += 2;
-    j->stage_end(2);
+    // batches of host-resident reads: [r0, r1) with at most batch_bytes bases (one read may
+    // exceed it alone); two device slots, H2D on a copy stream overlapping pass 1
+    std::vector<std::pair<uint64_t, uint64_t>> batches;
+    uint8_t* bbuf[2] = {nullptr, nullptr};
+    uint64_t* bofs[2] = {nullptr, nullptr};
+    uint64_t* btile[2] = {nullptr, nullptr};
+    if (host_reads) {
+        const uint64_t batch_bytes = (uint64_t)(j->opt.input_batch_mb ? j->opt.input_batch_mb : 1024) << 20;
+        uint64_t max_b = 0, max_r = 0;
+        for (uint64_t r0 = 0; r0 < n_reads;) {
+            const uint64_t lim = h_off[r0] + batch_bytes;
+            uint64_t r1 = (uint64_t)(std::upper_bound(h_off + r0 + 1, h_off + n_reads + 1, lim) - h_off) - 1;
+            if (r1 <= r0) r1 = r0 + 1;
+            batches.push_back({r0, r1});
+            max_b = std::max(max_b, h_off[r1] - h_off[r0]);
+            max_r = std::max(max_r, r1 - r0);
+            r0 = r1;
+        }
+        for (int t = 0; t < 2 && t < (int)batches.size(); ++t) {
+            bbuf[t] = ar.get<uint8_t>(max_b + 16);
+            bofs[t] = ar.get<uint64_t>(max_r + 1);
+            btile[t] = ar.get<uint64_t>(p1_num_tiles(max_b) + 1);
+        }
+        j->st.n_input_batches = batches.size();
+    }
+    auto run_p1 = [&](int mode) -> int {
+        if (!host_reads) {
+            CK(launch_tile_reads(d_off, n_reads, off0, n_tiles, tile_r_lo, s));
+            CK(launch_p1(mode, a, n_tiles, s));
+            return 2;
+        }
+        int nl = 0;
+        for (size_t b = 0; b < batches.size(); ++b) {
+            const int t = (int)(b & 1);
+            const uint64_t r0 = batches[b].first, r1 = batches[b].second;
+            const uint64_t nb = h_off[r1] - h_off[r0];
+            CK(cudaStreamWaitEvent(j->cs, j->ev_done[t], 0));
+            CK(cudaMemcpyAsync(bbuf[t], reads + (h_off[r0] - off0), nb, cudaMemcpyHostToDevice, j->cs));
+            CK(cudaMemcpyAsync(bofs[t], h_off + r0, (r1 - r0 + 1) * 8, cudaMemcpyHostToDevice, j->cs));
+            CK(cudaEventRecord(j->ev_copy[t], j->cs));
+            CK(cudaStreamWaitEvent(s, j->ev_copy[t], 0));
+            P1Args ab = a;
+            ab.reads = bbuf[t];
+            ab.offsets = bofs[t];
+            ab.n_reads = r1 - r0;
+            ab.off0 = h_off[r0];
+            ab.n_bases = nb;
+            ab.reads_aligned16 = ((uintptr_t)bbuf[t] & 15) == 0;
+            ab.tile_r_lo = btile[t];
+            const uint64_t nt = p1_num_tiles(nb);
+            CK(launch_tile_reads(bofs[t], r1 - r0, h_off[r0], nt, btile[t], s));
+            CK(launch_p1(mode, ab, nt, s));
+            CK(cudaEventRecord(j->ev_done[t], s));
+            nl += 2;
+        }
+        return nl;
+    };
+    if (host_reads) j->make_copy_stream();
+    const int nl1 = run_p1(P1_MODE_HIST);
+    j->launches += nl1;
+    j->stage_end(nl1);
 
     // ---- S4: plan
     const int RW = record_words(k);
@@ -421,7 +520,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         a.bin_rec_off = pa.bin_rec_off;
         a.bin_fill = bin_fill;
         a.bins = bins;
-        CK(launch_p1(P1_MODE_SCATTER, a, n_tiles, s));
+        j->launches += run_p1(P1_MODE_SCATTER) - 1;
     }
     j->launches += 1;
     j->stage_end(1);
@@ -507,89 +606,133 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         ar.release(rs.tile_off);
         ar.release(rs.scan_temp);
     } else if (large_windows > 0) {
-        // MSD split: per large bin, D top bits -> digit ranges in HBM -> chunks <= cap keys
+        // hashed split: per large bin, a D-bit digit -> digit ranges in HBM -> chunks <= cap
+        // keys.  Large bins are processed in groups whose keys fit the device budget.
         const int kcap = small_capacity(k);
         const int prec = msd_piece_records(k);
-        std::vector<LargeBin> lbins(large_ids.size());
-        std::vector<uint64_t> pp(large_ids.size() + 1, 0);
-        uint64_t key_base = 0, digit_base = 0;
-        int dmax = 1;
-        for (size_t i = 0; i < large_ids.size(); ++i) {
-            const uint64_t b = large_ids[i];
-            const int D = msd_digit_bits(bw[b], k, kcap);
-            dmax = std::max(dmax, D);
-            lbins[i] = LargeBin{key_base, digit_base, bo[b], (uint32_t)bw[b], (uint32_t)D, (uint32_t)bn[b], 0};
-            key_base += bw[b];
-            digit_base += 1ull << D;
-            pp[i + 1] = pp[i] + (bn[b] + prec - 1) / prec;
-        }
-        const uint64_t n_pieces = pp.back();
-        if (bw.size() && large_windows != key_base) {
-            set_err("large-bin table inconsistent");
-            throw Fail{KMC_ERR_INTERNAL};
-        }
-        LargeBin* d_lbins = ar.get<LargeBin>(lbins.size());
-        uint64_t* d_pp = ar.get<uint64_t>(pp.size());
-        Piece* d_pieces = ar.get<Piece>(n_pieces);
-        uint32_t* digit_cnt = ar.get<uint32_t>(digit_base);
-        uint32_t* digit_cur = ar.get<uint32_t>(digit_base);
-        Chunk* chunks = ar.get<Chunk>(digit_base);
-        Chunk* oversize = ar.get<Chunk>(digit_base);
-        unsigned long long* counters = ar.get<unsigned long long>(2);
-        void* lkeys = ar.alloc(large_windows * ksz);
-        CK(cudaMemcpyAsync(d_lbins, lbins.data(), lbins.size() * sizeof(LargeBin), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
-        j->stage_begin(KMC_STAGE_LARGE_SPLIT);
-        CK(cudaMemsetAsync(digit_cnt, 0, digit_base * 4, s));
-        CK(cudaMemsetAsync(counters, 0, 16, s));
-        CK(launch_make_pieces(d_lbins, d_pp, lbins.size(), (uint32_t)prec, d_pieces, s));
-        CK(launch_large_count(bins, d_pieces, n_pieces, d_lbins, k, digit_cnt, s));
-        GreedyArgs ga{};
-        ga.cnt = digit_cnt;
-        ga.lbins = d_lbins;
-        ga.cursor = digit_cur;
-        ga.cursor_abs = 0;
-        ga.chunks = chunks;
-        ga.oversize = oversize;
-        ga.counters = counters;
-        ga.cap = (uint32_t)kcap;
-        CK(launch_greedy_chunks(ga, lbins.size(), s));
-        CK(launch_large_scatter(bins, d_pieces, n_pieces, d_lbins, k, dmax, digit_cur, lkeys, s));
-        j->launches += 4;
-        j->stage_end(4);
-        CK(cudaMemcpyAsync(&hs[48], counters, 16, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        const uint64_t n_chunks = hs[48], n_over = hs[49];
-        j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
-        CK(launch_chunk_sort(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
-        j->launches += 1;
-        j->stage_end(1);
-        if (n_over > 0) {
-            std::vector<Chunk> ov(n_over);
-            CK(cudaMemcpyAsync(ov.data(), oversize, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            uint64_t maxn = 0;
-            for (auto& c : ov) maxn = std::max<uint64_t>(maxn, c.n);
-            RadixScratch rs{};
-            rs.keys_alt = ar.alloc(maxn * ksz);
-            const uint64_t nt = (maxn + radix_tile_items(kw) - 1) / radix_tile_items(kw);
-            rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
-            rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
-            rs.scan_temp = ar.alloc(radix_scan_temp_bytes(maxn, kw));
-            rs.red = ar.get<unsigned long long>(4);
-            rs.red_host = hs + 40;
-            int sl = 0;
-            j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
-            for (auto& c : ov) {
-                void* seg = (uint8_t*)lkeys + c.begin * ksz;
-                void* sorted = nullptr;
-                uint32_t* dummy = nullptr;
-                CK(device_radix_sort(kw, seg, nullptr, c.n, 2 * k, rs, s, &sorted, &dummy, &sl));
-                CK(launch_rle(kw, sorted, c.n, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
-                sl += 1;
+        // group budget in keys: the option, else everything at once if the key buffer can be
+        // allocated, else half the free device memory
+        uint64_t budget = j->opt.large_group_mkeys ? ((uint64_t)j->opt.large_group_mkeys << 20) : ~0ull;
+        void* lkeys = nullptr;
+        if (!j->opt.large_group_mkeys) {
+            lkeys = ar.try_alloc(large_windows * ksz);
+            if (!lkeys) {
+                size_t fr = 0, tot = 0;
+                CK(cudaMemGetInfo(&fr, &tot));
+                budget = std::max<uint64_t>((uint64_t)(fr / 2) / (ksz + 1), 1u << 20);
             }
-            j->launches += sl;
-            j->stage_end(sl);
+        }
+        std::vector<std::pair<size_t, size_t>> groups;
+        uint64_t max_gw = 0, max_gd = 0, max_gp = 0, max_gn = 0;
+        for (size_t i0 = 0; i0 < large_ids.size();) {
+            uint64_t gw = 0, gd = 0, gp = 0;
+            size_t i1 = i0;
+            while (i1 < large_ids.size()) {
+                const uint64_t b = large_ids[i1];
+                if (i1 > i0 && gw + bw[b] > budget) break;
+                gw += bw[b];
+                gd += 1ull << msd_digit_bits(bw[b], k, kcap);
+                gp += (bn[b] + prec - 1) / prec;
+                ++i1;
+            }
+            groups.push_back({i0, i1});
+            max_gw = std::max(max_gw, gw);
+            max_gd = std::max(max_gd, gd);
+            max_gp = std::max(max_gp, gp);
+            max_gn = std::max<uint64_t>(max_gn, i1 - i0);
+            i0 = i1;
+        }
+        j->st.n_large_groups = groups.size();
+        LargeBin* d_lbins = ar.get<LargeBin>(max_gn);
+        uint64_t* d_pp = ar.get<uint64_t>(max_gn + 1);
+        Piece* d_pieces = ar.get<Piece>(max_gp);
+        uint32_t* digit_cnt = ar.get<uint32_t>(max_gd);
+        uint32_t* digit_cur = ar.get<uint32_t>(max_gd);
+        Chunk* chunks = ar.get<Chunk>(max_gd);
+        Chunk* oversize = ar.get<Chunk>(max_gd);
+        unsigned long long* counters = ar.get<unsigned long long>(2);
+        if (!lkeys) lkeys = ar.alloc(max_gw * ksz);
+        RadixScratch rs{};
+        uint64_t rs_cap = 0;
+        int sl = 0;
+        for (const auto& g : groups) {
+            const size_t gn = g.second - g.first;
+            std::vector<LargeBin> lbins(gn);
+            std::vector<uint64_t> pp(gn + 1, 0);
+            uint64_t key_base = 0, digit_base = 0;
+            int dmax = 1;
+            for (size_t i = 0; i < gn; ++i) {
+                const uint64_t b = large_ids[g.first + i];
+                const int D = msd_digit_bits(bw[b], k, kcap);
+                dmax = std::max(dmax, D);
+                lbins[i] = LargeBin{key_base, digit_base, bo[b], (uint32_t)bw[b], (uint32_t)D, (uint32_t)bn[b], 0};
+                key_base += bw[b];
+                digit_base += 1ull << D;
+                pp[i + 1] = pp[i] + (bn[b] + prec - 1) / prec;
+            }
+            const uint64_t n_pieces = pp.back();
+            CK(cudaMemcpyAsync(d_lbins, lbins.data(), gn * sizeof(LargeBin), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
+            j->stage_begin(KMC_STAGE_LARGE_SPLIT);
+            CK(cudaMemsetAsync(digit_cnt, 0, digit_base * 4, s));
+            CK(cudaMemsetAsync(counters, 0, 16, s));
+            CK(launch_make_pieces(d_lbins, d_pp, gn, (uint32_t)prec, d_pieces, s));
+            CK(launch_large_count(bins, d_pieces, n_pieces, d_lbins, k, digit_cnt, s));
+            GreedyArgs ga{};
+            ga.cnt = digit_cnt;
+            ga.lbins = d_lbins;
+            ga.cursor = digit_cur;
+            ga.cursor_abs = 0;
+            ga.chunks = chunks;
+            ga.oversize = oversize;
+            ga.counters = counters;
+            ga.cap = (uint32_t)kcap;
+            CK(launch_greedy_chunks(ga, gn, s));
+            CK(launch_large_scatter(bins, d_pieces, n_pieces, d_lbins, k, dmax, digit_cur, lkeys, s));
+            j->launches += 4;
+            j->stage_end(4);
+            CK(cudaMemcpyAsync(&hs[48], counters, 16, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            const uint64_t n_chunks = hs[48], n_over = hs[49];
+            j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
+            CK(launch_chunk_sort(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+            j->launches += 1;
+            j->stage_end(1);
+            if (n_over > 0) {
+                // digits above CTA capacity (identical-key pile-ups): device LSD + run pass
+                std::vector<Chunk> ov(n_over);
+                CK(cudaMemcpyAsync(ov.data(), oversize, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                uint64_t maxn = 0;
+                for (auto& c : ov) maxn = std::max<uint64_t>(maxn, c.n);
+                if (maxn > rs_cap) {
+                    ar.release(rs.keys_alt);
+                    ar.release(rs.tile_hist);
+                    ar.release(rs.tile_off);
+                    ar.release(rs.scan_temp);
+                    rs.keys_alt = ar.alloc(maxn * ksz);
+                    const uint64_t nt = (maxn + radix_tile_items(kw) - 1) / radix_tile_items(kw);
+                    rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
+                    rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+                    rs.scan_temp = ar.alloc(radix_scan_temp_bytes(maxn, kw));
+                    if (!rs.red) rs.red = ar.get<unsigned long long>(4);
+                    rs.red_host = hs + 40;
+                    rs_cap = maxn;
+                }
+                int fl = 0;
+                j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
+                for (auto& c : ov) {
+                    void* seg = (uint8_t*)lkeys + c.begin * ksz;
+                    void* sorted = nullptr;
+                    uint32_t* dummy = nullptr;
+                    CK(device_radix_sort(kw, seg, nullptr, c.n, 2 * k, rs, s, &sorted, &dummy, &fl));
+                    CK(launch_rle(kw, sorted, c.n, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+                    fl += 1;
+                }
+                sl += fl;
+                j->launches += fl;
+                j->stage_end(fl);
+            }
         }
         ar.release(lkeys);
         j->st.n_large_bins = n_large;

@@ -247,3 +247,32 @@ def test_full_config_sampled(gpu, name):
 def test_full_c4_sampled(gpu):
     st = _sampled_full(gpu, "C4", n_sample=200)
     assert st["n_windows"] > 2_500_000_000
+
+
+# ---------------------------------------------------------------- f2: streamed input, bounded groups
+
+@pytest.mark.parametrize("opts", [dict(input_batch_mb=1), dict(input_batch_mb=1, distribute_path=1),
+                                  dict(input_batch_mb=2, large_group_mkeys=1, force_large=True)])
+def test_streamed_host_input(gpu, opts):
+    """Host-resident reads streamed through pass 1 in read-aligned batches (double-buffered
+    H2D) and large bins in memory-bounded groups give the oracle's bytes exactly."""
+    w = synth.make("C4", scale=0.002)  # 8 Mbases -> several 1-2 MiB batches
+    rh = torch.from_numpy(w.reads).pin_memory()
+    oh = torch.from_numpy(w.offsets.view(np.uint64))
+    res = gpu.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", **opts)
+    ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max)
+    assert res.stats["n_input_batches"] >= 4
+    if opts.get("large_group_mkeys"):
+        assert res.stats["n_large_groups"] >= 3
+    assert np.array_equal(res.kmers.numpy(), ref.keys) and np.array_equal(res.counts.numpy(), ref.counts)
+    assert res.stats["n_windows"] == ref.n_windows
+
+
+def test_streamed_equals_resident(gpu):
+    w = synth.make("C5", scale=0.01)
+    a = gpu_count(gpu, w)
+    rh = torch.from_numpy(w.reads)  # pageable host memory also works
+    oh = torch.from_numpy(w.offsets.view(np.uint64))
+    b = gpu.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", input_batch_mb=1,
+                  large_group_mkeys=1)
+    assert np.array_equal(a[0], b.kmers.numpy()) and np.array_equal(a[1], b.counts.numpy())
