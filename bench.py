@@ -161,6 +161,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-reads", type=int, default=400_000)
+    ap.add_argument("--count-path", type=int, default=0, choices=[0, 1],
+                    help="S7-S8 of large-bin chunks: 0 = SMEM hash count (default), 1 = SMEM radix sort + RLE")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     cfg = synth.CONFIGS[args.config]
@@ -187,7 +189,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(profile=True):
-        return kmc.count(reads_d, offs_d, k, p, ci, cx, profile=profile)
+        return kmc.count(reads_d, offs_d, k, p, ci, cx, profile=profile, count_path=args.count_path)
 
     for _ in range(max(3, args.warmup)):
         res = step()
@@ -227,7 +229,7 @@ def main():
     if not args.no_e2e:
         reads_h = torch.from_numpy(w.reads).pin_memory()
         offs_h = torch.from_numpy(w.offsets.view(np.uint64)).pin_memory()
-        r = kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu")
+        r = kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path)
         n_out = r.stats["n_out"]
         del r
         e_steps = max(1, min(args.steps, 3))
@@ -239,7 +241,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e_steps):
-            r = kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu")
+            r = kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path)
             del r
         e1.record(stream)
         torch.cuda.synchronize()
@@ -310,6 +312,7 @@ def main():
         "config": {"workload": f"{args.config}: {cfg.desc}", "scale": args.scale, "n_reads": w.n_reads,
                    "n_bases": n_bases, "k": k, "p": p, "cutoff_min": ci, "cutoff_max": cx,
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "count_path": ["smem_hash", "smem_radix_sort"][args.count_path],
                    "l2": "inputs (4 GB) larger than L2 (126 MB); no flush needed"},
         "kmers_per_s": world * last["n_windows"] / (ms / 1e3),
         "stats": {x: last[x] for x in ("n_windows", "n_superkmers", "n_records", "n_bins", "n_large_bins",

@@ -79,7 +79,8 @@ enum {
     KMC_STAGE_SMALL_BINS = 4, /* S6-S8 for bins that fit one CTA: expand + SMEM radix sort + compact */
     KMC_STAGE_LARGE_SPLIT = 5,  /* S6 + MSD step of S7 for large bins: expand, count top digits,
                                    plan chunks, scatter keys to HBM digit ranges */
-    KMC_STAGE_LARGE_CHUNKS = 6, /* S7-S8 for large bins: SMEM radix sort + compaction per chunk */
+    KMC_STAGE_LARGE_CHUNKS = 6, /* S7-S8 for large bins: per chunk, SMEM hash count (count_path 0)
+                                   or SMEM radix sort + compaction (count_path 1) */
     KMC_STAGE_LARGE_FALLBACK = 7,/* S7-S8 for oversize digits (or all large bins with
                                    large_path=1): device-wide LSD radix sort + run-length pass */
     KMC_STAGE_ORDER = 8,      /* S9: global ascending order of survivors */
@@ -125,7 +126,10 @@ typedef struct {
                                   the H2D copy of batch i+1 overlaps pass 1 on batch i */
     uint32_t large_group_mkeys;/* large bins are split/sorted in groups of at most this many Mi
                                   keys (0 = auto: as many as fit in free device memory) */
-    uint32_t reserved[1];
+    uint32_t count_path;       /* S7-S8 of the large-bin chunks.  0: count every chunk in a
+                                  shared-memory hash table (default; persistent CTAs, TMA-prefetched
+                                  chunks); 1: the paper's radix sort + run-length compaction of
+                                  every chunk in shared memory.  Same output. */
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).

@@ -616,7 +616,167 @@ __global__ void __launch_bounds__(SB_NT, 2) k_chunk_sort(const K* __restrict__ k
                                 GS_SURV, GS_UNIQUE, GS_BELOW, GS_ABOVE);
 }
 
+// ---------------------------------------------------------------- S7-S8 by counting in SMEM
+// Default counting of the large-bin chunks ("count_path 0").  The paper
+// sorts a bin's k-mers and merges equal neighbours; that only
+// has to produce, per distinct k-mer, its number of occurrences, and S9 sorts the
+// survivors globally anyway.  Here a persistent CTA (one per SM) counts each chunk in an
+// open-addressing hash table in shared memory (CAS claims a slot, atomicAdd counts),
+// while the TMA engine streams the NEXT chunk's keys into the other half of a
+// double-buffered staging area.  After a chunk, the table is scanned once: every key with
+// ci <= count <= cx is a survivor; the CTA reserves its output range with one global
+// atomic, writes the survivors, and clears the slots it used.
+constexpr int CH_NT = 1024;
+template <class K> struct HashCap;
+template <> struct HashCap<uint64_t> { static constexpr int slots = 8192; };
+template <> struct HashCap<K128> { static constexpr int slots = 4096; };
+
+template <class K> constexpr size_t chunk_hash_smem() {
+    return (size_t)HashCap<K>::slots * (sizeof(K) + 4) + 2 * ((size_t)SmallCap<K>::v * sizeof(K) + 16) + 16;
+}
+
+template <class K>
+__global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ keys, const Chunk* __restrict__ chunks,
+                                                         uint32_t n_chunks, uint32_t ci, uint32_t cx, K* sk,
+                                                         uint32_t* sc, unsigned long long* gstats) {
+    constexpr int TSMAX = HashCap<K>::slots, CAP = SmallCap<K>::v, NW = CH_NT / 32, SPT = TSMAX / CH_NT;
+    constexpr int PAD = 16 / sizeof(K) > 1 ? 16 / sizeof(K) : 1;  // keys of alignment slack per buffer
+    extern __shared__ __align__(128) uint8_t smem[];
+    K* T = reinterpret_cast<K*>(smem);
+    uint32_t* C = reinterpret_cast<uint32_t*>(T + TSMAX);
+    K* S0 = reinterpret_cast<K*>(C + TSMAX);
+    K* S1 = S0 + CAP + PAD;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(S1 + CAP + PAD);
+    __shared__ uint32_t wk[NW];
+    __shared__ unsigned long long wb[NW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t ltm = lanemask_lt();
+    const K E = key_empty<K>();
+    for (int i = threadIdx.x; i < TSMAX; i += CH_NT) {
+        T[i] = E;
+        C[i] = 0;
+    }
+    // chunk -> 16-byte aligned source range; the key buffer has 16 bytes of tail slack
+    auto issue = [&](uint32_t cc, int b) {
+        const Chunk ch = chunks[cc];
+        const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
+        const uint32_t bytes = (uint32_t)(((ch.begin + ch.n - a0) * sizeof(K) + 15) & ~(uint64_t)15);
+        mbar_expect_tx(mbar + b, bytes);
+        tma_load_1d(b ? S1 : S0, keys + a0, bytes, mbar + b);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        mbar_init(mbar + 1, 1);
+        mbar_init_fence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < n_chunks) issue(blockIdx.x, 0);
+    uint32_t uniq = 0, below = 0, above = 0;
+    for (uint32_t it = 0;; ++it) {
+        const uint32_t cc = blockIdx.x + it * gridDim.x;
+        if (cc >= n_chunks) break;
+        const int b = it & 1;
+        // the other buffer was released by the previous iteration's final barrier
+        if (threadIdx.x == 0 && cc + gridDim.x < n_chunks) {
+            fence_proxy_async_smem();
+            issue(cc + gridDim.x, b ^ 1);
+        }
+        const Chunk ch = chunks[cc];
+        const int n = (int)ch.n;
+        const int off = (int)(ch.begin & (uint64_t)(PAD - 1));
+        int lg = 6;
+        while ((1 << lg) < n + n / 3) ++lg;
+        const int TS = 1 << lg;
+        mbar_wait(mbar + b, (it >> 1) & 1);
+        const K* src = (b ? S1 : S0) + off;
+        for (int i = threadIdx.x; i < n; i += CH_NT) table_insert<K>(T, C, lg, src[i]);
+        __syncthreads();
+        uint32_t cv[SPT];
+        uint32_t keep = 0;
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) {
+            const int s = j * CH_NT + threadIdx.x;
+            cv[j] = s < TS ? C[s] : 0u;
+            if (cv[j]) {
+                ++uniq;
+                if (cv[j] < ci) {
+                    ++below;
+                    cv[j] = 0;
+                } else if (cv[j] > cx) {
+                    ++above;
+                    cv[j] = 0;
+                } else {
+                    ++keep;
+                }
+            }
+        }
+        keep = __reduce_add_sync(0xffffffffu, keep);
+        if (lane == 0) wk[warp] = keep;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t kw = lane < NW ? wk[lane] : 0u;
+            const uint32_t inc = warp_incl_sum(kw);
+            unsigned long long b0 = 0;
+            if (lane == NW - 1 && inc) b0 = atomicAdd(&gstats[GS_SURV], (unsigned long long)inc);
+            b0 = __shfl_sync(0xffffffffu, b0, NW - 1);
+            if (lane < NW) wb[lane] = b0 + inc - kw;
+        }
+        __syncthreads();
+        unsigned long long o = wb[warp];
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) {
+            if (j * CH_NT >= TS) break;
+            const int s = j * CH_NT + threadIdx.x;
+            const uint32_t bb = __ballot_sync(0xffffffffu, cv[j] != 0);
+            if (cv[j]) {
+                const unsigned long long q = o + __popc(bb & ltm);
+                sk[q] = T[s];
+                sc[q] = cv[j];
+            }
+            o += __popc(bb);
+            if (s < TS) {
+                T[s] = E;
+                C[s] = 0;
+            }
+        }
+        __syncthreads();
+    }
+    uniq = __reduce_add_sync(0xffffffffu, uniq);
+    below = __reduce_add_sync(0xffffffffu, below);
+    above = __reduce_add_sync(0xffffffffu, above);
+    if (lane == 0) {
+        if (uniq) atomicAdd(&gstats[GS_UNIQUE], (unsigned long long)uniq);
+        if (below) atomicAdd(&gstats[GS_BELOW], (unsigned long long)below);
+        if (above) atomicAdd(&gstats[GS_ABOVE], (unsigned long long)above);
+    }
+}
+
 }  // namespace
+
+size_t chunk_key_slack_bytes() { return 16; }
+
+cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
+                              uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
+                              int n_sms, cudaStream_t s) {
+    if (n_chunks == 0) return cudaSuccess;
+    if (n_chunks >= (1ull << 32)) return cudaErrorInvalidValue;
+    const unsigned grid = (unsigned)std::min<uint64_t>(n_chunks, (uint64_t)std::max(1, n_sms));
+    cudaError_t e;
+    if (k <= 32) {
+        const size_t sm = chunk_hash_smem<uint64_t>();
+        if ((e = cudaFuncSetAttribute(k_chunk_hash<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
+            return e;
+        k_chunk_hash<uint64_t><<<grid, CH_NT, sm, s>>>((const uint64_t*)keys, chunks, (uint32_t)n_chunks, ci, cx,
+                                                       (uint64_t*)surv_keys, surv_counts, gstats);
+    } else {
+        const size_t sm = chunk_hash_smem<K128>();
+        if ((e = cudaFuncSetAttribute(k_chunk_hash<K128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
+            return e;
+        k_chunk_hash<K128><<<grid, CH_NT, sm, s>>>((const K128*)keys, chunks, (uint32_t)n_chunks, ci, cx,
+                                                   (K128*)surv_keys, surv_counts, gstats);
+    }
+    return cudaGetLastError();
+}
 
 int small_capacity(int k) { return k <= 32 ? SB_CAP64 : SB_CAP128; }
 

@@ -125,6 +125,13 @@ struct Arena {
     }
 };
 
+int n_sms() {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return 148;
+    return v;
+}
+
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes at;
@@ -615,7 +622,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         uint64_t budget = j->opt.large_group_mkeys ? ((uint64_t)j->opt.large_group_mkeys << 20) : ~0ull;
         void* lkeys = nullptr;
         if (!j->opt.large_group_mkeys) {
-            lkeys = ar.try_alloc(large_windows * ksz);
+            lkeys = ar.try_alloc(large_windows * ksz + chunk_key_slack_bytes());
             if (!lkeys) {
                 size_t fr = 0, tot = 0;
                 CK(cudaMemGetInfo(&fr, &tot));
@@ -651,7 +658,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         Chunk* chunks = ar.get<Chunk>(max_gd);
         Chunk* oversize = ar.get<Chunk>(max_gd);
         unsigned long long* counters = ar.get<unsigned long long>(2);
-        if (!lkeys) lkeys = ar.alloc(max_gw * ksz);
+        if (!lkeys) lkeys = ar.alloc(max_gw * ksz + chunk_key_slack_bytes());
         RadixScratch rs{};
         uint64_t rs_cap = 0;
         int sl = 0;
@@ -695,7 +702,12 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             CK(cudaStreamSynchronize(s));
             const uint64_t n_chunks = hs[48], n_over = hs[49];
             j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
-            CK(launch_chunk_sort(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+            if (j->opt.count_path == 1)
+                CK(launch_chunk_sort(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats,
+                                     s));
+            else
+                CK(launch_chunk_hash(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats,
+                                     n_sms(), s));
             j->launches += 1;
             j->stage_end(1);
             if (n_over > 0) {

@@ -150,6 +150,102 @@ __device__ __forceinline__ uint32_t rec_sym(const uint32_t* rec, int j) {
     return (rec[g >> 5] >> (30 - (g & 31))) & 3u;
 }
 
+// ---------------------------------------------------------------- TMA bulk copy + mbarrier
+// 1-D bulk copies global -> shared (cp.async.bulk, the TMA engine) completing on an
+// mbarrier with a transaction byte count.  src, dst and bytes must be multiples of 16.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(m))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_addr(m)),
+        "r"(parity)
+        : "memory");
+}
+// Orders earlier generic-proxy shared-memory accesses before later async-proxy (TMA) ones.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- shared-memory hash table
+// Slot hash of a key for a table of 2^lg slots: two multiply-xorshift rounds, independent
+// of part_digit (the chunk's keys share their part_digit).
+__device__ __forceinline__ uint32_t slot_hash(uint64_t key, int lg) {
+    uint64_t x = key * 0xFF51AFD7ED558CCDull;
+    x ^= x >> 32;
+    x *= 0x9E3779B97F4A7C15ull;
+    return (uint32_t)(x >> (64 - lg));
+}
+__device__ __forceinline__ uint32_t slot_hash(const K128& key, int lg) {
+    uint64_t x = (key.lo ^ (key.hi * 0xC2B2AE3D27D4EB4Full)) * 0xFF51AFD7ED558CCDull;
+    x ^= x >> 32;
+    x *= 0x9E3779B97F4A7C15ull;
+    return (uint32_t)(x >> (64 - lg));
+}
+// Empty-slot marker: all ones.  It is never a canonical key: the all-T k-mer's reverse
+// complement (all A = 0) is smaller.
+template <class K> __device__ __forceinline__ K key_empty();
+template <> __device__ __forceinline__ uint64_t key_empty<uint64_t>() { return ~0ull; }
+template <> __device__ __forceinline__ K128 key_empty<K128>() { return K128{~0ull, ~0ull}; }
+
+__device__ __forceinline__ uint64_t smem_load_volatile(const uint64_t* p) {
+    return *reinterpret_cast<const volatile uint64_t*>(p);
+}
+__device__ __forceinline__ K128 smem_load_volatile(const K128* p) {
+    K128 r;
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r.lo), "=l"(r.hi) : "r"(smem_addr(p)));
+    return r;
+}
+// Claims an empty slot for key; returns the slot's previous content.
+__device__ __forceinline__ uint64_t smem_cas_empty(uint64_t* p, uint64_t key) {
+    return atomicCAS(reinterpret_cast<unsigned long long*>(p), ~0ull, (unsigned long long)key);
+}
+__device__ __forceinline__ K128 smem_cas_empty(K128* p, const K128& key) {
+    K128 o;
+    const uint64_t e = ~0ull;
+    asm volatile(
+        "{\n .reg .b128 c, n, o;\n mov.b128 c, {%2, %3};\n mov.b128 n, {%4, %5};\n"
+        " atom.shared.cas.b128 o, [%6], c, n;\n mov.b128 {%0, %1}, o;\n}"
+        : "=l"(o.lo), "=l"(o.hi)
+        : "l"(e), "l"(e), "l"(key.lo), "l"(key.hi), "r"(smem_addr(p))
+        : "memory");
+    return o;
+}
+
+// Counts key in the open-addressing table (T keys, C counts, 2^lg slots, linear probing):
+// the slot holding key, or an empty slot claimed with CAS, gets +1.  The table must keep
+// at least one empty slot (callers size it to >= 4/3 of the keys inserted).
+template <class K>
+__device__ __forceinline__ void table_insert(K* T, uint32_t* C, int lg, const K& key) {
+    const uint32_t mask = (1u << lg) - 1;
+    const K E = key_empty<K>();
+    uint32_t s = slot_hash(key, lg);
+    while (true) {
+        const K cur = smem_load_volatile(&T[s]);
+        if (key_eq(cur, key)) break;
+        if (key_eq(cur, E)) {
+            const K old = smem_cas_empty(&T[s], key);
+            if (key_eq(old, E) || key_eq(old, key)) break;
+        }
+        s = (s + 1) & mask;
+    }
+    atomicAdd(&C[s], 1u);
+}
+
 // ---------------------------------------------------------------- warp / block helpers
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
@@ -457,18 +553,28 @@ __device__ __forceinline__ void block_sort_inplace(K* A, uint32_t* VA, int n, in
     }
 }
 
+// Length of the run starting at i (its start bit is set): distance to the next start bit.
+__device__ __forceinline__ uint32_t rle_run_length(const uint32_t* bits, int i) {
+    const int pos = i + 1;
+    int wd = pos >> 5;
+    uint32_t m = bits[wd] & (0xFFFFFFFFu << (pos & 31));
+    while (m == 0) m = bits[++wd];
+    return (uint32_t)(wd * 32 + __ffs(m) - 1 - i);
+}
+
 // Run-length compaction of the sorted keys S[0..n) with the cutoffs ci <= count <= cx
-// (S8).  bits: (n+32)/32+1 uint32 of scratch.  Run starts are found with warp ballots; a
-// run's length is the distance to the next start bit.  Survivors are appended, in any
-// order, at ranges reserved with one global atomic per warp and round.
+// (S8).  bits: (n+32)/32 + 4 + 4*NW/32 uint32 of scratch.  Run starts are found with warp ballots; a
+// run's length is the distance to the next start bit.  The CTA's survivors are counted
+// first and their output range is reserved with ONE global atomic per CTA (a per-warp
+// atomic on the shared survivor cursor serialises at one L2 address: it was the bottleneck
+// of the chunk kernel); then every warp writes its survivors at its scanned offset.
 template <class K, int NT>
 __device__ __forceinline__ void block_rle_bitmask(const K* S, int n, uint32_t* bits, uint32_t ci, uint32_t cx,
                                                   K* out_keys, uint32_t* out_counts, unsigned long long* gstats,
                                                   uint32_t* wsum, unsigned int* scnt, unsigned long long* bcast,
                                                   int gs_surv, int gs_unique, int gs_below, int gs_above) {
-    (void)wsum;
-    (void)bcast;
-    const int lane = threadIdx.x & 31;
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwords = (n + 32) / 32;  // covers the sentinel bit n
     for (int base = (threadIdx.x & ~31); base < nwords * 32; base += NT) {
         const int i = base + lane;
@@ -476,54 +582,67 @@ __device__ __forceinline__ void block_rle_bitmask(const K* S, int n, uint32_t* b
         const uint32_t b = __ballot_sync(0xffffffffu, st);
         if (lane == 0) bits[base >> 5] = b;
     }
-    if (threadIdx.x < 4) scnt[threadIdx.x] = 0;
     __syncthreads();
-    uint32_t uniq = 0, below = 0, above = 0;
+    // pass A: unique / below / above / kept per warp
+    uint32_t uniq = 0, below = 0, above = 0, keep = 0;
+    for (int i0 = warp * 32; i0 < n; i0 += NT) {
+        const int i = i0 + lane;
+        if (i < n && ((bits[i0 >> 5] >> lane) & 1u)) {
+            const uint32_t run = rle_run_length(bits, i);
+            ++uniq;
+            if (run < ci) ++below;
+            else if (run > cx) ++above;
+            else ++keep;
+        }
+    }
+    uniq = __reduce_add_sync(0xffffffffu, uniq);
+    below = __reduce_add_sync(0xffffffffu, below);
+    above = __reduce_add_sync(0xffffffffu, above);
+    keep = __reduce_add_sync(0xffffffffu, keep);
+    // scratch after the bitmask: NW u64 warp offsets, then NW u32 kept + NW u32 unique
+    unsigned long long* woff = reinterpret_cast<unsigned long long*>(bits + ((nwords + 2) & ~1));
+    uint32_t* wkeep = reinterpret_cast<uint32_t*>(woff + NW);
+    if (lane == 0) {
+        wkeep[warp] = keep;
+        wkeep[NW + warp] = uniq;
+    }
+    (void)wsum;
+    (void)scnt;
+    (void)bcast;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t kw = lane < NW ? wkeep[lane] : 0u;
+        const uint32_t inc = warp_incl_sum(kw);
+        const uint32_t tu = __reduce_add_sync(0xffffffffu, lane < NW ? wkeep[NW + lane] : 0u);
+        unsigned long long b0 = 0;
+        if (lane == NW - 1 && inc) b0 = atomicAdd(&gstats[gs_surv], (unsigned long long)inc);
+        b0 = __shfl_sync(0xffffffffu, b0, NW - 1);
+        if (lane < NW) woff[lane] = b0 + inc - kw;
+        if (lane == 0 && tu) atomicAdd(&gstats[gs_unique], (unsigned long long)tu);
+    }
+    if (lane == 0) {
+        if (below) atomicAdd(&gstats[gs_below], (unsigned long long)below);
+        if (above) atomicAdd(&gstats[gs_above], (unsigned long long)above);
+    }
+    __syncthreads();
+    if (keep == 0) return;
+    // pass B: write survivors at the warp's reserved offset, in position order
+    unsigned long long slot = woff[warp];
     const uint32_t ltm = lanemask_lt();
-    for (int i0 = (threadIdx.x & ~31); i0 < n; i0 += NT) {
+    for (int i0 = warp * 32; i0 < n; i0 += NT) {
         const int i = i0 + lane;
         uint32_t run = 0;
-        const uint32_t w0 = bits[i0 >> 5];
-        if (i < n && ((w0 >> lane) & 1u)) {
-            int pos = i + 1, wd = pos >> 5;
-            uint32_t m = bits[wd] & (0xFFFFFFFFu << (pos & 31));
-            while (m == 0) m = bits[++wd];
-            run = (uint32_t)(wd * 32 + __ffs(m) - 1 - i);
-            ++uniq;
-            if (run < ci) {
-                ++below;
-                run = 0;
-            } else if (run > cx) {
-                ++above;
-                run = 0;
-            }
+        if (i < n && ((bits[i0 >> 5] >> lane) & 1u)) {
+            run = rle_run_length(bits, i);
+            if (run < ci || run > cx) run = 0;
         }
         const uint32_t b = __ballot_sync(0xffffffffu, run != 0);
-        if (b) {
-            unsigned long long slot = 0;
-            if (lane == 0) slot = atomicAdd(&gstats[gs_surv], (unsigned long long)__popc(b));
-            slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(b & ltm);
-            if (run) {
-                out_keys[slot] = S[i];
-                out_counts[slot] = run;
-            }
+        if (run) {
+            const unsigned long long o = slot + __popc(b & ltm);
+            out_keys[o] = S[i];
+            out_counts[o] = run;
         }
-    }
-    {
-        const uint32_t a = __reduce_add_sync(0xffffffffu, uniq);
-        const uint32_t b = __reduce_add_sync(0xffffffffu, below);
-        const uint32_t c = __reduce_add_sync(0xffffffffu, above);
-        if (lane == 0) {
-            if (a) atomicAdd(&scnt[1], a);
-            if (b) atomicAdd(&scnt[2], b);
-            if (c) atomicAdd(&scnt[3], c);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (scnt[1]) atomicAdd(&gstats[gs_unique], (unsigned long long)scnt[1]);
-        if (scnt[2]) atomicAdd(&gstats[gs_below], (unsigned long long)scnt[2]);
-        if (scnt[3]) atomicAdd(&gstats[gs_above], (unsigned long long)scnt[3]);
+        slot += __popc(b);
     }
 }
 

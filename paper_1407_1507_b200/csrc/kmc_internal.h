@@ -160,6 +160,12 @@ cudaError_t launch_large_scatter(const uint32_t* bins, const Piece* pieces, uint
 cudaError_t launch_chunk_sort(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
                               uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
                               cudaStream_t s);
+// S7-S8 of the chunks by SMEM hash counting (persistent, one CTA per SM, TMA-prefetched).
+// The key buffer must have chunk_key_slack_bytes() of readable slack past its last key.
+size_t chunk_key_slack_bytes();
+cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
+                              uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
+                              int n_sms, cudaStream_t s);
 cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, void* keys,
                                 unsigned long long* gstats, cudaStream_t s);
 

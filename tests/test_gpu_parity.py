@@ -101,7 +101,8 @@ def test_count_parity_configs(gpu, name, scale):
 
 @pytest.mark.parametrize("opts", [dict(force_large=True), dict(small_bin_capacity=64), dict(small_bin_capacity=1024),
                                   dict(large_path=1), dict(force_large=True, large_path=1),
-                                  dict(distribute_path=1)])
+                                  dict(distribute_path=1), dict(count_path=1),
+                                  dict(force_large=True, count_path=1)])
 def test_forced_paths(gpu, opts):
     w = synth.make("C5", scale=0.005)
     st = assert_same(gpu, w, **opts)
@@ -131,20 +132,30 @@ def test_revcomp_and_permutation_invariance(gpu):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+@pytest.mark.parametrize("force_large", [False, True])
 @pytest.mark.parametrize("k", [1, 2, 3, 15, 16, 17, 31, 32, 33, 47, 63, 64])
-def test_k_boundaries(gpu, k):
+def test_k_boundaries(gpu, k, force_large):
     p = min(k, 5)
     seqs = synth.random_reads(k, 600, 0, 200, n_frac=0.01, lower_frac=0.01, alphabet=b"ACGT")
-    assert_same(gpu, synth.from_strings(seqs, k, p, 1))
+    assert_same(gpu, synth.from_strings(seqs, k, p, 1), force_large=force_large)
 
 
-@pytest.mark.parametrize("large_path", [0, 1])
-def test_low_complexity_and_skew(gpu, large_path):
+@pytest.mark.parametrize("count_path", [0, 1])
+@pytest.mark.parametrize("name,scale", [("C3", 0.005), ("C2", 0.005), ("C1", 0.2)])
+def test_chunk_count_paths(gpu, name, scale, count_path):
+    # every bin through the large path: hashed split, then per-chunk SMEM hash count
+    # (count_path 0) or SMEM radix sort + run-length compaction (count_path 1)
+    st = assert_same(gpu, synth.make(name, scale=scale), force_large=True, count_path=count_path)
+    assert st["large_windows"] == st["n_windows"]
+
+
+@pytest.mark.parametrize("large_path,count_path", [(0, 0), (0, 1), (1, 0)])
+def test_low_complexity_and_skew(gpu, large_path, count_path):
     # poly-A / (AT)n pile-ups: one k-mer with ~25K copies -> an "oversize" MSD digit
     seqs = ["A" * 300, "T" * 250, "AT" * 120, "ACGT" * 60, "N" * 50, "", "ACG", "CA" * 100] * 50
     seqs += [s.decode() for s in synth.random_reads(9, 200, 50, 250)]
     for k, p in ((31, 9), (28, 7), (55, 11), (21, 3)):
-        assert_same(gpu, synth.from_strings(seqs, k, p, 2), large_path=large_path)
+        assert_same(gpu, synth.from_strings(seqs, k, p, 2), large_path=large_path, count_path=count_path)
 
 
 def test_edge_cases(gpu):
