@@ -107,6 +107,9 @@ typedef struct {
     uint64_t n_launches;       /* kernels this library launched for the call */
     uint64_t n_input_batches;  /* pass-1 batches of host-resident reads (0: reads were on the device) */
     uint64_t n_large_groups;   /* memory-bounded groups the large bins were processed in */
+    uint64_t chunk_capacity;   /* max keys per large-bin chunk (set from the measured distinct ratio) */
+    uint64_t n_overflow_chunks;/* chunks whose distinct keys overflowed the SMEM hash table
+                                  (counted by the device radix-sort fallback instead) */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;
@@ -130,6 +133,8 @@ typedef struct {
                                   shared-memory hash table (default; persistent CTAs, TMA-prefetched
                                   chunks); 1: the paper's radix sort + run-length compaction of
                                   every chunk in shared memory.  Same output. */
+    uint32_t chunk_capacity;   /* 0 = auto; else max keys per large-bin chunk (testing: large
+                                  values force hash-table overflows onto the fallback) */
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).

@@ -34,7 +34,8 @@ class _Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "n_reads", "n_bases", "n_invalid_bases", "n_windows", "n_superkmers", "n_records",
         "n_signatures_used", "n_bins", "n_large_bins", "max_bin_windows", "large_windows", "n_unique",
-        "n_below_min", "n_above_max", "n_out", "n_launches", "n_input_batches", "n_large_groups")] + [
+        "n_below_min", "n_above_max", "n_out", "n_launches", "n_input_batches", "n_large_groups",
+        "chunk_capacity", "n_overflow_chunks")] + [
         ("stage_ms", ctypes.c_float * len(STAGES)), ("stage_launches", ctypes.c_uint32 * len(STAGES))]
 
     def to_dict(self) -> dict:
@@ -48,7 +49,8 @@ class _Options(ctypes.Structure):
     _fields_ = [("profile", ctypes.c_uint32), ("small_bin_capacity", ctypes.c_uint32),
                 ("force_large", ctypes.c_uint32), ("large_path", ctypes.c_uint32),
                 ("distribute_path", ctypes.c_uint32), ("input_batch_mb", ctypes.c_uint32),
-                ("large_group_mkeys", ctypes.c_uint32), ("count_path", ctypes.c_uint32)]
+                ("large_group_mkeys", ctypes.c_uint32), ("count_path", ctypes.c_uint32),
+                ("chunk_capacity", ctypes.c_uint32)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
@@ -144,9 +146,10 @@ class Result:
 
 
 def _options(profile, small_bin_capacity, force_large, large_path=0, distribute_path=0, input_batch_mb=0,
-             large_group_mkeys=0, count_path=0):
+             large_group_mkeys=0, count_path=0, chunk_capacity=0):
     o = _Options()
     o.count_path = int(count_path)
+    o.chunk_capacity = int(chunk_capacity)
     o.distribute_path = int(distribute_path)
     o.input_batch_mb = int(input_batch_mb)
     o.large_group_mkeys = int(large_group_mkeys)
@@ -160,7 +163,7 @@ def _options(profile, small_bin_capacity, force_large, large_path=0, distribute_
 def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *, stream=None,
           profile: bool = False, small_bin_capacity: int = 0, force_large: bool = False,
           large_path: int = 0, distribute_path: int = 0, input_batch_mb: int = 0, large_group_mkeys: int = 0,
-          count_path: int = 0, out_device: str | None = None) -> Result:
+          count_path: int = 0, chunk_capacity: int = 0, out_device: str | None = None) -> Result:
     """Count canonical k-mers (KMC 2 hot path on the GPU).
 
     reads: uint8 tensor (cuda, or pinned/pageable cpu -- copied inside the call), n_bases bytes.
@@ -175,7 +178,7 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
     if n_reads < 0:
         raise ValueError("offsets must have n_reads + 1 entries")
     opt = _options(profile, small_bin_capacity, force_large, large_path, distribute_path, input_batch_mb,
-                   large_group_mkeys, count_path)
+                   large_group_mkeys, count_path, chunk_capacity)
     job = ctypes.c_void_p()
     n_out = ctypes.c_uint64()
     sh = _stream_handle(stream)

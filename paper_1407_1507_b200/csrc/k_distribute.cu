@@ -364,29 +364,52 @@ __global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
 }
 
 // S5 from the temporary stream: every record is copied into its bin (signature -> bin
-// map of the plan); one atomic per (warp, bin) reserves the slots.
-__global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ tmp_recs,
-                                                     const uint32_t* __restrict__ tmp_sig, uint64_t n, int RW,
-                                                     const uint32_t* __restrict__ sig2bin,
-                                                     const uint64_t* __restrict__ bin_rec_off,
-                                                     uint32_t* __restrict__ bin_fill, uint32_t* __restrict__ bins) {
+// map of the plan); one atomic per (warp, bin) reserves the slots.  Each thread carries
+// BS_U records through the dependent steps (signature -> bin -> slot -> copy) together,
+// so BS_U independent memory round trips are in flight per step instead of one.
+constexpr int BS_NT = 256, BS_U = 4;
+__global__ void __launch_bounds__(BS_NT) k_bin_scatter(const uint32_t* __restrict__ tmp_recs,
+                                                       const uint32_t* __restrict__ tmp_sig, uint64_t n, int RW,
+                                                       const uint32_t* __restrict__ sig2bin,
+                                                       const uint64_t* __restrict__ bin_rec_off,
+                                                       uint32_t* __restrict__ bin_fill, uint32_t* __restrict__ bins) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t ltm = lanemask_lt();
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = base + threadIdx.x;
-        const bool ok = i < n;
-        const uint32_t bin = ok ? sig2bin[tmp_sig[i]] : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-        const uint32_t leader = __ffs(peers) - 1;
-        uint32_t b = 0;
-        if (ok && lane == leader) b = atomicAdd(&bin_fill[bin], (uint32_t)__popc(peers));
-        b = __shfl_sync(0xffffffffu, b, leader);
-        if (ok) {
-            const uint64_t slot = bin_rec_off[bin] + b + __popc(peers & ltm);
-            const uint4* src = reinterpret_cast<const uint4*>(tmp_recs + i * (uint64_t)RW);
-            uint4* dst = reinterpret_cast<uint4*>(bins + slot * (uint64_t)RW);
-            dst[0] = src[0];
-            if (RW == 8) dst[1] = src[1];
+    constexpr uint64_t STEP = (uint64_t)BS_NT * BS_U;
+    for (uint64_t base = (uint64_t)blockIdx.x * STEP; base < n; base += (uint64_t)gridDim.x * STEP) {
+        uint32_t bin[BS_U];
+        uint64_t slot[BS_U];
+        uint4 r0[BS_U], r1[BS_U];
+#pragma unroll
+        for (int u = 0; u < BS_U; ++u) {
+            const uint64_t i = base + (uint64_t)u * BS_NT + threadIdx.x;
+            bin[u] = i < n ? __ldcs(tmp_sig + i) : 0xFFFFFFFFu;
+            if (i < n) {
+                const uint4* src = reinterpret_cast<const uint4*>(tmp_recs + i * (uint64_t)RW);
+                r0[u] = __ldcs(src);
+                if (RW == 8) r1[u] = __ldcs(src + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < BS_U; ++u)
+            if (bin[u] != 0xFFFFFFFFu) bin[u] = sig2bin[bin[u]];
+#pragma unroll
+        for (int u = 0; u < BS_U; ++u) {
+            const uint32_t peers = __match_any_sync(0xffffffffu, bin[u]);
+            const uint32_t leader = __ffs(peers) - 1;
+            uint32_t b = 0;
+            if (bin[u] != 0xFFFFFFFFu && lane == leader) b = atomicAdd(&bin_fill[bin[u]], (uint32_t)__popc(peers));
+            slot[u] = (uint64_t)__shfl_sync(0xffffffffu, b, leader) + __popc(peers & ltm);
+        }
+#pragma unroll
+        for (int u = 0; u < BS_U; ++u)
+            if (bin[u] != 0xFFFFFFFFu) slot[u] += bin_rec_off[bin[u]];
+#pragma unroll
+        for (int u = 0; u < BS_U; ++u) {
+            if (bin[u] == 0xFFFFFFFFu) continue;
+            uint4* dst = reinterpret_cast<uint4*>(bins + slot[u] * (uint64_t)RW);
+            dst[0] = r0[u];
+            if (RW == 8) dst[1] = r1[u];
         }
     }
 }
@@ -430,8 +453,8 @@ cudaError_t launch_bin_scatter(const uint32_t* tmp_recs, const uint32_t* tmp_sig
                                const uint32_t* sig2bin, const uint64_t* bin_rec_off, uint32_t* bin_fill,
                                uint32_t* bins, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-    k_bin_scatter<<<grid, 256, 0, s>>>(tmp_recs, tmp_sig, n, record_words(k), sig2bin, bin_rec_off, bin_fill, bins);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + BS_NT * BS_U - 1) / (BS_NT * BS_U), 148ull * 8);
+    k_bin_scatter<<<grid, BS_NT, 0, s>>>(tmp_recs, tmp_sig, n, record_words(k), sig2bin, bin_rec_off, bin_fill, bins);
     return cudaGetLastError();
 }
 

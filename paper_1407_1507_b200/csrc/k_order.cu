@@ -55,29 +55,40 @@ __global__ void __launch_bounds__(OR_NT) k_order_count(const K* __restrict__ key
     }
 }
 
+constexpr int OS_U = 4;  // pairs per thread per step, carried together through the dependent steps
 template <class K>
 __global__ void __launch_bounds__(OR_NT) k_order_scatter(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
                                                          uint64_t n, int twok, int D, uint32_t* __restrict__ cursor,
                                                          K* __restrict__ okeys, uint32_t* __restrict__ ovals) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t ltm = lanemask_lt();
-    for (uint64_t base = (uint64_t)blockIdx.x * OR_NT; base < n; base += (uint64_t)gridDim.x * OR_NT) {
-        const uint64_t i = base + threadIdx.x;
-        K key{};
-        uint32_t d = 0xFFFFFFFFu;
-        if (i < n) {
-            key = keys[i];
-            d = hi_digit(key, twok, D);
+    constexpr uint64_t STEP = (uint64_t)OR_NT * OS_U;
+    for (uint64_t base = (uint64_t)blockIdx.x * STEP; base < n; base += (uint64_t)gridDim.x * STEP) {
+        K key[OS_U];
+        uint32_t val[OS_U], d[OS_U], slot[OS_U];
+#pragma unroll
+        for (int u = 0; u < OS_U; ++u) {
+            const uint64_t i = base + (uint64_t)u * OR_NT + threadIdx.x;
+            d[u] = 0xFFFFFFFFu;
+            if (i < n) {
+                key[u] = ld_stream(keys + i);
+                val[u] = __ldcs(vals + i);
+                d[u] = hi_digit(key[u], twok, D);
+            }
         }
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t leader = __ffs(peers) - 1;
-        uint32_t b = 0;
-        if (d != 0xFFFFFFFFu && lane == leader) b = atomicAdd(&cursor[d], (uint32_t)__popc(peers));
-        b = __shfl_sync(0xffffffffu, b, leader);
-        if (d != 0xFFFFFFFFu) {
-            const uint32_t slot = b + __popc(peers & ltm);
-            okeys[slot] = key;
-            ovals[slot] = vals[i];
+#pragma unroll
+        for (int u = 0; u < OS_U; ++u) {
+            const uint32_t peers = __match_any_sync(0xffffffffu, d[u]);
+            const uint32_t leader = __ffs(peers) - 1;
+            uint32_t b = 0;
+            if (d[u] != 0xFFFFFFFFu && lane == leader) b = atomicAdd(&cursor[d[u]], (uint32_t)__popc(peers));
+            slot[u] = __shfl_sync(0xffffffffu, b, leader) + __popc(peers & ltm);
+        }
+#pragma unroll
+        for (int u = 0; u < OS_U; ++u) {
+            if (d[u] == 0xFFFFFFFFu) continue;
+            okeys[slot[u]] = key[u];
+            ovals[slot[u]] = val[u];
         }
     }
 }
@@ -135,7 +146,8 @@ cudaError_t order_t(const K* keys, const uint32_t* vals, uint64_t n, int k, K* o
     ga.counters = os.counters;
     ga.cap = OrderCap<K>::v;
     if ((e = launch_greedy_chunks(ga, greedy_segments(nd), s))) return e;
-    k_order_scatter<K><<<grid, OR_NT, 0, s>>>(keys, vals, n, twok, D, os.cursor, (K*)os.tmp_keys, os.tmp_vals);
+    const unsigned sgrid = (unsigned)std::min<uint64_t>((n + OR_NT * OS_U - 1) / (OR_NT * OS_U), 148ull * 8);
+    k_order_scatter<K><<<sgrid, OR_NT, 0, s>>>(keys, vals, n, twok, D, os.cursor, (K*)os.tmp_keys, os.tmp_vals);
     if ((e = cudaGetLastError())) return e;
     if ((e = cudaMemcpyAsync(os.host, os.counters, 16, cudaMemcpyDeviceToHost, s))) return e;
     if ((e = cudaStreamSynchronize(s))) return e;

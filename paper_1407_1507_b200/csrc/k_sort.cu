@@ -400,37 +400,8 @@ constexpr int MSD_NT = 256;
 constexpr int MSD_MAXD = 12;
 
 template <class K> struct MsdPiece;
-template <> struct MsdPiece<uint64_t> { static constexpr int REC = 128, MAXW = 60; };
-template <> struct MsdPiece<K128> { static constexpr int REC = 64, MAXW = 92; };
-
-template <class K>
-__global__ void __launch_bounds__(MSD_NT) k_large_count(const uint32_t* __restrict__ bins,
-                                                        const Piece* __restrict__ pieces,
-                                                        const LargeBin* __restrict__ lbins, int k,
-                                                        uint32_t* __restrict__ digit_cnt) {
-    constexpr int REC = MsdPiece<K>::REC;
-    __shared__ __align__(16) uint32_t R[REC * 8];
-    __shared__ uint32_t h[1 << MSD_MAXD];
-    const Piece pc = pieces[blockIdx.x];
-    const LargeBin lb = lbins[pc.lbin];
-    const int RW = record_words(k), D = (int)lb.D, nd = 1 << D;
-    for (int d = threadIdx.x; d < nd; d += MSD_NT) h[d] = 0;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(bins + pc.rec_begin * RW);
-        uint4* dst = reinterpret_cast<uint4*>(R);
-        const int nv = (int)pc.nrec * RW / 4;
-        for (int v = threadIdx.x; v < nv; v += MSD_NT) dst[v] = src[v];
-    }
-    __syncthreads();
-    for (int r = threadIdx.x; r < (int)pc.nrec; r += MSD_NT) {
-        uint32_t wd[RecWords<K>::v];
-        load_record<RecWords<K>::v>(R + r * RW, wd);
-        for_each_window<K, RecWords<K>::v>(wd, k, [&](int, const K& key) { atomicAdd(&h[part_digit(key, D)], 1u); });
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < nd; d += MSD_NT)
-        if (h[d]) atomicAdd(&digit_cnt[lb.digit_base + d], h[d]);
-}
+template <> struct MsdPiece<uint64_t> { static constexpr int REC = 512, MAXW = 60; };
+template <> struct MsdPiece<K128> { static constexpr int REC = 512, MAXW = 92; };
 
 // Greedy chunk planner.  One CTA per segment of consecutive digits (a large bin's 2^D
 // digits, or a 4096-digit window of S9's global digits): exclusive scan of the digit
@@ -523,63 +494,111 @@ __global__ void __launch_bounds__(GP_NT) k_greedy_chunks(GreedyArgs g) {
     }
 }
 
-template <class K> size_t scatter_smem(int k, int dmax) {
-    return (size_t)MsdPiece<K>::REC * record_max_windows(k) * sizeof(K) + MsdPiece<K>::REC * 8 * 4 +
-           ((size_t)1 << dmax) * 4 + 64;
+// Split of the large bins, upsweep/downsweep style over CTA "ranges".  The
+// pieces of all large bins (in bin order) are cut into R contiguous ranges, one per CTA;
+// the pair (range, bin) is a "segment".  The count kernel histograms the split digit of
+// every window of a segment in shared memory and stores it, without atomics, at
+// table[lb.tb + d * lb.nseg + j] (j = segment index within the bin).  An exclusive scan of
+// the table (bin-major, then digit, then segment) gives every segment the position of its
+// first key of digit d in the digit-contiguous layout of the bin's keys; the scatter
+// kernel re-expands its pieces and places every key at a shared-memory cursor seeded from
+// the scanned table -- no global atomics, and each CTA writes every digit as one run.
+// Pieces stream through a double-buffered TMA staging area (one 1-D bulk copy each).
+constexpr int SP_NT = 512;  // split CTA: one record of a piece per thread
+// digit counters, padded to 128 bytes (the TMA staging buffers that follow need 16-byte alignment)
+__host__ __device__ constexpr int split_hwords(int dmax) { return ((1 << dmax) + 31) & ~31; }
+template <class K> size_t split_smem(int k, int dmax) {
+    return (size_t)split_hwords(dmax) * 4 + 2 * (size_t)(MsdPiece<K>::REC * RecWords<K>::v + 8) * 4 +
+           (size_t)(SP_NT / 32) * ((32 * record_max_windows(k) + 15) & ~15) + 16;
 }
 
-template <class K>
-__global__ void __launch_bounds__(MSD_NT) k_large_scatter(const uint32_t* __restrict__ bins,
-                                                          const Piece* __restrict__ pieces,
-                                                          const LargeBin* __restrict__ lbins, int k, int dmax,
-                                                          uint32_t* __restrict__ digit_cur, K* __restrict__ out) {
-    constexpr int REC = MsdPiece<K>::REC;
-    constexpr int RWK = RecWords<K>::v;
-    extern __shared__ __align__(16) uint8_t smem[];
-    K* keys = reinterpret_cast<K*>(smem);
-    uint32_t* R = reinterpret_cast<uint32_t*>(keys + REC * record_max_windows(k));
-    uint32_t* h = R + REC * 8;
-    uint32_t* wsum = h + (1 << dmax);
-    const Piece pc = pieces[blockIdx.x];
-    const LargeBin lb = lbins[pc.lbin];
-    const int RW = record_words(k), D = (int)lb.D, nd = 1 << D;
-    for (int d = threadIdx.x; d < nd; d += MSD_NT) h[d] = 0;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(bins + pc.rec_begin * RW);
-        uint4* dst = reinterpret_cast<uint4*>(R);
-        const int nv = (int)pc.nrec * RW / 4;
-        for (int v = threadIdx.x; v < nv; v += MSD_NT) dst[v] = src[v];
+template <class K, bool SCATTER>
+__global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bins, const Piece* __restrict__ pieces,
+                                                 uint64_t n_pieces, const LargeBin* __restrict__ lbins, int k,
+                                                 int dmax, uint32_t* __restrict__ table, K* __restrict__ out) {
+    constexpr int REC = MsdPiece<K>::REC, RW = RecWords<K>::v;
+    constexpr int RBUF = REC * RW + 8;  // words per staging buffer (+ readable slack for funnel reads)
+    static_assert(REC == SP_NT, "one record per thread");
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int OWN = (32 * record_max_windows(k) + 15) & ~15;  // bytes of window->lane map per warp
+    uint32_t* h = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* RB = h + split_hwords(dmax);
+    uint8_t* own = reinterpret_cast<uint8_t*>(RB + 2 * RBUF) + warp * OWN;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(RB + 2 * RBUF) + (SP_NT / 32) * OWN);
+    const uint32_t R = gridDim.x, r = blockIdx.x;
+    const uint64_t p0 = (uint64_t)r * n_pieces / R, p1 = (uint64_t)(r + 1) * n_pieces / R;
+    if (p0 >= p1) return;
+    auto issue = [&](uint64_t p, int b) {
+        const Piece pc = pieces[p];
+        const uint32_t bytes = pc.nrec * RW * 4;
+        mbar_expect_tx(mbar + b, bytes);
+        tma_load_1d_hint(RB + b * RBUF, bins + pc.rec_begin * RW, bytes, mbar + b, l2_policy_evict_first());
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        mbar_init(mbar + 1, 1);
+        mbar_init_fence();
     }
     __syncthreads();
-    // expand (one record per thread; REC <= MSD_NT) and count digits
-    const int r = threadIdx.x;
-    uint32_t wd[RWK];
-    uint32_t nw = 0;
-    if (r < (int)pc.nrec) {
-        load_record<RWK>(R + r * RW, wd);
-        nw = wd[0] >> 24;
+    if (threadIdx.x == 0) issue(p0, 0);
+    uint32_t cur = 0xFFFFFFFFu;
+    LargeBin lb{};
+    uint64_t tab = 0;  // table index of digit 0 of the current segment
+    for (uint64_t p = p0; p < p1; ++p) {
+        const uint32_t it = (uint32_t)(p - p0);
+        const int b = it & 1;
+        if (threadIdx.x == 0 && p + 1 < p1) {
+            fence_proxy_async_smem();  // buffer b^1 was released by the previous iteration's barrier
+            issue(p + 1, b ^ 1);
+        }
+        const Piece pc = pieces[p];
+        if (pc.lbin != cur) {
+            if (!SCATTER && cur != 0xFFFFFFFFu) {
+                for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT) table[tab + (uint64_t)d * lb.nseg] = h[d];
+                __syncthreads();
+            }
+            cur = pc.lbin;
+            lb = lbins[cur];
+            tab = lb.tb + (r - lb.first_range);
+            for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT)
+                h[d] = SCATTER ? table[tab + (uint64_t)d * lb.nseg] : 0u;
+            __syncthreads();
+        }
+        mbar_wait(mbar + b, (it >> 1) & 1);
+        // warp w expands records [32w, 32w+32) of the piece, one lane per window (S6):
+        // warp scan of the records' window counts, then a window -> lane map in SMEM
+        const uint32_t* Rp = RB + b * RBUF;
+        const int rec = threadIdx.x;
+        const uint32_t n = rec < (int)pc.nrec ? rec_nwin(Rp + rec * RW) : 0u;
+        const uint32_t inc = warp_incl_sum(n);
+        const uint32_t pre = inc - n;
+        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+        for (uint32_t j = 0; j < n; ++j) own[pre + j] = (uint8_t)lane;
+        __syncwarp();
+        const int D = (int)lb.D;
+        for (uint32_t w0 = 0; w0 < tot; w0 += 32) {
+            const uint32_t w = w0 + lane;
+            const int l = w < tot ? own[w] : 0;
+            const uint32_t pl = __shfl_sync(0xffffffffu, pre, l);
+            if (w < tot) {
+                const K key = window_key<K>(Rp + (warp * 32 + l) * RW, (int)(w - pl), k);
+                const uint32_t slot = atomicAdd(&h[part_digit(key, D)], 1u);
+                if (SCATTER) out[slot] = key;
+            }
+        }
+        __syncthreads();
     }
-    uint32_t total;
-    const uint32_t pos = block_excl_sum<MSD_NT, uint32_t>(nw, wsum, &total);
-    if (nw) {
-        for_each_window<K, RWK>(wd, k, [&](int w, const K& key) {
-            keys[pos + w] = key;
-            atomicAdd(&h[part_digit(key, D)], 1u);
-        });
-    }
-    __syncthreads();
-    // reserve one range per non-empty digit (bin-relative cursors), then place keys
-    for (int d = threadIdx.x; d < nd; d += MSD_NT) {
-        const uint32_t c = h[d];
-        if (c) h[d] = atomicAdd(&digit_cur[lb.digit_base + d], c);
-    }
-    __syncthreads();
-    K* dst = out + lb.key_base;
-    for (uint32_t i = threadIdx.x; i < total; i += MSD_NT) {
-        const K key = keys[i];
-        const uint32_t slot = atomicAdd(&h[part_digit(key, D)], 1u);
-        dst[slot] = key;
-    }
+    if (!SCATTER)
+        for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT) table[tab + (uint64_t)d * lb.nseg] = h[d];
+}
+
+// Per-digit key counts of the large bins from the scanned segment table.
+__global__ void k_digit_totals(const LargeBin* __restrict__ lbins, const uint32_t* __restrict__ pos,
+                               uint32_t* __restrict__ cnt) {
+    const LargeBin lb = lbins[blockIdx.x];
+    for (int d = threadIdx.x; d < (1 << lb.D); d += blockDim.x)
+        cnt[lb.digit_base + d] = pos[lb.tb + (uint64_t)(d + 1) * lb.nseg] - pos[lb.tb + (uint64_t)d * lb.nseg];
 }
 
 __global__ void k_make_pieces(const LargeBin* __restrict__ lbins, const uint64_t* __restrict__ piece_prefix,
@@ -621,34 +640,69 @@ __global__ void __launch_bounds__(SB_NT, 2) k_chunk_sort(const K* __restrict__ k
 // sorts a bin's k-mers and merges equal neighbours; that only
 // has to produce, per distinct k-mer, its number of occurrences, and S9 sorts the
 // survivors globally anyway.  Here a persistent CTA (one per SM) counts each chunk in an
-// open-addressing hash table in shared memory (CAS claims a slot, atomicAdd counts),
-// while the TMA engine streams the NEXT chunk's keys into the other half of a
-// double-buffered staging area.  After a chunk, the table is scanned once: every key with
+// open-addressing hash table in shared memory (CAS claims a slot, atomicAdd counts).  The
+// chunk's keys stream through a ring of NBUF staging buffers filled by the TMA engine
+// (1-D bulk copies, evict-first), NBUF-1 sub-pieces ahead of the consumer, across chunk
+// boundaries.  After a chunk, the table is scanned once: every key with
 // ci <= count <= cx is a survivor; the CTA reserves its output range with one global
-// atomic, writes the survivors, and clears the slots it used.
+// atomic, writes the survivors, and clears the slots.  A chunk holds up to
+// chunk_hash_cap() keys but the table only ~3/4 of its slots in distinct keys: a probe
+// sequence longer than PROBE_MAX marks the chunk "overflowed" -- its partial counts are
+// dropped and the chunk is listed for the device radix-sort fallback.
 constexpr int CH_NT = 1024;
-template <class K> struct HashCap;
-template <> struct HashCap<uint64_t> { static constexpr int slots = 8192; };
-template <> struct HashCap<K128> { static constexpr int slots = 4096; };
+constexpr int PROBE_MAX = 256;
+template <class K> struct HashCfg;
+template <> struct HashCfg<uint64_t> { static constexpr int slots = 16384, sub = 1024, nbuf = 4; };
+template <> struct HashCfg<K128> { static constexpr int slots = 8192, sub = 512, nbuf = 4; };
 
 template <class K> constexpr size_t chunk_hash_smem() {
-    return (size_t)HashCap<K>::slots * (sizeof(K) + 4) + 2 * ((size_t)SmallCap<K>::v * sizeof(K) + 16) + 16;
+    return (size_t)HashCfg<K>::slots * (sizeof(K) + 4) +
+           (size_t)HashCfg<K>::nbuf * ((size_t)HashCfg<K>::sub * sizeof(K) + 16) + 64;
+}
+
+// Counts key; false if no slot was found within PROBE_MAX probes (table too full).
+template <class K>
+__device__ __forceinline__ bool table_insert_bounded(K* T, uint32_t* C, int lg, const K& key) {
+    const uint32_t mask = (1u << lg) - 1;
+    const K E = key_empty<K>();
+    uint32_t s = slot_hash(key, lg);
+    for (int pr = 0; pr < PROBE_MAX; ++pr) {
+        const K cur = smem_load_volatile(&T[s]);
+        if (!key_eq(cur, key)) {
+            if (!key_eq(cur, E)) {
+                s = (s + 1) & mask;
+                continue;
+            }
+            const K old = smem_cas_empty(&T[s], key);
+            if (!key_eq(old, E) && !key_eq(old, key)) {
+                s = (s + 1) & mask;
+                continue;
+            }
+        }
+        atomicAdd(&C[s], 1u);
+        return true;
+    }
+    return false;
 }
 
 template <class K>
 __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ keys, const Chunk* __restrict__ chunks,
                                                          uint32_t n_chunks, uint32_t ci, uint32_t cx, K* sk,
-                                                         uint32_t* sc, unsigned long long* gstats) {
-    constexpr int TSMAX = HashCap<K>::slots, CAP = SmallCap<K>::v, NW = CH_NT / 32, SPT = TSMAX / CH_NT;
-    constexpr int PAD = 16 / sizeof(K) > 1 ? 16 / sizeof(K) : 1;  // keys of alignment slack per buffer
+                                                         uint32_t* sc, unsigned long long* gstats,
+                                                         Chunk* __restrict__ overflow,
+                                                         unsigned long long* __restrict__ n_overflow) {
+    constexpr int TSMAX = HashCfg<K>::slots, SUB = HashCfg<K>::sub, NBUF = HashCfg<K>::nbuf;
+    constexpr int NW = CH_NT / 32, SPT = TSMAX / CH_NT;
+    constexpr int PAD = 16 / sizeof(K) > 1 ? 16 / sizeof(K) : 1;  // keys per 16 bytes
+    constexpr int BUFK = SUB + PAD;                                 // keys per staging buffer
     extern __shared__ __align__(128) uint8_t smem[];
     K* T = reinterpret_cast<K*>(smem);
     uint32_t* C = reinterpret_cast<uint32_t*>(T + TSMAX);
-    K* S0 = reinterpret_cast<K*>(C + TSMAX);
-    K* S1 = S0 + CAP + PAD;
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(S1 + CAP + PAD);
+    K* SB = reinterpret_cast<K*>(C + TSMAX);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(SB + NBUF * BUFK);
     __shared__ uint32_t wk[NW];
     __shared__ unsigned long long wb[NW];
+    __shared__ int ovf;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ltm = lanemask_lt();
     const K E = key_empty<K>();
@@ -656,41 +710,85 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
         T[i] = E;
         C[i] = 0;
     }
-    // chunk -> 16-byte aligned source range; the key buffer has 16 bytes of tail slack
-    auto issue = [&](uint32_t cc, int b) {
-        const Chunk ch = chunks[cc];
-        const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
-        const uint32_t bytes = (uint32_t)(((ch.begin + ch.n - a0) * sizeof(K) + 15) & ~(uint64_t)15);
-        mbar_expect_tx(mbar + b, bytes);
-        tma_load_1d(b ? S1 : S0, keys + a0, bytes, mbar + b);
-    };
     if (threadIdx.x == 0) {
-        mbar_init(mbar, 1);
-        mbar_init(mbar + 1, 1);
+        for (int b = 0; b < NBUF; ++b) mbar_init(mbar + b, 1);
         mbar_init_fence();
+        ovf = 0;
     }
     __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x < n_chunks) issue(blockIdx.x, 0);
+    // sub-piece q of chunk c: keys [a0 + q*SUB, a0 + (q+1)*SUB) clipped to the chunk, with
+    // a0 = chunk begin rounded down to 16 bytes
+    auto nsub_of = [&](const Chunk& ch) {
+        const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
+        return (uint32_t)((ch.begin + ch.n - a0 + SUB - 1) / SUB);
+    };
+    // producer cursor (thread 0 only): next (chunk iteration, sub-piece) to issue
+    uint32_t pit = 0, pq = 0, issued = 0;
+    Chunk pch{};
+    bool pvalid = false;
+    auto produce = [&]() {  // thread 0: issue the next sub-piece into buffer issued % NBUF
+        while (true) {
+            const uint32_t cc = blockIdx.x + pit * gridDim.x;
+            if (cc >= n_chunks) return;
+            if (!pvalid) {
+                pch = chunks[cc];
+                pvalid = true;
+            }
+            if (pq < nsub_of(pch)) break;
+            ++pit;
+            pq = 0;
+            pvalid = false;
+        }
+        const uint64_t a0 = pch.begin & ~(uint64_t)(PAD - 1);
+        const uint64_t s0 = a0 + (uint64_t)pq * SUB;
+        const uint64_t s1 = min(a0 + (uint64_t)(pq + 1) * SUB, pch.begin + pch.n);
+        const uint32_t bytes = (uint32_t)(((s1 - s0) * sizeof(K) + 15) & ~(uint64_t)15);
+        const int b = issued % NBUF;
+        fence_proxy_async_smem();
+        mbar_expect_tx(mbar + b, bytes);
+        tma_load_1d_hint(SB + b * BUFK, keys + s0, bytes, mbar + b, l2_policy_evict_first());
+        ++issued;
+        ++pq;
+    };
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NBUF - 1; ++i) produce();
     uint32_t uniq = 0, below = 0, above = 0;
+    uint32_t g = 0;  // consumed sub-pieces
     for (uint32_t it = 0;; ++it) {
         const uint32_t cc = blockIdx.x + it * gridDim.x;
         if (cc >= n_chunks) break;
-        const int b = it & 1;
-        // the other buffer was released by the previous iteration's final barrier
-        if (threadIdx.x == 0 && cc + gridDim.x < n_chunks) {
-            fence_proxy_async_smem();
-            issue(cc + gridDim.x, b ^ 1);
-        }
         const Chunk ch = chunks[cc];
-        const int n = (int)ch.n;
-        const int off = (int)(ch.begin & (uint64_t)(PAD - 1));
+        const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
+        const uint32_t nsub = nsub_of(ch);
         int lg = 6;
-        while ((1 << lg) < n + n / 3) ++lg;
+        const uint32_t want = ch.n + ch.n / 3 < (uint32_t)TSMAX ? ch.n + ch.n / 3 : (uint32_t)TSMAX;
+        while ((1u << lg) < want) ++lg;
         const int TS = 1 << lg;
-        mbar_wait(mbar + b, (it >> 1) & 1);
-        const K* src = (b ? S1 : S0) + off;
-        for (int i = threadIdx.x; i < n; i += CH_NT) table_insert<K>(T, C, lg, src[i]);
-        __syncthreads();
+        for (uint32_t q = 0; q < nsub; ++q, ++g) {
+            if (threadIdx.x == 0) produce();  // keeps NBUF-1 sub-pieces in flight
+            const int b = g % NBUF;
+            mbar_wait(mbar + b, (g / NBUF) & 1);
+            const uint64_t s0 = a0 + (uint64_t)q * SUB;
+            const uint64_t lo = max(s0, ch.begin), hi = min(s0 + SUB, ch.begin + ch.n);
+            const K* src = SB + b * BUFK + (lo - s0);
+            const int cnt = (int)(hi - lo);
+            bool ok = true;
+            for (int i = threadIdx.x; i < cnt; i += CH_NT) ok &= table_insert_bounded<K>(T, C, lg, src[i]);
+            if (!ok) ovf = 1;
+            __syncthreads();  // staging buffer b is free again
+        }
+        if (ovf) {
+            // too many distinct keys for the table: drop the partial counts, list the chunk
+            if (threadIdx.x == 0) overflow[atomicAdd(n_overflow, 1ull)] = ch;
+            for (int s = threadIdx.x; s < TS; s += CH_NT) {
+                T[s] = E;
+                C[s] = 0;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) ovf = 0;
+            __syncthreads();
+            continue;
+        }
         uint32_t cv[SPT];
         uint32_t keep = 0;
 #pragma unroll
@@ -729,9 +827,9 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
             const int s = j * CH_NT + threadIdx.x;
             const uint32_t bb = __ballot_sync(0xffffffffu, cv[j] != 0);
             if (cv[j]) {
-                const unsigned long long q = o + __popc(bb & ltm);
-                sk[q] = T[s];
-                sc[q] = cv[j];
+                const unsigned long long qq = o + __popc(bb & ltm);
+                sk[qq] = T[s];
+                sc[qq] = cv[j];
             }
             o += __popc(bb);
             if (s < TS) {
@@ -755,9 +853,11 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
 
 size_t chunk_key_slack_bytes() { return 16; }
 
+int chunk_hash_cap(int k) { return k <= 32 ? HashCfg<uint64_t>::slots : HashCfg<K128>::slots; }
+
 cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
                               uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
-                              int n_sms, cudaStream_t s) {
+                              Chunk* overflow, unsigned long long* n_overflow, int n_sms, cudaStream_t s) {
     if (n_chunks == 0) return cudaSuccess;
     if (n_chunks >= (1ull << 32)) return cudaErrorInvalidValue;
     const unsigned grid = (unsigned)std::min<uint64_t>(n_chunks, (uint64_t)std::max(1, n_sms));
@@ -767,13 +867,14 @@ cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_
         if ((e = cudaFuncSetAttribute(k_chunk_hash<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
             return e;
         k_chunk_hash<uint64_t><<<grid, CH_NT, sm, s>>>((const uint64_t*)keys, chunks, (uint32_t)n_chunks, ci, cx,
-                                                       (uint64_t*)surv_keys, surv_counts, gstats);
+                                                       (uint64_t*)surv_keys, surv_counts, gstats, overflow,
+                                                       n_overflow);
     } else {
         const size_t sm = chunk_hash_smem<K128>();
         if ((e = cudaFuncSetAttribute(k_chunk_hash<K128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
             return e;
         k_chunk_hash<K128><<<grid, CH_NT, sm, s>>>((const K128*)keys, chunks, (uint32_t)n_chunks, ci, cx,
-                                                   (K128*)surv_keys, surv_counts, gstats);
+                                                   (K128*)surv_keys, surv_counts, gstats, overflow, n_overflow);
     }
     return cudaGetLastError();
 }
@@ -827,14 +928,6 @@ int msd_digit_bits(uint64_t bin_windows, int k, int cap) {
     return D;
 }
 
-cudaError_t launch_large_count(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
-                               int k, uint32_t* digit_cnt, cudaStream_t s) {
-    if (n_pieces == 0) return cudaSuccess;
-    if (k <= 32) k_large_count<uint64_t><<<(unsigned)n_pieces, MSD_NT, 0, s>>>(bins, pieces, lbins, k, digit_cnt);
-    else k_large_count<K128><<<(unsigned)n_pieces, MSD_NT, 0, s>>>(bins, pieces, lbins, k, digit_cnt);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaStream_t s) {
     if (n_segments == 0) return cudaSuccess;
     const int sm = (int)((GP_SEG + 1 + 2 * GP_SEG) * 4);
@@ -846,23 +939,31 @@ cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaS
 
 uint64_t greedy_segments(uint64_t n_digits) { return (n_digits + GP_SEG - 1) / GP_SEG; }
 
-cudaError_t launch_large_scatter(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
-                                 int k, int dmax, uint32_t* digit_cur, void* keys, cudaStream_t s) {
-    if (n_pieces == 0) return cudaSuccess;
+template <class K, bool SC>
+cudaError_t split_t(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins, int k,
+                    int dmax, uint32_t n_ranges, uint32_t* table, void* keys, cudaStream_t s) {
+    const int sm = (int)split_smem<K>(k, dmax);
     cudaError_t e;
-    if (k <= 32) {
-        const int sm = (int)scatter_smem<uint64_t>(k, dmax);
-        if ((e = cudaFuncSetAttribute(k_large_scatter<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)))
-            return e;
-        k_large_scatter<uint64_t><<<(unsigned)n_pieces, MSD_NT, sm, s>>>(bins, pieces, lbins, k, dmax, digit_cur,
-                                                                         (uint64_t*)keys);
-    } else {
-        const int sm = (int)scatter_smem<K128>(k, dmax);
-        if ((e = cudaFuncSetAttribute(k_large_scatter<K128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)))
-            return e;
-        k_large_scatter<K128><<<(unsigned)n_pieces, MSD_NT, sm, s>>>(bins, pieces, lbins, k, dmax, digit_cur,
-                                                                     (K128*)keys);
-    }
+    if ((e = cudaFuncSetAttribute(k_split<K, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+    k_split<K, SC><<<n_ranges, SP_NT, sm, s>>>(bins, pieces, n_pieces, lbins, k, dmax, table, (K*)keys);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split(bool scatter, const uint32_t* bins, const Piece* pieces, uint64_t n_pieces,
+                         const LargeBin* lbins, int k, int dmax, uint32_t n_ranges, uint32_t* table, void* keys,
+                         cudaStream_t s) {
+    if (n_pieces == 0) return cudaSuccess;
+    if (k <= 32)
+        return scatter ? split_t<uint64_t, true>(bins, pieces, n_pieces, lbins, k, dmax, n_ranges, table, keys, s)
+                       : split_t<uint64_t, false>(bins, pieces, n_pieces, lbins, k, dmax, n_ranges, table, keys, s);
+    return scatter ? split_t<K128, true>(bins, pieces, n_pieces, lbins, k, dmax, n_ranges, table, keys, s)
+                   : split_t<K128, false>(bins, pieces, n_pieces, lbins, k, dmax, n_ranges, table, keys, s);
+}
+
+cudaError_t launch_digit_totals(const LargeBin* lbins, uint64_t n_lbins, const uint32_t* pos, uint32_t* cnt,
+                                cudaStream_t s) {
+    if (n_lbins == 0) return cudaSuccess;
+    k_digit_totals<<<(unsigned)n_lbins, 256, 0, s>>>(lbins, pos, cnt);
     return cudaGetLastError();
 }
 

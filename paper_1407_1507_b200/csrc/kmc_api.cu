@@ -576,7 +576,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         std::vector<uint64_t> pp(large_ids.size() + 1, 0);
         for (size_t i = 0; i < large_ids.size(); ++i) {
             const uint64_t b = large_ids[i];
-            lbins[i] = LargeBin{0, 0, bo[b], (uint32_t)bw[b], 0, (uint32_t)bn[b], 0};
+            lbins[i] = LargeBin{0, 0, bo[b], 0, (uint32_t)bw[b], 0, (uint32_t)bn[b], 0, 0, 0};
             pp[i + 1] = pp[i] + (bn[b] + PIECE_RECORDS - 1) / PIECE_RECORDS;
         }
         const uint64_t n_pieces = pp.back();
@@ -615,7 +615,24 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     } else if (large_windows > 0) {
         // hashed split: per large bin, a D-bit digit -> digit ranges in HBM -> chunks <= cap
         // keys.  Large bins are processed in groups whose keys fit the device budget.
-        const int kcap = small_capacity(k);
+        // chunk capacity (keys): the per-chunk radix sort holds small_capacity(k) keys; the
+        // hash table holds 3/4 of its slots in DISTINCT keys, so its chunks may carry more
+        // keys by the distinct/window ratio measured on the small bins (x1.5 margin; a
+        // chunk that still overflows is counted by the fallback)
+        int kcap = small_capacity(k);
+        if (j->opt.count_path != 1) {
+            const uint64_t safe = (uint64_t)chunk_hash_cap(k) * 3 / 4;
+            double r = 1.0;
+            const uint64_t small_w = n_windows - large_windows;
+            if (small_w >= (1u << 20)) {
+                CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                r = std::min(1.0, std::max(0.05, 1.5 * (double)hs[16 + GS_UNIQUE] / (double)small_w));
+            }
+            kcap = (int)std::min<uint64_t>(2ull * chunk_hash_cap(k), std::max<uint64_t>(safe, (uint64_t)(safe / r)));
+        }
+        if (j->opt.chunk_capacity) kcap = (int)std::min<uint32_t>(j->opt.chunk_capacity, 1u << 24);
+        j->st.chunk_capacity = (uint64_t)kcap;
         const int prec = msd_piece_records(k);
         // group budget in keys: the option, else everything at once if the key buffer can be
         // allocated, else half the free device memory
@@ -629,6 +646,8 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
                 budget = std::max<uint64_t>((uint64_t)(fr / 2) / (ksz + 1), 1u << 20);
             }
         }
+        // split positions are uint32 key indices within a group
+        budget = std::min<uint64_t>(budget, 0xFFFFFFFFull - 64);
         std::vector<std::pair<size_t, size_t>> groups;
         uint64_t max_gw = 0, max_gd = 0, max_gp = 0, max_gn = 0;
         for (size_t i0 = 0; i0 < large_ids.size();) {
@@ -650,15 +669,20 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             i0 = i1;
         }
         j->st.n_large_groups = groups.size();
+        // split ranges: one CTA each, a few per SM (the split kernels are ~40 KB of SMEM)
+        const uint32_t max_ranges = (uint32_t)n_sms() * 4;
         LargeBin* d_lbins = ar.get<LargeBin>(max_gn);
         uint64_t* d_pp = ar.get<uint64_t>(max_gn + 1);
         Piece* d_pieces = ar.get<Piece>(max_gp);
         uint32_t* digit_cnt = ar.get<uint32_t>(max_gd);
-        uint32_t* digit_cur = ar.get<uint32_t>(max_gd);
         Chunk* chunks = ar.get<Chunk>(max_gd);
         Chunk* oversize = ar.get<Chunk>(max_gd);
-        unsigned long long* counters = ar.get<unsigned long long>(2);
+        unsigned long long* counters = ar.get<unsigned long long>(3);
         if (!lkeys) lkeys = ar.alloc(max_gw * ksz + chunk_key_slack_bytes());
+        uint32_t* table = nullptr;
+        uint32_t* tpos = nullptr;
+        void* ttemp = nullptr;
+        uint64_t table_cap = 0;
         RadixScratch rs{};
         uint64_t rs_cap = 0;
         int sl = 0;
@@ -672,32 +696,58 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
                 const uint64_t b = large_ids[g.first + i];
                 const int D = msd_digit_bits(bw[b], k, kcap);
                 dmax = std::max(dmax, D);
-                lbins[i] = LargeBin{key_base, digit_base, bo[b], (uint32_t)bw[b], (uint32_t)D, (uint32_t)bn[b], 0};
+                lbins[i] = LargeBin{key_base, digit_base, bo[b], 0, (uint32_t)bw[b], (uint32_t)D, (uint32_t)bn[b], 0, 0, 0};
                 key_base += bw[b];
                 digit_base += 1ull << D;
                 pp[i + 1] = pp[i] + (bn[b] + prec - 1) / prec;
             }
             const uint64_t n_pieces = pp.back();
+            // ranges r = pieces [r*n/R, (r+1)*n/R); segments = (range, bin) pairs
+            const uint32_t R = (uint32_t)std::min<uint64_t>(n_pieces, max_ranges);
+            auto range_of = [&](uint64_t piece) {
+                uint64_t r = piece * R / n_pieces;
+                while (r + 1 < R && (r + 1) * n_pieces / R <= piece) ++r;
+                while (r > 0 && r * n_pieces / R > piece) --r;
+                return (uint32_t)r;
+            };
+            uint64_t tb = 0;
+            for (size_t i = 0; i < gn; ++i) {
+                const uint32_t f = range_of(pp[i]), l = range_of(pp[i + 1] - 1);
+                lbins[i].first_range = f;
+                lbins[i].nseg = l - f + 1;
+                lbins[i].tb = tb;
+                tb += (uint64_t)lbins[i].nseg << lbins[i].D;
+            }
+            if (tb + 1 > table_cap) {
+                ar.release(table);
+                ar.release(tpos);
+                ar.release(ttemp);
+                table_cap = tb + 1;
+                table = ar.get<uint32_t>(table_cap);
+                tpos = ar.get<uint32_t>(table_cap);
+                ttemp = ar.alloc(scan_temp_bytes(table_cap));
+            }
             CK(cudaMemcpyAsync(d_lbins, lbins.data(), gn * sizeof(LargeBin), cudaMemcpyHostToDevice, s));
             CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
             j->stage_begin(KMC_STAGE_LARGE_SPLIT);
-            CK(cudaMemsetAsync(digit_cnt, 0, digit_base * 4, s));
-            CK(cudaMemsetAsync(counters, 0, 16, s));
+            CK(cudaMemsetAsync(counters, 0, 24, s));
             CK(launch_make_pieces(d_lbins, d_pp, gn, (uint32_t)prec, d_pieces, s));
-            CK(launch_large_count(bins, d_pieces, n_pieces, d_lbins, k, digit_cnt, s));
+            CK(launch_split(false, bins, d_pieces, n_pieces, d_lbins, k, dmax, R, table, nullptr, s));
+            CK(scan_u32_to_u32(table, tpos, tb, ttemp, s));
+            CK(launch_digit_totals(d_lbins, gn, tpos, digit_cnt, s));
             GreedyArgs ga{};
             ga.cnt = digit_cnt;
             ga.lbins = d_lbins;
-            ga.cursor = digit_cur;
+            ga.cursor = nullptr;
             ga.cursor_abs = 0;
             ga.chunks = chunks;
             ga.oversize = oversize;
             ga.counters = counters;
             ga.cap = (uint32_t)kcap;
             CK(launch_greedy_chunks(ga, gn, s));
-            CK(launch_large_scatter(bins, d_pieces, n_pieces, d_lbins, k, dmax, digit_cur, lkeys, s));
-            j->launches += 4;
-            j->stage_end(4);
+            CK(launch_split(true, bins, d_pieces, n_pieces, d_lbins, k, dmax, R, tpos, lkeys, s));
+            j->launches += 7;
+            j->stage_end(7);
             CK(cudaMemcpyAsync(&hs[48], counters, 16, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             const uint64_t n_chunks = hs[48], n_over = hs[49];
@@ -707,13 +757,21 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
                                      s));
             else
                 CK(launch_chunk_hash(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats,
-                                     n_sms(), s));
+                                     oversize + n_over, counters + 2, n_sms(), s));
             j->launches += 1;
             j->stage_end(1);
-            if (n_over > 0) {
-                // digits above CTA capacity (identical-key pile-ups): device LSD + run pass
-                std::vector<Chunk> ov(n_over);
-                CK(cudaMemcpyAsync(ov.data(), oversize, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+            uint64_t n_ovf = 0;
+            if (j->opt.count_path != 1) {
+                CK(cudaMemcpyAsync(&hs[50], counters + 2, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                n_ovf = hs[50];
+                j->st.n_overflow_chunks += n_ovf;
+            }
+            if (n_over + n_ovf > 0) {
+                // digits above the chunk capacity (identical-key pile-ups) and chunks whose
+                // distinct keys overflowed the hash table: device LSD + run pass
+                std::vector<Chunk> ov(n_over + n_ovf);
+                CK(cudaMemcpyAsync(ov.data(), oversize, ov.size() * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
                 uint64_t maxn = 0;
                 for (auto& c : ov) maxn = std::max<uint64_t>(maxn, c.n);

@@ -120,6 +120,47 @@ __device__ __forceinline__ void for_each_window(const uint32_t (&wd)[RW], int k,
     }
 }
 
+// ---------------------------------------------------------------- window-parallel expansion
+// Canonical key of window j of a record in shared memory, computed directly from the
+// packed bits (no rolling): fwd = the 2k-bit field at bit 8+2j of the record's big-endian
+// bit string; rc = complement, 2-bit groups reversed.  One lane per window, so
+// records of different lengths do not idle the lanes of a warp.
+__device__ __forceinline__ uint64_t rev2_64(uint64_t x) {  // reverse the order of the 2-bit groups
+    x = __brevll(x);
+    return ((x >> 1) & 0x5555555555555555ull) | ((x & 0x5555555555555555ull) << 1);
+}
+// bits [b, b+64) of a big-endian bit string in shared memory words (b + 64 <= 32 * words)
+__device__ __forceinline__ uint64_t bits64_be(const uint32_t* w, int b) {
+    const int q = b >> 5, r = b & 31;
+    const uint32_t w0 = w[q], w1 = w[q + 1], w2 = w[q + 2];
+    const uint32_t hi = __funnelshift_l(w1, w0, r), lo = __funnelshift_l(w2, w1, r);
+    return ((uint64_t)hi << 32) | lo;
+}
+template <class K> __device__ __forceinline__ K window_key(const uint32_t* rec, int j, int k);
+template <> __device__ __forceinline__ uint64_t window_key<uint64_t>(const uint32_t* rec, int j, int k) {
+    // field of 2k <= 64 bits starting at bit 8+2j; the record has 4 words (+1 readable pad)
+    const uint64_t f = bits64_be(rec, 8 + 2 * j) >> (64 - 2 * k);
+    const uint64_t r = rev2_64(~f) >> (64 - 2 * k);
+    return f < r ? f : r;
+}
+template <> __device__ __forceinline__ K128 window_key<K128>(const uint32_t* rec, int j, int k) {
+    // 2k in (64, 128] bits at bit b = 8+2j: hi part = first 2k-64 bits, lo part = next 64
+    const int b = 8 + 2 * j, hb = 2 * k - 64;
+    K128 f;
+    f.hi = bits64_be(rec, b) >> (64 - hb);
+    f.lo = bits64_be(rec, b + hb);
+    // rc: reverse the 2k-bit string of complemented groups: lo' = rev of hi.. parts
+    const uint64_t nl = ~f.lo, nh = ~f.hi;  // complement (upper bits of nh beyond hb are junk)
+    // full 128-bit value V = nh:nl (hb + 64 bits used).  rev2 over 128 bits = (rev2(nl), rev2(nh)),
+    // then shift right by 128 - 2k = 64 - hb.
+    const uint64_t a = rev2_64(nl), c = rev2_64(nh);  // a = high word of reversed, c = low word
+    const int sh = 64 - hb;                           // 0 <= sh < 64
+    K128 r;
+    r.lo = sh ? ((c >> sh) | (a << (64 - sh))) : c;
+    r.hi = sh ? (a >> sh) : a;
+    return key_lt(r, f) ? r : f;
+}
+
 // Digit of the large-bin split: a multiplicative hash of the whole key (equal keys share
 // a digit; the top bits of a key are a poor digit, see k_sort.cu).  1 <= D <= 12.
 __device__ __forceinline__ uint32_t part_digit(uint64_t key, int D) {
@@ -169,6 +210,21 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
                  "l"(src), "r"(bytes), "r"(smem_addr(m))
                  : "memory");
 }
+// Same, with an L2 eviction-priority hint (a streaming source read once: evict_first, so
+// it does not push out lines the kernel still writes, e.g. partial sectors being filled).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes, uint64_t* m,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(m)), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
@@ -179,6 +235,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
 // Orders earlier generic-proxy shared-memory accesses before later async-proxy (TMA) ones.
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Streaming (evict-first) global loads of keys.
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p) {
+    return __ldcs(reinterpret_cast<const unsigned long long*>(p));
+}
+__device__ __forceinline__ K128 ld_stream(const K128* p) {
+    const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(p));
+    return K128{v.x, v.y};
 }
 
 // ---------------------------------------------------------------- shared-memory hash table
@@ -644,6 +709,28 @@ __device__ __forceinline__ void block_rle_bitmask(const K* S, int n, uint32_t* b
         }
         slot += __popc(b);
     }
+}
+
+// Per-window record lookup for a piece of nrec records (RW words each) in shared memory:
+// wpos[r] = first window of record r in the piece, own[w] = record of window w.  Returns the
+// piece's window count.  All threads must call; ends with __syncthreads().
+template <int NT>
+__device__ __forceinline__ int piece_window_map(const uint32_t* R, int nrec, int RW, uint32_t* wpos, uint16_t* own,
+                                                uint32_t* wsum) {
+    const int rpt = (nrec + NT - 1) / NT;
+    const int r0 = threadIdx.x * rpt, r1 = min(nrec, r0 + rpt);
+    uint32_t s = 0;
+    for (int r = r0; r < r1; ++r) s += rec_nwin(R + r * RW);
+    uint32_t total;
+    uint32_t pos = block_excl_sum<NT, uint32_t>(s, wsum, &total);
+    for (int r = r0; r < r1; ++r) {
+        const uint32_t n = rec_nwin(R + r * RW);
+        wpos[r] = pos;
+        for (uint32_t j = 0; j < n; ++j) own[pos + j] = (uint16_t)r;
+        pos += n;
+    }
+    __syncthreads();
+    return (int)total;
 }
 
 }  // namespace kmc

@@ -122,9 +122,12 @@ struct LargeBin {
     uint64_t key_base;
     uint64_t digit_base;
     uint64_t rec_off;
+    uint64_t tb;           // split table index of (digit 0, segment 0) of this bin
     uint32_t n;
     uint32_t D;
     uint32_t nrec;
+    uint32_t first_range;  // first split range (CTA) holding pieces of this bin
+    uint32_t nseg;         // split ranges holding pieces of this bin
     uint32_t pad;
 };
 // pieces[piece_prefix[i] + j] = records [j*rec_per_piece, ...) of large bin i
@@ -136,8 +139,6 @@ struct Chunk {
     uint32_t pad;
 };
 int msd_digit_bits(uint64_t bin_windows, int k, int cap);
-cudaError_t launch_large_count(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
-                               int k, uint32_t* digit_cnt, cudaStream_t s);
 // Greedy chunk planner: segments are either the large bins (lbins != nullptr; one CTA per
 // bin, 2^D digits each, chunk keys at key_base + bin-relative offsets) or 4096-digit windows
 // of a global digit array (lbins == nullptr; gstart = exclusive scan of cnt).
@@ -155,17 +156,26 @@ struct GreedyArgs {
 };
 cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaStream_t s);
 uint64_t greedy_segments(uint64_t n_digits);
-cudaError_t launch_large_scatter(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins,
-                                 int k, int dmax, uint32_t* digit_cur, void* keys, cudaStream_t s);
+// Split of the large bins into digit-contiguous key ranges (k_split): count pass (table of
+// per-(bin, digit, segment) counts), then, after an exclusive scan of the table, the scatter.
+cudaError_t launch_split(bool scatter, const uint32_t* bins, const Piece* pieces, uint64_t n_pieces,
+                         const LargeBin* lbins, int k, int dmax, uint32_t n_ranges, uint32_t* table, void* keys,
+                         cudaStream_t s);
+cudaError_t launch_digit_totals(const LargeBin* lbins, uint64_t n_lbins, const uint32_t* pos, uint32_t* cnt,
+                                cudaStream_t s);
 cudaError_t launch_chunk_sort(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
                               uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
                               cudaStream_t s);
 // S7-S8 of the chunks by SMEM hash counting (persistent, one CTA per SM, TMA-prefetched).
 // The key buffer must have chunk_key_slack_bytes() of readable slack past its last key.
+// Chunks that hold more distinct keys than the table (rare) are appended to overflow[] and
+// must be counted by another path.  chunk_hash_cap(k): table slots (distinct keys < 3/4 of it
+// are always safe).
 size_t chunk_key_slack_bytes();
+int chunk_hash_cap(int k);
 cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
                               uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
-                              int n_sms, cudaStream_t s);
+                              Chunk* overflow, unsigned long long* n_overflow, int n_sms, cudaStream_t s);
 cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, void* keys,
                                 unsigned long long* gstats, cudaStream_t s);
 

@@ -140,6 +140,17 @@ def test_k_boundaries(gpu, k, force_large):
     assert_same(gpu, synth.from_strings(seqs, k, p, 1), force_large=force_large)
 
 
+def test_chunk_hash_overflow_fallback(gpu):
+    # distinct-heavy large bins (random reads, no coverage) with a distinct ratio measured on
+    # low-coverage small bins: chunks sized for repeats overflow the table and must fall back
+    seqs = synth.random_reads(77, 6000, 100, 150, alphabet=b"ACGT")
+    w = synth.from_strings(seqs, 25, 5, 1)
+    st = assert_same(gpu, w, force_large=True, chunk_capacity=60000)
+    assert st["large_windows"] > 0 and st["n_overflow_chunks"] > 0
+    st = assert_same(gpu, w, force_large=True)
+    assert st["n_overflow_chunks"] == 0
+
+
 @pytest.mark.parametrize("count_path", [0, 1])
 @pytest.mark.parametrize("name,scale", [("C3", 0.005), ("C2", 0.005), ("C1", 0.2)])
 def test_chunk_count_paths(gpu, name, scale, count_path):
