@@ -657,7 +657,7 @@ template <> struct HashCfg<K128> { static constexpr int slots = 8192, sub = 512,
 
 template <class K> constexpr size_t chunk_hash_smem() {
     return (size_t)HashCfg<K>::slots * (sizeof(K) + 4) +
-           (size_t)HashCfg<K>::nbuf * ((size_t)HashCfg<K>::sub * sizeof(K) + 16) + 64;
+           (size_t)HashCfg<K>::nbuf * ((size_t)HashCfg<K>::sub * sizeof(K) + 16) + 2 * 8 * HashCfg<K>::nbuf + 16;
 }
 
 // Counts key; false if no slot was found within PROBE_MAX probes (table too full).
@@ -691,17 +691,22 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
                                                          uint32_t* sc, unsigned long long* gstats,
                                                          Chunk* __restrict__ overflow,
                                                          unsigned long long* __restrict__ n_overflow) {
+    // warp CW (the last) is the producer: it streams the sub-pieces of this CTA's chunks into
+    // the NBUF staging buffers (full[b] completes on the TMA byte count, empty[b] when every
+    // consumer warp has released the buffer).  Warps 0..CW-1 consume: insert, then -- per
+    // chunk, behind a named barrier among consumers only -- emit and clear the table.
     constexpr int TSMAX = HashCfg<K>::slots, SUB = HashCfg<K>::sub, NBUF = HashCfg<K>::nbuf;
-    constexpr int NW = CH_NT / 32, SPT = TSMAX / CH_NT;
+    constexpr int CW = CH_NT / 32 - 1, CT = CW * 32;  // consumer warps / threads
     constexpr int PAD = 16 / sizeof(K) > 1 ? 16 / sizeof(K) : 1;  // keys per 16 bytes
     constexpr int BUFK = SUB + PAD;                                 // keys per staging buffer
     extern __shared__ __align__(128) uint8_t smem[];
     K* T = reinterpret_cast<K*>(smem);
     uint32_t* C = reinterpret_cast<uint32_t*>(T + TSMAX);
     K* SB = reinterpret_cast<K*>(C + TSMAX);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(SB + NBUF * BUFK);
-    __shared__ uint32_t wk[NW];
-    __shared__ unsigned long long wb[NW];
+    uint64_t* full = reinterpret_cast<uint64_t*>(SB + NBUF * BUFK);
+    uint64_t* empty = full + NBUF;
+    __shared__ uint32_t wk[CW];
+    __shared__ unsigned long long wb[CW];
     __shared__ int ovf;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ltm = lanemask_lt();
@@ -711,125 +716,111 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
         C[i] = 0;
     }
     if (threadIdx.x == 0) {
-        for (int b = 0; b < NBUF; ++b) mbar_init(mbar + b, 1);
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(full + b, 1);
+            mbar_init(empty + b, CW);
+        }
         mbar_init_fence();
         ovf = 0;
     }
     __syncthreads();
-    // sub-piece q of chunk c: keys [a0 + q*SUB, a0 + (q+1)*SUB) clipped to the chunk, with
-    // a0 = chunk begin rounded down to 16 bytes
     auto nsub_of = [&](const Chunk& ch) {
         const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
         return (uint32_t)((ch.begin + ch.n - a0 + SUB - 1) / SUB);
     };
-    // producer cursor (thread 0 only): next (chunk iteration, sub-piece) to issue
-    uint32_t pit = 0, pq = 0, issued = 0;
-    Chunk pch{};
-    bool pvalid = false;
-    auto produce = [&]() {  // thread 0: issue the next sub-piece into buffer issued % NBUF
-        while (true) {
-            const uint32_t cc = blockIdx.x + pit * gridDim.x;
-            if (cc >= n_chunks) return;
-            if (!pvalid) {
-                pch = chunks[cc];
-                pvalid = true;
+    if (warp == CW) {
+        // ---- producer
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            uint32_t g = 0;
+            for (uint32_t cc = blockIdx.x; cc < n_chunks; cc += gridDim.x) {
+                const Chunk ch = chunks[cc];
+                const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
+                const uint32_t nsub = nsub_of(ch);
+                for (uint32_t q = 0; q < nsub; ++q, ++g) {
+                    const int b = g % NBUF;
+                    if (g >= NBUF) mbar_wait(empty + b, ((g / NBUF) - 1) & 1);
+                    const uint64_t s0 = a0 + (uint64_t)q * SUB;
+                    const uint64_t s1 = min(s0 + SUB, ch.begin + ch.n);
+                    const uint32_t bytes = (uint32_t)(((s1 - s0) * sizeof(K) + 15) & ~(uint64_t)15);
+                    fence_proxy_async_smem();
+                    mbar_expect_tx(full + b, bytes);
+                    tma_load_1d_hint(SB + b * BUFK, keys + s0, bytes, full + b, pol);
+                }
             }
-            if (pq < nsub_of(pch)) break;
-            ++pit;
-            pq = 0;
-            pvalid = false;
         }
-        const uint64_t a0 = pch.begin & ~(uint64_t)(PAD - 1);
-        const uint64_t s0 = a0 + (uint64_t)pq * SUB;
-        const uint64_t s1 = min(a0 + (uint64_t)(pq + 1) * SUB, pch.begin + pch.n);
-        const uint32_t bytes = (uint32_t)(((s1 - s0) * sizeof(K) + 15) & ~(uint64_t)15);
-        const int b = issued % NBUF;
-        fence_proxy_async_smem();
-        mbar_expect_tx(mbar + b, bytes);
-        tma_load_1d_hint(SB + b * BUFK, keys + s0, bytes, mbar + b, l2_policy_evict_first());
-        ++issued;
-        ++pq;
-    };
-    if (threadIdx.x == 0)
-        for (int i = 0; i < NBUF - 1; ++i) produce();
+        return;
+    }
+    // ---- consumers
+    const int ct = threadIdx.x;
     uint32_t uniq = 0, below = 0, above = 0;
-    uint32_t g = 0;  // consumed sub-pieces
-    for (uint32_t it = 0;; ++it) {
-        const uint32_t cc = blockIdx.x + it * gridDim.x;
-        if (cc >= n_chunks) break;
+    uint32_t g = 0;
+    for (uint32_t cc = blockIdx.x; cc < n_chunks; cc += gridDim.x) {
         const Chunk ch = chunks[cc];
         const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
         const uint32_t nsub = nsub_of(ch);
-        int lg = 6;
         const uint32_t want = ch.n + ch.n / 3 < (uint32_t)TSMAX ? ch.n + ch.n / 3 : (uint32_t)TSMAX;
+        int lg = 6;
         while ((1u << lg) < want) ++lg;
         const int TS = 1 << lg;
+        bool ok = true;
         for (uint32_t q = 0; q < nsub; ++q, ++g) {
-            if (threadIdx.x == 0) produce();  // keeps NBUF-1 sub-pieces in flight
             const int b = g % NBUF;
-            mbar_wait(mbar + b, (g / NBUF) & 1);
+            mbar_wait(full + b, (g / NBUF) & 1);
             const uint64_t s0 = a0 + (uint64_t)q * SUB;
             const uint64_t lo = max(s0, ch.begin), hi = min(s0 + SUB, ch.begin + ch.n);
             const K* src = SB + b * BUFK + (lo - s0);
             const int cnt = (int)(hi - lo);
-            bool ok = true;
-            for (int i = threadIdx.x; i < cnt; i += CH_NT) ok &= table_insert_bounded<K>(T, C, lg, src[i]);
-            if (!ok) ovf = 1;
-            __syncthreads();  // staging buffer b is free again
+            for (int i = ct; i < cnt; i += CT) ok &= table_insert_bounded<K>(T, C, lg, src[i]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + b);
         }
+        if (!ok) ovf = 1;
+        named_bar_sync(1, CT);
         if (ovf) {
             // too many distinct keys for the table: drop the partial counts, list the chunk
-            if (threadIdx.x == 0) overflow[atomicAdd(n_overflow, 1ull)] = ch;
-            for (int s = threadIdx.x; s < TS; s += CH_NT) {
+            if (ct == 0) overflow[atomicAdd(n_overflow, 1ull)] = ch;
+            for (int s = ct; s < TS; s += CT) {
                 T[s] = E;
                 C[s] = 0;
             }
-            __syncthreads();
-            if (threadIdx.x == 0) ovf = 0;
-            __syncthreads();
+            named_bar_sync(1, CT);
+            if (ct == 0) ovf = 0;
+            named_bar_sync(1, CT);
             continue;
         }
-        uint32_t cv[SPT];
         uint32_t keep = 0;
-#pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-            const int s = j * CH_NT + threadIdx.x;
-            cv[j] = s < TS ? C[s] : 0u;
-            if (cv[j]) {
+        for (int s = ct; s < TS; s += CT) {
+            const uint32_t c = C[s];
+            if (c) {
                 ++uniq;
-                if (cv[j] < ci) {
-                    ++below;
-                    cv[j] = 0;
-                } else if (cv[j] > cx) {
-                    ++above;
-                    cv[j] = 0;
-                } else {
-                    ++keep;
-                }
+                if (c < ci) ++below;
+                else if (c > cx) ++above;
+                else ++keep;
             }
         }
         keep = __reduce_add_sync(0xffffffffu, keep);
         if (lane == 0) wk[warp] = keep;
-        __syncthreads();
+        named_bar_sync(1, CT);
         if (warp == 0) {
-            const uint32_t kw = lane < NW ? wk[lane] : 0u;
+            const uint32_t kw = lane < CW ? wk[lane] : 0u;
             const uint32_t inc = warp_incl_sum(kw);
             unsigned long long b0 = 0;
-            if (lane == NW - 1 && inc) b0 = atomicAdd(&gstats[GS_SURV], (unsigned long long)inc);
-            b0 = __shfl_sync(0xffffffffu, b0, NW - 1);
-            if (lane < NW) wb[lane] = b0 + inc - kw;
+            if (lane == CW - 1 && inc) b0 = atomicAdd(&gstats[GS_SURV], (unsigned long long)inc);
+            b0 = __shfl_sync(0xffffffffu, b0, CW - 1);
+            if (lane < CW) wb[lane] = b0 + inc - kw;
         }
-        __syncthreads();
+        named_bar_sync(1, CT);
         unsigned long long o = wb[warp];
-#pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-            if (j * CH_NT >= TS) break;
-            const int s = j * CH_NT + threadIdx.x;
-            const uint32_t bb = __ballot_sync(0xffffffffu, cv[j] != 0);
-            if (cv[j]) {
+        for (int s0 = 0; s0 < TS; s0 += CT) {
+            const int s = s0 + ct;
+            const uint32_t c = s < TS ? C[s] : 0u;
+            const bool kp = c >= ci && c <= cx && c != 0;
+            const uint32_t bb = __ballot_sync(0xffffffffu, kp);
+            if (kp) {
                 const unsigned long long qq = o + __popc(bb & ltm);
                 sk[qq] = T[s];
-                sc[qq] = cv[j];
+                sc[qq] = c;
             }
             o += __popc(bb);
             if (s < TS) {
@@ -837,7 +828,7 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
                 C[s] = 0;
             }
         }
-        __syncthreads();
+        named_bar_sync(1, CT);
     }
     uniq = __reduce_add_sync(0xffffffffu, uniq);
     below = __reduce_add_sync(0xffffffffu, below);
