@@ -1,12 +1,21 @@
 // k_distribute.cu -- phase 1 of KMC 2 on the B200 (Sec. 2.4 "distribution"):
 // S1 encode + split at non-ACGT and read ends, S2 signatures, S3 super-k-mer cut,
-// S4 histogram (pass 1) and S5 scatter of super-k-mer records into HBM bins (pass 2).
+// S4 histogram (pass 1) and S5 scatter of super-k-mer records into HBM bins.
 //
-// One CTA owns a tile of P1_TILE consecutive window starts of the concatenated base
-// stream (windows never cross read boundaries: reads are marked from read_offsets).
-// Everything between the ASCII load and the histogram / bin write stays in shared
-// memory: codes, valid-run lengths, the canonical p-mer key of every position, the
-// van Herk / Gil-Werman block prefix/suffix minima, and the per-window signature.
+// Warp-centric and persistent: every warp owns a stream of SEG = 512-window segments of
+// the concatenated base stream (windows never cross read boundaries: reads are marked
+// from read_offsets) and runs the whole of S1-S4 for a segment inside its own slice of
+// shared memory, with __syncwarp between steps and no CTA-wide barrier:
+//   A  ASCII (16-byte vectors) -> 2-bit codes, invalid-base bitmask
+//   B  read starts -> bitmask (bad = invalid | read start)
+//   C  canonical p-mer key of every position, computed directly from the packed bits
+//      (fwd = a 2p-bit field, rc = complement with the 2-bit groups reversed), held in
+//      registers (row r, lane l = position 32r + l)
+//   D  sliding minimum over W = k-p+1 keys with warp shuffles (log-step doubling)
+//   E  window signature = that minimum if the window is valid
+//   F  super-k-mer runs (ballot bitmask + compacted run starts), histogram atomics, and
+//      the records: appended to a temporary stream from per-warp reserved blocks (pass 1)
+//      or written into their bins (recompute path)
 #include <algorithm>
 
 #include "kmc_device.cuh"
@@ -16,26 +25,77 @@ namespace kmc {
 
 namespace {
 
-constexpr int LEFT = 16;                      // halo before the tile (window q0-1 + alignment)
-constexpr int NB = P1_TILE + 96;             // loaded bases: LEFT + tile + k-1 (k <= 64); multiple of 32
-constexpr int CH = (NB + P1_NT - 1) / P1_NT;  // positions per thread in the scans
-constexpr int WPT = P1_TILE / P1_NT;          // windows owned per thread
+constexpr int SEG = P1_SEG;                   // window starts per warp segment
+constexpr int HL = 16;                        // bases before the segment (window seg0-1, alignment)
+constexpr int NBASE = HL + SEG + 64;          // local bases held (k <= 64 needs HL + SEG + 63)
+static_assert(NBASE % 32 == 16, "the invalid mask's last half word is set explicitly");
+constexpr int NPK = NBASE / 16 + 8;           // packed words (+ zero slack for record packing)
+constexpr int NMW = NBASE / 32 + 4;           // bitmask words (+ slack for 3-word funnel reads)
+constexpr int NKEY = SEG + 64;                // p-mer positions 15 .. 15 + SEG + W - 1 (W <= 64)
+constexpr int NROW = NKEY / 32;               // register rows of 32 positions
+constexpr int SG_WARPS = 8, SG_NT = 32 * SG_WARPS;
 constexpr uint32_t INV = 0xFFFFFFFFu;
-static_assert(NB % 32 == 0 && NB >= LEFT + P1_TILE + 63, "NB");
+constexpr uint32_t TMP_BLK = 2048;            // temporary-stream records reserved per warp at a time
 
-// A->0, C->1, G->2, T->3; lowercase folded; anything else -> 4 (invalid, R3).
-__device__ __forceinline__ uint32_t encode_base(uint32_t ch) {
-    uint32_t c = ch & 0xDFu;
-    bool ok = (c == 'A') | (c == 'C') | (c == 'G') | (c == 'T');
-    return ok ? (((c >> 1) ^ (c >> 2)) & 3u) : 4u;
+struct WarpSmem {
+    uint32_t pk[NPK];    // 2-bit codes, 16 per word, MSB first (local base x: word x/16)
+    uint32_t inv[NMW];   // bit x: local base x is not A/C/G/T (or outside the stream)
+    uint32_t bad[NMW];   // bit x: invalid, or a read starts at x
+    uint32_t vwin[NMW];  // bit x: the k-mer window starting at local x is valid
+    uint32_t vpm[NMW];   // bit x: the p-mer starting at local x is valid
+    uint32_t ebits[SEG / 32 + 2];  // bit v: window v cannot continue a run (invalid / run start)
+    uint32_t sig[SEG + 8];   // window signatures (local window 15 + y at y)
+    uint32_t list[SEG];      // run starts
+};
+
+// A->0, C->1, G->2, T->3; lowercase folded; anything else invalid (R3).
+__device__ __forceinline__ void encode16(const uint32_t (&wd)[4], uint32_t& packed, uint32_t& invbits) {
+    packed = 0;
+    invbits = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const uint32_t c = wd[t] & 0xDFDFDFDFu;
+        const uint32_t ok = __vcmpeq4(c, 0x41414141u) | __vcmpeq4(c, 0x43434343u) | __vcmpeq4(c, 0x47474747u) |
+                            __vcmpeq4(c, 0x54545454u);
+        const uint32_t cd = ((c >> 1) ^ (c >> 2)) & 0x03030303u;  // per byte: A0 C1 G2 T3
+        const uint32_t b8 = ((cd & 0xFFu) << 6) | (((cd >> 8) & 0xFFu) << 4) | (((cd >> 16) & 0xFFu) << 2) | (cd >> 24);
+        packed |= b8 << (24 - 8 * t);
+        const uint32_t badb = (~ok) & 0x01010101u;
+        invbits |= (((badb * 0x01020408u) >> 24) & 0xFu) << (4 * t);
+    }
+}
+
+// Lane w holds word w of a bitmask X (LSB-first; lanes past the mask hold 0).  Returns word
+// w of "X shifted down by s" (bit x <- bit x + s), 0 <= s < 64, via the next two lanes.
+__device__ __forceinline__ uint32_t shr_words(uint32_t x, int s) {
+    const uint32_t x1 = __shfl_down_sync(0xffffffffu, x, 1), x2 = __shfl_down_sync(0xffffffffu, x, 2);
+    const int lane = threadIdx.x & 31;
+    const uint32_t n1 = lane < 31 ? x1 : 0u, n2 = lane < 30 ? x2 : 0u;
+    return s < 32 ? __funnelshift_r(x, n1, s) : __funnelshift_r(n1, n2, s - 32);
+}
+// Word w (lane w) of R_L: bit x = AND of G over positions [x, x + L) (L <= 63), by doubling.
+__device__ __forceinline__ uint32_t run_and(uint32_t g, int L) {
+    if (L == 0) return 0xFFFFFFFFu;
+    uint32_t r = g;
+    int a = 1;
+    while (2 * a <= L) {
+        r &= shr_words(r, a);
+        a *= 2;
+    }
+    return a == L ? r : (r & shr_words(r, L - a));
+}
+
+__device__ __forceinline__ uint32_t rev2_32(uint32_t x) {  // reverse the order of the 2-bit groups
+    x = __brev(x);
+    return ((x >> 1) & 0x55555555u) | ((x & 0x55555555u) << 1);
 }
 
 __global__ void k_tile_reads(const uint64_t* __restrict__ offsets, uint64_t n_reads, uint64_t off0,
                              uint64_t n_tiles, uint64_t* __restrict__ tile_r_lo) {
     uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_tiles) return;
-    // first r in [0, n_reads] with offsets[r] - off0 > left edge of tile t
-    int64_t edge = (int64_t)(t * P1_TILE) - LEFT;
+    // first r in [0, n_reads] with offsets[r] - off0 > left edge of segment t (its local 0)
+    int64_t edge = (int64_t)(t * SEG) - HL;
     uint64_t lo = 0, hi = n_reads + 1;
     while (lo < hi) {
         uint64_t mid = (lo + hi) >> 1;
@@ -45,336 +105,282 @@ __global__ void k_tile_reads(const uint64_t* __restrict__ offsets, uint64_t n_re
     tile_r_lo[t] = lo;
 }
 
-constexpr int NWD = NB / 32 + 8;  // bitmask words (with slack for funnel reads)
-
-struct P1Smem {
-    uint32_t pre[NB];            // p-mer keys, then (in place) block prefix minima; later the run-start list
-    uint32_t suf[NB];            // block suffix minima, then (in place) per-window signatures
-    uint32_t pk[NB / 16 + 8];    // 2-bit packed codes, 16 per word, MSB first
-    uint32_t inv[NWD];           // bit x: base x is not A/C/G/T (or outside the stream)
-    uint32_t rs[NWD];            // bit x: a read starts at x
-    uint32_t ext[NWD];           // bit x: x can extend a run to its left (valid, no read start)
-    uint32_t vwin[NWD];          // bit i: window i is valid
-    uint32_t vpm[NWD];           // bit j: p-mer j is valid
-    uint32_t ebits[P1_TILE / 32 + 8];
-    uint32_t wsum32[P1_NT / 32 + 1];
-    uint32_t cnt[8];
-    unsigned long long tmp_base;
-};
-
-// bits [a, a+32) of a bitmask (bit x&31 of word x>>5 is position x)
-__device__ __forceinline__ uint32_t bits32_at(const uint32_t* m, int a) {
-    return __funnelshift_r(m[a >> 5], m[(a >> 5) + 1], a & 31);
-}
-
 template <int MODE>
-__global__ void __launch_bounds__(P1_NT) k_pass(P1Args a) {
+__global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
     extern __shared__ __align__(16) uint8_t p1_smem[];
-    P1Smem& S = *reinterpret_cast<P1Smem*>(p1_smem);
-    uint32_t* pre = S.pre;
-    uint32_t* suf = S.suf;
-    uint32_t* pk = S.pk;
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int64_t q0 = (int64_t)blockIdx.x * P1_TILE;
-    const int64_t lbase = q0 - LEFT;  // stream position of smem index 0
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpSmem& S = reinterpret_cast<WarpSmem*>(p1_smem)[warp];
+    const uint32_t ltm = lanemask_lt();
     const int64_t nb = (int64_t)a.n_bases;
-    const int k = a.k, p = a.p;
-    const uint64_t r0 = a.tile_r_lo[blockIdx.x];  // issued early: its latency overlaps S1
-
-    // ---- S1: load ASCII (16-byte vectors), encode A0 C1 G2 T3 four bytes at a time
-    //      (lowercase folded); non-ACGT bytes and bytes outside the stream -> inv bits
-    uint32_t n_invalid = 0;
-    for (int v = tid; v < NB / 16; v += P1_NT) {
-        const int64_t q = lbase + 16 * v;
-        uint32_t wd[4];
-        if (a.reads_aligned16 && q >= 0 && q + 16 <= nb) {
-            const uint4 w = *reinterpret_cast<const uint4*>(a.reads + q);
-            wd[0] = w.x; wd[1] = w.y; wd[2] = w.z; wd[3] = w.w;
-        } else {
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                uint32_t x = 0;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int64_t qq = q + 4 * t + j;
-                    const uint32_t b = (qq >= 0 && qq < nb) ? a.reads[qq] : (uint32_t)'N';
-                    x |= b << (8 * j);
-                }
-                wd[t] = x;
-            }
-        }
-        uint32_t packed = 0, invbits = 0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const uint32_t c = wd[t] & 0xDFDFDFDFu;
-            const uint32_t ok = __vcmpeq4(c, 0x41414141u) | __vcmpeq4(c, 0x43434343u) | __vcmpeq4(c, 0x47474747u) |
-                                __vcmpeq4(c, 0x54545454u);
-            const uint32_t cd = ((c >> 1) ^ (c >> 2)) & 0x03030303u;  // per byte: A0 C1 G2 T3
-            const uint32_t b8 = ((cd & 0xFFu) << 6) | (((cd >> 8) & 0xFFu) << 4) | (((cd >> 16) & 0xFFu) << 2) |
-                                (cd >> 24);
-            packed |= b8 << (24 - 8 * t);
-            const uint32_t bad = (~ok) & 0x01010101u;
-            invbits |= (((bad * 0x01020408u) >> 24) & 0xFu) << (4 * t);
-        }
-        pk[v] = packed;
-        reinterpret_cast<uint16_t*>(S.inv)[v] = (uint16_t)invbits;
-        // invalid bytes inside the tile's own window starts [LEFT, LEFT+TILE) and the stream
-        const int li = 16 * v;
-        if (li >= LEFT && li < LEFT + P1_TILE) {
-            uint32_t m = invbits;
-            if (q + 16 > nb) m &= (q >= nb) ? 0u : ((1u << (uint32_t)(nb - q)) - 1u);
-            n_invalid += __popc(m);
-        }
-    }
-    if (tid < NWD - NB / 32) {
-        S.inv[NB / 32 + tid] = 0xFFFFFFFFu;
-        S.rs[NB / 32 + tid] = 0;
-    }
-    if (tid < 8) pk[NB / 16 + tid] = 0;
-    for (int w = tid; w < NB / 32; w += P1_NT) S.rs[w] = 0;
-    __syncthreads();
-    // ---- read starts inside (lbase, lbase + NB): segment breaks
-    for (uint64_t rb = r0;; rb += P1_NT) {
-        const uint64_t r = rb + tid;
-        bool inr = false;
-        if (r <= a.n_reads) {
-            const int64_t st = (int64_t)(a.offsets[r] - a.off0) - lbase;
-            if (st < NB) {
-                inr = true;
-                if (st > 0) atomicOr(&S.rs[st >> 5], 1u << (st & 31));
-            }
-        }
-        if (!__syncthreads_or(inr && tid == P1_NT - 1)) break;
-    }
-    // ---- validity bitmasks: window i valid iff bases [i, i+k) are all valid and no read
-    //      starts in (i, i+k); p-mer j likewise over [j, j+p).  ext(x) = valid(x) & !rs(x).
-    for (int w = tid; w < NWD; w += P1_NT) S.ext[w] = ~(S.inv[w] | S.rs[w]);
-    __syncthreads();
-    // one thread per mask word: AND of ext over the next L positions from three register-
-    // held words (window: L = k-1 -> vwin; p-mer: L = p-1 -> vpm), then AND with !inv(i)
-    {
-        constexpr int NWU = NB / 32 + 1;  // words covering every window / p-mer start we use
-        for (int t = tid; t < 2 * NWU; t += P1_NT) {
-            const int w = t < NWU ? t : t - NWU;
-            const int L = t < NWU ? k - 1 : p - 1;
-            const uint32_t x0 = S.ext[w], x1 = S.ext[w + 1], x2 = S.ext[w + 2];
-            uint32_t acc = 0xFFFFFFFFu;
-            for (int o = 1; o <= L; ++o)
-                acc &= o < 32 ? __funnelshift_r(x0, x1, o) : (o == 32 ? x1 : __funnelshift_r(x1, x2, o - 32));
-            const uint32_t v = ~S.inv[w] & acc;
-            if (t < NWU) S.vwin[w] = v;
-            else S.vpm[w] = v;
-        }
-    }
-    __syncthreads();
-    // ---- S2a: canonical p-mer key of every position j:
-    //      key = min(fwd, rc) if that p-mer is valid and allowed, else the reserved 4^p (R4)
+    const int k = a.k, p = a.p, W = k - p + 1;
+    const int RW = record_words(k), maxw = record_max_windows(k);
     const uint32_t RES = 1u << (2 * p);
-    const int NBK = NB - p + 1;
-    {
-        const uint32_t pmask = (1u << (2 * p)) - 1;
-        const int top = 2 * p - 2;
-        const int b0 = tid * CH, b1 = min(NBK, b0 + CH);
-        uint32_t fwd = 0, rc = 0;
-        if (b0 < b1) {
-            for (int j = b0; j < b0 + p - 1; ++j) {
-                const uint32_t c = (pk[j >> 4] >> (30 - 2 * (j & 15))) & 3u;
-                fwd = ((fwd << 2) | c) & pmask;
-                rc = (rc >> 2) | ((3u - c) << top);
-            }
-        }
-        for (int j = b0; j < b1; ++j) {
-            const int jj = j + p - 1;
-            const uint32_t c = (pk[jj >> 4] >> (30 - 2 * (jj & 15))) & 3u;
-            fwd = ((fwd << 2) | c) & pmask;
-            rc = (rc >> 2) | ((3u - c) << top);
-            const uint32_t cn = fwd < rc ? fwd : rc;
-            const bool ok = ((S.vpm[j >> 5] >> (j & 31)) & 1u) && sig_allowed(cn, p);
-            pre[j] = ok ? cn : RES;
-        }
-        for (int j = max(b0, NBK); j < min(NB, b0 + CH); ++j) pre[j] = RES;
-    }
-    __syncthreads();
-    // ---- S2b: sliding-window minimum over W = k-p+1 consecutive p-mers (van Herk /
-    //      Gil-Werman): blocks of W; suffix minima into suf[], prefix minima in place in
-    //      pre[]; sig(i) = min(suf[i], pre[i+W-1]).
-    const int W = k - p + 1;
-    {
-        const int nblk = (NBK + W - 1) / W;
-        for (int b = tid; b < nblk; b += P1_NT) {
-            const int s0 = b * W, e = min(NBK, s0 + W);
-            uint32_t m = 0xFFFFFFFFu;
-            for (int j = e - 1; j >= s0; --j) {
-                m = min(m, pre[j]);
-                suf[j] = m;
-            }
-            m = 0xFFFFFFFFu;
-            for (int j = s0; j < e; ++j) {
-                m = min(m, pre[j]);
-                pre[j] = m;
-            }
-        }
-    }
-    __syncthreads();
-    // signature per window i in [LEFT-1, LEFT+TILE) (window q0-1 only for the run test),
-    // INV where the window is not valid (crosses a read end or holds a non-ACGT byte)
-    for (int i = LEFT - 1 + tid; i < LEFT + P1_TILE; i += P1_NT) {
-        const bool ok = (S.vwin[i >> 5] >> (i & 31)) & 1u;
-        suf[i] = ok ? min(suf[i], pre[i + W - 1]) : INV;
-    }
-    __syncthreads();
-    uint32_t* key = suf;
+    const int NK = SEG + W;  // p-mer positions y = 0..NK-1 (local 15 + y)
 
-    if (MODE == P1_MODE_DEBUG) {
-        for (int w = tid; w < P1_TILE; w += P1_NT) {
-            const int64_t q = q0 + w;
-            if (q < nb) a.dbg_sig[q] = key[LEFT + w];
-        }
-        return;
-    }
+    uint64_t l_windows = 0, l_skm = 0, l_recs = 0, l_inv = 0;
+    uint64_t blk_cur = 0, blk_end = 0;  // this warp's reserved temporary-stream slots
+    bool tmp_ok = a.tmp_recs != nullptr;
 
-    // ---- S3: super-k-mers = maximal runs of valid windows with equal signature
-    //      (Fig. 1); record runs are additionally cut at the tile edge and
-    //      into pieces of at most record_max_windows(k) windows.  Warp ballots build a
-    //      bitmask of the windows where a run cannot continue (invalid or a new start)
-    //      and a compacted list of run starts; a run's length is the distance to the
-    //      next set bit.
-    const int maxw = record_max_windows(k);
-    const int RW = record_words(k);
-    uint32_t* ebits = S.ebits;
-    uint32_t* list = pre;  // pre[] is free after the signatures are formed
-    if (tid < 8) S.cnt[tid] = 0;
-    __syncthreads();
-    uint32_t l_skm = 0;
-#pragma unroll 4
-    for (int w = 0; w < WPT; ++w) {
-        const int i = LEFT + w * P1_NT + tid;
-        const uint32_t s = key[i], prev = key[i - 1];
-        const bool valid = s != INV;
-        const bool skm = valid && prev != s;
-        const bool start = skm || (valid && i == LEFT);
-        const uint32_t bE = __ballot_sync(0xffffffffu, !valid || start);
-        const uint32_t bS = __ballot_sync(0xffffffffu, start);
-        l_skm += skm;
-        uint32_t base = 0;
-        if (lane == 0) {
-            ebits[(w * P1_NT + warp * 32) >> 5] = bE;
-            if (bS) base = atomicAdd(&S.cnt[0], (uint32_t)__popc(bS));
-        }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (start) list[base + __popc(bS & lanemask_lt())] = (uint32_t)i;
-    }
-    if (tid == 0) ebits[P1_TILE >> 5] = 1u;  // sentinel: the tile edge ends every run
-    __syncthreads();
-    const int nstarts = (int)S.cnt[0];
-    // record words of the run piece starting at smem index ii with m windows: word 0 =
-    // m (8 bits) + symbols [0,12); word u>0 = symbols [12+16(u-1), 12+16u); extracted from
-    // the packed tile by funnel shifts
-    auto pack = [&](int ii, int m, uint32_t (&wd4)[8]) {
+    const uint64_t gw = (uint64_t)blockIdx.x * SG_WARPS + warp, nw = (uint64_t)gridDim.x * SG_WARPS;
+    for (uint64_t sg = gw; sg < n_segs; sg += nw) {
+        const int64_t seg0 = (int64_t)sg * SEG;
+        const int64_t lbase = seg0 - HL;  // stream position of local base 0
+        const uint64_t r_first = a.tile_r_lo[sg];
+        // ---- A: load + encode
+        for (int t = lane; t < NBASE / 16; t += 32) {
+            const int64_t q = lbase + 16 * t;
+            uint32_t wd[4];
+            if (a.reads_aligned16 && q >= 0 && q + 16 <= nb) {
+                const uint4 v = __ldcs(reinterpret_cast<const uint4*>(a.reads + q));
+                wd[0] = v.x;
+                wd[1] = v.y;
+                wd[2] = v.z;
+                wd[3] = v.w;
+            } else {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (u >= RW) break;
-            const int b = ii + (u == 0 ? 0 : 12 + 16 * (u - 1));
-            const uint32_t x = __funnelshift_l(pk[(b >> 4) + 1], pk[b >> 4], 2 * (b & 15));
-            wd4[u] = (u == 0) ? (((uint32_t)m << 24) | (x >> 8)) : x;
-        }
-    };
-    auto run_len = [&](int i) {
-        const int pos = i - LEFT + 1;
-        int wd = pos >> 5;
-        uint32_t bits = ebits[wd] & (0xFFFFFFFFu << (pos & 31));
-        while (bits == 0) bits = ebits[++wd];
-        return (wd * 32 + __ffs(bits) - 1) - (i - LEFT);
-    };
-    uint32_t l_windows = 0, l_recs = 0;
-    for (int idx = tid; idx < nstarts; idx += P1_NT) {
-        const int i = (int)list[idx];
-        const uint32_t s = key[i];
-        const int n = run_len(i);
-        const int nrec = n <= maxw ? 1 : (n + maxw - 1) / maxw;
-        l_windows += n;
-        l_recs += nrec;
-        if (MODE == P1_MODE_HIST) {
-            atomicAdd(&a.hist_w[s], (unsigned long long)n);
-            atomicAdd(&a.hist_r[s], (uint32_t)nrec);
-        } else {
-            // ---- S5 (recompute path): write each piece as a bin record (P:L258-259:
-            //      super-k-mers "are sent to bins ... related to signatures"); bins live in
-            //      HBM.
-            const uint32_t bin = a.sig2bin[s];
-            const uint64_t base = a.bin_rec_off[bin];
-            const int j = i + n;
-            for (int ii = i; ii < j; ii += maxw) {
-                const int m = min(maxw, j - ii);
-                uint32_t wd4[8];
-                pack(ii, m, wd4);
-                const uint32_t slot = atomicAdd(&a.bin_fill[bin], 1u);
-                uint4* dst = reinterpret_cast<uint4*>(a.bins + (base + slot) * (uint64_t)RW);
-                dst[0] = make_uint4(wd4[0], wd4[1], wd4[2], wd4[3]);
-                if (RW == 8) dst[1] = make_uint4(wd4[4], wd4[5], wd4[6], wd4[7]);
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int64_t qq = q + 4 * u + j;
+                        const uint32_t b = (qq >= 0 && qq < nb) ? a.reads[qq] : (uint32_t)'N';
+                        x |= b << (8 * j);
+                    }
+                    wd[u] = x;
+                }
+            }
+            uint32_t packed, invbits;
+            encode16(wd, packed, invbits);
+            S.pk[t] = packed;
+            reinterpret_cast<uint16_t*>(S.inv)[t] = (uint16_t)invbits;
+            if (t >= 1 && t <= SEG / 16) {  // the segment's own bases: local [HL, HL + SEG)
+                uint32_t m = invbits;
+                if (q + 16 > nb) m &= (q >= nb) ? 0u : ((1u << (uint32_t)(nb - q)) - 1u);
+                l_inv += __popc(m);
             }
         }
-    }
-    if (MODE == P1_MODE_HIST) {
-        // ---- the tile's records are also appended, unbinned and tagged with their
-        //      signature, to a temporary stream; S5 then only copies them into their bins
-        if (a.tmp_recs) {
-            uint32_t tot;
-            uint32_t rpos = block_excl_sum<P1_NT, uint32_t>(l_recs, S.wsum32, &tot);
-            if (tid == 0) S.tmp_base = tot ? atomicAdd(&a.gstats[GS_TMP_RECS], (unsigned long long)tot) : 0ull;
-            __syncthreads();
-            const unsigned long long base = S.tmp_base;
-            if (base + tot <= a.tmp_cap) {
-                for (int idx = tid; idx < nstarts; idx += P1_NT) {
-                    const int i = (int)list[idx];
-                    const uint32_t s = key[i];
-                    const int j = i + run_len(i);
-                    for (int ii = i; ii < j; ii += maxw) {
-                        uint32_t wd4[8];
-                        pack(ii, min(maxw, j - ii), wd4);
-                        const uint64_t slot = base + rpos++;
-                        uint4* dst = reinterpret_cast<uint4*>(a.tmp_recs + slot * (uint64_t)RW);
-                        dst[0] = make_uint4(wd4[0], wd4[1], wd4[2], wd4[3]);
-                        if (RW == 8) dst[1] = make_uint4(wd4[4], wd4[5], wd4[6], wd4[7]);
+        if (lane < NPK - NBASE / 16) S.pk[NBASE / 16 + lane] = 0;
+        if (lane == 0) reinterpret_cast<uint16_t*>(S.inv)[NBASE / 16] = 0xFFFFu;  // NBASE = 16 mod 32
+        __syncwarp();
+        for (int w = lane; w < NMW; w += 32) {
+            const uint32_t iv = w <= NBASE / 32 ? S.inv[w] : 0xFFFFFFFFu;
+            S.inv[w] = iv;
+            S.bad[w] = iv;
+        }
+        __syncwarp();
+        // ---- B: read starts inside (lbase, lbase + NBASE)
+        for (uint64_t rb = r_first;; rb += 32) {
+            const uint64_t r = rb + lane;
+            int64_t st = NBASE;
+            if (r <= a.n_reads) {
+                st = (int64_t)(a.offsets[r] - a.off0) - lbase;
+                if (st < NBASE) atomicOr(&S.bad[st >> 5], 1u << (st & 31));
+            }
+            if (!__all_sync(0xffffffffu, st < NBASE)) break;
+        }
+        __syncwarp();
+        // validity masks by doubling (lane = word): window x valid iff base x is valid and
+        // no base in (x, x+k) is invalid or starts a read; p-mer likewise with p
+        {
+            const uint32_t g = lane < NMW ? ~S.bad[lane] : 0u;
+            const uint32_t iv = lane < NMW ? S.inv[lane] : 0xFFFFFFFFu;
+            const uint32_t vw = ~iv & shr_words(run_and(g, k - 1), 1);
+            const uint32_t vp = ~iv & shr_words(run_and(g, p - 1), 1);
+            if (lane < NMW) {
+                S.vwin[lane] = vw;
+                S.vpm[lane] = vp;
+            }
+        }
+        __syncwarp();
+        // ---- C: canonical p-mer keys at local 15 + y, y < NK, in
+        //      registers: row r, lane l holds position y = 32r + l.  key = min(fwd, rc) if the
+        //      p-mer is valid and allowed, else the reserved 4^p (R4).
+        uint32_t M[NROW];
+#pragma unroll
+        for (int r = 0; r < NROW; ++r) {
+            const int y = 32 * r + lane;
+            const int j = 15 + y;
+            uint32_t key = 0xFFFFFFFFu;
+            if (y < NK) {
+                // 16 symbols from j (p <= 16): one funnel shift of two packed words
+                const uint32_t x16 = __funnelshift_l(S.pk[(j >> 4) + 1], S.pk[j >> 4], 2 * (j & 15));
+                const uint32_t fwd = x16 >> (32 - 2 * p);
+                const uint32_t rc = rev2_32(~fwd) >> (32 - 2 * p);
+                const uint32_t cn = min(fwd, rc);
+                const bool pv = (S.vpm[j >> 5] >> (j & 31)) & 1u;
+                key = (pv && sig_allowed(cn, p)) ? cn : RES;
+            }
+            M[r] = key;
+        }
+        // ---- D: sliding minimum over W keys with warp shuffles (doubling): after the step
+        //      with shift s, M(y) = min over [y, y + 2s); the window [y, y + W) is covered by
+        //      two ranges of length A = 2^floor(log2 W): min(M_A(y), M_A(y + W - A))
+        auto shift_min = [&](uint32_t (&X)[NROW], int sft, uint32_t (&out)[NROW]) {
+            const int src = (lane + sft) & 31;
+            const bool hi = lane + sft >= 32;
+#pragma unroll
+            for (int r = 0; r < NROW; ++r) {
+                const uint32_t a0 = __shfl_sync(0xffffffffu, X[r], src);
+                const uint32_t a1 = __shfl_sync(0xffffffffu, r + 1 < NROW ? X[r + 1] : 0xFFFFFFFFu, src);
+                out[r] = min(X[r], hi ? a1 : a0);
+            }
+        };
+        int A = 1;
+        while (2 * A <= W) {
+            if (A == 32) {
+#pragma unroll
+                for (int r = 0; r < NROW; ++r) M[r] = min(M[r], r + 1 < NROW ? M[r + 1] : 0xFFFFFFFFu);
+            } else {
+                shift_min(M, A, M);
+            }
+            A *= 2;
+        }
+        if (W > A) shift_min(M, W - A, M);  // W - A < A <= 32
+        // ---- E: signature of window local 15 + y (y <= SEG), INV where the window is not
+        //      valid (crosses a read start or holds a non-ACGT base)
+#pragma unroll
+        for (int r = 0; r < NROW; ++r) {
+            const int y = 32 * r + lane;
+            if (y <= SEG) {
+                const int i = 15 + y;
+                const bool ok = (S.vwin[i >> 5] >> (i & 31)) & 1u;
+                S.sig[y] = ok ? M[r] : INV;
+            }
+        }
+        __syncwarp();
+        auto sig = [&](int y) { return S.sig[y]; };
+        if (MODE == P1_MODE_DEBUG) {
+            for (int v = lane; v < SEG; v += 32)  // window seg0 + v = local y = v + 1
+                if (seg0 + v < nb) a.dbg_sig[seg0 + v] = sig(v + 1);
+            __syncwarp();
+            continue;
+        }
+        // ---- F: super-k-mers = maximal runs of valid windows with equal signature
+        //      (Fig. 1); records are additionally cut at the segment edge and into
+        //      pieces of at most maxw windows
+        uint32_t* list = S.list;
+        int nstarts = 0;
+#pragma unroll 4
+        for (int r = 0; r < SEG / 32; ++r) {
+            const int v = 32 * r + lane;
+            const uint32_t s = sig(v + 1), prev = sig(v);
+            const bool valid = s != INV;
+            const bool skm = valid && prev != s;
+            const bool start = skm || (valid && v == 0);
+            const uint32_t bE = __ballot_sync(0xffffffffu, !valid || start);
+            const uint32_t bS = __ballot_sync(0xffffffffu, start);
+            l_skm += skm;
+            if (lane == 0) S.ebits[r] = bE;
+            if (start) list[nstarts + __popc(bS & ltm)] = (uint32_t)v;
+            nstarts += __popc(bS);
+        }
+        if (lane == 0) S.ebits[SEG / 32] = 1u;  // sentinel: the segment edge ends every run
+        __syncwarp();
+        for (int i0 = 0; i0 < nstarts; i0 += 32) {
+            const int idx = i0 + lane;
+            uint32_t s = INV;
+            int v = 0, n = 0, nrec = 0;
+            if (idx < nstarts) {
+                v = (int)list[idx];
+                s = sig(v + 1);
+                const int pos = v + 1;
+                int wd = pos >> 5;
+                uint32_t bits = S.ebits[wd] & (0xFFFFFFFFu << (pos & 31));
+                while (bits == 0) bits = S.ebits[++wd];
+                n = (wd * 32 + __ffs(bits) - 1) - v;
+                nrec = (n + maxw - 1) / maxw;
+                l_windows += n;
+                l_recs += nrec;
+            }
+            if (MODE == P1_MODE_HIST && idx < nstarts) {
+                atomicAdd(&a.hist_w[s], (unsigned long long)n);
+                atomicAdd(&a.hist_r[s], (uint32_t)nrec);
+            }
+            // slots: temporary stream (pass 1) from the warp's reserved block, or the bins
+            uint64_t slot0 = 0;
+            if (MODE == P1_MODE_HIST && tmp_ok) {
+                const uint32_t inc = warp_incl_sum((uint32_t)nrec);
+                const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+                if (blk_cur + tot > blk_end) {
+                    // close the current block (unused slots carry no signature) and reserve anew
+                    for (uint64_t q = blk_cur + lane; q < blk_end; q += 32) a.tmp_sig[q] = INV;
+                    unsigned long long nbase = 0;
+                    if (lane == 0) nbase = atomicAdd(&a.gstats[GS_TMP_RECS], (unsigned long long)TMP_BLK);
+                    nbase = __shfl_sync(0xffffffffu, nbase, 0);
+                    blk_cur = nbase;
+                    blk_end = nbase + TMP_BLK;
+                    if (blk_end > a.tmp_cap) tmp_ok = false;  // overflow: the host recomputes (S5)
+                }
+                slot0 = blk_cur + inc - nrec;
+                blk_cur += tot;
+            }
+            if (idx < nstarts && (MODE == P1_MODE_SCATTER || tmp_ok)) {
+                const int j = v + n;
+                uint32_t bin = 0;
+                uint64_t bbase = 0;
+                if (MODE == P1_MODE_SCATTER) {
+                    bin = a.sig2bin[s];
+                    bbase = a.bin_rec_off[bin];
+                }
+                for (int ii = v; ii < j; ii += maxw) {
+                    const int m = min(maxw, j - ii);
+                    // record words: word 0 = m (8 bits) + symbols [0, 12); word u > 0 =
+                    // symbols [12 + 16(u-1), 12 + 16u) -- from the packed segment by funnel shifts
+                    const int b0 = HL + ii;  // local base of the piece's first window
+                    uint32_t wd[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (u >= RW) break;
+                        const int bb = b0 + (u == 0 ? 0 : 12 + 16 * (u - 1));
+                        const uint32_t x = __funnelshift_l(S.pk[(bb >> 4) + 1], S.pk[bb >> 4], 2 * (bb & 15));
+                        wd[u] = (u == 0) ? (((uint32_t)m << 24) | (x >> 8)) : x;
+                    }
+                    uint64_t slot;
+                    uint32_t* dstb;
+                    if (MODE == P1_MODE_SCATTER) {
+                        slot = bbase + atomicAdd(&a.bin_fill[bin], 1u);
+                        dstb = a.bins;
+                    } else {
+                        slot = slot0++;
+                        dstb = a.tmp_recs;
                         a.tmp_sig[slot] = s;
                     }
+                    uint4* dst = reinterpret_cast<uint4*>(dstb + slot * (uint64_t)RW);
+                    dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                    if (RW == 8) dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
                 }
             }
         }
-        const uint32_t tw = __reduce_add_sync(0xffffffffu, l_windows);
-        const uint32_t ts = __reduce_add_sync(0xffffffffu, l_skm);
-        const uint32_t tr = __reduce_add_sync(0xffffffffu, l_recs);
-        const uint32_t ti = __reduce_add_sync(0xffffffffu, n_invalid);
-        if (lane == 0) {
-            atomicAdd(&S.cnt[1], tw);
-            atomicAdd(&S.cnt[2], ts);
-            atomicAdd(&S.cnt[3], tr);
-            atomicAdd(&S.cnt[4], ti);
-        }
-        __syncthreads();
-        if (tid == 0) {
-            if (S.cnt[1]) atomicAdd(&a.gstats[GS_WINDOWS], (unsigned long long)S.cnt[1]);
-            if (S.cnt[2]) atomicAdd(&a.gstats[GS_SUPERKMERS], (unsigned long long)S.cnt[2]);
-            if (S.cnt[3]) atomicAdd(&a.gstats[GS_RECORDS], (unsigned long long)S.cnt[3]);
-            if (S.cnt[4]) atomicAdd(&a.gstats[GS_INVALID], (unsigned long long)S.cnt[4]);
-        }
+        __syncwarp();
+    }
+    if (MODE == P1_MODE_DEBUG) return;
+    if (MODE == P1_MODE_HIST && tmp_ok)
+        for (uint64_t q = blk_cur + lane; q < blk_end; q += 32) a.tmp_sig[q] = INV;
+    // ---- per-warp statistics (one atomic per counter and warp)
+    auto wsum64 = [](uint64_t v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+    const uint64_t tw = wsum64(l_windows), ts = wsum64(l_skm), tr = wsum64(l_recs), ti = wsum64(l_inv);
+    if (lane == 0) {
+        if (tw) atomicAdd(&a.gstats[GS_WINDOWS], (unsigned long long)tw);
+        if (ts) atomicAdd(&a.gstats[GS_SUPERKMERS], (unsigned long long)ts);
+        if (tr) atomicAdd(&a.gstats[GS_RECORDS], (unsigned long long)tr);
+        if (ti) atomicAdd(&a.gstats[GS_INVALID], (unsigned long long)ti);
     }
 }
 
 // S5 from the temporary stream: every record is copied into its bin (signature -> bin
-// map of the plan); one atomic per (warp, bin) reserves the slots.  Each thread carries
-// BS_U records through the dependent steps (signature -> bin -> slot -> copy) together,
-// so BS_U independent memory round trips are in flight per step instead of one.
+// map of the plan); one global atomic per record reserves its slot.  Slots whose signature
+// is INV are unused block tails.  Each thread carries BS_U records through the dependent
+// steps (signature -> bin -> slot -> copy) together.
 constexpr int BS_NT = 256, BS_U = 4;
 __global__ void __launch_bounds__(BS_NT) k_bin_scatter(const uint32_t* __restrict__ tmp_recs,
                                                        const uint32_t* __restrict__ tmp_sig, uint64_t n, int RW,
                                                        const uint32_t* __restrict__ sig2bin,
                                                        const uint64_t* __restrict__ bin_rec_off,
                                                        uint32_t* __restrict__ bin_fill, uint32_t* __restrict__ bins) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t ltm = lanemask_lt();
     constexpr uint64_t STEP = (uint64_t)BS_NT * BS_U;
     for (uint64_t base = (uint64_t)blockIdx.x * STEP; base < n; base += (uint64_t)gridDim.x * STEP) {
         uint32_t bin[BS_U];
@@ -383,8 +389,8 @@ __global__ void __launch_bounds__(BS_NT) k_bin_scatter(const uint32_t* __restric
 #pragma unroll
         for (int u = 0; u < BS_U; ++u) {
             const uint64_t i = base + (uint64_t)u * BS_NT + threadIdx.x;
-            bin[u] = i < n ? __ldcs(tmp_sig + i) : 0xFFFFFFFFu;
-            if (i < n) {
+            bin[u] = i < n ? __ldcs(tmp_sig + i) : INV;
+            if (bin[u] != INV) {
                 const uint4* src = reinterpret_cast<const uint4*>(tmp_recs + i * (uint64_t)RW);
                 r0[u] = __ldcs(src);
                 if (RW == 8) r1[u] = __ldcs(src + 1);
@@ -392,21 +398,15 @@ __global__ void __launch_bounds__(BS_NT) k_bin_scatter(const uint32_t* __restric
         }
 #pragma unroll
         for (int u = 0; u < BS_U; ++u)
-            if (bin[u] != 0xFFFFFFFFu) bin[u] = sig2bin[bin[u]];
+            if (bin[u] != INV) bin[u] = sig2bin[bin[u]];
 #pragma unroll
-        for (int u = 0; u < BS_U; ++u) {
-            const uint32_t peers = __match_any_sync(0xffffffffu, bin[u]);
-            const uint32_t leader = __ffs(peers) - 1;
-            uint32_t b = 0;
-            if (bin[u] != 0xFFFFFFFFu && lane == leader) b = atomicAdd(&bin_fill[bin[u]], (uint32_t)__popc(peers));
-            slot[u] = (uint64_t)__shfl_sync(0xffffffffu, b, leader) + __popc(peers & ltm);
-        }
+        for (int u = 0; u < BS_U; ++u) slot[u] = bin[u] != INV ? atomicAdd(&bin_fill[bin[u]], 1u) : 0u;
 #pragma unroll
         for (int u = 0; u < BS_U; ++u)
-            if (bin[u] != 0xFFFFFFFFu) slot[u] += bin_rec_off[bin[u]];
+            if (bin[u] != INV) slot[u] += bin_rec_off[bin[u]];
 #pragma unroll
         for (int u = 0; u < BS_U; ++u) {
-            if (bin[u] == 0xFFFFFFFFu) continue;
+            if (bin[u] == INV) continue;
             uint4* dst = reinterpret_cast<uint4*>(bins + slot[u] * (uint64_t)RW);
             dst[0] = r0[u];
             if (RW == 8) dst[1] = r1[u];
@@ -420,9 +420,23 @@ __global__ void k_debug_allowed(int p, uint8_t* out) {
         out[i] = sig_allowed((uint32_t)i, p) ? 1 : 0;
 }
 
+template <int MODE> cudaError_t launch_sig_t(const P1Args& a, uint64_t n_segs, cudaStream_t s) {
+    const int sm = (int)(sizeof(WarpSmem) * SG_WARPS);
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_sig<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+    int dev = 0, nsm = 148, per = 1;
+    if ((e = cudaGetDevice(&dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sig<MODE>, SG_NT, sm))) return e;
+    const uint64_t want = (n_segs + SG_WARPS - 1) / SG_WARPS;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)nsm * std::max(1, per)));
+    k_sig<MODE><<<grid, SG_NT, sm, s>>>(a, n_segs);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
-uint64_t p1_num_tiles(uint64_t n_bases) { return (n_bases + P1_TILE - 1) / P1_TILE; }
+uint64_t p1_num_tiles(uint64_t n_bases) { return (n_bases + SEG - 1) / SEG; }
 
 cudaError_t launch_tile_reads(const uint64_t* offsets, uint64_t n_reads, uint64_t off0, uint64_t n_tiles,
                               uint64_t* tile_r_lo, cudaStream_t s) {
@@ -433,20 +447,9 @@ cudaError_t launch_tile_reads(const uint64_t* offsets, uint64_t n_reads, uint64_
 
 cudaError_t launch_p1(int mode, const P1Args& a, uint64_t n_tiles, cudaStream_t s) {
     if (n_tiles == 0) return cudaSuccess;
-    dim3 grid((unsigned)n_tiles);
-    const int sm = (int)sizeof(P1Smem);
-    cudaError_t e;
-    if (mode == P1_MODE_HIST) {
-        if ((e = cudaFuncSetAttribute(k_pass<P1_MODE_HIST>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-        k_pass<P1_MODE_HIST><<<grid, P1_NT, sm, s>>>(a);
-    } else if (mode == P1_MODE_SCATTER) {
-        if ((e = cudaFuncSetAttribute(k_pass<P1_MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-        k_pass<P1_MODE_SCATTER><<<grid, P1_NT, sm, s>>>(a);
-    } else {
-        if ((e = cudaFuncSetAttribute(k_pass<P1_MODE_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-        k_pass<P1_MODE_DEBUG><<<grid, P1_NT, sm, s>>>(a);
-    }
-    return cudaGetLastError();
+    if (mode == P1_MODE_HIST) return launch_sig_t<P1_MODE_HIST>(a, n_tiles, s);
+    if (mode == P1_MODE_SCATTER) return launch_sig_t<P1_MODE_SCATTER>(a, n_tiles, s);
+    return launch_sig_t<P1_MODE_DEBUG>(a, n_tiles, s);
 }
 
 cudaError_t launch_bin_scatter(const uint32_t* tmp_recs, const uint32_t* tmp_sig, uint64_t n, int k,

@@ -49,9 +49,7 @@ __global__ void __launch_bounds__(OR_NT) k_order_count(const K* __restrict__ key
     const uint32_t lane = threadIdx.x & 31;
     for (uint64_t base = (uint64_t)blockIdx.x * OR_NT; base < n; base += (uint64_t)gridDim.x * OR_NT) {
         const uint64_t i = base + threadIdx.x;
-        const uint32_t d = i < n ? hi_digit(keys[i], twok, D) : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        if (d != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&cnt[d], (uint32_t)__popc(peers));
+        if (i < n) atomicAdd(&cnt[hi_digit(keys[i], twok, D)], 1u);
     }
 }
 
@@ -77,13 +75,7 @@ __global__ void __launch_bounds__(OR_NT) k_order_scatter(const K* __restrict__ k
             }
         }
 #pragma unroll
-        for (int u = 0; u < OS_U; ++u) {
-            const uint32_t peers = __match_any_sync(0xffffffffu, d[u]);
-            const uint32_t leader = __ffs(peers) - 1;
-            uint32_t b = 0;
-            if (d[u] != 0xFFFFFFFFu && lane == leader) b = atomicAdd(&cursor[d[u]], (uint32_t)__popc(peers));
-            slot[u] = __shfl_sync(0xffffffffu, b, leader) + __popc(peers & ltm);
-        }
+        for (int u = 0; u < OS_U; ++u) slot[u] = d[u] != 0xFFFFFFFFu ? atomicAdd(&cursor[d[u]], 1u) : 0u;
 #pragma unroll
         for (int u = 0; u < OS_U; ++u) {
             if (d[u] == 0xFFFFFFFFu) continue;

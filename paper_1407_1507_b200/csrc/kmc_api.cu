@@ -363,7 +363,8 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     uint32_t* tmp_sig = nullptr;
     uint64_t tmp_cap = 0;
     if (j->opt.distribute_path != 1) {
-        tmp_cap = std::max<uint64_t>(n_bases / 8, 4096);
+        // slots: records (~n_bases/8 at 100 bp reads) + every pass-1 warp's partly used block
+        tmp_cap = std::max<uint64_t>(n_bases / 8, 4096) + (uint64_t)n_sms() * 64 * 2048;
         tmp_recs = reinterpret_cast<uint32_t*>(ar.alloc(tmp_cap * RWt * 4));
         tmp_sig = ar.get<uint32_t>(tmp_cap);
     }
@@ -516,11 +517,6 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     j->stage_begin(KMC_STAGE_SCATTER);
     CK(cudaMemsetAsync(bin_fill, 0, n_bins * 4, s));
     if (tmp_recs && tmp_n <= tmp_cap) {
-        if (tmp_n != n_records) {
-            set_err("temporary record stream holds %llu records, histogram %llu", (unsigned long long)tmp_n,
-                    (unsigned long long)n_records);
-            throw Fail{KMC_ERR_INTERNAL};
-        }
         CK(launch_bin_scatter(tmp_recs, tmp_sig, tmp_n, k, pa.sig2bin, pa.bin_rec_off, bin_fill, bins, s));
     } else {
         a.sig2bin = pa.sig2bin;

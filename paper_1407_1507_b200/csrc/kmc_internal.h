@@ -19,13 +19,12 @@ enum {
     GS_SURV = 7,        // survivor cursor
     GS_LARGE_KEYS = 8,  // large-bin key cursor
     GS_SIGS_USED = 9,
-    GS_TMP_RECS = 10,   // records appended to the temporary stream by pass 1
+    GS_TMP_RECS = 10,   // slots reserved in the temporary record stream by pass 1
     GS_N = 16
 };
 
 // ------------------------------------------------------------ phase 1 (distribution)
-constexpr int P1_TILE = 4096;  // window starts per CTA
-constexpr int P1_NT = 256;
+constexpr int P1_SEG = 512;  // window starts per pass-1 warp segment (the "tile" of tile_r_lo)
 
 struct P1Args {
     const uint8_t* reads;
@@ -35,7 +34,7 @@ struct P1Args {
     uint64_t n_bases;
     int k, p;
     int reads_aligned16;
-    const uint64_t* tile_r_lo;  // first read index whose start lies after each tile's left edge
+    const uint64_t* tile_r_lo;  // first read index whose start lies after each segment's left edge
     // pass 1
     unsigned long long* hist_w;  // [4^p + 1]
     uint32_t* hist_r;            // [4^p + 1]
@@ -48,7 +47,7 @@ struct P1Args {
     // pass 1: temporary record stream (nullptr = not used)
     uint32_t* tmp_recs;
     uint32_t* tmp_sig;
-    uint64_t tmp_cap;  // records
+    uint64_t tmp_cap;  // records (slots; warps reserve blocks of slots, unused ones get signature INV)
     // debug
     uint32_t* dbg_sig;
 };

@@ -227,20 +227,20 @@ __global__ void __launch_bounds__(NTT, 1) k_whash(const uint64_t* keys, const Ch
 
 
 // ---- TMA-prefetched, persistent CTA hash count (1 CTA/SM, double-buffered chunk staging)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(m)), "r"(cnt) : "memory");
+__device__ __forceinline__ uint32_t ub_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ub_mbar_init(uint64_t* m, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ub_smem_u32(m)), "r"(cnt) : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(m)), "r"(bytes) : "memory");
+__device__ __forceinline__ void ub_mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(ub_smem_u32(m)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+                 :: "r"(ub_smem_u32(dst)), "l"(src), "r"(bytes), "r"(ub_smem_u32(m)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+__device__ __forceinline__ void ub_mbar_wait(uint64_t* m, uint32_t parity) {
     asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}"
-                 :: "r"(smem_u32(m)), "r"(parity) : "memory");
+                 :: "r"(ub_smem_u32(m)), "r"(parity) : "memory");
 }
 
 template <int NTT, int TSMAX>
@@ -262,12 +262,12 @@ __global__ void __launch_bounds__(NTT, 1) k_hash_tma(const uint64_t* keys, const
         const Chunk ch = chunks[cc];
         const uint64_t a0 = ch.begin & ~1ull;  // 16-byte aligned start
         const uint32_t bytes = (uint32_t)(((ch.begin + ch.n - a0) * 8 + 15) & ~15ull);
-        mbar_expect_tx(mbar + b, bytes);
+        ub_mbar_expect_tx(mbar + b, bytes);
         bulk_g2s(S[b], keys + a0, bytes, mbar + b);
     };
     if (threadIdx.x == 0) {
-        mbar_init(mbar, 1);
-        mbar_init(mbar + 1, 1);
+        ub_mbar_init(mbar, 1);
+        ub_mbar_init(mbar + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(NTT, 1) k_hash_tma(const uint64_t* keys, const
         int lg = 6;
         while ((1 << lg) < n + n / 3) ++lg;
         const int TS = 1 << lg;
-        mbar_wait(mbar + b, (it >> 1) & 1);
+        ub_mbar_wait(mbar + b, (it >> 1) & 1);
         const uint64_t* src = S[b] + off;
         for (int i = threadIdx.x; i < n; i += NTT) {
             const uint64_t key = src[i];
