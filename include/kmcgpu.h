@@ -110,6 +110,7 @@ typedef struct {
     uint64_t chunk_capacity;   /* max keys per large-bin chunk (set from the measured distinct ratio) */
     uint64_t n_overflow_chunks;/* chunks whose distinct keys overflowed the SMEM hash table
                                   (counted by the device radix-sort fallback instead) */
+    uint64_t n_order_oversize; /* survivors in S9 buckets above one chunk (sorted by the device LSD) */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;

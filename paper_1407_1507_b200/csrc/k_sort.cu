@@ -652,13 +652,10 @@ __global__ void __launch_bounds__(SB_NT, 2) k_chunk_sort(const K* __restrict__ k
 constexpr int CH_NT = 1024;
 constexpr int PROBE_MAX = 256;
 template <class K> struct HashCfg;
-template <> struct HashCfg<uint64_t> { static constexpr int slots = 16384, sub = 1024, nbuf = 4; };
-template <> struct HashCfg<K128> { static constexpr int slots = 8192, sub = 512, nbuf = 4; };
+template <> struct HashCfg<uint64_t> { static constexpr int slots = 16384; };
+template <> struct HashCfg<K128> { static constexpr int slots = 8192; };
 
-template <class K> constexpr size_t chunk_hash_smem() {
-    return (size_t)HashCfg<K>::slots * (sizeof(K) + 4) +
-           (size_t)HashCfg<K>::nbuf * ((size_t)HashCfg<K>::sub * sizeof(K) + 16) + 2 * 8 * HashCfg<K>::nbuf + 16;
-}
+template <class K> constexpr size_t chunk_hash_smem() { return (size_t)HashCfg<K>::slots * (sizeof(K) + 4); }
 
 // Counts key; false if no slot was found within PROBE_MAX probes (table too full).
 template <class K>
@@ -691,22 +688,16 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
                                                          uint32_t* sc, unsigned long long* gstats,
                                                          Chunk* __restrict__ overflow,
                                                          unsigned long long* __restrict__ n_overflow) {
-    // warp CW (the last) is the producer: it streams the sub-pieces of this CTA's chunks into
-    // the NBUF staging buffers (full[b] completes on the TMA byte count, empty[b] when every
-    // consumer warp has released the buffer).  Warps 0..CW-1 consume: insert, then -- per
-    // chunk, behind a named barrier among consumers only -- emit and clear the table.
-    constexpr int TSMAX = HashCfg<K>::slots, SUB = HashCfg<K>::sub, NBUF = HashCfg<K>::nbuf;
-    constexpr int CW = CH_NT / 32 - 1, CT = CW * 32;  // consumer warps / threads
-    constexpr int PAD = 16 / sizeof(K) > 1 ? 16 / sizeof(K) : 1;  // keys per 16 bytes
-    constexpr int BUFK = SUB + PAD;                                 // keys per staging buffer
+    // Keys stream straight from HBM into registers: thread t takes the chunk's keys
+    // t, t + CH_NT, ...; UNR of them are in flight while the previous UNR are inserted, and
+    // the next chunk's first UNR are issued before the table of the current one is scanned.
+    constexpr int TSMAX = HashCfg<K>::slots, UNR = sizeof(K) == 8 ? 4 : 2;
+    constexpr int NW = CH_NT / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     K* T = reinterpret_cast<K*>(smem);
     uint32_t* C = reinterpret_cast<uint32_t*>(T + TSMAX);
-    K* SB = reinterpret_cast<K*>(C + TSMAX);
-    uint64_t* full = reinterpret_cast<uint64_t*>(SB + NBUF * BUFK);
-    uint64_t* empty = full + NBUF;
-    __shared__ uint32_t wk[CW];
-    __shared__ unsigned long long wb[CW];
+    __shared__ uint32_t wk[NW];
+    __shared__ unsigned long long wb[NW];
     __shared__ int ovf;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ltm = lanemask_lt();
@@ -715,82 +706,63 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
         T[i] = E;
         C[i] = 0;
     }
-    if (threadIdx.x == 0) {
-        for (int b = 0; b < NBUF; ++b) {
-            mbar_init(full + b, 1);
-            mbar_init(empty + b, CW);
-        }
-        mbar_init_fence();
-        ovf = 0;
-    }
+    if (threadIdx.x == 0) ovf = 0;
     __syncthreads();
-    auto nsub_of = [&](const Chunk& ch) {
-        const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
-        return (uint32_t)((ch.begin + ch.n - a0 + SUB - 1) / SUB);
-    };
-    if (warp == CW) {
-        // ---- producer
-        if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();
-            uint32_t g = 0;
-            for (uint32_t cc = blockIdx.x; cc < n_chunks; cc += gridDim.x) {
-                const Chunk ch = chunks[cc];
-                const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
-                const uint32_t nsub = nsub_of(ch);
-                for (uint32_t q = 0; q < nsub; ++q, ++g) {
-                    const int b = g % NBUF;
-                    if (g >= NBUF) mbar_wait(empty + b, ((g / NBUF) - 1) & 1);
-                    const uint64_t s0 = a0 + (uint64_t)q * SUB;
-                    const uint64_t s1 = min(s0 + SUB, ch.begin + ch.n);
-                    const uint32_t bytes = (uint32_t)(((s1 - s0) * sizeof(K) + 15) & ~(uint64_t)15);
-                    fence_proxy_async_smem();
-                    mbar_expect_tx(full + b, bytes);
-                    tma_load_1d_hint(SB + b * BUFK, keys + s0, bytes, full + b, pol);
-                }
-            }
+    const int t = threadIdx.x;
+    auto fetch = [&](const Chunk& ch, uint32_t u0, K (&buf)[UNR]) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t i = t + (u0 + u) * CH_NT;
+            if (i < ch.n) buf[u] = ld_stream(keys + ch.begin + i);
         }
-        return;
-    }
-    // ---- consumers
-    const int ct = threadIdx.x;
+    };
     uint32_t uniq = 0, below = 0, above = 0;
-    uint32_t g = 0;
+    K cur[UNR], nxt[UNR];
+    Chunk ch{};
+    if (blockIdx.x < n_chunks) {
+        ch = chunks[blockIdx.x];
+        fetch(ch, 0, cur);
+    }
     for (uint32_t cc = blockIdx.x; cc < n_chunks; cc += gridDim.x) {
-        const Chunk ch = chunks[cc];
-        const uint64_t a0 = ch.begin & ~(uint64_t)(PAD - 1);
-        const uint32_t nsub = nsub_of(ch);
         const uint32_t want = ch.n + ch.n / 3 < (uint32_t)TSMAX ? ch.n + ch.n / 3 : (uint32_t)TSMAX;
         int lg = 6;
         while ((1u << lg) < want) ++lg;
         const int TS = 1 << lg;
+        const uint32_t per = (ch.n + CH_NT - 1) / CH_NT;  // keys per thread (rounded up)
         bool ok = true;
-        for (uint32_t q = 0; q < nsub; ++q, ++g) {
-            const int b = g % NBUF;
-            mbar_wait(full + b, (g / NBUF) & 1);
-            const uint64_t s0 = a0 + (uint64_t)q * SUB;
-            const uint64_t lo = max(s0, ch.begin), hi = min(s0 + SUB, ch.begin + ch.n);
-            const K* src = SB + b * BUFK + (lo - s0);
-            const int cnt = (int)(hi - lo);
-            for (int i = ct; i < cnt; i += CT) ok &= table_insert_bounded<K>(T, C, lg, src[i]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + b);
+        for (uint32_t u0 = 0; u0 < per; u0 += UNR) {
+            if (u0 + UNR < per) fetch(ch, u0 + UNR, nxt);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t i = t + (u0 + u) * CH_NT;
+                if (i < ch.n) ok &= table_insert_bounded<K>(T, C, lg, cur[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) cur[u] = nxt[u];
         }
         if (!ok) ovf = 1;
-        named_bar_sync(1, CT);
+        // the next chunk's first keys are in flight while this table is scanned
+        const Chunk done = ch;
+        const uint32_t cn = cc + gridDim.x;
+        if (cn < n_chunks) {
+            ch = chunks[cn];
+            fetch(ch, 0, cur);
+        }
+        __syncthreads();
         if (ovf) {
             // too many distinct keys for the table: drop the partial counts, list the chunk
-            if (ct == 0) overflow[atomicAdd(n_overflow, 1ull)] = ch;
-            for (int s = ct; s < TS; s += CT) {
+            if (t == 0) overflow[atomicAdd(n_overflow, 1ull)] = done;
+            for (int s = t; s < TS; s += CH_NT) {
                 T[s] = E;
                 C[s] = 0;
             }
-            named_bar_sync(1, CT);
-            if (ct == 0) ovf = 0;
-            named_bar_sync(1, CT);
+            __syncthreads();
+            if (t == 0) ovf = 0;
+            __syncthreads();
             continue;
         }
         uint32_t keep = 0;
-        for (int s = ct; s < TS; s += CT) {
+        for (int s = t; s < TS; s += CH_NT) {
             const uint32_t c = C[s];
             if (c) {
                 ++uniq;
@@ -801,20 +773,19 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
         }
         keep = __reduce_add_sync(0xffffffffu, keep);
         if (lane == 0) wk[warp] = keep;
-        named_bar_sync(1, CT);
+        __syncthreads();
         if (warp == 0) {
-            const uint32_t kw = lane < CW ? wk[lane] : 0u;
+            const uint32_t kw = lane < NW ? wk[lane] : 0u;
             const uint32_t inc = warp_incl_sum(kw);
             unsigned long long b0 = 0;
-            if (lane == CW - 1 && inc) b0 = atomicAdd(&gstats[GS_SURV], (unsigned long long)inc);
-            b0 = __shfl_sync(0xffffffffu, b0, CW - 1);
-            if (lane < CW) wb[lane] = b0 + inc - kw;
+            if (lane == NW - 1 && inc) b0 = atomicAdd(&gstats[GS_SURV], (unsigned long long)inc);
+            b0 = __shfl_sync(0xffffffffu, b0, NW - 1);
+            if (lane < NW) wb[lane] = b0 + inc - kw;
         }
-        named_bar_sync(1, CT);
+        __syncthreads();
         unsigned long long o = wb[warp];
-        for (int s0 = 0; s0 < TS; s0 += CT) {
-            const int s = s0 + ct;
-            const uint32_t c = s < TS ? C[s] : 0u;
+        for (int s = t; s < TS; s += CH_NT) {  // TS is a multiple of 64: whole warps iterate
+            const uint32_t c = C[s];
             const bool kp = c >= ci && c <= cx && c != 0;
             const uint32_t bb = __ballot_sync(0xffffffffu, kp);
             if (kp) {
@@ -823,12 +794,10 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
                 sc[qq] = c;
             }
             o += __popc(bb);
-            if (s < TS) {
-                T[s] = E;
-                C[s] = 0;
-            }
+            T[s] = E;
+            C[s] = 0;
         }
-        named_bar_sync(1, CT);
+        __syncthreads();
     }
     uniq = __reduce_add_sync(0xffffffffu, uniq);
     below = __reduce_add_sync(0xffffffffu, below);

@@ -155,7 +155,7 @@ unsigned long long* pin_acquire() {
         }
     }
     unsigned long long* p = nullptr;
-    if (cudaMallocHost(&p, 64 * sizeof(unsigned long long)) != cudaSuccess) {
+    if (cudaMallocHost(&p, 256 * sizeof(unsigned long long)) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
@@ -835,12 +835,13 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     uint32_t* oc = dev_out ? out_counts : ar.get<uint32_t>(n);
     const uint64_t nd = 1ull << order_digit_bits(n, j->k);
     OrderScratch os{};
-    os.cnt = ar.get<uint32_t>(nd);
+    os.hist = ar.get<uint32_t>(nd);
     os.start = ar.get<uint32_t>(nd + 1);
     os.cursor = ar.get<uint32_t>(nd);
     os.chunks = ar.get<Chunk>(nd);
     os.oversize = ar.get<Chunk>(nd);
     os.counters = ar.get<unsigned long long>(2);
+    os.tiles = ar.get<OrdTile>(order_max_tiles(n, j->k));
     os.tmp_keys = ar.alloc(n * ksz);
     os.tmp_vals = ar.get<uint32_t>(n);
     os.scan_temp = ar.alloc(order_scan_temp_bytes(nd + 1));
@@ -848,26 +849,43 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     std::vector<OrderSegment> over;
     int sl = 0;
     j->stage_begin(KMC_STAGE_ORDER);
-    CK(launch_order(kw, j->surv_keys, j->surv_counts, n, j->k, ok, oc, os, s, &sl, &over));
+    void* seg_k = nullptr;
+    uint32_t* seg_v = nullptr;
+    CK(launch_order(kw, j->surv_keys, j->surv_counts, n, j->k, ok, oc, os, s, &sl, &over, &seg_k, &seg_v));
     if (!over.empty()) {
-        uint64_t maxn = 0;
-        for (auto& g : over) maxn = std::max(maxn, g.n);
+        // oversize buckets (more survivors than one chunk): gathered into one array, sorted
+        // together by the device LSD (they are disjoint, ascending key ranges, so the sorted
+        // concatenation is every bucket sorted, in bucket order), written to their places
+        uint64_t tot = 0;
+        for (auto& g : over) tot += g.n;
+        j->st.n_order_oversize = tot;
+        void* gk = ar.alloc(tot * ksz);
+        uint32_t* gv = ar.get<uint32_t>(tot);
+        uint64_t o = 0;
+        for (auto& g : over) {
+            CK(cudaMemcpyAsync((uint8_t*)gk + o * ksz, (uint8_t*)seg_k + g.begin * ksz, g.n * ksz,
+                               cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(gv + o, seg_v + g.begin, g.n * 4, cudaMemcpyDeviceToDevice, s));
+            o += g.n;
+        }
         RadixScratch rs{};
-        rs.keys_alt = ar.alloc(maxn * ksz);
-        rs.vals_alt = ar.get<uint32_t>(maxn);
-        const uint64_t nt = (maxn + radix_tile_items(kw) - 1) / radix_tile_items(kw);
+        rs.keys_alt = ar.alloc(tot * ksz);
+        rs.vals_alt = ar.get<uint32_t>(tot);
+        const uint64_t nt = (tot + radix_tile_items(kw) - 1) / radix_tile_items(kw);
         rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
         rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
-        rs.scan_temp = ar.alloc(radix_scan_temp_bytes(maxn, kw));
+        rs.scan_temp = ar.alloc(radix_scan_temp_bytes(tot, kw));
         rs.red = ar.get<unsigned long long>(4);
         rs.red_host = j->host_small + 40;
+        void* rk = nullptr;
+        uint32_t* rv = nullptr;
+        CK(device_radix_sort(kw, gk, gv, tot, 2 * j->k, rs, s, &rk, &rv, &sl));
+        o = 0;
         for (auto& g : over) {
-            void* rk = nullptr;
-            uint32_t* rv = nullptr;
-            CK(device_radix_sort(kw, (uint8_t*)os.tmp_keys + g.begin * ksz, os.tmp_vals + g.begin, g.n, 2 * j->k, rs, s,
-                                 &rk, &rv, &sl));
-            CK(cudaMemcpyAsync((uint8_t*)ok + g.begin * ksz, rk, g.n * ksz, cudaMemcpyDeviceToDevice, s));
-            CK(cudaMemcpyAsync(oc + g.begin, rv, g.n * 4, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync((uint8_t*)ok + g.begin * ksz, (uint8_t*)rk + o * ksz, g.n * ksz, cudaMemcpyDeviceToDevice,
+                               s));
+            CK(cudaMemcpyAsync(oc + g.begin, rv + o, g.n * 4, cudaMemcpyDeviceToDevice, s));
+            o += g.n;
         }
     }
     j->launches += sl;

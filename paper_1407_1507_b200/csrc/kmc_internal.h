@@ -199,28 +199,39 @@ cudaError_t launch_rle(int key_words, const void* keys, uint64_t n, uint32_t ci,
                        uint32_t* surv_counts, unsigned long long* gstats, cudaStream_t s);
 
 // ------------------------------------------------------------ S9 global order
+// Most-significant-digit passes of <= 8 bits each, every tile of survivors sorted by its
+// digit in shared memory before it is written (coalesced runs), then one shared-memory sort
+// per chunk of consecutive buckets.
+struct OrdTile {
+    uint64_t begin;   // first item
+    uint32_t n;       // items (<= order_tile_items)
+    uint32_t bucket;  // histogram / cursor row (pass 2: the pass-1 digit)
+};
 struct OrderScratch {
-    uint32_t* cnt;          // [2^D] digit counts
-    uint32_t* start;        // [2^D + 1] exclusive scan
-    uint32_t* cursor;       // [2^D] scatter cursors
-    Chunk* chunks;          // [2^D]
-    Chunk* oversize;        // [2^D]
+    uint32_t* hist;         // [2^order_digit_bits] histogram of the current pass
+    uint32_t* start;        // [2^order_digit_bits + 1] exclusive scan of hist
+    uint32_t* cursor;       // [2^order_digit_bits] scatter cursors
+    Chunk* chunks;          // [2^order_digit_bits]
+    Chunk* oversize;        // [2^order_digit_bits]
     unsigned long long* counters;  // [2]
+    OrdTile* tiles;         // [order_max_tiles(n, k)]
     void* tmp_keys;         // [n] K
     uint32_t* tmp_vals;     // [n]
-    void* scan_temp;        // order_scan_temp_bytes(2^D)
-    unsigned long long* host;  // pinned, 2 entries
+    void* scan_temp;        // order_scan_temp_bytes(2^(D1+D2) + 1)
+    unsigned long long* host;  // pinned, >= 2 entries
 };
 struct OrderSegment {
-    uint64_t begin, n;  // in the scattered (tmp) arrays == in the output
+    uint64_t begin, n;  // items of an oversize bucket in (*seg_keys, *seg_vals) after launch_order
 };
-int order_digit_bits(uint64_t n, int k);
+int order_digit_bits(uint64_t n, int k);  // bits of all MSD passes
+uint64_t order_tile_items(int key_words);
+uint64_t order_max_tiles(uint64_t n, int k);
 size_t order_scan_temp_bytes(uint64_t n_digits);
-// Sorts (keys, vals) ascending into (out_keys, out_vals).  Segments whose digit holds more
-// than the chunk capacity are left, grouped, in os.tmp_keys/tmp_vals and returned in
-// *oversize for the caller to sort with device_radix_sort.
-cudaError_t launch_order(int key_words, const void* keys, const uint32_t* vals, uint64_t n, int k, void* out_keys,
+// Sorts (keys, vals) ascending into (out_keys, out_vals); keys/vals are used as scratch.
+// Buckets holding more than the chunk capacity are left, grouped, in (*seg_keys, *seg_vals)
+// and returned in *oversize for the caller to sort with device_radix_sort and copy out.
+cudaError_t launch_order(int key_words, void* keys, uint32_t* vals, uint64_t n, int k, void* out_keys,
                          uint32_t* out_vals, const OrderScratch& os, cudaStream_t s, int* launches,
-                         std::vector<OrderSegment>* oversize);
+                         std::vector<OrderSegment>* oversize, void** seg_keys, uint32_t** seg_vals);
 
 }  // namespace kmc
