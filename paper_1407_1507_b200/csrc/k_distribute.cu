@@ -371,47 +371,101 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
     }
 }
 
-// S5 from the temporary stream: every record is copied into its bin (signature -> bin
-// map of the plan); one global atomic per record reserves its slot.  Slots whose signature
-// is INV are unused block tails.  Each thread carries BS_U records through the dependent
-// steps (signature -> bin -> slot -> copy) together.
-constexpr int BS_NT = 256, BS_U = 4;
-__global__ void __launch_bounds__(BS_NT) k_bin_scatter(const uint32_t* __restrict__ tmp_recs,
-                                                       const uint32_t* __restrict__ tmp_sig, uint64_t n, int RW,
+// S5 from the temporary stream: the records are sorted by bin id with most-significant-digit
+// passes of <= 8 bits (the bins are laid out in bin-id order, so bucket v of a pass starts
+// at bin_rec_off[first bin of v] and the last pass writes the final bins).  Each CTA takes
+// a tile of records (within one bucket of the previous pass), sorts it by its digit in
+// shared memory and writes it as runs of consecutive records -- an unsorted scatter of
+// 16-byte records into ~10^4-10^5 bins is bound by partial-sector writes.  Pass 1 reads the
+// signature tags (INV = unused slot) and maps them to bins; later passes carry bin ids.
+constexpr int RS_NT = 512;
+template <int RW> struct RecTile { static constexpr int v = RW == 4 ? 2048 : 1024; };
+template <int RW> constexpr size_t rec_scatter_smem() {
+    return (size_t)RecTile<RW>::v * (RW * 4 + 4 + 1) + (3 * 256 + 64) * 4 + 64;
+}
+
+template <int RW>
+__global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restrict__ in_recs,
+                                                       const uint32_t* __restrict__ in_ids,
                                                        const uint32_t* __restrict__ sig2bin,
-                                                       const uint64_t* __restrict__ bin_rec_off,
-                                                       uint32_t* __restrict__ bin_fill, uint32_t* __restrict__ bins) {
-    constexpr uint64_t STEP = (uint64_t)BS_NT * BS_U;
-    for (uint64_t base = (uint64_t)blockIdx.x * STEP; base < n; base += (uint64_t)gridDim.x * STEP) {
-        uint32_t bin[BS_U];
-        uint64_t slot[BS_U];
-        uint4 r0[BS_U], r1[BS_U];
+                                                       const RecTile2* __restrict__ tiles, int shift, int D,
+                                                       unsigned long long* __restrict__ cursor,
+                                                       uint32_t* __restrict__ out_recs, uint32_t* __restrict__ out_ids) {
+    constexpr int TI = RecTile<RW>::v, IPT = TI / RS_NT;
+    using V = uint4;
+    extern __shared__ __align__(16) uint8_t rsm[];
+    V* srec = reinterpret_cast<V*>(rsm);  // TI records
+    uint32_t* sid = reinterpret_cast<uint32_t*>(srec + TI * (RW / 4));
+    uint32_t* lh = sid + TI;              // 256: counts, then local offsets
+    unsigned long long* gb = reinterpret_cast<unsigned long long*>(lh + 256);  // 256 run bases
+    uint32_t* wsum = reinterpret_cast<uint32_t*>(gb + 256);
+    uint8_t* sd = reinterpret_cast<uint8_t*>(wsum + 64);
+    __shared__ uint32_t s_tot;
+    const RecTile2 t = tiles[blockIdx.x];
+    const int nd = 1 << D;
+    for (int d = threadIdx.x; d < 256; d += RS_NT) lh[d] = 0;
+    __syncthreads();
+    V r0[IPT], r1[IPT];
+    uint32_t bin[IPT], dr[IPT];
 #pragma unroll
-        for (int u = 0; u < BS_U; ++u) {
-            const uint64_t i = base + (uint64_t)u * BS_NT + threadIdx.x;
-            bin[u] = i < n ? __ldcs(tmp_sig + i) : INV;
-            if (bin[u] != INV) {
-                const uint4* src = reinterpret_cast<const uint4*>(tmp_recs + i * (uint64_t)RW);
+    for (int u = 0; u < IPT; ++u) {
+        const uint32_t i = threadIdx.x + u * RS_NT;
+        dr[u] = INV;
+        bin[u] = INV;
+        if (i < t.n) {
+            uint32_t b = __ldcs(in_ids + t.begin + i);
+            if (sig2bin && b != INV) b = sig2bin[b];
+            if (b != INV) {
+                const V* src = reinterpret_cast<const V*>(in_recs + (t.begin + i) * (uint64_t)RW);
                 r0[u] = __ldcs(src);
                 if (RW == 8) r1[u] = __ldcs(src + 1);
+                bin[u] = b;
+                const uint32_t d = (b >> shift) & (uint32_t)(nd - 1);
+                dr[u] = (d << 16) | atomicAdd(&lh[d], 1u);  // rank < TI
             }
         }
-#pragma unroll
-        for (int u = 0; u < BS_U; ++u)
-            if (bin[u] != INV) bin[u] = sig2bin[bin[u]];
-#pragma unroll
-        for (int u = 0; u < BS_U; ++u) slot[u] = bin[u] != INV ? atomicAdd(&bin_fill[bin[u]], 1u) : 0u;
-#pragma unroll
-        for (int u = 0; u < BS_U; ++u)
-            if (bin[u] != INV) slot[u] += bin_rec_off[bin[u]];
-#pragma unroll
-        for (int u = 0; u < BS_U; ++u) {
-            if (bin[u] == INV) continue;
-            uint4* dst = reinterpret_cast<uint4*>(bins + slot[u] * (uint64_t)RW);
-            dst[0] = r0[u];
-            if (RW == 8) dst[1] = r1[u];
-        }
     }
+    __syncthreads();
+    {
+        const uint32_t c = threadIdx.x < (unsigned)nd ? lh[threadIdx.x] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_sum<RS_NT, uint32_t>(c, wsum, &tot);
+        if (threadIdx.x < (unsigned)nd) {
+            gb[threadIdx.x] =
+                c ? atomicAdd(&cursor[((uint64_t)t.bucket << D) + threadIdx.x], (unsigned long long)c) : 0ull;
+            lh[threadIdx.x] = ex;
+        }
+        if (threadIdx.x == 0) s_tot = tot;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+        if (dr[u] == INV) continue;
+        const uint32_t d = dr[u] >> 16, pos = lh[d] + (dr[u] & 0xFFFFu);
+        srec[pos * (RW / 4)] = r0[u];
+        if (RW == 8) srec[pos * 2 + 1] = r1[u];
+        sid[pos] = bin[u];
+        sd[pos] = (uint8_t)d;
+    }
+    __syncthreads();
+    const uint32_t tot = s_tot;
+    for (uint32_t i = threadIdx.x; i < tot; i += RS_NT) {
+        const uint32_t d = sd[i];
+        const uint64_t o = gb[d] + (i - lh[d]);
+        V* dst = reinterpret_cast<V*>(out_recs + o * (uint64_t)RW);
+        dst[0] = srec[i * (RW / 4)];
+        if (RW == 8) dst[1] = srec[i * 2 + 1];
+        if (out_ids) out_ids[o] = sid[i];
+    }
+}
+
+// cursor[v] = first record of bucket v = bins [v << shift, (v+1) << shift)
+__global__ void k_bucket_cursors(const uint64_t* __restrict__ bin_rec_off, uint64_t n_bins, uint64_t n_records,
+                                 int shift, uint64_t n_buckets, unsigned long long* __restrict__ cursor) {
+    const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n_buckets) return;
+    const uint64_t b = v << shift;
+    cursor[v] = b < n_bins ? bin_rec_off[b] : n_records;
 }
 
 __global__ void k_debug_allowed(int p, uint8_t* out) {
@@ -452,12 +506,32 @@ cudaError_t launch_p1(int mode, const P1Args& a, uint64_t n_tiles, cudaStream_t 
     return launch_sig_t<P1_MODE_DEBUG>(a, n_tiles, s);
 }
 
-cudaError_t launch_bin_scatter(const uint32_t* tmp_recs, const uint32_t* tmp_sig, uint64_t n, int k,
-                               const uint32_t* sig2bin, const uint64_t* bin_rec_off, uint32_t* bin_fill,
-                               uint32_t* bins, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::min<uint64_t>((n + BS_NT * BS_U - 1) / (BS_NT * BS_U), 148ull * 8);
-    k_bin_scatter<<<grid, BS_NT, 0, s>>>(tmp_recs, tmp_sig, n, record_words(k), sig2bin, bin_rec_off, bin_fill, bins);
+size_t rec_tile_items(int k) { return record_words(k) == 4 ? RecTile<4>::v : RecTile<8>::v; }
+
+cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* in_ids, const uint32_t* sig2bin,
+                               const RecTile2* tiles, uint64_t n_tiles, int shift, int D,
+                               unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids, cudaStream_t s) {
+    if (n_tiles == 0) return cudaSuccess;
+    cudaError_t e;
+    if (record_words(k) == 4) {
+        const int sm = (int)rec_scatter_smem<4>();
+        if ((e = cudaFuncSetAttribute(k_rec_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+        k_rec_scatter<4><<<(unsigned)n_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, shift, D, cursor,
+                                                             out_recs, out_ids);
+    } else {
+        const int sm = (int)rec_scatter_smem<8>();
+        if ((e = cudaFuncSetAttribute(k_rec_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+        k_rec_scatter<8><<<(unsigned)n_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, shift, D, cursor,
+                                                             out_recs, out_ids);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_cursors(const uint64_t* bin_rec_off, uint64_t n_bins, uint64_t n_records, int shift,
+                                  uint64_t n_buckets, unsigned long long* cursor, cudaStream_t s) {
+    if (n_buckets == 0) return cudaSuccess;
+    k_bucket_cursors<<<(unsigned)((n_buckets + 255) / 256), 256, 0, s>>>(bin_rec_off, n_bins, n_records, shift,
+                                                                         n_buckets, cursor);
     return cudaGetLastError();
 }
 

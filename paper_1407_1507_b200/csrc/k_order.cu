@@ -197,6 +197,7 @@ cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uin
             b0 += c;
         }
         const uint64_t nd = nbk << D[l];
+        if (tl.empty()) continue;  // (n > 0, so only a pass after an empty previous one)
         if ((e = cudaMemcpyAsync(os.tiles, tl.data(), tl.size() * sizeof(OrdTile), cudaMemcpyHostToDevice, s)))
             return e;
         if ((e = cudaMemsetAsync(os.hist, 0, nd * 4, s))) return e;
@@ -267,7 +268,11 @@ uint64_t order_tile_items(int key_words) { return key_words == 1 ? OrderTile<uin
 
 uint64_t order_max_tiles(uint64_t n, int k) {
     // at most one partial tile per bucket of the previous level beyond n / tile
-    return n / order_tile_items(k <= 32 ? 1 : 2) + (1ull << std::max(0, order_digit_bits(n, k) - 8)) + 1;
+    int D[4];
+    const int L = order_levels(n, k, k <= 32 ? OrderCap<uint64_t>::v : OrderCap<K128>::v, D);
+    int prev = 0;
+    for (int l = 0; l + 1 < L; ++l) prev += D[l];
+    return n / order_tile_items(k <= 32 ? 1 : 2) + (1ull << prev) + 1;
 }
 
 size_t order_scan_temp_bytes(uint64_t n_digits) { return scan_detail::scan_temp_elems<uint64_t>(n_digits) * 8; }

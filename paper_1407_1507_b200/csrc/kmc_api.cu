@@ -512,21 +512,69 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     // ---- S5: records into bins -- a copy from pass 1's temporary stream, or (if the stream
     //      overflowed its estimate) pass 2 = S1-S3 recomputed + scatter
     uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4));
-    uint32_t* bin_fill = ar.get<uint32_t>(n_bins);
     const uint64_t tmp_n = hs[16 + GS_TMP_RECS];
     j->stage_begin(KMC_STAGE_SCATTER);
-    CK(cudaMemsetAsync(bin_fill, 0, n_bins * 4, s));
+    int s5_launches = 0;
     if (tmp_recs && tmp_n <= tmp_cap) {
-        CK(launch_bin_scatter(tmp_recs, tmp_sig, tmp_n, k, pa.sig2bin, pa.bin_rec_off, bin_fill, bins, s));
+        // MSD passes of <= 8 bits over the bin id; the last one writes the bins
+        int B = 1;
+        while ((1ull << B) < n_bins) ++B;
+        std::vector<int> D;
+        for (int bits = 0; bits < B; bits += D.back()) D.push_back(std::min(8, B - bits));
+        const int L = (int)D.size();
+        const uint64_t TI = rec_tile_items(k);
+        unsigned long long* cursor = ar.get<unsigned long long>((1ull << B) + 1);
+        RecTile2* d_tiles = ar.get<RecTile2>(std::max(tmp_n, n_records) / TI + n_bins + 2);  // + one partial tile per bucket
+        uint32_t* x_recs = L > 1 ? reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4)) : nullptr;
+        uint32_t* x_ids = L > 1 ? ar.get<uint32_t>(n_records) : nullptr;
+        const uint32_t* in_r = tmp_recs;
+        const uint32_t* in_i = tmp_sig;
+        std::vector<RecTile2> tl;
+        int prefix = 0;
+        for (int l = 0; l < L; ++l) {
+            const int shift_prev = B - prefix;
+            prefix += D[l];
+            const int shift = B - prefix;
+            tl.clear();
+            if (l == 0) {
+                for (uint64_t o = 0; o < tmp_n; o += TI)
+                    tl.push_back(RecTile2{o, (uint32_t)std::min<uint64_t>(TI, tmp_n - o), 0});
+            } else {
+                const uint64_t nbp = (n_bins + (1ull << shift_prev) - 1) >> shift_prev;
+                for (uint64_t v = 0; v < nbp; ++v) {
+                    const uint64_t b0 = v << shift_prev, b1 = std::min<uint64_t>(n_bins, (v + 1) << shift_prev);
+                    const uint64_t r0 = bo[b0], r1 = b1 < n_bins ? bo[b1] : n_records;
+                    for (uint64_t o = r0; o < r1; o += TI)
+                        tl.push_back(RecTile2{o, (uint32_t)std::min<uint64_t>(TI, r1 - o), (uint32_t)v});
+                }
+            }
+            const uint64_t nbk = (n_bins + (1ull << shift) - 1) >> shift;
+            CK(launch_bucket_cursors(pa.bin_rec_off, n_bins, n_records, shift, nbk, cursor, s));
+            if (!tl.empty())
+                CK(cudaMemcpyAsync(d_tiles, tl.data(), tl.size() * sizeof(RecTile2), cudaMemcpyHostToDevice, s));
+            // ping-pong: the last pass writes the bins; others alternate x / tmp buffers
+            uint32_t* out_r = (l == L - 1) ? bins : ((l & 1) == 0 ? x_recs : tmp_recs);
+            uint32_t* out_i = (l == L - 1) ? nullptr : ((l & 1) == 0 ? x_ids : tmp_sig);
+            CK(launch_rec_scatter(k, in_r, in_i, l == 0 ? pa.sig2bin : nullptr, d_tiles, tl.size(), shift, D[l],
+                                  cursor, out_r, out_i, s));
+            // the pass reads from in_* while writing out_*: tmp is only an output from pass 2 on
+            in_r = out_r;
+            in_i = out_i;
+            s5_launches += 2;
+        }
+        ar.release(x_recs);
+        ar.release(x_ids);
     } else {
+        uint32_t* bin_fill = ar.get<uint32_t>(n_bins);
+        CK(cudaMemsetAsync(bin_fill, 0, n_bins * 4, s));
         a.sig2bin = pa.sig2bin;
         a.bin_rec_off = pa.bin_rec_off;
         a.bin_fill = bin_fill;
         a.bins = bins;
-        j->launches += run_p1(P1_MODE_SCATTER) - 1;
+        s5_launches = run_p1(P1_MODE_SCATTER) - 1;
     }
-    j->launches += 1;
-    j->stage_end(1);
+    j->launches += s5_launches;
+    j->stage_end(s5_launches);
     ar.release(tmp_recs);
     ar.release(tmp_sig);
     ar.release(hist_w);

@@ -59,9 +59,20 @@ cudaError_t launch_tile_reads(const uint64_t* offsets, uint64_t n_reads, uint64_
                               uint64_t* tile_r_lo, cudaStream_t s);
 cudaError_t launch_p1(int mode, const P1Args& a, uint64_t n_tiles, cudaStream_t s);
 cudaError_t launch_debug_allowed(int p, uint8_t* out, cudaStream_t s);
-cudaError_t launch_bin_scatter(const uint32_t* tmp_recs, const uint32_t* tmp_sig, uint64_t n, int k,
-                               const uint32_t* sig2bin, const uint64_t* bin_rec_off, uint32_t* bin_fill,
-                               uint32_t* bins, cudaStream_t s);
+// S5: records of the temporary stream sorted into their bins by MSD passes over the bin id
+// (k_rec_scatter).  A tile holds <= rec_tile_items(k) records of one bucket of the previous
+// pass; bucket ids of pass l are bin >> shift_l, cursors start at the buckets' first record.
+struct RecTile2 {
+    uint64_t begin;
+    uint32_t n;
+    uint32_t bucket;  // bucket of the previous pass (cursor row)
+};
+size_t rec_tile_items(int k);
+cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* in_ids, const uint32_t* sig2bin,
+                               const RecTile2* tiles, uint64_t n_tiles, int shift, int D,
+                               unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids, cudaStream_t s);
+cudaError_t launch_bucket_cursors(const uint64_t* bin_rec_off, uint64_t n_bins, uint64_t n_records, int shift,
+                                  uint64_t n_buckets, unsigned long long* cursor, cudaStream_t s);
 
 // ------------------------------------------------------------ scans / plan
 // out[0..n] exclusive prefix sums (out[n] = total) of in[0..n) (uint64).
