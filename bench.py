@@ -37,21 +37,25 @@ METRIC = "input bases/s (k-mers counted/s and HBM-roofline fraction alongside)"
 
 
 def stage_bytes(st: dict, n_reads: int, k: int) -> dict:
+    """Algorithmic HBM bytes per stage and call: what the step must read and
+    write, not what the kernels happen to move."""
     ksz = 8 if k <= 32 else 16
     rw = 16 if k <= 32 else 32
     nb = st["n_bases"]
     off = 8 * (n_reads + 1)
     rec = st["n_records"] * rw
+    tags = st["n_records"] * 4
     lw = st["large_windows"]
     nout = st["n_out"]
     lfrac = lw / st["n_windows"] if st["n_windows"] else 0.0
     small_rec = rec * (1 - lfrac)
     large_rec = rec - small_rec
     return {
-        "signature": nb + off,                               # ASCII + offsets read (histogram is noise)
-        "scatter": nb + off + rec,                           # ASCII + offsets read, records written
+        "signature": nb + off + rec + tags,                  # ASCII + offsets read; records + tags written
+        "scatter": 2 * rec + tags,                           # records + tags read, records written into bins
         "small_bins": small_rec + (1 - lfrac) * nout * (ksz + 4),  # records read, survivors written
-        "large_split": 2 * large_rec + lw * ksz,             # records read (count + scatter), keys written
+        "large_split": large_rec,                            # records read (digit counts)
+        "large_scatter": large_rec + lw * ksz,               # records read, keys written
         "large_chunks": lw * ksz + lfrac * nout * (ksz + 4),  # keys read, survivors written
         "large_fallback": 2 * lw * ksz,                      # (LSD path only) keys read + written once
         "order": 2 * nout * (ksz + 4),                       # survivors read + written once
@@ -273,7 +277,7 @@ def main():
     dom_ms = per_stage[dom]["ms"]
     achieved = sb.get(dom, 0.0) / (dom_ms / 1e3) / 1e9
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")  # written from an ncu capture
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         if tj.get("workload") == args.config and float(tj.get("scale", 0)) == args.scale and dom in tj["stages"]:
@@ -283,8 +287,8 @@ def main():
             "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
             "alg_bytes_per_launch": int(sb.get(dom, 0.0)), "ms_per_launch": dom_ms,
             "peak_source": peaks["source"],
-            "whole_step": {"alg_bytes": int(sum(v for s_, v in sb.items() if s_ in ("signature", "scatter"))),
-                           "note": "see DESIGN.md 6 for B_alg of the full pipeline"}}
+            "note": "per-stage CUDA events inside kmc_count (the stage is one kernel but for a few "
+                    "tiny scans); traffic = ncu DRAM bytes of the same kernel (profiles/r01_traffic.json)"}
     b_alg = n_bases + 8 * (w.n_reads + 1) + 2 * last["n_records"] * (16 if k <= 32 else 32) + \
         last["n_out"] * ((8 if k <= 32 else 16) + 4)
     roof["pipeline"] = {"B_alg": int(b_alg), "frac_of_step": round(b_alg / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}

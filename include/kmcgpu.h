@@ -77,15 +77,17 @@ enum {
     KMC_STAGE_SCATTER = 3,    /* S5: super-k-mer records into HBM bins (copy of pass 1's record
                                  stream, or S1-S3 recomputed as pass 2) */
     KMC_STAGE_SMALL_BINS = 4, /* S6-S8 for bins that fit one CTA: expand + SMEM radix sort + compact */
-    KMC_STAGE_LARGE_SPLIT = 5,  /* S6 + MSD step of S7 for large bins: expand, count top digits,
-                                   plan chunks, scatter keys to HBM digit ranges */
+    KMC_STAGE_LARGE_SPLIT = 5,  /* S6 + split of S7 for large bins, count half: expand, count the
+                                   hash digits per CTA range, scan, plan chunks */
     KMC_STAGE_LARGE_CHUNKS = 6, /* S7-S8 for large bins: per chunk, SMEM hash count (count_path 0)
                                    or SMEM radix sort + compaction (count_path 1) */
     KMC_STAGE_LARGE_FALLBACK = 7,/* S7-S8 for oversize digits (or all large bins with
                                    large_path=1): device-wide LSD radix sort + run-length pass */
     KMC_STAGE_ORDER = 8,      /* S9: global ascending order of survivors */
     KMC_STAGE_OUTPUT = 9,     /* copy of the sorted survivors into the caller's buffers */
-    KMC_N_STAGES = 10
+    KMC_STAGE_LARGE_SCATTER = 10, /* S6 + split of S7 for large bins, scatter half: re-expand and
+                                     place every key in its digit range in HBM */
+    KMC_N_STAGES = 11
 };
 
 typedef struct {

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libkmcgpu.so")
 
 KMC_OK, KMC_ERR_INVALID_ARG, KMC_ERR_OUT_CAPACITY, KMC_ERR_ALLOC, KMC_ERR_CUDA, KMC_ERR_INTERNAL = range(6)
 STAGES = ["input", "signature", "plan", "scatter", "small_bins", "large_split", "large_chunks",
-          "large_fallback", "order", "output"]
+          "large_fallback", "order", "output", "large_scatter"]
 
 
 class KmcError(RuntimeError):

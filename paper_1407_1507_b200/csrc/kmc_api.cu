@@ -789,9 +789,12 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             ga.counters = counters;
             ga.cap = (uint32_t)kcap;
             CK(launch_greedy_chunks(ga, gn, s));
+            j->launches += 6;
+            j->stage_end(6);
+            j->stage_begin(KMC_STAGE_LARGE_SCATTER);
             CK(launch_split(true, bins, d_pieces, n_pieces, d_lbins, k, dmax, R, tpos, lkeys, s));
-            j->launches += 7;
-            j->stage_end(7);
+            j->launches += 1;
+            j->stage_end(1);
             CK(cudaMemcpyAsync(&hs[48], counters, 16, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             const uint64_t n_chunks = hs[48], n_over = hs[49];
