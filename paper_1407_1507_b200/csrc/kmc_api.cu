@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -174,8 +175,32 @@ struct StageEv {
 
 }  // namespace
 
+// State carried between the phases of a count (pass 1 -> plan -> bins/count), so that the
+// sharded entry points (kmc_shard_*) can stop between them for the caller's exchanges.
+struct PlanCtx {
+    PlanArgs pa{};
+    uint64_t ns = 0, n_bins = 0, n_windows = 0, n_records = 0;
+    uint64_t tmp_cap = 0, tmp_n = 0;  // record stream slots (capacity, used)
+    int cap = 0;                      // small-bin capacity in keys
+    bool check_p1 = true;             // the plan must match the pass-1 counters (not when sharded)
+    unsigned long long* hist_w = nullptr;
+    uint32_t* hist_r = nullptr;
+    unsigned long long* gstats = nullptr;
+    uint32_t* tmp_recs = nullptr;
+    uint32_t* tmp_sig = nullptr;
+    std::vector<uint64_t> bw, bn, bo;  // per bin: windows, records, first record
+    P1Args a{};
+    std::function<int(int)> run_p1;  // pass-1 recompute (S5 fallback), unset when sharded
+    // sharded: bin -> owning rank
+    std::vector<uint32_t> owner;
+};
+
 struct kmc_job {
     cudaStream_t s = 0;
+    PlanCtx ctx;
+    bool shard = false;
+    int world = 1, rank = 0;
+    uint64_t n_local_records = 0;
     int k = 0, p = 0, key_words = 1;
     uint32_t ci = 1, cx = 0;
     kmc_options opt{};
@@ -279,6 +304,9 @@ void read_extent(kmc_job* j, const uint64_t* offsets, uint64_t n_reads, uint64_t
         *offN = offsets[n_reads];
     }
 }
+
+void plan_phase(kmc_job* j, PlanCtx& c);
+void count_phase(kmc_job* j, PlanCtx& c);
 
 void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads) {
     const int k = j->k, p = j->p, kw = j->key_words;
@@ -433,12 +461,44 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     j->launches += nl1;
     j->stage_end(nl1);
 
+    PlanCtx& c = j->ctx;
+    c.ns = ns;
+    c.hist_w = hist_w;
+    c.hist_r = hist_r;
+    c.gstats = gstats;
+    c.tmp_recs = tmp_recs;
+    c.tmp_sig = tmp_sig;
+    c.tmp_cap = tmp_cap;
+    c.a = a;
+    if (j->shard) return;  // sharded: the caller exchanges histograms and records (kmc_shard_*)
+    c.run_p1 = [&](int mode) {
+        a = c.a;
+        return run_p1(mode);
+    };
+    plan_phase(j, c);
+    count_phase(j, c);
+    c.run_p1 = nullptr;
+}
+
+// S4 on the histograms in c.hist_w / c.hist_r: plan arrays on the device, bin tables on the host.
+void plan_phase(kmc_job* j, PlanCtx& c) {
+    const int k = j->k, kw = j->key_words;
+    const size_t ksz = kw == 1 ? 8 : 16;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    const uint64_t ns = c.ns;
+    unsigned long long* hist_w = c.hist_w;
+    uint32_t* hist_r = c.hist_r;
+    unsigned long long* gstats = c.gstats;
+    (void)ksz;
     // ---- S4: plan
     const int RW = record_words(k);
     int cap = small_capacity(k);
     if (j->opt.small_bin_capacity) cap = std::min<int>(cap, (int)j->opt.small_bin_capacity);
     if (j->opt.force_large) cap = 0;
-    PlanArgs pa{};
+    c.cap = cap;
+    PlanArgs& pa = c.pa;
+    pa = PlanArgs{};
     pa.hist_w = hist_w;
     pa.hist_r = hist_r;
     pa.ns = ns;
@@ -467,27 +527,58 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const uint64_t n_bins = hs[0], n_windows = hs[1], n_records = hs[2];
+    c.n_bins = n_bins;
+    c.n_windows = n_windows;
+    c.n_records = n_records;
+    c.tmp_n = hs[16 + GS_TMP_RECS];
     j->st.n_windows = n_windows;
     j->st.n_superkmers = hs[16 + GS_SUPERKMERS];
     j->st.n_records = n_records;
     j->st.n_invalid_bases = hs[16 + GS_INVALID];
     j->st.n_signatures_used = hs[16 + GS_SIGS_USED];
     j->st.n_bins = n_bins;
-    if (hs[16 + GS_WINDOWS] != n_windows || hs[16 + GS_RECORDS] != n_records) {
+    if (c.check_p1 && (hs[16 + GS_WINDOWS] != n_windows || hs[16 + GS_RECORDS] != n_records)) {
         set_err("histogram totals disagree with pass-1 counters (%llu/%llu windows, %llu/%llu records)",
                 (unsigned long long)n_windows, (unsigned long long)hs[16 + GS_WINDOWS], (unsigned long long)n_records,
                 (unsigned long long)hs[16 + GS_RECORDS]);
         throw Fail{KMC_ERR_INTERNAL};
     }
-    if (n_windows == 0) {
-        j->n_surv = 0;
-        return;
-    }
-    std::vector<uint64_t> bw(n_bins), bn(n_bins), bo(n_bins);
+    if (n_windows == 0) return;
+    std::vector<uint64_t>& bw = c.bw;
+    std::vector<uint64_t>& bn = c.bn;
+    std::vector<uint64_t>& bo = c.bo;
+    bw.assign(n_bins, 0);
+    bn.assign(n_bins, 0);
+    bo.assign(n_bins, 0);
     CK(cudaMemcpyAsync(bw.data(), pa.bin_w, n_bins * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(bn.data(), pa.bin_nrec, n_bins * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(bo.data(), pa.bin_rec_off, n_bins * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+}
+
+// S5-S8 from the record stream in c (tmp_recs / tmp_sig, tmp_n slots) and the plan:
+// bins, then small and large bins counted into the survivor buffer.
+void count_phase(kmc_job* j, PlanCtx& c) {
+    const int k = j->k, kw = j->key_words;
+    const size_t ksz = kw == 1 ? 8 : 16;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    const int RW = record_words(k);
+    const int cap = c.cap;
+    PlanArgs& pa = c.pa;
+    unsigned long long* hs = j->host_small;
+    unsigned long long* gstats = c.gstats;
+    const uint64_t n_bins = c.n_bins, n_windows = c.n_windows, n_records = c.n_records;
+    const std::vector<uint64_t>& bw = c.bw;
+    const std::vector<uint64_t>& bn = c.bn;
+    const std::vector<uint64_t>& bo = c.bo;
+    uint32_t* tmp_recs = c.tmp_recs;
+    uint32_t* tmp_sig = c.tmp_sig;
+    const uint64_t tmp_cap = c.tmp_cap;
+    if (n_windows == 0) {
+        j->n_surv = 0;
+        return;
+    }
     // ---- host: classify bins (small: one CTA in SMEM; large: multi-CTA path)
     std::vector<uint32_t> small;
     std::vector<uint64_t> large_ids;
@@ -512,7 +603,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     // ---- S5: records into bins -- a copy from pass 1's temporary stream, or (if the stream
     //      overflowed its estimate) pass 2 = S1-S3 recomputed + scatter
     uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4));
-    const uint64_t tmp_n = hs[16 + GS_TMP_RECS];
+    const uint64_t tmp_n = c.tmp_n;
     j->stage_begin(KMC_STAGE_SCATTER);
     int s5_launches = 0;
     if (tmp_recs && tmp_n <= tmp_cap) {
@@ -565,20 +656,25 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         ar.release(x_recs);
         ar.release(x_ids);
     } else {
+        if (!c.run_p1) {
+            set_err("the record stream overflowed its capacity (%llu > %llu slots)", (unsigned long long)tmp_n,
+                    (unsigned long long)tmp_cap);
+            throw Fail{KMC_ERR_INTERNAL};
+        }
         uint32_t* bin_fill = ar.get<uint32_t>(n_bins);
         CK(cudaMemsetAsync(bin_fill, 0, n_bins * 4, s));
-        a.sig2bin = pa.sig2bin;
-        a.bin_rec_off = pa.bin_rec_off;
-        a.bin_fill = bin_fill;
-        a.bins = bins;
-        s5_launches = run_p1(P1_MODE_SCATTER) - 1;
+        c.a.sig2bin = pa.sig2bin;
+        c.a.bin_rec_off = pa.bin_rec_off;
+        c.a.bin_fill = bin_fill;
+        c.a.bins = bins;
+        s5_launches = c.run_p1(P1_MODE_SCATTER) - 1;
     }
     j->launches += s5_launches;
     j->stage_end(s5_launches);
     ar.release(tmp_recs);
     ar.release(tmp_sig);
-    ar.release(hist_w);
-    ar.release(hist_r);
+    ar.release(c.hist_w);
+    ar.release(c.hist_r);
     ar.release(pa.cost_scan);
     ar.release(pa.bnd_scan);
     ar.release(pa.win_scan);
