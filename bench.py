@@ -7,8 +7,11 @@ full kmc_count call (S1-S9) over the whole read set, inputs resident in HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kmcgpu|reference] [--config C4]
 
-N > 1 runs under torchrun; every rank counts its own copy of the workload (independent
-problems, no data-path collective: weak scaling); the time is the max over ranks.
+N > 1 runs under torchrun, one rank per GPU: rank r holds its own read sample of the same
+genome (C4 reads each: weak scaling) and the ranks count the union with the sharded path
+(kmc_shard_*): NCCL all-reduce of the signature histograms, all-to-all of the
+super-k-mer records by bin owner, each rank counting and outputting its own bins.  The time
+is the max over ranks.
 ``--impl reference`` times the CPU oracle (oracle/) on the host cores, rank 0 only.
 Prints ONE JSON line (rank 0).
 """
@@ -185,7 +188,10 @@ def main():
     kmc.use_torch_allocator(True)
 
     gen_threads = max(1, (os.cpu_count() or 8) // max(1, world))
-    w = synth.make(args.config, scale=args.scale, n_threads=gen_threads)
+    # N > 1: rank r holds its own read sample of the same genome (weak scaling) and the ranks
+    # count the union together: histogram all-reduce + all-to-all of the super-k-mer records
+    # by bin owner over NCCL; each rank outputs the k-mers of its bins
+    w = synth.make(args.config, scale=args.scale, n_threads=gen_threads, shard=rank)
     n_bases = w.n_bases
     reads_d = torch.from_numpy(w.reads).cuda()
     offs_d = torch.from_numpy(w.offsets.view(np.uint64)).cuda()
@@ -193,6 +199,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(profile=True):
+        if world > 1:
+            return kmc.count_sharded(reads_d, offs_d, k, p, ci, cx, profile=profile, count_path=args.count_path)
         return kmc.count(reads_d, offs_d, k, p, ci, cx, profile=profile, count_path=args.count_path)
 
     for _ in range(max(3, args.warmup)):
@@ -233,7 +241,11 @@ def main():
     if not args.no_e2e:
         reads_h = torch.from_numpy(w.reads).pin_memory()
         offs_h = torch.from_numpy(w.offsets.view(np.uint64)).pin_memory()
-        r = kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path)
+        def e2e_step():
+            if world > 1:
+                return kmc.count_sharded(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path)
+            return kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path)
+        r = e2e_step()
         n_out = r.stats["n_out"]
         del r
         e_steps = max(1, min(args.steps, 3))
@@ -245,7 +257,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e_steps):
-            r = kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path)
+            r = e2e_step()
             del r
         e1.record(stream)
         torch.cuda.synchronize()
@@ -254,6 +266,11 @@ def main():
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(w.reads.nbytes + w.offsets.nbytes),
                "d2h_bytes_per_step": int(n_out * ((8 if k <= 32 else 16) + 4))}
 
+    windows_all = float(last["n_windows"])  # N > 1: this rank's bins; summed over ranks below
+    if world > 1:
+        t = torch.tensor([windows_all], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        windows_all = float(t.item())
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -315,10 +332,12 @@ def main():
         "data": "synthetic (seeded; BASELINE.json configs, SURVEY 8(d) recipe)",
         "config": {"workload": f"{args.config}: {cfg.desc}", "scale": args.scale, "n_reads": w.n_reads,
                    "n_bases": n_bases, "k": k, "p": p, "cutoff_min": ci, "cutoff_max": cx,
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "parallelism": (f"sharded x{world}: reads split by rank, NCCL all-reduce of the signature "
+                                   f"histogram + all-to-all of super-k-mer records by bin owner")
+                   if world > 1 else "1 GPU",
                    "count_path": ["smem_hash", "smem_radix_sort"][args.count_path],
                    "l2": "inputs (4 GB) larger than L2 (126 MB); no flush needed"},
-        "kmers_per_s": world * last["n_windows"] / (ms / 1e3),
+        "kmers_per_s": windows_all / (ms / 1e3),
         "stats": {x: last[x] for x in ("n_windows", "n_superkmers", "n_records", "n_bins", "n_large_bins",
                                       "max_bin_windows", "large_windows", "n_unique", "n_out")},
         "stages": per_stage,

@@ -176,6 +176,36 @@ kmc_status kmc_count_finish(kmc_job* job, uint64_t* out_kmers, uint32_t* out_cou
                             uint64_t out_capacity, kmc_stats* stats);
 void kmc_job_free(kmc_job* job);
 
+/* ---- Sharded counting over several GPUs.  Every rank holds a slice of the
+ * reads and runs, on its own GPU:
+ *   1. kmc_shard_pass1: S1-S4 on the slice -> its per-signature histograms hist_w (windows)
+ *      and hist_r (records), [4^p + 1] uint64 each (device or host), and *n_records, the
+ *      number of super-k-mer records it holds (the size of its send buffers).
+ *   2. the caller sums hist_w and hist_r over all ranks (an all-reduce);
+ *   3. kmc_shard_partition with the global histograms: the bin plan (identical on every
+ *      rank) gives every bin to one rank (kmc_shard_owners: contiguous bins, balanced by
+ *      windows), and the rank's records are written to the caller's send buffers grouped by
+ *      destination rank: send_records [n_records * kmc_record_words(k)] uint32,
+ *      send_sigs [n_records] uint32 (device), send_counts [world] (host) records per rank;
+ *   4. the caller exchanges them (all-to-all) -- records from every rank for this rank's bins;
+ *   5. kmc_shard_count on the received records counts the rank's bins (S5-S8) and returns
+ *      *n_out; kmc_count_finish writes its (k-mer, count) pairs, ascending.
+ * The k-mer sets of different ranks are disjoint and their union is the single-GPU result
+ * of all slices together.  The job is freed by kmc_count_finish or kmc_job_free. */
+kmc_status kmc_shard_pass1(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads,
+                           int k, int p, uint32_t cutoff_min, uint32_t cutoff_max,
+                           void* stream, const kmc_options* opt, kmc_job** job,
+                           uint64_t* hist_w, uint64_t* hist_r, uint64_t* n_records);
+kmc_status kmc_shard_partition(kmc_job* job, const uint64_t* global_hist_w, const uint64_t* global_hist_r,
+                               int world, int rank, uint32_t* send_records, uint32_t* send_sigs,
+                               uint64_t* send_counts);
+kmc_status kmc_shard_count(kmc_job* job, const uint32_t* recv_records, const uint32_t* recv_sigs,
+                           uint64_t n_recv, uint64_t* n_out);
+/* Bin -> rank map of the sharded plan (host only, no GPU): contiguous bins, each rank taking
+ * about total/world windows; owner[b] = the rank whose share holds the bin's midpoint. */
+void kmc_shard_owners(const uint64_t* bin_windows, uint64_t n_bins, int world, uint32_t* owner);
+int kmc_record_words(int k);  /* uint32 words per super-k-mer record: 4 (k <= 32) or 8 */
+
 /* Test hook for S2 parity: out_sig[j] (n_bases uint32, device or host) = signature of
  * the window starting at base j (the minimum over its k-p+1 p-mers of the canonical
  * p-mer value if allowed by P:L206-208, else the reserved value 4^p), or 0xFFFFFFFF if

@@ -92,6 +92,17 @@ def load():
         lib.kmc_version.restype = I
         lib.kmc_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, P]
         lib.kmc_set_allocator.restype = None
+        lib.kmc_shard_pass1.argtypes = [P, P, U64, I, I, U32, U32, P, ctypes.POINTER(_Options), ctypes.POINTER(P),
+                                        P, P, ctypes.POINTER(U64)]
+        lib.kmc_shard_pass1.restype = I
+        lib.kmc_shard_partition.argtypes = [P, P, P, I, I, P, P, P]
+        lib.kmc_shard_partition.restype = I
+        lib.kmc_shard_count.argtypes = [P, P, P, U64, ctypes.POINTER(U64)]
+        lib.kmc_shard_count.restype = I
+        lib.kmc_shard_owners.argtypes = [P, U64, I, P]
+        lib.kmc_shard_owners.restype = None
+        lib.kmc_record_words.argtypes = [I]
+        lib.kmc_record_words.restype = I
         _lib = lib
         return lib
 
@@ -184,8 +195,12 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
     sh = _stream_handle(stream)
     _check(lib.kmc_count_begin(_ptr(reads), _ptr(offsets), n_reads, k, p, cutoff_min, cutoff_max, sh,
                                ctypes.byref(opt), ctypes.byref(job), ctypes.byref(n_out)))
-    n = int(n_out.value)
     dev = out_device or (reads.device if hasattr(reads, "device") else "cpu")
+    return _finish(lib, job, int(n_out.value), k, dev)
+
+
+def _finish(lib, job, n: int, k: int, dev) -> Result:
+    import torch
     shape = (n,) if k <= 32 else (n, 2)
     pin = str(dev) == "cpu" and torch.cuda.is_available()
     try:
@@ -197,6 +212,132 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
     st = _Stats()
     _check(lib.kmc_count_finish(job, _ptr(kmers), _ptr(counts), n, ctypes.byref(st)))
     return Result(kmers, counts, st.to_dict())
+
+
+# ---------------------------------------------------------------- sharded counting
+
+def shard_owners(bin_windows, world: int) -> np.ndarray:
+    """Bin -> rank map of the sharded plan (host only; kmc_shard_owners)."""
+    w = np.ascontiguousarray(bin_windows, dtype=np.uint64)
+    out = np.zeros(w.shape[0], dtype=np.uint32)
+    load().kmc_shard_owners(w.ctypes.data, w.shape[0], int(world), out.ctypes.data)
+    return out
+
+
+class _Shard:
+    """One rank's sharded job: pass 1 -> (all-reduce) -> partition -> (all-to-all) -> count."""
+
+    def __init__(self, reads, offsets, k, p, cutoff_min, cutoff_max, stream=None, **opts):
+        import torch
+        self.lib = load()
+        self.k = k
+        self.dev = reads.device if hasattr(reads, "device") else torch.device("cuda")
+        ns = 4 ** p + 1
+        self.hist_w = torch.zeros(ns, dtype=torch.int64, device=self.dev)
+        self.hist_r = torch.zeros(ns, dtype=torch.int64, device=self.dev)
+        self.job = ctypes.c_void_p()
+        nrec = ctypes.c_uint64()
+        opts = dict(opts)
+        self.opt = _options(opts.pop("profile", False), opts.pop("small_bin_capacity", 0),
+                            opts.pop("force_large", False), **opts)
+        n_reads = int(offsets.shape[0]) - 1
+        _check(self.lib.kmc_shard_pass1(_ptr(reads), _ptr(offsets), n_reads, k, p, cutoff_min, cutoff_max,
+                                        _stream_handle(stream), ctypes.byref(self.opt), ctypes.byref(self.job),
+                                        _ptr(self.hist_w), _ptr(self.hist_r), ctypes.byref(nrec)))
+        self.n_records = int(nrec.value)
+        self.rw = int(self.lib.kmc_record_words(k))
+
+    def partition(self, global_w, global_r, world: int, rank: int):
+        """Records grouped by destination rank: (records int32 [n, rw], signatures int32 [n], counts [world])."""
+        import torch
+        recs = torch.empty((self.n_records, self.rw), dtype=torch.int32, device=self.dev)
+        sigs = torch.empty((self.n_records,), dtype=torch.int32, device=self.dev)
+        counts = (ctypes.c_uint64 * world)()
+        _check(self.lib.kmc_shard_partition(self.job, _ptr(global_w), _ptr(global_r), world, rank, _ptr(recs),
+                                            _ptr(sigs), counts))
+        return recs, sigs, [int(c) for c in counts]
+
+    def count(self, recv_recs, recv_sigs, out_device=None) -> Result:
+        n_out = ctypes.c_uint64()
+        _check(self.lib.kmc_shard_count(self.job, _ptr(recv_recs), _ptr(recv_sigs), int(recv_sigs.shape[0]),
+                                        ctypes.byref(n_out)))
+        job, self.job = self.job, None
+        return _finish(self.lib, job, int(n_out.value), self.k, out_device or self.dev)
+
+    def __del__(self):
+        if getattr(self, "job", None):
+            self.lib.kmc_job_free(self.job)
+
+
+def exchange(recs, sigs, send_counts, group=None):
+    """All-to-all of the partitioned records (torch.distributed, NCCL on GPUs / gloo on CPU):
+    rank r receives, in source-rank order, every rank's records for r's bins."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "gloo" and recs.is_cuda:
+        # gloo moves host tensors: stage through the host (tests run several ranks on one GPU)
+        rr, rs, rc = exchange(recs.cpu(), sigs.cpu(), send_counts, group)
+        return rr.to(recs.device), rs.to(sigs.device), rc
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=recs.device)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = [int(x) for x in rc.tolist()]
+    rw = recs.shape[1]
+    rr = torch.empty((sum(recv_counts), rw), dtype=recs.dtype, device=recs.device)
+    rs = torch.empty((sum(recv_counts),), dtype=sigs.dtype, device=sigs.device)
+    dist.all_to_all_single(rr, recs, output_split_sizes=recv_counts, input_split_sizes=list(send_counts), group=group)
+    dist.all_to_all_single(rs, sigs, output_split_sizes=recv_counts, input_split_sizes=list(send_counts), group=group)
+    assert len(recv_counts) == world
+    return rr, rs, recv_counts
+
+
+def count_sharded(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *,
+                  group=None, stream=None, out_device=None, **opts) -> Result:
+    """Sharded count over the ranks of ``group`` (torch.distributed): this rank holds a slice
+    of the reads; histograms are all-reduced and super-k-mer records exchanged all-to-all
+    (SURVEY 8(e)); returns this rank's share of the (k-mer, count) pairs -- disjoint from the
+    other ranks', ascending; the union is the count of all slices together."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    sh = _Shard(reads, offsets, k, p, cutoff_min, cutoff_max, stream=stream, **opts)
+    if world > 1:
+        if dist.get_backend(group) == "gloo" and sh.hist_w.is_cuda:
+            hw, hr = sh.hist_w.cpu(), sh.hist_r.cpu()
+            dist.all_reduce(hw, group=group)
+            dist.all_reduce(hr, group=group)
+            sh.hist_w.copy_(hw)
+            sh.hist_r.copy_(hr)
+        else:
+            dist.all_reduce(sh.hist_w, group=group)
+            dist.all_reduce(sh.hist_r, group=group)
+    recs, sigs, counts = sh.partition(sh.hist_w, sh.hist_r, world, rank)
+    if world > 1:
+        recs, sigs, _ = exchange(recs, sigs, counts, group)
+    return sh.count(recs, sigs, out_device=out_device)
+
+
+def count_sharded_local(slices, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *, stream=None,
+                        **opts):
+    """The sharded path with W virtual ranks in one process (one GPU, run one after another):
+    slices = [(reads, offsets), ...]; the all-reduce is a sum and the all-to-all a regrouping
+    of the send buffers.  Returns one Result per virtual rank."""
+    import torch
+    shards = [_Shard(r, o, k, p, cutoff_min, cutoff_max, stream=stream, **opts) for r, o in slices]
+    w = len(shards)
+    gw = sum(s.hist_w for s in shards)
+    gr = sum(s.hist_r for s in shards)
+    parts = [s.partition(gw, gr, w, r) for r, s in enumerate(shards)]
+    out = []
+    for r, s in enumerate(shards):
+        rr, rs = [], []
+        for recs, sigs, counts in parts:
+            o = sum(counts[:r])
+            rr.append(recs[o:o + counts[r]])
+            rs.append(sigs[o:o + counts[r]])
+        out.append(s.count(torch.cat(rr).contiguous(), torch.cat(rs).contiguous()))
+    return out
 
 
 def count_into(reads, offsets, k: int, p: int, cutoff_min: int, cutoff_max: int, out_kmers, out_counts, *,

@@ -390,7 +390,8 @@ __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restric
                                                        const uint32_t* __restrict__ sig2bin,
                                                        const RecTile2* __restrict__ tiles, int shift, int D,
                                                        unsigned long long* __restrict__ cursor,
-                                                       uint32_t* __restrict__ out_recs, uint32_t* __restrict__ out_ids) {
+                                                       uint32_t* __restrict__ out_recs, uint32_t* __restrict__ out_ids,
+                                                       int out_orig_ids) {
     constexpr int TI = RecTile<RW>::v, IPT = TI / RS_NT;
     using V = uint4;
     extern __shared__ __align__(16) uint8_t rsm[];
@@ -413,13 +414,15 @@ __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restric
         dr[u] = INV;
         bin[u] = INV;
         if (i < t.n) {
-            uint32_t b = __ldcs(in_ids + t.begin + i);
+            const uint32_t id = __ldcs(in_ids + t.begin + i);
+            uint32_t b = id;
             if (sig2bin && b != INV) b = sig2bin[b];
             if (b != INV) {
                 const V* src = reinterpret_cast<const V*>(in_recs + (t.begin + i) * (uint64_t)RW);
                 r0[u] = __ldcs(src);
                 if (RW == 8) r1[u] = __ldcs(src + 1);
-                bin[u] = b;
+                bin[u] = out_orig_ids ? id : b;
+                b = out_orig_ids ? sig2bin[id] : b;
                 const uint32_t d = (b >> shift) & (uint32_t)(nd - 1);
                 dr[u] = (d << 16) | atomicAdd(&lh[d], 1u);  // rank < TI
             }
@@ -468,6 +471,35 @@ __global__ void k_bucket_cursors(const uint64_t* __restrict__ bin_rec_off, uint6
     cursor[v] = b < n_bins ? bin_rec_off[b] : n_records;
 }
 
+// Sharded counting helpers.  map2[s] = map_b[map_a[s]] (signature -> bin -> owner rank).
+__global__ void k_compose_map(const uint32_t* __restrict__ map_a, const uint32_t* __restrict__ map_b, uint64_t n,
+                              uint32_t* __restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = map_b[map_a[i]];
+}
+// Records of the stream per owner rank (slots tagged INV are skipped).
+__global__ void k_owner_count(const uint32_t* __restrict__ sig, uint64_t n, const uint32_t* __restrict__ sig2owner,
+                              int world, unsigned long long* __restrict__ counts) {
+    __shared__ uint32_t h[256];
+    for (int d = threadIdx.x; d < world; d += blockDim.x) h[d] = 0;
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t sg = __ldcs(sig + i);
+        if (sg != INV) atomicAdd(&h[sig2owner[sg]], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < world; d += blockDim.x)
+        if (h[d]) atomicAdd(&counts[d], (unsigned long long)h[d]);
+}
+__global__ void k_widen(const uint32_t* __restrict__ in, uint64_t n, uint64_t* __restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+__global__ void k_narrow(const uint64_t* __restrict__ in, uint64_t n, uint32_t* __restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[i] < 0xFFFFFFFFull ? (uint32_t)in[i] : 0xFFFFFFFFu;
+}
+
 __global__ void k_debug_allowed(int p, uint8_t* out) {
     uint64_t n = 1ull << (2 * p);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -510,19 +542,20 @@ size_t rec_tile_items(int k) { return record_words(k) == 4 ? RecTile<4>::v : Rec
 
 cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* in_ids, const uint32_t* sig2bin,
                                const RecTile2* tiles, uint64_t n_tiles, int shift, int D,
-                               unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids, cudaStream_t s) {
+                               unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids, cudaStream_t s,
+                               int out_orig_ids) {
     if (n_tiles == 0) return cudaSuccess;
     cudaError_t e;
     if (record_words(k) == 4) {
         const int sm = (int)rec_scatter_smem<4>();
         if ((e = cudaFuncSetAttribute(k_rec_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
         k_rec_scatter<4><<<(unsigned)n_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, shift, D, cursor,
-                                                             out_recs, out_ids);
+                                                             out_recs, out_ids, out_orig_ids);
     } else {
         const int sm = (int)rec_scatter_smem<8>();
         if ((e = cudaFuncSetAttribute(k_rec_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
         k_rec_scatter<8><<<(unsigned)n_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, shift, D, cursor,
-                                                             out_recs, out_ids);
+                                                             out_recs, out_ids, out_orig_ids);
     }
     return cudaGetLastError();
 }
@@ -532,6 +565,30 @@ cudaError_t launch_bucket_cursors(const uint64_t* bin_rec_off, uint64_t n_bins, 
     if (n_buckets == 0) return cudaSuccess;
     k_bucket_cursors<<<(unsigned)((n_buckets + 255) / 256), 256, 0, s>>>(bin_rec_off, n_bins, n_records, shift,
                                                                          n_buckets, cursor);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compose_map(const uint32_t* map_a, const uint32_t* map_b, uint64_t n, uint32_t* out,
+                               cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_compose_map<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, s>>>(map_a, map_b, n, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_owner_count(const uint32_t* sig, uint64_t n, const uint32_t* sig2owner, int world,
+                               unsigned long long* counts, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_owner_count<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(sig, n, sig2owner, world,
+                                                                                      counts);
+    return cudaGetLastError();
+}
+cudaError_t launch_widen(const uint32_t* in, uint64_t n, uint64_t* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_widen<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, s>>>(in, n, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_narrow(const uint64_t* in, uint64_t n, uint32_t* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_narrow<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, s>>>(in, n, out);
     return cudaGetLastError();
 }
 

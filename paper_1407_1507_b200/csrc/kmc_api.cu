@@ -1154,6 +1154,220 @@ kmc_status kmc_count(const uint8_t* reads, const uint64_t* read_offsets, uint64_
                         out_capacity, stats, stream, nullptr);
 }
 
+// ---------------------------------------------------------------- sharded counting
+void kmc_shard_owners(const uint64_t* bin_windows, uint64_t n_bins, int world, uint32_t* owner) {
+    uint64_t total = 0;
+    for (uint64_t b = 0; b < n_bins; ++b) total += bin_windows[b];
+    uint64_t pre = 0;
+    for (uint64_t b = 0; b < n_bins; ++b) {
+        // contiguous ranges of bins, balanced by windows: the rank whose share holds the bin's midpoint
+        const unsigned __int128 mid2 = (unsigned __int128)(2 * pre + bin_windows[b]) * (unsigned)world;
+        uint64_t r = total ? (uint64_t)(mid2 / (2 * (unsigned __int128)total)) : 0;
+        owner[b] = (uint32_t)std::min<uint64_t>(r, (uint64_t)world - 1);
+        pre += bin_windows[b];
+    }
+}
+
+kmc_status kmc_shard_pass1(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads, int k, int p,
+                           uint32_t cutoff_min, uint32_t cutoff_max, void* stream, const kmc_options* opt,
+                           kmc_job** job, uint64_t* hist_w, uint64_t* hist_r, uint64_t* n_records) {
+    if (!job || !hist_w || !hist_r || !n_records) {
+        set_err("job, hist_w, hist_r and n_records must be non-NULL");
+        return KMC_ERR_INVALID_ARG;
+    }
+    *job = nullptr;
+    *n_records = 0;
+    kmc_status v = validate(k, p, cutoff_min, cutoff_max);
+    if (v != KMC_OK) return v;
+    if (n_reads > 0 && (!reads || !read_offsets)) {
+        set_err("reads and read_offsets must be non-NULL when n_reads > 0");
+        return KMC_ERR_INVALID_ARG;
+    }
+    kmc_job* j = new kmc_job();
+    j->s = (cudaStream_t)stream;
+    j->k = k;
+    j->p = p;
+    j->key_words = k <= 32 ? 1 : 2;
+    j->ci = cutoff_min ? cutoff_min : 1;
+    j->cx = cutoff_max;
+    if (opt) j->opt = *opt;
+    j->shard = true;
+    j->arena.bind(j->s);
+    try {
+        run_begin(j, reads, read_offsets, n_reads);
+        PlanCtx& c = j->ctx;
+        Arena& ar = j->arena;
+        cudaStream_t s = j->s;
+        const uint64_t ns = (1ull << (2 * p)) + 1;
+        if (!c.hist_w) {  // no window in this slice: empty histograms, empty stream
+            c.ns = ns;
+            c.hist_w = ar.get<unsigned long long>(ns);
+            c.hist_r = ar.get<uint32_t>(ns);
+            c.gstats = ar.get<unsigned long long>(GS_N);
+            CK(cudaMemsetAsync(c.hist_w, 0, ns * 8, s));
+            CK(cudaMemsetAsync(c.hist_r, 0, ns * 4, s));
+            CK(cudaMemsetAsync(c.gstats, 0, GS_N * 8, s));
+        }
+        uint64_t* hr = ar.get<uint64_t>(ns);
+        CK(launch_widen(c.hist_r, ns, hr, s));
+        CK(cudaMemcpyAsync(hist_w, c.hist_w, ns * 8, cudaMemcpyDefault, s));
+        CK(cudaMemcpyAsync(hist_r, hr, ns * 8, cudaMemcpyDefault, s));
+        unsigned long long* hs = j->host_small;
+        CK(cudaMemcpyAsync(&hs[16], c.gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ar.release(hr);
+        c.tmp_n = hs[16 + GS_TMP_RECS];
+        if (c.tmp_recs && c.tmp_n > c.tmp_cap) {
+            set_err("the record stream overflowed its capacity (%llu > %llu slots)", (unsigned long long)c.tmp_n,
+                    (unsigned long long)c.tmp_cap);
+            throw Fail{KMC_ERR_INTERNAL};
+        }
+        j->n_local_records = hs[16 + GS_RECORDS];
+    } catch (const Fail& f) {
+        cudaStreamSynchronize(j->s);
+        delete j;
+        return f.st;
+    }
+    *n_records = j->n_local_records;
+    *job = j;
+    return KMC_OK;
+}
+
+kmc_status kmc_shard_partition(kmc_job* j, const uint64_t* global_hist_w, const uint64_t* global_hist_r, int world,
+                               int rank, uint32_t* send_records, uint32_t* send_sigs, uint64_t* send_counts) {
+    if (!j || !j->shard || !global_hist_w || !global_hist_r || !send_counts || world < 1 || world > 256 || rank < 0 ||
+        rank >= world) {
+        set_err("invalid kmc_shard_partition arguments");
+        return KMC_ERR_INVALID_ARG;
+    }
+    if (j->n_local_records > 0 && (!send_records || !send_sigs)) {
+        set_err("NULL send buffers");
+        return KMC_ERR_INVALID_ARG;
+    }
+    try {
+        PlanCtx& c = j->ctx;
+        Arena& ar = j->arena;
+        cudaStream_t s = j->s;
+        const uint64_t ns = c.ns;
+        j->world = world;
+        j->rank = rank;
+        // the global histograms replace the local ones: every rank derives the same plan
+        uint64_t* gr = ar.get<uint64_t>(ns);
+        CK(cudaMemcpyAsync(c.hist_w, global_hist_w, ns * 8, cudaMemcpyDefault, s));
+        CK(cudaMemcpyAsync(gr, global_hist_r, ns * 8, cudaMemcpyDefault, s));
+        CK(launch_narrow(gr, ns, c.hist_r, s));
+        c.check_p1 = false;
+        plan_phase(j, c);
+        ar.release(gr);
+        c.owner.assign(c.n_bins, 0);
+        if (c.n_bins) kmc_shard_owners(c.bw.data(), c.n_bins, world, c.owner.data());
+        for (int r = 0; r < world; ++r) send_counts[r] = 0;
+        if (j->n_local_records > 0) {
+            uint32_t* d_owner = ar.get<uint32_t>(c.n_bins);
+            uint32_t* sig2owner = ar.get<uint32_t>(ns);
+            unsigned long long* counts = ar.get<unsigned long long>(world);
+            unsigned long long* cursor = ar.get<unsigned long long>(world);
+            CK(cudaMemcpyAsync(d_owner, c.owner.data(), c.n_bins * 4, cudaMemcpyHostToDevice, s));
+            CK(launch_compose_map(c.pa.sig2bin, d_owner, ns, sig2owner, s));
+            CK(cudaMemsetAsync(counts, 0, world * 8, s));
+            CK(launch_owner_count(c.tmp_sig, c.tmp_n, sig2owner, world, counts, s));
+            std::vector<unsigned long long> hc(world), cur(world);
+            CK(cudaMemcpyAsync(hc.data(), counts, world * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            unsigned long long o = 0;
+            for (int r = 0; r < world; ++r) {
+                cur[r] = o;
+                o += hc[r];
+                send_counts[r] = hc[r];
+            }
+            if (o != j->n_local_records) {
+                set_err("partitioned %llu records, pass 1 wrote %llu", o, (unsigned long long)j->n_local_records);
+                throw Fail{KMC_ERR_INTERNAL};
+            }
+            CK(cudaMemcpyAsync(cursor, cur.data(), world * 8, cudaMemcpyHostToDevice, s));
+            int D = 1;
+            while ((1 << D) < world) ++D;
+            const uint64_t TI = rec_tile_items(j->k);
+            std::vector<RecTile2> tl;
+            for (uint64_t t = 0; t < c.tmp_n; t += TI)
+                tl.push_back(RecTile2{t, (uint32_t)std::min<uint64_t>(TI, c.tmp_n - t), 0});
+            RecTile2* d_tiles = ar.get<RecTile2>(tl.size());
+            CK(cudaMemcpyAsync(d_tiles, tl.data(), tl.size() * sizeof(RecTile2), cudaMemcpyHostToDevice, s));
+            CK(launch_rec_scatter(j->k, c.tmp_recs, c.tmp_sig, sig2owner, d_tiles, tl.size(), 0, D, cursor,
+                                  send_records, send_sigs, s, 1));
+            j->launches += 4;
+            CK(cudaStreamSynchronize(s));
+            ar.release(d_tiles);
+            ar.release(d_owner);
+            ar.release(sig2owner);
+            ar.release(counts);
+            ar.release(cursor);
+        }
+    } catch (const Fail& f) {
+        return f.st;
+    }
+    return KMC_OK;
+}
+
+kmc_status kmc_shard_count(kmc_job* j, const uint32_t* recv_records, const uint32_t* recv_sigs, uint64_t n_recv,
+                           uint64_t* n_out) {
+    if (!j || !j->shard || !n_out || (n_recv > 0 && (!recv_records || !recv_sigs))) {
+        set_err("invalid kmc_shard_count arguments");
+        return KMC_ERR_INVALID_ARG;
+    }
+    *n_out = 0;
+    try {
+        PlanCtx& c = j->ctx;
+        Arena& ar = j->arena;
+        cudaStream_t s = j->s;
+        const int RW = record_words(j->k);
+        // this rank's bins only: the records of every bin it owns, from all ranks
+        uint64_t nrec = 0, nwin = 0;
+        for (uint64_t b = 0; b < c.n_bins; ++b) {
+            if (c.owner[b] != (uint32_t)j->rank) {
+                c.bw[b] = 0;
+                c.bn[b] = 0;
+            }
+            c.bo[b] = nrec;
+            nrec += c.bn[b];
+            nwin += c.bw[b];
+        }
+        if (nrec != n_recv) {
+            set_err("received %llu records, the plan gives this rank %llu", (unsigned long long)n_recv,
+                    (unsigned long long)nrec);
+            throw Fail{KMC_ERR_INVALID_ARG};
+        }
+        c.n_records = nrec;
+        c.n_windows = nwin;
+        j->st.n_records = nrec;
+        j->st.n_windows = nwin;
+        if (c.n_bins) {
+            CK(cudaMemcpyAsync(c.pa.bin_w, c.bw.data(), c.n_bins * 8, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(c.pa.bin_nrec, c.bn.data(), c.n_bins * 8, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(c.pa.bin_rec_off, c.bo.data(), c.n_bins * 8, cudaMemcpyHostToDevice, s));
+        }
+        ar.release(c.tmp_recs);
+        ar.release(c.tmp_sig);
+        c.tmp_recs = c.tmp_sig = nullptr;
+        if (n_recv > 0) {
+            c.tmp_recs = reinterpret_cast<uint32_t*>(ar.alloc(n_recv * RW * 4));
+            c.tmp_sig = ar.get<uint32_t>(n_recv);
+            CK(cudaMemcpyAsync(c.tmp_recs, recv_records, n_recv * RW * 4, cudaMemcpyDefault, s));
+            CK(cudaMemcpyAsync(c.tmp_sig, recv_sigs, n_recv * 4, cudaMemcpyDefault, s));
+        }
+        c.tmp_n = c.tmp_cap = n_recv;
+        CK(cudaMemsetAsync(c.gstats, 0, GS_N * 8, s));
+        count_phase(j, c);
+        CK(cudaStreamSynchronize(s));
+    } catch (const Fail& f) {
+        return f.st;
+    }
+    *n_out = j->n_surv;
+    return KMC_OK;
+}
+
+int kmc_record_words(int k) { return record_words(k); }
+
 kmc_status kmc_debug_signatures(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads, int k, int p,
                                 uint32_t* out_sig, void* stream) {
     kmc_status v = validate(k, p, 1, 1);

@@ -68,9 +68,18 @@ struct RecTile2 {
     uint32_t bucket;  // bucket of the previous pass (cursor row)
 };
 size_t rec_tile_items(int k);
+// out_orig_ids: write the input ids (not the mapped ones) to out_ids.
 cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* in_ids, const uint32_t* sig2bin,
                                const RecTile2* tiles, uint64_t n_tiles, int shift, int D,
-                               unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids, cudaStream_t s);
+                               unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids, cudaStream_t s,
+                               int out_orig_ids = 0);
+// sharded counting helpers
+cudaError_t launch_compose_map(const uint32_t* map_a, const uint32_t* map_b, uint64_t n, uint32_t* out,
+                               cudaStream_t s);
+cudaError_t launch_owner_count(const uint32_t* sig, uint64_t n, const uint32_t* sig2owner, int world,
+                               unsigned long long* counts, cudaStream_t s);
+cudaError_t launch_widen(const uint32_t* in, uint64_t n, uint64_t* out, cudaStream_t s);
+cudaError_t launch_narrow(const uint64_t* in, uint64_t n, uint32_t* out, cudaStream_t s);
 cudaError_t launch_bucket_cursors(const uint64_t* bin_rec_off, uint64_t n_bins, uint64_t n_records, int shift,
                                   uint64_t n_buckets, unsigned long long* cursor, cudaStream_t s);
 

@@ -149,9 +149,11 @@ class Workload:
         return int(self.offsets[-1] - self.offsets[0])
 
 
-def make(name: str, scale: float = 1.0, n_threads: int = 0, **overrides) -> Workload:
+def make(name: str, scale: float = 1.0, n_threads: int = 0, shard: int = 0, **overrides) -> Workload:
     """Generate config ``name`` (C1..C5).  ``scale`` < 1 shrinks genome, read count and
-    repeat copies together (coverage and composition are kept)."""
+    repeat copies together (coverage and composition are kept).  ``shard`` > 0 draws an
+    independent read sample of the same genome (the slice of rank ``shard`` in multi-GPU
+    runs); shard 0 is the config itself."""
     cfg = dataclasses.replace(CONFIGS[name], **overrides)
     lib = _load()
     G = max(1000, int(cfg.genome_len * scale))
@@ -160,7 +162,7 @@ def make(name: str, scale: float = 1.0, n_threads: int = 0, **overrides) -> Work
                        BASE_SEED + 16 * cfg.genome_id)
     n_reads = max(1, int(round(cfg.n_reads * scale)))
     rp = _ReadParams(n_reads, cfg.len_min, cfg.len_max, cfg.err, cfg.n_iid, cfg.n_run_start,
-                     cfg.n_run_min, cfg.n_run_max, 1, BASE_SEED + 16 * cfg.index + 1)
+                     cfg.n_run_min, cfg.n_run_max, 1, BASE_SEED + 16 * cfg.index + 1 + 1000003 * shard)
     genome = np.empty(G, dtype=np.uint8)
     lib.synth_genome(ctypes.byref(gp), genome.ctypes.data)
     offsets = np.empty(n_reads + 1, dtype=np.uint64)
