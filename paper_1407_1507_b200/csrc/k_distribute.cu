@@ -44,7 +44,7 @@ struct WarpSmem {
     uint32_t vwin[NMW];  // bit x: the k-mer window starting at local x is valid
     uint32_t vpm[NMW];   // bit x: the p-mer starting at local x is valid
     uint32_t ebits[SEG / 32 + 2];  // bit v: window v cannot continue a run (invalid / run start)
-    uint32_t sig[SEG + 8];   // window signatures (local window 15 + y at y)
+    uint32_t lsig[SEG];      // signature of each run start
     uint32_t list[SEG];      // run starts
 };
 
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
     const int64_t nb = (int64_t)a.n_bases;
     const int k = a.k, p = a.p, W = k - p + 1;
     const int RW = record_words(k), maxw = record_max_windows(k);
+    const uint32_t maxw_magic = ((1u << 20) + maxw - 1) / maxw;  // ceil(2^20 / maxw)
     const uint32_t RES = 1u << (2 * p);
     const int NK = SEG + W;  // p-mer positions y = 0..NK-1 (local 15 + y)
 
@@ -237,33 +238,28 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
         }
         if (W > A) shift_min(M, W - A, M);  // W - A < A <= 32
         // ---- E: signature of window local 15 + y (y <= SEG), INV where the window is not
-        //      valid (crosses a read start or holds a non-ACGT base)
+        //      valid (crosses a read start or holds a non-ACGT base); kept in registers
 #pragma unroll
-        for (int r = 0; r < NROW; ++r) {
-            const int y = 32 * r + lane;
-            if (y <= SEG) {
-                const int i = 15 + y;
-                const bool ok = (S.vwin[i >> 5] >> (i & 31)) & 1u;
-                S.sig[y] = ok ? M[r] : INV;
-            }
-        }
-        __syncwarp();
-        auto sig = [&](int y) { return S.sig[y]; };
-        if (MODE == P1_MODE_DEBUG) {
-            for (int v = lane; v < SEG; v += 32)  // window seg0 + v = local y = v + 1
-                if (seg0 + v < nb) a.dbg_sig[seg0 + v] = sig(v + 1);
-            __syncwarp();
-            continue;
+        for (int r = 0; r <= SEG / 32; ++r) {
+            const int i = 15 + 32 * r + lane;
+            const bool ok = (S.vwin[i >> 5] >> (i & 31)) & 1u;
+            M[r] = ok ? M[r] : INV;
         }
         // ---- F: super-k-mers = maximal runs of valid windows with equal signature
         //      (Fig. 1); records are additionally cut at the segment edge and into
-        //      pieces of at most maxw windows
+        //      pieces of at most maxw windows.  Window v (= local y = v + 1) compares its
+        //      signature with window v - 1's (y = v): one shuffle per row.
         uint32_t* list = S.list;
         int nstarts = 0;
-#pragma unroll 4
+#pragma unroll
         for (int r = 0; r < SEG / 32; ++r) {
             const int v = 32 * r + lane;
-            const uint32_t s = sig(v + 1), prev = sig(v);
+            const uint32_t s = __shfl_sync(0xffffffffu, lane == 0 ? M[r + 1] : M[r], (lane + 1) & 31);
+            const uint32_t prev = M[r];
+            if (MODE == P1_MODE_DEBUG) {
+                if (seg0 + v < nb) a.dbg_sig[seg0 + v] = s;
+                continue;
+            }
             const bool valid = s != INV;
             const bool skm = valid && prev != s;
             const bool start = skm || (valid && v == 0);
@@ -271,9 +267,14 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             const uint32_t bS = __ballot_sync(0xffffffffu, start);
             l_skm += skm;
             if (lane == 0) S.ebits[r] = bE;
-            if (start) list[nstarts + __popc(bS & ltm)] = (uint32_t)v;
+            if (start) {
+                const int at = nstarts + __popc(bS & ltm);
+                list[at] = (uint32_t)v;
+                S.lsig[at] = s;
+            }
             nstarts += __popc(bS);
         }
+        if (MODE == P1_MODE_DEBUG) continue;
         if (lane == 0) S.ebits[SEG / 32] = 1u;  // sentinel: the segment edge ends every run
         __syncwarp();
         for (int i0 = 0; i0 < nstarts; i0 += 32) {
@@ -282,13 +283,13 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             int v = 0, n = 0, nrec = 0;
             if (idx < nstarts) {
                 v = (int)list[idx];
-                s = sig(v + 1);
+                s = S.lsig[idx];
                 const int pos = v + 1;
                 int wd = pos >> 5;
                 uint32_t bits = S.ebits[wd] & (0xFFFFFFFFu << (pos & 31));
                 while (bits == 0) bits = S.ebits[++wd];
                 n = (wd * 32 + __ffs(bits) - 1) - v;
-                nrec = (n + maxw - 1) / maxw;
+                nrec = (int)(((uint32_t)(n + maxw - 1) * maxw_magic) >> 20);  // exact: (n+maxw)*maxw < 2^20
                 l_windows += n;
                 l_recs += nrec;
             }
