@@ -44,9 +44,12 @@ struct WarpSmem {
     uint32_t vwin[NMW];  // bit x: the k-mer window starting at local x is valid
     uint32_t vpm[NMW];   // bit x: the p-mer starting at local x is valid
     uint32_t ebits[SEG / 32 + 2];  // bit v: window v cannot continue a run (invalid / run start)
-    uint32_t lsig[SEG];      // signature of each run start
-    uint32_t list[SEG];      // run starts
+    // phase D: keys (KS, 18 * 32 positions) and block prefix minima (PS, + overrun slack);
+    // phases F-G: signature of each run start (xs[0, SEG)) and run starts (xs[SEG, 2 SEG))
+    alignas(16) uint32_t xs[NROW * 32 + NROW * 32 + 64];
 };
+static_assert(NROW * 32 * 2 + 64 >= 2 * SEG, "run lists fit the phase-D scratch");
+static_assert(NROW == 18, "the block minimum uses 32 lanes x 18 positions");
 
 // A->0, C->1, G->2, T->3; lowercase folded; anything else invalid (R3).
 __device__ __forceinline__ void encode16(const uint32_t (&wd)[4], uint32_t& packed, uint32_t& invbits) {
@@ -193,63 +196,107 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             }
         }
         __syncwarp();
-        // ---- C: canonical p-mer keys at local 15 + y, y < NK, in
-        //      registers: row r, lane l holds position y = 32r + l.  key = min(fwd, rc) if the
-        //      p-mer is valid and allowed, else the reserved 4^p (R4).
-        uint32_t M[NROW];
+        // ---- C: canonical p-mer keys at local 15 + y, in registers:
+        //      lane l holds positions y = 18 l + o, o < 18 (NROW * 32 = 576 >= SEG + W).
+        //      key = min(fwd, rc) if the p-mer is valid and allowed, else the reserved 4^p (R4).
+        const int y0 = 18 * lane;
+        uint32_t K[18];
+        {
+            const int j0 = 15 + y0;  // local base of position y0
+            const int w0 = j0 >> 4, sh = 2 * (j0 & 15);
+            const uint32_t W0 = S.pk[w0], W1 = S.pk[w0 + 1], W2 = S.pk[w0 + 2], W3 = S.pk[w0 + 3];
+            const uint32_t sA = __funnelshift_l(W1, W0, sh), sB = __funnelshift_l(W2, W1, sh),
+                           sC = __funnelshift_l(W3, W2, sh);  // symbols j0 .. j0 + 47, MSB first
+            const uint32_t pvb = __funnelshift_r(S.vpm[j0 >> 5], S.vpm[(j0 >> 5) + 1], j0 & 31);
 #pragma unroll
-        for (int r = 0; r < NROW; ++r) {
-            const int y = 32 * r + lane;
-            const int j = 15 + y;
-            uint32_t key = 0xFFFFFFFFu;
-            if (y < NK) {
-                // 16 symbols from j (p <= 16): one funnel shift of two packed words
-                const uint32_t x16 = __funnelshift_l(S.pk[(j >> 4) + 1], S.pk[j >> 4], 2 * (j & 15));
+            for (int o = 0; o < 18; ++o) {
+                const uint32_t x16 = o < 16 ? __funnelshift_l(sB, sA, 2 * o) : __funnelshift_l(sC, sB, 2 * (o - 16));
                 const uint32_t fwd = x16 >> (32 - 2 * p);
                 const uint32_t rc = rev2_32(~fwd) >> (32 - 2 * p);
                 const uint32_t cn = min(fwd, rc);
-                const bool pv = (S.vpm[j >> 5] >> (j & 31)) & 1u;
-                key = (pv && sig_allowed(cn, p)) ? cn : RES;
+                K[o] = (((pvb >> o) & 1u) && sig_allowed(cn, p)) ? cn : RES;
             }
-            M[r] = key;
         }
-        // ---- D: sliding minimum over W keys with warp shuffles (doubling): after the step
-        //      with shift s, M(y) = min over [y, y + 2s); the window [y, y + W) is covered by
-        //      two ranges of length A = 2^floor(log2 W): min(M_A(y), M_A(y + W - A))
-        auto shift_min = [&](uint32_t (&X)[NROW], int sft, uint32_t (&out)[NROW]) {
-            const int src = (lane + sft) & 31;
-            const bool hi = lane + sft >= 32;
-#pragma unroll
-            for (int r = 0; r < NROW; ++r) {
-                const uint32_t a0 = __shfl_sync(0xffffffffu, X[r], src);
-                const uint32_t a1 = __shfl_sync(0xffffffffu, r + 1 < NROW ? X[r + 1] : 0xFFFFFFFFu, src);
-                out[r] = min(X[r], hi ? a1 : a0);
-            }
-        };
-        int A = 1;
-        while (2 * A <= W) {
-            if (A == 32) {
-#pragma unroll
-                for (int r = 0; r < NROW; ++r) M[r] = min(M[r], r + 1 < NROW ? M[r + 1] : 0xFFFFFFFFu);
-            } else {
-                shift_min(M, A, M);
-            }
-            A *= 2;
-        }
-        if (W > A) shift_min(M, W - A, M);  // W - A < A <= 32
+        // ---- D: sliding minimum over W keys: window y = min over keys [y, y + W)
         // ---- E: signature of window local 15 + y (y <= SEG), INV where the window is not
-        //      valid (crosses a read start or holds a non-ACGT base); kept in registers
+        //      valid (crosses a read start or holds a non-ACGT base); rows M[r] (lane l: y = 32 r + l)
+        uint32_t* KS = S.xs;
+        uint32_t M[NROW];
+        if (W >= 19) {
+            // van Herk / Gil-Werman over blocks of 18 positions.  W >= 19 means every window
+            // leaves its own block: min = suffix min in the own block, minima of the blocks it
+            // covers fully, prefix min of the block it ends in (read from PS).
+            uint32_t* PS = S.xs + NROW * 32;
+            uint32_t T = 0xFFFFFFFFu;
 #pragma unroll
-        for (int r = 0; r <= SEG / 32; ++r) {
-            const int i = 15 + 32 * r + lane;
-            const bool ok = (S.vwin[i >> 5] >> (i & 31)) & 1u;
-            M[r] = ok ? M[r] : INV;
+            for (int o = 0; o < 18; o += 2) {  // 64-bit: 9 l + o / 2 is conflict-free per half warp
+                const uint32_t p0 = min(T, K[o]), p1 = min(p0, K[o + 1]);
+                *reinterpret_cast<uint2*>(PS + y0 + o) = make_uint2(p0, p1);
+                T = p1;
+            }
+#pragma unroll
+            for (int o = 16; o >= 0; --o) K[o] = min(K[o], K[o + 1]);  // suffix minima
+            const uint32_t T1 = __shfl_sync(0xffffffffu, T, (lane + 1) & 31);
+            const uint32_t T2 = min(T1, __shfl_sync(0xffffffffu, T, (lane + 2) & 31));
+            const uint32_t T3 = min(T2, __shfl_sync(0xffffffffu, T, (lane + 3) & 31));
+            // window i ends in block l + m, m = (i + W - 1) / 18 in {m0, m0 + 1}
+            const int m0 = (W - 1) / 18, isplit = 18 * (m0 + 1) - (W - 1);
+            const uint32_t midA = m0 == 1 ? 0xFFFFFFFFu : m0 == 2 ? T1 : T2;
+            const uint32_t midB = m0 == 1 ? T1 : m0 == 2 ? T2 : T3;
+            const int i0 = 15 + y0;  // window y0's local base
+            const uint32_t vwb = __funnelshift_r(S.vwin[i0 >> 5], S.vwin[(i0 >> 5) + 1], i0 & 31);
+            __syncwarp();
+            const uint32_t* pe = PS + y0 + (W - 1);
+#pragma unroll
+            for (int o = 0; o < 18; o += 2) {
+                uint32_t w0 = min(min(K[o], o < isplit ? midA : midB), pe[o]);
+                uint32_t w1 = min(min(K[o + 1], o + 1 < isplit ? midA : midB), pe[o + 1]);
+                w0 = ((vwb >> o) & 1u) ? w0 : INV;
+                w1 = ((vwb >> (o + 1)) & 1u) ? w1 : INV;
+                *reinterpret_cast<uint2*>(KS + y0 + o) = make_uint2(w0, w1);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r <= SEG / 32; ++r) M[r] = KS[32 * r + lane];
+        } else {
+            // short windows: doubling with warp shuffles over rows; after the step with shift
+            // s, M(y) = min over [y, y + 2s); [y, y + W) = two ranges of length A = 2^floor(log2 W)
+#pragma unroll
+            for (int o = 0; o < 18; o += 2)
+                *reinterpret_cast<uint2*>(KS + y0 + o) = make_uint2(K[o], K[o + 1]);
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < NROW; ++r) M[r] = KS[32 * r + lane];
+            auto shift_min = [&](int sft) {
+                const int src = (lane + sft) & 31;
+                const bool hi = lane + sft >= 32;
+#pragma unroll
+                for (int r = 0; r < NROW; ++r) {
+                    const uint32_t a0 = __shfl_sync(0xffffffffu, M[r], src);
+                    const uint32_t a1 = __shfl_sync(0xffffffffu, r + 1 < NROW ? M[r + 1] : 0xFFFFFFFFu, src);
+                    M[r] = min(M[r], hi ? a1 : a0);
+                }
+            };
+            int A = 1;
+            while (2 * A <= W) {
+                shift_min(A);
+                A *= 2;
+            }
+            if (W > A) shift_min(W - A);  // W - A < A <= 16
+#pragma unroll
+            for (int r = 0; r <= SEG / 32; ++r) {
+                const int i = 15 + 32 * r + lane;
+                const bool ok = (S.vwin[i >> 5] >> (i & 31)) & 1u;
+                M[r] = ok ? M[r] : INV;
+            }
         }
+        __syncwarp();
         // ---- F: super-k-mers = maximal runs of valid windows with equal signature
         //      (Fig. 1); records are additionally cut at the segment edge and into
         //      pieces of at most maxw windows.  Window v (= local y = v + 1) compares its
         //      signature with window v - 1's (y = v): one shuffle per row.
-        uint32_t* list = S.list;
+        uint32_t* list = S.xs + SEG;
+        uint32_t* lsig = S.xs;
         int nstarts = 0;
 #pragma unroll
         for (int r = 0; r < SEG / 32; ++r) {
@@ -270,7 +317,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             if (start) {
                 const int at = nstarts + __popc(bS & ltm);
                 list[at] = (uint32_t)v;
-                S.lsig[at] = s;
+                lsig[at] = s;
             }
             nstarts += __popc(bS);
         }
@@ -283,7 +330,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             int v = 0, n = 0, nrec = 0;
             if (idx < nstarts) {
                 v = (int)list[idx];
-                s = S.lsig[idx];
+                s = lsig[idx];
                 const int pos = v + 1;
                 int wd = pos >> 5;
                 uint32_t bits = S.ebits[wd] & (0xFFFFFFFFu << (pos & 31));

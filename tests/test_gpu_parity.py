@@ -73,7 +73,7 @@ def test_signature_fig1_golden(gpu):
     assert got[:7].tolist() == sig and all(x == 0xFFFFFFFF for x in got[7:])
 
 
-@pytest.mark.parametrize("k,p", [(25, 7), (28, 9), (31, 9), (55, 11), (64, 12), (8, 8), (12, 3), (5, 1), (33, 5)])
+@pytest.mark.parametrize("k,p", [(25, 7), (28, 9), (31, 9), (55, 11), (64, 12), (8, 8), (12, 3), (5, 1), (33, 5), (64, 1), (37, 1), (36, 1), (46, 10)])
 def test_signature_parity_random(gpu, k, p):
     seqs = synth.random_reads(k * 100 + p, 400, 0, 300, n_frac=0.01, lower_frac=0.02)
     _sig_case(gpu, synth.from_strings(seqs, k), k, p)
