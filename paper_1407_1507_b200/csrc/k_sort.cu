@@ -527,6 +527,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     uint8_t* own = reinterpret_cast<uint8_t*>(RB + 2 * RBUF) + warp * OWN;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(RB + 2 * RBUF) + (SP_NT / 32) * OWN);
     const uint32_t R = gridDim.x, r = blockIdx.x;
+    const int U = k + 3 <= 32 ? 4 : 33 - k;  // windows per unit (64-bit keys): k + U - 1 <= 32
     const uint64_t p0 = (uint64_t)r * n_pieces / R, p1 = (uint64_t)(r + 1) * n_pieces / R;
     if (p0 >= p1) return;
     auto issue = [&](uint64_t p, int b) {
@@ -566,25 +567,58 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
             __syncthreads();
         }
         mbar_wait(mbar + b, (it >> 1) & 1);
-        // warp w expands records [32w, 32w+32) of the piece, one lane per window (S6):
-        // warp scan of the records' window counts, then a window -> lane map in SMEM
+        // warp w expands records [32w, 32w+32) of the piece (S6): a lane takes a unit of up
+        // to U consecutive windows of one record (warp scan of the records' unit counts, then
+        // a unit -> lane map in SMEM).  64-bit keys: one 64-bit field holds the unit's
+        // k + U - 1 <= 32 symbols; the windows' forward keys are shifts of it and their reverse
+        // complements shifts of its one reversal.
         const uint32_t* Rp = RB + b * RBUF;
         const int rec = threadIdx.x;
-        const uint32_t n = rec < (int)pc.nrec ? rec_nwin(Rp + rec * RW) : 0u;
-        const uint32_t inc = warp_incl_sum(n);
-        const uint32_t pre = inc - n;
-        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-        for (uint32_t j = 0; j < n; ++j) own[pre + j] = (uint8_t)lane;
-        __syncwarp();
         const int D = (int)lb.D;
-        for (uint32_t w0 = 0; w0 < tot; w0 += 32) {
-            const uint32_t w = w0 + lane;
-            const int l = w < tot ? own[w] : 0;
-            const uint32_t pl = __shfl_sync(0xffffffffu, pre, l);
-            if (w < tot) {
-                const K key = window_key<K>(Rp + (warp * 32 + l) * RW, (int)(w - pl), k);
-                const uint32_t slot = atomicAdd(&h[part_digit(key, D)], 1u);
-                if (SCATTER) out[slot] = key;
+        const uint32_t n = rec < (int)pc.nrec ? rec_nwin(Rp + rec * RW) : 0u;
+        if constexpr (sizeof(K) == 8) {
+            const uint32_t nu = U == 4 ? (n + 3) >> 2 : U == 2 ? (n + 1) >> 1 : U == 1 ? n : (n + 2) / 3;
+            const uint32_t inc = warp_incl_sum(nu);
+            const uint32_t pre = inc - nu;
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            for (uint32_t j = 0; j < nu; ++j) own[pre + j] = (uint8_t)lane;
+            __syncwarp();
+            for (uint32_t w0 = 0; w0 < tot; w0 += 32) {
+                const uint32_t w = w0 + lane;
+                const int l = w < tot ? own[w] : 0;
+                const uint32_t pl = __shfl_sync(0xffffffffu, pre, l), nl = __shfl_sync(0xffffffffu, n, l);
+                if (w < tot) {
+                    const int first = U * (int)(w - pl);
+                    const int cnt = min(U, (int)nl - first);
+                    const uint64_t g = bits64_be(Rp + (warp * 32 + l) * RW, 8 + 2 * first);
+                    const uint64_t rg = rev2_64(~g);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        if (t < cnt) {
+                            const uint64_t f = (g << (2 * t)) >> (64 - 2 * k);
+                            const uint64_t rc = (rg << (64 - 2 * t - 2 * k)) >> (64 - 2 * k);
+                            const uint64_t key = f < rc ? f : rc;
+                            const uint32_t slot = atomicAdd(&h[part_digit(key, D)], 1u);
+                            if (SCATTER) out[slot] = (K)key;
+                        }
+                    }
+                }
+            }
+        } else {
+            const uint32_t inc = warp_incl_sum(n);
+            const uint32_t pre = inc - n;
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            for (uint32_t j = 0; j < n; ++j) own[pre + j] = (uint8_t)lane;
+            __syncwarp();
+            for (uint32_t w0 = 0; w0 < tot; w0 += 32) {
+                const uint32_t w = w0 + lane;
+                const int l = w < tot ? own[w] : 0;
+                const uint32_t pl = __shfl_sync(0xffffffffu, pre, l);
+                if (w < tot) {
+                    const K key = window_key<K>(Rp + (warp * 32 + l) * RW, (int)(w - pl), k);
+                    const uint32_t slot = atomicAdd(&h[part_digit(key, D)], 1u);
+                    if (SCATTER) out[slot] = key;
+                }
             }
         }
         __syncthreads();
