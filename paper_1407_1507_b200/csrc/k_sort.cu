@@ -495,21 +495,42 @@ __global__ void __launch_bounds__(GP_NT) k_greedy_chunks(GreedyArgs g) {
 }
 
 // Split of the large bins, upsweep/downsweep style over CTA "ranges".  The
-// pieces of all large bins (in bin order) are cut into R contiguous ranges, one per CTA;
-// the pair (range, bin) is a "segment".  The count kernel histograms the split digit of
-// every window of a segment in shared memory and stores it, without atomics, at
+// pieces of all large bins (in bin order) are cut into R contiguous ranges, one per CTA.
+// A bin's keys are counted per "segment" and digit: the count kernel histograms the split
+// digit of every window of a segment in shared memory and stores it, without atomics, at
 // table[lb.tb + d * lb.nseg + j] (j = segment index within the bin).  An exclusive scan of
 // the table (bin-major, then digit, then segment) gives every segment the position of its
 // first key of digit d in the digit-contiguous layout of the bin's keys; the scatter
-// kernel re-expands its pieces and places every key at a shared-memory cursor seeded from
-// the scanned table -- no global atomics, and each CTA writes every digit as one run.
-// Pieces stream through a double-buffered TMA staging area (one 1-D bulk copy each).
-constexpr int SP_NT = 512;  // split CTA: one record of a piece per thread
+// kernel re-expands the segment and places every key -- no global atomics.
+// Segments are either (range, bin) pairs ("range mode": the scatter places every key at a
+// shared-memory cursor seeded from the table, each CTA writing every digit as one run) or,
+// for 64-bit keys and bins with D <= SP_PM_DMAX, single pieces ("piece mode", lb.pad = 1):
+// the scatter then knows every digit's key count in the piece before expanding it, stages
+// the piece's keys in shared memory grouped by digit and writes them out coalesced
+// (consecutive threads, consecutive addresses) instead of 8-byte stores scattered over up
+// to 2^D runs.  Pieces stream through a double-buffered TMA staging area (one 1-D bulk copy
+// each).
+constexpr int SP_NT = 512;      // split CTA: one record of a piece per thread
+constexpr int SP_PM_DMAX = 8;   // piece mode: digits per bin <= 256 (<= SP_NT)
+constexpr int SP_STAGE = 8192;  // keys of a piece staged in shared memory (more: direct stores)
 // digit counters, padded to 128 bytes (the TMA staging buffers that follow need 16-byte alignment)
 __host__ __device__ constexpr int split_hwords(int dmax) { return ((1 << dmax) + 31) & ~31; }
-template <class K> size_t split_smem(int k, int dmax) {
-    return (size_t)split_hwords(dmax) * 4 + 2 * (size_t)(MsdPiece<K>::REC * RecWords<K>::v + 8) * 4 +
-           (size_t)(SP_NT / 32) * ((32 * record_max_windows(k) + 15) & ~15) + 16;
+template <class K> __host__ __device__ constexpr int split_unit(int k) {
+    return sizeof(K) == 8 ? (k + 3 <= 32 ? 4 : 33 - k) : 1;  // windows per lane unit
+}
+template <class K> __host__ __device__ int split_own_bytes(int k) {  // unit -> lane map per warp
+    const int U = split_unit<K>(k);
+    return (32 * ((record_max_windows(k) + U - 1) / U) + 15) & ~15;
+}
+// bytes of the counter region; the scatter of 64-bit keys aliases it with the piece stage
+template <class K, bool SC> __host__ __device__ int split_hreg(int dmax) {
+    const int hb = split_hwords(dmax) * 4;
+    const int st = (SC && sizeof(K) == 8) ? SP_STAGE * 9 : 0;  // keys + digit bytes
+    return hb > st ? hb : st;
+}
+template <class K, bool SC> size_t split_smem(int k, int dmax) {
+    return (size_t)split_hreg<K, SC>(dmax) + 3 * 256 * 4 + 2 * (size_t)(MsdPiece<K>::REC * RecWords<K>::v + 8) * 4 +
+           (size_t)(SP_NT / 32) * split_own_bytes<K>(k) + 16;
 }
 
 template <class K, bool SCATTER>
@@ -519,15 +540,23 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     constexpr int REC = MsdPiece<K>::REC, RW = RecWords<K>::v;
     constexpr int RBUF = REC * RW + 8;  // words per staging buffer (+ readable slack for funnel reads)
     static_assert(REC == SP_NT, "one record per thread");
+    static_assert((1 << SP_PM_DMAX) <= SP_NT, "one thread per digit in piece mode");
     extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t wsum[SP_NT / 32 + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int OWN = (32 * record_max_windows(k) + 15) & ~15;  // bytes of window->lane map per warp
+    const int OWN = split_own_bytes<K>(k);
+    const int HREG = split_hreg<K, SCATTER>(dmax);
     uint32_t* h = reinterpret_cast<uint32_t*>(smem);
-    uint32_t* RB = h + split_hwords(dmax);
+    K* stage = reinterpret_cast<K*>(smem);                // piece mode (scatter): keys by digit
+    uint8_t* sdig = smem + (size_t)SP_STAGE * sizeof(K);  // ... and their digits
+    uint32_t* gst = reinterpret_cast<uint32_t*>(smem + HREG);  // piece mode: first position of digit d
+    uint32_t* lof = gst + 256;                                 // ... its offset in the stage
+    uint32_t* lc = lof + 256;                                  // ... keys placed so far
+    uint32_t* RB = lc + 256;
     uint8_t* own = reinterpret_cast<uint8_t*>(RB + 2 * RBUF) + warp * OWN;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(RB + 2 * RBUF) + (SP_NT / 32) * OWN);
     const uint32_t R = gridDim.x, r = blockIdx.x;
-    const int U = k + 3 <= 32 ? 4 : 33 - k;  // windows per unit (64-bit keys): k + U - 1 <= 32
+    const int U = split_unit<K>(k);
     const uint64_t p0 = (uint64_t)r * n_pieces / R, p1 = (uint64_t)(r + 1) * n_pieces / R;
     if (p0 >= p1) return;
     auto issue = [&](uint64_t p, int b) {
@@ -546,6 +575,8 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     uint32_t cur = 0xFFFFFFFFu;
     LargeBin lb{};
     uint64_t tab = 0;  // table index of digit 0 of the current segment
+    bool pm = false, staged = false;
+    uint32_t npk = 0;  // piece mode: keys of the piece
     for (uint64_t p = p0; p < p1; ++p) {
         const uint32_t it = (uint32_t)(p - p0);
         const int b = it & 1;
@@ -555,15 +586,40 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
         }
         const Piece pc = pieces[p];
         if (pc.lbin != cur) {
-            if (!SCATTER && cur != 0xFFFFFFFFu) {
+            if (!SCATTER && cur != 0xFFFFFFFFu && !pm) {
                 for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT) table[tab + (uint64_t)d * lb.nseg] = h[d];
                 __syncthreads();
             }
             cur = pc.lbin;
             lb = lbins[cur];
-            tab = lb.tb + (r - lb.first_range);
-            for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT)
-                h[d] = SCATTER ? table[tab + (uint64_t)d * lb.nseg] : 0u;
+            pm = sizeof(K) == 8 && lb.pad != 0;
+            if (!pm) {
+                tab = lb.tb + (r - lb.first_range);
+                for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT)
+                    h[d] = SCATTER ? table[tab + (uint64_t)d * lb.nseg] : 0u;
+            }
+            __syncthreads();
+        }
+        const int D = (int)lb.D;
+        if (pm) {
+            // segment = this piece (first_range holds the bin's first piece)
+            tab = lb.tb + (p - lb.first_range);
+            const bool mine = threadIdx.x < (1u << D);
+            if (SCATTER) {
+                uint32_t c = 0;
+                if (mine) {
+                    const uint64_t ix = tab + (uint64_t)threadIdx.x * lb.nseg;
+                    const uint32_t g0 = table[ix];
+                    c = table[ix + 1] - g0;  // next entry: same digit, next piece (or next digit)
+                    gst[threadIdx.x] = g0;
+                    lc[threadIdx.x] = 0;
+                }
+                const uint32_t lo = block_excl_sum<SP_NT, uint32_t>(c, wsum, &npk);
+                if (mine) lof[threadIdx.x] = lo;
+                staged = npk <= (uint32_t)SP_STAGE;
+            } else if (mine) {
+                h[threadIdx.x] = 0;
+            }
             __syncthreads();
         }
         mbar_wait(mbar + b, (it >> 1) & 1);
@@ -574,7 +630,6 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
         // complements shifts of its one reversal.
         const uint32_t* Rp = RB + b * RBUF;
         const int rec = threadIdx.x;
-        const int D = (int)lb.D;
         const uint32_t n = rec < (int)pc.nrec ? rec_nwin(Rp + rec * RW) : 0u;
         if constexpr (sizeof(K) == 8) {
             const uint32_t nu = U == 4 ? (n + 3) >> 2 : U == 2 ? (n + 1) >> 1 : U == 1 ? n : (n + 2) / 3;
@@ -598,8 +653,22 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                             const uint64_t f = (g << (2 * t)) >> (64 - 2 * k);
                             const uint64_t rc = (rg << (64 - 2 * t - 2 * k)) >> (64 - 2 * k);
                             const uint64_t key = f < rc ? f : rc;
-                            const uint32_t slot = atomicAdd(&h[part_digit(key, D)], 1u);
-                            if (SCATTER) out[slot] = (K)key;
+                            const uint32_t dg = part_digit(key, D);
+                            if (!pm) {
+                                const uint32_t slot = atomicAdd(&h[dg], 1u);
+                                if (SCATTER) out[slot] = (K)key;
+                            } else if (!SCATTER) {
+                                atomicAdd(&h[dg], 1u);
+                            } else {
+                                const uint32_t rk = atomicAdd(&lc[dg], 1u);
+                                if (staged) {
+                                    const uint32_t q = lof[dg] + rk;
+                                    stage[q] = (K)key;
+                                    sdig[q] = (uint8_t)dg;
+                                } else {
+                                    out[gst[dg] + rk] = (K)key;
+                                }
+                            }
                         }
                     }
                 }
@@ -622,8 +691,22 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
             }
         }
         __syncthreads();
+        if (pm) {
+            if (SCATTER) {
+                if (staged) {  // the piece's keys, digit after digit: coalesced runs
+                    for (uint32_t i = threadIdx.x; i < npk; i += SP_NT) {
+                        const uint32_t d = sdig[i];
+                        out[gst[d] + (i - lof[d])] = stage[i];
+                    }
+                    __syncthreads();
+                }
+            } else if (threadIdx.x < (1u << D)) {
+                // the same thread zeroes h[d] for the next piece (or range-mode bin)
+                table[tab + (uint64_t)threadIdx.x * lb.nseg] = h[threadIdx.x];
+            }
+        }
     }
-    if (!SCATTER)
+    if (!SCATTER && !pm)
         for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT) table[tab + (uint64_t)d * lb.nseg] = h[d];
 }
 
@@ -911,6 +994,8 @@ cudaError_t launch_make_pieces(const LargeBin* lbins, const uint64_t* piece_pref
     return cudaGetLastError();
 }
 
+int split_piece_mode_dmax(int k) { return k <= 32 ? SP_PM_DMAX : -1; }
+
 int msd_piece_records(int k) { return k <= 32 ? MsdPiece<uint64_t>::REC : MsdPiece<K128>::REC; }
 
 int msd_digit_bits(uint64_t bin_windows, int k, int cap) {
@@ -936,7 +1021,7 @@ uint64_t greedy_segments(uint64_t n_digits) { return (n_digits + GP_SEG - 1) / G
 template <class K, bool SC>
 cudaError_t split_t(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins, int k,
                     int dmax, uint32_t n_ranges, uint32_t* table, void* keys, cudaStream_t s) {
-    const int sm = (int)split_smem<K>(k, dmax);
+    const int sm = (int)split_smem<K, SC>(k, dmax);
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_split<K, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
     k_split<K, SC><<<n_ranges, SP_NT, sm, s>>>(bins, pieces, n_pieces, lbins, k, dmax, table, (K*)keys);

@@ -850,11 +850,22 @@ void count_phase(kmc_job* j, PlanCtx& c) {
                 while (r > 0 && r * n_pieces / R > piece) --r;
                 return (uint32_t)r;
             };
+            // segments: single pieces for bins in piece mode (staged coalesced scatter) while
+            // the table stays small, else (range, bin) pairs
             uint64_t tb = 0;
+            const int pm_dmax = split_piece_mode_dmax(k);
             for (size_t i = 0; i < gn; ++i) {
-                const uint32_t f = range_of(pp[i]), l = range_of(pp[i + 1] - 1);
-                lbins[i].first_range = f;
-                lbins[i].nseg = l - f + 1;
+                const uint64_t np_b = pp[i + 1] - pp[i];
+                const bool pm = (int)lbins[i].D <= pm_dmax && tb + (np_b << lbins[i].D) <= (1ull << 26);
+                if (pm) {
+                    lbins[i].first_range = (uint32_t)pp[i];
+                    lbins[i].nseg = (uint32_t)np_b;
+                    lbins[i].pad = 1;
+                } else {
+                    const uint32_t f = range_of(pp[i]), l = range_of(pp[i + 1] - 1);
+                    lbins[i].first_range = f;
+                    lbins[i].nseg = l - f + 1;
+                }
                 lbins[i].tb = tb;
                 tb += (uint64_t)lbins[i].nseg << lbins[i].D;
             }

@@ -145,10 +145,12 @@ struct LargeBin {
     uint32_t n;
     uint32_t D;
     uint32_t nrec;
-    uint32_t first_range;  // first split range (CTA) holding pieces of this bin
-    uint32_t nseg;         // split ranges holding pieces of this bin
-    uint32_t pad;
+    uint32_t first_range;  // range mode: first split range (CTA) holding pieces of this bin;
+                           // piece mode: the bin's first piece
+    uint32_t nseg;         // split segments of this bin (ranges, or pieces in piece mode)
+    uint32_t pad;          // 1: piece mode (segment = one piece; staged coalesced scatter)
 };
+int split_piece_mode_dmax(int k);  // largest digit bits of a piece-mode bin (-1: none)
 // pieces[piece_prefix[i] + j] = records [j*rec_per_piece, ...) of large bin i
 cudaError_t launch_make_pieces(const LargeBin* lbins, const uint64_t* piece_prefix, uint64_t n_lbins,
                                uint32_t rec_per_piece, Piece* pieces, cudaStream_t s);

@@ -160,6 +160,18 @@ def test_chunk_count_paths(gpu, name, scale, count_path):
     assert st["large_windows"] == st["n_windows"]
 
 
+def test_split_piece_and_range_modes(gpu):
+    # piece-mode bins whose pieces hold more keys than the shared-memory stage (long poly-A /
+    # (AC)n super-k-mers: maxw windows per record) next to ordinary ones
+    seqs = ["A" * 3000, "AC" * 1500, "ACGTTGCA" * 300] * 40
+    seqs += [s.decode() for s in synth.random_reads(21, 3000, 100, 300)]
+    assert_same(gpu, synth.from_strings(seqs, 28, 9, 1), force_large=True)
+    # tiny chunks: bins with more than 2^8 digits take range mode, the rest piece mode, in
+    # the same split launch
+    st = assert_same(gpu, synth.make("C2", scale=0.005), force_large=True, chunk_capacity=128)
+    assert st["chunk_capacity"] == 128
+
+
 @pytest.mark.parametrize("large_path,count_path", [(0, 0), (0, 1), (1, 0)])
 def test_low_complexity_and_skew(gpu, large_path, count_path):
     # poly-A / (AT)n pile-ups: one k-mer with ~25K copies -> an "oversize" MSD digit
