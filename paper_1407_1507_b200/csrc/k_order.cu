@@ -13,6 +13,8 @@
 // (k_greedy_chunks) and every chunk is sorted in shared memory and written straight into
 // the caller's output at its offset.  A bucket holding more than CAP survivors is returned
 // to the caller for the device-wide LSD path.
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <vector>
 
@@ -226,13 +228,11 @@ cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uin
     ga.cnt = os.hist;
     ga.gstart = os.start;
     ga.n_digits = nbk;
-    ga.cursor = nullptr;
-    ga.cursor_abs = 1;
     ga.chunks = os.chunks;
     ga.oversize = os.oversize;
     ga.counters = os.counters;
     ga.cap = OrderCap<K>::v;
-    if ((e = launch_greedy_chunks(ga, greedy_segments(nbk), s))) return e;
+    if ((e = launch_greedy_chunks(ga, n, s))) return e;
     if ((e = cudaMemcpyAsync(os.host, os.counters, 16, cudaMemcpyDeviceToHost, s))) return e;
     if ((e = cudaStreamSynchronize(s))) return e;
     const uint64_t n_chunks = os.host[0], n_over = os.host[1];

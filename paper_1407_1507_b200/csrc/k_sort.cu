@@ -403,93 +403,98 @@ template <class K> struct MsdPiece;
 template <> struct MsdPiece<uint64_t> { static constexpr int REC = 512, MAXW = 60; };
 template <> struct MsdPiece<K128> { static constexpr int REC = 512, MAXW = 92; };
 
-// Greedy chunk planner.  One CTA per segment of consecutive digits (a large bin's 2^D
-// digits, or a 4096-digit window of S9's global digits): exclusive scan of the digit
-// counts -> per-digit cursors; then consecutive digits are packed greedily into chunks of
-// at most cap keys (a digit above cap becomes an "oversize" chunk of its own).  Chunks are
-// collected in shared memory and appended with one atomic per list per CTA.
+// Chunk planner over a flat sequence of digits (consecutive key ranges: digit d holds
+// cnt[d] keys from gstart[d]; the large bins' digits bin after bin, or S9's buckets).
+// Consecutive digits are packed greedily into chunks of at most cap keys; a digit above cap
+// becomes an "oversize" chunk of its own.  Any contiguous key range is a valid chunk: a
+// k-mer's keys share one bin and one digit.  One CTA per segment of g.seg digits: a block
+// scan gives the prefix P of the segment's counts, then one thread walks the greedy chain
+// -- each chunk's end is found by a galloping search on P, so the serial work is
+// O(chunks x log(digits per chunk)) -- and the CTA appends its chunks with one atomic per
+// list.  The host sizes segments to hold ~64 chunks.
 constexpr int GP_NT = 256;
-constexpr int GP_SEG = 4096;
+constexpr int GP_SEGMAX = 8192;
 
 __global__ void __launch_bounds__(GP_NT) k_greedy_chunks(GreedyArgs g) {
     extern __shared__ __align__(16) uint32_t gsm[];
-    uint32_t* pre = gsm;                 // GP_SEG + 1
-    uint32_t* cs = pre + GP_SEG + 1;     // chunk starts (relative)
-    uint32_t* cn = cs + GP_SEG;          // chunk sizes; oversize chunks are marked by bit 31
+    const int seg = (int)g.seg;
+    uint32_t* P = gsm;              // seg + 1
+    uint32_t* cs = P + seg + 1;     // chunk starts (segment-relative)
+    uint32_t* cn = cs + seg;        // chunk sizes; bit 31: oversize
     __shared__ uint32_t wsum[GP_NT / 32 + 1];
-    __shared__ uint32_t nl_s, nreg_s, nover_s;
+    __shared__ uint32_t nl_s, nreg_s;
     __shared__ unsigned long long base_reg, base_over;
-    uint64_t dbase, kbase;
-    int nd;
-    if (g.lbins) {
-        const LargeBin lb = g.lbins[blockIdx.x];
-        dbase = lb.digit_base;
-        nd = 1 << lb.D;
-        kbase = lb.key_base;
-    } else {
-        dbase = (uint64_t)blockIdx.x * GP_SEG;
-        nd = (int)((g.n_digits - dbase) < (uint64_t)GP_SEG ? (g.n_digits - dbase) : (uint64_t)GP_SEG);
-        kbase = g.gstart[dbase];
-    }
+    const uint64_t dbase = (uint64_t)blockIdx.x * seg;
+    const int nd = (int)((g.n_digits - dbase) < (uint64_t)seg ? (g.n_digits - dbase) : (uint64_t)seg);
     const int ipt = (nd + GP_NT - 1) / GP_NT;
     const int d0 = threadIdx.x * ipt, d1 = min(nd, d0 + ipt);
-    uint32_t s = 0;
-    for (int d = d0; d < d1; ++d) s += g.cnt[dbase + d];
+    uint32_t sum = 0;
+    for (int d = d0; d < d1; ++d) sum += g.cnt[dbase + d];
     uint32_t total;
-    uint32_t P = block_excl_sum<GP_NT, uint32_t>(s, wsum, &total);
+    uint32_t run = block_excl_sum<GP_NT, uint32_t>(sum, wsum, &total);
     for (int d = d0; d < d1; ++d) {
-        pre[d] = P;
-        if (g.cursor) g.cursor[dbase + d] = g.cursor_abs ? (uint32_t)(kbase + P) : P;
-        P += g.cnt[dbase + d];
+        P[d] = run;
+        run += g.cnt[dbase + d];
     }
-    if (threadIdx.x == 0) pre[nd] = total;
+    if (threadIdx.x == 0) P[nd] = total;
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t nl = 0, nreg = 0, nover = 0, cstart = 0, acc = 0;
-        for (int d = 0; d < nd; ++d) {
-            const uint32_t c = pre[d + 1] - pre[d];
-            if (c > g.cap) {
-                if (acc) { cs[nl] = cstart; cn[nl++] = acc; ++nreg; acc = 0; }
-                cs[nl] = pre[d]; cn[nl++] = c | 0x80000000u; ++nover;
+        const uint32_t cap = g.cap;
+        int nl = 0, nreg = 0;
+        for (int d = 0; d < nd;) {
+            const uint32_t pd = P[d];
+            if (P[d + 1] - pd > cap) {
+                cs[nl] = pd;
+                cn[nl++] = (P[d + 1] - pd) | 0x80000000u;
+                ++d;
                 continue;
             }
-            if (acc + c > g.cap) { cs[nl] = cstart; cn[nl++] = acc; ++nreg; acc = 0; }
-            if (acc == 0) cstart = pre[d];
-            acc += c;
+            // largest e in (d, nd] with P[e] - P[d] <= cap: gallop, then bisect
+            int lo = d + 1, step = 1;
+            while (lo + step <= nd && P[lo + step] - pd <= cap) {
+                lo += step;
+                step *= 2;
+            }
+            int hi = min(lo + step, nd + 1);  // P[hi] - pd > cap, or hi = nd + 1
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (P[mid] - pd <= cap) lo = mid;
+                else hi = mid;
+            }
+            if (P[lo] != pd) {
+                cs[nl] = pd;
+                cn[nl++] = P[lo] - pd;
+                ++nreg;
+            }
+            d = lo;
         }
-        if (acc) { cs[nl] = cstart; cn[nl++] = acc; ++nreg; }
         nl_s = nl;
-        base_reg = nreg ? atomicAdd(&g.counters[0], (unsigned long long)nreg) : 0ull;
-        base_over = nover ? atomicAdd(&g.counters[1], (unsigned long long)nover) : 0ull;
         nreg_s = nreg;
-        nover_s = nover;
+        base_reg = nreg ? atomicAdd(&g.counters[0], (unsigned long long)nreg) : 0ull;
+        base_over = nl - nreg ? atomicAdd(&g.counters[1], (unsigned long long)(nl - nreg)) : 0ull;
     }
     __syncthreads();
-    // stable placement inside the CTA's reserved ranges (ballot ranks per list)
-    const uint32_t nl = nl_s;
-    __shared__ uint32_t run_reg, run_over;
+    // append in chain order (ballot ranks per list)
+    const uint64_t kbase = g.gstart[dbase];
+    const int nl = (int)nl_s;
+    __shared__ uint32_t run_reg, run_over, wr[GP_NT / 32], wo[GP_NT / 32];
     if (threadIdx.x == 0) { run_reg = 0; run_over = 0; }
     __syncthreads();
-    for (uint32_t i0 = 0; i0 < nl; i0 += GP_NT) {
-        const uint32_t i = i0 + threadIdx.x;
-        const bool ok = i < nl;
-        const uint32_t c = ok ? cn[i] : 0u;
-        const bool over = ok && (c & 0x80000000u);
-        const bool reg = ok && !over;
-        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lt = lanemask_lt();
+    for (int i0 = 0; i0 < nl; i0 += GP_NT) {
+        const int i = i0 + threadIdx.x;
+        const uint32_t c = i < nl ? cn[i] : 0u;
+        const bool over = i < nl && (c & 0x80000000u), reg = i < nl && !over;
         const uint32_t br = __ballot_sync(0xffffffffu, reg), bo = __ballot_sync(0xffffffffu, over);
-        __shared__ uint32_t wr[GP_NT / 32], wo[GP_NT / 32];
         if (lane == 0) { wr[warp] = __popc(br); wo[warp] = __popc(bo); }
         __syncthreads();
         uint32_t orr = run_reg, oo = run_over;
         for (uint32_t w = 0; w < warp; ++w) { orr += wr[w]; oo += wo[w]; }
-        const uint32_t lt = lanemask_lt();
         if (reg) g.chunks[base_reg + orr + __popc(br & lt)] = Chunk{kbase + cs[i], c, 0};
         if (over) g.oversize[base_over + oo + __popc(bo & lt)] = Chunk{kbase + cs[i], c & 0x7FFFFFFFu, 0};
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0)
             for (uint32_t w = 0; w < GP_NT / 32; ++w) { run_reg += wr[w]; run_over += wo[w]; }
-        }
         __syncthreads();
     }
 }
@@ -712,10 +717,13 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
 
 // Per-digit key counts of the large bins from the scanned segment table.
 __global__ void k_digit_totals(const LargeBin* __restrict__ lbins, const uint32_t* __restrict__ pos,
-                               uint32_t* __restrict__ cnt) {
+                               uint32_t* __restrict__ cnt, uint32_t* __restrict__ start) {
     const LargeBin lb = lbins[blockIdx.x];
-    for (int d = threadIdx.x; d < (1 << lb.D); d += blockDim.x)
-        cnt[lb.digit_base + d] = pos[lb.tb + (uint64_t)(d + 1) * lb.nseg] - pos[lb.tb + (uint64_t)d * lb.nseg];
+    for (int d = threadIdx.x; d < (1 << lb.D); d += blockDim.x) {
+        const uint32_t s0 = pos[lb.tb + (uint64_t)d * lb.nseg];
+        cnt[lb.digit_base + d] = pos[lb.tb + (uint64_t)(d + 1) * lb.nseg] - s0;
+        start[lb.digit_base + d] = s0;
+    }
 }
 
 __global__ void k_make_pieces(const LargeBin* __restrict__ lbins, const uint64_t* __restrict__ piece_prefix,
@@ -1007,16 +1015,21 @@ int msd_digit_bits(uint64_t bin_windows, int k, int cap) {
     return D;
 }
 
-cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaStream_t s) {
-    if (n_segments == 0) return cudaSuccess;
-    const int sm = (int)((GP_SEG + 1 + 2 * GP_SEG) * 4);
+cudaError_t launch_greedy_chunks(GreedyArgs g, uint64_t n_keys, cudaStream_t s) {
+    if (g.n_digits == 0) return cudaSuccess;
+    // ~64 chunks per segment: seg ~ 64 cap / (keys per digit), a power of two in [256, 8192]
+    const double per = std::max(1.0, (double)n_keys / (double)g.n_digits);
+    const double want = 64.0 * g.cap / per;
+    int seg = 256;
+    while (seg < GP_SEGMAX && seg < want) seg *= 2;
+    g.seg = (uint32_t)seg;
+    const uint64_t n_segments = (g.n_digits + seg - 1) / seg;
+    const int sm = (int)((3 * (size_t)seg + 1) * 4);
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_greedy_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
     k_greedy_chunks<<<(unsigned)n_segments, GP_NT, sm, s>>>(g);
     return cudaGetLastError();
 }
-
-uint64_t greedy_segments(uint64_t n_digits) { return (n_digits + GP_SEG - 1) / GP_SEG; }
 
 template <class K, bool SC>
 cudaError_t split_t(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins, int k,
@@ -1040,9 +1053,10 @@ cudaError_t launch_split(bool scatter, const uint32_t* bins, const Piece* pieces
 }
 
 cudaError_t launch_digit_totals(const LargeBin* lbins, uint64_t n_lbins, const uint32_t* pos, uint32_t* cnt,
+                                uint32_t* start,
                                 cudaStream_t s) {
     if (n_lbins == 0) return cudaSuccess;
-    k_digit_totals<<<(unsigned)n_lbins, 256, 0, s>>>(lbins, pos, cnt);
+    k_digit_totals<<<(unsigned)n_lbins, 256, 0, s>>>(lbins, pos, cnt, start);
     return cudaGetLastError();
 }
 

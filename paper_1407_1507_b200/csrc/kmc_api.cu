@@ -815,6 +815,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         uint64_t* d_pp = ar.get<uint64_t>(max_gn + 1);
         Piece* d_pieces = ar.get<Piece>(max_gp);
         uint32_t* digit_cnt = ar.get<uint32_t>(max_gd);
+        uint32_t* digit_start = ar.get<uint32_t>(max_gd);
         Chunk* chunks = ar.get<Chunk>(max_gd);
         Chunk* oversize = ar.get<Chunk>(max_gd);
         unsigned long long* counters = ar.get<unsigned long long>(3);
@@ -885,17 +886,16 @@ void count_phase(kmc_job* j, PlanCtx& c) {
             CK(launch_make_pieces(d_lbins, d_pp, gn, (uint32_t)prec, d_pieces, s));
             CK(launch_split(false, bins, d_pieces, n_pieces, d_lbins, k, dmax, R, table, nullptr, s));
             CK(scan_u32_to_u32(table, tpos, tb, ttemp, s));
-            CK(launch_digit_totals(d_lbins, gn, tpos, digit_cnt, s));
+            CK(launch_digit_totals(d_lbins, gn, tpos, digit_cnt, digit_start, s));
             GreedyArgs ga{};
             ga.cnt = digit_cnt;
-            ga.lbins = d_lbins;
-            ga.cursor = nullptr;
-            ga.cursor_abs = 0;
+            ga.gstart = digit_start;
+            ga.n_digits = digit_base;
             ga.chunks = chunks;
             ga.oversize = oversize;
             ga.counters = counters;
             ga.cap = (uint32_t)kcap;
-            CK(launch_greedy_chunks(ga, gn, s));
+            CK(launch_greedy_chunks(ga, key_base, s));
             j->launches += 6;
             j->stage_end(6);
             j->stage_begin(KMC_STAGE_LARGE_SCATTER);

@@ -164,25 +164,24 @@ int msd_digit_bits(uint64_t bin_windows, int k, int cap);
 // bin, 2^D digits each, chunk keys at key_base + bin-relative offsets) or 4096-digit windows
 // of a global digit array (lbins == nullptr; gstart = exclusive scan of cnt).
 struct GreedyArgs {
-    const uint32_t* cnt;
-    const LargeBin* lbins;
-    const uint32_t* gstart;
+    const uint32_t* cnt;     // keys per digit
+    const uint32_t* gstart;  // position of each digit's first key
     uint64_t n_digits;
-    uint32_t* cursor;     // per-digit scatter cursor (may be nullptr)
-    int cursor_abs;       // 1: cursor = key_base + prefix; 0: bin-relative prefix
     Chunk* chunks;
     Chunk* oversize;
     unsigned long long* counters;  // [0] chunks, [1] oversize
     uint32_t cap;
+    uint32_t seg;  // digits per CTA (set by launch_greedy_chunks)
 };
-cudaError_t launch_greedy_chunks(const GreedyArgs& g, uint64_t n_segments, cudaStream_t s);
-uint64_t greedy_segments(uint64_t n_digits);
+// n_keys: total keys of the digits (sizes the segments)
+cudaError_t launch_greedy_chunks(GreedyArgs g, uint64_t n_keys, cudaStream_t s);
 // Split of the large bins into digit-contiguous key ranges (k_split): count pass (table of
 // per-(bin, digit, segment) counts), then, after an exclusive scan of the table, the scatter.
 cudaError_t launch_split(bool scatter, const uint32_t* bins, const Piece* pieces, uint64_t n_pieces,
                          const LargeBin* lbins, int k, int dmax, uint32_t n_ranges, uint32_t* table, void* keys,
                          cudaStream_t s);
 cudaError_t launch_digit_totals(const LargeBin* lbins, uint64_t n_lbins, const uint32_t* pos, uint32_t* cnt,
+                                uint32_t* start,
                                 cudaStream_t s);
 cudaError_t launch_chunk_sort(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
                               uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
