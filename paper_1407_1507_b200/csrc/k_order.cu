@@ -13,8 +13,6 @@
 // (k_greedy_chunks) and every chunk is sorted in shared memory and written straight into
 // the caller's output at its offset.  A bucket holding more than CAP survivors is returned
 // to the caller for the device-wide LSD path.
-#include <cstdio>
-#include <cstdlib>
 #include <algorithm>
 #include <vector>
 
