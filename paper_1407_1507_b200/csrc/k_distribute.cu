@@ -199,22 +199,48 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
         // ---- C: canonical p-mer keys at local 15 + y, in registers:
         //      lane l holds positions y = 18 l + o, o < 18 (NROW * 32 = 576 >= SEG + W).
         //      key = min(fwd, rc) if the p-mer is valid and allowed, else the reserved 4^p (R4).
+        //      The lane's 32 symbols from its first position are one 64-bit field X (MSB
+        //      first); its complement reversed, R, holds every reverse complement:
+        //      rc(o) = (R >> 2o) mod 4^p.  Allowedness (R2) is evaluated for all positions
+        //      at once on 2-bit-spaced indicator masks of the LSB-first stream Y = ~R:
+        //      forward p-mer at o is excluded iff an AA pair starts in [o+1, o+p-2] or ACA
+        //      starts at o; its reverse complement iff a TT pair starts in [o, o+p-3] or TGT
+        //      starts at o+p-3.
         const int y0 = 18 * lane;
         uint32_t K[18];
         {
             const int j0 = 15 + y0;  // local base of position y0
             const int w0 = j0 >> 4, sh = 2 * (j0 & 15);
-            const uint32_t W0 = S.pk[w0], W1 = S.pk[w0 + 1], W2 = S.pk[w0 + 2], W3 = S.pk[w0 + 3];
-            const uint32_t sA = __funnelshift_l(W1, W0, sh), sB = __funnelshift_l(W2, W1, sh),
-                           sC = __funnelshift_l(W3, W2, sh);  // symbols j0 .. j0 + 47, MSB first
+            const uint32_t W0 = S.pk[w0], W1 = S.pk[w0 + 1], W2 = S.pk[w0 + 2];
+            const uint32_t sA = __funnelshift_l(W1, W0, sh), sB = __funnelshift_l(W2, W1, sh);  // X = sA:sB
+            const uint32_t Rlo = rev2_32(~sA), Rhi = rev2_32(~sB);
             const uint32_t pvb = __funnelshift_r(S.vpm[j0 >> 5], S.vpm[(j0 >> 5) + 1], j0 & 31);
+            uint64_t fbad = 0, rbad = 0;  // bit 2o: the forward / reverse p-mer at o is not allowed
+            if (p >= 3) {
+                constexpr uint64_t M5 = 0x5555555555555555ull;
+                const uint64_t Y = ~(((uint64_t)Rhi << 32) | Rlo), y1 = Y >> 1;
+                const uint64_t iA = ~(Y | y1) & M5, iT = Y & y1 & M5, iC = Y & ~y1 & M5, iG = ~Y & y1 & M5;
+                uint64_t ua = iA & (iA >> 2), ut = iT & (iT >> 2);  // AA / TT pair starts
+                const int L = p - 2;  // OR over [i, i + L) by doubling
+                int A = 1;
+                while (2 * A <= L) {
+                    ua |= ua >> (2 * A);
+                    ut |= ut >> (2 * A);
+                    A *= 2;
+                }
+                ua |= ua >> (2 * (L - A));
+                ut |= ut >> (2 * (L - A));
+                fbad = (ua >> 2) | (iA & (iC >> 2) & (iA >> 4));
+                rbad = ut | ((iT & (iG >> 2) & (iT >> 4)) >> (2 * (p - 3)));
+            }
+            const uint32_t mp = (uint32_t)(RES - 1);
 #pragma unroll
             for (int o = 0; o < 18; ++o) {
-                const uint32_t x16 = o < 16 ? __funnelshift_l(sB, sA, 2 * o) : __funnelshift_l(sC, sB, 2 * (o - 16));
-                const uint32_t fwd = x16 >> (32 - 2 * p);
-                const uint32_t rc = rev2_32(~fwd) >> (32 - 2 * p);
-                const uint32_t cn = min(fwd, rc);
-                K[o] = (((pvb >> o) & 1u) && sig_allowed(cn, p)) ? cn : RES;
+                const uint32_t fwd = (o < 16 ? __funnelshift_l(sB, sA, 2 * o) : (sB << (2 * (o - 16)))) >> (32 - 2 * p);
+                const uint32_t rc = (o < 16 ? __funnelshift_r(Rlo, Rhi, 2 * o) : (Rhi >> (2 * (o - 16)))) & mp;
+                const bool fw = fwd <= rc;
+                const uint32_t bad = (uint32_t)((fw ? fbad : rbad) >> (2 * o)) & 1u;
+                K[o] = (((pvb >> o) & 1u) && !bad) ? (fw ? fwd : rc) : RES;
             }
         }
         // ---- D: sliding minimum over W keys: window y = min over keys [y, y + W)
