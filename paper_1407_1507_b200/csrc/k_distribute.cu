@@ -462,7 +462,8 @@ template <int RW>
 __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restrict__ in_recs,
                                                        const uint32_t* __restrict__ in_ids,
                                                        const uint32_t* __restrict__ sig2bin,
-                                                       const RecTile2* __restrict__ tiles, int shift, int D,
+                                                       const RecTile2* __restrict__ tiles,
+                                                       const uint64_t* __restrict__ n_tiles, int shift, int D,
                                                        unsigned long long* __restrict__ cursor,
                                                        uint32_t* __restrict__ out_recs, uint32_t* __restrict__ out_ids,
                                                        int out_orig_ids) {
@@ -476,6 +477,7 @@ __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restric
     uint32_t* wsum = reinterpret_cast<uint32_t*>(gb + 256);
     uint8_t* sd = reinterpret_cast<uint8_t*>(wsum + 64);
     __shared__ uint32_t s_tot;
+    if (n_tiles && blockIdx.x >= *n_tiles) return;
     const RecTile2 t = tiles[blockIdx.x];
     const int nd = 1 << D;
     for (int d = threadIdx.x; d < 256; d += RS_NT) lh[d] = 0;
@@ -615,21 +617,21 @@ cudaError_t launch_p1(int mode, const P1Args& a, uint64_t n_tiles, cudaStream_t 
 size_t rec_tile_items(int k) { return record_words(k) == 4 ? RecTile<4>::v : RecTile<8>::v; }
 
 cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* in_ids, const uint32_t* sig2bin,
-                               const RecTile2* tiles, uint64_t n_tiles, int shift, int D,
-                               unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids, cudaStream_t s,
-                               int out_orig_ids) {
-    if (n_tiles == 0) return cudaSuccess;
+                               const RecTile2* tiles, uint64_t max_tiles, const uint64_t* n_tiles_dev, int shift,
+                               int D, unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids,
+                               cudaStream_t s, int out_orig_ids) {
+    if (max_tiles == 0) return cudaSuccess;
     cudaError_t e;
     if (record_words(k) == 4) {
         const int sm = (int)rec_scatter_smem<4>();
         if ((e = cudaFuncSetAttribute(k_rec_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-        k_rec_scatter<4><<<(unsigned)n_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, shift, D, cursor,
-                                                             out_recs, out_ids, out_orig_ids);
+        k_rec_scatter<4><<<(unsigned)max_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, n_tiles_dev, shift, D,
+                                                               cursor, out_recs, out_ids, out_orig_ids);
     } else {
         const int sm = (int)rec_scatter_smem<8>();
         if ((e = cudaFuncSetAttribute(k_rec_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-        k_rec_scatter<8><<<(unsigned)n_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, shift, D, cursor,
-                                                             out_recs, out_ids, out_orig_ids);
+        k_rec_scatter<8><<<(unsigned)max_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, n_tiles_dev, shift, D,
+                                                               cursor, out_recs, out_ids, out_orig_ids);
     }
     return cudaGetLastError();
 }

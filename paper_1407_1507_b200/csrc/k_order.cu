@@ -58,8 +58,10 @@ __device__ __forceinline__ uint32_t hi_digit(const K128& key, int twok, int D) {
 // Histogram of the digit (bits [top - D, top)) over one tile per CTA.
 template <class K>
 __global__ void __launch_bounds__(OT_NT) k_ord_hist(const K* __restrict__ keys, const OrdTile* __restrict__ tiles,
-                                                    int top, int D, uint32_t* __restrict__ hist) {
+                                                    const uint64_t* __restrict__ n_tiles, int top, int D,
+                                                    uint32_t* __restrict__ hist) {
     __shared__ uint32_t h[256];
+    if (blockIdx.x >= *n_tiles) return;
     const OrdTile t = tiles[blockIdx.x];
     for (int d = threadIdx.x; d < (1 << D); d += OT_NT) h[d] = 0;
     __syncthreads();
@@ -74,7 +76,8 @@ __global__ void __launch_bounds__(OT_NT) k_ord_hist(const K* __restrict__ keys, 
 // the tile's run, then the tile is written in digit order -- consecutive addresses per run.
 template <class K>
 __global__ void __launch_bounds__(OT_NT) k_ord_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                       const OrdTile* __restrict__ tiles, int top, int D,
+                                                       const OrdTile* __restrict__ tiles,
+                                                       const uint64_t* __restrict__ n_tiles, int top, int D,
                                                        uint32_t* __restrict__ cursor, K* __restrict__ kout,
                                                        uint32_t* __restrict__ vout) {
     constexpr int TI = OrderTile<K>::v, IPT = TI / OT_NT;
@@ -85,6 +88,7 @@ __global__ void __launch_bounds__(OT_NT) k_ord_scatter(const K* __restrict__ kin
     uint32_t* gb = lh + 256;    // 256: global base of the tile's run per digit
     uint32_t* wsum = gb + 256;  // scan scratch
     uint8_t* sd = reinterpret_cast<uint8_t*>(wsum + 64);
+    if (blockIdx.x >= *n_tiles) return;
     const OrdTile t = tiles[blockIdx.x];
     const int nd = 1 << D;
     for (int d = threadIdx.x; d < 256; d += OT_NT) lh[d] = 0;
@@ -156,6 +160,153 @@ __global__ void __launch_bounds__(OC_NT, 2) k_order_chunk_sort(const K* __restri
     }
 }
 
+// ---- after the MSD passes (64-bit keys): most buckets hold a few survivors (7 on average
+// at C4, 221 at most), so they are sorted by warps in registers instead of by CTA radix
+// sorts.  k_ord_classify puts every bucket into a list by size: "groups" of consecutive
+// buckets of <= 32 survivors that start in the same 32-item window of the array (so a
+// group holds < 64 items; sorting the union of whole, consecutive buckets by the full key
+// is the same as sorting each bucket), buckets of 33-64 / 65-128 / 129-256 survivors, up to
+// the chunk capacity (CTA radix sort), and above it (oversize, device LSD).  Lists are
+// appended with one atomic per CTA and list; their order is irrelevant.
+constexpr int WS_NT = 256;
+
+__global__ void __launch_bounds__(WS_NT) k_ord_classify(const uint32_t* __restrict__ cnt,
+                                                        const uint32_t* __restrict__ start, uint64_t nbk,
+                                                        uint32_t n, uint32_t cap, uint2* __restrict__ wl,
+                                                        Chunk* __restrict__ big, Chunk* __restrict__ over,
+                                                        unsigned long long* __restrict__ counters) {
+    __shared__ uint32_t wsum[WS_NT / 32 + 1];
+    __shared__ unsigned long long base[5];
+    const uint64_t d = (uint64_t)blockIdx.x * WS_NT + threadIdx.x;
+    int cls = -1;  // 0/1/2: warp sort of 64/128/256 items, 3: CTA sort, 4: oversize
+    uint32_t st = 0, sz = 0;
+    if (d < nbk) {
+        const uint32_t c = cnt[d];
+        st = start[d];
+        if (c > 32) {
+            sz = c;
+            cls = c <= 64 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= cap ? 3 : 4;
+        } else {
+            const bool lead = d == 0 || cnt[d - 1] > 32 || (start[d - 1] >> 5) != (st >> 5);
+            if (lead) {
+                uint64_t e = d + 1;
+                while (e < nbk && cnt[e] <= 32 && (start[e] >> 5) == (st >> 5)) ++e;
+                sz = (e < nbk ? start[e] : n) - st;
+                if (sz) cls = 0;
+            }
+        }
+    }
+    uint32_t off[5], tot[5];
+#pragma unroll
+    for (int l = 0; l < 5; ++l) off[l] = block_excl_sum<WS_NT, uint32_t>(cls == l ? 1u : 0u, wsum, &tot[l]);
+    if (threadIdx.x < 5) {
+        const uint32_t t = tot[0] * (threadIdx.x == 0) + tot[1] * (threadIdx.x == 1) + tot[2] * (threadIdx.x == 2) +
+                           tot[3] * (threadIdx.x == 3) + tot[4] * (threadIdx.x == 4);
+        base[threadIdx.x] = t ? atomicAdd(&counters[threadIdx.x], (unsigned long long)t) : 0ull;
+    }
+    __syncthreads();
+    if (cls >= 0) {
+        const Chunk ch{st, sz, 0};
+        const uint64_t q = base[cls] + off[cls];
+        if (cls == 0) wl[q] = make_uint2(st, sz);
+        else if (cls == 1) wl[nbk + q] = make_uint2(st, sz);
+        else if (cls == 2) wl[2 * nbk - 1 - q] = make_uint2(st, sz);
+        else if (cls == 3) big[q] = ch;
+        else over[q] = ch;
+    }
+}
+
+// One warp sorts one list item of <= 32 R (key, count) pairs in registers: element
+// i = lane + 32 r, padded with the all-ones key (never a canonical k-mer); bitonic network,
+// exchanges across lanes by shuffles (distance < 32) or between a lane's registers.
+// PACK (2k <= 56): the network sorts key << 8 | i (one 64-bit word per element) and the
+// counts follow through a shared-memory permutation afterwards.
+template <int R, bool PACK>
+__global__ void __launch_bounds__(WS_NT) k_ord_wsort(const uint64_t* __restrict__ keys,
+                                                     const uint32_t* __restrict__ vals, const uint2* __restrict__ items,
+                                                     uint64_t n_items, int dir, uint64_t* __restrict__ out_keys,
+                                                     uint32_t* __restrict__ out_vals) {
+    constexpr int N = 32 * R;
+    __shared__ uint32_t svals[PACK ? WS_NT / 32 : 1][PACK ? N : 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t w = (uint64_t)blockIdx.x * (WS_NT / 32) + wid;
+    if (w >= n_items) return;
+    const uint2 it = items[dir * (int64_t)w];  // dir = -1: the list grows downwards from items
+    const Chunk c{it.x, it.y, 0};
+    uint64_t k[R];
+    uint32_t v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = lane + 32 * r;
+        const uint64_t key = i < c.n ? ld_stream(keys + c.begin + i) : ~0ull;
+        const uint32_t val = i < c.n ? __ldcs(vals + c.begin + i) : 0u;
+        if (PACK) {
+            k[r] = i < c.n ? (key << 8) | i : ~0ull;
+            svals[wid][i] = val;
+        } else {
+            k[r] = key;
+            v[r] = val;
+        }
+    }
+#pragma unroll
+    for (int sz = 2; sz <= N; sz <<= 1) {
+#pragma unroll
+        for (int j = sz >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j / 32;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r & jr) continue;
+                    const int h = r | jr;
+                    const bool up = ((lane + 32 * r) & sz) == 0;
+                    const uint64_t lo = k[r] < k[h] ? k[r] : k[h], hi = k[r] < k[h] ? k[h] : k[r];
+                    if (PACK) {
+                        k[r] = up ? lo : hi;
+                        k[h] = up ? hi : lo;
+                    } else if (up ? k[r] > k[h] : k[r] < k[h]) {
+                        k[r] = up ? lo : hi;
+                        k[h] = up ? hi : lo;
+                        const uint32_t tv = v[r];
+                        v[r] = v[h];
+                        v[h] = tv;
+                    }
+                }
+            } else {
+                const bool lower = (lane & j) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint64_t pk = __shfl_xor_sync(0xffffffffu, k[r], j);
+                    const bool want_min = (((lane + 32 * r) & sz) == 0) == lower;
+                    if (PACK) {
+                        k[r] = want_min ? (pk < k[r] ? pk : k[r]) : (pk > k[r] ? pk : k[r]);
+                    } else {
+                        const uint32_t pv = __shfl_xor_sync(0xffffffffu, v[r], j);
+                        const bool take = want_min ? pk < k[r] : pk > k[r];
+                        if (take) {
+                            k[r] = pk;
+                            v[r] = pv;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (PACK) __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = lane + 32 * r;
+        if (i < c.n) {
+            if (PACK) {
+                out_keys[c.begin + i] = k[r] >> 8;
+                out_vals[c.begin + i] = svals[wid][k[r] & 0xFF];
+            } else {
+                out_keys[c.begin + i] = k[r];
+                out_vals[c.begin + i] = v[r];
+            }
+        }
+    }
+}
+
 // MSD levels: D_l <= 8 bits each, until the average bucket holds at most cap/8 survivors
 int order_levels(uint64_t n, int k, int cap, int* D) {
     const int twok = 2 * k;
@@ -182,70 +333,106 @@ cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uin
     uint32_t* cv = vals;
     K* ok = (K*)os.tmp_keys;  // the other buffers
     uint32_t* ov = os.tmp_vals;
-    std::vector<uint32_t> counts(1, (uint32_t)n);  // items per bucket of the previous level
-    uint64_t nbk = 1;                               // buckets of the previous level
+    uint64_t nbk = 1;  // buckets of the previous level
     int top = twok;
-    std::vector<OrdTile> tl;
+    static_assert(sizeof(OrdTile) == sizeof(RecTile2), "tiles share the generator");
     for (int l = 0; l < L; ++l) {
-        // tiles of at most TI items inside each bucket of the previous level
-        tl.clear();
-        uint64_t b0 = 0;
-        for (uint64_t b = 0; b < nbk; ++b) {
-            const uint64_t c = counts[b];
-            for (uint64_t o = 0; o < c; o += TI)
-                tl.push_back(OrdTile{b0 + o, (uint32_t)std::min<uint64_t>(TI, c - o), (uint32_t)b});
-            b0 += c;
-        }
-        const uint64_t nd = nbk << D[l];
-        if (tl.empty()) continue;  // (n > 0, so only a pass after an empty previous one)
-        if ((e = cudaMemcpyAsync(os.tiles, tl.data(), tl.size() * sizeof(OrdTile), cudaMemcpyHostToDevice, s)))
+        // tiles of at most TI items inside each bucket of the previous level, built on the
+        // device from the previous level's bucket starts (before this level's scan
+        // overwrites them)
+        const uint64_t mt = n / TI + nbk;
+        const TileSrc src = l == 0 ? TileSrc{nullptr, 0, 0, 0, n} : TileSrc{os.start, 0, nbk, 0, n};
+        if ((e = launch_make_tiles(src, nbk, (uint32_t)TI, mt, os.tprefix, os.ttemp,
+                                   reinterpret_cast<RecTile2*>(os.tiles), s)))
             return e;
+        const uint64_t* ntl = os.tprefix + nbk;
+        const uint64_t nd = nbk << D[l];
         if ((e = cudaMemsetAsync(os.hist, 0, nd * 4, s))) return e;
-        k_ord_hist<K><<<(unsigned)tl.size(), OT_NT, 0, s>>>(ck, os.tiles, top, D[l], os.hist);
+        k_ord_hist<K><<<(unsigned)mt, OT_NT, 0, s>>>(ck, os.tiles, ntl, top, D[l], os.hist);
         if ((e = cudaGetLastError())) return e;
         if ((e = scan_detail::scan_generic<uint32_t>(scan_detail::ArrayIn<uint32_t>{os.hist}, nd, os.start,
                                                      (uint32_t*)os.scan_temp, s, launches)))
             return e;
         if ((e = cudaMemcpyAsync(os.cursor, os.start, nd * 4, cudaMemcpyDeviceToDevice, s))) return e;
-        k_ord_scatter<K><<<(unsigned)tl.size(), OT_NT, osm, s>>>(ck, cv, os.tiles, top, D[l], os.cursor, ok, ov);
+        k_ord_scatter<K><<<(unsigned)mt, OT_NT, osm, s>>>(ck, cv, os.tiles, ntl, top, D[l], os.cursor, ok, ov);
         if ((e = cudaGetLastError())) return e;
-        *launches += 2;
+        *launches += 5;
         std::swap(ck, ok);
         std::swap(cv, ov);
         top -= D[l];
         nbk = nd;
-        if (l + 1 < L) {
-            counts.resize(nd);
-            if ((e = cudaMemcpyAsync(counts.data(), os.hist, nd * 4, cudaMemcpyDeviceToHost, s))) return e;
-            if ((e = cudaStreamSynchronize(s))) return e;
-        }
     }
-    // ---- chunks of consecutive buckets, sorted in shared memory into the output
-    if ((e = cudaMemsetAsync(os.counters, 0, 16, s))) return e;
-    GreedyArgs ga{};
-    ga.cnt = os.hist;
-    ga.gstart = os.start;
-    ga.n_digits = nbk;
-    ga.chunks = os.chunks;
-    ga.oversize = os.oversize;
-    ga.counters = os.counters;
-    ga.cap = OrderCap<K>::v;
-    if ((e = launch_greedy_chunks(ga, n, s))) return e;
-    if ((e = cudaMemcpyAsync(os.host, os.counters, 16, cudaMemcpyDeviceToHost, s))) return e;
-    if ((e = cudaStreamSynchronize(s))) return e;
-    const uint64_t n_chunks = os.host[0], n_over = os.host[1];
+    // ---- the buckets, sorted into the output: by warps (64-bit keys, buckets <= 256 items),
+    //      by CTAs in shared memory (chunks of consecutive buckets), or returned as oversize
+    if ((e = cudaMemsetAsync(os.counters, 0, 64, s))) return e;
+    uint64_t n_chunks = 0, n_over = 0;
+    const Chunk* chunk_list = os.chunks;
+    const Chunk* over_list = os.oversize;
     const size_t sm = order_smem<K>();
     if ((e = cudaFuncSetAttribute(k_order_chunk_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
+    if constexpr (sizeof(K) == 8) {
+        // lists in buffers the MSD passes are done with: the warp-sort lists {begin, n} in
+        // os.chunks (2 nbk uint2: 64-item sorts from the front of the first half, 128 / 256
+        // from both ends of the second), CTA chunks in os.oversize, oversize buckets (at
+        // most n / cap + 1 of them) in os.cursor
+        uint2* wlist = reinterpret_cast<uint2*>(os.chunks);
+        Chunk* big = os.oversize;
+        Chunk* over = reinterpret_cast<Chunk*>(os.cursor);
+        static_assert(sizeof(Chunk) == 2 * sizeof(uint2), "two list entries per chunk slot");
+        k_ord_classify<<<(unsigned)((nbk + WS_NT - 1) / WS_NT), WS_NT, 0, s>>>(
+            os.hist, os.start, nbk, (uint32_t)n, OrderCap<K>::v, wlist, big, over, os.counters);
+        chunk_list = big;
+        over_list = over;
+        if ((e = cudaGetLastError())) return e;
+        if ((e = cudaMemcpyAsync(os.host, os.counters, 40, cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaStreamSynchronize(s))) return e;
+        const uint64_t nw0 = os.host[0], nw1 = os.host[1], nw2 = os.host[2];
+        n_chunks = os.host[3];
+        n_over = os.host[4];
+        constexpr int WPB = WS_NT / 32;
+        const uint2* wl[3] = {wlist, wlist + nbk, wlist + 2 * nbk - 1};
+        const int dir[3] = {1, 1, -1};
+        const uint64_t nw[3] = {nw0, nw1, nw2};
+        const bool pack = twok <= 56;
+        for (int q = 0; q < 3; ++q) {
+            if (!nw[q]) continue;
+            const unsigned g = (unsigned)((nw[q] + WPB - 1) / WPB);
+#define KMC_WSORT(R)                                                                                          \
+    (pack ? k_ord_wsort<R, true><<<g, WS_NT, 0, s>>>(ck, cv, wl[q], nw[q], dir[q], out_keys, out_vals)          \
+          : k_ord_wsort<R, false><<<g, WS_NT, 0, s>>>(ck, cv, wl[q], nw[q], dir[q], out_keys, out_vals))
+            if (q == 0) KMC_WSORT(2);
+            if (q == 1) KMC_WSORT(4);
+            if (q == 2) KMC_WSORT(8);
+#undef KMC_WSORT
+        }
+        if ((e = cudaGetLastError())) return e;
+        *launches += 1 + (nw0 > 0) + (nw1 > 0) + (nw2 > 0);
+    } else {
+        GreedyArgs ga{};
+        ga.cnt = os.hist;
+        ga.gstart = os.start;
+        ga.n_digits = nbk;
+        ga.chunks = os.chunks;
+        ga.oversize = os.oversize;
+        ga.counters = os.counters;
+        ga.cap = OrderCap<K>::v;
+        if ((e = launch_greedy_chunks(ga, n, s))) return e;
+        if ((e = cudaMemcpyAsync(os.host, os.counters, 16, cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaStreamSynchronize(s))) return e;
+        n_chunks = os.host[0];
+        n_over = os.host[1];
+        *launches += 1;
+    }
     if (n_chunks)
-        k_order_chunk_sort<K><<<(unsigned)n_chunks, OC_NT, sm, s>>>(ck, cv, os.chunks, twok, out_keys, out_vals);
+        k_order_chunk_sort<K><<<(unsigned)n_chunks, OC_NT, sm, s>>>(ck, cv, chunk_list, twok, out_keys, out_vals);
     if ((e = cudaGetLastError())) return e;
-    *launches += 2;
+    *launches += n_chunks > 0;
     oversize->clear();
     *seg_keys = ck;
     *seg_vals = cv;
     if (n_over) {
         std::vector<Chunk> ovs(n_over);
-        if ((e = cudaMemcpyAsync(ovs.data(), os.oversize, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaMemcpyAsync(ovs.data(), over_list, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s))) return e;
         if ((e = cudaStreamSynchronize(s))) return e;
         for (auto& c : ovs) oversize->push_back(OrderSegment{c.begin, c.n});
     }
@@ -271,6 +458,14 @@ uint64_t order_max_tiles(uint64_t n, int k) {
     int prev = 0;
     for (int l = 0; l + 1 < L; ++l) prev += D[l];
     return n / order_tile_items(k <= 32 ? 1 : 2) + (1ull << prev) + 1;
+}
+
+uint64_t order_prev_buckets(uint64_t n, int k) {
+    int D[4];
+    const int L = order_levels(n, k, k <= 32 ? OrderCap<uint64_t>::v : OrderCap<K128>::v, D);
+    int prev = 0;
+    for (int l = 0; l + 1 < L; ++l) prev += D[l];
+    return 1ull << prev;
 }
 
 size_t order_scan_temp_bytes(uint64_t n_digits) { return scan_detail::scan_temp_elems<uint64_t>(n_digits) * 8; }

@@ -75,7 +75,49 @@ __global__ void k_bins(uint64_t ns, const uint64_t* B, const uint64_t* bin_first
     }
 }
 
+__device__ __forceinline__ uint64_t tile_src_start(const TileSrc& t, uint64_t b) {
+    if (!t.base) return b == 0 ? 0 : t.total;
+    const uint64_t i = b << t.sh;
+    if (i >= t.nbase) return t.total;
+    return t.is64 ? reinterpret_cast<const uint64_t*>(t.base)[i] : reinterpret_cast<const uint32_t*>(t.base)[i];
+}
+
+__global__ void k_tile_count(TileSrc t, uint64_t nb, uint32_t TI, uint64_t* __restrict__ cnt) {
+    const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    cnt[b] = (tile_src_start(t, b + 1) - tile_src_start(t, b) + TI - 1) / TI;
+}
+
+// thread per tile: its bucket by binary search on the tile prefix
+__global__ void k_tile_fill(TileSrc t, uint64_t nb, uint32_t TI, const uint64_t* __restrict__ prefix,
+                            RecTile2* __restrict__ tiles) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= prefix[nb]) return;
+    uint64_t lo = 0, hi = nb;  // last b with prefix[b] <= i
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (prefix[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    const uint64_t s0 = tile_src_start(t, lo), s1 = tile_src_start(t, lo + 1);
+    const uint64_t beg = s0 + (i - prefix[lo]) * TI;
+    tiles[i] = RecTile2{beg, (uint32_t)(s1 - beg < TI ? s1 - beg : TI), (uint32_t)lo};
+}
+
 }  // namespace
+
+cudaError_t launch_make_tiles(const TileSrc& src, uint64_t nb, uint32_t TI, uint64_t max_tiles, uint64_t* prefix,
+                              void* temp, RecTile2* tiles, cudaStream_t s) {
+    cudaError_t e;
+    if (nb == 0) return cudaMemsetAsync(prefix, 0, 8, s);
+    k_tile_count<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(src, nb, TI, prefix);
+    if ((e = cudaGetLastError())) return e;
+    // in-place exclusive scan: the scan reads its input before writing each output block
+    if ((e = scan_generic<uint64_t>(ArrayIn<uint64_t>{prefix}, nb, prefix, (uint64_t*)temp, s, nullptr))) return e;
+    if (max_tiles == 0) return cudaSuccess;
+    k_tile_fill<<<(unsigned)((max_tiles + 255) / 256), 256, 0, s>>>(src, nb, TI, prefix, tiles);
+    return cudaGetLastError();
+}
 
 size_t scan_temp_bytes(uint64_t n) { return scan_temp_elems<uint64_t>(n) * sizeof(uint64_t); }
 

@@ -615,43 +615,40 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         const int L = (int)D.size();
         const uint64_t TI = rec_tile_items(k);
         unsigned long long* cursor = ar.get<unsigned long long>((1ull << B) + 1);
-        RecTile2* d_tiles = ar.get<RecTile2>(std::max(tmp_n, n_records) / TI + n_bins + 2);  // + one partial tile per bucket
+        const uint64_t max_tiles = std::max(tmp_n, n_records) / TI + n_bins + 2;  // + one partial tile per bucket
+        RecTile2* d_tiles = ar.get<RecTile2>(max_tiles);
+        uint64_t* t_prefix = ar.get<uint64_t>(n_bins + 2);
+        void* t_temp = ar.alloc(scan_temp_bytes(n_bins + 2));
         uint32_t* x_recs = L > 1 ? reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4)) : nullptr;
         uint32_t* x_ids = L > 1 ? ar.get<uint32_t>(n_records) : nullptr;
         const uint32_t* in_r = tmp_recs;
         const uint32_t* in_i = tmp_sig;
-        std::vector<RecTile2> tl;
         int prefix = 0;
         for (int l = 0; l < L; ++l) {
             const int shift_prev = B - prefix;
             prefix += D[l];
             const int shift = B - prefix;
-            tl.clear();
-            if (l == 0) {
-                for (uint64_t o = 0; o < tmp_n; o += TI)
-                    tl.push_back(RecTile2{o, (uint32_t)std::min<uint64_t>(TI, tmp_n - o), 0});
-            } else {
-                const uint64_t nbp = (n_bins + (1ull << shift_prev) - 1) >> shift_prev;
-                for (uint64_t v = 0; v < nbp; ++v) {
-                    const uint64_t b0 = v << shift_prev, b1 = std::min<uint64_t>(n_bins, (v + 1) << shift_prev);
-                    const uint64_t r0 = bo[b0], r1 = b1 < n_bins ? bo[b1] : n_records;
-                    for (uint64_t o = r0; o < r1; o += TI)
-                        tl.push_back(RecTile2{o, (uint32_t)std::min<uint64_t>(TI, r1 - o), (uint32_t)v});
-                }
+            // tiles (device-built): pass 0 cuts the stream, later passes every bucket of the
+            // previous pass (bins [v << shift_prev, (v + 1) << shift_prev))
+            uint64_t nbp = 1, mt = tmp_n / TI + 1;
+            TileSrc src{nullptr, 1, 0, 0, tmp_n};
+            if (l > 0) {
+                nbp = (n_bins + (1ull << shift_prev) - 1) >> shift_prev;
+                mt = n_records / TI + nbp;
+                src = TileSrc{pa.bin_rec_off, 1, n_bins, shift_prev, n_records};
             }
+            CK(launch_make_tiles(src, nbp, (uint32_t)TI, mt, t_prefix, t_temp, d_tiles, s));
             const uint64_t nbk = (n_bins + (1ull << shift) - 1) >> shift;
             CK(launch_bucket_cursors(pa.bin_rec_off, n_bins, n_records, shift, nbk, cursor, s));
-            if (!tl.empty())
-                CK(cudaMemcpyAsync(d_tiles, tl.data(), tl.size() * sizeof(RecTile2), cudaMemcpyHostToDevice, s));
             // ping-pong: the last pass writes the bins; others alternate x / tmp buffers
             uint32_t* out_r = (l == L - 1) ? bins : ((l & 1) == 0 ? x_recs : tmp_recs);
             uint32_t* out_i = (l == L - 1) ? nullptr : ((l & 1) == 0 ? x_ids : tmp_sig);
-            CK(launch_rec_scatter(k, in_r, in_i, l == 0 ? pa.sig2bin : nullptr, d_tiles, tl.size(), shift, D[l],
-                                  cursor, out_r, out_i, s));
+            CK(launch_rec_scatter(k, in_r, in_i, l == 0 ? pa.sig2bin : nullptr, d_tiles, mt, t_prefix + nbp, shift,
+                                  D[l], cursor, out_r, out_i, s));
             // the pass reads from in_* while writing out_*: tmp is only an output from pass 2 on
             in_r = out_r;
             in_i = out_i;
-            s5_launches += 2;
+            s5_launches += 5;
         }
         ar.release(x_recs);
         ar.release(x_ids);
@@ -998,8 +995,10 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     os.cursor = ar.get<uint32_t>(nd);
     os.chunks = ar.get<Chunk>(nd);
     os.oversize = ar.get<Chunk>(nd);
-    os.counters = ar.get<unsigned long long>(2);
+    os.counters = ar.get<unsigned long long>(8);
     os.tiles = ar.get<OrdTile>(order_max_tiles(n, j->k));
+    os.tprefix = ar.get<uint64_t>(order_prev_buckets(n, j->k) + 1);
+    os.ttemp = ar.alloc(scan_temp_bytes(order_prev_buckets(n, j->k) + 1));
     os.tmp_keys = ar.alloc(n * ksz);
     os.tmp_vals = ar.get<uint32_t>(n);
     os.scan_temp = ar.alloc(order_scan_temp_bytes(nd + 1));
@@ -1299,14 +1298,14 @@ kmc_status kmc_shard_partition(kmc_job* j, const uint64_t* global_hist_w, const 
             int D = 1;
             while ((1 << D) < world) ++D;
             const uint64_t TI = rec_tile_items(j->k);
-            std::vector<RecTile2> tl;
-            for (uint64_t t = 0; t < c.tmp_n; t += TI)
-                tl.push_back(RecTile2{t, (uint32_t)std::min<uint64_t>(TI, c.tmp_n - t), 0});
-            RecTile2* d_tiles = ar.get<RecTile2>(tl.size());
-            CK(cudaMemcpyAsync(d_tiles, tl.data(), tl.size() * sizeof(RecTile2), cudaMemcpyHostToDevice, s));
-            CK(launch_rec_scatter(j->k, c.tmp_recs, c.tmp_sig, sig2owner, d_tiles, tl.size(), 0, D, cursor,
+            const uint64_t mt = c.tmp_n / TI + 1;
+            RecTile2* d_tiles = ar.get<RecTile2>(mt);
+            uint64_t* t_prefix = ar.get<uint64_t>(2);
+            void* t_temp = ar.alloc(scan_temp_bytes(2));
+            CK(launch_make_tiles(TileSrc{nullptr, 1, 0, 0, c.tmp_n}, 1, (uint32_t)TI, mt, t_prefix, t_temp, d_tiles, s));
+            CK(launch_rec_scatter(j->k, c.tmp_recs, c.tmp_sig, sig2owner, d_tiles, mt, t_prefix + 1, 0, D, cursor,
                                   send_records, send_sigs, s, 1));
-            j->launches += 4;
+            j->launches += 7;
             CK(cudaStreamSynchronize(s));
             ar.release(d_tiles);
             ar.release(d_owner);

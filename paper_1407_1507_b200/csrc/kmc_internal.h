@@ -68,11 +68,27 @@ struct RecTile2 {
     uint32_t bucket;  // bucket of the previous pass (cursor row)
 };
 size_t rec_tile_items(int k);
-// out_orig_ids: write the input ids (not the mapped ones) to out_ids.
+// Tiles of <= TI items over nb buckets, generated on the device (no host round trip):
+// bucket b holds items [start(b), start(b+1)), start(b) = base[b << sh] (uint64 or uint32
+// array of nbase entries; b << sh >= nbase: total; base == nullptr: one bucket [0, total)).
+// prefix (nb + 1 uint64) receives the exclusive scan of the tiles per bucket, so
+// prefix[nb] is the tile count; consumers launch an upper bound of CTAs and those at or
+// past prefix[nb] exit.  temp: scan_temp_bytes(nb + 1).
+struct TileSrc {
+    const void* base;
+    int is64;
+    uint64_t nbase;
+    int sh;
+    uint64_t total;
+};
+cudaError_t launch_make_tiles(const TileSrc& src, uint64_t nb, uint32_t TI, uint64_t max_tiles, uint64_t* prefix,
+                              void* temp, RecTile2* tiles, cudaStream_t s);
+// out_orig_ids: write the input ids (not the mapped ones) to out_ids.  n_tiles_dev: the
+// tile count in device memory (grid = max_tiles CTAs).
 cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* in_ids, const uint32_t* sig2bin,
-                               const RecTile2* tiles, uint64_t n_tiles, int shift, int D,
-                               unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids, cudaStream_t s,
-                               int out_orig_ids = 0);
+                               const RecTile2* tiles, uint64_t max_tiles, const uint64_t* n_tiles_dev, int shift,
+                               int D, unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids,
+                               cudaStream_t s, int out_orig_ids = 0);
 // sharded counting helpers
 cudaError_t launch_compose_map(const uint32_t* map_a, const uint32_t* map_b, uint64_t n, uint32_t* out,
                                cudaStream_t s);
@@ -234,8 +250,10 @@ struct OrderScratch {
     uint32_t* cursor;       // [2^order_digit_bits] scatter cursors
     Chunk* chunks;          // [2^order_digit_bits]
     Chunk* oversize;        // [2^order_digit_bits]
-    unsigned long long* counters;  // [2]
+    unsigned long long* counters;  // [8]
     OrdTile* tiles;         // [order_max_tiles(n, k)]
+    uint64_t* tprefix;      // [order_prev_buckets(n, k) + 1] tiles per bucket (device-built tiles)
+    void* ttemp;            // scan_temp_bytes(order_prev_buckets(n, k) + 1)
     void* tmp_keys;         // [n] K
     uint32_t* tmp_vals;     // [n]
     void* scan_temp;        // order_scan_temp_bytes(2^(D1+D2) + 1)
@@ -245,6 +263,7 @@ struct OrderSegment {
     uint64_t begin, n;  // items of an oversize bucket in (*seg_keys, *seg_vals) after launch_order
 };
 int order_digit_bits(uint64_t n, int k);  // bits of all MSD passes
+uint64_t order_prev_buckets(uint64_t n, int k);  // buckets before the last MSD pass
 uint64_t order_tile_items(int key_words);
 uint64_t order_max_tiles(uint64_t n, int k);
 size_t order_scan_temp_bytes(uint64_t n_digits);
