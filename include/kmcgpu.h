@@ -66,7 +66,8 @@ typedef enum {
     KMC_ERR_OUT_CAPACITY = 2,  /* out_capacity < n_out; stats->n_out holds the required count */
     KMC_ERR_ALLOC = 3,         /* scratch allocation failed */
     KMC_ERR_CUDA = 4,          /* a CUDA runtime call or kernel failed */
-    KMC_ERR_INTERNAL = 5       /* internal consistency check failed (a bug) */
+    KMC_ERR_INTERNAL = 5,      /* internal consistency check failed (a bug) */
+    KMC_ERR_IO = 6             /* an output file could not be written (kmc_write_db) */
 } kmc_status;
 
 /* Pipeline stages timed with CUDA events when kmc_options.profile != 0. */
@@ -216,6 +217,32 @@ kmc_status kmc_debug_signatures(const uint8_t* reads, const uint64_t* read_offse
 /* Signature-rule test hook: out[i] = 1 if the p-mer with value i (i < 4^p) is an allowed
  * signature -- evaluated by the same device function the kernels use. */
 kmc_status kmc_debug_allowed(int p, uint8_t* out_allowed, void* stream);
+
+/* KMC 2 database files: writes <path>.kmc_pre and <path>.kmc_suf in the
+ * layout of the paper's supplement, Sec. 4 "Database format":
+ *   .kmc_pre = "KMCP" | prefixes | map | header | header position | "KMCP"; all integers
+ *   little-endian; header = uint32 kmer_length, mode (0), counter_size,
+ *   lut_prefix_length, signature_length (p), min_count (cutoff_min), max_count (cutoff_max),
+ *   uint64 total_kmers (n), uint32 tmp[7] (0), uint32 KMC_VER (0x200), 68 bytes; header
+ *   position = 68 (the header's distance from that field); map = uint32
+ *   [4^p + 1], the prefixes-array id of every signature (4^p = "no allowed p-mer");
+ *   prefixes = per id, uint64[4^lut]: index of the first record with that id and that
+ *   lut-symbol prefix, then one guard = n.
+ *   .kmc_suf = "KMCS" | n records | "KMCS"; record = the k-mer without its lut-symbol prefix,
+ *   4 symbols per byte with the leftmost in the top bits, then
+ *   min(count, counter_max) on counter_size little-endian bytes.
+ * Records are ordered by (id, k-mer).  Readings (DESIGN.md R-DB): id = signature >> G,
+ * G = max(0, 2p - 14); lut = the largest of k mod 4, k mod 4 + 4, k mod 4 + 8 that is <= k
+ * and keeps ids * 4^lut <= 2^23; counter_size = the fewest bytes that hold counter_max
+ * (-cs).  The signature of a stored k-mer is the smallest allowed canonical p-mer
+ * over its k-p+1 p-mers, the same rule as kmc_count's binning.
+ * kmers: n canonical keys, strictly ascending, in kmc_count's output layout (k <= 32: one
+ * uint64 each; else [lo, hi] pairs); counts: n uint32; both device or host memory, read only.
+ * n < 2^32.  Errors: KMC_ERR_INVALID_ARG (NULL path, k outside [1, 64], p outside
+ * [1, min(k, 12)], counter_max = 0, NULL arrays with n > 0), KMC_ERR_IO (file not written),
+ * KMC_ERR_ALLOC / KMC_ERR_CUDA.  Synchronous on `stream`. */
+kmc_status kmc_write_db(const void* kmers, const uint32_t* counts, uint64_t n, int k, int p, uint32_t cutoff_min,
+                        uint32_t cutoff_max, uint32_t counter_max, const char* path, void* stream);
 
 const char* kmc_last_error(void);
 int kmc_version(void);

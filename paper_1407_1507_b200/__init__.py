@@ -102,6 +102,8 @@ def load():
         lib.kmc_shard_owners.argtypes = [P, U64, I, P]
         lib.kmc_shard_owners.restype = None
         lib.kmc_record_words.argtypes = [I]
+        lib.kmc_write_db.argtypes = [P, P, U64, I, I, U32, U32, U32, ctypes.c_char_p, P]
+        lib.kmc_write_db.restype = I
         lib.kmc_record_words.restype = I
         _lib = lib
         return lib
@@ -371,6 +373,26 @@ def debug_allowed(p: int) -> np.ndarray:
     import torch
     _check(lib.kmc_debug_allowed(p, out.ctypes.data, _stream_handle(torch.cuda.current_stream())))
     return out
+
+
+def write_db(path: str, kmers, counts, k: int, p: int, cutoff_min: int, cutoff_max: int,
+             counter_max: int = 255) -> None:
+    """KMC 2 database files <path>.kmc_pre / <path>.kmc_suf (kmc_write_db, include/kmcgpu.h;
+    Suppl. Sec. 4) from count()'s k-mers and counts (torch tensors on cuda or
+    cpu, or numpy arrays).  counter_max is KMC's -cs: stored counters saturate there."""
+    import torch
+    lib = load()
+    if isinstance(kmers, np.ndarray):
+        kmers = torch.from_numpy(np.ascontiguousarray(kmers))
+    if isinstance(counts, np.ndarray):
+        counts = torch.from_numpy(np.ascontiguousarray(counts))
+    kmers = kmers.contiguous()
+    counts = counts.contiguous()
+    n = int(counts.shape[0])
+    stream = torch.cuda.current_stream() if kmers.is_cuda else None
+    _check(lib.kmc_write_db(kmers.data_ptr() if n else None, counts.data_ptr() if n else None, n, k, p,
+                            max(0, int(cutoff_min)), int(cutoff_max), int(counter_max), path.encode(),
+                            _stream_handle(stream) if stream is not None else None))
 
 
 def version() -> int:

@@ -1461,4 +1461,118 @@ kmc_status kmc_debug_allowed(int p, uint8_t* out_allowed, void* stream) {
     return KMC_OK;
 }
 
+kmc_status kmc_write_db(const void* kmers, const uint32_t* counts, uint64_t n, int k, int p, uint32_t cutoff_min,
+                        uint32_t cutoff_max, uint32_t counter_max, const char* path, void* stream) {
+    if (!path || k < 1 || k > 64 || p < 1 || p > 12 || p > k || counter_max == 0 ||
+        (n > 0 && (!kmers || !counts)) || n >= (1ull << 32)) {
+        set_err("invalid kmc_write_db arguments (path=%p k=%d p=%d counter_max=%u n=%llu)", (const void*)path, k, p,
+                counter_max, (unsigned long long)n);
+        return KMC_ERR_INVALID_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena ar;
+    ar.bind(s);
+    try {
+        const int kw = k <= 32 ? 1 : 2;
+        const size_t ksz = 8 * (size_t)kw;
+        const int G = db_group_shift(p), lut = db_lut_length(k, p), cb = db_counter_bytes(counter_max);
+        const uint64_t na = db_n_arrays(p), entries = na << (2 * lut);
+        const int nb = (k - lut) / 4, rec = nb + cb;
+        std::vector<uint64_t> hpos(entries + 1, 0);
+        std::vector<uint8_t> hrec((size_t)n * rec);
+        if (n > 0) {
+            const void* dk = kmers;
+            const uint32_t* dc = counts;
+            if (!is_device_ptr(kmers)) {
+                void* t = ar.alloc(n * ksz);
+                CK(cudaMemcpyAsync(t, kmers, n * ksz, cudaMemcpyHostToDevice, s));
+                dk = t;
+            }
+            if (!is_device_ptr(counts)) {
+                uint32_t* t = ar.get<uint32_t>(n);
+                CK(cudaMemcpyAsync(t, counts, n * 4, cudaMemcpyHostToDevice, s));
+                dc = t;
+            }
+            // ids (signature >> G), then a stable sort by id: k-mers stay ascending per id
+            uint64_t* ids = ar.get<uint64_t>(n);
+            uint32_t* idx = ar.get<uint32_t>(n);
+            CK(launch_db_ids(kw, dk, n, k, p, ids, idx, s));
+            int nbits = 1;
+            while ((1ull << nbits) < na) ++nbits;
+            RadixScratch rs{};
+            rs.keys_alt = ar.alloc(n * 8);
+            rs.vals_alt = ar.get<uint32_t>(n);
+            const uint64_t nt = (n + radix_tile_items(1) - 1) / radix_tile_items(1);
+            rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
+            rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+            rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n, 1));
+            rs.red = ar.get<unsigned long long>(4);
+            unsigned long long* red_host = nullptr;
+            CK(cudaMallocHost(&red_host, 4 * sizeof(unsigned long long)));
+            rs.red_host = red_host;
+            void* sk = nullptr;
+            uint32_t* perm = nullptr;
+            int sl = 0;
+            const cudaError_t se = device_radix_sort(1, ids, idx, n, nbits, rs, s, &sk, &perm, &sl);
+            cudaFreeHost(red_host);
+            CK(se);
+            // prefixes region: exclusive scan of the records per (id, prefix), + guard
+            unsigned long long* cnt = ar.get<unsigned long long>(entries + 1);
+            CK(cudaMemsetAsync(cnt, 0, (entries + 1) * 8, s));
+            CK(launch_db_hist(kw, dk, (const uint64_t*)sk, perm, n, k, lut, cnt, s));
+            uint64_t* pos = ar.get<uint64_t>(entries + 1);
+            void* temp = ar.alloc(scan_temp_bytes(entries + 1));
+            CK(scan_u64((const uint64_t*)cnt, pos, entries, temp, s));
+            uint8_t* recs = ar.get<uint8_t>((size_t)n * rec);
+            CK(launch_db_records(kw, dk, dc, perm, n, k, lut, cb, counter_max, recs, s));
+            CK(cudaMemcpyAsync(hpos.data(), pos, (entries + 1) * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(hrec.data(), recs, (size_t)n * rec, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        // .kmc_pre
+        std::vector<uint32_t> amap((1ull << (2 * p)) + 1);
+        for (uint64_t sg = 0; sg < amap.size(); ++sg) amap[sg] = (uint32_t)(sg >> G);
+        uint8_t hdr[68];
+        auto put32 = [&](int o, uint32_t v) { memcpy(hdr + o, &v, 4); };
+        memset(hdr, 0, sizeof(hdr));
+        put32(0, (uint32_t)k);
+        put32(4, 0u);  // mode: occurrence counters
+        put32(8, (uint32_t)cb);
+        put32(12, (uint32_t)lut);
+        put32(16, (uint32_t)p);
+        put32(20, cutoff_min);
+        put32(24, cutoff_max);
+        memcpy(hdr + 28, &n, 8);
+        put32(64, 0x200u);  // KMC_VER (tmp[7] at 36..63 stays 0)
+        const uint32_t hpos_field = sizeof(hdr);
+        const std::string pre_path = std::string(path) + ".kmc_pre", suf_path = std::string(path) + ".kmc_suf";
+        FILE* f = fopen(pre_path.c_str(), "wb");
+        bool ok = f != nullptr;
+        if (ok) {
+            ok = fwrite("KMCP", 1, 4, f) == 4 && fwrite(hpos.data(), 8, hpos.size(), f) == hpos.size() &&
+                 fwrite(amap.data(), 4, amap.size(), f) == amap.size() && fwrite(hdr, 1, sizeof(hdr), f) == sizeof(hdr) &&
+                 fwrite(&hpos_field, 4, 1, f) == 1 && fwrite("KMCP", 1, 4, f) == 4;
+            ok = (fclose(f) == 0) && ok;
+        }
+        if (ok) {
+            f = fopen(suf_path.c_str(), "wb");
+            ok = f != nullptr;
+            if (ok) {
+                ok = fwrite("KMCS", 1, 4, f) == 4 && fwrite(hrec.data(), 1, hrec.size(), f) == hrec.size() &&
+                     fwrite("KMCS", 1, 4, f) == 4;
+                ok = (fclose(f) == 0) && ok;
+            }
+        }
+        if (!ok) {
+            set_err("cannot write %s / %s", pre_path.c_str(), suf_path.c_str());
+            throw Fail{KMC_ERR_IO};
+        }
+    } catch (const Fail& e) {
+        ar.release_all();
+        return e.st;
+    }
+    ar.release_all();
+    return KMC_OK;
+}
+
 }  // extern "C"

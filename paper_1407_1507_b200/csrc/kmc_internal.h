@@ -228,6 +228,17 @@ struct RadixScratch {
 };
 uint64_t radix_tile_items(int key_words);
 size_t radix_scan_temp_bytes(uint64_t n, int key_words);
+// KMC 2 database writer (k_db.cu; Suppl. Sec. 4; reading R-DB)
+int db_group_shift(int p);
+uint64_t db_n_arrays(int p);
+int db_lut_length(int k, int p);
+int db_counter_bytes(uint32_t cs);
+cudaError_t launch_db_ids(int key_words, const void* keys, uint64_t n, int k, int p, uint64_t* ids, uint32_t* idx,
+                          cudaStream_t s);
+cudaError_t launch_db_hist(int key_words, const void* keys, const uint64_t* sids, const uint32_t* perm, uint64_t n,
+                           int k, int lut, unsigned long long* cnt, cudaStream_t s);
+cudaError_t launch_db_records(int key_words, const void* keys, const uint32_t* counts, const uint32_t* perm,
+                              uint64_t n, int k, int lut, int cb, uint32_t cs, uint8_t* out, cudaStream_t s);
 cudaError_t device_radix_sort(int key_words, void* keys, uint32_t* vals, uint64_t n, int nbits,
                               const RadixScratch& rs, cudaStream_t s, void** res_keys, uint32_t** res_vals,
                               int* n_launches);
