@@ -57,6 +57,9 @@ def _load():
             lib = ctypes.CDLL(build())
             lib.oracle_count.argtypes = [_P, _P, _U64, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, _P, _P, _U64, _P]
             lib.oracle_count.restype = ctypes.c_int64
+            lib.oracle_count_ex.argtypes = [_P, _P, _U64, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, _P, _P, _U64,
+                                            _P, ctypes.c_int]
+            lib.oracle_count_ex.restype = ctypes.c_int64
             lib.oracle_n_windows.argtypes = [_P, _P, _U64, ctypes.c_int]
             lib.oracle_n_windows.restype = _U64
             lib.oracle_n_windows_par.argtypes = [_P, _P, _U64, ctypes.c_int]
@@ -90,8 +93,9 @@ class Result:
         self.n_windows, self.n_unique, self.n_below_min, self.n_above_max, self.n_out = (int(x) for x in stats)
 
 
-def count(reads, offsets, k: int, cutoff_min: int = 1, cutoff_max: int = 10**9) -> Result:
-    """Exact canonical k-mer counts with cutoffs (C++ oracle)."""
+def count(reads, offsets, k: int, cutoff_min: int = 1, cutoff_max: int = 10**9, canonical: bool = True) -> Result:
+    """Exact canonical k-mer counts with cutoffs (C++ oracle); canonical=False counts the
+    k-mers as they occur in the reads (KMC's -b)."""
     lib = _load()
     reads, offsets = _arrays(reads, offsets)
     n_reads = offsets.shape[0] - 1
@@ -100,8 +104,8 @@ def count(reads, offsets, k: int, cutoff_min: int = 1, cutoff_max: int = 10**9) 
     keys = np.zeros((max(cap, 1), w), dtype=np.uint64)
     counts = np.zeros(max(cap, 1), dtype=np.uint32)
     stats = np.zeros(5, dtype=np.uint64)
-    n = lib.oracle_count(reads.ctypes.data, offsets.ctypes.data, n_reads, k, cutoff_min, cutoff_max,
-                         keys.ctypes.data, counts.ctypes.data, cap, stats.ctypes.data)
+    n = lib.oracle_count_ex(reads.ctypes.data, offsets.ctypes.data, n_reads, k, cutoff_min, cutoff_max,
+                            keys.ctypes.data, counts.ctypes.data, cap, stats.ctypes.data, int(canonical))
     if n < 0:
         raise ValueError("bad k")
     keys = keys[:n, 0].copy() if w == 1 else keys[:n].copy()
@@ -207,14 +211,15 @@ def segments(read: str):
         yield "".join(cur)
 
 
-def count_strings(reads, k: int, cutoff_min: int = 1, cutoff_max: int = 10**9) -> dict:
-    """{canonical k-mer string: count} for ci <= count <= cx (string operations only)."""
+def count_strings(reads, k: int, cutoff_min: int = 1, cutoff_max: int = 10**9, canonical: bool = True) -> dict:
+    """{canonical k-mer string: count} for ci <= count <= cx (string operations only);
+    canonical=False keys the k-mers as they occur (-b)."""
     c = collections.Counter()
     for r in reads:
         r = r.decode() if isinstance(r, (bytes, bytearray)) else r
         for seg in segments(r):
             for i in range(len(seg) - k + 1):
-                c[canonical_str(seg[i:i + k])] += 1
+                c[canonical_str(seg[i:i + k]) if canonical else seg[i:i + k]] += 1
     ci = max(1, cutoff_min)
     return {kmer: n for kmer, n in c.items() if ci <= n <= cutoff_max}
 

@@ -76,7 +76,7 @@ static u128 canonical_value(const uint8_t* w, int k) {
 template <typename K>
 static int64_t count_impl(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k,
                           uint32_t ci, uint32_t cx, uint64_t* out_keys, uint32_t* out_counts,
-                          uint64_t cap, uint64_t* stats) {
+                          uint64_t cap, uint64_t* stats, int canonical) {
     std::vector<K> keys;
     uint64_t n_windows = 0;
     for (uint64_t i = 0; i < n_reads; ++i) {
@@ -85,7 +85,8 @@ static int64_t count_impl(const uint8_t* reads, const uint64_t* offsets, uint64_
         for (uint64_t s = b; s + k <= e; ++s) {
             const uint8_t* w = reads + (s - offsets[0]);
             if (!window_valid(w, k)) continue;
-            keys.push_back((K)canonical_value(w, k));
+            /* -b: "turn off transformation of k-mers into canonical form" */
+            keys.push_back((K)(canonical ? canonical_value(w, k) : forward_value(w, k)));
             ++n_windows;
         }
     }
@@ -131,8 +132,18 @@ int64_t oracle_count(const uint8_t* reads, const uint64_t* offsets, uint64_t n_r
                      uint32_t ci, uint32_t cx, uint64_t* out_keys, uint32_t* out_counts,
                      uint64_t cap, uint64_t* stats) {
     if (k < 1 || k > 64) return -1;
-    if (k <= 32) return count_impl<uint64_t>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, cap, stats);
-    return count_impl<u128>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, cap, stats);
+    if (k <= 32) return count_impl<uint64_t>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, cap, stats, 1);
+    return count_impl<u128>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, cap, stats, 1);
+}
+
+/* Same with canonical = 0: forward k-mers as they occur in the reads (-b). */
+int64_t oracle_count_ex(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k,
+                        uint32_t ci, uint32_t cx, uint64_t* out_keys, uint32_t* out_counts,
+                        uint64_t cap, uint64_t* stats, int canonical) {
+    if (k < 1 || k > 64) return -1;
+    if (k <= 32)
+        return count_impl<uint64_t>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, cap, stats, canonical);
+    return count_impl<u128>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, cap, stats, canonical);
 }
 
 /* Number of valid k-windows (upper bound for the survivor list). */

@@ -316,3 +316,42 @@ def test_synth_deterministic_and_shaped():
     c1 = synth.make("C1", scale=0.1)
     assert c1.n_reads == 10_000 and c1.n_bases == 1_000_000
     assert set(np.unique(c1.reads).tolist()) <= set(b"ACGT")
+
+
+# --- -b: non-canonical counting ----------------------------------------------
+
+def _oracle_dict(res, k):
+    out = {}
+    for i in range(len(res.counts)):
+        key = int(res.keys[i]) if k <= 32 else (int(res.keys[i, 1]) << 64) | int(res.keys[i, 0])
+        out[oracle.value_str(key, k)] = int(res.counts[i])
+    return out
+
+
+@pytest.mark.parametrize("k", [1, 5, 12, 31, 40])
+def test_noncanonical_homopolymer_closed_form(k):
+    # T^L: every window is T^k read forward; its canonical form is A^k
+    L = 90
+    w = synth.from_strings(["T" * L], k)
+    nc = _oracle_dict(oracle.count(w.reads, w.offsets, k, canonical=False), k)
+    cc = _oracle_dict(oracle.count(w.reads, w.offsets, k, canonical=True), k)
+    assert nc == {"T" * k: L - k + 1}
+    assert cc == {"A" * k: L - k + 1}
+
+
+@pytest.mark.parametrize("k", [3, 8, 21, 33])
+def test_noncanonical_folds_to_canonical(k):
+    # canonical count of x = forward count of x + forward count of rc(x) (x != rc(x)),
+    # the forward count for palindromes (P:L143-145 applied to each window)
+    seqs = synth.random_reads(700 + k, 120, 0, 200, n_frac=0.02, lower_frac=0.05)
+    seqs += [b"ACGT" * 30, b"AATT" * 20, b"GATC" * 15]
+    w = synth.from_strings(seqs, k)
+    nc = _oracle_dict(oracle.count(w.reads, w.offsets, k, canonical=False), k)
+    cc = _oracle_dict(oracle.count(w.reads, w.offsets, k, canonical=True), k)
+    fold = {}
+    for x, c in nc.items():
+        y = oracle.canonical_str(x)
+        fold[y] = fold.get(y, 0) + c
+    assert fold == cc
+    # and the string implementation agrees on the forward counts
+    assert oracle.count_strings(seqs, k, canonical=False) == nc
