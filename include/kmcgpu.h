@@ -139,6 +139,11 @@ typedef struct {
                                   every chunk in shared memory.  Same output. */
     uint32_t chunk_capacity;   /* 0 = auto; else max keys per large-bin chunk (testing: large
                                   values force hash-table overflows onto the fallback) */
+    uint32_t non_canonical;    /* 1: count k-mers as they occur in the reads, not their canonical
+                                  form (KMC's -b).  Signatures and binning stay canonical
+                                  (a k-mer and its reverse complement share a bin either way).
+                                  k = 32 and k = 64 are rejected (KMC_ERR_INVALID_ARG): the
+                                  all-T k-mer is the all-ones key, the kernels' empty marker. */
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).

@@ -50,7 +50,7 @@ class _Options(ctypes.Structure):
                 ("force_large", ctypes.c_uint32), ("large_path", ctypes.c_uint32),
                 ("distribute_path", ctypes.c_uint32), ("input_batch_mb", ctypes.c_uint32),
                 ("large_group_mkeys", ctypes.c_uint32), ("count_path", ctypes.c_uint32),
-                ("chunk_capacity", ctypes.c_uint32)]
+                ("chunk_capacity", ctypes.c_uint32), ("non_canonical", ctypes.c_uint32)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
@@ -159,8 +159,9 @@ class Result:
 
 
 def _options(profile, small_bin_capacity, force_large, large_path=0, distribute_path=0, input_batch_mb=0,
-             large_group_mkeys=0, count_path=0, chunk_capacity=0):
+             large_group_mkeys=0, count_path=0, chunk_capacity=0, canonical=True):
     o = _Options()
+    o.non_canonical = 0 if canonical else 1
     o.count_path = int(count_path)
     o.chunk_capacity = int(chunk_capacity)
     o.distribute_path = int(distribute_path)
@@ -176,8 +177,10 @@ def _options(profile, small_bin_capacity, force_large, large_path=0, distribute_
 def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *, stream=None,
           profile: bool = False, small_bin_capacity: int = 0, force_large: bool = False,
           large_path: int = 0, distribute_path: int = 0, input_batch_mb: int = 0, large_group_mkeys: int = 0,
-          count_path: int = 0, chunk_capacity: int = 0, out_device: str | None = None) -> Result:
-    """Count canonical k-mers (KMC 2 hot path on the GPU).
+          count_path: int = 0, chunk_capacity: int = 0, out_device: str | None = None,
+          canonical: bool = True) -> Result:
+    """Count canonical k-mers (KMC 2 hot path on the GPU); canonical=False counts them as
+    they occur in the reads (KMC's -b).
 
     reads: uint8 tensor (cuda, or pinned/pageable cpu -- copied inside the call), n_bases bytes.
     offsets: uint64/int64 tensor, n_reads+1 read boundaries (same device rules).
@@ -191,7 +194,7 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
     if n_reads < 0:
         raise ValueError("offsets must have n_reads + 1 entries")
     opt = _options(profile, small_bin_capacity, force_large, large_path, distribute_path, input_batch_mb,
-                   large_group_mkeys, count_path, chunk_capacity)
+                   large_group_mkeys, count_path, chunk_capacity, canonical)
     job = ctypes.c_void_p()
     n_out = ctypes.c_uint64()
     sh = _stream_handle(stream)

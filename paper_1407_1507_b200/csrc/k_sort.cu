@@ -34,11 +34,11 @@ template <class K> __host__ __device__ constexpr size_t small_smem_bytes() {
 
 // Expand one record into n canonical keys at dst[0..n) (min(fwd, rc)).
 template <class K>
-__device__ __forceinline__ void expand_record(const uint32_t* rec, int k, K* dst) {
+__device__ __forceinline__ void expand_record(const uint32_t* rec, int k, bool canonical, K* dst) {
     constexpr int RW = RecWords<K>::v;
     uint32_t wd[RW];
     load_record<RW>(rec, wd);
-    for_each_window<K, RW>(wd, k, [&](int w, const K& key) { dst[w] = key; });
+    for_each_window<K, RW>(wd, k, canonical, [&](int w, const K& key) { dst[w] = key; });
 }
 
 // Run-length compaction of the sorted keys S[0..n) with the cutoffs (S8); cnt is a free
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(SB_NT, 2) k_small_bins(SmallArgs a) {
         uint32_t pos = block_excl_sum<SB_NT, uint32_t>(s, wsum, nullptr);
         for (int r = r0; r < r1; ++r) {
             const uint32_t* rec = R + r * RW;
-            expand_record<K>(rec, k, A + pos);
+            expand_record<K>(rec, k, a.canonical, A + pos);
             pos += rec_nwin(rec);
         }
     }
@@ -144,8 +144,8 @@ constexpr int LE_NT = 256;
 
 template <class K>
 __global__ void __launch_bounds__(LE_NT) k_large_expand(const uint32_t* __restrict__ bins,
-                                                        const Piece* __restrict__ pieces, int k, K* keys,
-                                                        unsigned long long* gstats) {
+                                                        const Piece* __restrict__ pieces, int k, int canonical,
+                                                        K* keys, unsigned long long* gstats) {
     __shared__ __align__(16) uint32_t R[PIECE_RECORDS * 8];
     __shared__ uint32_t wsum[LE_NT / 32 + 1];
     __shared__ unsigned long long bcast;
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(LE_NT) k_large_expand(const uint32_t* __restri
     K* out = keys + bcast;
     for (int r = r0; r < r1; ++r) {
         const uint32_t* rec = R + r * RW;
-        expand_record<K>(rec, k, out + pos);
+        expand_record<K>(rec, k, canonical != 0, out + pos);
         pos += rec_nwin(rec);
     }
 }
@@ -538,7 +538,7 @@ template <class K, bool SC> size_t split_smem(int k, int dmax) {
            (size_t)(SP_NT / 32) * split_own_bytes<K>(k) + 16;
 }
 
-template <class K, bool SCATTER>
+template <class K, bool SCATTER, bool CANON>
 __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bins, const Piece* __restrict__ pieces,
                                                  uint64_t n_pieces, const LargeBin* __restrict__ lbins, int k,
                                                  int dmax, uint32_t* __restrict__ table, K* __restrict__ out) {
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                         if (t < cnt) {
                             const uint64_t f = (g << (2 * t)) >> (64 - 2 * k);
                             const uint64_t rc = (rg << (64 - 2 * t - 2 * k)) >> (64 - 2 * k);
-                            const uint64_t key = f < rc ? f : rc;
+                            const uint64_t key = (f < rc || !CANON) ? f : rc;
                             const uint32_t dg = part_digit(key, D);
                             if (!pm) {
                                 const uint32_t slot = atomicAdd(&h[dg], 1u);
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                 const int l = w < tot ? own[w] : 0;
                 const uint32_t pl = __shfl_sync(0xffffffffu, pre, l);
                 if (w < tot) {
-                    const K key = window_key<K>(Rp + (warp * 32 + l) * RW, (int)(w - pl), k);
+                    const K key = window_key<K>(Rp + (warp * 32 + l) * RW, (int)(w - pl), k, CANON);
                     const uint32_t slot = atomicAdd(&h[part_digit(key, D)], 1u);
                     if (SCATTER) out[slot] = key;
                 }
@@ -985,13 +985,14 @@ cudaError_t launch_small_bins(const SmallArgs& a, uint64_t n_small, cudaStream_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, void* keys,
+cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, int canonical,
+                                void* keys,
                                 unsigned long long* gstats, cudaStream_t s) {
     if (n_pieces == 0) return cudaSuccess;
     if (k <= 32)
-        k_large_expand<uint64_t><<<(unsigned)n_pieces, LE_NT, 0, s>>>(bins, pieces, k, (uint64_t*)keys, gstats);
+        k_large_expand<uint64_t><<<(unsigned)n_pieces, LE_NT, 0, s>>>(bins, pieces, k, canonical, (uint64_t*)keys, gstats);
     else
-        k_large_expand<K128><<<(unsigned)n_pieces, LE_NT, 0, s>>>(bins, pieces, k, (K128*)keys, gstats);
+        k_large_expand<K128><<<(unsigned)n_pieces, LE_NT, 0, s>>>(bins, pieces, k, canonical, (K128*)keys, gstats);
     return cudaGetLastError();
 }
 
@@ -1033,23 +1034,30 @@ cudaError_t launch_greedy_chunks(GreedyArgs g, uint64_t n_keys, cudaStream_t s) 
 
 template <class K, bool SC>
 cudaError_t split_t(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const LargeBin* lbins, int k,
-                    int dmax, uint32_t n_ranges, uint32_t* table, void* keys, cudaStream_t s) {
+                    int canonical, int dmax, uint32_t n_ranges, uint32_t* table, void* keys, cudaStream_t s) {
     const int sm = (int)split_smem<K, SC>(k, dmax);
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_split<K, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-    k_split<K, SC><<<n_ranges, SP_NT, sm, s>>>(bins, pieces, n_pieces, lbins, k, dmax, table, (K*)keys);
+    if (canonical) {
+        if ((e = cudaFuncSetAttribute(k_split<K, SC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+        k_split<K, SC, true><<<n_ranges, SP_NT, sm, s>>>(bins, pieces, n_pieces, lbins, k, dmax, table, (K*)keys);
+    } else {
+        if ((e = cudaFuncSetAttribute(k_split<K, SC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+        k_split<K, SC, false><<<n_ranges, SP_NT, sm, s>>>(bins, pieces, n_pieces, lbins, k, dmax, table, (K*)keys);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_split(bool scatter, const uint32_t* bins, const Piece* pieces, uint64_t n_pieces,
-                         const LargeBin* lbins, int k, int dmax, uint32_t n_ranges, uint32_t* table, void* keys,
-                         cudaStream_t s) {
+                         const LargeBin* lbins, int k, int canonical, int dmax, uint32_t n_ranges, uint32_t* table,
+                         void* keys, cudaStream_t s) {
     if (n_pieces == 0) return cudaSuccess;
     if (k <= 32)
-        return scatter ? split_t<uint64_t, true>(bins, pieces, n_pieces, lbins, k, dmax, n_ranges, table, keys, s)
-                       : split_t<uint64_t, false>(bins, pieces, n_pieces, lbins, k, dmax, n_ranges, table, keys, s);
-    return scatter ? split_t<K128, true>(bins, pieces, n_pieces, lbins, k, dmax, n_ranges, table, keys, s)
-                   : split_t<K128, false>(bins, pieces, n_pieces, lbins, k, dmax, n_ranges, table, keys, s);
+        return scatter ? split_t<uint64_t, true>(bins, pieces, n_pieces, lbins, k, canonical, dmax, n_ranges, table,
+                                                 keys, s)
+                       : split_t<uint64_t, false>(bins, pieces, n_pieces, lbins, k, canonical, dmax, n_ranges, table,
+                                                  keys, s);
+    return scatter ? split_t<K128, true>(bins, pieces, n_pieces, lbins, k, canonical, dmax, n_ranges, table, keys, s)
+                   : split_t<K128, false>(bins, pieces, n_pieces, lbins, k, canonical, dmax, n_ranges, table, keys, s);
 }
 
 cudaError_t launch_digit_totals(const LargeBin* lbins, uint64_t n_lbins, const uint32_t* pos, uint32_t* cnt,

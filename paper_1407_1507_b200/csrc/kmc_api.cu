@@ -695,6 +695,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         sa.bin_nrec = pa.bin_nrec;
         sa.bin_w = pa.bin_w;
         sa.k = k;
+        sa.canonical = !j->opt.non_canonical;
         sa.ci = j->ci;
         sa.cx = j->cx;
         sa.surv_keys = j->surv_keys;
@@ -725,7 +726,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         void* lkeys = ar.alloc(large_windows * ksz);
         j->stage_begin(KMC_STAGE_LARGE_SPLIT);
         CK(launch_make_pieces(d_lbins, d_pp, lbins.size(), PIECE_RECORDS, d_pieces, s));
-        CK(launch_large_expand(bins, d_pieces, n_pieces, k, lkeys, gstats, s));
+        CK(launch_large_expand(bins, d_pieces, n_pieces, k, !j->opt.non_canonical, lkeys, gstats, s));
         j->launches += 2;
         j->stage_end(2);
         RadixScratch rs{};
@@ -881,7 +882,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
             j->stage_begin(KMC_STAGE_LARGE_SPLIT);
             CK(cudaMemsetAsync(counters, 0, 24, s));
             CK(launch_make_pieces(d_lbins, d_pp, gn, (uint32_t)prec, d_pieces, s));
-            CK(launch_split(false, bins, d_pieces, n_pieces, d_lbins, k, dmax, R, table, nullptr, s));
+            CK(launch_split(false, bins, d_pieces, n_pieces, d_lbins, k, !j->opt.non_canonical, dmax, R, table, nullptr, s));
             CK(scan_u32_to_u32(table, tpos, tb, ttemp, s));
             CK(launch_digit_totals(d_lbins, gn, tpos, digit_cnt, digit_start, s));
             GreedyArgs ga{};
@@ -896,7 +897,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
             j->launches += 6;
             j->stage_end(6);
             j->stage_begin(KMC_STAGE_LARGE_SCATTER);
-            CK(launch_split(true, bins, d_pieces, n_pieces, d_lbins, k, dmax, R, tpos, lkeys, s));
+            CK(launch_split(true, bins, d_pieces, n_pieces, d_lbins, k, !j->opt.non_canonical, dmax, R, tpos, lkeys, s));
             j->launches += 1;
             j->stage_end(1);
             CK(cudaMemcpyAsync(&hs[48], counters, 16, cudaMemcpyDeviceToHost, s));
@@ -1098,6 +1099,13 @@ kmc_status kmc_count_begin(const uint8_t* reads, const uint64_t* read_offsets, u
     j->ci = cutoff_min ? cutoff_min : 1;
     j->cx = cutoff_max;
     if (opt) j->opt = *opt;
+    if (j->opt.non_canonical && (k == 32 || k == 64)) {
+        // the all-T k-mer is the all-ones key, the empty-slot / padding marker (never a
+        // canonical key, but a forward one)
+        set_err("non_canonical needs k != 32 and k != 64 (k=%d)", k);
+        delete j;
+        return KMC_ERR_INVALID_ARG;
+    }
     j->arena.bind(j->s);
     try {
         run_begin(j, reads, read_offsets, n_reads);
@@ -1201,6 +1209,11 @@ kmc_status kmc_shard_pass1(const uint8_t* reads, const uint64_t* read_offsets, u
     j->ci = cutoff_min ? cutoff_min : 1;
     j->cx = cutoff_max;
     if (opt) j->opt = *opt;
+    if (j->opt.non_canonical && (k == 32 || k == 64)) {
+        set_err("non_canonical needs k != 32 and k != 64 (k=%d)", k);
+        delete j;
+        return KMC_ERR_INVALID_ARG;
+    }
     j->shard = true;
     j->arena.bind(j->s);
     try {

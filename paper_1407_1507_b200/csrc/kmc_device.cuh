@@ -50,6 +50,7 @@ struct Roll64 {
         rc = (rc >> 2) | ((uint64_t)(3u - c) << top);
     }
     __device__ __forceinline__ uint64_t canon() const { return fwd < rc ? fwd : rc; }
+    __device__ __forceinline__ uint64_t key(bool canonical) const { return canonical ? canon() : fwd; }
 };
 
 struct Roll128 {  // 33 <= k <= 64
@@ -70,6 +71,7 @@ struct Roll128 {  // 33 <= k <= 64
         K128 f{flo, fhi}, r{rlo, rhi};
         return key_lt(r, f) ? r : f;
     }
+    __device__ __forceinline__ K128 key(bool canonical) const { return canonical ? canon() : K128{flo, fhi}; }
 };
 
 template <class K> struct RollFor;
@@ -108,7 +110,7 @@ template <> struct RecWords<K128> { static constexpr int v = 8; };
 // canonical key min(fwd, rc) of every window.  The symbol loop is fully
 // unrolled so every symbol's word and shift are compile-time constants.
 template <class K, int RW, class F>
-__device__ __forceinline__ void for_each_window(const uint32_t (&wd)[RW], int k, F&& emit) {
+__device__ __forceinline__ void for_each_window(const uint32_t (&wd)[RW], int k, bool canonical, F&& emit) {
     typename RollFor<K>::T roll(k);
     const int nb = (int)(wd[0] >> 24) + k - 1;
 #pragma unroll
@@ -116,7 +118,7 @@ __device__ __forceinline__ void for_each_window(const uint32_t (&wd)[RW], int k,
         if (j >= nb) break;
         const int g = 8 + 2 * j;
         roll.push((wd[g >> 5] >> (30 - (g & 31))) & 3u);
-        if (j >= k - 1) emit(j - (k - 1), roll.canon());
+        if (j >= k - 1) emit(j - (k - 1), roll.key(canonical));
     }
 }
 
@@ -136,14 +138,15 @@ __device__ __forceinline__ uint64_t bits64_be(const uint32_t* w, int b) {
     const uint32_t hi = __funnelshift_l(w1, w0, r), lo = __funnelshift_l(w2, w1, r);
     return ((uint64_t)hi << 32) | lo;
 }
-template <class K> __device__ __forceinline__ K window_key(const uint32_t* rec, int j, int k);
-template <> __device__ __forceinline__ uint64_t window_key<uint64_t>(const uint32_t* rec, int j, int k) {
+template <class K> __device__ __forceinline__ K window_key(const uint32_t* rec, int j, int k, bool canonical);
+template <>
+__device__ __forceinline__ uint64_t window_key<uint64_t>(const uint32_t* rec, int j, int k, bool canonical) {
     // field of 2k <= 64 bits starting at bit 8+2j; the record has 4 words (+1 readable pad)
     const uint64_t f = bits64_be(rec, 8 + 2 * j) >> (64 - 2 * k);
     const uint64_t r = rev2_64(~f) >> (64 - 2 * k);
-    return f < r ? f : r;
+    return (f < r || !canonical) ? f : r;
 }
-template <> __device__ __forceinline__ K128 window_key<K128>(const uint32_t* rec, int j, int k) {
+template <> __device__ __forceinline__ K128 window_key<K128>(const uint32_t* rec, int j, int k, bool canonical) {
     // 2k in (64, 128] bits at bit b = 8+2j: hi part = first 2k-64 bits, lo part = next 64
     const int b = 8 + 2 * j, hb = 2 * k - 64;
     K128 f;
@@ -158,7 +161,7 @@ template <> __device__ __forceinline__ K128 window_key<K128>(const uint32_t* rec
     K128 r;
     r.lo = sh ? ((c >> sh) | (a << (64 - sh))) : c;
     r.hi = sh ? (a >> sh) : a;
-    return key_lt(r, f) ? r : f;
+    return (key_lt(r, f) && canonical) ? r : f;
 }
 
 // Digit of the large-bin split: a multiplicative hash of the whole key (equal keys share

@@ -135,6 +135,7 @@ struct SmallArgs {
     const uint64_t* bin_nrec;
     const uint64_t* bin_w;
     int k;
+    int canonical;                // 0: forward k-mers (-b)
     uint32_t ci, cx;
     void* surv_keys;              // K*
     uint32_t* surv_counts;
@@ -194,8 +195,8 @@ cudaError_t launch_greedy_chunks(GreedyArgs g, uint64_t n_keys, cudaStream_t s);
 // Split of the large bins into digit-contiguous key ranges (k_split): count pass (table of
 // per-(bin, digit, segment) counts), then, after an exclusive scan of the table, the scatter.
 cudaError_t launch_split(bool scatter, const uint32_t* bins, const Piece* pieces, uint64_t n_pieces,
-                         const LargeBin* lbins, int k, int dmax, uint32_t n_ranges, uint32_t* table, void* keys,
-                         cudaStream_t s);
+                         const LargeBin* lbins, int k, int canonical, int dmax, uint32_t n_ranges, uint32_t* table,
+                         void* keys, cudaStream_t s);
 cudaError_t launch_digit_totals(const LargeBin* lbins, uint64_t n_lbins, const uint32_t* pos, uint32_t* cnt,
                                 uint32_t* start,
                                 cudaStream_t s);
@@ -212,8 +213,8 @@ int chunk_hash_cap(int k);
 cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_chunks, int k, uint32_t ci,
                               uint32_t cx, void* surv_keys, uint32_t* surv_counts, unsigned long long* gstats,
                               Chunk* overflow, unsigned long long* n_overflow, int n_sms, cudaStream_t s);
-cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, void* keys,
-                                unsigned long long* gstats, cudaStream_t s);
+cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, int canonical,
+                                void* keys, unsigned long long* gstats, cudaStream_t s);
 
 // Device-wide LSD radix sort of n keys (+ optional uint32 values).  Result lands in
 // (*res_keys, *res_vals) which is either the input or the alternate buffers.

@@ -310,3 +310,35 @@ def test_streamed_equals_resident(gpu):
     b = gpu.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", input_batch_mb=1,
                   large_group_mkeys=1)
     assert np.array_equal(a[0], b.kmers.numpy()) and np.array_equal(a[1], b.counts.numpy())
+
+
+# --- -b: non-canonical counting -----------------------------------------------
+
+@pytest.mark.parametrize("name,scale,k,opts", [
+    ("C1", 0.02, None, {}), ("C5", 0.002, None, {}), ("C3", 0.002, None, {}), ("C4", 0.0005, None, {}),
+    ("C2", 0.005, None, dict(force_large=True)), ("C2", 0.005, None, dict(force_large=True, count_path=1)),
+    ("C1", 0.02, None, dict(large_path=1, force_large=True)), ("C1", 0.01, 31, dict(force_large=True)),
+    ("C1", 0.01, 33, {}), ("C1", 0.01, 47, dict(force_large=True)), ("C1", 0.01, 12, dict(small_bin_capacity=64))])
+def test_noncanonical_parity(gpu, name, scale, k, opts):
+    w = synth.make(name, scale=scale) if k is None else synth.make(name, scale=scale, k=k)
+    keys, counts, st = gpu_count(gpu, w, canonical=False, **opts)
+    ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max, canonical=False)
+    assert keys.shape[0] == ref.keys.shape[0]
+    assert np.array_equal(keys, ref.keys) and np.array_equal(counts, ref.counts)
+    assert st["n_windows"] == ref.n_windows and st["n_unique"] == ref.n_unique
+
+
+def test_noncanonical_low_complexity(gpu):
+    seqs = ["T" * 300, "A" * 250, "AT" * 120, "ACGT" * 60, "CA" * 100, "N" * 40, ""] * 30
+    for k, p in ((28, 9), (21, 5), (45, 11)):
+        w = synth.from_strings(seqs, k, p, 1)
+        keys, counts, _ = gpu_count(gpu, w, canonical=False)
+        ref = oracle.count(w.reads, w.offsets, k, 1, 10**9, canonical=False)
+        assert np.array_equal(keys, ref.keys) and np.array_equal(counts, ref.counts)
+
+
+def test_noncanonical_rejects_k32(gpu):
+    w = synth.from_strings(["ACGT" * 20], 32, 9, 1)
+    r, o = to_dev(w)
+    with pytest.raises(Exception):
+        gpu.count(r, o, 32, 9, 1, 10**9, canonical=False)
