@@ -114,6 +114,7 @@ typedef struct {
     uint64_t n_overflow_chunks;/* chunks whose distinct keys overflowed the SMEM hash table
                                   (counted by the device radix-sort fallback instead) */
     uint64_t n_order_oversize; /* survivors in S9 buckets above one chunk (sorted by the device LSD) */
+    uint64_t max_signature_windows; /* windows of the most frequent signature (Table 6) */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;
@@ -144,6 +145,9 @@ typedef struct {
                                   (a k-mer and its reverse complement share a bin either way).
                                   k = 32 and k = 64 are rejected (KMC_ERR_INVALID_ARG): the
                                   all-T k-mer is the all-ones key, the kernels' empty marker. */
+    uint32_t plain_minimizers; /* 1 (diagnostic): signatures are plain canonical minimizers, without
+                                  the P:L206-208 restrictions -- the "Minimizers" columns of
+                                  Table 6.  Same counts; different bins. */
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).
@@ -218,6 +222,9 @@ int kmc_record_words(int k);  /* uint32 words per super-k-mer record: 4 (k <= 32
  * no valid window starts at j. */
 kmc_status kmc_debug_signatures(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads,
                                 int k, int p, uint32_t* out_sig, void* stream);
+/* Same, plain_minimizers = 1: the minimum canonical p-mer with no restriction (Table 6). */
+kmc_status kmc_debug_signatures_ex(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads,
+                                   int k, int p, int plain_minimizers, uint32_t* out_sig, void* stream);
 
 /* Signature-rule test hook: out[i] = 1 if the p-mer with value i (i < 4^p) is an allowed
  * signature -- evaluated by the same device function the kernels use. */

@@ -35,7 +35,7 @@ class _Stats(ctypes.Structure):
         "n_reads", "n_bases", "n_invalid_bases", "n_windows", "n_superkmers", "n_records",
         "n_signatures_used", "n_bins", "n_large_bins", "max_bin_windows", "large_windows", "n_unique",
         "n_below_min", "n_above_max", "n_out", "n_launches", "n_input_batches", "n_large_groups",
-        "chunk_capacity", "n_overflow_chunks", "n_order_oversize")] + [
+        "chunk_capacity", "n_overflow_chunks", "n_order_oversize", "max_signature_windows")] + [
         ("stage_ms", ctypes.c_float * len(STAGES)), ("stage_launches", ctypes.c_uint32 * len(STAGES))]
 
     def to_dict(self) -> dict:
@@ -50,7 +50,8 @@ class _Options(ctypes.Structure):
                 ("force_large", ctypes.c_uint32), ("large_path", ctypes.c_uint32),
                 ("distribute_path", ctypes.c_uint32), ("input_batch_mb", ctypes.c_uint32),
                 ("large_group_mkeys", ctypes.c_uint32), ("count_path", ctypes.c_uint32),
-                ("chunk_capacity", ctypes.c_uint32), ("non_canonical", ctypes.c_uint32)]
+                ("chunk_capacity", ctypes.c_uint32), ("non_canonical", ctypes.c_uint32),
+                ("plain_minimizers", ctypes.c_uint32)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
@@ -84,6 +85,8 @@ def load():
                                      ctypes.POINTER(_Options)]
         lib.kmc_count_ex.restype = I
         lib.kmc_debug_signatures.argtypes = [P, P, U64, I, I, P, P]
+        lib.kmc_debug_signatures_ex.argtypes = [P, P, U64, I, I, I, P, P]
+        lib.kmc_debug_signatures_ex.restype = I
         lib.kmc_debug_signatures.restype = I
         lib.kmc_debug_allowed.argtypes = [I, P, P]
         lib.kmc_debug_allowed.restype = I
@@ -159,9 +162,10 @@ class Result:
 
 
 def _options(profile, small_bin_capacity, force_large, large_path=0, distribute_path=0, input_batch_mb=0,
-             large_group_mkeys=0, count_path=0, chunk_capacity=0, canonical=True):
+             large_group_mkeys=0, count_path=0, chunk_capacity=0, canonical=True, plain_minimizers=False):
     o = _Options()
     o.non_canonical = 0 if canonical else 1
+    o.plain_minimizers = int(bool(plain_minimizers))
     o.count_path = int(count_path)
     o.chunk_capacity = int(chunk_capacity)
     o.distribute_path = int(distribute_path)
@@ -178,7 +182,7 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
           profile: bool = False, small_bin_capacity: int = 0, force_large: bool = False,
           large_path: int = 0, distribute_path: int = 0, input_batch_mb: int = 0, large_group_mkeys: int = 0,
           count_path: int = 0, chunk_capacity: int = 0, out_device: str | None = None,
-          canonical: bool = True) -> Result:
+          canonical: bool = True, plain_minimizers: bool = False) -> Result:
     """Count canonical k-mers (KMC 2 hot path on the GPU); canonical=False counts them as
     they occur in the reads (KMC's -b).
 
@@ -194,7 +198,7 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
     if n_reads < 0:
         raise ValueError("offsets must have n_reads + 1 entries")
     opt = _options(profile, small_bin_capacity, force_large, large_path, distribute_path, input_batch_mb,
-                   large_group_mkeys, count_path, chunk_capacity, canonical)
+                   large_group_mkeys, count_path, chunk_capacity, canonical, plain_minimizers)
     job = ctypes.c_void_p()
     n_out = ctypes.c_uint64()
     sh = _stream_handle(stream)
@@ -358,14 +362,16 @@ def count_into(reads, offsets, k: int, p: int, cutoff_min: int, cutoff_max: int,
     return st.to_dict()
 
 
-def debug_signatures(reads, offsets, k: int, p: int, stream=None):
-    """Per-position window signature (S2 test hook): uint32 [n_bases], 0xFFFFFFFF = no window."""
+def debug_signatures(reads, offsets, k: int, p: int, stream=None, plain_minimizers: bool = False):
+    """Per-position window signature (S2 test hook): uint32 [n_bases], 0xFFFFFFFF = no window;
+    plain_minimizers: without the P:L206-208 restrictions (Table 6 diagnostic)."""
     import torch
     lib = load()
     n_reads = int(offsets.shape[0]) - 1
     n_bases = int(reads.shape[0])
     out = torch.empty((max(n_bases, 1),), dtype=torch.uint32, device=reads.device)
-    _check(lib.kmc_debug_signatures(_ptr(reads), _ptr(offsets), n_reads, k, p, _ptr(out), _stream_handle(stream)))
+    _check(lib.kmc_debug_signatures_ex(_ptr(reads), _ptr(offsets), n_reads, k, p, int(bool(plain_minimizers)),
+                                       _ptr(out), _stream_handle(stream)))
     return out[:n_bases]
 
 

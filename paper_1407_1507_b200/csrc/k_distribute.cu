@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             const uint32_t Rlo = rev2_32(~sA), Rhi = rev2_32(~sB);
             const uint32_t pvb = __funnelshift_r(S.vpm[j0 >> 5], S.vpm[(j0 >> 5) + 1], j0 & 31);
             uint64_t fbad = 0, rbad = 0;  // bit 2o: the forward / reverse p-mer at o is not allowed
-            if (p >= 3) {
+            if (p >= 3 && a.rules) {
                 constexpr uint64_t M5 = 0x5555555555555555ull;
                 const uint64_t Y = ~(((uint64_t)Rhi << 32) | Rlo), y1 = Y >> 1;
                 const uint64_t iA = ~(Y | y1) & M5, iT = Y & y1 & M5, iC = Y & ~y1 & M5, iG = ~Y & y1 & M5;

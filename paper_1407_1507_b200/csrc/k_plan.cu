@@ -61,6 +61,13 @@ __global__ void k_sig2bin(BoundaryIn bf, uint64_t ns, const uint64_t* B, uint32_
     }
     uint32_t t = block_sum<256, uint32_t>(used, ws);
     if (threadIdx.x == 0 && t) atomicAdd(&gstats[GS_SIGS_USED], (unsigned long long)t);
+    unsigned long long mx = i < ns ? hw[i] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(&gstats[GS_MAX_SIG], mx);
 }
 
 __global__ void k_bins(uint64_t ns, const uint64_t* B, const uint64_t* bin_first, const uint64_t* Wp,

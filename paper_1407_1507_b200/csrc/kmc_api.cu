@@ -379,6 +379,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     a.n_bases = n_bases;
     a.k = k;
     a.p = p;
+    a.rules = j->opt.plain_minimizers ? 0 : 1;
     a.reads_aligned16 = ((uintptr_t)d_reads & 15) == 0;
     a.tile_r_lo = tile_r_lo;
     a.hist_w = hist_w;
@@ -536,6 +537,7 @@ void plan_phase(kmc_job* j, PlanCtx& c) {
     j->st.n_records = n_records;
     j->st.n_invalid_bases = hs[16 + GS_INVALID];
     j->st.n_signatures_used = hs[16 + GS_SIGS_USED];
+    j->st.max_signature_windows = hs[16 + GS_MAX_SIG];
     j->st.n_bins = n_bins;
     if (c.check_p1 && (hs[16 + GS_WINDOWS] != n_windows || hs[16 + GS_RECORDS] != n_records)) {
         set_err("histogram totals disagree with pass-1 counters (%llu/%llu windows, %llu/%llu records)",
@@ -1393,6 +1395,11 @@ int kmc_record_words(int k) { return record_words(k); }
 
 kmc_status kmc_debug_signatures(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads, int k, int p,
                                 uint32_t* out_sig, void* stream) {
+    return kmc_debug_signatures_ex(reads, read_offsets, n_reads, k, p, 0, out_sig, stream);
+}
+
+kmc_status kmc_debug_signatures_ex(const uint8_t* reads, const uint64_t* read_offsets, uint64_t n_reads, int k, int p,
+                                   int plain_minimizers, uint32_t* out_sig, void* stream) {
     kmc_status v = validate(k, p, 1, 1);
     if (v != KMC_OK) return v;
     kmc_job j;
@@ -1437,6 +1444,7 @@ kmc_status kmc_debug_signatures(const uint8_t* reads, const uint64_t* read_offse
         a.n_bases = n_bases;
         a.k = k;
         a.p = p;
+        a.rules = plain_minimizers ? 0 : 1;
         a.reads_aligned16 = ((uintptr_t)d_reads & 15) == 0;
         a.tile_r_lo = tile_r_lo;
         a.dbg_sig = d_out;

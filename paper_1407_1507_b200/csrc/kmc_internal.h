@@ -20,6 +20,7 @@ enum {
     GS_LARGE_KEYS = 8,  // large-bin key cursor
     GS_SIGS_USED = 9,
     GS_TMP_RECS = 10,   // slots reserved in the temporary record stream by pass 1
+    GS_MAX_SIG = 11,    // windows of the most frequent signature
     GS_N = 16
 };
 
@@ -33,6 +34,7 @@ struct P1Args {
     uint64_t off0;
     uint64_t n_bases;
     int k, p;
+    int rules;  // 1: signatures obey P:L206-208; 0: plain canonical minimizers (diagnostic)
     int reads_aligned16;
     const uint64_t* tile_r_lo;  // first read index whose start lies after each segment's left edge
     // pass 1

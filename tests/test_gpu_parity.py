@@ -342,3 +342,28 @@ def test_noncanonical_rejects_k32(gpu):
     r, o = to_dev(w)
     with pytest.raises(Exception):
         gpu.count(r, o, 32, 9, 1, 10**9, canonical=False)
+
+
+# --- Table 6 diagnostic: plain canonical minimizers vs signatures ---------
+
+@pytest.mark.parametrize("k,p", [(28, 5), (28, 7), (55, 8), (21, 9), (12, 3)])
+def test_plain_minimizer_signatures(gpu, k, p):
+    seqs = synth.random_reads(k * 7 + p, 300, 0, 300, n_frac=0.01)
+    seqs += [b"A" * 200, b"ACA" * 50, b"AAT" * 40]
+    w = synth.from_strings(seqs, k, p, 1)
+    r, o = to_dev(w)
+    got = gpu.debug_signatures(r, o, k, p, plain_minimizers=True).cpu().numpy()
+    assert np.array_equal(got, oracle.signatures(w.reads, w.offsets, k, p, rules=False))
+
+
+@pytest.mark.parametrize("rules", [True, False])
+@pytest.mark.parametrize("name,scale", [("C1", 0.02), ("C3", 0.002)])
+def test_plain_minimizer_counts_and_stats(gpu, name, scale, rules):
+    w = synth.make(name, scale=scale)
+    keys, counts, st = gpu_count(gpu, w, plain_minimizers=not rules)
+    ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max)
+    assert np.array_equal(keys, ref.keys) and np.array_equal(counts, ref.counts)  # same counts either way
+    sig = oracle.signatures(w.reads, w.offsets, w.k, w.p, rules=rules)
+    sig = sig[sig != 0xFFFFFFFF]
+    assert st["max_signature_windows"] == int(np.bincount(sig).max())
+    assert st["n_superkmers"] == len(oracle.superkmers(w.reads, w.offsets, w.k, w.p, rules=rules))
