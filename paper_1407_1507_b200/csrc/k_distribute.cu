@@ -52,19 +52,22 @@ static_assert(NROW * 32 * 2 + 64 >= 2 * SEG, "run lists fit the phase-D scratch"
 static_assert(NROW == 18, "the block minimum uses 32 lanes x 18 positions");
 
 // A->0, C->1, G->2, T->3; lowercase folded; anything else invalid (R3).
+// Per 4 bytes: c = byte & 0xDF (case fold); code = ((c >> 1) ^ (c >> 2)) & 3 is 0/1/2/3 for
+// A/C/G/T; the byte is valid iff it equals the letter of its own code, looked up with one
+// byte permute; the 4 codes are packed by one multiply (byte i lands at bits 6-2i).
 __device__ __forceinline__ void encode16(const uint32_t (&wd)[4], uint32_t& packed, uint32_t& invbits) {
     packed = 0;
     invbits = 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const uint32_t c = wd[t] & 0xDFDFDFDFu;
-        const uint32_t ok = __vcmpeq4(c, 0x41414141u) | __vcmpeq4(c, 0x43434343u) | __vcmpeq4(c, 0x47474747u) |
-                            __vcmpeq4(c, 0x54545454u);
-        const uint32_t cd = ((c >> 1) ^ (c >> 2)) & 0x03030303u;  // per byte: A0 C1 G2 T3
-        const uint32_t b8 = ((cd & 0xFFu) << 6) | (((cd >> 8) & 0xFFu) << 4) | (((cd >> 16) & 0xFFu) << 2) | (cd >> 24);
-        packed |= b8 << (24 - 8 * t);
-        const uint32_t badb = (~ok) & 0x01010101u;
-        invbits |= (((badb * 0x01020408u) >> 24) & 0xFu) << (4 * t);
+        const uint32_t cd = ((c >> 1) ^ (c >> 2)) & 0x03030303u;         // per byte: A0 C1 G2 T3
+        const uint32_t sx = (cd | (cd >> 4)) & 0x00FF00FFu;                // codes as nibbles 0,1 | 2,3
+        const uint32_t sel = (sx | (sx >> 8)) & 0xFFFFu;
+        const uint32_t diff = __byte_perm(0x54474341u, 0u, sel) ^ c;        // 0 where the byte is its letter
+        const uint32_t bad = (((diff & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | diff) & 0x80808080u;  // bit 7: byte != 0
+        packed |= ((cd * 0x40100401u) >> 24) << (24 - 8 * t);
+        invbits |= (((bad >> 7) * 0x01020408u) >> 24 & 0xFu) << (4 * t);
     }
 }
 
