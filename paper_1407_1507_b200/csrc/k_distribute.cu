@@ -236,6 +236,17 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                 fbad = (ua >> 2) | (iA & (iC >> 2) & (iA >> 4));
                 rbad = ut | ((iT & (iG >> 2) & (iT >> 4)) >> (2 * (p - 3)));
             }
+            {  // invalid p-mers (bit o of pvb clear) count as not allowed in both orientations
+                uint64_t x = pvb & 0x3FFFFu;  // spread bit o to bit 2o
+                x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+                x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+                x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+                x = (x | (x << 2)) & 0x3333333333333333ull;
+                x = (x | (x << 1)) & 0x5555555555555555ull;
+                const uint64_t nv = ~x & 0x5555555555555555ull;
+                fbad |= nv;
+                rbad |= nv;
+            }
             const uint32_t mp = (uint32_t)(RES - 1);
 #pragma unroll
             for (int o = 0; o < 18; ++o) {
@@ -243,7 +254,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                 const uint32_t rc = (o < 16 ? __funnelshift_r(Rlo, Rhi, 2 * o) : (Rhi >> (2 * (o - 16)))) & mp;
                 const bool fw = fwd <= rc;
                 const uint32_t bad = (uint32_t)((fw ? fbad : rbad) >> (2 * o)) & 1u;
-                K[o] = (((pvb >> o) & 1u) && !bad) ? (fw ? fwd : rc) : RES;
+                K[o] = bad ? RES : (fw ? fwd : rc);
             }
         }
         // ---- D: sliding minimum over W keys: window y = min over keys [y, y + W)
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             const bool start = skm || (valid && v == 0);
             const uint32_t bE = __ballot_sync(0xffffffffu, !valid || start);
             const uint32_t bS = __ballot_sync(0xffffffffu, start);
-            l_skm += skm;
+            if (r == 0 && lane == 0) l_skm -= start && !skm;  // the segment-edge start is no new run
             if (lane == 0) S.ebits[r] = bE;
             if (start) {
                 const int at = nstarts + __popc(bS & ltm);
@@ -351,7 +362,10 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             nstarts += __popc(bS);
         }
         if (MODE == P1_MODE_DEBUG) continue;
-        if (lane == 0) S.ebits[SEG / 32] = 1u;  // sentinel: the segment edge ends every run
+        if (lane == 0) {
+            S.ebits[SEG / 32] = 1u;  // sentinel: the segment edge ends every run
+            l_skm += nstarts;        // starts that are super-k-mer starts (the edge one corrected above)
+        }
         __syncwarp();
         for (int i0 = 0; i0 < nstarts; i0 += 32) {
             const int idx = i0 + lane;
