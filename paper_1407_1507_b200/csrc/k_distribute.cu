@@ -499,26 +499,33 @@ __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restric
     const int nd = 1 << D;
     for (int d = threadIdx.x; d < 256; d += RS_NT) lh[d] = 0;
     __syncthreads();
+    // all loads of the tile are issued before any is used (ids, records, then the bin lookups)
     V r0[IPT], r1[IPT];
-    uint32_t bin[IPT], dr[IPT];
+    uint32_t id[IPT], bin[IPT], dr[IPT];
 #pragma unroll
     for (int u = 0; u < IPT; ++u) {
         const uint32_t i = threadIdx.x + u * RS_NT;
+        id[u] = i < t.n ? __ldcs(in_ids + t.begin + i) : INV;
+    }
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+        const uint32_t i = threadIdx.x + u * RS_NT;
+        if (i < t.n) {  // slots tagged INV hold no record; loading them is harmless
+            const V* src = reinterpret_cast<const V*>(in_recs + (t.begin + i) * (uint64_t)RW);
+            r0[u] = __ldcs(src);
+            if (RW == 8) r1[u] = __ldcs(src + 1);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) bin[u] = (sig2bin && id[u] != INV) ? sig2bin[id[u]] : id[u];
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
         dr[u] = INV;
-        bin[u] = INV;
-        if (i < t.n) {
-            const uint32_t id = __ldcs(in_ids + t.begin + i);
-            uint32_t b = id;
-            if (sig2bin && b != INV) b = sig2bin[b];
-            if (b != INV) {
-                const V* src = reinterpret_cast<const V*>(in_recs + (t.begin + i) * (uint64_t)RW);
-                r0[u] = __ldcs(src);
-                if (RW == 8) r1[u] = __ldcs(src + 1);
-                bin[u] = out_orig_ids ? id : b;
-                b = out_orig_ids ? sig2bin[id] : b;
-                const uint32_t d = (b >> shift) & (uint32_t)(nd - 1);
-                dr[u] = (d << 16) | atomicAdd(&lh[d], 1u);  // rank < TI
-            }
+        if (bin[u] != INV) {
+            const uint32_t b = bin[u];
+            if (out_orig_ids) bin[u] = id[u];
+            const uint32_t d = (b >> shift) & (uint32_t)(nd - 1);
+            dr[u] = (d << 16) | atomicAdd(&lh[d], 1u);  // rank < TI
         }
     }
     __syncthreads();
