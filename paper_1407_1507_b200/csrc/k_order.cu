@@ -65,7 +65,18 @@ __global__ void __launch_bounds__(OT_NT) k_ord_hist(const K* __restrict__ keys, 
     const OrdTile t = tiles[blockIdx.x];
     for (int d = threadIdx.x; d < (1 << D); d += OT_NT) h[d] = 0;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < t.n; i += OT_NT) atomicAdd(&h[hi_digit(ld_stream(keys + t.begin + i), top, D)], 1u);
+    constexpr int HU = 4;  // loads in flight per thread
+    for (uint32_t i0 = threadIdx.x; i0 < t.n; i0 += HU * OT_NT) {
+        K kk[HU];
+#pragma unroll
+        for (int u = 0; u < HU; ++u) {
+            const uint32_t i = i0 + u * OT_NT;
+            if (i < t.n) kk[u] = ld_stream(keys + t.begin + i);
+        }
+#pragma unroll
+        for (int u = 0; u < HU; ++u)
+            if (i0 + u * OT_NT < t.n) atomicAdd(&h[hi_digit(kk[u], top, D)], 1u);
+    }
     __syncthreads();
     for (int d = threadIdx.x; d < (1 << D); d += OT_NT)
         if (h[d]) atomicAdd(&hist[((uint64_t)t.bucket << D) + d], h[d]);
@@ -96,12 +107,18 @@ __global__ void __launch_bounds__(OT_NT) k_ord_scatter(const K* __restrict__ kin
     K key[IPT];
     uint32_t val[IPT], dr[IPT];
 #pragma unroll
+    for (int u = 0; u < IPT; ++u) {  // every load of the tile in flight before the first use
+        const uint32_t i = threadIdx.x + u * OT_NT;
+        if (i < t.n) {
+            key[u] = ld_stream(kin + t.begin + i);
+            val[u] = __ldcs(vin + t.begin + i);
+        }
+    }
+#pragma unroll
     for (int u = 0; u < IPT; ++u) {
         const uint32_t i = threadIdx.x + u * OT_NT;
         dr[u] = 0xFFFFFFFFu;
         if (i < t.n) {
-            key[u] = ld_stream(kin + t.begin + i);
-            val[u] = __ldcs(vin + t.begin + i);
             const uint32_t d = hi_digit(key[u], top, D);
             dr[u] = (d << 16) | atomicAdd(&lh[d], 1u);  // rank < TI <= 4096
         }

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(SB_NT, 2) k_small_bins(SmallArgs a) {
         const uint4* src = reinterpret_cast<const uint4*>(a.bins + rec0 * RW);
         uint4* dst = reinterpret_cast<uint4*>(R);
         const int nv = nrec * RW / 4;
+#pragma unroll 4
         for (int v = threadIdx.x; v < nv; v += SB_NT) dst[v] = src[v];
     }
     __syncthreads();
