@@ -260,10 +260,10 @@ __device__ __forceinline__ K128 ld_stream(const K128* p) {
 // Slot hash of a key for a table of 2^lg slots: two multiply-xorshift rounds, independent
 // of part_digit (the chunk's keys share their part_digit).
 __device__ __forceinline__ uint32_t slot_hash(uint64_t key, int lg) {
-    uint64_t x = key * 0xFF51AFD7ED558CCDull;
-    x ^= x >> 32;
-    x *= 0x9E3779B97F4A7C15ull;
-    return (uint32_t)(x >> (64 - lg));
+    // two 32-bit multiply rounds (the high half mixed in first); constants differ from
+    // part_digit's so a chunk's common digit bits do not bias the slots
+    const uint32_t h = (((uint32_t)(key >> 32) * 0x2C1B3C6Du) ^ (uint32_t)key) * 0x297A2D39u;
+    return (h ^ (h >> 16)) * 0x7FEB352Du >> (32 - lg);
 }
 __device__ __forceinline__ uint32_t slot_hash(const K128& key, int lg) {
     uint64_t x = (key.lo ^ (key.hi * 0xC2B2AE3D27D4EB4Full)) * 0xFF51AFD7ED558CCDull;
