@@ -189,6 +189,8 @@ struct PlanCtx {
     uint32_t* tmp_recs = nullptr;
     uint32_t* tmp_sig = nullptr;
     std::vector<uint64_t> bw, bn, bo;  // per bin: windows, records, first record
+    bool tables_pending = false;       // bw/bn/bo not yet copied to the host (fetch_tables)
+    cudaEvent_t ev_plan = nullptr;     // recorded on the job stream right after the plan
     P1Args a{};
     std::function<int(int)> run_p1;  // pass-1 recompute (S5 fallback), unset when sharded
     // sharded: bin -> owning rank
@@ -259,6 +261,7 @@ struct kmc_job {
             cudaEventDestroy(e.b);
         }
         if (cur_a) cudaEventDestroy(cur_a);
+        if (ctx.ev_plan) cudaEventDestroy(ctx.ev_plan);
         if (cs) {
             cudaStreamSynchronize(cs);
             for (int t = 0; t < 2; ++t) {
@@ -306,6 +309,7 @@ void read_extent(kmc_job* j, const uint64_t* offsets, uint64_t n_reads, uint64_t
 }
 
 void plan_phase(kmc_job* j, PlanCtx& c);
+void fetch_tables(kmc_job* j, PlanCtx& c);
 void count_phase(kmc_job* j, PlanCtx& c);
 
 void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads) {
@@ -546,16 +550,28 @@ void plan_phase(kmc_job* j, PlanCtx& c) {
         throw Fail{KMC_ERR_INTERNAL};
     }
     if (n_windows == 0) return;
-    std::vector<uint64_t>& bw = c.bw;
-    std::vector<uint64_t>& bn = c.bn;
-    std::vector<uint64_t>& bo = c.bo;
-    bw.assign(n_bins, 0);
-    bn.assign(n_bins, 0);
-    bo.assign(n_bins, 0);
-    CK(cudaMemcpyAsync(bw.data(), pa.bin_w, n_bins * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(bn.data(), pa.bin_nrec, n_bins * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(bo.data(), pa.bin_rec_off, n_bins * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    c.tables_pending = true;  // the per-bin tables reach the host later (fetch_tables)
+    CK(cudaEventCreateWithFlags(&c.ev_plan, cudaEventDisableTiming));
+    CK(cudaEventRecord(c.ev_plan, s));
+}
+
+// Per-bin host tables (windows, records, first record), copied on the copy stream once the
+// plan is done, so that the caller can enqueue device work (S5) before waiting for them.
+void fetch_tables(kmc_job* j, PlanCtx& c) {
+    if (!c.tables_pending) return;
+    c.tables_pending = false;
+    const uint64_t n_bins = c.n_bins;
+    c.bw.assign(n_bins, 0);
+    c.bn.assign(n_bins, 0);
+    c.bo.assign(n_bins, 0);
+    j->make_copy_stream();
+    CK(cudaStreamWaitEvent(j->cs, c.ev_plan, 0));
+    cudaEventDestroy(c.ev_plan);
+    c.ev_plan = nullptr;
+    CK(cudaMemcpyAsync(c.bw.data(), c.pa.bin_w, n_bins * 8, cudaMemcpyDeviceToHost, j->cs));
+    CK(cudaMemcpyAsync(c.bn.data(), c.pa.bin_nrec, n_bins * 8, cudaMemcpyDeviceToHost, j->cs));
+    CK(cudaMemcpyAsync(c.bo.data(), c.pa.bin_rec_off, n_bins * 8, cudaMemcpyDeviceToHost, j->cs));
+    CK(cudaStreamSynchronize(j->cs));
 }
 
 // S5-S8 from the record stream in c (tmp_recs / tmp_sig, tmp_n slots) and the plan:
@@ -581,27 +597,6 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         j->n_surv = 0;
         return;
     }
-    // ---- host: classify bins (small: one CTA in SMEM; large: multi-CTA path)
-    std::vector<uint32_t> small;
-    std::vector<uint64_t> large_ids;
-    uint64_t large_windows = 0, n_large = 0, max_bin = 0;
-    for (uint64_t b = 0; b < n_bins; ++b) {
-        if (bw[b] == 0) continue;
-        max_bin = std::max(max_bin, bw[b]);
-        const uint64_t cost = std::max<uint64_t>(bw[b], bn[b] * pa.recw);
-        if (cost <= (uint64_t)cap && !j->opt.force_large) {
-            small.push_back((uint32_t)b);
-        } else {
-            ++n_large;
-            large_windows += bw[b];
-            large_ids.push_back(b);
-        }
-    }
-    std::sort(small.begin(), small.end(), [&](uint32_t x, uint32_t y) { return bw[x] > bw[y] || (bw[x] == bw[y] && x < y); });
-    j->st.n_large_bins = n_large;
-    j->st.large_windows = large_windows;
-    j->st.max_bin_windows = max_bin;
-
     // ---- S5: records into bins -- a copy from pass 1's temporary stream, or (if the stream
     //      overflowed its estimate) pass 2 = S1-S3 recomputed + scatter
     uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4));
@@ -680,6 +675,29 @@ void count_phase(kmc_job* j, PlanCtx& c) {
     ar.release(pa.rec_scan);
     ar.release(pa.bin_first);
     ar.release(pa.temp);
+
+    // the per-bin tables were copied to the host while S5 runs on the device
+    fetch_tables(j, c);
+    // ---- host: classify bins (small: one CTA in SMEM; large: multi-CTA path)
+    std::vector<uint32_t> small;
+    std::vector<uint64_t> large_ids;
+    uint64_t large_windows = 0, n_large = 0, max_bin = 0;
+    for (uint64_t b = 0; b < n_bins; ++b) {
+        if (bw[b] == 0) continue;
+        max_bin = std::max(max_bin, bw[b]);
+        const uint64_t cost = std::max<uint64_t>(bw[b], bn[b] * pa.recw);
+        if (cost <= (uint64_t)cap && !j->opt.force_large) {
+            small.push_back((uint32_t)b);
+        } else {
+            ++n_large;
+            large_windows += bw[b];
+            large_ids.push_back(b);
+        }
+    }
+    std::sort(small.begin(), small.end(), [&](uint32_t x, uint32_t y) { return bw[x] > bw[y] || (bw[x] == bw[y] && x < y); });
+    j->st.n_large_bins = n_large;
+    j->st.large_windows = large_windows;
+    j->st.max_bin_windows = max_bin;
 
     // ---- survivors buffer: every survivor has count >= ci, counts sum to n_windows
     const uint64_t surv_cap = n_windows / j->ci + 1;
@@ -829,8 +847,12 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         int sl = 0;
         for (const auto& g : groups) {
             const size_t gn = g.second - g.first;
-            std::vector<LargeBin> lbins(gn);
-            std::vector<uint64_t> pp(gn + 1, 0);
+            // host tables reused across calls on this thread (fresh MB-sized vectors cost
+            // page faults on the critical path between the small-bin and split kernels)
+            static thread_local std::vector<LargeBin> lbins;
+            static thread_local std::vector<uint64_t> pp;
+            lbins.resize(gn);
+            pp.assign(gn + 1, 0);
             uint64_t key_base = 0, digit_base = 0;
             int dmax = 1;
             for (size_t i = 0; i < gn; ++i) {
@@ -1283,6 +1305,7 @@ kmc_status kmc_shard_partition(kmc_job* j, const uint64_t* global_hist_w, const 
         CK(launch_narrow(gr, ns, c.hist_r, s));
         c.check_p1 = false;
         plan_phase(j, c);
+        fetch_tables(j, c);
         ar.release(gr);
         c.owner.assign(c.n_bins, 0);
         if (c.n_bins) kmc_shard_owners(c.bw.data(), c.n_bins, world, c.owner.data());
