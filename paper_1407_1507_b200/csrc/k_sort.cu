@@ -583,6 +583,8 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     uint64_t tab = 0;  // table index of digit 0 of the current segment
     bool pm = false, staged = false;
     uint32_t npk = 0;  // piece mode: keys of the piece
+    uint32_t pf0 = 0, pf1 = 0;        // scatter, piece mode: prefetched table entries ...
+    uint64_t pf_piece = ~0ull;        // ... of this piece
     for (uint64_t p = p0; p < p1; ++p) {
         const uint32_t it = (uint32_t)(p - p0);
         const int b = it & 1;
@@ -614,9 +616,16 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
             if (SCATTER) {
                 uint32_t c = 0;
                 if (mine) {
-                    const uint64_t ix = tab + (uint64_t)threadIdx.x * lb.nseg;
-                    const uint32_t g0 = table[ix];
-                    c = table[ix + 1] - g0;  // next entry: same digit, next piece (or next digit)
+                    uint32_t g0, g1;
+                    if (pf_piece == p) {  // prefetched during the previous piece
+                        g0 = pf0;
+                        g1 = pf1;
+                    } else {
+                        const uint64_t ix = tab + (uint64_t)threadIdx.x * lb.nseg;
+                        g0 = table[ix];
+                        g1 = table[ix + 1];  // next entry: same digit, next piece (or next digit)
+                    }
+                    c = g1 - g0;
                     gst[threadIdx.x] = g0;
                     lc[threadIdx.x] = 0;
                 }
@@ -627,6 +636,16 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                 h[threadIdx.x] = 0;
             }
             __syncthreads();
+        }
+        if (SCATTER && sizeof(K) == 8 && p + 1 < p1) {
+            // the next piece's table entries are loaded now and used after this piece
+            const Piece pn = pieces[p + 1];
+            if (pn.lbin == cur && pm && threadIdx.x < (1u << D)) {
+                const uint64_t ix = lb.tb + (p + 1 - lb.first_range) + (uint64_t)threadIdx.x * lb.nseg;
+                pf0 = table[ix];
+                pf1 = table[ix + 1];
+                pf_piece = p + 1;
+            }
         }
         mbar_wait(mbar + b, (it >> 1) & 1);
         // warp w expands records [32w, 32w+32) of the piece (S6): a lane takes a unit of up
