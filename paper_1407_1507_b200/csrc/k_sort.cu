@@ -585,6 +585,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     uint32_t npk = 0;  // piece mode: keys of the piece
     uint32_t pf0 = 0, pf1 = 0;        // scatter, piece mode: prefetched table entries ...
     uint64_t pf_piece = ~0ull;        // ... of this piece
+    Piece pnext = pieces[p0];  // piece descriptors are loaded one iteration ahead
     for (uint64_t p = p0; p < p1; ++p) {
         const uint32_t it = (uint32_t)(p - p0);
         const int b = it & 1;
@@ -592,7 +593,8 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
             fence_proxy_async_smem();  // buffer b^1 was released by the previous iteration's barrier
             issue(p + 1, b ^ 1);
         }
-        const Piece pc = pieces[p];
+        const Piece pc = pnext;
+        if (p + 1 < p1) pnext = pieces[p + 1];
         if (pc.lbin != cur) {
             if (!SCATTER && cur != 0xFFFFFFFFu && !pm) {
                 for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT) table[tab + (uint64_t)d * lb.nseg] = h[d];
@@ -639,7 +641,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
         }
         if (SCATTER && sizeof(K) == 8 && p + 1 < p1) {
             // the next piece's table entries are loaded now and used after this piece
-            const Piece pn = pieces[p + 1];
+            const Piece pn = pnext;
             if (pn.lbin == cur && pm && threadIdx.x < (1u << D)) {
                 const uint64_t ix = lb.tb + (p + 1 - lb.first_range) + (uint64_t)threadIdx.x * lb.nseg;
                 pf0 = table[ix];
