@@ -811,20 +811,13 @@ __device__ __forceinline__ bool table_insert_bounded(K* T, uint32_t* C, int lg, 
     const K E = key_empty<K>();
     uint32_t s = slot_hash(key, lg);
     for (int pr = 0; pr < PROBE_MAX; ++pr) {
-        const K cur = smem_load_volatile(&T[s]);
-        if (!key_eq(cur, key)) {
-            if (!key_eq(cur, E)) {
-                s = (s + 1) & mask;
-                continue;
-            }
-            const K old = smem_cas_empty(&T[s], key);
-            if (!key_eq(old, E) && !key_eq(old, key)) {
-                s = (s + 1) & mask;
-                continue;
-            }
+        // one shared CAS per probe: it claims an empty slot, or returns the key that holds it
+        const K old = smem_cas_empty(&T[s], key);
+        if (key_eq(old, E) || key_eq(old, key)) {
+            atomicAdd(&C[s], 1u);
+            return true;
         }
-        atomicAdd(&C[s], 1u);
-        return true;
+        s = (s + 1) & mask;
     }
     return false;
 }
