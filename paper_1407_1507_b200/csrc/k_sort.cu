@@ -585,6 +585,12 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     uint32_t npk = 0;  // piece mode: keys of the piece
     uint32_t pf0 = 0, pf1 = 0;        // scatter, piece mode: prefetched table entries ...
     uint64_t pf_piece = ~0ull;        // ... of this piece
+    __shared__ uint32_t s_npk;
+    uint32_t* hp = lof;               // count, piece mode: this piece's digit counters (lof / lc)
+    if (!SCATTER) {
+        for (int d = threadIdx.x; d < 512; d += SP_NT) lof[d] = 0;  // lof and lc (adjacent)
+        __syncthreads();
+    }
     Piece pnext = pieces[p0];  // piece descriptors are loaded one iteration ahead
     for (uint64_t p = p0; p < p1; ++p) {
         const uint32_t it = (uint32_t)(p - p0);
@@ -631,13 +637,22 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                     gst[threadIdx.x] = g0;
                     lc[threadIdx.x] = 0;
                 }
-                const uint32_t lo = block_excl_sum<SP_NT, uint32_t>(c, wsum, &npk);
-                if (mine) lof[threadIdx.x] = lo;
+                if (D <= 5) {  // every digit in warp 0: shuffle scan, one barrier
+                    if (warp == 0) {
+                        const uint32_t inc = warp_incl_sum(c);
+                        if (mine) lof[lane] = inc - c;
+                        if (lane == 31) s_npk = inc;
+                    }
+                    __syncthreads();
+                    npk = s_npk;
+                } else {
+                    const uint32_t lo = block_excl_sum<SP_NT, uint32_t>(c, wsum, &npk);
+                    if (mine) lof[threadIdx.x] = lo;
+                    __syncthreads();
+                }
                 staged = npk <= (uint32_t)SP_STAGE;
-            } else if (mine) {
-                h[threadIdx.x] = 0;
             }
-            __syncthreads();
+            // count: the piece's counters (lof / lc alternately) were zeroed after their last use
         }
         if (SCATTER && sizeof(K) == 8 && p + 1 < p1) {
             // the next piece's table entries are loaded now and used after this piece
@@ -685,7 +700,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                                 const uint32_t slot = atomicAdd(&h[dg], 1u);
                                 if (SCATTER) out[slot] = (K)key;
                             } else if (!SCATTER) {
-                                atomicAdd(&h[dg], 1u);
+                                atomicAdd(&hp[dg], 1u);
                             } else {
                                 const uint32_t rk = atomicAdd(&lc[dg], 1u);
                                 if (staged) {
@@ -727,9 +742,13 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                     }
                     __syncthreads();
                 }
-            } else if (threadIdx.x < (1u << D)) {
-                // the same thread zeroes h[d] for the next piece (or range-mode bin)
-                table[tab + (uint64_t)threadIdx.x * lb.nseg] = h[threadIdx.x];
+            } else {
+                if (threadIdx.x < (1u << D)) {
+                    // written and zeroed for the piece after next (double-buffered counters)
+                    table[tab + (uint64_t)threadIdx.x * lb.nseg] = hp[threadIdx.x];
+                    hp[threadIdx.x] = 0;
+                }
+                hp = (hp == lof) ? lc : lof;
             }
         }
     }
