@@ -193,42 +193,46 @@ __global__ void __launch_bounds__(WS_NT) k_ord_classify(const uint32_t* __restri
                                                         Chunk* __restrict__ big, Chunk* __restrict__ over,
                                                         unsigned long long* __restrict__ counters) {
     __shared__ uint32_t wsum[WS_NT / 32 + 1];
-    __shared__ unsigned long long base[5];
+    __shared__ unsigned long long base[6];
     const uint64_t d = (uint64_t)blockIdx.x * WS_NT + threadIdx.x;
-    int cls = -1;  // 0/1/2: warp sort of 64/128/256 items, 3: CTA sort, 4: oversize
+    int cls = -1;  // 0/1/2/3: warp sort of 32/64/128/256 items, 4: CTA sort, 5: oversize
     uint32_t st = 0, sz = 0;
     if (d < nbk) {
         const uint32_t c = cnt[d];
         st = start[d];
         if (c > 32) {
             sz = c;
-            cls = c <= 64 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= cap ? 3 : 4;
+            cls = c <= 64 ? 1 : c <= 128 ? 2 : c <= 256 ? 3 : c <= cap ? 4 : 5;
         } else {
             const bool lead = d == 0 || cnt[d - 1] > 32 || (start[d - 1] >> 5) != (st >> 5);
             if (lead) {
                 uint64_t e = d + 1;
                 while (e < nbk && cnt[e] <= 32 && (start[e] >> 5) == (st >> 5)) ++e;
                 sz = (e < nbk ? start[e] : n) - st;
-                if (sz) cls = 0;
+                if (sz) cls = sz <= 32 ? 0 : 1;
             }
         }
     }
-    uint32_t off[5], tot[5];
+    uint32_t off[6], tot[6];
 #pragma unroll
-    for (int l = 0; l < 5; ++l) off[l] = block_excl_sum<WS_NT, uint32_t>(cls == l ? 1u : 0u, wsum, &tot[l]);
-    if (threadIdx.x < 5) {
-        const uint32_t t = tot[0] * (threadIdx.x == 0) + tot[1] * (threadIdx.x == 1) + tot[2] * (threadIdx.x == 2) +
-                           tot[3] * (threadIdx.x == 3) + tot[4] * (threadIdx.x == 4);
+    for (int l = 0; l < 6; ++l) off[l] = block_excl_sum<WS_NT, uint32_t>(cls == l ? 1u : 0u, wsum, &tot[l]);
+    if (threadIdx.x < 6) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int l = 0; l < 6; ++l) t = threadIdx.x == l ? tot[l] : t;
         base[threadIdx.x] = t ? atomicAdd(&counters[threadIdx.x], (unsigned long long)t) : 0ull;
     }
     __syncthreads();
     if (cls >= 0) {
         const Chunk ch{st, sz, 0};
         const uint64_t q = base[cls] + off[cls];
+        // warp-sort lists in 2 nbk slots: sizes <= 32 / <= 64 from both ends of the first half
+        // (together at most one item per bucket), <= 128 / <= 256 from both ends of the second
         if (cls == 0) wl[q] = make_uint2(st, sz);
-        else if (cls == 1) wl[nbk + q] = make_uint2(st, sz);
-        else if (cls == 2) wl[2 * nbk - 1 - q] = make_uint2(st, sz);
-        else if (cls == 3) big[q] = ch;
+        else if (cls == 1) wl[nbk - 1 - q] = make_uint2(st, sz);
+        else if (cls == 2) wl[nbk + q] = make_uint2(st, sz);
+        else if (cls == 3) wl[2 * nbk - 1 - q] = make_uint2(st, sz);
+        else if (cls == 4) big[q] = ch;
         else over[q] = ch;
     }
 }
@@ -401,29 +405,30 @@ cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uin
         chunk_list = big;
         over_list = over;
         if ((e = cudaGetLastError())) return e;
-        if ((e = cudaMemcpyAsync(os.host, os.counters, 40, cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaMemcpyAsync(os.host, os.counters, 48, cudaMemcpyDeviceToHost, s))) return e;
         if ((e = cudaStreamSynchronize(s))) return e;
-        const uint64_t nw0 = os.host[0], nw1 = os.host[1], nw2 = os.host[2];
-        n_chunks = os.host[3];
-        n_over = os.host[4];
+        const uint64_t nw[4] = {os.host[0], os.host[1], os.host[2], os.host[3]};
+        n_chunks = os.host[4];
+        n_over = os.host[5];
         constexpr int WPB = WS_NT / 32;
-        const uint2* wl[3] = {wlist, wlist + nbk, wlist + 2 * nbk - 1};
-        const int dir[3] = {1, 1, -1};
-        const uint64_t nw[3] = {nw0, nw1, nw2};
+        const uint2* wl[4] = {wlist, wlist + nbk - 1, wlist + nbk, wlist + 2 * nbk - 1};
+        const int dir[4] = {1, -1, 1, -1};
         const bool pack = twok <= 56;
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < 4; ++q) {
             if (!nw[q]) continue;
             const unsigned g = (unsigned)((nw[q] + WPB - 1) / WPB);
 #define KMC_WSORT(R)                                                                                          \
     (pack ? k_ord_wsort<R, true><<<g, WS_NT, 0, s>>>(ck, cv, wl[q], nw[q], dir[q], out_keys, out_vals)          \
           : k_ord_wsort<R, false><<<g, WS_NT, 0, s>>>(ck, cv, wl[q], nw[q], dir[q], out_keys, out_vals))
-            if (q == 0) KMC_WSORT(2);
-            if (q == 1) KMC_WSORT(4);
-            if (q == 2) KMC_WSORT(8);
+            if (q == 0) KMC_WSORT(1);
+            if (q == 1) KMC_WSORT(2);
+            if (q == 2) KMC_WSORT(4);
+            if (q == 3) KMC_WSORT(8);
 #undef KMC_WSORT
+            *launches += 1;
         }
         if ((e = cudaGetLastError())) return e;
-        *launches += 1 + (nw0 > 0) + (nw1 > 0) + (nw2 > 0);
+        *launches += 1;
     } else {
         GreedyArgs ga{};
         ga.cnt = os.hist;
