@@ -301,26 +301,6 @@ __device__ __forceinline__ K128 smem_cas_empty(K128* p, const K128& key) {
     return o;
 }
 
-// Counts key in the open-addressing table (T keys, C counts, 2^lg slots, linear probing):
-// the slot holding key, or an empty slot claimed with CAS, gets +1.  The table must keep
-// at least one empty slot (callers size it to >= 4/3 of the keys inserted).
-template <class K>
-__device__ __forceinline__ void table_insert(K* T, uint32_t* C, int lg, const K& key) {
-    const uint32_t mask = (1u << lg) - 1;
-    const K E = key_empty<K>();
-    uint32_t s = slot_hash(key, lg);
-    while (true) {
-        const K cur = smem_load_volatile(&T[s]);
-        if (key_eq(cur, key)) break;
-        if (key_eq(cur, E)) {
-            const K old = smem_cas_empty(&T[s], key);
-            if (key_eq(old, E) || key_eq(old, key)) break;
-        }
-        s = (s + 1) & mask;
-    }
-    atomicAdd(&C[s], 1u);
-}
-
 // ---------------------------------------------------------------- warp / block helpers
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
