@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
     const uint32_t RES = 1u << (2 * p);
     const int NK = SEG + W;  // p-mer positions y = 0..NK-1 (local 15 + y)
 
-    uint64_t l_windows = 0, l_skm = 0, l_recs = 0, l_inv = 0;
+    uint32_t l_windows = 0, l_skm = 0, l_recs = 0, l_inv = 0;  // per lane (< 2^32: a lane sees < 2^32 bases)
     uint64_t blk_cur = 0, blk_end = 0;  // this warp's reserved temporary-stream slots
     bool tmp_ok = a.tmp_recs != nullptr;
 
