@@ -531,7 +531,7 @@ template <class K> __host__ __device__ int split_own_bytes(int k) {  // unit -> 
 // bytes of the counter region; the scatter of 64-bit keys aliases it with the piece stage
 template <class K, bool SC> __host__ __device__ int split_hreg(int dmax) {
     const int hb = split_hwords(dmax) * 4;
-    const int st = (SC && sizeof(K) == 8) ? SP_STAGE * 9 : 0;  // keys + digit bytes
+    const int st = (SC && sizeof(K) == 8) ? SP_STAGE * 8 : 0;  // staged keys
     return hb > st ? hb : st;
 }
 template <class K, bool SC> size_t split_smem(int k, int dmax) {
@@ -553,8 +553,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     const int OWN = split_own_bytes<K>(k);
     const int HREG = split_hreg<K, SCATTER>(dmax);
     uint32_t* h = reinterpret_cast<uint32_t*>(smem);
-    K* stage = reinterpret_cast<K*>(smem);                // piece mode (scatter): keys by digit
-    uint8_t* sdig = smem + (size_t)SP_STAGE * sizeof(K);  // ... and their digits
+    K* stage = reinterpret_cast<K*>(smem);  // piece mode (scatter): keys by digit
     uint32_t* gst = reinterpret_cast<uint32_t*>(smem + HREG);  // piece mode: first position of digit d
     uint32_t* lof = gst + 256;                                 // ... its offset in the stage
     uint32_t* lc = lof + 256;                                  // ... keys placed so far
@@ -583,6 +582,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     uint64_t tab = 0;  // table index of digit 0 of the current segment
     bool pm = false, staged = false;
     uint32_t npk = 0;  // piece mode: keys of the piece
+    bool bulk_pending = false;        // scatter: this thread's bulk copy may still read the stage
     uint32_t pf0 = 0, pf1 = 0;        // scatter, piece mode: prefetched table entries ...
     uint64_t pf_piece = ~0ull;        // ... of this piece
     __shared__ uint32_t s_npk;
@@ -601,7 +601,12 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
         }
         const Piece pc = pnext;
         if (p + 1 < p1) pnext = pieces[p + 1];
+        if (SCATTER && bulk_pending) {  // the previous piece's stage has been read out
+            bulk_wait_read();
+            bulk_pending = false;
+        }
         if (pc.lbin != cur) {
+            if (SCATTER) __syncthreads();  // h aliases the stage: every copy has read it
             if (!SCATTER && cur != 0xFFFFFFFFu && !pm) {
                 for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT) table[tab + (uint64_t)d * lb.nseg] = h[d];
                 __syncthreads();
@@ -637,20 +642,25 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                     gst[threadIdx.x] = g0;
                     lc[threadIdx.x] = 0;
                 }
+                // stage layout: one spare slot per digit so that every digit's run starts at
+                // the parity of its global position (16-byte aligned bulk copies out)
+                const uint32_t cp = mine ? c + 1 : 0u;
+                uint32_t P;
                 if (D <= 5) {  // every digit in warp 0: shuffle scan, one barrier
                     if (warp == 0) {
-                        const uint32_t inc = warp_incl_sum(c);
-                        if (mine) lof[lane] = inc - c;
+                        const uint32_t inc = warp_incl_sum(cp);
+                        P = inc - cp;
                         if (lane == 31) s_npk = inc;
+                        if (mine) lof[lane] = P + ((P ^ gst[lane]) & 1u);
                     }
                     __syncthreads();
                     npk = s_npk;
                 } else {
-                    const uint32_t lo = block_excl_sum<SP_NT, uint32_t>(c, wsum, &npk);
-                    if (mine) lof[threadIdx.x] = lo;
+                    P = block_excl_sum<SP_NT, uint32_t>(cp, wsum, &npk);
+                    if (mine) lof[threadIdx.x] = P + ((P ^ gst[threadIdx.x]) & 1u);
                     __syncthreads();
                 }
-                staged = npk <= (uint32_t)SP_STAGE;
+                staged = npk <= (uint32_t)SP_STAGE;  // npk: keys + one spare slot per digit
             }
             // count: the piece's counters (lof / lc alternately) were zeroed after their last use
         }
@@ -704,9 +714,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                             } else {
                                 const uint32_t rk = atomicAdd(&lc[dg], 1u);
                                 if (staged) {
-                                    const uint32_t q = lof[dg] + rk;
-                                    stage[q] = (K)key;
-                                    sdig[q] = (uint8_t)dg;
+                                    stage[lof[dg] + rk] = (K)key;
                                 } else {
                                     out[gst[dg] + rk] = (K)key;
                                 }
@@ -732,15 +740,29 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                 }
             }
         }
+        if (SCATTER && pm && staged) fence_proxy_async_smem();  // stage writes -> the bulk copies
         __syncthreads();
         if (pm) {
             if (SCATTER) {
-                if (staged) {  // the piece's keys, digit after digit: coalesced runs
-                    for (uint32_t i = threadIdx.x; i < npk; i += SP_NT) {
-                        const uint32_t d = sdig[i];
-                        out[gst[d] + (i - lof[d])] = stage[i];
+                if (staged && threadIdx.x < (1u << D)) {
+                    // digit d's run leaves by one TMA bulk copy (its aligned body) and at most
+                    // two single stores (an odd head / tail element)
+                    const uint32_t d = threadIdx.x, c = lc[d], s0 = lof[d];
+                    const uint64_t g = gst[d];
+                    if (c) {
+                        uint32_t i = 0;
+                        if (s0 & 1u) {
+                            out[g] = stage[s0];
+                            i = 1;
+                        }
+                        const uint32_t m = (c - i) & ~1u;
+                        if (m) {
+                            tma_store_1d(out + g + i, stage + s0 + i, m * (uint32_t)sizeof(K));
+                            bulk_commit();
+                            bulk_pending = true;
+                        }
+                        if (i + m < c) out[g + i + m] = stage[s0 + i + m];
                     }
-                    __syncthreads();
                 }
             } else {
                 if (threadIdx.x < (1u << D)) {
@@ -754,6 +776,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
     }
     if (!SCATTER && !pm)
         for (int d = threadIdx.x; d < (1 << lb.D); d += SP_NT) table[tab + (uint64_t)d * lb.nseg] = h[d];
+    if (SCATTER && bulk_pending) bulk_wait_all();
 }
 
 // Per-digit key counts of the large bins from the scanned segment table.
