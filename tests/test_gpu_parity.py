@@ -367,3 +367,49 @@ def test_plain_minimizer_counts_and_stats(gpu, name, scale, rules):
     sig = sig[sig != 0xFFFFFFFF]
     assert st["max_signature_windows"] == int(np.bincount(sig).max())
     assert st["n_superkmers"] == len(oracle.superkmers(w.reads, w.offsets, w.k, w.p, rules=rules))
+
+
+# --- randomized sweep: random k, p, read shapes and options against the oracle -----------
+
+def _mutated_reads(seed, n, L):
+    """Reads from a small random genome with repeats, errors and N runs (duplicated k-mers,
+    reverse complements, low complexity) -- cheap shapes the configs do not cover."""
+    rng = np.random.default_rng(seed)
+    G = rng.choice(np.frombuffer(b"ACGT", dtype=np.uint8), size=4000)
+    G[1000:1300] = ord("A")                                     # poly-A tract
+    G[2000:2400] = np.tile(np.frombuffer(b"AC", dtype=np.uint8), 200)  # (AC)n
+    comp = np.zeros(256, dtype=np.uint8)
+    for a, b in zip(b"ACGT", b"TGCA"):
+        comp[a] = b
+    out = []
+    for _ in range(n):
+        ln = int(rng.integers(1, L + 1))
+        st = int(rng.integers(0, len(G) - ln))
+        r = G[st:st + ln].copy()
+        if rng.random() < 0.5:
+            r = comp[r[::-1]]
+        err = rng.random(ln) < 0.01
+        r[err] = rng.choice(np.frombuffer(b"ACGTN", dtype=np.uint8), size=int(err.sum()))
+        if rng.random() < 0.1:
+            r = np.where(rng.random(ln) < 0.3, r + 32, r).astype(np.uint8)  # lowercase stretch
+        out.append(r.tobytes())
+    return out
+
+
+@pytest.mark.parametrize("seed", list(range(40)))
+def test_random_sweep(gpu, seed):
+    rng = random.Random(seed)
+    k = rng.choice([1, 2, 5, 11, 16, 17, 21, 25, 28, 31, 33, 40, 47, 55, 63, 64])
+    p = rng.randint(1, min(k, 12))
+    ci = rng.choice([1, 1, 2, 3])
+    cx = rng.choice([10**9, 10**9, 50, 7])
+    opts = rng.choice([{}, dict(force_large=True), dict(small_bin_capacity=256), dict(force_large=True, count_path=1),
+                       dict(force_large=True, chunk_capacity=512), dict(large_path=1, force_large=True),
+                       dict(canonical=False) if k not in (32, 64) else {}, dict(plain_minimizers=True)])
+    seqs = _mutated_reads(seed, rng.randint(50, 400), rng.choice([60, 150, 400]))
+    w = synth.from_strings(seqs, k, p, ci, cx)
+    keys, counts, st = gpu_count(gpu, w, ci=ci, cx=cx, **opts)
+    ref = oracle.count(w.reads, w.offsets, k, ci, cx, canonical=opts.get("canonical", True))
+    assert keys.shape[0] == ref.keys.shape[0], (seed, k, p, opts)
+    assert np.array_equal(keys, ref.keys) and np.array_equal(counts, ref.counts), (seed, k, p, opts)
+    assert st["n_windows"] == ref.n_windows and st["n_unique"] == ref.n_unique
