@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(WS_NT) k_ord_classify(const uint32_t* __restri
                                                         uint32_t n, uint32_t cap, uint2* __restrict__ wl,
                                                         Chunk* __restrict__ big, Chunk* __restrict__ over,
                                                         unsigned long long* __restrict__ counters) {
-    __shared__ uint32_t wsum[WS_NT / 32 + 1];
+    __shared__ unsigned long long wsum64[WS_NT / 32 + 1];
     __shared__ unsigned long long base[6];
     const uint64_t d = (uint64_t)blockIdx.x * WS_NT + threadIdx.x;
     int cls = -1;  // 0/1/2/3: warp sort of 32/64/128/256 items, 4: CTA sort, 5: oversize
@@ -213,19 +213,18 @@ __global__ void __launch_bounds__(WS_NT) k_ord_classify(const uint32_t* __restri
             }
         }
     }
-    uint32_t off[6], tot[6];
-#pragma unroll
-    for (int l = 0; l < 6; ++l) off[l] = block_excl_sum<WS_NT, uint32_t>(cls == l ? 1u : 0u, wsum, &tot[l]);
+    // one block scan of the six class counters packed in 10-bit fields of a uint64
+    unsigned long long tot;
+    const unsigned long long off =
+        block_excl_sum<WS_NT, unsigned long long>(cls >= 0 ? 1ull << (10 * cls) : 0ull, wsum64, &tot);
     if (threadIdx.x < 6) {
-        uint32_t t = 0;
-#pragma unroll
-        for (int l = 0; l < 6; ++l) t = threadIdx.x == l ? tot[l] : t;
+        const uint32_t t = (uint32_t)(tot >> (10 * threadIdx.x)) & 1023u;
         base[threadIdx.x] = t ? atomicAdd(&counters[threadIdx.x], (unsigned long long)t) : 0ull;
     }
     __syncthreads();
     if (cls >= 0) {
         const Chunk ch{st, sz, 0};
-        const uint64_t q = base[cls] + off[cls];
+        const uint64_t q = base[cls] + ((off >> (10 * cls)) & 1023u);
         // warp-sort lists in 2 nbk slots: sizes <= 32 / <= 64 from both ends of the first half
         // (together at most one item per bucket), <= 128 / <= 256 from both ends of the second
         if (cls == 0) wl[q] = make_uint2(st, sz);
