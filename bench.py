@@ -294,18 +294,30 @@ def main():
     dom_ms = per_stage[dom]["ms"]
     achieved = sb.get(dom, 0.0) / (dom_ms / 1e3) / 1e9
     traffic = None
+    issue = None
     tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")  # written from an ncu capture
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         if tj.get("workload") == args.config and float(tj.get("scale", 0)) == args.scale and dom in tj["stages"]:
             e = tj["stages"][dom]
             traffic = int(e["dram_bytes_read"] + e["dram_bytes_write"])
+            if e.get("warp_inst"):
+                # the issue side of the same kernel: ncu warp instructions per launch over the
+                # live time, against 4 schedulers x SMs x the measured SM clock
+                peak_gi = 4 * torch.cuda.get_device_properties(0).multi_processor_count * \
+                    float(tj.get("sm_clock_ghz", 1.965))
+                gi = e["warp_inst"] / (dom_ms / 1e3) / 1e9
+                issue = {"warp_inst_per_launch": int(e["warp_inst"]), "achieved_ginst_s": round(gi, 1),
+                         "peak_ginst_s": round(peak_gi, 1), "frac": round(gi / peak_gi, 4),
+                         "source": "ncu smsp__inst_executed.sum (profiles/r01_traffic.json)"}
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
             "alg_bytes_per_launch": int(sb.get(dom, 0.0)), "ms_per_launch": dom_ms,
             "peak_source": peaks["source"],
             "note": "per-stage CUDA events inside kmc_count (the stage is one kernel but for a few "
                     "tiny scans); traffic = ncu DRAM bytes of the same kernel (profiles/r01_traffic.json)"}
+    if issue:
+        roof["issue"] = issue
     b_alg = n_bases + 8 * (w.n_reads + 1) + 2 * last["n_records"] * (16 if k <= 32 else 32) + \
         last["n_out"] * ((8 if k <= 32 else 16) + 4)
     roof["pipeline"] = {"B_alg": int(b_alg), "frac_of_step": round(b_alg / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
