@@ -328,6 +328,8 @@ __global__ void __launch_bounds__(WS_NT) k_ord_wsort(const uint64_t* __restrict_
 }
 
 // MSD levels: D_l <= 8 bits each, until the average bucket holds at most cap/8 survivors
+// 64-bit keys end in warp sorts of buckets of a few tens: the last level takes only the
+// bits that bring the average bucket to ~20 (fewer, fuller buckets to classify and sort).
 int order_levels(uint64_t n, int k, int cap, int* D) {
     const int twok = 2 * k;
     int L = 0, bits = 0;
@@ -335,6 +337,12 @@ int order_levels(uint64_t n, int k, int cap, int* D) {
         D[L] = std::min(8, twok - bits);
         bits += D[L++];
     } while (bits < twok && L < 4 && (n >> bits) > (uint64_t)cap / 8);
+    if (k <= 32) {
+        const uint64_t before = n >> (bits - D[L - 1]);
+        int d = 1;
+        while (d < D[L - 1] && (before >> d) > 20) ++d;
+        D[L - 1] = d;
+    }
     return L;
 }
 
