@@ -185,7 +185,6 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     kmc.load()
-    kmc.use_torch_allocator(True)
 
     gen_threads = max(1, (os.cpu_count() or 8) // max(1, world))
     # N > 1: rank r holds its own read sample of the same genome (weak scaling) and the ranks

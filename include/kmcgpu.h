@@ -33,8 +33,9 @@
  * CUDA driver which); host inputs are copied to the device inside the call,
  * host outputs are written by a device-to-host copy.  The caller owns every
  * buffer passed in; the library never frees caller memory.  Scratch comes from
- * the allocator set by kmc_set_allocator (default: cudaMallocAsync on a pool
- * that keeps its memory between calls) and is released before return.
+ * the allocator set by kmc_set_allocator (default: the library's block cache,
+ * which keeps cudaMalloc'd blocks between calls, see kmc_empty_cache) and is
+ * released to it before return.
  *
  * Streams and blocking.  All work is enqueued on `stream` (cudaStream_t passed
  * as void*, 0 = legacy default stream).  kmc_count_begin synchronizes the
@@ -151,10 +152,20 @@ typedef struct {
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).
- * Passing NULL restores the default (cudaMallocAsync / cudaFreeAsync on a retained pool). */
+ * Passing NULL restores the default: a process-wide cache of cudaMalloc'd blocks.  A block
+ * freed by a call stays cached, tagged with the call's stream, and is handed out again only
+ * to allocations on that stream and device (stream order makes the reuse safe); when
+ * cudaMalloc runs out of memory the cache is synchronised, emptied and the allocation
+ * retried once.  Not a performance detail: a C4-sized call needs ~40 GB of scratch, and
+ * mapping it anew every call costs more than the count. */
 typedef void* (*kmc_alloc_fn)(uint64_t bytes, void* stream, void* ctx);
 typedef void (*kmc_free_fn)(void* ptr, void* stream, void* ctx);
 void kmc_set_allocator(kmc_alloc_fn alloc_fn, kmc_free_fn free_fn, void* ctx);
+
+/* Returns every cached block of the default allocator to the driver (after a device
+ * synchronisation).  Call it when other code in the process needs the memory.  Safe at
+ * any time no kmc call is running; a no-op when the cache is empty. */
+void kmc_empty_cache(void);
 
 /* One-call form.  reads: n_bases bytes, read i = reads[offsets[i]-offsets[0] ..
  * offsets[i+1]-offsets[0]); read_offsets: n_reads+1 nondecreasing uint64 (offsets[0] may

@@ -95,6 +95,8 @@ def load():
         lib.kmc_version.restype = I
         lib.kmc_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, P]
         lib.kmc_set_allocator.restype = None
+        lib.kmc_empty_cache.argtypes = []
+        lib.kmc_empty_cache.restype = None
         lib.kmc_shard_pass1.argtypes = [P, P, U64, I, I, U32, U32, P, ctypes.POINTER(_Options), ctypes.POINTER(P),
                                         P, P, ctypes.POINTER(U64)]
         lib.kmc_shard_pass1.restype = I
@@ -110,6 +112,11 @@ def load():
         lib.kmc_record_words.restype = I
         _lib = lib
         return lib
+
+
+def empty_cache():
+    """Return the default allocator's cached scratch blocks to the driver (kmc_empty_cache)."""
+    load().kmc_empty_cache()
 
 
 def use_torch_allocator(enable: bool = True):

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -27,7 +28,6 @@ std::mutex g_alloc_mu;
 kmc_alloc_fn g_alloc = nullptr;
 kmc_free_fn g_free = nullptr;
 void* g_ctx = nullptr;
-std::once_flag g_pool_once;
 
 void set_err(const char* fmt, ...) {
     char buf[512];
@@ -51,21 +51,68 @@ struct Fail {
         }                                                                                              \
     } while (0)
 
-void init_pool() {
-    std::call_once(g_pool_once, [] {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return;
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+// Default scratch allocator: a process-wide cache of cudaMalloc'd device blocks.  A call
+// needs tens of GB of scratch in a few dozen blocks of nearly the same sizes every time;
+// mapping that anew per call (cudaMalloc / cudaFree, or a stream-ordered pool that gives
+// physical pages back and re-maps them) costs more than the count itself on the host-input
+// path.  Freed blocks stay cached, tagged with the stream that freed them; an allocation
+// on the same stream and device takes the smallest cached block that fits without wasting
+// more than a quarter (stream order makes the reuse safe, as in a caching allocator).  On
+// an out-of-memory cudaMalloc the cache is synchronised and returned to the driver, then
+// the allocation is retried once.
+struct CachedBlock {
+    void* p;
+    size_t size;
+    int dev;
+    cudaStream_t s;
+};
+std::mutex g_cache_mu;
+std::multimap<size_t, CachedBlock> g_cache;
+
+size_t cache_round(size_t bytes) {
+    const size_t g = bytes >= ((size_t)1 << 20) ? ((size_t)2 << 20) : (size_t)512;
+    return (bytes + g - 1) / g * g;
+}
+void cache_flush_locked() {
+    if (g_cache.empty()) return;
+    cudaDeviceSynchronize();
+    for (auto& e : g_cache) cudaFree(e.second.p);
+    g_cache.clear();
+    cudaGetLastError();
+}
+void* cache_alloc(size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    for (auto it = g_cache.lower_bound(bytes); it != g_cache.end() && it->first <= bytes + bytes / 4; ++it) {
+        if (it->second.dev == dev && it->second.s == s) {
+            void* p = it->second.p;
+            g_cache.erase(it);
+            return p;
         }
-    });
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        cache_flush_locked();
+        p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+    }
+    return p;
+}
+void cache_free(void* p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    g_cache.insert({bytes, CachedBlock{p, bytes, dev, s}});
 }
 
 struct Arena {
     cudaStream_t s = 0;
-    std::vector<void*> ptrs;
+    std::vector<std::pair<void*, size_t>> ptrs;
     kmc_alloc_fn af = nullptr;
     kmc_free_fn ff = nullptr;
     void* ctx = nullptr;
@@ -75,53 +122,41 @@ struct Arena {
         af = g_alloc;
         ff = g_free;
         ctx = g_ctx;
-        if (!af) init_pool();
     }
-    void* alloc(size_t bytes) {
-        if (bytes == 0) bytes = 16;
-        bytes = (bytes + 255) & ~(size_t)255;
-        void* p = nullptr;
-        if (af) {
-            p = af(bytes, (void*)s, ctx);
-        } else {
-            if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) p = nullptr;
-        }
-        if (!p) {
-            cudaGetLastError();
-            set_err("scratch allocation of %zu bytes failed", bytes);
-            throw Fail{KMC_ERR_ALLOC};
-        }
-        ptrs.push_back(p);
-        return p;
-    }
-    template <class T> T* get(size_t n) { return reinterpret_cast<T*>(alloc(n * sizeof(T))); }
     // nullptr instead of an error when the allocator is out of memory
     void* try_alloc(size_t bytes) {
-        bytes = (bytes + 255) & ~(size_t)255;
-        if (bytes == 0) bytes = 256;
-        void* p = nullptr;
-        if (af) p = af(bytes, (void*)s, ctx);
-        else if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) p = nullptr;
+        bytes = cache_round(bytes == 0 ? 16 : bytes);
+        void* p = af ? af(bytes, (void*)s, ctx) : cache_alloc(bytes, s);
         if (!p) {
             cudaGetLastError();
             return nullptr;
         }
-        ptrs.push_back(p);
+        ptrs.push_back({p, bytes});
         return p;
+    }
+    void* alloc(size_t bytes) {
+        void* p = try_alloc(bytes);
+        if (!p) {
+            set_err("scratch allocation of %zu bytes failed", bytes);
+            throw Fail{KMC_ERR_ALLOC};
+        }
+        return p;
+    }
+    template <class T> T* get(size_t n) { return reinterpret_cast<T*>(alloc(n * sizeof(T))); }
+    void give_back(void* p, size_t bytes) {
+        if (ff) ff(p, (void*)s, ctx);
+        else cache_free(p, bytes, s);
     }
     void release(void* p) {
         if (!p) return;
-        auto it = std::find(ptrs.begin(), ptrs.end(), p);
+        auto it = std::find_if(ptrs.begin(), ptrs.end(), [p](const std::pair<void*, size_t>& e) { return e.first == p; });
         if (it == ptrs.end()) return;
+        const size_t b = it->second;
         ptrs.erase(it);
-        if (ff) ff(p, (void*)s, ctx);
-        else cudaFreeAsync(p, s);
+        give_back(p, b);
     }
     void release_all() {
-        for (void* p : ptrs) {
-            if (ff) ff(p, (void*)s, ctx);
-            else cudaFreeAsync(p, s);
-        }
+        for (auto& e : ptrs) give_back(e.first, e.second);
         ptrs.clear();
     }
 };
@@ -1095,6 +1130,11 @@ void kmc_set_allocator(kmc_alloc_fn alloc_fn, kmc_free_fn free_fn, void* ctx) {
         g_free = nullptr;
         g_ctx = nullptr;
     }
+}
+
+void kmc_empty_cache(void) {
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    cache_flush_locked();
 }
 
 const char* kmc_last_error(void) { return g_err.c_str(); }
