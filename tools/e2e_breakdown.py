@@ -52,11 +52,11 @@ def timed(tag, n=2, **kw):
         del r
 
 
-timed("native pool, legacy stream")
+timed("default block cache, legacy stream")
 st = torch.cuda.Stream()
-timed("native pool, own stream", stream=st)
+timed("default block cache, own stream", stream=st)
 kmc.use_torch_allocator(True)
 timed("torch allocator, legacy stream")
 timed("torch allocator, own stream", stream=st)
 kmc.use_torch_allocator(False)
-timed("native pool again, legacy stream")
+timed("default block cache again, legacy stream")
