@@ -116,6 +116,8 @@ typedef struct {
                                   (counted by the device radix-sort fallback instead) */
     uint64_t n_order_oversize; /* survivors in S9 buckets above one chunk (sorted by the device LSD) */
     uint64_t max_signature_windows; /* windows of the most frequent signature (Table 6) */
+    uint64_t n_small_sorted;   /* small bins whose distinct keys overfilled the SMEM hash table
+                                  (sorted + run-length compacted in SMEM instead) */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;

@@ -35,7 +35,7 @@ class _Stats(ctypes.Structure):
         "n_reads", "n_bases", "n_invalid_bases", "n_windows", "n_superkmers", "n_records",
         "n_signatures_used", "n_bins", "n_large_bins", "max_bin_windows", "large_windows", "n_unique",
         "n_below_min", "n_above_max", "n_out", "n_launches", "n_input_batches", "n_large_groups",
-        "chunk_capacity", "n_overflow_chunks", "n_order_oversize", "max_signature_windows")] + [
+        "chunk_capacity", "n_overflow_chunks", "n_order_oversize", "max_signature_windows", "n_small_sorted")] + [
         ("stage_ms", ctypes.c_float * len(STAGES)), ("stage_launches", ctypes.c_uint32 * len(STAGES))]
 
     def to_dict(self) -> dict:

@@ -90,6 +90,33 @@ __device__ __forceinline__ void block_rle_emit(const K* S, int n, uint32_t* cnt,
     }
 }
 
+constexpr int PROBE_MAX = 256;
+
+// Counts key; false if no slot was found within PROBE_MAX probes (table too full).
+template <class K>
+__device__ __forceinline__ bool table_insert_bounded(K* T, uint32_t* C, int lg, const K& key) {
+    const uint32_t mask = (1u << lg) - 1;
+    const K E = key_empty<K>();
+    uint32_t s = slot_hash(key, lg);
+    for (int pr = 0; pr < PROBE_MAX; ++pr) {
+        // one shared CAS per probe: it claims an empty slot, or returns the key that holds it
+        const K old = smem_cas_empty(&T[s], key);
+        if (key_eq(old, E) || key_eq(old, key)) {
+            atomicAdd(&C[s], 1u);
+            return true;
+        }
+        s = (s + 1) & mask;
+    }
+    return false;
+}
+
+// Small-bin table: the B region (CAP keys) once the records are expanded, as 2^lg key slots +
+// 2^lg uint32 counters.
+template <class K> struct SmallSlots;
+template <> struct SmallSlots<uint64_t> { static constexpr int lg = 12; };  // 4096 x 12 B = 48 KB
+template <> struct SmallSlots<K128> { static constexpr int lg = 11; };      // 2048 x 20 B = 40 KB
+static_assert((1 << 12) * 12 <= SB_CAP64 * 8 && (1 << 11) * 20 <= SB_CAP128 * 16, "table fits the B region");
+
 template <class K>
 __global__ void __launch_bounds__(SB_NT, 2) k_small_bins(SmallArgs a) {
     constexpr int CAP = SmallCap<K>::v;
@@ -133,6 +160,67 @@ __global__ void __launch_bounds__(SB_NT, 2) k_small_bins(SmallArgs a) {
         }
     }
     __syncthreads();
+    // ---- S7-S8 by counting: the bin's keys into a hash table in the B region (one shared
+    // CAS per probe claims a slot or finds the key, atomicAdd counts), then one scan of the
+    // table emits the survivors (S9 orders them).  Same counts as sorting + run-length
+    // compaction; a bin whose distinct keys overfill the table (a probe sequence longer
+    // than PROBE_MAX) is sorted instead.
+    {
+        constexpr int LGMAX = SmallSlots<K>::lg;
+        int lg = 6;
+        while (lg < LGMAX && (1 << lg) < n + n / 3) ++lg;
+        const int TS = 1 << lg;
+        K* T = reinterpret_cast<K*>(B);
+        uint32_t* C = reinterpret_cast<uint32_t*>(T + (1 << LGMAX));
+        const K E = key_empty<K>();
+        for (int i = threadIdx.x; i < TS; i += SB_NT) {
+            T[i] = E;
+            C[i] = 0;
+        }
+        if (threadIdx.x == 0) *scnt = 0;
+        __syncthreads();
+        bool ok = true;
+        for (int i = threadIdx.x; i < n; i += SB_NT) ok &= table_insert_bounded<K>(T, C, lg, A[i]);
+        if (!ok) *scnt = 1;
+        __syncthreads();
+        if (*scnt != 0 && threadIdx.x == 0) atomicAdd(&a.gstats[GS_SMALL_SORTED], 1ull);
+        if (*scnt == 0) {
+            uint32_t uniq = 0, below = 0, above = 0, keep = 0;
+            for (int i = threadIdx.x; i < TS; i += SB_NT) {
+                const uint32_t c = C[i];
+                if (c) {
+                    ++uniq;
+                    if (c < a.ci) ++below;
+                    else if (c > a.cx) ++above;
+                    else ++keep;
+                }
+            }
+            uint32_t total;
+            const uint32_t ex = block_excl_sum<SB_NT, uint32_t>(keep, wsum, &total);
+            const uint32_t tu = block_sum<SB_NT, uint32_t>(uniq, wsum);
+            const uint32_t tb = block_sum<SB_NT, uint32_t>(below, wsum);
+            const uint32_t ta = block_sum<SB_NT, uint32_t>(above, wsum);
+            if (threadIdx.x == 0) {
+                *bcast = total ? atomicAdd(&a.gstats[GS_SURV], (unsigned long long)total) : 0ull;
+                if (tu) atomicAdd(&a.gstats[GS_UNIQUE], (unsigned long long)tu);
+                if (tb) atomicAdd(&a.gstats[GS_BELOW], (unsigned long long)tb);
+                if (ta) atomicAdd(&a.gstats[GS_ABOVE], (unsigned long long)ta);
+            }
+            __syncthreads();
+            uint64_t o = *bcast + ex;
+            K* ok_keys = reinterpret_cast<K*>(a.surv_keys);
+            for (int i = threadIdx.x; i < TS; i += SB_NT) {
+                const uint32_t c = C[i];
+                if (c >= a.ci && c <= a.cx && c != 0) {
+                    ok_keys[o] = T[i];
+                    a.surv_counts[o] = c;
+                    ++o;
+                }
+            }
+            return;
+        }
+        __syncthreads();
+    }
     // ---- S7: LSD radix sort in shared memory (in place)
     block_sort_inplace<K, SB_NT, CAP / SB_NT, false>(A, nullptr, n, 2 * k, whist, wsum, red);
     // ---- S8: run-length compaction + cutoffs
@@ -839,30 +927,11 @@ __global__ void __launch_bounds__(SB_NT, 2) k_chunk_sort(const K* __restrict__ k
 // sequence longer than PROBE_MAX marks the chunk "overflowed" -- its partial counts are
 // dropped and the chunk is listed for the device radix-sort fallback.
 constexpr int CH_NT = 1024;
-constexpr int PROBE_MAX = 256;
 template <class K> struct HashCfg;
 template <> struct HashCfg<uint64_t> { static constexpr int slots = 16384; };
 template <> struct HashCfg<K128> { static constexpr int slots = 8192; };
 
 template <class K> constexpr size_t chunk_hash_smem() { return (size_t)HashCfg<K>::slots * (sizeof(K) + 4); }
-
-// Counts key; false if no slot was found within PROBE_MAX probes (table too full).
-template <class K>
-__device__ __forceinline__ bool table_insert_bounded(K* T, uint32_t* C, int lg, const K& key) {
-    const uint32_t mask = (1u << lg) - 1;
-    const K E = key_empty<K>();
-    uint32_t s = slot_hash(key, lg);
-    for (int pr = 0; pr < PROBE_MAX; ++pr) {
-        // one shared CAS per probe: it claims an empty slot, or returns the key that holds it
-        const K old = smem_cas_empty(&T[s], key);
-        if (key_eq(old, E) || key_eq(old, key)) {
-            atomicAdd(&C[s], 1u);
-            return true;
-        }
-        s = (s + 1) & mask;
-    }
-    return false;
-}
 
 template <class K>
 __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ keys, const Chunk* __restrict__ chunks,

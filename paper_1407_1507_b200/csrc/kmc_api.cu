@@ -1025,6 +1025,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
     j->st.n_unique = hs[16 + GS_UNIQUE];
     j->st.n_below_min = hs[16 + GS_BELOW];
     j->st.n_above_max = hs[16 + GS_ABOVE];
+    j->st.n_small_sorted = hs[16 + GS_SMALL_SORTED];
     if (j->opt.large_path == 1 && hs[16 + GS_LARGE_KEYS] != large_windows) {
         set_err("large-bin expansion produced %llu keys, plan says %llu", (unsigned long long)hs[16 + GS_LARGE_KEYS],
                 (unsigned long long)large_windows);

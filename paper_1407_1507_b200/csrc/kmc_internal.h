@@ -21,6 +21,7 @@ enum {
     GS_SIGS_USED = 9,
     GS_TMP_RECS = 10,   // slots reserved in the temporary record stream by pass 1
     GS_MAX_SIG = 11,    // windows of the most frequent signature
+    GS_SMALL_SORTED = 12,  // small bins whose hash table overflowed (sorted instead)
     GS_N = 16
 };
 

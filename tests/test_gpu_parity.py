@@ -151,6 +151,20 @@ def test_chunk_hash_overflow_fallback(gpu):
     assert st["n_overflow_chunks"] == 0
 
 
+def test_small_bin_hash_and_sort_fallback(gpu):
+    # small bins are counted in a shared-memory hash table; bins whose distinct keys overfill
+    # it (random reads: nearly every k-mer distinct, bins near the small capacity) are
+    # sorted instead.  Both in one call, both exact.
+    seqs = synth.random_reads(91, 20000, 80, 120, alphabet=b"ACGT")
+    for k, p in [(25, 5), (25, 6), (40, 5)]:
+        w = synth.from_strings(seqs, k, p, 1)
+        st = assert_same(gpu, w)
+        assert st["n_small_sorted"] > 0 and st["n_small_sorted"] < st["n_bins"], st
+    # repeats: every small bin by the table
+    st = assert_same(gpu, synth.make("C2", scale=0.01))
+    assert st["n_small_sorted"] == 0 and st["n_bins"] > st["n_large_bins"]
+
+
 @pytest.mark.parametrize("count_path", [0, 1])
 @pytest.mark.parametrize("name,scale", [("C3", 0.005), ("C2", 0.005), ("C1", 0.2)])
 def test_chunk_count_paths(gpu, name, scale, count_path):
