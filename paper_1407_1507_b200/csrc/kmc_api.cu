@@ -740,6 +740,29 @@ void count_phase(kmc_job* j, PlanCtx& c) {
     j->surv_counts = ar.get<uint32_t>(surv_cap);
 
     // ---- S6-S8 small bins
+    // The hash path sizes its chunks by the distinct/window ratio of the small bins.  With
+    // enough small windows, every 8th small bin runs first as the sample; its distinct-key
+    // count is read back while the other small bins run, so the host's large-bin setup
+    // overlaps them instead of waiting for all small bins.
+    uint64_t small_w = 0, sample_w = 0;
+    for (uint32_t b : small) small_w += bw[b];
+    size_t n_first = small.size();
+    cudaEvent_t ev_sample = nullptr;
+    struct EvGuard {
+        cudaEvent_t& e;
+        ~EvGuard() {
+            if (e) cudaEventDestroy(e);
+        }
+    } ev_sample_guard{ev_sample};
+    const bool hash_path = large_windows > 0 && j->opt.large_path != 1 && j->opt.count_path != 1;
+    if (hash_path && small_w >= (8u << 20)) {
+        std::vector<uint32_t> first, rest;
+        for (size_t i = 0; i < small.size(); ++i) (i % 8 == 0 ? first : rest).push_back(small[i]);
+        for (uint32_t b : first) sample_w += bw[b];
+        n_first = first.size();
+        small = first;
+        small.insert(small.end(), rest.begin(), rest.end());
+    }
     if (!small.empty()) {
         uint32_t* d_small = ar.get<uint32_t>(small.size());
         CK(cudaMemcpyAsync(d_small, small.data(), small.size() * 4, cudaMemcpyHostToDevice, s));
@@ -757,9 +780,18 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         sa.surv_counts = j->surv_counts;
         sa.gstats = gstats;
         j->stage_begin(KMC_STAGE_SMALL_BINS);
-        CK(launch_small_bins(sa, small.size(), s));
-        j->launches += 1;
-        j->stage_end(1);
+        CK(launch_small_bins(sa, n_first, s));
+        int sl = 1;
+        if (n_first < small.size()) {
+            CK(cudaMemcpyAsync(&hs[64], gstats + GS_UNIQUE, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaEventCreateWithFlags(&ev_sample, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev_sample, s));
+            sa.small_list = d_small + n_first;
+            CK(launch_small_bins(sa, small.size() - n_first, s));
+            ++sl;
+        }
+        j->launches += sl;
+        j->stage_end(sl);
     }
     // ---- S6-S8 large bins
     if (large_windows > 0 && j->opt.large_path == 1) {
@@ -816,8 +848,10 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         if (j->opt.count_path != 1) {
             const uint64_t safe = (uint64_t)chunk_hash_cap(k) * 3 / 4;
             double r = 1.0;
-            const uint64_t small_w = n_windows - large_windows;
-            if (small_w >= (1u << 20)) {
+            if (ev_sample) {  // distinct keys of the sampled small bins (the rest still run)
+                CK(cudaEventSynchronize(ev_sample));
+                r = std::min(1.0, std::max(0.05, 1.5 * (double)hs[64] / (double)sample_w));
+            } else if (small_w >= (1u << 20)) {
                 CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
                 r = std::min(1.0, std::max(0.05, 1.5 * (double)hs[16 + GS_UNIQUE] / (double)small_w));
