@@ -55,19 +55,26 @@ static_assert(NROW == 18, "the block minimum uses 32 lanes x 18 positions");
 // Per 4 bytes: c = byte & 0xDF (case fold); code = ((c >> 1) ^ (c >> 2)) & 3 is 0/1/2/3 for
 // A/C/G/T; the byte is valid iff it equals the letter of its own code, looked up with one
 // byte permute; the 4 codes are packed by one multiply (byte i lands at bits 6-2i).
+// One 4-byte word: the packed 8 bits (first base in the top 2) and the invalid nibble.
+__device__ __forceinline__ void encode4(uint32_t w, uint32_t& packed8, uint32_t& inv4) {
+    const uint32_t c = w & 0xDFDFDFDFu;
+    const uint32_t cd = ((c >> 1) ^ (c >> 2)) & 0x03030303u;         // per byte: A0 C1 G2 T3
+    const uint32_t sx = (cd | (cd >> 4)) & 0x00FF00FFu;                // codes as nibbles 0,1 | 2,3
+    const uint32_t sel = (sx | (sx >> 8)) & 0xFFFFu;
+    const uint32_t diff = __byte_perm(0x54474341u, 0u, sel) ^ c;        // 0 where the byte is its letter
+    const uint32_t bad = (((diff & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | diff) & 0x80808080u;  // bit 7: byte != 0
+    packed8 = (cd * 0x40100401u) >> 24;
+    inv4 = ((bad >> 7) * 0x01020408u) >> 24 & 0xFu;
+}
 __device__ __forceinline__ void encode16(const uint32_t (&wd)[4], uint32_t& packed, uint32_t& invbits) {
     packed = 0;
     invbits = 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-        const uint32_t c = wd[t] & 0xDFDFDFDFu;
-        const uint32_t cd = ((c >> 1) ^ (c >> 2)) & 0x03030303u;         // per byte: A0 C1 G2 T3
-        const uint32_t sx = (cd | (cd >> 4)) & 0x00FF00FFu;                // codes as nibbles 0,1 | 2,3
-        const uint32_t sel = (sx | (sx >> 8)) & 0xFFFFu;
-        const uint32_t diff = __byte_perm(0x54474341u, 0u, sel) ^ c;        // 0 where the byte is its letter
-        const uint32_t bad = (((diff & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | diff) & 0x80808080u;  // bit 7: byte != 0
-        packed |= ((cd * 0x40100401u) >> 24) << (24 - 8 * t);
-        invbits |= (((bad >> 7) * 0x01020408u) >> 24 & 0xFu) << (4 * t);
+        uint32_t p8, i4;
+        encode4(wd[t], p8, i4);
+        packed |= p8 << (24 - 8 * t);
+        invbits |= i4 << (4 * t);
     }
 }
 
@@ -134,7 +141,8 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
         const int64_t lbase = seg0 - HL;  // stream position of local base 0
         const uint64_t r_first = a.tile_r_lo[sg];
         // ---- A: load + encode
-        for (int t = lane; t < NBASE / 16; t += 32) {
+        {  // chunks 0..31: one 16-byte chunk per lane
+            const int t = lane;
             const int64_t q = lbase + 16 * t;
             uint32_t wd[4];
             if (a.reads_aligned16 && q >= 0 && q + 16 <= nb) {
@@ -160,10 +168,43 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             encode16(wd, packed, invbits);
             S.pk[t] = packed;
             reinterpret_cast<uint16_t*>(S.inv)[t] = (uint16_t)invbits;
-            if (t >= 1 && t <= SEG / 16) {  // the segment's own bases: local [HL, HL + SEG)
+            if (t >= 1) {  // the segment's own bases: local [HL, HL + SEG) = chunks 1 .. SEG/16
                 uint32_t m = invbits;
                 if (q + 16 > nb) m &= (q >= nb) ? 0u : ((1u << (uint32_t)(nb - q)) - 1u);
                 l_inv += __popc(m);
+            }
+        }
+        {  // the tail chunks 32 .. NBASE/16 - 1: one 4-byte word per lane
+            static_assert(SEG / 16 == 32 && NBASE / 16 - 32 <= 8, "tail chunks fit one word per lane");
+            constexpr int NTW = 4 * (NBASE / 16 - 32);
+            const int t = 32 + (lane >> 2), u = lane & 3;
+            const int64_t q = lbase + 16 * t + 4 * u;
+            uint32_t x = 0;
+            if (lane < NTW) {
+                if (a.reads_aligned16 && q >= 0 && q + 4 <= nb) {
+                    x = __ldcs(reinterpret_cast<const unsigned int*>(a.reads + q));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int64_t qq = q + j;
+                        const uint32_t b = (qq >= 0 && qq < nb) ? a.reads[qq] : (uint32_t)'N';
+                        x |= b << (8 * j);
+                    }
+                }
+            }
+            uint32_t p8, i4;
+            encode4(x, p8, i4);
+            uint32_t iv = lane < NTW ? i4 << (4 * u) : 0u;
+            iv |= __shfl_xor_sync(0xffffffffu, iv, 1);
+            iv |= __shfl_xor_sync(0xffffffffu, iv, 2);
+            if (lane < NTW) {
+                reinterpret_cast<uint8_t*>(S.pk)[4 * t + 3 - u] = (uint8_t)p8;
+                if (u == 0) reinterpret_cast<uint16_t*>(S.inv)[t] = (uint16_t)iv;
+                if (t == SEG / 16) {  // the last chunk of the segment's own bases
+                    uint32_t m = i4;
+                    if (q + 4 > nb) m &= (q >= nb) ? 0u : ((1u << (uint32_t)(nb - q)) - 1u);
+                    l_inv += __popc(m);
+                }
             }
         }
         if (lane < NPK - NBASE / 16) S.pk[NBASE / 16 + lane] = 0;
