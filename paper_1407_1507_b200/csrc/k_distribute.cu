@@ -572,11 +572,13 @@ __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restric
     __syncthreads();
     {
         const uint32_t c = threadIdx.x < (unsigned)nd ? lh[threadIdx.x] : 0u;
+        // the run reservation is issued first; its round trip overlaps the block scan
+        const unsigned long long g =
+            c ? atomicAdd(&cursor[((uint64_t)t.bucket << D) + threadIdx.x], (unsigned long long)c) : 0ull;
         uint32_t tot;
         const uint32_t ex = block_excl_sum<RS_NT, uint32_t>(c, wsum, &tot);
         if (threadIdx.x < (unsigned)nd) {
-            gb[threadIdx.x] =
-                c ? atomicAdd(&cursor[((uint64_t)t.bucket << D) + threadIdx.x], (unsigned long long)c) : 0ull;
+            gb[threadIdx.x] = g;
             lh[threadIdx.x] = ex;
         }
         if (threadIdx.x == 0) s_tot = tot;
