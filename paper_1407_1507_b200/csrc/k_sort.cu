@@ -732,7 +732,6 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                     }
                     c = g1 - g0;
                     gst[threadIdx.x] = g0;
-                    lc[threadIdx.x] = 0;
                 }
                 // stage layout: one spare slot per digit so that every digit's run starts at
                 // the parity of its global position (16-byte aligned bulk copies out)
@@ -743,13 +742,13 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                         const uint32_t inc = warp_incl_sum(cp);
                         P = inc - cp;
                         if (lane == 31) s_npk = inc;
-                        if (mine) lof[lane] = P + ((P ^ gst[lane]) & 1u);
+                        if (mine) lof[lane] = lc[lane] = P + ((P ^ gst[lane]) & 1u);
                     }
                     __syncthreads();
                     npk = s_npk;
                 } else {
                     P = block_excl_sum<SP_NT, uint32_t>(cp, wsum, &npk);
-                    if (mine) lof[threadIdx.x] = P + ((P ^ gst[threadIdx.x]) & 1u);
+                    if (mine) lof[threadIdx.x] = lc[threadIdx.x] = P + ((P ^ gst[threadIdx.x]) & 1u);
                     __syncthreads();
                 }
                 staged = npk <= (uint32_t)SP_STAGE;  // npk: keys + one spare slot per digit
@@ -818,11 +817,11 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                             } else if (!SCATTER) {
                                 atomicAdd(&hp[dg], 1u);
                             } else {
-                                const uint32_t rk = atomicAdd(&lc[dg], 1u);
+                                const uint32_t q = atomicAdd(&lc[dg], 1u);  // stage slot (lc starts at lof)
                                 if (staged) {
-                                    stage[lof[dg] + rk] = (K)key;
+                                    stage[q] = (K)key;
                                 } else {
-                                    out[gst[dg] + rk] = (K)key;
+                                    out[gst[dg] + (q - lof[dg])] = (K)key;
                                 }
                             }
                         }
@@ -857,11 +856,11 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                             } else if (!SCATTER) {
                                 atomicAdd(&hp[dg], 1u);
                             } else {
-                                const uint32_t rk = atomicAdd(&lc[dg], 1u);
+                                const uint32_t q = atomicAdd(&lc[dg], 1u);  // stage slot (lc starts at lof)
                                 if (staged) {
-                                    stage[lof[dg] + rk] = (K)key;
+                                    stage[q] = (K)key;
                                 } else {
-                                    out[gst[dg] + rk] = (K)key;
+                                    out[gst[dg] + (q - lof[dg])] = (K)key;
                                 }
                             }
                         }
@@ -893,7 +892,7 @@ __global__ void __launch_bounds__(SP_NT) k_split(const uint32_t* __restrict__ bi
                 if (staged && threadIdx.x < (1u << D)) {
                     // digit d's run leaves by one TMA bulk copy (its aligned body) and at most
                     // two single stores (an odd head / tail element)
-                    const uint32_t d = threadIdx.x, c = lc[d], s0 = lof[d];
+                    const uint32_t d = threadIdx.x, s0 = lof[d], c = lc[d] - s0;
                     const uint64_t g = gst[d];
                     if (c) {
                         uint32_t i = 0;
