@@ -1004,8 +1004,6 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
     extern __shared__ __align__(128) uint8_t smem[];
     K* T = reinterpret_cast<K*>(smem);
     uint32_t* C = reinterpret_cast<uint32_t*>(T + TSMAX);
-    __shared__ uint32_t wk[NW];
-    __shared__ unsigned long long wb[NW];
     __shared__ int ovf;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ltm = lanemask_lt();
@@ -1079,19 +1077,12 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
                 else ++keep;
             }
         }
+        // every warp reserves the output range of the survivors it counted (it writes the same
+        // slots below): no barrier, and the atomic's round trip overlaps the other warps' work
         keep = __reduce_add_sync(0xffffffffu, keep);
-        if (lane == 0) wk[warp] = keep;
-        __syncthreads();
-        if (warp == 0) {
-            const uint32_t kw = lane < NW ? wk[lane] : 0u;
-            const uint32_t inc = warp_incl_sum(kw);
-            unsigned long long b0 = 0;
-            if (lane == NW - 1 && inc) b0 = atomicAdd(&gstats[GS_SURV], (unsigned long long)inc);
-            b0 = __shfl_sync(0xffffffffu, b0, NW - 1);
-            if (lane < NW) wb[lane] = b0 + inc - kw;
-        }
-        __syncthreads();
-        unsigned long long o = wb[warp];
+        unsigned long long o = 0;
+        if (lane == 0 && keep) o = atomicAdd(&gstats[GS_SURV], (unsigned long long)keep);
+        o = __shfl_sync(0xffffffffu, o, 0);
         for (int s = t; s < TS; s += CH_NT) {  // TS is a multiple of 64: whole warps iterate
             const uint32_t c = C[s];
             const bool kp = c >= ci && c <= cx && c != 0;
