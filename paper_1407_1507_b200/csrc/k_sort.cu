@@ -195,19 +195,21 @@ __global__ void __launch_bounds__(SB_NT, 2) k_small_bins(SmallArgs a) {
                     else ++keep;
                 }
             }
-            uint32_t total;
-            const uint32_t ex = block_excl_sum<SB_NT, uint32_t>(keep, wsum, &total);
-            const uint32_t tu = block_sum<SB_NT, uint32_t>(uniq, wsum);
-            const uint32_t tb = block_sum<SB_NT, uint32_t>(below, wsum);
-            const uint32_t ta = block_sum<SB_NT, uint32_t>(above, wsum);
-            if (threadIdx.x == 0) {
-                *bcast = total ? atomicAdd(&a.gstats[GS_SURV], (unsigned long long)total) : 0ull;
+            // per-warp reservations and statistics (the warp writes the slots it counted): no
+            // block reductions, no barriers
+            const uint32_t kin = warp_incl_sum(keep);
+            const uint32_t ktot = __shfl_sync(0xffffffffu, kin, 31);
+            const uint32_t tu = __reduce_add_sync(0xffffffffu, uniq);
+            const uint32_t tb = __reduce_add_sync(0xffffffffu, below);
+            const uint32_t ta = __reduce_add_sync(0xffffffffu, above);
+            unsigned long long base = 0;
+            if ((threadIdx.x & 31) == 0) {
+                if (ktot) base = atomicAdd(&a.gstats[GS_SURV], (unsigned long long)ktot);
                 if (tu) atomicAdd(&a.gstats[GS_UNIQUE], (unsigned long long)tu);
                 if (tb) atomicAdd(&a.gstats[GS_BELOW], (unsigned long long)tb);
                 if (ta) atomicAdd(&a.gstats[GS_ABOVE], (unsigned long long)ta);
             }
-            __syncthreads();
-            uint64_t o = *bcast + ex;
+            uint64_t o = __shfl_sync(0xffffffffu, base, 0) + kin - keep;
             K* ok_keys = reinterpret_cast<K*>(a.surv_keys);
             for (int i = threadIdx.x; i < TS; i += SB_NT) {
                 const uint32_t c = C[i];
