@@ -39,31 +39,56 @@ METRIC = "input bases/s (k-mers counted/s and HBM-roofline fraction alongside)"
 # computed from the per-call statistics.
 
 
+def compact_bin_bytes(st: dict, k: int) -> float:
+    """Bytes of the bins in SURVEY 8(d)'s model: every super-k-mer stored once as a 1-byte
+    length header + its n + k - 1 symbols at 2 bits (n windows).  From the call's statistics:
+    sum(n + k - 1) = n_windows + n_superkmers * (k - 1)."""
+    return st["n_superkmers"] * 1.0 + 2.0 * (st["n_windows"] + st["n_superkmers"] * (k - 1)) / 8.0
+
+
 def stage_bytes(st: dict, n_reads: int, k: int) -> dict:
-    """Algorithmic HBM bytes per stage and call: what the step must read and
-    write, not what the kernels happen to move."""
+    """Algorithmic HBM bytes per stage and call, SURVEY 8(d):
+    B_alg = input (ASCII + offsets) + 2 x compact bins (written once, read once) + output.
+    Each byte of B_alg is charged to the stage that must move it: pass 1 reads the input and
+    writes the bins, the counting stages read them, S9 writes the output.  Passes the model
+    does not have (S5's re-sort, the large-bin key split and its re-read) get 0: their traffic
+    is implementation overhead, reported as B_impl (ncu), never as algorithmic."""
     ksz = 8 if k <= 32 else 16
-    rw = 16 if k <= 32 else 32
     nb = st["n_bases"]
     off = 8 * (n_reads + 1)
-    rec = st["n_records"] * rw
-    tags = st["n_records"] * 4
+    bins = compact_bin_bytes(st, k)
     lw = st["large_windows"]
-    nout = st["n_out"]
     lfrac = lw / st["n_windows"] if st["n_windows"] else 0.0
-    small_rec = rec * (1 - lfrac)
-    large_rec = rec - small_rec
     return {
-        "signature": nb + off + rec + tags,                  # ASCII + offsets read; records + tags written
-        "scatter": 2 * rec + tags,                           # records + tags read, records written into bins
-        "small_bins": small_rec + (1 - lfrac) * nout * (ksz + 4),  # records read, survivors written
-        "large_split": large_rec,                            # records read (digit counts)
-        "large_scatter": large_rec + lw * ksz,               # records read, keys written
-        "large_chunks": lw * ksz + lfrac * nout * (ksz + 4),  # keys read, survivors written
-        "large_fallback": 2 * lw * ksz,                      # (LSD path only) keys read + written once
-        "order": 2 * nout * (ksz + 4),                       # survivors read + written once
-        "output": 2 * nout * (ksz + 4),
+        "signature": nb + off + bins,        # input read, bins written once
+        "scatter": 0.0,                      # implementation pass (record stream -> bins)
+        "small_bins": (1 - lfrac) * bins,    # bins read once
+        "large_split": lfrac * bins,         # bins read once
+        "large_scatter": 0.0,                # implementation pass (key split)
+        "large_chunks": 0.0,                 # implementation pass (re-read of the split keys)
+        "large_fallback": 0.0,
+        "order": st["n_out"] * (ksz + 4),    # output written once
+        "output": 0.0,
     }
+
+
+def b_alg(st: dict, n_reads: int, k: int) -> float:
+    ksz = 8 if k <= 32 else 16
+    return st["n_bases"] + 8 * (n_reads + 1) + 2 * compact_bin_bytes(st, k) + st["n_out"] * (ksz + 4)
+
+
+def latest_traffic(config: str, scale: float):
+    """The newest profiles/r*_traffic.json written from ncu captures of this workload."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json"))):
+        try:
+            tj = json.load(open(path))
+        except (OSError, ValueError):
+            continue
+        if tj.get("workload") == config and float(tj.get("scale", 0)) == scale:
+            best = (path, tj)
+    return best
 
 
 class ClockSampler:
@@ -128,13 +153,15 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def run_oracle_sample(w, n_reads_sample: int):
+def run_oracle_sample(w, n_reads_sample: int, threads: int):
+    """The oracle, as it stands, on the first n_reads_sample reads: the key-range-partitioned
+    form (SURVEY 8(d) "Oracle timing") on `threads` host threads."""
     import oracle
     n = min(n_reads_sample, w.n_reads)
     offs = w.offsets[: n + 1]
     reads = w.reads[: int(offs[-1])]
     t0 = time.perf_counter()
-    r = oracle.count(reads, offs, w.k, w.cutoff_min, w.cutoff_max)
+    r = oracle.count_partitioned(reads, offs, w.k, w.cutoff_min, w.cutoff_max, threads=threads)
     dt = time.perf_counter() - t0
     return dt, int(offs[-1] - offs[0]), r.n_windows, n
 
@@ -167,7 +194,9 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-reads", type=int, default=400_000)
+    ap.add_argument("--cpu-sample-reads", type=int, default=3_000_000)
+    ap.add_argument("--no-sort-path", action="store_true",
+                    help="skip the second timing of the paper's per-chunk radix sort (count_path 1)")
     ap.add_argument("--count-path", type=int, default=0, choices=[0, 1],
                     help="S7-S8 of large-bin chunks: 0 = SMEM hash count (default), 1 = SMEM radix sort + RLE")
     args = ap.parse_args()
@@ -235,6 +264,33 @@ def main():
     clk = clocks.stop()
     ms = reduce_max(ev0.elapsed_time(ev1) / args.steps, world, "cuda")
 
+    # ---- the paper's method (per-chunk radix sort + run-length compaction, count_path 1) timed
+    #      from the same build next to the default hash counting (reading R-S7)
+    other = None
+    if world == 1 and not args.no_sort_path:
+        cp2 = 1 - args.count_path
+        for _ in range(2):
+            res = kmc.count(reads_d, offs_d, k, p, ci, cx, profile=True, count_path=cp2)
+            del res
+        torch.cuda.synchronize()
+        o_steps = max(1, min(args.steps, 3))
+        o_stage = {}
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(o_steps):
+            res = kmc.count(reads_d, offs_d, k, p, ci, cx, profile=True, count_path=cp2)
+            for s_, v in res.stats["stage_ms"].items():
+                o_stage[s_] = o_stage.get(s_, 0.0) + v
+            o_out = res.stats["n_out"]
+            del res
+        q1.record(stream)
+        torch.cuda.synchronize()
+        o_ms = q0.elapsed_time(q1) / o_steps
+        other = {"count_path": ["smem_hash", "smem_radix_sort"][cp2], "ms_per_step": round(o_ms, 3),
+                 "value": n_bases / (o_ms / 1e3), "unit": "bases/s", "n_out": o_out,
+                 "stages_ms": {s_: round(v / o_steps, 3) for s_, v in o_stage.items() if v > 0}}
+
     # ---- e2e: same call with pinned HOST buffers (H2D of inputs and D2H of outputs inside)
     e2e = None
     if not args.no_e2e:
@@ -276,7 +332,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant stage
+    # ---- roofline of the dominant stage (SURVEY 8(d) bytes)
     peaks = measured_peaks()
     sb = stage_bytes(last, w.n_reads, k)
     per_stage = {}
@@ -294,10 +350,12 @@ def main():
     achieved = sb.get(dom, 0.0) / (dom_ms / 1e3) / 1e9
     traffic = None
     issue = None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")  # written from an ncu capture
-    if os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        if tj.get("workload") == args.config and float(tj.get("scale", 0)) == args.scale and dom in tj["stages"]:
+    impl = None
+    lt = latest_traffic(args.config, args.scale)
+    if lt is not None:
+        tpath, tj = lt
+        rel = os.path.relpath(tpath, ROOT)
+        if dom in tj.get("stages", {}):
             e = tj["stages"][dom]
             traffic = int(e["dram_bytes_read"] + e["dram_bytes_write"])
             if e.get("warp_inst"):
@@ -308,25 +366,39 @@ def main():
                 gi = e["warp_inst"] / (dom_ms / 1e3) / 1e9
                 issue = {"warp_inst_per_launch": int(e["warp_inst"]), "achieved_ginst_s": round(gi, 1),
                          "peak_ginst_s": round(peak_gi, 1), "frac": round(gi / peak_gi, 4),
-                         "source": "ncu smsp__inst_executed.sum (profiles/r01_traffic.json)"}
+                         "thread_inst_per_window": round(32 * e["warp_inst"] / last["n_windows"], 1),
+                         "source": f"ncu smsp__inst_executed.sum ({rel})"}
+        if tj.get("call"):
+            impl = {"B_impl": int(tj["call"]["dram_bytes"]),
+                    "thread_inst_per_window": round(32 * tj["call"]["warp_inst"] / last["n_windows"], 1),
+                    "source": f"ncu launch list, all kernels of one call ({rel})"}
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
             "alg_bytes_per_launch": int(sb.get(dom, 0.0)), "ms_per_launch": dom_ms,
             "peak_source": peaks["source"],
-            "note": "per-stage CUDA events inside kmc_count (the stage is one kernel but for a few "
-                    "tiny scans); traffic = ncu DRAM bytes of the same kernel (profiles/r01_traffic.json)"}
+            "note": "achieved = SURVEY 8(d) algorithmic bytes of the stage (input + compact bins for "
+                    "pass 1) / its live CUDA-event time; traffic = ncu DRAM bytes of the same kernel"}
     if issue:
         roof["issue"] = issue
-    b_alg = n_bases + 8 * (w.n_reads + 1) + 2 * last["n_records"] * (16 if k <= 32 else 32) + \
-        last["n_out"] * ((8 if k <= 32 else 16) + 4)
-    roof["pipeline"] = {"B_alg": int(b_alg), "frac_of_step": round(b_alg / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
+    B_alg = b_alg(last, w.n_reads, k)
+    ksz_ = 8 if k <= 32 else 16
+    B_sort = B_alg + 2 * last["n_windows"] * ksz_
+    pipe = {"B_alg": int(B_alg), "compact_bins": int(compact_bin_bytes(last, k)),
+            "frac_of_step": round(B_alg / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
+            "B_sort": int(B_sort), "B_sort_frac_of_step": round(B_sort / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
+    if impl:
+        pipe.update({"B_impl": impl["B_impl"], "B_impl_over_B_alg": round(impl["B_impl"] / B_alg, 2),
+                     "thread_inst_per_window": impl["thread_inst_per_window"], "impl_source": impl["source"]})
+    roof["pipeline"] = pipe
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        dt, nb_s, nw_s, nr_s = run_oracle_sample(w, args.cpu_sample_reads)
-        cpu = {"value": nb_s / dt, "unit": "bases/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {nr_s} reads of {args.config} ({nb_s} bases, {nw_s} windows), single thread",
-               "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+        T = os.cpu_count() or 1
+        dt, nb_s, nw_s, nr_s = run_oracle_sample(w, args.cpu_sample_reads, T)
+        cpu = {"value": nb_s / dt, "unit": "bases/s", "cores": T, "kind": "oracle",
+               "sample": f"first {nr_s} reads of {args.config} ({nb_s} bases, {nw_s} windows), "
+                         f"key-range-partitioned oracle on {T} threads, {dt:.1f} s",
+               "kmers_per_s": nw_s / dt, "cpu_model": cpu_model()}
 
     out = {
         "metric": METRIC,
@@ -354,6 +426,7 @@ def main():
         "stages": per_stage,
         "roofline": roof,
         "cpu_baseline": cpu,
+        "other_count_path": other,
         "e2e": e2e,
         "gpu_launches": n_launches,
         "clocks": clk,
@@ -369,12 +442,13 @@ def reference_arm(args, world, rank, cfg):
     if rank != 0:
         return
     w = synth.make(args.config, scale=args.scale)
-    n_sample = 200_000
+    n_sample = 1_000_000
+    T = os.cpu_count() or 1
     for _ in range(args.warmup):
         pass  # the oracle has no warm state worth excluding; warm-up steps are not run
     t_tot, nb_tot, nw_tot = 0.0, 0, 0
     for s in range(args.steps):
-        dt, nb_s, nw_s, nr_s = run_oracle_sample(w, n_sample)
+        dt, nb_s, nw_s, nr_s = run_oracle_sample(w, n_sample, T)
         t_tot += dt
         nb_tot += nb_s
         nw_tot += nw_s
@@ -384,8 +458,9 @@ def reference_arm(args, world, rank, cfg):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64" if cfg.k <= 32 else "u128",
            "data": "synthetic", "config": {"workload": f"{args.config}: {cfg.desc}", "scale": args.scale},
            "kmers_per_s": nw_tot / t_tot,
-           "cpu_baseline": {"value": v, "unit": "bases/s", "cores": 1, "kind": "oracle",
-                            "sample": f"first {n_sample} reads of {args.config} per step, single thread",
+           "cpu_baseline": {"value": v, "unit": "bases/s", "cores": T, "kind": "oracle",
+                            "sample": f"first {n_sample} reads of {args.config} per step, key-range-partitioned "
+                                      f"oracle on {T} threads",
                             "cpu_model": cpu_model()},
            "e2e": {"value": v, "unit": "bases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))

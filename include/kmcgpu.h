@@ -142,7 +142,9 @@ typedef struct {
                                   chunks); 1: the paper's radix sort + run-length compaction of
                                   every chunk in shared memory.  Same output. */
     uint32_t chunk_capacity;   /* 0 = auto; else max keys per large-bin chunk (testing: large
-                                  values force hash-table overflows onto the fallback) */
+                                  values force hash-table overflows onto the fallback).  With
+                                  count_path 1 it is clamped to the per-chunk sort's shared-memory
+                                  capacity (6144 keys for k <= 32, 3072 above). */
     uint32_t non_canonical;    /* 1: count k-mers as they occur in the reads, not their canonical
                                   form (KMC's -b).  Signatures and binning stay canonical
                                   (a k-mer and its reverse complement share a bin either way).

@@ -60,6 +60,12 @@ def _load():
             lib.oracle_count_ex.argtypes = [_P, _P, _U64, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, _P, _P, _U64,
                                             _P, ctypes.c_int]
             lib.oracle_count_ex.restype = ctypes.c_int64
+            lib.oracle_count_par.argtypes = [_P, _P, _U64, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
+                                             ctypes.POINTER(_P), ctypes.POINTER(_P), _P, ctypes.c_int, ctypes.c_int,
+                                             _U64]
+            lib.oracle_count_par.restype = ctypes.c_int64
+            lib.oracle_free.argtypes = [_P]
+            lib.oracle_free.restype = None
             lib.oracle_n_windows.argtypes = [_P, _P, _U64, ctypes.c_int]
             lib.oracle_n_windows.restype = _U64
             lib.oracle_n_windows_par.argtypes = [_P, _P, _U64, ctypes.c_int]
@@ -110,6 +116,46 @@ def count(reads, offsets, k: int, cutoff_min: int = 1, cutoff_max: int = 10**9, 
         raise ValueError("bad k")
     keys = keys[:n, 0].copy() if w == 1 else keys[:n].copy()
     return Result(keys, counts[:n].copy(), stats)
+
+
+def count_partitioned(reads, offsets, k: int, cutoff_min: int = 1, cutoff_max: int = 10**9, canonical: bool = True,
+                      threads: int | None = None, round_keys: int = 1 << 28) -> Result:
+    """Same result as :func:`count`, computed over contiguous key ranges by ``threads`` host
+    threads (SURVEY 8(d) "Oracle timing"; kmc_oracle.cpp count_par_impl).  ``round_keys``
+    bounds the values held in memory at once."""
+    lib = _load()
+    reads, offsets = _arrays(reads, offsets)
+    n_reads = offsets.shape[0] - 1
+    T = int(threads or os.cpu_count() or 1)
+    kp, cp = _P(), _P()
+    stats = np.zeros(5, dtype=np.uint64)
+    n = lib.oracle_count_par(reads.ctypes.data, offsets.ctypes.data, n_reads, k, cutoff_min, cutoff_max,
+                             ctypes.byref(kp), ctypes.byref(cp), stats.ctypes.data, int(canonical), T,
+                             int(round_keys))
+    if n < 0:
+        raise ValueError("bad k")
+    try:
+        w = 1 if k <= 32 else 2
+        kbuf = (ctypes.c_uint64 * max(1, n * w)).from_address(kp.value)
+        cbuf = (ctypes.c_uint32 * max(1, n)).from_address(cp.value)
+        keys = np.frombuffer(kbuf, dtype=np.uint64, count=n * w).copy()
+        counts = np.frombuffer(cbuf, dtype=np.uint32, count=n).copy()
+    finally:
+        lib.oracle_free(kp)
+        lib.oracle_free(cp)
+    if w == 2:
+        keys = keys.reshape(n, 2)
+    return Result(keys, counts, stats)
+
+
+def digest(keys, counts) -> str:
+    """SHA-256 of the little-endian key words (lo, hi for k > 32) followed by the uint32
+    counts: a fingerprint of a sorted (k-mer, count) list (tests/golden/full_configs.json)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(keys, dtype="<u8").tobytes())
+    h.update(np.ascontiguousarray(counts, dtype="<u4").tobytes())
+    return h.hexdigest()
 
 
 def n_windows(reads, offsets, k: int) -> int:

@@ -29,7 +29,9 @@
  */
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 typedef unsigned __int128 u128;
@@ -121,7 +123,185 @@ static int64_t count_impl(const uint8_t* reads, const uint64_t* offsets, uint64_
     return (int64_t)n_out;
 }
 
+/* ---------------------------------------------------------------------------------------
+ * Key-range-partitioned, multi-threaded form of the same definition (SURVEY 8(d) "Oracle
+ * timing"; used for the full-size configs, where one sorted array of every window would not
+ * fit, and for the CPU baseline on all host cores).  The key space is cut into R contiguous
+ * ranges [bound[j], bound[j+1]) at quantiles of a sample of the windows' values (every
+ * SAMPLE-th valid window).  Equal keys fall into one range, so the sorted per-range
+ * histograms, concatenated in range order, are the histogram of all windows.  Ranges are
+ * processed T at a time ("rounds", bounding memory): in a round every thread scans its
+ * slice of the reads, recomputes f and r per window exactly as count_impl does, and keeps
+ * the values that fall into the round's ranges, one vector per range; then thread t owns
+ * range t of the round, concatenates the threads' vectors for it, std::sorts them and
+ * counts equal neighbours.  Nothing but the partition differs from count_impl.
+ * --------------------------------------------------------------------------------------- */
+template <typename K>
+static int64_t count_par_impl(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k,
+                              uint32_t ci, uint32_t cx, uint64_t** out_keys, uint32_t** out_counts,
+                              uint64_t* stats, int canonical, int T, uint64_t round_keys) {
+    const uint64_t SAMPLE = 61;
+    if (T < 1) T = 1;
+    if (ci == 0) ci = 1;
+    /* read slices: equal numbers of bases per thread */
+    std::vector<uint64_t> rs(T + 1, n_reads);
+    {
+        const uint64_t nb = offsets[n_reads] - offsets[0];
+        uint64_t r = 0;
+        for (int t = 0; t <= T; ++t) {
+            const uint64_t lim = offsets[0] + (nb * (uint64_t)t) / (uint64_t)T;
+            while (r < n_reads && offsets[r] < lim) ++r;
+            rs[t] = (t == T) ? n_reads : r;
+        }
+        rs[0] = 0;
+    }
+    auto for_windows = [&](int t, auto&& fn) {
+        for (uint64_t i = rs[t]; i < rs[t + 1]; ++i) {
+            const uint64_t b = offsets[i], e = offsets[i + 1];
+            if (e < b + (uint64_t)k) continue;
+            for (uint64_t s = b; s + k <= e; ++s) {
+                const uint8_t* w = reads + (s - offsets[0]);
+                if (!window_valid(w, k)) continue;
+                fn((K)(canonical ? canonical_value(w, k) : forward_value(w, k)));
+            }
+        }
+    };
+    /* 1: window count and a value sample per thread */
+    std::vector<std::vector<K>> samp(T);
+    std::vector<uint64_t> nwin(T, 0);
+    {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                uint64_t c = 0;
+                for_windows(t, [&](K v) {
+                    if (c % SAMPLE == 0) samp[t].push_back(v);
+                    ++c;
+                });
+                nwin[t] = c;
+            });
+        for (auto& x : th) x.join();
+    }
+    uint64_t n_windows = 0;
+    std::vector<K> all;
+    for (int t = 0; t < T; ++t) {
+        n_windows += nwin[t];
+        all.insert(all.end(), samp[t].begin(), samp[t].end());
+        std::vector<K>().swap(samp[t]);
+    }
+    std::sort(all.begin(), all.end());
+    /* 2: ranges -- a multiple of T, each expected to hold about round_keys / T values */
+    uint64_t R = (uint64_t)T;
+    if (round_keys == 0) round_keys = 1;
+    while (R * (round_keys / (uint64_t)T + 1) < n_windows && R < (1ull << 20)) R += (uint64_t)T;
+    std::vector<K> bound;  /* lower bounds of ranges 1..R-1 (range 0 starts at the minimum) */
+    for (uint64_t j = 1; j < R && !all.empty(); ++j) {
+        const K b = all[(size_t)((all.size() * j) / R)];
+        if (bound.empty() || bound.back() < b) bound.push_back(b);
+    }
+    std::vector<K>().swap(all);
+    const uint64_t NR = bound.size() + 1; /* distinct ranges */
+    auto range_of = [&](K v) { return (uint64_t)(std::upper_bound(bound.begin(), bound.end(), v) - bound.begin()); };
+    /* 3: rounds of T ranges */
+    uint64_t n_unique = 0, n_below = 0, n_above = 0, n_out = 0;
+    std::vector<uint64_t> ok;  /* survivors: 1 or 2 words per key, as in oracle_count */
+    std::vector<uint32_t> oc;
+    for (uint64_t r0 = 0; r0 < NR; r0 += (uint64_t)T) {
+        const uint64_t r1 = std::min<uint64_t>(NR, r0 + (uint64_t)T);
+        const int nr = (int)(r1 - r0);
+        std::vector<std::vector<std::vector<K>>> part(T, std::vector<std::vector<K>>(nr));
+        {
+            std::vector<std::thread> th;
+            for (int t = 0; t < T; ++t)
+                th.emplace_back([&, t] {
+                    for_windows(t, [&](K v) {
+                        const uint64_t j = range_of(v);
+                        if (j >= r0 && j < r1) part[t][j - r0].push_back(v);
+                    });
+                });
+            for (auto& x : th) x.join();
+        }
+        /* per range: sort + count equal neighbours (thread j - r0 owns range j) */
+        struct RangeOut {
+            std::vector<K> keys;
+            std::vector<uint32_t> counts;
+            uint64_t uniq = 0, below = 0, above = 0;
+        };
+        std::vector<RangeOut> ro(nr);
+        {
+            std::vector<std::thread> th;
+            for (int q = 0; q < nr; ++q)
+                th.emplace_back([&, q] {
+                    std::vector<K> keys;
+                    size_t tot = 0;
+                    for (int t = 0; t < T; ++t) tot += part[t][q].size();
+                    keys.reserve(tot);
+                    for (int t = 0; t < T; ++t) {
+                        keys.insert(keys.end(), part[t][q].begin(), part[t][q].end());
+                        std::vector<K>().swap(part[t][q]);
+                    }
+                    std::sort(keys.begin(), keys.end());
+                    RangeOut& o = ro[q];
+                    for (size_t a = 0; a < keys.size();) {
+                        size_t z = a;
+                        while (z < keys.size() && keys[z] == keys[a]) ++z;
+                        const uint64_t c = z - a;
+                        ++o.uniq;
+                        if (c < ci) ++o.below;
+                        else if (c > cx) ++o.above;
+                        else {
+                            o.keys.push_back(keys[a]);
+                            o.counts.push_back((uint32_t)(c > 0xFFFFFFFFull ? 0xFFFFFFFFull : c));
+                        }
+                        a = z;
+                    }
+                });
+            for (auto& x : th) x.join();
+        }
+        for (int q = 0; q < nr; ++q) {
+            RangeOut& o = ro[q];
+            n_unique += o.uniq;
+            n_below += o.below;
+            n_above += o.above;
+            for (size_t i = 0; i < o.keys.size(); ++i, ++n_out) {
+                const u128 v = (u128)o.keys[i];
+                ok.push_back((uint64_t)v);
+                if (sizeof(K) == 16) ok.push_back((uint64_t)(v >> 64));
+                oc.push_back(o.counts[i]);
+            }
+            std::vector<K>().swap(o.keys);
+            std::vector<uint32_t>().swap(o.counts);
+        }
+    }
+    /* exactly-sized outputs, released by oracle_free */
+    *out_keys = (uint64_t*)malloc(std::max<size_t>(1, ok.size()) * 8);
+    *out_counts = (uint32_t*)malloc(std::max<size_t>(1, oc.size()) * 4);
+    if (!ok.empty()) memcpy(*out_keys, ok.data(), ok.size() * 8);
+    if (!oc.empty()) memcpy(*out_counts, oc.data(), oc.size() * 4);
+    if (stats) {
+        stats[0] = n_windows; stats[1] = n_unique; stats[2] = n_below; stats[3] = n_above; stats[4] = n_out;
+    }
+    return (int64_t)n_out;
+}
+
 extern "C" {
+
+/* Key-range-partitioned, multi-threaded oracle_count (same outputs and stats; see
+ * count_par_impl).  threads: host threads (>= 1); round_keys: values held in memory per
+ * round (bounds RAM at about 2 x round_keys x key bytes).  *out_keys / *out_counts are
+ * malloc'd with exactly n_out entries (keys: 1 or 2 words each); free with oracle_free. */
+int64_t oracle_count_par(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k, uint32_t ci,
+                         uint32_t cx, uint64_t** out_keys, uint32_t** out_counts, uint64_t* stats, int canonical,
+                         int threads, uint64_t round_keys) {
+    if (k < 1 || k > 64) return -1;
+    if (k <= 32)
+        return count_par_impl<uint64_t>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, stats, canonical,
+                                        threads, round_keys);
+    return count_par_impl<u128>(reads, offsets, n_reads, k, ci, cx, out_keys, out_counts, stats, canonical,
+                                threads, round_keys);
+}
+
+void oracle_free(void* p) { free(p); }
 
 /* Exact sorted (canonical k-mer, count) list with cutoffs.
  * reads: host ASCII bytes; read i = reads[offsets[i]-offsets[0] .. offsets[i+1]-offsets[0]).

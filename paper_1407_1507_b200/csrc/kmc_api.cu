@@ -80,13 +80,17 @@ void cache_flush_locked() {
     g_cache.clear();
     cudaGetLastError();
 }
-void* cache_alloc(size_t bytes, cudaStream_t s) {
+// *actual receives the size of the block handed out (a cached block may be up to 1.25x the
+// request); the caller gives that size back to cache_free so the block keeps its true label.
+void* cache_alloc(size_t bytes, cudaStream_t s, size_t* actual) {
     int dev = 0;
+    *actual = bytes;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> g(g_cache_mu);
     for (auto it = g_cache.lower_bound(bytes); it != g_cache.end() && it->first <= bytes + bytes / 4; ++it) {
         if (it->second.dev == dev && it->second.s == s) {
             void* p = it->second.p;
+            *actual = it->second.size;
             g_cache.erase(it);
             return p;
         }
@@ -126,12 +130,13 @@ struct Arena {
     // nullptr instead of an error when the allocator is out of memory
     void* try_alloc(size_t bytes) {
         bytes = cache_round(bytes == 0 ? 16 : bytes);
-        void* p = af ? af(bytes, (void*)s, ctx) : cache_alloc(bytes, s);
+        size_t got = bytes;
+        void* p = af ? af(bytes, (void*)s, ctx) : cache_alloc(bytes, s, &got);
         if (!p) {
             cudaGetLastError();
             return nullptr;
         }
-        ptrs.push_back({p, bytes});
+        ptrs.push_back({p, got});
         return p;
     }
     void* alloc(size_t bytes) {
@@ -859,6 +864,8 @@ void count_phase(kmc_job* j, PlanCtx& c) {
             kcap = (int)std::min<uint64_t>(2ull * chunk_hash_cap(k), std::max<uint64_t>(safe, (uint64_t)(safe / r)));
         }
         if (j->opt.chunk_capacity) kcap = (int)std::min<uint32_t>(j->opt.chunk_capacity, 1u << 24);
+        // the per-chunk radix sort holds at most small_capacity(k) keys in shared memory
+        if (j->opt.count_path == 1) kcap = std::min(kcap, small_capacity(k));
         j->st.chunk_capacity = (uint64_t)kcap;
         const int prec = msd_piece_records(k);
         // group budget in keys: the option, else everything at once if the key buffer can be

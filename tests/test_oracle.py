@@ -305,6 +305,57 @@ def test_count_queries_matches_full():
     assert np.array_equal(got, full.counts[idx].astype(np.uint64))
 
 
+@pytest.mark.parametrize("name,scale,k", [("C1", 0.05, None), ("C2", 0.002, None), ("C3", 0.002, None),
+                                          ("C4", 0.0003, None), ("C5", 0.002, None), ("C1", 0.01, 12),
+                                          ("C1", 0.01, 32), ("C1", 0.01, 64)])
+def test_partitioned_oracle_equals_plain(name, scale, k):
+    """The key-range-partitioned multi-threaded oracle is pinned to the plain
+    one: same arrays and statistics for any thread count and any number of ranges (round_keys
+    small enough to force many rounds of ranges; equal keys never straddle two ranges)."""
+    w = synth.make(name, scale=scale) if k is None else synth.make(name, scale=scale, k=k)
+    ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max)
+    nw = ref.n_windows
+    for T, rk in ((1, 1 << 40), (3, max(64, nw // 7)), (8, max(64, nw // 40))):
+        got = oracle.count_partitioned(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max, threads=T,
+                                       round_keys=rk)
+        assert np.array_equal(got.keys, ref.keys) and np.array_equal(got.counts, ref.counts), (T, rk)
+        assert (got.n_windows, got.n_unique, got.n_below_min, got.n_above_max, got.n_out) == \
+            (ref.n_windows, ref.n_unique, ref.n_below_min, ref.n_above_max, ref.n_out)
+    # the non-canonical switch passes through the partition too
+    fwd = oracle.count(w.reads, w.offsets, w.k, 1, canonical=False)
+    got = oracle.count_partitioned(w.reads, w.offsets, w.k, 1, canonical=False, threads=4,
+                                   round_keys=max(64, nw // 9))
+    assert np.array_equal(got.keys, fwd.keys) and np.array_equal(got.counts, fwd.counts)
+
+
+def test_partitioned_oracle_edge_cases():
+    for seqs, k, ci in ((["ACG"], 5, 1), (["N" * 50], 7, 1), ([], 9, 1), (["A" * 100, "T" * 40], 28, 2),
+                        (["ACGTACGT"], 4, 2)):
+        w = synth.from_strings(seqs, k, min(k, 3), ci)
+        ref = oracle.count(w.reads, w.offsets, k, ci)
+        got = oracle.count_partitioned(w.reads, w.offsets, k, ci, threads=5, round_keys=2)
+        assert np.array_equal(got.keys, ref.keys) and np.array_equal(got.counts, ref.counts)
+        assert got.n_windows == ref.n_windows and got.n_unique == ref.n_unique
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 0.05), ("C5", 0.003), ("C4", 0.0005)])
+def test_parallel_window_count_equals_serial(name, scale):
+    """oracle_n_windows_par (the full-size window-count checker) = the serial count = the sum
+    of the counts with ci = 1."""
+    w = synth.make(name, scale=scale)
+    n = oracle.n_windows(w.reads, w.offsets, w.k)
+    assert oracle.n_windows_parallel(w.reads, w.offsets, w.k) == n
+    assert int(oracle.count(w.reads, w.offsets, w.k, 1).counts.sum(dtype=np.uint64)) == n
+
+
+def test_digest_is_order_and_value_sensitive():
+    k = np.array([1, 2, 3], dtype=np.uint64)
+    c = np.array([5, 6, 7], dtype=np.uint32)
+    d = oracle.digest(k, c)
+    assert d == oracle.digest(k.copy(), c.copy())
+    assert d != oracle.digest(k[::-1], c[::-1]) and d != oracle.digest(k, c + 1)
+
+
 def test_synth_deterministic_and_shaped():
     a = synth.make("C5", scale=0.01, n_threads=1)
     b = synth.make("C5", scale=0.01, n_threads=4)
