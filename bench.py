@@ -46,7 +46,7 @@ def compact_bin_bytes(st: dict, k: int) -> float:
     return st["n_superkmers"] * 1.0 + 2.0 * (st["n_windows"] + st["n_superkmers"] * (k - 1)) / 8.0
 
 
-def stage_bytes(st: dict, n_reads: int, k: int) -> dict:
+def stage_bytes(st: dict, n_reads: int, k: int, split_ran: bool = True) -> dict:
     """Algorithmic HBM bytes per stage and call, SURVEY 8(d):
     B_alg = input (ASCII + offsets) + 2 x compact bins (written once, read once) + output.
     Each byte of B_alg is charged to the stage that must move it: pass 1 reads the input and
@@ -63,9 +63,10 @@ def stage_bytes(st: dict, n_reads: int, k: int) -> dict:
         "signature": nb + off + bins,        # input read, bins written once
         "scatter": 0.0,                      # implementation pass (record stream -> bins)
         "small_bins": (1 - lfrac) * bins,    # bins read once
-        "large_split": lfrac * bins,         # bins read once
+        # large bins: read once by the split (large_path 2) or by the cluster kernel (default)
+        "large_split": lfrac * bins if split_ran else 0.0,
         "large_scatter": 0.0,                # implementation pass (key split)
-        "large_chunks": 0.0,                 # implementation pass (re-read of the split keys)
+        "large_chunks": 0.0 if split_ran else lfrac * bins,
         "large_fallback": 0.0,
         "order": st["n_out"] * (ksz + 4),    # output written once
         "output": 0.0,
@@ -334,7 +335,7 @@ def main():
 
     # ---- roofline of the dominant stage (SURVEY 8(d) bytes)
     peaks = measured_peaks()
-    sb = stage_bytes(last, w.n_reads, k)
+    sb = stage_bytes(last, w.n_reads, k, split_ran=stage_ms.get("large_split", 0.0) > 0)
     per_stage = {}
     for s_, tot in stage_ms.items():
         if tot <= 0:
@@ -422,7 +423,8 @@ def main():
                    "l2": "inputs (4 GB) larger than L2 (126 MB); no flush needed"},
         "kmers_per_s": windows_all / (ms / 1e3),
         "stats": {x: last[x] for x in ("n_windows", "n_superkmers", "n_records", "n_bins", "n_large_bins",
-                                      "max_bin_windows", "large_windows", "n_unique", "n_out")},
+                                      "max_bin_windows", "large_windows", "n_unique", "n_out", "n_cluster_items",
+                                      "n_single_items", "n_spilled_keys", "cluster_size", "cluster_ctas")},
         "stages": per_stage,
         "roofline": roof,
         "cpu_baseline": cpu,

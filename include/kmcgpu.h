@@ -118,6 +118,12 @@ typedef struct {
     uint64_t max_signature_windows; /* windows of the most frequent signature (Table 6) */
     uint64_t n_small_sorted;   /* small bins whose distinct keys overfilled the SMEM hash table
                                   (sorted + run-length compacted in SMEM instead) */
+    uint64_t n_cluster_items;  /* (bin, round) items counted by thread-block clusters (large_path 3) */
+    uint64_t n_single_items;   /* large bins counted by one CTA's table (large_path 3) */
+    uint64_t n_spilled_keys;   /* windows whose key found no slot in an overfull table (counted by
+                                  the device radix-sort fallback) */
+    uint64_t cluster_size;     /* CTAs per cluster of the large-bin path (0: not used) */
+    uint64_t cluster_ctas;     /* CTAs the large-bin cluster kernel ran with */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;
@@ -128,8 +134,13 @@ typedef struct {
                                     (clamped to the kernel maximum); smaller values force
                                     more bins down the large path (testing) */
     uint32_t force_large;      /* 1: every bin takes the large (multi-CTA) path (testing) */
-    uint32_t large_path;       /* 0: hashed split + per-chunk SMEM sort (default);
-                                  1: device-wide LSD radix sort of all large-bin keys (testing) */
+    uint32_t large_path;       /* 0 (default) / 2: hashed split of every large bin into HBM key
+                                  chunks, each counted by count_path.
+                                  1: device-wide LSD radix sort of all large-bin keys (testing).
+                                  3 (k <= 32, count_path 0; measured slower):
+                                  thread-block clusters count each large bin in their CTAs'
+                                  shared-memory tables, keys routed to their owner CTA through
+                                  distributed shared memory -- no key spill to HBM */
     uint32_t distribute_path;  /* 0: pass 1 streams its records, S5 copies them into bins (default);
                                   1: S5 recomputes pass 1 from the reads (testing) */
     uint32_t input_batch_mb;   /* host-resident reads are streamed through pass 1 in read-aligned
@@ -153,6 +164,13 @@ typedef struct {
     uint32_t plain_minimizers; /* 1 (diagnostic): signatures are plain canonical minimizers, without
                                   the P:L206-208 restrictions -- the "Minimizers" columns of
                                   Table 6.  Same counts; different bins. */
+    uint32_t cluster_size;     /* large_path 3: CTAs per cluster, 0 = auto (16 where the device
+                                  holds such clusters, else 8), or 1, 4, 8, 16 (1: single-CTA
+                                  tables only -- bins above one table spill; testing) */
+    uint32_t table_keys;       /* large_path 3, testing: distinct keys one CTA's table is planned
+                                  for (0 = 3/4 of its slots); small values force many rounds */
+    uint32_t spill_keys;       /* large_path 3, testing: spill list capacity (0 = auto); a spill
+                                  beyond it reruns the large bins on the split path */
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).

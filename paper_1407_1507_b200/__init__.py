@@ -35,7 +35,8 @@ class _Stats(ctypes.Structure):
         "n_reads", "n_bases", "n_invalid_bases", "n_windows", "n_superkmers", "n_records",
         "n_signatures_used", "n_bins", "n_large_bins", "max_bin_windows", "large_windows", "n_unique",
         "n_below_min", "n_above_max", "n_out", "n_launches", "n_input_batches", "n_large_groups",
-        "chunk_capacity", "n_overflow_chunks", "n_order_oversize", "max_signature_windows", "n_small_sorted")] + [
+        "chunk_capacity", "n_overflow_chunks", "n_order_oversize", "max_signature_windows", "n_small_sorted",
+        "n_cluster_items", "n_single_items", "n_spilled_keys", "cluster_size", "cluster_ctas")] + [
         ("stage_ms", ctypes.c_float * len(STAGES)), ("stage_launches", ctypes.c_uint32 * len(STAGES))]
 
     def to_dict(self) -> dict:
@@ -51,7 +52,8 @@ class _Options(ctypes.Structure):
                 ("distribute_path", ctypes.c_uint32), ("input_batch_mb", ctypes.c_uint32),
                 ("large_group_mkeys", ctypes.c_uint32), ("count_path", ctypes.c_uint32),
                 ("chunk_capacity", ctypes.c_uint32), ("non_canonical", ctypes.c_uint32),
-                ("plain_minimizers", ctypes.c_uint32)]
+                ("plain_minimizers", ctypes.c_uint32), ("cluster_size", ctypes.c_uint32),
+                ("table_keys", ctypes.c_uint32), ("spill_keys", ctypes.c_uint32)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
@@ -169,8 +171,12 @@ class Result:
 
 
 def _options(profile, small_bin_capacity, force_large, large_path=0, distribute_path=0, input_batch_mb=0,
-             large_group_mkeys=0, count_path=0, chunk_capacity=0, canonical=True, plain_minimizers=False):
+             large_group_mkeys=0, count_path=0, chunk_capacity=0, canonical=True, plain_minimizers=False,
+             cluster_size=0, table_keys=0, spill_keys=0):
     o = _Options()
+    o.cluster_size = int(cluster_size)
+    o.table_keys = int(table_keys)
+    o.spill_keys = int(spill_keys)
     o.non_canonical = 0 if canonical else 1
     o.plain_minimizers = int(bool(plain_minimizers))
     o.count_path = int(count_path)
@@ -189,7 +195,8 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
           profile: bool = False, small_bin_capacity: int = 0, force_large: bool = False,
           large_path: int = 0, distribute_path: int = 0, input_batch_mb: int = 0, large_group_mkeys: int = 0,
           count_path: int = 0, chunk_capacity: int = 0, out_device: str | None = None,
-          canonical: bool = True, plain_minimizers: bool = False) -> Result:
+          canonical: bool = True, plain_minimizers: bool = False, cluster_size: int = 0, table_keys: int = 0,
+          spill_keys: int = 0) -> Result:
     """Count canonical k-mers (KMC 2 hot path on the GPU); canonical=False counts them as
     they occur in the reads (KMC's -b).
 
@@ -205,7 +212,8 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
     if n_reads < 0:
         raise ValueError("offsets must have n_reads + 1 entries")
     opt = _options(profile, small_bin_capacity, force_large, large_path, distribute_path, input_batch_mb,
-                   large_group_mkeys, count_path, chunk_capacity, canonical, plain_minimizers)
+                   large_group_mkeys, count_path, chunk_capacity, canonical, plain_minimizers, cluster_size,
+                   table_keys, spill_keys)
     job = ctypes.c_void_p()
     n_out = ctypes.c_uint64()
     sh = _stream_handle(stream)

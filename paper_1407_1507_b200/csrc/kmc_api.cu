@@ -6,6 +6,7 @@
 //   -> large bins: expand (S6) + device radix sort (S7) + RLE (S8)
 //   -> sync: survivor count -> [finish] global order (S9) -> output copy.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -798,8 +799,113 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         j->launches += sl;
         j->stage_end(sl);
     }
+    // distinct keys per window, estimated from the sampled small bins (x margin); 1 without a
+    // sample (every window distinct: the safe assumption)
+    auto distinct_ratio = [&](double margin) -> double {
+        double r = 1.0;
+        if (ev_sample) {  // distinct keys of the sampled small bins (the rest still run)
+            CK(cudaEventSynchronize(ev_sample));
+            r = std::min(1.0, std::max(0.05, margin * (double)hs[64] / (double)sample_w));
+        } else if (small_w >= (1u << 20)) {
+            CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            r = std::min(1.0, std::max(0.05, margin * (double)hs[16 + GS_UNIQUE] / (double)small_w));
+        }
+        return r;
+    };
     // ---- S6-S8 large bins
-    if (large_windows > 0 && j->opt.large_path == 1) {
+    bool large_done = false;
+    if (large_windows > 0 && k <= 32 && j->opt.large_path == 3 && j->opt.count_path != 1) {
+        // thread-block clusters count every large bin in their CTAs' shared-memory tables
+        // (k_cluster.cu): no key spill to HBM, one expansion per window and round
+        int C = (int)j->opt.cluster_size;
+        if (C == 0) C = cluster_max_active(16) > 0 ? 16 : cluster_max_active(8) > 0 ? 8 : 1;
+        if (C != 1 && C != 4 && C != 8 && C != 16) {
+            set_err("cluster_size=%d not in {0, 1, 4, 8, 16}", C);
+            throw Fail{KMC_ERR_INVALID_ARG};
+        }
+        if (C > 1 && cluster_max_active(C) < 1) {
+            set_err("the device holds no cluster of %d CTAs", C);
+            throw Fail{KMC_ERR_INVALID_ARG};
+        }
+        const double r = distinct_ratio(1.25);
+        const double cap = j->opt.table_keys ? (double)j->opt.table_keys : (double)cl_table_slots() * 3 / 4;
+        std::vector<ClItem> items;  // cluster items first, then single items
+        std::vector<ClItem> singles;
+        for (const uint64_t b : large_ids) {
+            const double d = (double)bw[b] * r;
+            if (C == 1 || d <= cap) {
+                singles.push_back(ClItem{bo[b], (uint32_t)bn[b], 0, 1});
+            } else {
+                const uint64_t R = std::min<uint64_t>(65535, (uint64_t)std::ceil(d / ((double)C * cap)));
+                for (uint64_t q = 0; q < R; ++q) items.push_back(ClItem{bo[b], (uint32_t)bn[b], (uint16_t)q, (uint16_t)R});
+            }
+        }
+        auto by_size = [](const ClItem& x, const ClItem& y) {
+            return x.nrec > y.nrec || (x.nrec == y.nrec && (x.rec_off < y.rec_off || (x.rec_off == y.rec_off && x.round < y.round)));
+        };
+        std::sort(items.begin(), items.end(), by_size);
+        std::sort(singles.begin(), singles.end(), by_size);
+        const uint64_t n_ci = items.size(), n_si = singles.size();
+        items.insert(items.end(), singles.begin(), singles.end());
+        ClItem* d_items = ar.get<ClItem>(items.size());
+        CK(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(ClItem), cudaMemcpyHostToDevice, s));
+        unsigned long long* ctr = ar.get<unsigned long long>(4);
+        CK(cudaMemsetAsync(ctr, 0, 32, s));
+        const uint64_t spill_cap =
+            j->opt.spill_keys ? (uint64_t)j->opt.spill_keys : std::max<uint64_t>(1u << 20, large_windows / 16);
+        uint64_t* spill = ar.get<uint64_t>(spill_cap);
+        unsigned long long* gsnap = ar.get<unsigned long long>(GS_N);
+        CK(cudaMemcpyAsync(gsnap, gstats, GS_N * 8, cudaMemcpyDeviceToDevice, s));
+        int n_ctas = 0;
+        j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
+        CK(launch_cluster_count(bins, d_items, n_ci, d_items + n_ci, n_si, C, k, !j->opt.non_canonical, j->ci, j->cx,
+                                ctr, spill, spill_cap, j->surv_keys, j->surv_counts, gstats, 0, s, &n_ctas));
+        j->launches += 1;
+        j->stage_end(1);
+        CK(cudaMemcpyAsync(&hs[48], ctr, 24, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t n_spill = hs[50];
+        j->st.n_cluster_items = n_ci;
+        j->st.n_single_items = n_si;
+        j->st.n_spilled_keys = n_spill;
+        j->st.cluster_size = (uint64_t)C;
+        j->st.cluster_ctas = (uint64_t)n_ctas;
+        if (n_spill > spill_cap) {
+            // the spill list overflowed: forget this pass's counts, take the split path
+            CK(cudaMemcpyAsync(gstats, gsnap, GS_N * 8, cudaMemcpyDeviceToDevice, s));
+        } else {
+            if (n_spill > 0) {
+                // keys that found no slot: disjoint from every table's keys (all their copies
+                // fail alike), counted by the device radix sort + run pass
+                RadixScratch rs{};
+                rs.keys_alt = ar.alloc(n_spill * 8);
+                const uint64_t nt = (n_spill + radix_tile_items(1) - 1) / radix_tile_items(1);
+                rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
+                rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+                rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n_spill, 1));
+                rs.red = ar.get<unsigned long long>(4);
+                rs.red_host = hs + 40;
+                void* sorted = nullptr;
+                uint32_t* dummy = nullptr;
+                int fl = 0;
+                j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
+                CK(device_radix_sort(1, spill, nullptr, n_spill, 2 * k, rs, s, &sorted, &dummy, &fl));
+                CK(launch_rle(1, sorted, n_spill, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+                j->launches += fl + 1;
+                j->stage_end(fl + 1);
+                ar.release(rs.keys_alt);
+                ar.release(rs.tile_hist);
+                ar.release(rs.tile_off);
+                ar.release(rs.scan_temp);
+            }
+            large_done = true;
+        }
+        ar.release(spill);
+        ar.release(d_items);
+    }
+    if (large_done) {
+    } else if (large_windows > 0 && j->opt.large_path == 1) {
         // device-wide LSD radix sort of all large-bin keys together (a bin partitions the
         // k-mer space, so sorting the union sorts every bin); kept for testing
         std::vector<LargeBin> lbins(large_ids.size());
@@ -852,15 +958,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         int kcap = small_capacity(k);
         if (j->opt.count_path != 1) {
             const uint64_t safe = (uint64_t)chunk_hash_cap(k) * 3 / 4;
-            double r = 1.0;
-            if (ev_sample) {  // distinct keys of the sampled small bins (the rest still run)
-                CK(cudaEventSynchronize(ev_sample));
-                r = std::min(1.0, std::max(0.05, 1.5 * (double)hs[64] / (double)sample_w));
-            } else if (small_w >= (1u << 20)) {
-                CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
-                CK(cudaStreamSynchronize(s));
-                r = std::min(1.0, std::max(0.05, 1.5 * (double)hs[16 + GS_UNIQUE] / (double)small_w));
-            }
+            const double r = distinct_ratio(1.5);
             kcap = (int)std::min<uint64_t>(2ull * chunk_hash_cap(k), std::max<uint64_t>(safe, (uint64_t)(safe / r)));
         }
         if (j->opt.chunk_capacity) kcap = (int)std::min<uint32_t>(j->opt.chunk_capacity, 1u << 24);

@@ -219,6 +219,25 @@ cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_
 cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, int canonical,
                                 void* keys, unsigned long long* gstats, cudaStream_t s);
 
+// S6-S8 of the large bins by thread-block clusters (k_cluster.cu, k <= 32): a cluster item is
+// (bin, round r of R) counted by all CTAs of a cluster with keys routed to their owner CTA
+// through distributed shared memory; a single item is a bin counted by one CTA's table.
+struct ClItem {
+    uint64_t rec_off;  // first record of the bin
+    uint32_t nrec;
+    uint16_t round, nround;
+};
+int cl_table_slots();
+int cl_records_per_piece(int k);
+int cluster_max_active(int cluster);  // 0 if the device cannot hold such clusters
+// ctr: 3 zeroed uint64 ([2] = spilled keys on return; spill holds min(ctr[2], spill_cap) keys).
+// max_ctas: 0 = every SM; else at most this many CTAs.  *n_ctas: CTAs launched.
+cudaError_t launch_cluster_count(const uint32_t* bins, const ClItem* citems, uint64_t n_citems, const ClItem* sitems,
+                                 uint64_t n_sitems, int cluster, int k, int canonical, uint32_t ci, uint32_t cx,
+                                 unsigned long long* ctr, uint64_t* spill, uint64_t spill_cap, void* surv_keys,
+                                 uint32_t* surv_counts, unsigned long long* gstats, int max_ctas, cudaStream_t s,
+                                 int* n_ctas);
+
 // Device-wide LSD radix sort of n keys (+ optional uint32 values).  Result lands in
 // (*res_keys, *res_vals) which is either the input or the alternate buffers.
 struct RadixScratch {

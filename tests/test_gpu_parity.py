@@ -103,7 +103,9 @@ def test_count_parity_configs(gpu, name, scale):
 @pytest.mark.parametrize("opts", [dict(force_large=True), dict(small_bin_capacity=64), dict(small_bin_capacity=1024),
                                   dict(large_path=1), dict(force_large=True, large_path=1),
                                   dict(distribute_path=1), dict(count_path=1),
-                                  dict(force_large=True, count_path=1)])
+                                  dict(force_large=True, count_path=1), dict(force_large=True, large_path=2),
+                                  dict(force_large=True, large_path=3, cluster_size=4, table_keys=100),
+                                  dict(force_large=True, large_path=3, cluster_size=1)])
 def test_forced_paths(gpu, opts):
     w = synth.make("C5", scale=0.005)
     st = assert_same(gpu, w, **opts)
@@ -146,13 +148,49 @@ def test_chunk_hash_overflow_fallback(gpu):
     # low-coverage small bins: chunks sized for repeats overflow the table and must fall back
     seqs = synth.random_reads(77, 6000, 100, 150, alphabet=b"ACGT")
     w = synth.from_strings(seqs, 25, 5, 1)
-    st = assert_same(gpu, w, force_large=True, chunk_capacity=60000)
+    st = assert_same(gpu, w, force_large=True, chunk_capacity=60000, large_path=2)
     assert st["large_windows"] > 0 and st["n_overflow_chunks"] > 0
-    st = assert_same(gpu, w, force_large=True)
+    st = assert_same(gpu, w, force_large=True, large_path=2)
     assert st["n_overflow_chunks"] == 0
     # the sort path clamps an oversize chunk capacity to its shared-memory array
     st = assert_same(gpu, w, force_large=True, count_path=1, chunk_capacity=60000)
     assert st["chunk_capacity"] <= 6144
+
+
+# ---------------------------------------------------------------- large bins by thread-block clusters
+
+@pytest.mark.parametrize("cluster_size", [1, 4, 8, 16])
+@pytest.mark.parametrize("table_keys", [0, 40, 3000])
+def test_cluster_path(gpu, cluster_size, table_keys):
+    """Large bins counted by clusters of 1-16 CTAs (keys routed to their owner CTA through
+    distributed shared memory); small table_keys plans many rounds per bin and cluster items
+    whose slices hold fewer records than CTAs."""
+    w = synth.make("C2", scale=0.003)
+    st = assert_same(gpu, w, force_large=True, large_path=3, cluster_size=cluster_size, table_keys=table_keys)
+    assert st["cluster_size"] == cluster_size and st["large_windows"] == st["n_windows"]
+    if cluster_size > 1 and table_keys:
+        assert st["n_cluster_items"] > 0
+
+
+@pytest.mark.parametrize("k", [12, 25, 28, 29, 30, 31, 32])
+def test_cluster_path_units(gpu, k):
+    # every expansion unit width (4 windows for k <= 29, 33 - k above) and records up to maxw
+    seqs = ["A" * 400, "AC" * 200] * 20 + [s.decode() for s in synth.random_reads(k, 1500, 30, 300, n_frac=0.01)]
+    assert_same(gpu, synth.from_strings(seqs, k, 5, 1), force_large=True, large_path=3, cluster_size=8, table_keys=50)
+
+
+def test_cluster_spill_and_fallback(gpu):
+    # distinct-heavy bins far above one table (p = 3: a few huge signatures, random reads):
+    # single-CTA tables overfill, the keys that find no slot are spilled and counted by the
+    # device radix sort; a spill list too small for them reruns the large bins on the split path
+    seqs = synth.random_reads(5, 8000, 100, 150, alphabet=b"ACGT")
+    w = synth.from_strings(seqs, 25, 3, 1)
+    st = assert_same(gpu, w, force_large=True, large_path=3, cluster_size=1, spill_keys=1 << 24)
+    assert st["n_spilled_keys"] > 0
+    st = assert_same(gpu, w, force_large=True, large_path=3, cluster_size=1, spill_keys=1000)
+    assert st["n_spilled_keys"] > 1000  # overflowed -> split path
+    st = assert_same(gpu, w, force_large=True, large_path=3, cluster_size=16)
+    assert st["n_cluster_items"] > 0
 
 
 def test_small_bin_hash_and_sort_fallback(gpu):
@@ -169,12 +207,14 @@ def test_small_bin_hash_and_sort_fallback(gpu):
     assert st["n_small_sorted"] == 0 and st["n_bins"] > st["n_large_bins"]
 
 
-@pytest.mark.parametrize("count_path", [0, 1])
+@pytest.mark.parametrize("large_path,count_path", [(3, 0), (0, 0), (0, 1)])
 @pytest.mark.parametrize("name,scale", [("C3", 0.005), ("C2", 0.005), ("C1", 0.2)])
-def test_chunk_count_paths(gpu, name, scale, count_path):
-    # every bin through the large path: hashed split, then per-chunk SMEM hash count
-    # (count_path 0) or SMEM radix sort + run-length compaction (count_path 1)
-    st = assert_same(gpu, synth.make(name, scale=scale), force_large=True, count_path=count_path)
+def test_chunk_count_paths(gpu, name, scale, large_path, count_path):
+    # every bin through the large path: cluster tables (large_path 3, k <= 32), or the hashed
+    # split and per-chunk SMEM hash count (count_path 0) or SMEM radix sort + run-length
+    # compaction (count_path 1)
+    st = assert_same(gpu, synth.make(name, scale=scale), force_large=True, count_path=count_path,
+                     large_path=large_path)
     assert st["large_windows"] == st["n_windows"]
 
 
@@ -183,14 +223,14 @@ def test_split_piece_and_range_modes(gpu):
     # (AC)n super-k-mers: maxw windows per record) next to ordinary ones
     seqs = ["A" * 3000, "AC" * 1500, "ACGTTGCA" * 300] * 40
     seqs += [s.decode() for s in synth.random_reads(21, 3000, 100, 300)]
-    assert_same(gpu, synth.from_strings(seqs, 28, 9, 1), force_large=True)
+    assert_same(gpu, synth.from_strings(seqs, 28, 9, 1), force_large=True, large_path=2)
     # tiny chunks: bins with more than 2^8 digits take range mode, the rest piece mode, in
     # the same split launch
-    st = assert_same(gpu, synth.make("C2", scale=0.005), force_large=True, chunk_capacity=128)
+    st = assert_same(gpu, synth.make("C2", scale=0.005), force_large=True, chunk_capacity=128, large_path=2)
     assert st["chunk_capacity"] == 128
 
 
-@pytest.mark.parametrize("large_path,count_path", [(0, 0), (0, 1), (1, 0)])
+@pytest.mark.parametrize("large_path,count_path", [(0, 0), (0, 1), (1, 0), (3, 0)])
 def test_low_complexity_and_skew(gpu, large_path, count_path):
     # poly-A / (AT)n pile-ups: one k-mer with ~25K copies -> an "oversize" MSD digit
     seqs = ["A" * 300, "T" * 250, "AT" * 120, "ACGT" * 60, "N" * 50, "", "ACG", "CA" * 100] * 50
@@ -434,7 +474,10 @@ def test_random_sweep(gpu, seed):
     ci = rng.choice([1, 1, 2, 3])
     cx = rng.choice([10**9, 10**9, 50, 7])
     opts = rng.choice([{}, dict(force_large=True), dict(small_bin_capacity=256), dict(force_large=True, count_path=1),
-                       dict(force_large=True, chunk_capacity=512), dict(large_path=1, force_large=True),
+                       dict(force_large=True, chunk_capacity=512, large_path=2), dict(large_path=1, force_large=True),
+                       dict(force_large=True, large_path=3, cluster_size=rng.choice([4, 8, 16]),
+                            table_keys=rng.choice([8, 100])),
+                       dict(force_large=True, large_path=3, cluster_size=1),
                        dict(canonical=False) if k not in (32, 64) else {}, dict(plain_minimizers=True)])
     seqs = _mutated_reads(seed, rng.randint(50, 400), rng.choice([60, 150, 400]))
     w = synth.from_strings(seqs, k, p, ci, cx)
