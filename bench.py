@@ -424,7 +424,8 @@ def main():
         "kmers_per_s": windows_all / (ms / 1e3),
         "stats": {x: last[x] for x in ("n_windows", "n_superkmers", "n_records", "n_bins", "n_large_bins",
                                       "max_bin_windows", "large_windows", "n_unique", "n_out", "n_cluster_items",
-                                      "n_single_items", "n_spilled_keys", "cluster_size", "cluster_ctas")},
+                                      "n_single_items", "n_spilled_keys", "cluster_size", "cluster_ctas",
+                                      "n_split_overflow", "n_overflow_chunks", "chunk_capacity")},
         "stages": per_stage,
         "roofline": roof,
         "cpu_baseline": cpu,

@@ -124,6 +124,8 @@ typedef struct {
                                   the device radix-sort fallback) */
     uint64_t cluster_size;     /* CTAs per cluster of the large-bin path (0: not used) */
     uint64_t cluster_ctas;     /* CTAs the large-bin cluster kernel ran with */
+    uint64_t n_split_overflow; /* large-bin keys whose digit overfilled its region in the one-pass
+                                  split (counted by the device radix-sort fallback) */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;

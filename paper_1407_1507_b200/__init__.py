@@ -36,7 +36,8 @@ class _Stats(ctypes.Structure):
         "n_signatures_used", "n_bins", "n_large_bins", "max_bin_windows", "large_windows", "n_unique",
         "n_below_min", "n_above_max", "n_out", "n_launches", "n_input_batches", "n_large_groups",
         "chunk_capacity", "n_overflow_chunks", "n_order_oversize", "max_signature_windows", "n_small_sorted",
-        "n_cluster_items", "n_single_items", "n_spilled_keys", "cluster_size", "cluster_ctas")] + [
+        "n_cluster_items", "n_single_items", "n_spilled_keys", "cluster_size", "cluster_ctas",
+        "n_split_overflow")] + [
         ("stage_ms", ctypes.c_float * len(STAGES)), ("stage_launches", ctypes.c_uint32 * len(STAGES))]
 
     def to_dict(self) -> dict:

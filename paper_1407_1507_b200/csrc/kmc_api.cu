@@ -615,6 +615,211 @@ void fetch_tables(kmc_job* j, PlanCtx& c) {
     CK(cudaStreamSynchronize(j->cs));
 }
 
+// Large bins of the default path for k <= 32 (k_split1.cu): one sized split pass puts every
+// key of a bin into the region of its hashed digit (a bin of W windows: nd ~ W / (0.8 kcap)
+// digits of rc ~ 1.05 W / nd slots), then every digit that fits its region is one chunk of the
+// SMEM hash count.  Digits that overflowed their region (region part + the overflow list)
+// and chunks whose distinct keys overflow the hash table are counted by the device radix sort.
+// Bins are processed in groups whose regions fit the device budget.
+template <class DR>
+void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vector<uint64_t>& large_ids, int kcap,
+                  DR&& distinct_ratio) {
+    (void)distinct_ratio;
+    const int k = j->k;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    unsigned long long* hs = j->host_small;
+    unsigned long long* gstats = c.gstats;
+    const std::vector<uint64_t>& bw = c.bw;
+    const std::vector<uint64_t>& bn = c.bn;
+    const std::vector<uint64_t>& bo = c.bo;
+    // digit target 0.75 kcap; regions 1.25x the mean + 256 (hashed digits are near-uniform,
+    // but a k-mer of multiplicity m moves m keys at once: repeat families skew them)
+    const double target = std::max(1.0, 0.75 * kcap);
+    const uint32_t rpp = (uint32_t)split1_piece_records(k);
+    const size_t nl = large_ids.size();
+    std::vector<uint32_t> nd(nl), rc(nl);
+    uint64_t total = 0;
+    for (size_t i = 0; i < nl; ++i) {
+        const uint64_t b = large_ids[i];
+        uint64_t d = (uint64_t)std::ceil((double)bw[b] / target);
+        d = std::min<uint64_t>(std::max<uint64_t>(d, 1), (uint64_t)S1_DMAX);
+        uint64_t r = (uint64_t)std::ceil((double)bw[b] / (double)d * 1.25) + 256;
+        r = std::min<uint64_t>((r + 1) & ~1ull, 0x7FFFFFFEull);
+        nd[i] = (uint32_t)d;
+        rc[i] = (uint32_t)r;
+        total += d * r;
+    }
+    // group budget in region keys: the option, else everything if the key buffer can be
+    // allocated, else half the free device memory
+    uint64_t budget = j->opt.large_group_mkeys ? ((uint64_t)j->opt.large_group_mkeys << 20) : ~0ull;
+    void* lkeys = nullptr;
+    if (!j->opt.large_group_mkeys) {
+        lkeys = ar.try_alloc(total * 8 + chunk_key_slack_bytes());
+        if (!lkeys) {
+            size_t fr = 0, tot = 0;
+            CK(cudaMemGetInfo(&fr, &tot));
+            budget = std::max<uint64_t>((uint64_t)(fr / 2) / 9, 1u << 20);
+        }
+    }
+    std::vector<std::pair<size_t, size_t>> groups;
+    uint64_t max_gk = 0, max_gd = 0, max_gp = 0, max_gn = 0;
+    for (size_t i0 = 0; i0 < nl;) {
+        uint64_t gk = 0, gd = 0, gp = 0;
+        size_t i1 = i0;
+        while (i1 < nl) {
+            const uint64_t need = (uint64_t)nd[i1] * rc[i1];
+            if (i1 > i0 && gk + need > budget) break;
+            gk += need;
+            gd += nd[i1];
+            gp += (bn[large_ids[i1]] + rpp - 1) / rpp;
+            ++i1;
+        }
+        groups.push_back({i0, i1});
+        max_gk = std::max(max_gk, gk);
+        max_gd = std::max(max_gd, gd);
+        max_gp = std::max(max_gp, gp);
+        max_gn = std::max<uint64_t>(max_gn, i1 - i0);
+        i0 = i1;
+    }
+    j->st.n_large_groups = groups.size();
+    LargeBin* d_lbins = ar.get<LargeBin>(max_gn);
+    S1Bin* d_sbins = ar.get<S1Bin>(max_gn);
+    uint64_t* d_pp = ar.get<uint64_t>(max_gn + 1);
+    Piece* d_pieces = ar.get<Piece>(max_gp);
+    uint32_t* cur = ar.get<uint32_t>(max_gd);
+    Chunk* chunks = ar.get<Chunk>(max_gd);
+    Chunk* over = ar.get<Chunk>(max_gd);
+    Chunk* ovd = ar.get<Chunk>(max_gd);
+    Chunk* tovf = ar.get<Chunk>(max_gd);  // chunks whose distinct keys overflowed the hash table
+    unsigned long long* ctr = ar.get<unsigned long long>(5);  // chunks, oversize, overflowed digits, overflow keys, table overflows
+    if (!lkeys) lkeys = ar.alloc(max_gk * 8 + chunk_key_slack_bytes());
+    uint64_t ovf_cap = std::max<uint64_t>(1u << 20, max_gk / 32);
+    uint64_t* ovf = ar.get<uint64_t>(ovf_cap);
+    RadixScratch rs{};
+    uint64_t rs_cap = 0;
+    auto sort_rle = [&](uint64_t* keys, uint64_t n, int& nlaunch) {
+        if (n == 0) return;
+        if (n > rs_cap) {
+            ar.release(rs.keys_alt);
+            ar.release(rs.tile_hist);
+            ar.release(rs.tile_off);
+            ar.release(rs.scan_temp);
+            rs.keys_alt = ar.alloc(n * 8);
+            const uint64_t nt = (n + radix_tile_items(1) - 1) / radix_tile_items(1);
+            rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
+            rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+            rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n, 1));
+            if (!rs.red) rs.red = ar.get<unsigned long long>(4);
+            rs.red_host = hs + 40;
+            rs_cap = n;
+        }
+        void* sorted = nullptr;
+        uint32_t* dummy = nullptr;
+        CK(device_radix_sort(1, keys, nullptr, n, 2 * k, rs, s, &sorted, &dummy, &nlaunch));
+        CK(launch_rle(1, sorted, n, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+        nlaunch += 1;
+    };
+    static thread_local std::vector<LargeBin> lbins;
+    static thread_local std::vector<S1Bin> sbins;
+    static thread_local std::vector<uint64_t> pp;
+    for (const auto& g : groups) {
+        const size_t gn = g.second - g.first;
+        lbins.resize(gn);
+        sbins.resize(gn);
+        pp.assign(gn + 1, 0);
+        uint64_t key_base = 0, dbase = 0;
+        for (size_t i = 0; i < gn; ++i) {
+            const size_t li = g.first + i;
+            const uint64_t b = large_ids[li];
+            lbins[i] = LargeBin{0, 0, bo[b], 0, (uint32_t)bw[b], 0, (uint32_t)bn[b], 0, 0, 0};
+            sbins[i] = S1Bin{key_base, nd[li], rc[li], (uint32_t)dbase, 0};
+            key_base += (uint64_t)nd[li] * rc[li];
+            dbase += nd[li];
+            pp[i + 1] = pp[i] + (bn[b] + rpp - 1) / rpp;
+        }
+        const uint64_t n_pieces = pp.back();
+        CK(cudaMemcpyAsync(d_lbins, lbins.data(), gn * sizeof(LargeBin), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_sbins, sbins.data(), gn * sizeof(S1Bin), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
+        uint64_t n_chunks = 0, n_over = 0, n_ovd = 0, n_ovk = 0;
+        for (;;) {
+            j->stage_begin(KMC_STAGE_LARGE_SCATTER);
+            CK(cudaMemsetAsync(cur, 0, dbase * 4, s));
+            CK(cudaMemsetAsync(ctr, 0, 40, s));
+            CK(launch_make_pieces(d_lbins, d_pp, gn, rpp, d_pieces, s));
+            CK(launch_split1(bins, d_pieces, n_pieces, d_sbins, k, !j->opt.non_canonical, cur, (uint64_t*)lkeys, ovf,
+                             ctr + 3, ovf_cap, 2 * n_sms(), s));
+            CK(launch_split1_chunks(d_sbins, gn, cur, 0xFFFFFFFFu, chunks, over, ovd, ctr, s));
+            j->launches += 3;
+            j->stage_end(3);
+            CK(cudaMemcpyAsync(&hs[48], ctr, 32, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            n_chunks = hs[48];
+            n_over = hs[49];
+            n_ovd = hs[50];
+            n_ovk = hs[51];
+            if (n_ovk <= ovf_cap) break;
+            // the overflow list was too small for the digits' excess keys (the same amount on
+            // a rerun: it depends only on the keys): grow it and split the group again
+            ar.release(ovf);
+            ovf_cap = n_ovk + (n_ovk >> 3) + 1024;
+            ovf = ar.get<uint64_t>(ovf_cap);
+        }
+        j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
+        CK(launch_chunk_hash(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, tovf,
+                             ctr + 4, n_sms(), s));
+        j->launches += 1;
+        j->stage_end(1);
+        CK(cudaMemcpyAsync(&hs[52], ctr + 4, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t n_tovf = hs[52];
+        j->st.n_overflow_chunks += n_tovf;
+        if (n_over + n_ovd + n_ovk + n_tovf == 0) continue;
+        int fl = 0;
+        j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
+        if (n_ovd + n_ovk > 0) {
+            // overflowed digits: their region parts join their excess keys in the overflow list
+            std::vector<Chunk> od(n_ovd);
+            if (n_ovd) {
+                CK(cudaMemcpyAsync(od.data(), ovd, n_ovd * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+            }
+            uint64_t need = n_ovk;
+            for (const Chunk& x : od) need += x.n;
+            j->st.n_split_overflow += need;
+            uint64_t* all = ovf;
+            if (need > ovf_cap) {
+                all = ar.get<uint64_t>(need);
+                if (n_ovk) CK(cudaMemcpyAsync(all, ovf, n_ovk * 8, cudaMemcpyDeviceToDevice, s));
+            }
+            uint64_t o = n_ovk;
+            for (const Chunk& x : od) {
+                CK(cudaMemcpyAsync(all + o, (uint64_t*)lkeys + x.begin, (size_t)x.n * 8, cudaMemcpyDeviceToDevice, s));
+                o += x.n;
+            }
+            sort_rle(all, need, fl);
+            if (all != ovf) ar.release(all);
+        }
+        if (n_over + n_tovf > 0) {
+            std::vector<Chunk> ov(n_over + n_tovf);
+            if (n_over) CK(cudaMemcpyAsync(ov.data(), over, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+            if (n_tovf)
+                CK(cudaMemcpyAsync(ov.data() + n_over, tovf, n_tovf * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (const Chunk& x : ov) sort_rle((uint64_t*)lkeys + x.begin, x.n, fl);
+        }
+        j->launches += fl;
+        j->stage_end(fl);
+    }
+    ar.release(lkeys);
+    ar.release(ovf);
+    ar.release(rs.keys_alt);
+    ar.release(rs.tile_hist);
+    ar.release(rs.tile_off);
+    ar.release(rs.scan_temp);
+}
+
 // S5-S8 from the record stream in c (tmp_recs / tmp_sig, tmp_n slots) and the plan:
 // bins, then small and large bins counted into the survivor buffer.
 void count_phase(kmc_job* j, PlanCtx& c) {
@@ -813,6 +1018,22 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         }
         return r;
     };
+    // chunk capacity (keys): the per-chunk radix sort holds small_capacity(k) keys; the hash
+    // table holds 3/4 of its slots in DISTINCT keys, so its chunks may carry more keys by the
+    // distinct/window ratio measured on the small bins (x1.5 margin; a chunk that still
+    // overflows is counted by the fallback)
+    auto chunk_cap = [&]() -> int {
+        int kcap = small_capacity(k);
+        if (j->opt.count_path != 1) {
+            const uint64_t safe = (uint64_t)chunk_hash_cap(k) * 3 / 4;
+            const double r = distinct_ratio(1.5);
+            kcap = (int)std::min<uint64_t>(2ull * chunk_hash_cap(k), std::max<uint64_t>(safe, (uint64_t)(safe / r)));
+        }
+        if (j->opt.chunk_capacity) kcap = (int)std::min<uint32_t>(j->opt.chunk_capacity, 1u << 24);
+        // the per-chunk radix sort holds at most small_capacity(k) keys in shared memory
+        if (j->opt.count_path == 1) kcap = std::min(kcap, small_capacity(k));
+        return kcap;
+    };
     // ---- S6-S8 large bins
     bool large_done = false;
     if (large_windows > 0 && k <= 32 && j->opt.large_path == 3 && j->opt.count_path != 1) {
@@ -948,22 +1169,14 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         ar.release(rs.tile_hist);
         ar.release(rs.tile_off);
         ar.release(rs.scan_temp);
+    } else if (large_windows > 0 && k <= 32 && j->opt.large_path == 0 && j->opt.count_path != 1) {
+        const int kcap = chunk_cap();
+        j->st.chunk_capacity = (uint64_t)kcap;
+        large_split1(j, c, bins, large_ids, kcap, distinct_ratio);
     } else if (large_windows > 0) {
         // hashed split: per large bin, a D-bit digit -> digit ranges in HBM -> chunks <= cap
         // keys.  Large bins are processed in groups whose keys fit the device budget.
-        // chunk capacity (keys): the per-chunk radix sort holds small_capacity(k) keys; the
-        // hash table holds 3/4 of its slots in DISTINCT keys, so its chunks may carry more
-        // keys by the distinct/window ratio measured on the small bins (x1.5 margin; a
-        // chunk that still overflows is counted by the fallback)
-        int kcap = small_capacity(k);
-        if (j->opt.count_path != 1) {
-            const uint64_t safe = (uint64_t)chunk_hash_cap(k) * 3 / 4;
-            const double r = distinct_ratio(1.5);
-            kcap = (int)std::min<uint64_t>(2ull * chunk_hash_cap(k), std::max<uint64_t>(safe, (uint64_t)(safe / r)));
-        }
-        if (j->opt.chunk_capacity) kcap = (int)std::min<uint32_t>(j->opt.chunk_capacity, 1u << 24);
-        // the per-chunk radix sort holds at most small_capacity(k) keys in shared memory
-        if (j->opt.count_path == 1) kcap = std::min(kcap, small_capacity(k));
+        const int kcap = chunk_cap();
         j->st.chunk_capacity = (uint64_t)kcap;
         const int prec = msd_piece_records(k);
         // group budget in keys: the option, else everything at once if the key buffer can be

@@ -348,6 +348,23 @@ template <int NT, class T> __device__ __forceinline__ T block_excl_sum(T v, T* w
     return r;
 }
 
+// Exclusive block-wide sum with ONE barrier: wsum (NT/32 entries) must not be reused by
+// another call until every thread has returned from this one (alternate two buffers, or
+// separate the calls by a barrier).  All threads must call.
+template <int NT, class T> __device__ __forceinline__ T block_excl_sum1(T v, T* wsum, T* total) {
+    constexpr int NW = NT / 32;
+    static_assert(NW <= 32, "one warp holds the warp totals");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const T inc = warp_incl_sum(v);
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    const T wt = lane < NW ? wsum[lane] : T(0);
+    const T wi = warp_incl_sum(wt);
+    const T before = __shfl_sync(0xffffffffu, wi - wt, warp);
+    *total = __shfl_sync(0xffffffffu, wi, NW - 1);
+    return before + inc - v;
+}
+
 template <int NT, class T> __device__ __forceinline__ T block_sum(T v, T* wsum) {
     T tot;
     block_excl_sum<NT, T>(v, wsum, &tot);

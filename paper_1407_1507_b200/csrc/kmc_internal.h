@@ -219,6 +219,23 @@ cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_
 cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, int k, int canonical,
                                 void* keys, unsigned long long* gstats, cudaStream_t s);
 
+// One-pass sized split of the large bins (k_split1.cu, k <= 32): bin b gets nd digits
+// (digit = (hash(key) * nd) >> 32), digit d owns key slots [key_base + d * rc, + rc).
+constexpr int S1_DMAX = 256;
+struct S1Bin {
+    uint64_t key_base;
+    uint32_t nd, rc, dbase, pad;
+};
+int split1_piece_records(int k);
+// cur: per-digit key counts (zeroed; may exceed rc: overflow); ovf_ctr: keys beyond their
+// region (written to ovf while below ovf_cap)
+cudaError_t launch_split1(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const S1Bin* sbins, int k,
+                          int canonical, uint32_t* cur, uint64_t* keys, uint64_t* ovf, unsigned long long* ovf_ctr,
+                          uint64_t ovf_cap, int n_ctas, cudaStream_t s);
+// ctr[0] chunks, ctr[1] oversize (> hard_cap), ctr[2] overflowed digits (region parts in ovd)
+cudaError_t launch_split1_chunks(const S1Bin* sbins, uint64_t n_bins, const uint32_t* cur, uint32_t hard_cap,
+                                 Chunk* chunks, Chunk* over, Chunk* ovd, unsigned long long* ctr, cudaStream_t s);
+
 // S6-S8 of the large bins by thread-block clusters (k_cluster.cu, k <= 32): a cluster item is
 // (bin, round r of R) counted by all CTAs of a cluster with keys routed to their owner CTA
 // through distributed shared memory; a single item is a bin counted by one CTA's table.
