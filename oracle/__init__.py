@@ -78,6 +78,8 @@ def _load():
             lib.oracle_signatures.restype = None
             lib.oracle_superkmers.argtypes = [_P, _P, _U64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P, _U64]
             lib.oracle_superkmers.restype = _U64
+            lib.oracle_kx_count.argtypes = [_P, _P, _U64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+            lib.oracle_kx_count.restype = _U64
             _lib = lib
     return _lib
 
@@ -209,6 +211,14 @@ def superkmers(reads, offsets, k: int, p: int, rules: bool = True):
     return [(int(st[i]), int(nw[i]), int(sg[i])) for i in range(n)]
 
 
+def kx_count(reads, offsets, k: int, p: int, x: int, rules: bool = True) -> int:
+    """Number of (k,x)-mers the super-k-mers of the reads break into (C++; Table 7's sorted
+    fraction is this over the number of valid windows)."""
+    lib = _load()
+    reads, offsets = _arrays(reads, offsets)
+    return int(lib.oracle_kx_count(reads.ctypes.data, offsets.ctypes.data, offsets.shape[0] - 1, k, p, x, int(rules)))
+
+
 # ---------------------------------------------------------------------------
 # Pure-Python string oracle (second, independent implementation; small inputs)
 # ---------------------------------------------------------------------------
@@ -287,6 +297,98 @@ def signature_str(kmer: str, p: int, rules: bool = True) -> str | None:
         if best is None or c < best:
             best = c
     return best
+
+
+def orientation_str(kmer: str) -> int:
+    """0: the k-mer is its own canonical form (forward), 1: its reverse complement is
+    (reverse), 2: palindrome (both)."""
+    r = revcomp_str(kmer)
+    return 0 if kmer < r else (1 if kmer > r else 2)
+
+
+def kx_split_str(seq: str, k: int, x: int):
+    """(k,x)-mers of an ACGT string (Sec. 2.3; Fig. 2): the k-mers of
+    seq, left to right, are cut greedily into runs of at most x+1 consecutive k-mers of one
+    orientation; a forward run is stored as the stretch it covers, a reverse run as the
+    reverse complement of that stretch, so every k-mer inside a record is in canonical form.
+    A palindromic k-mer joins the run in progress and starts a run as forward (reading R-KX,
+    DESIGN.md).  Returns the records as strings of length k+x', 0 <= x' <= x."""
+    n = len(seq) - k + 1
+    out = []
+    i = 0
+    while i < n:
+        o = orientation_str(seq[i:i + k])
+        run = 0 if o == 2 else o
+        j = i + 1
+        while j < n and j - i <= x:
+            oj = orientation_str(seq[j:j + k])
+            if oj != run and oj != 2:
+                break
+            j += 1
+        stretch = seq[i:j - 1 + k]
+        out.append(stretch if run == 0 else revcomp_str(stretch))
+        i = j
+    return out
+
+
+def kx_merge_counts_str(records, k: int, x: int) -> dict:
+    """k-mer counts from (k,x)-mers by the paper's merge (Sec. 2.4, generalised from
+    x = 1 to x <= 3): the records are sorted per length class k+x'; for every class x' and
+    offset j <= x', the records agreeing on their first j symbols form one sorted sub-array
+    whose k-mers (symbols j .. j+k-1) come out in nondecreasing order (R_0, R_1 and R_A..R_T for
+    x = 1: 6 cursors; sum_{x'<=x} sum_{j<=x'} 4^j = 112 for x = 3).  All cursors are scanned in
+    parallel, the smallest k-mer taken each step; equal k-mers accumulate one count."""
+    classes = {}
+    for r in records:
+        classes.setdefault(len(r) - k, []).append(r)
+    cursors = []
+    for xp, recs in classes.items():
+        recs.sort()
+        for j in range(xp + 1):
+            groups = {}
+            for r in recs:
+                groups.setdefault(r[:j], []).append(r[j:j + k])
+            for pre in sorted(groups):
+                cursors.append(groups[pre])  # each nondecreasing by construction
+    for c in cursors:
+        assert all(c[i] <= c[i + 1] for i in range(len(c) - 1)), "a sub-array is not sorted"
+    pos = [0] * len(cursors)
+    out = {}
+    last = None
+    while True:
+        best = None
+        for ci, c in enumerate(cursors):
+            if pos[ci] < len(c) and (best is None or c[pos[ci]] < cursors[best][pos[best]]):
+                best = ci
+        if best is None:
+            break
+        kmer = cursors[best][pos[best]]
+        pos[best] += 1
+        if kmer != last:
+            out[kmer] = 0
+            last = kmer
+        out[kmer] += 1
+    return out, len(cursors)
+
+
+def count_kx_str(reads, k: int, p: int, x: int, cutoff_min: int = 1, cutoff_max: int = 10**9,
+                 rules: bool = True) -> dict:
+    """Counting the paper's way with (k,x)-mers (small inputs): every read segment is split into
+    super-k-mers (split_str), super-k-mers are binned by signature, and every bin's (k,x)-mers
+    are merged (kx_merge_counts_str).  Same result as count_strings for every x."""
+    bins = {}
+    for r in reads:
+        r = r.decode() if isinstance(r, (bytes, bytearray)) else r
+        for seg in segments(r):
+            for sub, sig in split_str(seg, k, p, rules):
+                bins.setdefault(sig, []).extend(kx_split_str(sub, k, x))
+    total = {}
+    for recs in bins.values():
+        counts, _ = kx_merge_counts_str(recs, k, x)
+        for km, c in counts.items():
+            total[km] = total.get(km, 0) + c
+    ci = max(1, cutoff_min)
+    return {km: c for km, c in total.items() if ci <= c <= cutoff_max}
 
 
 def split_str(seg: str, k: int, p: int, rules: bool = True):

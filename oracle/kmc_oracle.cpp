@@ -452,4 +452,42 @@ uint64_t oracle_superkmers(const uint8_t* reads, const uint64_t* offsets, uint64
     return n;
 }
 
+/* Number of (k,x)-mers (Sec. 2.3) the super-k-mers of the reads break into: per
+ * super-k-mer (as oracle_superkmers), the k-mers left to right are cut greedily into runs of at
+ * most x+1 consecutive k-mers of one orientation (forward: f < r; reverse: f > r; a palindrome
+ * f == r joins the run in progress and starts a run as forward -- reading R-KX).  With the
+ * number of valid windows this is Table 7's "sorted fraction". */
+uint64_t oracle_kx_count(const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads, int k, int p, int x,
+                         int rules) {
+    uint64_t n_rec = 0;
+    for (uint64_t i = 0; i < n_reads; ++i) {
+        uint64_t prev_sig = ~0ull;
+        bool in_run = false;  /* inside a super-k-mer */
+        int run_o = 0, run_len = 0;
+        for (uint64_t s = offsets[i]; s + k <= offsets[i + 1]; ++s) {
+            const uint8_t* w = reads + (s - offsets[0]);
+            if (!window_valid(w, k)) { in_run = false; continue; }
+            const uint64_t sg = window_signature(w, k, p, rules);
+            const u128 f = forward_value(w, k), r = revcomp_value(w, k);
+            const int o = f < r ? 0 : (f > r ? 1 : 2);
+            if (!(in_run && sg == prev_sig)) {  /* a new super-k-mer: a new (k,x)-mer */
+                in_run = true;
+                prev_sig = sg;
+                run_o = (o == 2) ? 0 : o;
+                run_len = 1;
+                ++n_rec;
+                continue;
+            }
+            if (run_len <= x && (o == run_o || o == 2)) {
+                ++run_len;
+            } else {
+                run_o = (o == 2) ? 0 : o;
+                run_len = 1;
+                ++n_rec;
+            }
+        }
+    }
+    return n_rec;
+}
+
 }  /* extern "C" */
