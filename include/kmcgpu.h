@@ -126,6 +126,9 @@ typedef struct {
     uint64_t cluster_ctas;     /* CTAs the large-bin cluster kernel ran with */
     uint64_t n_split_overflow; /* large-bin keys whose digit overfilled its region in the one-pass
                                   split (counted by the device radix-sort fallback) */
+    uint64_t n_kxmers;         /* (k,x)-mers sorted (kx > 0): Table 7's "sorted fraction" is
+                                  n_kxmers / kx_windows */
+    uint64_t kx_windows;       /* windows of the bins counted through (k,x)-mers (the small bins) */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;
@@ -171,6 +174,11 @@ typedef struct {
                                   tables only -- bins above one table spill; testing) */
     uint32_t table_keys;       /* large_path 3, testing: distinct keys one CTA's table is planned
                                   for (0 = 3/4 of its slots); small values force many rounds */
+    uint32_t kx;               /* x of (k,x)-mers (Sec. 2.3), 0..3: the small bins are
+                                  counted the paper's way -- records split into (k,x)-mers, sorted,
+                                  the sorted sub-arrays merged; large bins keep plain
+                                  k-mers (their split routes single k-mers by hash).  Needs
+                                  k + x <= 31 and canonical counting.  Same output for every x. */
     uint32_t spill_keys;       /* large_path 3, testing: spill list capacity (0 = auto); a spill
                                   beyond it reruns the large bins on the split path */
 } kmc_options;

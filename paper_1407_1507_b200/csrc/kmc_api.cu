@@ -541,6 +541,7 @@ void plan_phase(kmc_job* j, PlanCtx& c) {
     const int RW = record_words(k);
     int cap = small_capacity(k);
     if (j->opt.small_bin_capacity) cap = std::min<int>(cap, (int)j->opt.small_bin_capacity);
+    if (j->opt.kx) cap = std::min(cap, kx_capacity());  // the (k,x)-mer kernel's bins
     if (j->opt.force_large) cap = 0;
     c.cap = cap;
     PlanArgs& pa = c.pa;
@@ -991,14 +992,18 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         sa.surv_counts = j->surv_counts;
         sa.gstats = gstats;
         j->stage_begin(KMC_STAGE_SMALL_BINS);
-        CK(launch_small_bins(sa, n_first, s));
+        // (k,x)-mers (kx > 0): the paper's sorter on every small bin (k_kxmer.cu)
+        auto small_launch = [&](uint64_t n) {
+            return j->opt.kx ? launch_small_kx(sa, n, (int)j->opt.kx, s) : launch_small_bins(sa, n, s);
+        };
+        CK(small_launch(n_first));
         int sl = 1;
         if (n_first < small.size()) {
             CK(cudaMemcpyAsync(&hs[64], gstats + GS_UNIQUE, 8, cudaMemcpyDeviceToHost, s));
             CK(cudaEventCreateWithFlags(&ev_sample, cudaEventDisableTiming));
             CK(cudaEventRecord(ev_sample, s));
             sa.small_list = d_small + n_first;
-            CK(launch_small_bins(sa, small.size() - n_first, s));
+            CK(small_launch(small.size() - n_first));
             ++sl;
         }
         j->launches += sl;
@@ -1378,6 +1383,8 @@ void count_phase(kmc_job* j, PlanCtx& c) {
     j->st.n_below_min = hs[16 + GS_BELOW];
     j->st.n_above_max = hs[16 + GS_ABOVE];
     j->st.n_small_sorted = hs[16 + GS_SMALL_SORTED];
+    j->st.n_kxmers = hs[16 + GS_KX];
+    j->st.kx_windows = hs[16 + GS_KX_WIN];
     if (j->opt.large_path == 1 && hs[16 + GS_LARGE_KEYS] != large_windows) {
         set_err("large-bin expansion produced %llu keys, plan says %llu", (unsigned long long)hs[16 + GS_LARGE_KEYS],
                 (unsigned long long)large_windows);
@@ -1520,6 +1527,11 @@ kmc_status kmc_count_begin(const uint8_t* reads, const uint64_t* read_offsets, u
         // the all-T k-mer is the all-ones key, the empty-slot / padding marker (never a
         // canonical key, but a forward one)
         set_err("non_canonical needs k != 32 and k != 64 (k=%d)", k);
+        delete j;
+        return KMC_ERR_INVALID_ARG;
+    }
+    if (j->opt.kx && (j->opt.kx > 3 || k + (int)j->opt.kx > 31 || j->opt.non_canonical)) {
+        set_err("kx=%u needs kx <= 3, k + kx <= 31 and canonical counting (k=%d)", j->opt.kx, k);
         delete j;
         return KMC_ERR_INVALID_ARG;
     }

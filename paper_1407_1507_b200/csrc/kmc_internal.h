@@ -22,6 +22,8 @@ enum {
     GS_TMP_RECS = 10,   // slots reserved in the temporary record stream by pass 1
     GS_MAX_SIG = 11,    // windows of the most frequent signature
     GS_SMALL_SORTED = 12,  // small bins whose hash table overflowed (sorted instead)
+    GS_KX = 13,            // (k,x)-mers sorted (kx path)
+    GS_KX_WIN = 14,        // windows of the bins counted through (k,x)-mers
     GS_N = 16
 };
 
@@ -145,6 +147,10 @@ struct SmallArgs {
     unsigned long long* gstats;
 };
 int small_capacity(int k);  // max windows per small bin for this key width
+// (k,x)-mer path of the small bins (k_kxmer.cu): x in 1..3, k + x <= 31, canonical only;
+// bins of at most kx_capacity() windows
+int kx_capacity();
+cudaError_t launch_small_kx(const SmallArgs& a, uint64_t n_small, int x, cudaStream_t s);
 cudaError_t launch_small_bins(const SmallArgs& a, uint64_t n_small, cudaStream_t s);
 
 struct Piece {

@@ -486,3 +486,48 @@ def test_random_sweep(gpu, seed):
     assert keys.shape[0] == ref.keys.shape[0], (seed, k, p, opts)
     assert np.array_equal(keys, ref.keys) and np.array_equal(counts, ref.counts), (seed, k, p, opts)
     assert st["n_windows"] == ref.n_windows and st["n_unique"] == ref.n_unique
+
+
+# ---------------------------------------------------------------- f1: (k,x)-mers
+
+@pytest.mark.parametrize("x", [1, 2, 3])
+@pytest.mark.parametrize("name,scale,k", [("C1", 0.05, None), ("C2", 0.003, None), ("C4", 0.0005, None),
+                                          ("C5", 0.002, 27), ("C1", 0.02, 12), ("C1", 0.02, 28)])
+def test_kxmer_parity(gpu, x, name, scale, k):
+    """Small bins counted through (k,x)-mers -- records split into orientation runs, sorted,
+    the sorted sub-arrays merged -- give the plain counts for every x,
+    bit for bit against the oracle."""
+    w = synth.make(name, scale=scale) if k is None else synth.make(name, scale=scale, k=k)
+    st = assert_same(gpu, w, kx=x)
+    assert st["kx_windows"] > 0 and 0 < st["n_kxmers"] <= st["kx_windows"]
+
+
+def test_kxmer_edge_reads(gpu):
+    # palindromes (even k), homopolymers, (AT)n, N runs, lowercase, empty and short reads
+    seqs = ["A" * 300, "AT" * 120, "ACGT" * 60, "N" * 50, "", "ACG", "CA" * 100, "acgtTGCA" * 30] * 20
+    seqs += [s.decode() for s in synth.random_reads(3, 400, 20, 250, n_frac=0.02, lower_frac=0.05)]
+    for k, p, x in ((28, 7, 3), (16, 5, 2), (20, 4, 1), (4, 3, 3), (1, 1, 2)):
+        assert_same(gpu, synth.from_strings(seqs, k, p, 1), kx=x)
+
+
+def test_kxmer_sorted_fraction(gpu):
+    """Table 7: at x = 3 about half the k-mers remain to be sorted (0.49 printed
+    for G. gallus, k = 28).  The GPU's records are super-k-mer pieces (cut at segment edges and
+    every maxw windows), so its fraction sits just above the oracle's super-k-mer figure."""
+    w = synth.make("C4", scale=0.0005)
+    fr = {}
+    for x in (1, 2, 3):
+        _, _, st = gpu_count(gpu, w, kx=x, small_bin_capacity=4096)
+        fr[x] = st["n_kxmers"] / st["kx_windows"]
+    ref3 = oracle.kx_count(w.reads, w.offsets, w.k, w.p, 3) / oracle.n_windows(w.reads, w.offsets, w.k)
+    assert fr[1] > fr[2] > fr[3]
+    assert 0.40 <= fr[3] <= 0.60 and ref3 <= fr[3] <= ref3 + 0.05, (fr, ref3)
+
+
+def test_kxmer_invalid(gpu):
+    w = synth.make("C1", scale=0.001)
+    r, o = to_dev(w)
+    for k, x, canon in ((25, 4, True), (30, 2, True), (25, 1, False)):
+        with pytest.raises(gpu.KmcError) as ei:
+            gpu.count(r, o, k, 7, 1, 10**9, kx=x, canonical=canon)
+        assert ei.value.status == gpu.KMC_ERR_INVALID_ARG
