@@ -5,7 +5,7 @@
 // counting chunk each (every copy of a k-mer shares its digit, so a digit is counted on its
 // own; S9 orders the survivors globally).  Round 1 counted every (piece, digit) in a first
 // pass, scanned the counts and re-expanded the bins in a second pass.  Here the digit regions
-// are SIZED from the bin's window count instead: a bin of W windows gets nd = W / (0.75 x chunk
+// are SIZED from the bin's window count instead: a bin of W windows gets nd = W / (chunk
 // capacity) digits, digit = (h(key) x nd) >> 32, and each digit a region of rc ~ 1.25 W / nd
 // key slots (hashed digits are near-uniform, but a k-mer of multiplicity m moves m keys at
 // once, so repeat families can still overfill a digit).  One kernel per piece of 512 records (TMA, double-buffered):

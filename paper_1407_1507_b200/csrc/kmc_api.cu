@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -634,9 +635,11 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
     const std::vector<uint64_t>& bw = c.bw;
     const std::vector<uint64_t>& bn = c.bn;
     const std::vector<uint64_t>& bo = c.bo;
-    // digit target 0.75 kcap; regions 1.25x the mean + 256 (hashed digits are near-uniform,
-    // but a k-mer of multiplicity m moves m keys at once: repeat families skew them)
-    const double target = std::max(1.0, 0.75 * kcap);
+    // digit target = kcap keys; regions 1.25x the mean + 256 (hashed digits are near-uniform,
+    // but a k-mer of multiplicity m moves m keys at once: repeat families skew them).  C4
+    // (tools/stage_run.py, target / kcap 0.6 .. 1.1): 62.4, 60.8, 60.1, 60.0, 59.9 ms/step,
+    // overflow 6.0 M .. 0.4 M keys; bigger digits absorb pile-ups and need fewer reservations.
+    const double target = std::max(1.0, (double)kcap);
     const uint32_t rpp = (uint32_t)split1_piece_records(k);
     const size_t nl = large_ids.size();
     std::vector<uint32_t> nd(nl), rc(nl);
