@@ -46,7 +46,7 @@ def compact_bin_bytes(st: dict, k: int) -> float:
     return st["n_superkmers"] * 1.0 + 2.0 * (st["n_windows"] + st["n_superkmers"] * (k - 1)) / 8.0
 
 
-def stage_bytes(st: dict, n_reads: int, k: int, split_ran: bool = True) -> dict:
+def stage_bytes(st: dict, n_reads: int, k: int, ran: set = frozenset({"large_split"})) -> dict:
     """Algorithmic HBM bytes per stage and call, SURVEY 8(d):
     B_alg = input (ASCII + offsets) + 2 x compact bins (written once, read once) + output.
     Each byte of B_alg is charged to the stage that must move it: pass 1 reads the input and
@@ -59,18 +59,22 @@ def stage_bytes(st: dict, n_reads: int, k: int, split_ran: bool = True) -> dict:
     bins = compact_bin_bytes(st, k)
     lw = st["large_windows"]
     lfrac = lw / st["n_windows"] if st["n_windows"] else 0.0
-    return {
+    # the large bins' records are read by the first large stage that ran: the count pass of the
+    # two-pass split (large_path 2), else the one-pass split (default), else the cluster kernel
+    large_reader = next((x for x in ("large_split", "large_scatter", "large_chunks") if x in ran), "large_split")
+    out = {
         "signature": nb + off + bins,        # input read, bins written once
         "scatter": 0.0,                      # implementation pass (record stream -> bins)
         "small_bins": (1 - lfrac) * bins,    # bins read once
-        # large bins: read once by the split (large_path 2) or by the cluster kernel (default)
-        "large_split": lfrac * bins if split_ran else 0.0,
-        "large_scatter": 0.0,                # implementation pass (key split)
-        "large_chunks": 0.0 if split_ran else lfrac * bins,
+        "large_split": 0.0,
+        "large_scatter": 0.0,
+        "large_chunks": 0.0,                 # implementation pass (re-read of the split keys)
         "large_fallback": 0.0,
         "order": st["n_out"] * (ksz + 4),    # output written once
         "output": 0.0,
     }
+    out[large_reader] = lfrac * bins         # large bins read once
+    return out
 
 
 def b_alg(st: dict, n_reads: int, k: int) -> float:
@@ -335,7 +339,7 @@ def main():
 
     # ---- roofline of the dominant stage (SURVEY 8(d) bytes)
     peaks = measured_peaks()
-    sb = stage_bytes(last, w.n_reads, k, split_ran=stage_ms.get("large_split", 0.0) > 0)
+    sb = stage_bytes(last, w.n_reads, k, ran={s_ for s_, v in stage_ms.items() if v > 0})
     per_stage = {}
     for s_, tot in stage_ms.items():
         if tot <= 0:
@@ -345,7 +349,8 @@ def main():
         per_stage[s_] = {"ms": round(per_step, 3), "share": round(per_step / ms, 4),
                          "launches": stage_launches.get(s_, 0) // args.steps,
                          "alg_bytes": int(bytes_),
-                         "gbs": round(bytes_ / (per_step / 1e3) / 1e9, 1) if bytes_ else None}
+                         "gbs": round(bytes_ / (per_step / 1e3) / 1e9, 1) if bytes_ else None,
+                         "frac": round(bytes_ / (per_step / 1e3) / 1e9 / peaks["hbm_gbs"], 4) if bytes_ else 0.0}
     dom = max(per_stage, key=lambda s_: per_stage[s_]["ms"])
     dom_ms = per_stage[dom]["ms"]
     achieved = sb.get(dom, 0.0) / (dom_ms / 1e3) / 1e9

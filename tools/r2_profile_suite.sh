@@ -1,0 +1,13 @@
+# Round-2 evidence on one B200: bench line, ncu launch list of the bench command, full captures
+set -x
+OUT=${OUT:-gpurun_out/r2p}
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc $?"
+timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum \
+  --clock-control none --csv --log-file $OUT/launches.csv \
+  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-sort-path > $OUT/ncu_bench.log 2>&1; echo "ncu list rc $?"
+for kr in k_sig k_split1 k_chunk_hash; do
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:$kr -c 1 -f -o $OUT/full_$kr \
+    python tools/profile_run.py C4 1.0 1 > $OUT/full_$kr.log 2>&1; echo "ncu $kr rc $?"
+done
