@@ -9,7 +9,7 @@
 // capacity) digits, digit = (h(key) x nd) >> 32, and each digit a region of rc ~ 1.25 W / nd
 // key slots (hashed digits are near-uniform, but a k-mer of multiplicity m moves m keys at
 // once, so repeat families can still overfill a digit).  One kernel per piece of 512 records (TMA, double-buffered):
-//   A  expand every window (one lane per unit of <= 4 windows: one 64-bit field holds the
+//   A  expand every window (one lane per unit of <= 5 windows: one 64-bit field holds the
 //      unit's symbols; keys min(fwd, rc)) and histogram the digits in SMEM;
 //   R  reserve each digit's run in its region with one global atomic per (piece, digit);
 //   B  expand again and place every key in a shared-memory stage grouped by digit (each run
@@ -32,6 +32,7 @@ constexpr int S1_REC = 512;       // records per piece at most
 constexpr int S1_UMAX = 7680;     // units per piece (umap entries)
 constexpr int S1_STAGE = 8192;    // keys staged per piece (+ one spare slot per digit)
 constexpr int S1_RBW = S1_REC * 4 + 8;
+constexpr int S1_UNIT = 5;        // windows per expansion unit at most (k + unit - 1 <= 32 symbols)
 
 __device__ __forceinline__ uint32_t s1_digit(uint64_t key, uint32_t nd) {
     const uint32_t h = (((uint32_t)(key >> 32) * 0x85EBCA6Bu) ^ (uint32_t)key) * 0x9E3779B1u;
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         uint32_t n = 0, nu = 0;
         if ((uint32_t)tid < pc.nrec) {
             n = rec_nwin(Rp + tid * 4);
-            nu = U == 4 ? (n + 3) >> 2 : U == 2 ? (n + 1) >> 1 : U == 1 ? n : (n + 2) / 3;
+            nu = (n + U - 1) / U;
         }
         if (bulk_pending) {  // the previous piece's stage has been read by its bulk copies
             bulk_wait_read();
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
             const uint64_t g = bits64_be(Rp + l * 4, 8 + 2 * first);
             const uint64_t rg = rev2_64(~g);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < S1_UNIT; ++t) {
                 if (t < cnt) {
                     const uint64_t f = (g << (2 * t)) >> (64 - 2 * k);
                     const uint64_t rc = (rg << (64 - 2 * t - 2 * k)) >> (64 - 2 * k);
@@ -227,7 +228,7 @@ __global__ void k_split1_chunks(const S1Bin* __restrict__ sbins, const uint32_t*
 }  // namespace
 
 int split1_piece_records(int k) {
-    const int U = k + 3 <= 32 ? 4 : 33 - k;
+    const int U = std::min(S1_UNIT, 33 - k);
     const int upr = (record_max_windows(k) + U - 1) / U;
     return std::min(S1_REC, S1_UMAX / upr);
 }
@@ -237,7 +238,7 @@ cudaError_t launch_split1(const uint32_t* bins, const Piece* pieces, uint64_t n_
                           uint64_t ovf_cap, int n_ctas, cudaStream_t s) {
     if (n_pieces == 0) return cudaSuccess;
     if (k > 32) return cudaErrorInvalidValue;
-    const int unit = k + 3 <= 32 ? 4 : 33 - k;
+    const int unit = std::min(S1_UNIT, 33 - k);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(n_pieces, (uint64_t)n_ctas));
     cudaError_t e;
     if (canonical) {
