@@ -9,8 +9,9 @@ full kmc_count call (S1-S9) over the whole read set, inputs resident in HBM.
 
 N > 1 runs under torchrun, one rank per GPU: rank r holds its own read sample of the same
 genome (C4 reads each: weak scaling) and the ranks count the union with the sharded path
-(kmc_shard_*): NCCL all-reduce of the signature histograms, all-to-all of the
-super-k-mer records by bin owner, each rank counting and outputting its own bins.  The time
+(kmc_shard_*): NCCL all-reduce of the signature histograms, the partition pass
+writing every super-k-mer record into its bin owner's receive buffer over peer memory (the
+fused exchange), each rank counting and outputting its own bins.  The time
 is the max over ranks.
 ``--impl reference`` times the CPU oracle (oracle/) on the host cores, rank 0 only.
 Prints ONE JSON line (rank 0).
@@ -422,7 +423,8 @@ def main():
         "config": {"workload": f"{args.config}: {cfg.desc}", "scale": args.scale, "n_reads": w.n_reads,
                    "n_bases": n_bases, "k": k, "p": p, "cutoff_min": ci, "cutoff_max": cx,
                    "parallelism": (f"sharded x{world}: reads split by rank, NCCL all-reduce of the signature "
-                                   f"histogram + all-to-all of super-k-mer records by bin owner")
+                                   f"histogram; super-k-mer records written by the partition pass straight "
+                                   f"into the owner rank's receive buffers over NVLink (CUDA IPC peer memory)")
                    if world > 1 else "1 GPU",
                    "count_path": ["smem_hash", "smem_radix_sort"][args.count_path],
                    "l2": "inputs (4 GB) larger than L2 (126 MB); no flush needed"},

@@ -254,6 +254,33 @@ kmc_status kmc_shard_partition(kmc_job* job, const uint64_t* global_hist_w, cons
                                uint64_t* send_counts);
 kmc_status kmc_shard_count(kmc_job* job, const uint32_t* recv_records, const uint32_t* recv_sigs,
                            uint64_t n_recv, uint64_t* n_out);
+/* ---- The same exchange fused into the partition pass over peer memory (
+ * DESIGN.md 8).  Instead of grouping records into send buffers for an all-to-all, the
+ * partition kernel writes every record straight into its owner rank's receive buffer, mapped
+ * from the peer through CUDA IPC (NVLink / NVSwitch between the GPUs of one node), so the
+ * transfer overlaps the partition tile by tile and no separate collective moves records:
+ *   3a. kmc_shard_plan(job, global_hist_w, global_hist_r, world, rank, send_counts): the plan
+ *       and bin owners (as kmc_shard_partition) and this rank's record count per destination
+ *       (send_counts [world], host); no record moves;
+ *   3b. the caller all-gathers send_counts into C[src][dst] (world x world);
+ *   3c. kmc_shard_recv_alloc(job, n_recv, handles): this rank's receive buffers for
+ *       n_recv = sum_src C[src][rank] records (records, then signature tags: two cudaMalloc
+ *       allocations) and their CUDA IPC handles, 2 x 64 bytes into handles;
+ *   3d. the caller all-gathers the handles (world x 128 bytes, rank order);
+ *   3e. kmc_shard_send_peers(job, all_handles, dst_offsets): dst_offsets[d] = first slot of
+ *       this rank's records in rank d's buffers = sum_{src < rank} C[src][d]; maps every
+ *       peer's buffers, writes every record into its owner's buffers and waits for the
+ *       writes; the mappings are closed before returning;
+ *   3f. the caller barriers (every rank's writes are then complete);
+ *   5'. kmc_shard_count_recv(job, n_out): counts this rank's receive buffers (S5-S8).
+ * All ranks must be processes on GPUs of one node that can map each other's memory (the same
+ * GPU included).  Errors: KMC_ERR_CUDA (e.g. cudaIpcOpenMemHandle refused), INVALID_ARG. */
+kmc_status kmc_shard_plan(kmc_job* job, const uint64_t* global_hist_w, const uint64_t* global_hist_r, int world,
+                          int rank, uint64_t* send_counts);
+kmc_status kmc_shard_recv_alloc(kmc_job* job, uint64_t n_recv, uint8_t* handles /* 128 bytes */);
+kmc_status kmc_shard_send_peers(kmc_job* job, const uint8_t* all_handles /* world x 128 bytes */,
+                                const uint64_t* dst_offsets /* [world] */);
+kmc_status kmc_shard_count_recv(kmc_job* job, uint64_t* n_out);
 /* Bin -> rank map of the sharded plan (host only, no GPU): contiguous bins, each rank taking
  * about total/world windows; owner[b] = the rank whose share holds the bin's midpoint. */
 void kmc_shard_owners(const uint64_t* bin_windows, uint64_t n_bins, int world, uint32_t* owner);

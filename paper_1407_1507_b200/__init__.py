@@ -107,6 +107,14 @@ def load():
         lib.kmc_shard_partition.restype = I
         lib.kmc_shard_count.argtypes = [P, P, P, U64, ctypes.POINTER(U64)]
         lib.kmc_shard_count.restype = I
+        lib.kmc_shard_plan.argtypes = [P, P, P, I, I, P]
+        lib.kmc_shard_plan.restype = I
+        lib.kmc_shard_recv_alloc.argtypes = [P, U64, P]
+        lib.kmc_shard_recv_alloc.restype = I
+        lib.kmc_shard_send_peers.argtypes = [P, P, P]
+        lib.kmc_shard_send_peers.restype = I
+        lib.kmc_shard_count_recv.argtypes = [P, ctypes.POINTER(U64)]
+        lib.kmc_shard_count_recv.restype = I
         lib.kmc_shard_owners.argtypes = [P, U64, I, P]
         lib.kmc_shard_owners.restype = None
         lib.kmc_record_words.argtypes = [I]
@@ -283,6 +291,32 @@ class _Shard:
                                             _ptr(sigs), counts))
         return recs, sigs, [int(c) for c in counts]
 
+    # ---- fused exchange over peer memory (kmc_shard_plan / recv_alloc / send_peers / count_recv)
+    def plan(self, global_w, global_r, world: int, rank: int):
+        """The shared plan and this rank's record count per destination rank (no record moves)."""
+        counts = (ctypes.c_uint64 * world)()
+        _check(self.lib.kmc_shard_plan(self.job, _ptr(global_w), _ptr(global_r), world, rank, counts))
+        return [int(c) for c in counts]
+
+    def recv_alloc(self, n_recv: int) -> bytes:
+        """This rank's receive buffers; returns their CUDA IPC handles (128 bytes)."""
+        h = (ctypes.c_uint8 * 128)()
+        _check(self.lib.kmc_shard_recv_alloc(self.job, int(n_recv), h))
+        return bytes(h)
+
+    def send_peers(self, all_handles: bytes, dst_offsets):
+        """The partition pass writing every record into its owner's receive buffers."""
+        world = len(dst_offsets)
+        hb = (ctypes.c_uint8 * len(all_handles)).from_buffer_copy(all_handles)
+        offs = (ctypes.c_uint64 * world)(*[int(x) for x in dst_offsets])
+        _check(self.lib.kmc_shard_send_peers(self.job, hb, offs))
+
+    def count_recv(self, out_device=None) -> Result:
+        n_out = ctypes.c_uint64()
+        _check(self.lib.kmc_shard_count_recv(self.job, ctypes.byref(n_out)))
+        job, self.job = self.job, None
+        return _finish(self.lib, job, int(n_out.value), self.k, out_device or self.dev)
+
     def count(self, recv_recs, recv_sigs, out_device=None) -> Result:
         n_out = ctypes.c_uint64()
         _check(self.lib.kmc_shard_count(self.job, _ptr(recv_recs), _ptr(recv_sigs), int(recv_sigs.shape[0]),
@@ -318,11 +352,31 @@ def exchange(recs, sigs, send_counts, group=None):
     return rr, rs, recv_counts
 
 
+def exchange_p2p(sh, world: int, rank: int, group=None):
+    """Fused partition + exchange over peer memory: the record counts per
+    (source, destination) are all-gathered, every rank allocates its receive buffers and
+    all-gathers their CUDA IPC handles, then every rank's partition pass writes its records
+    straight into the owners' buffers (NVLink / NVSwitch between the GPUs of one node) and a
+    barrier ends the exchange.  Only counts and handles travel through torch.distributed."""
+    import torch.distributed as dist
+    counts = sh.plan(sh.hist_w, sh.hist_r, world, rank)
+    allc = [None] * world
+    dist.all_gather_object(allc, counts, group=group)
+    n_recv = sum(allc[s_][rank] for s_ in range(world))
+    handles = [None] * world
+    dist.all_gather_object(handles, sh.recv_alloc(n_recv), group=group)
+    dst_offsets = [sum(allc[s_][d] for s_ in range(rank)) for d in range(world)]
+    sh.send_peers(b"".join(handles), dst_offsets)
+    dist.barrier(group=group)  # every rank's writes into this rank's buffers are complete
+
+
 def count_sharded(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *,
-                  group=None, stream=None, out_device=None, **opts) -> Result:
+                  group=None, stream=None, out_device=None, exchange_mode: str = "p2p", **opts) -> Result:
     """Sharded count over the ranks of ``group`` (torch.distributed): this rank holds a slice
-    of the reads; histograms are all-reduced and super-k-mer records exchanged all-to-all
-    (SURVEY 8(e)); returns this rank's share of the (k-mer, count) pairs -- disjoint from the
+    of the reads; histograms are all-reduced and super-k-mer records exchanged:
+    ``exchange_mode="p2p"`` (default, ranks on one node) fuses the exchange into the
+    partition pass over peer memory, ``"collective"`` groups the records into send buffers for
+    an all-to-all.  Returns this rank's share of the (k-mer, count) pairs -- disjoint from the
     other ranks', ascending; the union is the count of all slices together."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -338,6 +392,9 @@ def count_sharded(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_ma
         else:
             dist.all_reduce(sh.hist_w, group=group)
             dist.all_reduce(sh.hist_r, group=group)
+    if world > 1 and exchange_mode == "p2p" and sh.hist_w.is_cuda:
+        exchange_p2p(sh, world, rank, group)
+        return sh.count_recv(out_device=out_device)
     recs, sigs, counts = sh.partition(sh.hist_w, sh.hist_r, world, rank)
     if world > 1:
         recs, sigs, _ = exchange(recs, sigs, counts, group)

@@ -524,7 +524,8 @@ __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restric
                                                        const uint64_t* __restrict__ n_tiles, int shift, int D,
                                                        unsigned long long* __restrict__ cursor,
                                                        uint32_t* __restrict__ out_recs, uint32_t* __restrict__ out_ids,
-                                                       int out_orig_ids) {
+                                                       int out_orig_ids, uint32_t* const* __restrict__ peer_recs,
+                                                       uint32_t* const* __restrict__ peer_ids) {
     constexpr int TI = RecTile<RW>::v, IPT = TI / RS_NT;
     using V = uint4;
     extern __shared__ __align__(16) uint8_t rsm[];
@@ -598,10 +599,14 @@ __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restric
     for (uint32_t i = threadIdx.x; i < tot; i += RS_NT) {
         const uint32_t d = sd[i];
         const uint64_t o = gb[d] + (i - lh[d]);
-        V* dst = reinterpret_cast<V*>(out_recs + o * (uint64_t)RW);
+        // peer mode (fused exchange): digit d is a destination rank, its run goes straight into
+        // that rank's receive buffers (mapped peer memory), cursor d counting in them
+        uint32_t* orec = peer_recs ? peer_recs[d] : out_recs;
+        uint32_t* oid = peer_recs ? peer_ids[d] : out_ids;
+        V* dst = reinterpret_cast<V*>(orec + o * (uint64_t)RW);
         dst[0] = srec[i * (RW / 4)];
         if (RW == 8) dst[1] = srec[i * 2 + 1];
-        if (out_ids) out_ids[o] = sid[i];
+        if (oid) oid[o] = sid[i];
     }
 }
 
@@ -686,19 +691,22 @@ size_t rec_tile_items(int k) { return record_words(k) == 4 ? RecTile<4>::v : Rec
 cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* in_ids, const uint32_t* sig2bin,
                                const RecTile2* tiles, uint64_t max_tiles, const uint64_t* n_tiles_dev, int shift,
                                int D, unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids,
-                               cudaStream_t s, int out_orig_ids) {
+                               cudaStream_t s, int out_orig_ids, uint32_t* const* peer_recs,
+                               uint32_t* const* peer_ids) {
     if (max_tiles == 0) return cudaSuccess;
     cudaError_t e;
     if (record_words(k) == 4) {
         const int sm = (int)rec_scatter_smem<4>();
         if ((e = cudaFuncSetAttribute(k_rec_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
         k_rec_scatter<4><<<(unsigned)max_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, n_tiles_dev, shift, D,
-                                                               cursor, out_recs, out_ids, out_orig_ids);
+                                                               cursor, out_recs, out_ids, out_orig_ids, peer_recs,
+                                                               peer_ids);
     } else {
         const int sm = (int)rec_scatter_smem<8>();
         if ((e = cudaFuncSetAttribute(k_rec_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
         k_rec_scatter<8><<<(unsigned)max_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, n_tiles_dev, shift, D,
-                                                               cursor, out_recs, out_ids, out_orig_ids);
+                                                               cursor, out_recs, out_ids, out_orig_ids, peer_recs,
+                                                               peer_ids);
     }
     return cudaGetLastError();
 }

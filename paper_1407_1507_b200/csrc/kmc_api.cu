@@ -259,6 +259,12 @@ struct kmc_job {
     cudaEvent_t cur_a = nullptr;
     unsigned long long* host_small = nullptr;  // pinned readback area
     cudaStream_t cs = nullptr;                 // copy stream for streamed input batches
+    // sharded, fused exchange: this rank's receive buffers (plain cudaMalloc: IPC-mappable)
+    uint32_t* sig2owner = nullptr;
+    std::vector<uint64_t> send_counts;
+    uint32_t* recv_recs = nullptr;
+    uint32_t* recv_sigs = nullptr;
+    uint64_t n_recv = 0;
     cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
 
     void make_copy_stream() {
@@ -314,6 +320,8 @@ struct kmc_job {
         }
         arena.release_all();
         pin_release(host_small);
+        if (recv_recs) cudaFree(recv_recs);
+        if (recv_sigs) cudaFree(recv_sigs);
     }
 };
 
@@ -1688,6 +1696,86 @@ kmc_status kmc_shard_pass1(const uint8_t* reads, const uint64_t* read_offsets, u
     return KMC_OK;
 }
 
+namespace {
+
+// The sharded plan (every rank derives the same one from the global histograms), the bin ->
+// rank map and this rank's record count per destination (j->send_counts); j->sig2owner holds
+// signature -> rank on the device.
+void shard_plan(kmc_job* j, const uint64_t* global_hist_w, const uint64_t* global_hist_r, int world, int rank) {
+    PlanCtx& c = j->ctx;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    const uint64_t ns = c.ns;
+    j->world = world;
+    j->rank = rank;
+    // the global histograms replace the local ones: every rank derives the same plan
+    uint64_t* gr = ar.get<uint64_t>(ns);
+    CK(cudaMemcpyAsync(c.hist_w, global_hist_w, ns * 8, cudaMemcpyDefault, s));
+    CK(cudaMemcpyAsync(gr, global_hist_r, ns * 8, cudaMemcpyDefault, s));
+    CK(launch_narrow(gr, ns, c.hist_r, s));
+    c.check_p1 = false;
+    plan_phase(j, c);
+    fetch_tables(j, c);
+    ar.release(gr);
+    c.owner.assign(c.n_bins, 0);
+    if (c.n_bins) kmc_shard_owners(c.bw.data(), c.n_bins, world, c.owner.data());
+    j->send_counts.assign(world, 0);
+    if (j->n_local_records == 0) return;
+    uint32_t* d_owner = ar.get<uint32_t>(c.n_bins);
+    j->sig2owner = ar.get<uint32_t>(ns);
+    unsigned long long* counts = ar.get<unsigned long long>(world);
+    CK(cudaMemcpyAsync(d_owner, c.owner.data(), c.n_bins * 4, cudaMemcpyHostToDevice, s));
+    CK(launch_compose_map(c.pa.sig2bin, d_owner, ns, j->sig2owner, s));
+    CK(cudaMemsetAsync(counts, 0, world * 8, s));
+    CK(launch_owner_count(c.tmp_sig, c.tmp_n, j->sig2owner, world, counts, s));
+    std::vector<unsigned long long> hc(world);
+    CK(cudaMemcpyAsync(hc.data(), counts, world * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    uint64_t o = 0;
+    for (int r = 0; r < world; ++r) {
+        j->send_counts[r] = hc[r];
+        o += hc[r];
+    }
+    if (o != j->n_local_records) {
+        set_err("partitioned %llu records, pass 1 wrote %llu", (unsigned long long)o,
+                (unsigned long long)j->n_local_records);
+        throw Fail{KMC_ERR_INTERNAL};
+    }
+    ar.release(d_owner);
+    ar.release(counts);
+}
+
+// One MSD pass of k_rec_scatter over the record stream with digit = owner rank; every rank's
+// run starts at cursor0[rank] of its output.  Plain mode writes into out_recs / out_sigs;
+// peer mode (peer_recs != nullptr) into the device array of per-rank base pointers.
+void shard_scatter(kmc_job* j, const std::vector<uint64_t>& cursor0, uint32_t* out_recs, uint32_t* out_sigs,
+                   uint32_t* const* peer_recs, uint32_t* const* peer_sigs) {
+    PlanCtx& c = j->ctx;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    const int world = j->world;
+    unsigned long long* cursor = ar.get<unsigned long long>(world);
+    CK(cudaMemcpyAsync(cursor, cursor0.data(), world * 8, cudaMemcpyHostToDevice, s));
+    int D = 1;
+    while ((1 << D) < world) ++D;
+    const uint64_t TI = rec_tile_items(j->k);
+    const uint64_t mt = c.tmp_n / TI + 1;
+    RecTile2* d_tiles = ar.get<RecTile2>(mt);
+    uint64_t* t_prefix = ar.get<uint64_t>(2);
+    void* t_temp = ar.alloc(scan_temp_bytes(2));
+    CK(launch_make_tiles(TileSrc{nullptr, 1, 0, 0, c.tmp_n}, 1, (uint32_t)TI, mt, t_prefix, t_temp, d_tiles, s));
+    CK(launch_rec_scatter(j->k, c.tmp_recs, c.tmp_sig, j->sig2owner, d_tiles, mt, t_prefix + 1, 0, D, cursor, out_recs,
+                          out_sigs, s, 1, peer_recs, peer_sigs));
+    j->launches += 7;
+    CK(cudaStreamSynchronize(s));
+    ar.release(d_tiles);
+    ar.release(t_prefix);
+    ar.release(t_temp);
+    ar.release(cursor);
+}
+
+}  // namespace
+
 kmc_status kmc_shard_partition(kmc_job* j, const uint64_t* global_hist_w, const uint64_t* global_hist_r, int world,
                                int rank, uint32_t* send_records, uint32_t* send_sigs, uint64_t* send_counts) {
     if (!j || !j->shard || !global_hist_w || !global_hist_r || !send_counts || world < 1 || world > 256 || rank < 0 ||
@@ -1700,69 +1788,115 @@ kmc_status kmc_shard_partition(kmc_job* j, const uint64_t* global_hist_w, const 
         return KMC_ERR_INVALID_ARG;
     }
     try {
-        PlanCtx& c = j->ctx;
-        Arena& ar = j->arena;
-        cudaStream_t s = j->s;
-        const uint64_t ns = c.ns;
-        j->world = world;
-        j->rank = rank;
-        // the global histograms replace the local ones: every rank derives the same plan
-        uint64_t* gr = ar.get<uint64_t>(ns);
-        CK(cudaMemcpyAsync(c.hist_w, global_hist_w, ns * 8, cudaMemcpyDefault, s));
-        CK(cudaMemcpyAsync(gr, global_hist_r, ns * 8, cudaMemcpyDefault, s));
-        CK(launch_narrow(gr, ns, c.hist_r, s));
-        c.check_p1 = false;
-        plan_phase(j, c);
-        fetch_tables(j, c);
-        ar.release(gr);
-        c.owner.assign(c.n_bins, 0);
-        if (c.n_bins) kmc_shard_owners(c.bw.data(), c.n_bins, world, c.owner.data());
-        for (int r = 0; r < world; ++r) send_counts[r] = 0;
-        if (j->n_local_records > 0) {
-            uint32_t* d_owner = ar.get<uint32_t>(c.n_bins);
-            uint32_t* sig2owner = ar.get<uint32_t>(ns);
-            unsigned long long* counts = ar.get<unsigned long long>(world);
-            unsigned long long* cursor = ar.get<unsigned long long>(world);
-            CK(cudaMemcpyAsync(d_owner, c.owner.data(), c.n_bins * 4, cudaMemcpyHostToDevice, s));
-            CK(launch_compose_map(c.pa.sig2bin, d_owner, ns, sig2owner, s));
-            CK(cudaMemsetAsync(counts, 0, world * 8, s));
-            CK(launch_owner_count(c.tmp_sig, c.tmp_n, sig2owner, world, counts, s));
-            std::vector<unsigned long long> hc(world), cur(world);
-            CK(cudaMemcpyAsync(hc.data(), counts, world * 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            unsigned long long o = 0;
-            for (int r = 0; r < world; ++r) {
-                cur[r] = o;
-                o += hc[r];
-                send_counts[r] = hc[r];
-            }
-            if (o != j->n_local_records) {
-                set_err("partitioned %llu records, pass 1 wrote %llu", o, (unsigned long long)j->n_local_records);
-                throw Fail{KMC_ERR_INTERNAL};
-            }
-            CK(cudaMemcpyAsync(cursor, cur.data(), world * 8, cudaMemcpyHostToDevice, s));
-            int D = 1;
-            while ((1 << D) < world) ++D;
-            const uint64_t TI = rec_tile_items(j->k);
-            const uint64_t mt = c.tmp_n / TI + 1;
-            RecTile2* d_tiles = ar.get<RecTile2>(mt);
-            uint64_t* t_prefix = ar.get<uint64_t>(2);
-            void* t_temp = ar.alloc(scan_temp_bytes(2));
-            CK(launch_make_tiles(TileSrc{nullptr, 1, 0, 0, c.tmp_n}, 1, (uint32_t)TI, mt, t_prefix, t_temp, d_tiles, s));
-            CK(launch_rec_scatter(j->k, c.tmp_recs, c.tmp_sig, sig2owner, d_tiles, mt, t_prefix + 1, 0, D, cursor,
-                                  send_records, send_sigs, s, 1));
-            j->launches += 7;
-            CK(cudaStreamSynchronize(s));
-            ar.release(d_tiles);
-            ar.release(d_owner);
-            ar.release(sig2owner);
-            ar.release(counts);
-            ar.release(cursor);
+        shard_plan(j, global_hist_w, global_hist_r, world, rank);
+        std::vector<uint64_t> cur(world, 0);
+        uint64_t o = 0;
+        for (int r = 0; r < world; ++r) {
+            send_counts[r] = j->send_counts[r];
+            cur[r] = o;
+            o += j->send_counts[r];
         }
+        if (j->n_local_records > 0) shard_scatter(j, cur, send_records, send_sigs, nullptr, nullptr);
     } catch (const Fail& f) {
         return f.st;
     }
     return KMC_OK;
+}
+
+kmc_status kmc_shard_plan(kmc_job* j, const uint64_t* global_hist_w, const uint64_t* global_hist_r, int world,
+                          int rank, uint64_t* send_counts) {
+    if (!j || !j->shard || !global_hist_w || !global_hist_r || !send_counts || world < 1 || world > 256 || rank < 0 ||
+        rank >= world) {
+        set_err("invalid kmc_shard_plan arguments");
+        return KMC_ERR_INVALID_ARG;
+    }
+    try {
+        shard_plan(j, global_hist_w, global_hist_r, world, rank);
+        for (int r = 0; r < world; ++r) send_counts[r] = j->send_counts[r];
+    } catch (const Fail& f) {
+        return f.st;
+    }
+    return KMC_OK;
+}
+
+kmc_status kmc_shard_recv_alloc(kmc_job* j, uint64_t n_recv, uint8_t* handles) {
+    if (!j || !j->shard || !handles || j->recv_recs) {
+        set_err("invalid kmc_shard_recv_alloc arguments");
+        return KMC_ERR_INVALID_ARG;
+    }
+    try {
+        const int RW = record_words(j->k);
+        // at least one record each, so that every rank has a mappable allocation
+        const uint64_t n = n_recv > 0 ? n_recv : 1;
+        CK(cudaMalloc(&j->recv_recs, n * RW * 4));
+        CK(cudaMalloc(&j->recv_sigs, n * 4));
+        j->n_recv = n_recv;
+        cudaIpcMemHandle_t h[2];
+        CK(cudaIpcGetMemHandle(&h[0], j->recv_recs));
+        CK(cudaIpcGetMemHandle(&h[1], j->recv_sigs));
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handles");
+        memcpy(handles, h, 128);
+    } catch (const Fail& f) {
+        return f.st;
+    }
+    return KMC_OK;
+}
+
+kmc_status kmc_shard_send_peers(kmc_job* j, const uint8_t* all_handles, const uint64_t* dst_offsets) {
+    if (!j || !j->shard || !all_handles || !dst_offsets || !j->recv_recs || j->world < 1) {
+        set_err("invalid kmc_shard_send_peers arguments (kmc_shard_plan and kmc_shard_recv_alloc first)");
+        return KMC_ERR_INVALID_ARG;
+    }
+    const int world = j->world;
+    std::vector<void*> opened;
+    kmc_status st = KMC_OK;
+    try {
+        std::vector<uint32_t*> pr(world), ps(world);
+        for (int r = 0; r < world; ++r) {
+            if (r == j->rank) {
+                pr[r] = j->recv_recs;
+                ps[r] = j->recv_sigs;
+                continue;
+            }
+            cudaIpcMemHandle_t h[2];
+            memcpy(h, all_handles + 128 * (size_t)r, 128);
+            void* a = nullptr;
+            void* b = nullptr;
+            CK(cudaIpcOpenMemHandle(&a, h[0], cudaIpcMemLazyEnablePeerAccess));
+            opened.push_back(a);
+            CK(cudaIpcOpenMemHandle(&b, h[1], cudaIpcMemLazyEnablePeerAccess));
+            opened.push_back(b);
+            pr[r] = (uint32_t*)a;
+            ps[r] = (uint32_t*)b;
+        }
+        if (j->n_local_records > 0) {
+            uint32_t** d_ptrs = j->arena.get<uint32_t*>(2 * world);
+            std::vector<uint32_t*> both(pr);
+            both.insert(both.end(), ps.begin(), ps.end());
+            CK(cudaMemcpyAsync(d_ptrs, both.data(), 2 * world * sizeof(uint32_t*), cudaMemcpyHostToDevice, j->s));
+            std::vector<uint64_t> cur(dst_offsets, dst_offsets + world);
+            shard_scatter(j, cur, nullptr, nullptr, d_ptrs, d_ptrs + world);
+            j->arena.release(d_ptrs);
+        }
+        CK(cudaStreamSynchronize(j->s));
+    } catch (const Fail& f) {
+        st = f.st;
+    }
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    return st;
+}
+
+namespace {
+kmc_status shard_count_impl(kmc_job* j, const uint32_t* recv_records, const uint32_t* recv_sigs, uint64_t n_recv,
+                            uint64_t* n_out, bool in_place);
+}
+
+kmc_status kmc_shard_count_recv(kmc_job* j, uint64_t* n_out) {
+    if (!j || !j->shard || !n_out || !j->recv_recs) {
+        set_err("invalid kmc_shard_count_recv arguments");
+        return KMC_ERR_INVALID_ARG;
+    }
+    return shard_count_impl(j, j->recv_recs, j->recv_sigs, j->n_recv, n_out, true);
 }
 
 kmc_status kmc_shard_count(kmc_job* j, const uint32_t* recv_records, const uint32_t* recv_sigs, uint64_t n_recv,
@@ -1771,6 +1905,14 @@ kmc_status kmc_shard_count(kmc_job* j, const uint32_t* recv_records, const uint3
         set_err("invalid kmc_shard_count arguments");
         return KMC_ERR_INVALID_ARG;
     }
+    return shard_count_impl(j, recv_records, recv_sigs, n_recv, n_out, false);
+}
+
+namespace {
+// in_place: the received records already sit in job-owned buffers (the fused exchange's
+// receive buffers), read where they are instead of being copied into scratch
+kmc_status shard_count_impl(kmc_job* j, const uint32_t* recv_records, const uint32_t* recv_sigs, uint64_t n_recv,
+                            uint64_t* n_out, bool in_place) {
     *n_out = 0;
     try {
         PlanCtx& c = j->ctx;
@@ -1805,7 +1947,10 @@ kmc_status kmc_shard_count(kmc_job* j, const uint32_t* recv_records, const uint3
         ar.release(c.tmp_recs);
         ar.release(c.tmp_sig);
         c.tmp_recs = c.tmp_sig = nullptr;
-        if (n_recv > 0) {
+        if (n_recv > 0 && in_place) {
+            c.tmp_recs = const_cast<uint32_t*>(recv_records);  // not arena memory: release() skips it
+            c.tmp_sig = const_cast<uint32_t*>(recv_sigs);
+        } else if (n_recv > 0) {
             c.tmp_recs = reinterpret_cast<uint32_t*>(ar.alloc(n_recv * RW * 4));
             c.tmp_sig = ar.get<uint32_t>(n_recv);
             CK(cudaMemcpyAsync(c.tmp_recs, recv_records, n_recv * RW * 4, cudaMemcpyDefault, s));
@@ -1821,6 +1966,7 @@ kmc_status kmc_shard_count(kmc_job* j, const uint32_t* recv_records, const uint3
     *n_out = j->n_surv;
     return KMC_OK;
 }
+}  // namespace
 
 int kmc_record_words(int k) { return record_words(k); }
 

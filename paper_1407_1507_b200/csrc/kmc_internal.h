@@ -93,7 +93,8 @@ cudaError_t launch_make_tiles(const TileSrc& src, uint64_t nb, uint32_t TI, uint
 cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* in_ids, const uint32_t* sig2bin,
                                const RecTile2* tiles, uint64_t max_tiles, const uint64_t* n_tiles_dev, int shift,
                                int D, unsigned long long* cursor, uint32_t* out_recs, uint32_t* out_ids,
-                               cudaStream_t s, int out_orig_ids = 0);
+                               cudaStream_t s, int out_orig_ids = 0, uint32_t* const* peer_recs = nullptr,
+                               uint32_t* const* peer_ids = nullptr);
 // sharded counting helpers
 cudaError_t launch_compose_map(const uint32_t* map_a, const uint32_t* map_b, uint64_t n, uint32_t* out,
                                cudaStream_t s);

@@ -150,7 +150,7 @@ def test_sharded_world1_equals_count(gpu):
     assert torch.equal(a.kmers, b.kmers) and torch.equal(a.counts, b.counts)
 
 
-def _sharded_gpu_worker(rank, world, port, name, scale, q):
+def _sharded_gpu_worker(rank, world, port, name, scale, q, mode="collective", opts=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     sys.path.insert(0, ROOT)
     import paper_1407_1507_b200 as kmc
@@ -162,18 +162,26 @@ def _sharded_gpu_worker(rank, world, port, name, scale, q):
     off = w.offsets[cuts[rank]:cuts[rank + 1] + 1]
     reads = torch.from_numpy(np.ascontiguousarray(w.reads[int(off[0]):int(off[-1])])).cuda()
     offs = torch.from_numpy(np.ascontiguousarray(off).view(np.uint64)).cuda()
-    res = kmc.count_sharded(reads, offs, w.k, w.p, w.cutoff_min, w.cutoff_max)
+    res = kmc.count_sharded(reads, offs, w.k, w.p, w.cutoff_min, w.cutoff_max, exchange_mode=mode, **(opts or {}))
     q.put((rank, res.kmers.cpu().numpy(), res.counts.cpu().numpy()))
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-def test_count_sharded_two_processes_gloo(gpu):
-    # two ranks (processes) on one GPU; the exchange goes through gloo on the host
+@pytest.mark.parametrize("mode,world,name,opts", [("collective", 2, "C5", None), ("p2p", 2, "C5", None),
+                                                  ("p2p", 3, "C2", dict(force_large=True)),
+                                                  ("p2p", 2, "C3", None)])
+def test_count_sharded_processes(gpu, mode, world, name, opts):
+    # ranks as processes on one GPU (gloo for the host-side exchanges).  "collective": records
+    # grouped into send buffers, all-to-all through gloo; "p2p": the fused exchange -- every
+    # rank's partition pass writes into the owners' receive buffers mapped through CUDA IPC
+    # (here the peers are other processes on the same device; on a node, other GPUs over NVLink)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    world, name, scale = 2, "C5", 0.003
-    procs = [ctx.Process(target=_sharded_gpu_worker, args=(r, world, 29561, name, scale, q)) for r in range(world)]
+    scale = 0.003
+    port = 29561 + 7 * world + (mode == "p2p") + 3 * (name == "C3")
+    procs = [ctx.Process(target=_sharded_gpu_worker, args=(r, world, port, name, scale, q, mode, opts))
+             for r in range(world)]
     for p in procs:
         p.start()
     got = sorted(q.get(timeout=600) for _ in range(world))
@@ -183,6 +191,10 @@ def test_count_sharded_two_processes_gloo(gpu):
     w = synth.make(name, scale=scale)
     keys = np.concatenate([g[1] for g in got])
     counts = np.concatenate([g[2] for g in got])
-    order = np.argsort(keys, kind="stable")
+    if keys.ndim == 1:
+        order = np.argsort(keys, kind="stable")
+    else:
+        keys = keys.reshape(-1, 2)
+        order = np.lexsort((keys[:, 0], keys[:, 1]))
     ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max)
     assert np.array_equal(keys[order], ref.keys) and np.array_equal(counts[order], ref.counts)
