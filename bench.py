@@ -232,10 +232,21 @@ def main():
     k, p, ci, cx = w.k, w.p, w.cutoff_min, w.cutoff_max
     stream = torch.cuda.current_stream()
 
+    xmode = {"mode": "p2p"}  # N > 1: the fused exchange over peer memory, else the all-to-all
+
     def step(profile=True):
         if world > 1:
-            return kmc.count_sharded(reads_d, offs_d, k, p, ci, cx, profile=profile, count_path=args.count_path)
+            return kmc.count_sharded(reads_d, offs_d, k, p, ci, cx, profile=profile, count_path=args.count_path,
+                                     exchange_mode=xmode["mode"])
         return kmc.count(reads_d, offs_d, k, p, ci, cx, profile=profile, count_path=args.count_path)
+
+    if world > 1:
+        try:
+            del_res = step()
+            del del_res
+        except kmc.KmcError as e:  # every rank raises together (the exchange's success is all-reduced)
+            print(f"rank {rank}: fused P2P exchange unavailable ({e}); using the NCCL all-to-all", file=sys.stderr)
+            xmode["mode"] = "collective"
 
     for _ in range(max(3, args.warmup)):
         res = step()
@@ -304,7 +315,8 @@ def main():
         offs_h = torch.from_numpy(w.offsets.view(np.uint64)).pin_memory()
         def e2e_step():
             if world > 1:
-                return kmc.count_sharded(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path)
+                return kmc.count_sharded(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path,
+                                         exchange_mode=xmode["mode"])
             return kmc.count(reads_h, offs_h, k, p, ci, cx, out_device="cpu", count_path=args.count_path)
         r = e2e_step()
         n_out = r.stats["n_out"]
@@ -424,7 +436,10 @@ def main():
                    "n_bases": n_bases, "k": k, "p": p, "cutoff_min": ci, "cutoff_max": cx,
                    "parallelism": (f"sharded x{world}: reads split by rank, NCCL all-reduce of the signature "
                                    f"histogram; super-k-mer records written by the partition pass straight "
-                                   f"into the owner rank's receive buffers over NVLink (CUDA IPC peer memory)")
+                                   f"into the owner rank's receive buffers over NVLink (CUDA IPC peer memory)"
+                                   if xmode["mode"] == "p2p" else
+                                   f"sharded x{world}: reads split by rank, NCCL all-reduce of the signature "
+                                   f"histogram + all-to-all of super-k-mer records by bin owner")
                    if world > 1 else "1 GPU",
                    "count_path": ["smem_hash", "smem_radix_sort"][args.count_path],
                    "l2": "inputs (4 GB) larger than L2 (126 MB); no flush needed"},

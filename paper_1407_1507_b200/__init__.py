@@ -366,8 +366,19 @@ def exchange_p2p(sh, world: int, rank: int, group=None):
     handles = [None] * world
     dist.all_gather_object(handles, sh.recv_alloc(n_recv), group=group)
     dst_offsets = [sum(allc[s_][d] for s_ in range(rank)) for d in range(world)]
-    sh.send_peers(b"".join(handles), dst_offsets)
-    dist.barrier(group=group)  # every rank's writes into this rank's buffers are complete
+    import torch
+    ok, err = 1, None
+    try:
+        sh.send_peers(b"".join(handles), dst_offsets)
+    except KmcError as e:  # e.g. peer memory not mappable: every rank must learn it
+        ok, err = 0, e
+    # the barrier that ends the exchange (every rank's writes into this rank's buffers are
+    # complete), carrying every rank's success
+    flag = torch.tensor([ok], dtype=torch.int32,
+                        device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 0:
+        raise KmcError(KMC_ERR_CUDA, f"fused P2P exchange failed on a rank ({err})")
 
 
 def count_sharded(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int = 10**9, *,
