@@ -181,6 +181,9 @@ typedef struct {
                                   k + x <= 31 and canonical counting.  Same output for every x. */
     uint32_t spill_keys;       /* large_path 3, testing: spill list capacity (0 = auto); a spill
                                   beyond it reruns the large bins on the split path */
+    uint32_t split_tight;      /* testing (one-pass split): 1 = digit regions without slack
+                                  (ceil(W / nd) + 2 slots), so digits overflow into the overflow
+                                  list and the fallback is exercised */
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).

@@ -656,7 +656,8 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
         const uint64_t b = large_ids[i];
         uint64_t d = (uint64_t)std::ceil((double)bw[b] / target);
         d = std::min<uint64_t>(std::max<uint64_t>(d, 1), (uint64_t)S1_DMAX);
-        uint64_t r = (uint64_t)std::ceil((double)bw[b] / (double)d * 1.25) + 256;
+        uint64_t r = j->opt.split_tight ? (bw[b] + d - 1) / d + 2
+                                        : (uint64_t)std::ceil((double)bw[b] / (double)d * 1.25) + 256;
         r = std::min<uint64_t>((r + 1) & ~1ull, 0x7FFFFFFEull);
         nd[i] = (uint32_t)d;
         rc[i] = (uint32_t)r;

@@ -157,6 +157,21 @@ def test_chunk_hash_overflow_fallback(gpu):
     assert st["chunk_capacity"] <= 6144
 
 
+@pytest.mark.parametrize("name,scale,opts", [("C2", 0.005, {}), ("C5", 0.004, {}), ("C4", 0.001, {}),
+                                             ("C1", 0.1, dict(chunk_capacity=2000)), ("C2", 0.004, dict(canonical=False))])
+def test_split_region_overflow(gpu, name, scale, opts):
+    """One-pass split with regions of exactly the mean digit size: digits overflow, their excess
+    keys go to the overflow list and the overflowed digits (region part + excess) are counted
+    by the device radix-sort fallback -- same bytes as the oracle."""
+    w = synth.make(name, scale=scale)
+    opts = dict(opts)
+    opts.setdefault("chunk_capacity", 512)  # many digits per bin
+    keys, counts, st = gpu_count(gpu, w, force_large=True, split_tight=True, **opts)
+    ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max, canonical=opts.get("canonical", True))
+    assert np.array_equal(keys, ref.keys) and np.array_equal(counts, ref.counts)
+    assert st["n_split_overflow"] > 0
+
+
 # ---------------------------------------------------------------- large bins by thread-block clusters
 
 @pytest.mark.parametrize("cluster_size", [1, 4, 8, 16])
