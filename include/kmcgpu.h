@@ -129,6 +129,7 @@ typedef struct {
     uint64_t n_kxmers;         /* (k,x)-mers sorted (kx > 0): Table 7's "sorted fraction" is
                                   n_kxmers / kx_windows */
     uint64_t kx_windows;       /* windows of the bins counted through (k,x)-mers (the small bins) */
+    uint64_t n_passes;         /* passes over bin ranges (host-resident reads beyond HBM); 1 = one pass */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;
@@ -181,6 +182,10 @@ typedef struct {
                                   k + x <= 31 and canonical counting.  Same output for every x. */
     uint32_t spill_keys;       /* large_path 3, testing: spill list capacity (0 = auto); a spill
                                   beyond it reruns the large bins on the split path */
+    uint32_t pass_mb;          /* host-resident reads: count in passes over ranges of bins whose
+                                  records take at most this many MiB of device memory (0 = auto:
+                                  passes only when the single-pass working set would not fit the
+                                  free device memory) -- f2, inputs beyond HBM */
     uint32_t split_tight;      /* testing (one-pass split): 1 = digit regions without slack
                                   (ceil(W / nd) + 2 slots), so digits overflow into the overflow
                                   list and the fallback is exercised */

@@ -454,7 +454,9 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                     bin = a.sig2bin[s];
                     bbase = a.bin_rec_off[bin];
                 }
-                for (int ii = v; ii < j; ii += maxw) {
+                // a pass over a range of bins (inputs beyond HBM): other bins' records are skipped
+                const bool skip = MODE == P1_MODE_SCATTER && (bin < a.bin_lo || bin >= a.bin_hi);
+                for (int ii = v; ii < j && !skip; ii += maxw) {
                     const int m = min(maxw, j - ii);
                     // record words: word 0 = m (8 bits) + symbols [0, 12); word u > 0 =
                     // symbols [12 + 16(u-1), 12 + 16u) -- from the packed segment by funnel shifts

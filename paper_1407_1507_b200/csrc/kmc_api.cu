@@ -237,6 +237,7 @@ struct PlanCtx {
     std::function<int(int)> run_p1;  // pass-1 recompute (S5 fallback), unset when sharded
     // sharded: bin -> owning rank
     std::vector<uint32_t> owner;
+    bool multipass = false;  // host reads beyond HBM: passes over ranges of bins (f2)
 };
 
 struct kmc_job {
@@ -252,6 +253,7 @@ struct kmc_job {
     void* surv_keys = nullptr;
     uint32_t* surv_counts = nullptr;
     uint64_t n_surv = 0;
+    uint64_t surv_cap = 0;
     kmc_stats st{};
     int launches = 0;
     std::vector<StageEv> evs;
@@ -361,6 +363,9 @@ void read_extent(kmc_job* j, const uint64_t* offsets, uint64_t n_reads, uint64_t
 void plan_phase(kmc_job* j, PlanCtx& c);
 void fetch_tables(kmc_job* j, PlanCtx& c);
 void count_phase(kmc_job* j, PlanCtx& c);
+void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t b_hi);
+void count_multipass(kmc_job* j, PlanCtx& c);
+void release_plan_scratch(kmc_job* j, PlanCtx& c);
 
 void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads) {
     const int k = j->k, p = j->p, kw = j->key_words;
@@ -436,6 +441,8 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     a.rules = j->opt.plain_minimizers ? 0 : 1;
     a.reads_aligned16 = ((uintptr_t)d_reads & 15) == 0;
     a.tile_r_lo = tile_r_lo;
+    a.bin_lo = 0;
+    a.bin_hi = 0xFFFFFFFFu;
     a.hist_w = hist_w;
     a.hist_r = hist_r;
     a.gstats = gstats;
@@ -445,7 +452,19 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     uint32_t* tmp_recs = nullptr;
     uint32_t* tmp_sig = nullptr;
     uint64_t tmp_cap = 0;
-    if (j->opt.distribute_path != 1) {
+    // Inputs beyond HBM (f2): host-resident reads whose single-pass working set (record stream
+    // + bins, ~(2 RW*4 + 4) bytes per record, ~n_bases/8 records) does not fit the free device
+    // memory -- or a forced pass size -- are counted in passes over ranges of bins: pass 1
+    // builds only the histogram, then every pass streams the reads again and keeps the
+    // records of its bins.
+    j->ctx.multipass = false;
+    if (host_reads && !j->shard) {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        const double est = (double)(n_bases / 8 + 1) * (2.0 * RWt * 4 + 4) * 1.2;
+        j->ctx.multipass = j->opt.pass_mb > 0 || est > 0.7 * (double)fr;
+    }
+    if (j->opt.distribute_path != 1 && !j->ctx.multipass) {
         // slots: records (~n_bases/8 at 100 bp reads) + every pass-1 warp's partly used block
         tmp_cap = std::max<uint64_t>(n_bases / 8, 4096) + (uint64_t)n_sms() * 64 * 2048;
         tmp_recs = reinterpret_cast<uint32_t*>(ar.alloc(tmp_cap * RWt * 4));
@@ -695,7 +714,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
         max_gn = std::max<uint64_t>(max_gn, i1 - i0);
         i0 = i1;
     }
-    j->st.n_large_groups = groups.size();
+    j->st.n_large_groups += groups.size();
     LargeBin* d_lbins = ar.get<LargeBin>(max_gn);
     S1Bin* d_sbins = ar.get<S1Bin>(max_gn);
     uint64_t* d_pp = ar.get<uint64_t>(max_gn + 1);
@@ -856,6 +875,11 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         j->n_surv = 0;
         return;
     }
+    j->st.n_passes = 1;
+    if (c.multipass) {
+        count_multipass(j, c);
+        return;
+    }
     // ---- S5: records into bins -- a copy from pass 1's temporary stream, or (if the stream
     //      overflowed its estimate) pass 2 = S1-S3 recomputed + scatter
     uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4));
@@ -926,6 +950,18 @@ void count_phase(kmc_job* j, PlanCtx& c) {
     j->stage_end(s5_launches);
     ar.release(tmp_recs);
     ar.release(tmp_sig);
+    release_plan_scratch(j, c);
+
+    // the per-bin tables were copied to the host while S5 runs on the device
+    fetch_tables(j, c);
+    count_bins(j, c, bins, 0, n_bins);
+    ar.release(bins);
+}
+
+// Frees the histograms and the plan's scans (the per-bin tables stay).
+void release_plan_scratch(kmc_job* j, PlanCtx& c) {
+    Arena& ar = j->arena;
+    PlanArgs& pa = c.pa;
     ar.release(c.hist_w);
     ar.release(c.hist_r);
     ar.release(pa.cost_scan);
@@ -934,15 +970,88 @@ void count_phase(kmc_job* j, PlanCtx& c) {
     ar.release(pa.rec_scan);
     ar.release(pa.bin_first);
     ar.release(pa.temp);
+}
 
-    // the per-bin tables were copied to the host while S5 runs on the device
+// Inputs beyond HBM (f2; host-resident reads): pass 1 has built only the histogram; the bins
+// are cut into consecutive ranges whose records (and their counting) fit the device budget,
+// and for every range the reads are streamed through pass 1 again, which now writes the
+// records of the range's bins straight into them (P1_MODE_SCATTER with a bin filter), then
+// the range is counted (S6-S8) into the growing survivor buffer; S9 orders all survivors.
+void count_multipass(kmc_job* j, PlanCtx& c) {
+    const int RW = record_words(j->k);
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    PlanArgs& pa = c.pa;
+    release_plan_scratch(j, c);
     fetch_tables(j, c);
+    const std::vector<uint64_t>& bn = c.bn;
+    const std::vector<uint64_t>& bo = c.bo;
+    const uint64_t n_bins = c.n_bins;
+    // records per pass: the option, else a share of the free device memory (bins 16-32 B,
+    // survivors up to 12-20 B per window / ci, the large-bin key regions are grouped anyway)
+    uint64_t budget;
+    if (j->opt.pass_mb) {
+        budget = std::max<uint64_t>(1, ((uint64_t)j->opt.pass_mb << 20) / (RW * 4));
+    } else {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        budget = std::max<uint64_t>(1u << 20, (uint64_t)(0.3 * (double)fr) / (RW * 4 + 120));
+    }
+    std::vector<std::pair<uint64_t, uint64_t>> passes;
+    for (uint64_t b0 = 0; b0 < n_bins;) {
+        uint64_t b1 = b0, recs = 0;
+        while (b1 < n_bins && (b1 == b0 || recs + bn[b1] <= budget)) recs += bn[b1++];
+        passes.push_back({b0, b1});
+        b0 = b1;
+    }
+    j->st.n_passes = passes.size();
+    uint32_t* bin_fill = ar.get<uint32_t>(n_bins);
+    for (const auto& ps : passes) {
+        const uint64_t b0 = ps.first, b1 = ps.second;
+        const uint64_t r0 = bo[b0], r1 = b1 < n_bins ? bo[b1] : c.n_records;
+        if (r1 == r0) continue;
+        uint32_t* buf = reinterpret_cast<uint32_t*>(ar.alloc((r1 - r0) * RW * 4 + 64));
+        // the kernels address records by their global record index: a base pointer r0
+        // records before the buffer makes [r0, r1) land in it
+        uint32_t* bins_v = buf - r0 * RW;
+        CK(cudaMemsetAsync(bin_fill, 0, n_bins * 4, s));
+        c.a.sig2bin = pa.sig2bin;
+        c.a.bin_rec_off = pa.bin_rec_off;
+        c.a.bin_fill = bin_fill;
+        c.a.bins = bins_v;
+        c.a.bin_lo = (uint32_t)b0;
+        c.a.bin_hi = (uint32_t)b1;
+        j->stage_begin(KMC_STAGE_SCATTER);
+        const int nl = c.run_p1(P1_MODE_SCATTER);
+        j->launches += nl;
+        j->stage_end(nl);
+        count_bins(j, c, bins_v, b0, b1);
+        ar.release(buf);
+    }
+    ar.release(bin_fill);
+}
+
+// S6-S8 of the bins [b_lo, b_hi) (records in `bins`, addressed by global record index) into
+// the survivor buffer, grown to hold every survivor possible so far.
+void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t b_hi) {
+    const int k = j->k, kw = j->key_words;
+    const size_t ksz = kw == 1 ? 8 : 16;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    const int cap = c.cap;
+    PlanArgs& pa = c.pa;
+    unsigned long long* hs = j->host_small;
+    unsigned long long* gstats = c.gstats;
+    const std::vector<uint64_t>& bw = c.bw;
+    const std::vector<uint64_t>& bn = c.bn;
+    const std::vector<uint64_t>& bo = c.bo;
     // ---- host: classify bins (small: one CTA in SMEM; large: multi-CTA path)
     std::vector<uint32_t> small;
     std::vector<uint64_t> large_ids;
-    uint64_t large_windows = 0, n_large = 0, max_bin = 0;
-    for (uint64_t b = 0; b < n_bins; ++b) {
+    uint64_t large_windows = 0, n_large = 0, max_bin = 0, range_windows = 0;
+    for (uint64_t b = b_lo; b < b_hi; ++b) {
         if (bw[b] == 0) continue;
+        range_windows += bw[b];
         max_bin = std::max(max_bin, bw[b]);
         const uint64_t cost = std::max<uint64_t>(bw[b], bn[b] * pa.recw);
         if (cost <= (uint64_t)cap && !j->opt.force_large) {
@@ -954,14 +1063,27 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         }
     }
     std::sort(small.begin(), small.end(), [&](uint32_t x, uint32_t y) { return bw[x] > bw[y] || (bw[x] == bw[y] && x < y); });
-    j->st.n_large_bins = n_large;
-    j->st.large_windows = large_windows;
-    j->st.max_bin_windows = max_bin;
+    j->st.n_large_bins += n_large;
+    j->st.large_windows += large_windows;
+    j->st.max_bin_windows = std::max<uint64_t>(j->st.max_bin_windows, max_bin);
 
-    // ---- survivors buffer: every survivor has count >= ci, counts sum to n_windows
-    const uint64_t surv_cap = n_windows / j->ci + 1;
-    j->surv_keys = ar.alloc(surv_cap * ksz);
-    j->surv_counts = ar.get<uint32_t>(surv_cap);
+    // ---- survivors buffer: every survivor has count >= ci, the range's counts sum to its
+    //      windows; grown (the survivors so far copied) when a later range needs more room
+    const uint64_t need = j->n_surv + range_windows / j->ci + 1;
+    if (need > j->surv_cap) {
+        void* nk = ar.alloc(need * ksz);
+        uint32_t* nc = ar.get<uint32_t>(need);
+        if (j->n_surv) {
+            CK(cudaMemcpyAsync(nk, j->surv_keys, j->n_surv * ksz, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(nc, j->surv_counts, j->n_surv * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        ar.release(j->surv_keys);
+        ar.release(j->surv_counts);
+        j->surv_keys = nk;
+        j->surv_counts = nc;
+        j->surv_cap = need;
+    }
+    const uint64_t surv_cap = j->surv_cap;
 
     // ---- S6-S8 small bins
     // The hash path sizes its chunks by the distinct/window ratio of the small bins.  With
@@ -1161,6 +1283,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
         void* lkeys = ar.alloc(large_windows * ksz);
         j->stage_begin(KMC_STAGE_LARGE_SPLIT);
+        CK(cudaMemsetAsync(gstats + GS_LARGE_KEYS, 0, 8, s));  // this range's key cursor
         CK(launch_make_pieces(d_lbins, d_pp, lbins.size(), PIECE_RECORDS, d_pieces, s));
         CK(launch_large_expand(bins, d_pieces, n_pieces, k, !j->opt.non_canonical, lkeys, gstats, s));
         j->launches += 2;
@@ -1230,7 +1353,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
             max_gn = std::max<uint64_t>(max_gn, i1 - i0);
             i0 = i1;
         }
-        j->st.n_large_groups = groups.size();
+        j->st.n_large_groups += groups.size();
         // split ranges: one CTA each, a few per SM (the split kernels are ~40 KB of SMEM)
         const uint32_t max_ranges = (uint32_t)n_sms() * 4;
         LargeBin* d_lbins = ar.get<LargeBin>(max_gn);
@@ -1385,7 +1508,6 @@ void count_phase(kmc_job* j, PlanCtx& c) {
             }
         }
         ar.release(lkeys);
-        j->st.n_large_bins = n_large;
         hs[16 + GS_LARGE_KEYS] = large_windows;  // the split writes exactly the planned keys
     }
     CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
@@ -1406,7 +1528,6 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         set_err("survivor overflow");
         throw Fail{KMC_ERR_INTERNAL};
     }
-    ar.release(bins);
 }
 
 void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {

@@ -49,6 +49,7 @@ struct P1Args {
     const uint64_t* bin_rec_off;
     uint32_t* bin_fill;
     uint32_t* bins;
+    uint32_t bin_lo, bin_hi;  // pass 2 writes only the records of bins [bin_lo, bin_hi)
     // pass 1: temporary record stream (nullptr = not used)
     uint32_t* tmp_recs;
     uint32_t* tmp_sig;

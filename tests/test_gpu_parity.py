@@ -546,3 +546,38 @@ def test_kxmer_invalid(gpu):
         with pytest.raises(gpu.KmcError) as ei:
             gpu.count(r, o, k, 7, 1, 10**9, kx=x, canonical=canon)
         assert ei.value.status == gpu.KMC_ERR_INVALID_ARG
+
+
+# ---------------------------------------------------------------- f2: inputs beyond HBM (passes over bin ranges)
+
+@pytest.mark.parametrize("name,scale,opts", [("C4", 0.002, dict(pass_mb=1)), ("C5", 0.004, dict(pass_mb=1)),
+                                             ("C3", 0.005, dict(pass_mb=1)), ("C2", 0.004, dict(pass_mb=1, large_path=1)),
+                                             ("C1", 0.3, dict(pass_mb=1, count_path=1, force_large=True)),
+                                             ("C2", 0.004, dict(pass_mb=1, kx=3)),
+                                             ("C4", 0.001, dict(pass_mb=1, input_batch_mb=1))])
+def test_multipass_host_input(gpu, name, scale, opts):
+    """Host-resident reads counted in passes over ranges of bins (pass 1 builds only the
+    histogram; every pass streams the reads again and keeps its bins' records): the oracle's
+    bytes, with several passes."""
+    w = synth.make(name, scale=scale)
+    rh = torch.from_numpy(w.reads).pin_memory()
+    oh = torch.from_numpy(w.offsets.view(np.uint64))
+    res = gpu.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", **opts)
+    ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max)
+    assert res.stats["n_passes"] >= 2, res.stats["n_passes"]
+    assert np.array_equal(res.kmers.numpy(), ref.keys) and np.array_equal(res.counts.numpy(), ref.counts)
+    for f in ("n_windows", "n_unique", "n_below_min", "n_above_max", "n_out"):
+        assert res.stats[f] == getattr(ref, f), f
+
+
+def test_multipass_full_c4_digest(gpu):
+    """The whole C4 read set (4 G bases, host-resident) counted in forced passes of <= 1 GiB of
+    records gives exactly the oracle's digest (tests/golden/full_configs.json)."""
+    w = synth.make("C4")
+    rh = torch.from_numpy(w.reads).pin_memory()
+    oh = torch.from_numpy(w.offsets.view(np.uint64))
+    res = gpu.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", pass_mb=1024)
+    g = GOLD["C4"]
+    assert res.stats["n_passes"] >= 4
+    assert res.stats["n_out"] == g["n_out"] and res.stats["n_unique"] == g["n_unique"]
+    assert oracle.digest(res.kmers.numpy(), res.counts.numpy()) == g["sha256"]
