@@ -109,6 +109,16 @@ void* cache_alloc(size_t bytes, cudaStream_t s, size_t* actual) {
     }
     return p;
 }
+// bytes of this device's blocks held by the cache (free for a call that reuses them)
+size_t cache_bytes() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    size_t b = 0;
+    for (auto& e : g_cache)
+        if (e.second.dev == dev) b += e.second.size;
+    return b;
+}
 void cache_free(void* p, size_t bytes, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -462,7 +472,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
         const double est = (double)(n_bases / 8 + 1) * (2.0 * RWt * 4 + 4) * 1.2;
-        j->ctx.multipass = j->opt.pass_mb > 0 || est > 0.7 * (double)fr;
+        j->ctx.multipass = j->opt.pass_mb > 0 || est > 0.7 * (double)(fr + cache_bytes());
     }
     if (j->opt.distribute_path != 1 && !j->ctx.multipass) {
         // slots: records (~n_bases/8 at 100 bp reads) + every pass-1 warp's partly used block
@@ -993,9 +1003,14 @@ void count_multipass(kmc_job* j, PlanCtx& c) {
     if (j->opt.pass_mb) {
         budget = std::max<uint64_t>(1, ((uint64_t)j->opt.pass_mb << 20) / (RW * 4));
     } else {
+        // per record of a pass: the record, the survivor room of its windows (count >= ci)
+        // and about 10 bytes per window of large-bin key regions (the split groups bins by
+        // the memory left, so this only sizes the pass); memory = free + this process's cache
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
-        budget = std::max<uint64_t>(1u << 20, (uint64_t)(0.3 * (double)fr) / (RW * 4 + 120));
+        const double wpr = c.n_records ? (double)c.n_windows / (double)c.n_records : 10.0;
+        const double per = RW * 4 + wpr * ((j->key_words == 1 ? 12.0 : 20.0) / j->ci + 10.0);
+        budget = std::max<uint64_t>(1u << 20, (uint64_t)(0.6 * (double)(fr + cache_bytes()) / per));
     }
     std::vector<std::pair<uint64_t, uint64_t>> passes;
     for (uint64_t b0 = 0; b0 < n_bins;) {

@@ -229,7 +229,7 @@ cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint6
 
 // One-pass sized split of the large bins (k_split1.cu, k <= 32): bin b gets nd digits
 // (digit = (hash(key) * nd) >> 32), digit d owns key slots [key_base + d * rc, + rc).
-constexpr int S1_DMAX = 256;
+constexpr int S1_DMAX = 512;
 struct S1Bin {
     uint64_t key_base;
     uint32_t nd, rc, dbase, pad;

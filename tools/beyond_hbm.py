@@ -34,13 +34,17 @@ oh = torch.from_numpy(w.offsets.view(np.uint64)).pin_memory()
 t_pin = time.time() - t0
 kmc.load()
 runs = []
-for it in range(2):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    res = kmc.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", profile=True)
-    torch.cuda.synchronize()
-    runs.append(time.perf_counter() - t0)
-st = res.stats
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+res = kmc.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", profile=True)
+torch.cuda.synchronize()
+runs.append(time.perf_counter() - t0)  # includes pinning the output tensors (host)
+# again into the same pinned output buffers: the call alone
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+st = kmc.count_into(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, res.kmers, res.counts, profile=True)
+torch.cuda.synchronize()
+runs.append(time.perf_counter() - t0)
 keys, counts = res.kmers.numpy(), res.counts.numpy()
 # checks the oracle can afford at this size
 t0 = time.time()
@@ -53,7 +57,8 @@ out = {
     "workload": f"C4 x{scale}: {w.n_reads} reads, {w.n_bases} bases (host-resident, pinned)",
     "device_free_gb": round(free / 1e9, 1), "device_total_gb": round(total / 1e9, 1),
     "single_pass_working_set_gb_est": round(w.n_bases * 5.4 / 1e9, 1),
-    "seconds": [round(x, 3) for x in runs], "bases_per_s": w.n_bases / min(runs),
+    "seconds": [round(x, 3) for x in runs], "bases_per_s": w.n_bases / runs[1],
+    "note": "seconds[0] includes pinning the 17 GB output tensors; seconds[1] is kmc_count_ex into them",
     "n_passes": st["n_passes"], "n_input_batches": st["n_input_batches"],
     "stats": {x: st[x] for x in ("n_windows", "n_unique", "n_out", "n_large_bins", "max_bin_windows")},
     "stage_ms": {x: round(v, 1) for x, v in st["stage_ms"].items() if v > 0},
