@@ -518,7 +518,7 @@ template <int RW> constexpr size_t rec_scatter_smem() {
     return (size_t)RecTile<RW>::v * (RW * 4 + 4 + 1) + (3 * 256 + 64) * 4 + 64;
 }
 
-template <int RW>
+template <int RW, bool PEER>
 __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restrict__ in_recs,
                                                        const uint32_t* __restrict__ in_ids,
                                                        const uint32_t* __restrict__ sig2bin,
@@ -603,8 +603,8 @@ __global__ void __launch_bounds__(RS_NT) k_rec_scatter(const uint32_t* __restric
         const uint64_t o = gb[d] + (i - lh[d]);
         // peer mode (fused exchange): digit d is a destination rank, its run goes straight into
         // that rank's receive buffers (mapped peer memory), cursor d counting in them
-        uint32_t* orec = peer_recs ? peer_recs[d] : out_recs;
-        uint32_t* oid = peer_recs ? peer_ids[d] : out_ids;
+        uint32_t* orec = PEER ? peer_recs[d] : out_recs;
+        uint32_t* oid = PEER ? peer_ids[d] : out_ids;
         V* dst = reinterpret_cast<V*>(orec + o * (uint64_t)RW);
         dst[0] = srec[i * (RW / 4)];
         if (RW == 8) dst[1] = srec[i * 2 + 1];
@@ -697,19 +697,21 @@ cudaError_t launch_rec_scatter(int k, const uint32_t* in_recs, const uint32_t* i
                                uint32_t* const* peer_ids) {
     if (max_tiles == 0) return cudaSuccess;
     cudaError_t e;
-    if (record_words(k) == 4) {
-        const int sm = (int)rec_scatter_smem<4>();
-        if ((e = cudaFuncSetAttribute(k_rec_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-        k_rec_scatter<4><<<(unsigned)max_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, n_tiles_dev, shift, D,
-                                                               cursor, out_recs, out_ids, out_orig_ids, peer_recs,
-                                                               peer_ids);
-    } else {
-        const int sm = (int)rec_scatter_smem<8>();
-        if ((e = cudaFuncSetAttribute(k_rec_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-        k_rec_scatter<8><<<(unsigned)max_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, n_tiles_dev, shift, D,
-                                                               cursor, out_recs, out_ids, out_orig_ids, peer_recs,
-                                                               peer_ids);
-    }
+    auto go = [&](auto kern, int sm) -> cudaError_t {
+        cudaError_t e2;
+        if ((e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e2;
+        kern<<<(unsigned)max_tiles, RS_NT, sm, s>>>(in_recs, in_ids, sig2bin, tiles, n_tiles_dev, shift, D, cursor,
+                                                   out_recs, out_ids, out_orig_ids, peer_recs, peer_ids);
+        return cudaSuccess;
+    };
+    const bool peer = peer_recs != nullptr;
+    if (record_words(k) == 4)
+        e = peer ? go(k_rec_scatter<4, true>, (int)rec_scatter_smem<4>())
+                 : go(k_rec_scatter<4, false>, (int)rec_scatter_smem<4>());
+    else
+        e = peer ? go(k_rec_scatter<8, true>, (int)rec_scatter_smem<8>())
+                 : go(k_rec_scatter<8, false>, (int)rec_scatter_smem<8>());
+    if (e) return e;
     return cudaGetLastError();
 }
 
