@@ -271,48 +271,45 @@ template <class K> struct RadixTile;
 template <> struct RadixTile<uint64_t> { static constexpr int NT = 256, TI = 4096; };
 template <> struct RadixTile<K128> { static constexpr int NT = 256, TI = 2048; };
 
-template <class K>
-__global__ void k_orand(const K* __restrict__ keys, uint64_t n, unsigned long long* red) {
-    uint64_t o = 0, an = ~0ull, oh = 0, ah = ~0ull;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        key_or_and_accum(keys[i], o, an, oh, ah);
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-        o |= __shfl_xor_sync(0xffffffffu, o, s);
-        an &= __shfl_xor_sync(0xffffffffu, an, s);
-        oh |= __shfl_xor_sync(0xffffffffu, oh, s);
-        ah &= __shfl_xor_sync(0xffffffffu, ah, s);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicOr(&red[0], (unsigned long long)o);
-        atomicAnd(&red[1], (unsigned long long)an);
-        atomicOr(&red[2], (unsigned long long)oh);
-        atomicAnd(&red[3], (unsigned long long)ah);
-    }
-}
+// Onesweep-style LSD radix sort (north star: "a device-wide onesweep-style radix pass for
+// large ones"): ONE histogram pass over the keys gives the digit counts of every 8-bit digit
+// position at once (constant digits are skipped); then every varying digit takes ONE kernel:
+// a CTA claims the next tile in order (atomic counter), ranks its keys by the digit in shared
+// memory (stable), publishes its per-digit counts and finds the keys of its digits in all
+// earlier tiles by decoupled look-back (status words flag | pass tag | value: an aggregate, or
+// the inclusive prefix once known), then writes its keys at digit base + prefix + rank.
+constexpr uint64_t OS_AGG = 1ull << 62, OS_PRE = 2ull << 62, OS_VAL = (1ull << 56) - 1;
 
 template <class K>
-__global__ void k_upsweep(const K* __restrict__ keys, uint64_t n, int shift, uint32_t* __restrict__ tile_hist,
-                          uint64_t ntiles) {
-    constexpr int NT = RadixTile<K>::NT, TI = RadixTile<K>::TI;
-    __shared__ uint32_t h[RADIX];
-    for (int d = threadIdx.x; d < RADIX; d += NT) h[d] = 0;
+__global__ void __launch_bounds__(256) k_digit_hist_all(const K* __restrict__ keys, uint64_t n, int npass,
+                                                        uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[16 * RADIX];
+    for (int i = threadIdx.x; i < npass * RADIX; i += 256) h[i] = 0;
     __syncthreads();
-    const uint64_t base = (uint64_t)blockIdx.x * TI;
-    for (int j = threadIdx.x; j < TI; j += NT) {
-        const uint64_t i = base + j;
-        if (i < n) atomicAdd(&h[key_digit(keys[i], shift)], 1u);
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+        const K key = keys[i];
+        for (int p = 0; p < npass; ++p) atomicAdd(&h[p * RADIX + key_digit(key, p * RADIX_BITS)], 1u);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < RADIX; d += NT) tile_hist[(uint64_t)d * ntiles + blockIdx.x] = h[d];
+    for (int i = threadIdx.x; i < npass * RADIX; i += 256)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// bases[p][d] = exclusive scan over d of hist[p][d]; one CTA per digit position
+__global__ void __launch_bounds__(RADIX) k_digit_bases(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases) {
+    __shared__ uint32_t wsum[RADIX / 32 + 1];
+    const uint32_t c = hist[blockIdx.x * RADIX + threadIdx.x];
+    bases[blockIdx.x * RADIX + threadIdx.x] = block_excl_sum<RADIX, uint32_t>(c, wsum, nullptr);
 }
 
 template <class K, bool VALS>
-__global__ void __launch_bounds__(RadixTile<K>::NT) k_downsweep(const K* __restrict__ kin,
-                                                                const uint32_t* __restrict__ vin, K* __restrict__ kout,
-                                                                uint32_t* __restrict__ vout, uint64_t n, int shift,
-                                                                const uint32_t* __restrict__ tile_off, uint64_t ntiles) {
+__global__ void __launch_bounds__(RadixTile<K>::NT) k_onesweep(const K* __restrict__ kin,
+                                                               const uint32_t* __restrict__ vin, K* __restrict__ kout,
+                                                               uint32_t* __restrict__ vout, uint64_t n, int shift,
+                                                               uint64_t tag, const uint32_t* __restrict__ bases,
+                                                               unsigned long long* status, uint32_t* tile_ctr) {
     constexpr int NT = RadixTile<K>::NT, TI = RadixTile<K>::TI, NW = NT / 32;
+    static_assert(NT == RADIX, "one thread per digit in the look-back");
     extern __shared__ __align__(16) uint8_t smem[];
     K* A = reinterpret_cast<K*>(smem);
     K* B = A + TI;
@@ -322,15 +319,41 @@ __global__ void __launch_bounds__(RadixTile<K>::NT) k_downsweep(const K* __restr
     uint32_t* wsum = whist + RADIX * NW;
     uint32_t* dstart = wsum + NW + 1;  // RADIX + 1
     uint32_t* goff = dstart + RADIX + 1;
-    const uint64_t base = (uint64_t)blockIdx.x * TI;
+    __shared__ uint32_t s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);  // tiles claimed in order: look-back never waits on an unscheduled tile
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * TI;
     const int cnt = (int)((n - base) < (uint64_t)TI ? (n - base) : (uint64_t)TI);
     for (int j = threadIdx.x; j < cnt; j += NT) {
         A[j] = kin[base + j];
         if (VALS) VA[j] = vin[base + j];
     }
-    for (int d = threadIdx.x; d < RADIX; d += NT) goff[d] = tile_off[(uint64_t)d * ntiles + blockIdx.x];
     __syncthreads();
     block_digit_pass<K, NT, VALS>(A, B, VA, VB, cnt, shift, whist, wsum, dstart);
+    {
+        const int d = threadIdx.x;
+        const uint64_t mine = dstart[d + 1] - dstart[d];
+        volatile unsigned long long* st = status + tile * RADIX + d;
+        const uint64_t tg = tag << 56;
+        uint64_t excl = 0;
+        if (tile == 0) {
+            *st = OS_PRE | tg | mine;
+        } else {
+            *st = OS_AGG | tg | mine;
+            for (int64_t t = (int64_t)tile - 1; t >= 0;) {
+                // volatile: re-read from L2 on every spin (a plain load may be served by a stale L1 line)
+                const uint64_t v = *reinterpret_cast<volatile unsigned long long*>(status + (uint64_t)t * RADIX + d);
+                if (((v >> 56) & 63) != tag || (v >> 62) == 0) continue;  // not published in this pass yet
+                excl += v & OS_VAL;
+                if ((v >> 62) == 2) break;  // an inclusive prefix: done
+                --t;
+            }
+            *st = OS_PRE | tg | (excl + mine);
+        }
+        goff[d] = bases[d] + (uint32_t)excl;
+    }
+    __syncthreads();
     for (int j = threadIdx.x; j < cnt; j += NT) {
         const K key = B[j];
         const uint32_t d = key_digit(key, shift);
@@ -354,22 +377,25 @@ cudaError_t radix_sort_t(K* keys, uint32_t* vals, uint64_t n, int nbits, const R
     if (n <= 1) return cudaSuccess;
     if (n >= (1ull << 32)) return cudaErrorInvalidValue;
     cudaError_t e;
-    // constant digits are skipped: bitwise OR / AND over all keys
-    if ((e = cudaMemsetAsync(rs.red, 0, 4 * sizeof(unsigned long long), s)) != cudaSuccess) return e;
-    {
-        unsigned long long init[4] = {0ull, ~0ull, 0ull, ~0ull};
-        if ((e = cudaMemcpyAsync(rs.red, init, sizeof(init), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
-    }
-    const unsigned og = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8);
-    k_orand<K><<<og, 256, 0, s>>>(keys, n, rs.red);
-    *launches += 1;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(rs.red_host, rs.red, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s)) !=
-        cudaSuccess)
-        return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    const uint64_t vlo = rs.red_host[0] ^ rs.red_host[1], vhi = rs.red_host[2] ^ rs.red_host[3];
+    const int npass = (nbits + RADIX_BITS - 1) / RADIX_BITS;  // <= 16
     const uint64_t ntiles = (n + TI - 1) / TI;
+    // scratch: tile_off = hist [16][RADIX] | bases [16][RADIX] | tile counters [16];
+    //          tile_hist = look-back status, ntiles x RADIX uint64
+    uint32_t* hist = rs.tile_off;
+    uint32_t* bases = hist + 16 * RADIX;
+    uint32_t* ctrs = bases + 16 * RADIX;
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(rs.tile_hist);
+    if ((e = cudaMemsetAsync(hist, 0, (32 * RADIX + 16) * 4, s))) return e;
+    if ((e = cudaMemsetAsync(status, 0, ntiles * RADIX * 8, s))) return e;
+    const unsigned hg = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 4);
+    k_digit_hist_all<K><<<hg, 256, 0, s>>>(keys, n, npass, hist);
+    k_digit_bases<<<npass, RADIX, 0, s>>>(hist, bases);
+    *launches += 2;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // a digit position is constant iff one digit holds every key: skipped
+    std::vector<uint32_t> hv((size_t)npass * RADIX);
+    if ((e = cudaMemcpyAsync(hv.data(), hist, hv.size() * 4, cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
     K* src = keys;
     K* dst = reinterpret_cast<K*>(rs.keys_alt);
     uint32_t* vsrc = vals;
@@ -377,27 +403,25 @@ cudaError_t radix_sort_t(K* keys, uint32_t* vals, uint64_t n, int nbits, const R
     const bool has_vals = vals != nullptr;
     const size_t sm = has_vals ? downsweep_smem<K, true>() : downsweep_smem<K, false>();
     if (has_vals) {
-        if ((e = cudaFuncSetAttribute(k_downsweep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) !=
-            cudaSuccess)
+        if ((e = cudaFuncSetAttribute(k_onesweep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
             return e;
     } else {
-        if ((e = cudaFuncSetAttribute(k_downsweep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) !=
-            cudaSuccess)
+        if ((e = cudaFuncSetAttribute(k_onesweep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
             return e;
     }
-    for (int shift = 0; shift < nbits; shift += RADIX_BITS) {
-        const bool varies = shift < 64 ? ((vlo >> shift) & 0xFF) != 0 : ((vhi >> (shift - 64)) & 0xFF) != 0;
+    for (int p = 0; p < npass; ++p) {
+        bool varies = true;
+        for (int d = 0; d < RADIX; ++d)
+            if (hv[(size_t)p * RADIX + d] == n) varies = false;
         if (!varies) continue;
-        k_upsweep<K><<<(unsigned)ntiles, NT, 0, s>>>(src, n, shift, rs.tile_hist, ntiles);
-        *launches += 1;
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        if ((e = scan_u32_to_u32(rs.tile_hist, rs.tile_off, RADIX * ntiles, rs.scan_temp, s)) != cudaSuccess) return e;
-        *launches += 2;
+        const int shift = p * RADIX_BITS;
+        const uint64_t tag = (uint64_t)p + 1;
         if (has_vals)
-            k_downsweep<K, true><<<(unsigned)ntiles, NT, sm, s>>>(src, vsrc, dst, vdst, n, shift, rs.tile_off, ntiles);
+            k_onesweep<K, true><<<(unsigned)ntiles, NT, sm, s>>>(src, vsrc, dst, vdst, n, shift, tag,
+                                                                 bases + p * RADIX, status, ctrs + p);
         else
-            k_downsweep<K, false><<<(unsigned)ntiles, NT, sm, s>>>(src, nullptr, dst, nullptr, n, shift, rs.tile_off,
-                                                                   ntiles);
+            k_onesweep<K, false><<<(unsigned)ntiles, NT, sm, s>>>(src, nullptr, dst, nullptr, n, shift, tag,
+                                                                  bases + p * RADIX, status, ctrs + p);
         *launches += 1;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         std::swap(src, dst);
@@ -1268,9 +1292,15 @@ cudaError_t launch_chunk_sort(const void* keys, const Chunk* chunks, uint64_t n_
 uint64_t radix_tile_items(int key_words) { return key_words == 1 ? RadixTile<uint64_t>::TI : RadixTile<K128>::TI; }
 
 size_t radix_scan_temp_bytes(uint64_t n, int key_words) {
-    const uint64_t ntiles = (n + radix_tile_items(key_words) - 1) / radix_tile_items(key_words);
-    return scan_temp_bytes(RADIX * ntiles + 1);
+    (void)n;
+    (void)key_words;
+    return 16;  // the onesweep sort needs no scan scratch
 }
+uint64_t radix_status_words(uint64_t n, int key_words) {
+    const uint64_t ntiles = (n + radix_tile_items(key_words) - 1) / radix_tile_items(key_words);
+    return 2 * RADIX * ntiles + 64;
+}
+uint64_t radix_aux_words() { return 32 * RADIX + 64; }
 
 cudaError_t device_radix_sort(int key_words, void* keys, uint32_t* vals, uint64_t n, int nbits,
                               const RadixScratch& rs, cudaStream_t s, void** res_keys, uint32_t** res_vals,

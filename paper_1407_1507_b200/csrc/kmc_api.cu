@@ -748,9 +748,8 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             ar.release(rs.tile_off);
             ar.release(rs.scan_temp);
             rs.keys_alt = ar.alloc(n * 8);
-            const uint64_t nt = (n + radix_tile_items(1) - 1) / radix_tile_items(1);
-            rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
-            rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+            rs.tile_hist = ar.get<uint32_t>(radix_status_words(n, 1));
+            rs.tile_off = ar.get<uint32_t>(radix_aux_words());
             rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n, 1));
             if (!rs.red) rs.red = ar.get<unsigned long long>(4);
             rs.red_host = hs + 40;
@@ -1255,9 +1254,8 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
                 // fail alike), counted by the device radix sort + run pass
                 RadixScratch rs{};
                 rs.keys_alt = ar.alloc(n_spill * 8);
-                const uint64_t nt = (n_spill + radix_tile_items(1) - 1) / radix_tile_items(1);
-                rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
-                rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+                rs.tile_hist = ar.get<uint32_t>(radix_status_words(n_spill, 1));
+                rs.tile_off = ar.get<uint32_t>(radix_aux_words());
                 rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n_spill, 1));
                 rs.red = ar.get<unsigned long long>(4);
                 rs.red_host = hs + 40;
@@ -1305,9 +1303,8 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
         j->stage_end(2);
         RadixScratch rs{};
         rs.keys_alt = ar.alloc(large_windows * ksz);
-        const uint64_t nt = (large_windows + radix_tile_items(kw) - 1) / radix_tile_items(kw);
-        rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
-        rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+        rs.tile_hist = ar.get<uint32_t>(radix_status_words(large_windows, kw));
+        rs.tile_off = ar.get<uint32_t>(radix_aux_words());
         rs.scan_temp = ar.alloc(radix_scan_temp_bytes(large_windows, kw));
         rs.red = ar.get<unsigned long long>(4);
         rs.red_host = hs + 40;
@@ -1499,9 +1496,8 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
                     ar.release(rs.tile_off);
                     ar.release(rs.scan_temp);
                     rs.keys_alt = ar.alloc(maxn * ksz);
-                    const uint64_t nt = (maxn + radix_tile_items(kw) - 1) / radix_tile_items(kw);
-                    rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
-                    rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+                    rs.tile_hist = ar.get<uint32_t>(radix_status_words(maxn, kw));
+                    rs.tile_off = ar.get<uint32_t>(radix_aux_words());
                     rs.scan_temp = ar.alloc(radix_scan_temp_bytes(maxn, kw));
                     if (!rs.red) rs.red = ar.get<unsigned long long>(4);
                     rs.red_host = hs + 40;
@@ -1596,9 +1592,8 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
         RadixScratch rs{};
         rs.keys_alt = ar.alloc(tot * ksz);
         rs.vals_alt = ar.get<uint32_t>(tot);
-        const uint64_t nt = (tot + radix_tile_items(kw) - 1) / radix_tile_items(kw);
-        rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
-        rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+        rs.tile_hist = ar.get<uint32_t>(radix_status_words(tot, kw));
+        rs.tile_off = ar.get<uint32_t>(radix_aux_words());
         rs.scan_temp = ar.alloc(radix_scan_temp_bytes(tot, kw));
         rs.red = ar.get<unsigned long long>(4);
         rs.red_host = j->host_small + 40;
@@ -2237,9 +2232,8 @@ kmc_status kmc_write_db(const void* kmers, const uint32_t* counts, uint64_t n, i
             RadixScratch rs{};
             rs.keys_alt = ar.alloc(n * 8);
             rs.vals_alt = ar.get<uint32_t>(n);
-            const uint64_t nt = (n + radix_tile_items(1) - 1) / radix_tile_items(1);
-            rs.tile_hist = ar.get<uint32_t>(RADIX * nt + 1);
-            rs.tile_off = ar.get<uint32_t>(RADIX * nt + 1);
+            rs.tile_hist = ar.get<uint32_t>(radix_status_words(n, 1));
+            rs.tile_off = ar.get<uint32_t>(radix_aux_words());
             rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n, 1));
             rs.red = ar.get<unsigned long long>(4);
             unsigned long long* red_host = nullptr;

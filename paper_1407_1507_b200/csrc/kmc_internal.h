@@ -268,14 +268,18 @@ cudaError_t launch_cluster_count(const uint32_t* bins, const ClItem* citems, uin
 struct RadixScratch {
     void* keys_alt;
     uint32_t* vals_alt;
-    uint32_t* tile_hist;   // RADIX * ntiles
-    uint32_t* tile_off;    // RADIX * ntiles
+    uint32_t* tile_hist;   // radix_status_words(n): the onesweep look-back status
+    uint32_t* tile_off;    // radix_aux_words(): per-pass digit histograms, bases, tile counters
     void* scan_temp;
     unsigned long long* red;  // 4 entries
     unsigned long long* red_host;  // pinned 4 entries
 };
 uint64_t radix_tile_items(int key_words);
 size_t radix_scan_temp_bytes(uint64_t n, int key_words);
+// onesweep scratch: tile_hist needs radix_status_words(n) uint32 (look-back status), tile_off
+// radix_aux_words() uint32 (per-pass histograms, digit bases, tile counters)
+uint64_t radix_status_words(uint64_t n, int key_words);
+uint64_t radix_aux_words();
 // KMC 2 database writer (k_db.cu; Suppl. Sec. 4; reading R-DB)
 int db_group_shift(int p);
 uint64_t db_n_arrays(int p);
