@@ -38,7 +38,9 @@ constexpr uint32_t INV = 0xFFFFFFFFu;
 constexpr uint32_t TMP_BLK = 2048;            // temporary-stream records reserved per warp at a time
 
 struct WarpSmem {
-    uint32_t pk[NPK];    // 2-bit codes, 16 per word, MSB first (local base x: word x/16)
+    uint32_t pk[2][NPK]; // 2-bit codes, 16 per word, MSB first (local base x: word x/16); two
+                         // segments: runs carried over from the previous one are emitted with
+                         // the next one's
     uint32_t inv[NMW];   // bit x: local base x is not A/C/G/T (or outside the stream)
     uint32_t bad[NMW];   // bit x: invalid, or a read starts at x
     uint32_t vwin[NMW];  // bit x: the k-mer window starting at local x is valid
@@ -47,6 +49,7 @@ struct WarpSmem {
     // phase D: keys (KS, 18 * 32 positions) and block prefix minima (PS, + overrun slack);
     // phases F-G: signature of each run start (xs[0, SEG)) and run starts (xs[SEG, 2 SEG))
     alignas(16) uint32_t xs[NROW * 32 + NROW * 32 + 64];
+    uint32_t pv[32], ps[32], pn[32];  // carried-over runs: first window, signature, windows
 };
 static_assert(NROW * 32 * 2 + 64 >= 2 * SEG, "run lists fit the phase-D scratch");
 static_assert(NROW == 18, "the block minimum uses 32 lanes x 18 positions");
@@ -136,7 +139,11 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
     bool tmp_ok = a.tmp_recs != nullptr;
 
     const uint64_t gw = (uint64_t)blockIdx.x * SG_WARPS + warp, nw = (uint64_t)gridDim.x * SG_WARPS;
-    for (uint64_t sg = gw; sg < n_segs; sg += nw) {
+    int npend = 0;      // runs of the previous segment waiting for a full round of 32 lanes
+    uint32_t pbuf = 0;  // this segment's packed-base buffer
+    for (uint64_t sg = gw; sg < n_segs; sg += nw, pbuf ^= 1u) {
+        uint32_t* PK = S.pk[pbuf];
+        const uint32_t* PKprev = S.pk[pbuf ^ 1u];
         const int64_t seg0 = (int64_t)sg * SEG;
         const int64_t lbase = seg0 - HL;  // stream position of local base 0
         const uint64_t r_first = a.tile_r_lo[sg];
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             }
             uint32_t packed, invbits;
             encode16(wd, packed, invbits);
-            S.pk[t] = packed;
+            PK[t] = packed;
             reinterpret_cast<uint16_t*>(S.inv)[t] = (uint16_t)invbits;
             if (t >= 1) {  // the segment's own bases: local [HL, HL + SEG) = chunks 1 .. SEG/16
                 uint32_t m = invbits;
@@ -198,7 +205,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             iv |= __shfl_xor_sync(0xffffffffu, iv, 1);
             iv |= __shfl_xor_sync(0xffffffffu, iv, 2);
             if (lane < NTW) {
-                reinterpret_cast<uint8_t*>(S.pk)[4 * t + 3 - u] = (uint8_t)p8;
+                reinterpret_cast<uint8_t*>(PK)[4 * t + 3 - u] = (uint8_t)p8;
                 if (u == 0) reinterpret_cast<uint16_t*>(S.inv)[t] = (uint16_t)iv;
                 if (t == SEG / 16) {  // the last chunk of the segment's own bases
                     uint32_t m = i4;
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                 }
             }
         }
-        if (lane < NPK - NBASE / 16) S.pk[NBASE / 16 + lane] = 0;
+        if (lane < NPK - NBASE / 16) PK[NBASE / 16 + lane] = 0;
         if (lane == 0) reinterpret_cast<uint16_t*>(S.inv)[NBASE / 16] = 0xFFFFu;  // NBASE = 16 mod 32
         __syncwarp();
         for (int w = lane; w < NMW; w += 32) {
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
         {
             const int j0 = 15 + y0;  // local base of position y0
             const int w0 = j0 >> 4, sh = 2 * (j0 & 15);
-            const uint32_t W0 = S.pk[w0], W1 = S.pk[w0 + 1], W2 = S.pk[w0 + 2];
+            const uint32_t W0 = PK[w0], W1 = PK[w0 + 1], W2 = PK[w0 + 2];
             const uint32_t sA = __funnelshift_l(W1, W0, sh), sB = __funnelshift_l(W2, W1, sh);  // X = sA:sB
             const uint32_t Rlo = rev2_32(~sA), Rhi = rev2_32(~sB);
             const uint32_t pvb = __funnelshift_r(S.vpm[j0 >> 5], S.vpm[(j0 >> 5) + 1], j0 & 31);
@@ -408,23 +415,42 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             l_skm += nstarts;        // starts that are super-k-mer starts (the edge one corrected above)
         }
         __syncwarp();
-        for (int i0 = 0; i0 < nstarts; i0 += 32) {
+        // G: records of the runs, 32 runs per round.  The runs of this segment follow the ones
+        // carried over from the previous segment; only full rounds are emitted, and the rest
+        // (< 32 runs of this segment) wait for the next segment -- a segment holds ~37 runs,
+        // so a second round per segment would run mostly idle.  The last segment of the warp
+        // (or one whose runs do not fill a round together with the carried ones) emits all.
+        auto run_windows = [&](int v) {  // distance from window v to the next end mark
+            const int pos = v + 1;
+            int wd = pos >> 5;
+            uint32_t bits = S.ebits[wd] & (0xFFFFFFFFu << (pos & 31));
+            while (bits == 0) bits = S.ebits[++wd];
+            return (wd * 32 + __ffs(bits) - 1) - v;
+        };
+        const int total = npend + nstarts;
+        int emit_end = (sg + nw >= n_segs) ? total : (total / 32) * 32;
+        if (emit_end < npend) emit_end = total;
+        for (int i0 = 0; i0 < emit_end; i0 += 32) {
             const int idx = i0 + lane;
             uint32_t s = INV;
             int v = 0, n = 0, nrec = 0;
-            if (idx < nstarts) {
-                v = (int)list[idx];
-                s = lsig[idx];
-                const int pos = v + 1;
-                int wd = pos >> 5;
-                uint32_t bits = S.ebits[wd] & (0xFFFFFFFFu << (pos & 31));
-                while (bits == 0) bits = S.ebits[++wd];
-                n = (wd * 32 + __ffs(bits) - 1) - v;
+            const uint32_t* pkb = PK;
+            if (idx < emit_end) {
+                if (idx < npend) {
+                    v = (int)S.pv[idx];
+                    s = S.ps[idx];
+                    n = (int)S.pn[idx];
+                    pkb = PKprev;
+                } else {
+                    v = (int)list[idx - npend];
+                    s = lsig[idx - npend];
+                    n = run_windows(v);
+                }
                 nrec = (int)(((uint32_t)(n + maxw - 1) * maxw_magic) >> 20);  // exact: (n+maxw)*maxw < 2^20
                 l_windows += n;
                 l_recs += nrec;
             }
-            if (MODE == P1_MODE_HIST && idx < nstarts) {
+            if (MODE == P1_MODE_HIST && idx < emit_end) {
                 atomicAdd(&a.hist_w[s], (unsigned long long)n);
                 atomicAdd(&a.hist_r[s], (uint32_t)nrec);
             }
@@ -446,7 +472,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                 slot0 = blk_cur + inc - nrec;
                 blk_cur += tot;
             }
-            if (idx < nstarts && (MODE == P1_MODE_SCATTER || tmp_ok)) {
+            if (idx < emit_end && (MODE == P1_MODE_SCATTER || tmp_ok)) {
                 const int j = v + n;
                 uint32_t bin = 0;
                 uint64_t bbase = 0;
@@ -466,7 +492,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                     for (int u = 0; u < 8; ++u) {
                         if (u >= RW) break;
                         const int bb = b0 + (u == 0 ? 0 : 12 + 16 * (u - 1));
-                        const uint32_t x = __funnelshift_l(S.pk[(bb >> 4) + 1], S.pk[bb >> 4], 2 * (bb & 15));
+                        const uint32_t x = __funnelshift_l(pkb[(bb >> 4) + 1], pkb[bb >> 4], 2 * (bb & 15));
                         wd[u] = (u == 0) ? (((uint32_t)m << 24) | (x >> 8)) : x;
                     }
                     uint64_t slot;
@@ -485,6 +511,17 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                 }
             }
         }
+        __syncwarp();
+        // carry the rest (runs of this segment only: emit_end >= npend) to the next segment
+        const int carry = total - emit_end;
+        if (lane < carry) {
+            const int jj = emit_end + lane - npend;
+            const int v = (int)list[jj];
+            S.pv[lane] = (uint32_t)v;
+            S.ps[lane] = lsig[jj];
+            S.pn[lane] = (uint32_t)run_windows(v);
+        }
+        npend = carry;
         __syncwarp();
     }
     if (MODE == P1_MODE_DEBUG) return;
