@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 SO = os.path.join(PKG, "libkmcgpu.so")
-SOURCES = ["k_distribute.cu", "k_plan.cu", "k_sort.cu", "k_cluster.cu", "k_split1.cu", "k_kxmer.cu", "k_order.cu", "k_db.cu", "kmc_api.cu"]
+SOURCES = ["k_distribute.cu", "k_plan.cu", "k_sort.cu", "k_cluster.cu", "k_split1.cu", "k_subsplit.cu", "k_kxmer.cu", "k_order.cu", "k_db.cu", "kmc_api.cu"]
 HEADERS = ["kmc_device.cuh", "kmc_internal.h", "kmc_scan.cuh"]
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

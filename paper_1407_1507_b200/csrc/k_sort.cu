@@ -90,26 +90,6 @@ __device__ __forceinline__ void block_rle_emit(const K* S, int n, uint32_t* cnt,
     }
 }
 
-constexpr int PROBE_MAX = 256;
-
-// Counts key; false if no slot was found within PROBE_MAX probes (table too full).
-template <class K>
-__device__ __forceinline__ bool table_insert_bounded(K* T, uint32_t* C, int lg, const K& key) {
-    const uint32_t mask = (1u << lg) - 1;
-    const K E = key_empty<K>();
-    uint32_t s = slot_hash(key, lg);
-    for (int pr = 0; pr < PROBE_MAX; ++pr) {
-        // one shared CAS per probe: it claims an empty slot, or returns the key that holds it
-        const K old = smem_cas_empty(&T[s], key);
-        if (key_eq(old, E) || key_eq(old, key)) {
-            atomicAdd(&C[s], 1u);
-            return true;
-        }
-        s = (s + 1) & mask;
-    }
-    return false;
-}
-
 // Small-bin table: the B region (CAP keys) once the records are expanded, as 2^lg key slots +
 // 2^lg uint32 counters.
 template <class K> struct SmallSlots;

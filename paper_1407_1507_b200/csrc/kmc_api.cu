@@ -861,6 +861,241 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
     ar.release(rs.scan_temp);
 }
 
+// Large bins through sub-signatures (k_subsplit.cu, large_path 4): a bin of W windows gets
+// nd ~ W / kcap digits; k_subsplit cuts its records into sub-records by digit, k_subcount
+// counts every digit in one CTA's SMEM hash table (in hash-range rounds when its distinct keys
+// overflow the table).  A digit's sub-records fill its region (sized for 1 sub-record per 3
+// windows: C4 has 5.3), then pool blocks claimed on the device; digits whose sub-records
+// overflowed their block table -- and the overflow list -- are expanded and counted by the
+// device radix sort.  Bins are processed in groups whose regions fit the device.
+void large_subsplit(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vector<uint64_t>& large_ids, int kcap) {
+    const int k = j->k;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    unsigned long long* hs = j->host_small;
+    unsigned long long* gstats = c.gstats;
+    const std::vector<uint64_t>& bw = c.bw;
+    const std::vector<uint64_t>& bn = c.bn;
+    const std::vector<uint64_t>& bo = c.bo;
+    const double target = std::max(1.0, (double)kcap);
+    const uint32_t rpp = (uint32_t)subsplit_piece_records(k);
+    const size_t nl = large_ids.size();
+    std::vector<uint32_t> nd(nl), rc(nl);
+    uint64_t total_slots = 0;
+    for (size_t i = 0; i < nl; ++i) {
+        const uint64_t b = large_ids[i];
+        uint64_t d = (uint64_t)std::ceil((double)bw[b] / target);
+        d = std::min<uint64_t>(std::max<uint64_t>(d, 1), (uint64_t)SS_DMAX);
+        nd[i] = (uint32_t)d;
+        const uint64_t r = (bw[b] / d) / 3 + 32;
+        rc[i] = (uint32_t)std::min<uint64_t>(r, 1u << 30);
+        total_slots += d * rc[i];
+    }
+    const size_t slot_bytes = 16;
+    // group budget in region slots: the option, else everything if the pool can be allocated,
+    // else half the free device memory
+    uint64_t budget = j->opt.large_group_mkeys ? (((uint64_t)j->opt.large_group_mkeys << 20) / 3 + 1) : ~0ull;
+    uint64_t n_blocks = std::max<uint64_t>(256, total_slots / 16 / SS_BLK);  // extra blocks (lumpy digits)
+    void* pool = nullptr;
+    uint64_t pool_slots = 0;
+    if (!j->opt.large_group_mkeys) {
+        pool = ar.try_alloc((total_slots + n_blocks * SS_BLK) * slot_bytes);
+        if (pool) {
+            pool_slots = total_slots;
+        } else {
+            size_t fr = 0, tot = 0;
+            CK(cudaMemGetInfo(&fr, &tot));
+            budget = std::max<uint64_t>((uint64_t)(fr / 2) / slot_bytes, 1u << 16);
+        }
+    }
+    std::vector<std::pair<size_t, size_t>> groups;
+    uint64_t max_gs = 0, max_gd = 0, max_gp = 0, max_gn = 0;
+    for (size_t i0 = 0; i0 < nl;) {
+        uint64_t gs = 0, gd = 0, gp = 0;
+        size_t i1 = i0;
+        while (i1 < nl) {
+            const uint64_t need = (uint64_t)nd[i1] * rc[i1];
+            if (i1 > i0 && gs + need > budget) break;
+            gs += need;
+            gd += nd[i1];
+            gp += (bn[large_ids[i1]] + rpp - 1) / rpp;
+            ++i1;
+        }
+        groups.push_back({i0, i1});
+        max_gs = std::max(max_gs, gs);
+        max_gd = std::max(max_gd, gd);
+        max_gp = std::max(max_gp, gp);
+        max_gn = std::max<uint64_t>(max_gn, i1 - i0);
+        i0 = i1;
+    }
+    j->st.n_large_groups += groups.size();
+    if (!pool) {
+        pool_slots = max_gs;
+        n_blocks = std::max<uint64_t>(256, max_gs / 16 / SS_BLK);
+        pool = ar.alloc((pool_slots + n_blocks * SS_BLK) * slot_bytes);
+    }
+    SSBin* d_sbins = ar.get<SSBin>(max_gn);
+    LargeBin* d_lbins = ar.get<LargeBin>(max_gn);
+    uint64_t* d_pp = ar.get<uint64_t>(max_gn + 1);
+    Piece* d_pieces = ar.get<Piece>(max_gp);
+    uint32_t* cur = ar.get<uint32_t>(2 * max_gd);  // sub-records, then windows per digit
+    uint32_t* btab = ar.get<uint32_t>(max_gd * SS_MAXB);
+    uint32_t* fb = ar.get<uint32_t>(max_gd);
+    uint2* dinfo = ar.get<uint2>(max_gd);
+    uint32_t* drc = ar.get<uint32_t>(max_gd);
+    unsigned long long* ctr = ar.get<unsigned long long>(4);  // blocks, overflow sub-records, fallback digits, error
+    uint64_t ovf_cap = 1u << 16;
+    uint4* ovf = ar.get<uint4>(ovf_cap);
+    static thread_local std::vector<LargeBin> lbins;
+    static thread_local std::vector<SSBin> sbins;
+    static thread_local std::vector<uint64_t> pp;
+    for (const auto& g : groups) {
+        const size_t gn = g.second - g.first;
+        lbins.resize(gn);
+        sbins.resize(gn);
+        pp.assign(gn + 1, 0);
+        uint32_t dbase = 0;
+        uint64_t rbase = 0;
+        for (size_t i = 0; i < gn; ++i) {
+            const size_t li = g.first + i;
+            const uint64_t b = large_ids[li];
+            lbins[i] = LargeBin{0, 0, bo[b], 0, (uint32_t)bw[b], 0, (uint32_t)bn[b], 0, 0, 0};
+            sbins[i] = SSBin{rbase, nd[li], dbase, rc[li], 0};
+            dbase += nd[li];
+            rbase += (uint64_t)nd[li] * rc[li];
+            pp[i + 1] = pp[i] + (bn[b] + rpp - 1) / rpp;
+        }
+        const uint64_t n_pieces = pp.back();
+        CK(cudaMemcpyAsync(d_lbins, lbins.data(), gn * sizeof(LargeBin), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_sbins, sbins.data(), gn * sizeof(SSBin), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
+        uint64_t n_ovs = 0;
+        for (;;) {
+            j->stage_begin(KMC_STAGE_LARGE_SCATTER);
+            CK(cudaMemsetAsync(cur, 0, (size_t)dbase * 8, s));
+            CK(cudaMemsetAsync(btab, 0, (size_t)dbase * SS_MAXB * 4, s));
+            CK(cudaMemsetAsync(ctr, 0, 32, s));
+            CK(launch_make_pieces(d_lbins, d_pp, gn, rpp, d_pieces, s));
+            CK(launch_subsplit(bins, d_pieces, n_pieces, d_sbins, k, cur, cur + dbase, btab, pool, pool_slots, n_blocks,
+                               ovf, ovf_cap, ctr, 2 * n_sms(), s));
+            j->launches += 2;
+            j->stage_end(2);
+            CK(cudaMemcpyAsync(&hs[48], ctr, 16, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            const uint64_t used = hs[48];
+            n_ovs = hs[49];
+            if (used <= n_blocks && n_ovs <= ovf_cap) break;
+            // the extra blocks (or the overflow list) were too few: the same amount on a rerun
+            // (it depends only on the records), so grow them and split the group again
+            if (used > n_blocks) {
+                ar.release(pool);
+                n_blocks = used + used / 8 + 64;
+                pool = ar.alloc((pool_slots + n_blocks * SS_BLK) * slot_bytes);
+            }
+            if (n_ovs > ovf_cap) {
+                ar.release(ovf);
+                ovf_cap = n_ovs + n_ovs / 8 + 1024;
+                ovf = ar.get<uint4>(ovf_cap);
+            }
+        }
+        j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
+        CK(launch_subcount(pool, pool_slots, d_sbins, (uint32_t)gn, dinfo, drc, cur, cur + dbase, btab, dbase, k,
+                           !j->opt.non_canonical, j->ci, j->cx, (uint64_t*)j->surv_keys, j->surv_counts, gstats, fb,
+                           ctr + 2, n_sms(), s));
+        j->launches += 2;
+        j->stage_end(2);
+        CK(cudaMemcpyAsync(&hs[52], ctr + 2, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t n_fb = hs[52];
+        if (hs[53]) {
+            set_err("sub-signature count: a digit overflowed 2^20 hash-range rounds");
+            throw Fail{KMC_ERR_INTERNAL};
+        }
+        if (n_fb == 0) continue;
+        // ---- fallback: the listed digits' sub-records (region, extra blocks, the overflow
+        // list) are expanded into keys and counted by the device radix sort (digits partition
+        // the keys, so one sort of their union counts each of them)
+        int fl = 0;
+        j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
+        std::vector<uint32_t> fd(n_fb), fn(n_fb), fw(n_fb);
+        CK(cudaMemcpyAsync(fd.data(), fb, n_fb * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<uint32_t> tabs(n_fb * (size_t)SS_MAXB);
+        for (uint64_t i = 0; i < n_fb; ++i) {
+            CK(cudaMemcpyAsync(&fn[i], cur + fd[i], 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&fw[i], cur + dbase + fd[i], 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(tabs.data() + i * SS_MAXB, btab + (size_t)fd[i] * SS_MAXB, SS_MAXB * 4,
+                               cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
+        uint64_t nsub = n_ovs, nkeys = 0;
+        for (uint64_t i = 0; i < n_fb; ++i) {
+            const size_t bi = std::upper_bound(sbins.begin(), sbins.end(), fd[i],
+                                               [](uint32_t d, const SSBin& x) { return d < x.dbase; }) -
+                              sbins.begin() - 1;
+            nsub += std::min<uint64_t>(fn[i], (uint64_t)sbins[bi].rc + (uint64_t)SS_MAXB * SS_BLK);
+            nkeys += fw[i];
+        }
+        j->st.n_split_overflow += nkeys;
+        uint4* subs = ar.get<uint4>(nsub + 1);
+        uint64_t o = 0;
+        for (uint64_t i = 0; i < n_fb; ++i) {
+            const size_t bi = std::upper_bound(sbins.begin(), sbins.end(), fd[i],
+                                               [](uint32_t d, const SSBin& x) { return d < x.dbase; }) -
+                              sbins.begin() - 1;
+            const SSBin& sb = sbins[bi];
+            const uint64_t m = std::min<uint64_t>(fn[i], (uint64_t)sb.rc + (uint64_t)SS_MAXB * SS_BLK);
+            const uint64_t mr = std::min<uint64_t>(m, sb.rc);
+            CK(cudaMemcpyAsync(subs + o, (uint4*)pool + sb.rbase + (uint64_t)(fd[i] - sb.dbase) * sb.rc, mr * 16,
+                               cudaMemcpyDeviceToDevice, s));
+            o += mr;
+            for (uint64_t q = 0; mr + q * SS_BLK < m; ++q) {
+                const uint64_t e = std::min<uint64_t>(SS_BLK, m - mr - q * SS_BLK);
+                CK(cudaMemcpyAsync(subs + o, (uint4*)pool + pool_slots + (uint64_t)(tabs[i * SS_MAXB + q] - 1) * SS_BLK,
+                                   e * 16, cudaMemcpyDeviceToDevice, s));
+                o += e;
+            }
+        }
+        if (n_ovs) CK(cudaMemcpyAsync(subs + o, ovf, n_ovs * 16, cudaMemcpyDeviceToDevice, s));
+        o += n_ovs;
+        // pieces of PIECE_RECORDS sub-records over the gathered array
+        std::vector<Piece> pcs;
+        for (uint64_t q = 0; q < o; q += PIECE_RECORDS)
+            pcs.push_back(Piece{q, (uint32_t)std::min<uint64_t>(PIECE_RECORDS, o - q), 0});
+        Piece* d_fp = ar.get<Piece>(pcs.size());
+        CK(cudaMemcpyAsync(d_fp, pcs.data(), pcs.size() * sizeof(Piece), cudaMemcpyHostToDevice, s));
+        uint64_t* keys = ar.get<uint64_t>(nkeys + 1);
+        CK(cudaMemsetAsync(gstats + GS_LARGE_KEYS, 0, 8, s));
+        CK(launch_large_expand((const uint32_t*)subs, d_fp, pcs.size(), k, !j->opt.non_canonical, keys, gstats, s));
+        ++fl;
+        RadixScratch rs{};
+        rs.keys_alt = ar.alloc(nkeys * 8 + 8);
+        rs.tile_hist = ar.get<uint32_t>(radix_status_words(nkeys, 1));
+        rs.tile_off = ar.get<uint32_t>(radix_aux_words());
+        rs.scan_temp = ar.alloc(radix_scan_temp_bytes(nkeys, 1));
+        rs.red = ar.get<unsigned long long>(4);
+        rs.red_host = hs + 40;
+        void* sorted = nullptr;
+        uint32_t* dummy = nullptr;
+        CK(device_radix_sort(1, keys, nullptr, nkeys, 2 * k, rs, s, &sorted, &dummy, &fl));
+        CK(launch_rle(1, sorted, nkeys, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+        ++fl;
+        j->launches += fl;
+        j->stage_end(fl);
+        CK(cudaStreamSynchronize(s));  // the host vectors above are released on return
+        ar.release(subs);
+        ar.release(d_fp);
+        ar.release(keys);
+        ar.release(rs.keys_alt);
+        ar.release(rs.tile_hist);
+        ar.release(rs.tile_off);
+        ar.release(rs.scan_temp);
+        ar.release(rs.red);
+    }
+    ar.release(pool);
+    ar.release(ovf);
+}
+
 // S5-S8 from the record stream in c (tmp_recs / tmp_sig, tmp_n slots) and the plan:
 // bins, then small and large bins counted into the survivor buffer.
 void count_phase(kmc_job* j, PlanCtx& c) {
@@ -1321,6 +1556,11 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
         ar.release(rs.tile_hist);
         ar.release(rs.tile_off);
         ar.release(rs.scan_temp);
+    } else if (large_windows > 0 && k >= SS_KMIN && k <= SS_KMAX && j->opt.large_path == 4 &&
+               j->opt.count_path != 1) {
+        const int kcap = chunk_cap();
+        j->st.chunk_capacity = (uint64_t)kcap;
+        large_subsplit(j, c, bins, large_ids, kcap);
     } else if (large_windows > 0 && k <= 32 && j->opt.large_path == 0 && j->opt.count_path != 1) {
         const int kcap = chunk_cap();
         j->st.chunk_capacity = (uint64_t)kcap;
@@ -1530,6 +1770,7 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
     j->st.n_small_sorted = hs[16 + GS_SMALL_SORTED];
     j->st.n_kxmers = hs[16 + GS_KX];
     j->st.kx_windows = hs[16 + GS_KX_WIN];
+    j->st.n_overflow_chunks += hs[16 + GS_SUB_OVF];
     if (j->opt.large_path == 1 && hs[16 + GS_LARGE_KEYS] != large_windows) {
         set_err("large-bin expansion produced %llu keys, plan says %llu", (unsigned long long)hs[16 + GS_LARGE_KEYS],
                 (unsigned long long)large_windows);

@@ -24,6 +24,7 @@ enum {
     GS_SMALL_SORTED = 12,  // small bins whose hash table overflowed (sorted instead)
     GS_KX = 13,            // (k,x)-mers sorted (kx path)
     GS_KX_WIN = 14,        // windows of the bins counted through (k,x)-mers
+    GS_SUB_OVF = 15,       // sub-signature digits whose table overflowed (counted in rounds)
     GS_N = 16
 };
 
@@ -243,6 +244,37 @@ cudaError_t launch_split1(const uint32_t* bins, const Piece* pieces, uint64_t n_
 // ctr[0] chunks, ctr[1] oversize (> hard_cap), ctr[2] overflowed digits (region parts in ovd)
 cudaError_t launch_split1_chunks(const S1Bin* sbins, uint64_t n_bins, const uint32_t* cur, uint32_t hard_cap,
                                  Chunk* chunks, Chunk* over, Chunk* ovd, unsigned long long* ctr, cudaStream_t s);
+
+// S6-S8 of the large bins through sub-signatures (k_subsplit.cu, large_path 4, SS_KMIN <= k <=
+// SS_KMAX): bin b gets nd digits, digit = hash of the window's sub-signature (the minimum
+// hashed canonical q-mer); the sub-records (bin record format, 16 bytes) of a digit fill its
+// region of rc slots, then pool blocks of SS_BLK slots from the digit's block table (at most
+// SS_MAXB; btab[digit * SS_MAXB + i] = block id + 1, block j = slots xbase + j * SS_BLK of the
+// same array), then the overflow list.
+constexpr int SS_KMIN = 22, SS_KMAX = 32;
+constexpr int SS_BLK = 512;
+constexpr int SS_MAXB = 64;
+constexpr int SS_DMAX = 256;
+struct SSBin {
+    uint64_t rbase;  // slot of the bin's digit 0 region; digit d's region starts at rbase + d * rc
+    uint32_t nd, dbase, rc, pad;
+};
+int subsplit_piece_records(int k);
+// cur / cur_w: sub-records / windows per digit (zeroed); btab: zeroed; ctr[0] pool blocks
+// claimed (> n_blocks: rerun with a larger pool), ctr[1] sub-records beyond the block tables
+// (written to ovf while below ovf_cap)
+cudaError_t launch_subsplit(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const SSBin* sbins, int k,
+                            uint32_t* cur, uint32_t* cur_w, uint32_t* btab, void* pool, uint64_t xbase,
+                            uint64_t n_blocks, void* ovf, uint64_t ovf_cap, unsigned long long* ctr, int n_ctas,
+                            cudaStream_t s);
+// fb_list / fb_ctr[0]: digits whose sub-records overflowed the block table (for the
+// fallback); fb_ctr[1] = 1 if a digit could not be counted in 2^20 rounds (internal error)
+// dinfo / drc: n_digits scratch entries (each digit's region, filled here)
+cudaError_t launch_subcount(const void* pool, uint64_t xbase, const SSBin* sbins, uint32_t n_bins, uint2* dinfo,
+                            uint32_t* drc, const uint32_t* cur, const uint32_t* cur_w, const uint32_t* btab, uint32_t n_digits, int k, int canonical,
+                            uint32_t ci, uint32_t cx, uint64_t* surv_keys, uint32_t* surv_counts,
+                            unsigned long long* gstats, uint32_t* fb_list, unsigned long long* fb_ctr, int n_sms,
+                            cudaStream_t s);
 
 // S6-S8 of the large bins by thread-block clusters (k_cluster.cu, k <= 32): a cluster item is
 // (bin, round r of R) counted by all CTAs of a cluster with keys routed to their owner CTA

@@ -14,6 +14,6 @@ r = torch.from_numpy(w.reads).cuda()
 o = torch.from_numpy(w.offsets.view(np.uint64)).cuda()
 kmc.use_torch_allocator(True)
 for _ in range(calls):
-    res = kmc.count(r, o, w.k, w.p, w.cutoff_min, w.cutoff_max, profile=True)
+    res = kmc.count(r, o, w.k, w.p, w.cutoff_min, w.cutoff_max, profile=True, **eval(os.environ.get('KMC_OPTS', 'dict()')))
 torch.cuda.synchronize()
-print({k: round(v, 3) for k, v in res.stats["stage_ms"].items()}, res.stats["n_out"])
+print({k: round(v, 3) for k, v in res.stats["stage_ms"].items()}, res.stats["n_out"], res.stats["n_overflow_chunks"])
