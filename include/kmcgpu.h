@@ -130,6 +130,8 @@ typedef struct {
                                   n_kxmers / kx_windows */
     uint64_t kx_windows;       /* windows of the bins counted through (k,x)-mers (the small bins) */
     uint64_t n_passes;         /* passes over bin ranges (host-resident reads beyond HBM); 1 = one pass */
+    uint64_t n_distribute_reruns; /* sampled distribution: 1 if a bin overflowed its sampled capacity
+                                  and pass 1 was repeated on the exact plan */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;
@@ -147,8 +149,12 @@ typedef struct {
                                   thread-block clusters count each large bin in their CTAs'
                                   shared-memory tables, keys routed to their owner CTA through
                                   distributed shared memory -- no key spill to HBM */
-    uint32_t distribute_path;  /* 0: pass 1 streams its records, S5 copies them into bins (default);
-                                  1: S5 recomputes pass 1 from the reads (testing) */
+    uint32_t distribute_path;  /* 0 (default): inputs of >= 64 Mi bases take the sampled distribution
+                                  (2), smaller ones the record stream: pass 1 streams its records
+                                  and S5 copies them into bins.  1: S5 recomputes pass 1 from the
+                                  reads (testing).  2: always sampled -- the bin plan comes from a
+                                  sample of the reads and pass 1 writes every record
+                                  straight into its bin (no record stream, no S5 copy) */
     uint32_t input_batch_mb;   /* host-resident reads are streamed through pass 1 in read-aligned
                                   batches of this many MiB (0 = default 1024), double-buffered so
                                   the H2D copy of batch i+1 overlaps pass 1 on batch i */

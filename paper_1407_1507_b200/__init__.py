@@ -37,7 +37,7 @@ class _Stats(ctypes.Structure):
         "n_below_min", "n_above_max", "n_out", "n_launches", "n_input_batches", "n_large_groups",
         "chunk_capacity", "n_overflow_chunks", "n_order_oversize", "max_signature_windows", "n_small_sorted",
         "n_cluster_items", "n_single_items", "n_spilled_keys", "cluster_size", "cluster_ctas",
-        "n_split_overflow", "n_kxmers", "kx_windows", "n_passes")] + [
+        "n_split_overflow", "n_kxmers", "kx_windows", "n_passes", "n_distribute_reruns")] + [
         ("stage_ms", ctypes.c_float * len(STAGES)), ("stage_launches", ctypes.c_uint32 * len(STAGES))]
 
     def to_dict(self) -> dict:

@@ -141,7 +141,11 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
     const uint64_t gw = (uint64_t)blockIdx.x * SG_WARPS + warp, nw = (uint64_t)gridDim.x * SG_WARPS;
     int npend = 0;      // runs of the previous segment waiting for a full round of 32 lanes
     uint32_t pbuf = 0;  // this segment's packed-base buffer
-    for (uint64_t sg = gw; sg < n_segs; sg += nw, pbuf ^= 1u) {
+    // the sample pass (seg_step s > 1) visits every s-th segment
+    const uint64_t step = a.seg_step > 1 ? a.seg_step : 1;
+    const uint64_t n_iter = (n_segs + step - 1) / step;
+    for (uint64_t it = gw; it < n_iter; it += nw, pbuf ^= 1u) {
+        const uint64_t sg = it * step;
         uint32_t* PK = S.pk[pbuf];
         const uint32_t* PKprev = S.pk[pbuf ^ 1u];
         const int64_t seg0 = (int64_t)sg * SEG;
@@ -428,7 +432,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             return (wd * 32 + __ffs(bits) - 1) - v;
         };
         const int total = npend + nstarts;
-        int emit_end = (sg + nw >= n_segs) ? total : (total / 32) * 32;
+        int emit_end = (it + nw >= n_iter) ? total : (total / 32) * 32;
         if (emit_end < npend) emit_end = total;
         for (int i0 = 0; i0 < emit_end; i0 += 32) {
             const int idx = i0 + lane;
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                 l_windows += n;
                 l_recs += nrec;
             }
-            if (MODE == P1_MODE_HIST && idx < emit_end) {
+            if ((MODE == P1_MODE_HIST || (MODE == P1_MODE_SCATTER && a.scatter_hist)) && idx < emit_end) {
                 atomicAdd(&a.hist_w[s], (unsigned long long)n);
                 atomicAdd(&a.hist_r[s], (uint32_t)nrec);
             }
@@ -474,14 +478,22 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             }
             if (idx < emit_end && (MODE == P1_MODE_SCATTER || tmp_ok)) {
                 const int j = v + n;
-                uint32_t bin = 0;
+                uint32_t bin = 0, cap = 0xFFFFFFFFu, f0 = 0;
                 uint64_t bbase = 0;
                 if (MODE == P1_MODE_SCATTER) {
-                    bin = a.sig2bin[s];
-                    bbase = a.bin_rec_off[bin];
+                    if (a.sig_dest) {  // (bin, capacity, first slot) in one load
+                        const uint4 dd = a.sig_dest[s];
+                        bin = dd.x;
+                        cap = dd.y;
+                        bbase = ((uint64_t)dd.w << 32) | dd.z;
+                    } else {
+                        bin = a.sig2bin[s];
+                        bbase = a.bin_rec_off[bin];
+                    }
                 }
                 // a pass over a range of bins (inputs beyond HBM): other bins' records are skipped
                 const bool skip = MODE == P1_MODE_SCATTER && (bin < a.bin_lo || bin >= a.bin_hi);
+                if (MODE == P1_MODE_SCATTER && !skip) f0 = atomicAdd(&a.bin_fill[bin], (uint32_t)nrec);
                 for (int ii = v; ii < j && !skip; ii += maxw) {
                     const int m = min(maxw, j - ii);
                     // record words: word 0 = m (8 bits) + symbols [0, 12); word u > 0 =
@@ -498,7 +510,12 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                     uint64_t slot;
                     uint32_t* dstb;
                     if (MODE == P1_MODE_SCATTER) {
-                        slot = bbase + atomicAdd(&a.bin_fill[bin], 1u);
+                        const uint32_t f = f0++;
+                        if (f >= cap) {  // beyond the sampled capacity
+                            atomicAdd(&a.gstats[GS_P1_OVF], 1ull);
+                            continue;
+                        }
+                        slot = bbase + f;
                         dstb = a.bins;
                     } else {
                         slot = slot0++;
@@ -701,7 +718,8 @@ template <int MODE> cudaError_t launch_sig_t(const P1Args& a, uint64_t n_segs, c
     if ((e = cudaGetDevice(&dev))) return e;
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sig<MODE>, SG_NT, sm))) return e;
-    const uint64_t want = (n_segs + SG_WARPS - 1) / SG_WARPS;
+    const uint64_t n_iter = a.seg_step > 1 ? (n_segs + a.seg_step - 1) / a.seg_step : n_segs;
+    const uint64_t want = (n_iter + SG_WARPS - 1) / SG_WARPS;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)nsm * std::max(1, per)));
     k_sig<MODE><<<grid, SG_NT, sm, s>>>(a, n_segs);
     return cudaGetLastError();

@@ -159,4 +159,98 @@ cudaError_t launch_plan(const PlanArgs& a, cudaStream_t s, int* n_launches) {
     return cudaGetLastError();
 }
 
+namespace {
+__global__ void k_scale_hist(unsigned long long* hw, uint32_t* hr, uint64_t ns, uint64_t num, uint64_t den,
+                             uint32_t fw, uint32_t fr) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += (uint64_t)gridDim.x * blockDim.x) {
+        hw[i] = (hw[i] * num + den - 1) / den + fw;
+        const uint64_t v = ((uint64_t)hr[i] * num + den - 1) / den + fr;
+        hr[i] = (uint32_t)(v < 0xFFFFFFFFull ? v : 0xFFFFFFFFull);
+    }
+}
+__global__ void k_bin_caps(const uint64_t* est, uint64_t n_bins, double F, double z, uint32_t margin, uint32_t* cap,
+                           uint64_t* cap64) {
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n_bins;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const double e = (double)est[b];
+        const double c = e + z * sqrt(F * e) + (double)margin;
+        const uint32_t v = c >= 4.0e9 ? 0xFFFFFFFFu : (uint32_t)c;
+        cap[b] = v;
+        cap64[b] = v;
+    }
+}
+__global__ void k_sig_dest(const uint32_t* sig2bin, const uint32_t* cap, const uint64_t* off, uint64_t ns,
+                           uint4* out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = sig2bin[i];
+        const uint64_t o = off[b];
+        out[i] = make_uint4(b, cap[b], (uint32_t)o, (uint32_t)(o >> 32));
+    }
+}
+__global__ void k_bins_exact(uint64_t ns, const uint64_t* B, const uint64_t* bin_first, const uint64_t* Wp,
+                             const uint64_t* Rp, uint64_t* bin_w, uint64_t* bin_nrec) {
+    const uint64_t n_bins = B[ns];
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n_bins;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t fs = bin_first[b], fe = bin_first[b + 1];
+        bin_w[b] = Wp[fe] - Wp[fs];
+        bin_nrec[b] = Rp[fe] - Rp[fs];
+    }
+}
+__global__ void k_hist_stats(const unsigned long long* hw, uint64_t ns, unsigned long long* gstats) {
+    __shared__ uint32_t ws[9];
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long v = i < ns ? hw[i] : 0ull;
+    const uint32_t t = block_sum<256, uint32_t>(v != 0, ws);
+    if (threadIdx.x == 0 && t) atomicAdd(&gstats[GS_SIGS_USED], (unsigned long long)t);
+    unsigned long long mx = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(&gstats[GS_MAX_SIG], mx);
+}
+}  // namespace
+
+cudaError_t launch_scale_hist(unsigned long long* hist_w, uint32_t* hist_r, uint64_t ns, uint64_t num, uint64_t den,
+                              uint32_t floor_w, uint32_t floor_r, cudaStream_t s) {
+    k_scale_hist<<<(unsigned)std::min<uint64_t>((ns + 255) / 256, 4096), 256, 0, s>>>(hist_w, hist_r, ns, num, den,
+                                                                                        floor_w, floor_r);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sig_dest(const uint32_t* sig2bin, const uint32_t* bin_cap, const uint64_t* bin_rec_off, uint64_t ns,
+                            uint4* sig_dest, cudaStream_t s) {
+    k_sig_dest<<<(unsigned)std::min<uint64_t>((ns + 255) / 256, 4096), 256, 0, s>>>(sig2bin, bin_cap, bin_rec_off, ns,
+                                                                                     sig_dest);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bin_caps(const uint64_t* bin_nrec, uint64_t n_bins, double F, double z, uint32_t margin,
+                            uint32_t* bin_cap, uint64_t* bin_cap_u64, uint64_t* out_scan, void* temp, cudaStream_t s) {
+    if (n_bins == 0) return cudaMemsetAsync(out_scan, 0, 8, s);
+    k_bin_caps<<<(unsigned)std::min<uint64_t>((n_bins + 255) / 256, 4096), 256, 0, s>>>(bin_nrec, n_bins, F, z, margin,
+                                                                                          bin_cap, bin_cap_u64);
+    cudaError_t e;
+    if ((e = cudaGetLastError())) return e;
+    return scan_generic<uint64_t>(ArrayIn<uint64_t>{bin_cap_u64}, n_bins, out_scan, (uint64_t*)temp, s, nullptr);
+}
+
+cudaError_t launch_exact_tables(const PlanArgs& a, uint64_t n_bins, cudaStream_t s, int* n_launches) {
+    cudaError_t e;
+    uint64_t* tmp = (uint64_t*)a.temp;
+    if ((e = scan_generic<uint64_t>(ArrayIn<unsigned long long>{a.hist_w}, a.ns, a.win_scan, tmp, s, n_launches)) !=
+        cudaSuccess)
+        return e;
+    if ((e = scan_generic<uint64_t>(ArrayIn<uint32_t>{a.hist_r}, a.ns, a.rec_scan, tmp, s, n_launches)) != cudaSuccess)
+        return e;
+    k_bins_exact<<<(unsigned)std::min<uint64_t>((n_bins + 255) / 256 + 1, 4096), 256, 0, s>>>(
+        a.ns, a.bnd_scan, a.bin_first, a.win_scan, a.rec_scan, a.bin_w, a.bin_nrec);
+    if ((e = cudaGetLastError())) return e;
+    k_hist_stats<<<(unsigned)((a.ns + 255) / 256), 256, 0, s>>>(a.hist_w, a.ns, a.gstats);
+    if (n_launches) *n_launches += 2;
+    return cudaGetLastError();
+}
+
 }  // namespace kmc

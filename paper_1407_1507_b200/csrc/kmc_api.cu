@@ -229,6 +229,9 @@ struct StageEv {
 
 // State carried between the phases of a count (pass 1 -> plan -> bins/count), so that the
 // sharded entry points (kmc_shard_*) can stop between them for the caller's exchanges.
+// inputs of at least this many Mi bases take the sampled distribution by default
+constexpr uint32_t SAMPLE_MIN_MBASES = 64;
+
 struct PlanCtx {
     PlanArgs pa{};
     uint64_t ns = 0, n_bins = 0, n_windows = 0, n_records = 0;
@@ -248,6 +251,7 @@ struct PlanCtx {
     // sharded: bin -> owning rank
     std::vector<uint32_t> owner;
     bool multipass = false;  // host reads beyond HBM: passes over ranges of bins (f2)
+    uint32_t* bins_ready = nullptr;  // sampled distribution: pass 1 wrote the records into their bins
 };
 
 struct kmc_job {
@@ -474,7 +478,17 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         const double est = (double)(n_bases / 8 + 1) * (2.0 * RWt * 4 + 4) * 1.2;
         j->ctx.multipass = j->opt.pass_mb > 0 || est > 0.7 * (double)(fr + cache_bytes());
     }
-    if (j->opt.distribute_path != 1 && !j->ctx.multipass) {
+    // The paper's sampled distribution: the bin plan comes from a sample of the
+    // reads (every 32nd pass-1 segment; with host-resident reads every 4th segment of the first
+    // batch), bins get the sampled record count + 6 standard deviations of the estimate + a
+    // margin, and pass 1 then writes every record straight into its bin while it counts the
+    // exact histograms -- no record stream, no S5 re-sort.  A record beyond its bin's capacity
+    // (a sample far off) makes the call plan again from the exact histograms and repeat the
+    // scatter.  Small inputs keep the exact histogram + record stream + S5.
+    const bool sampled = !j->shard && !j->ctx.multipass &&
+                         (j->opt.distribute_path == 2 ||
+                          (j->opt.distribute_path == 0 && n_bases >= ((uint64_t)SAMPLE_MIN_MBASES << 20)));
+    if (j->opt.distribute_path == 0 && !sampled && !j->ctx.multipass) {
         // slots: records (~n_bases/8 at 100 bp reads) + every pass-1 warp's partly used block
         tmp_cap = std::max<uint64_t>(n_bases / 8, 4096) + (uint64_t)n_sms() * 64 * 2048;
         tmp_recs = reinterpret_cast<uint32_t*>(ar.alloc(tmp_cap * RWt * 4));
@@ -508,22 +522,32 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         }
         j->st.n_input_batches = batches.size();
     }
-    auto run_p1 = [&](int mode) -> int {
+    // max_batches: stop after that many batches (the sample pass: the first one); b0_resident:
+    // batch 0 is still in its device slot from the previous pass (no copy)
+    bool b0_resident = false, tiles_ready = false;
+    auto run_p1 = [&](int mode, size_t max_batches = ~(size_t)0) -> int {
         if (!host_reads) {
-            CK(launch_tile_reads(d_off, n_reads, off0, n_tiles, tile_r_lo, s));
+            int nl = 1;
+            if (!tiles_ready) {  // the segment -> first read table of device-resident reads is kept
+                CK(launch_tile_reads(d_off, n_reads, off0, n_tiles, tile_r_lo, s));
+                tiles_ready = true;
+                ++nl;
+            }
             CK(launch_p1(mode, a, n_tiles, s));
-            return 2;
+            return nl;
         }
         int nl = 0;
-        for (size_t b = 0; b < batches.size(); ++b) {
+        for (size_t b = 0; b < batches.size() && b < max_batches; ++b) {
             const int t = (int)(b & 1);
             const uint64_t r0 = batches[b].first, r1 = batches[b].second;
             const uint64_t nb = h_off[r1] - h_off[r0];
-            CK(cudaStreamWaitEvent(j->cs, j->ev_done[t], 0));
-            CK(cudaMemcpyAsync(bbuf[t], reads + (h_off[r0] - off0), nb, cudaMemcpyHostToDevice, j->cs));
-            CK(cudaMemcpyAsync(bofs[t], h_off + r0, (r1 - r0 + 1) * 8, cudaMemcpyHostToDevice, j->cs));
-            CK(cudaEventRecord(j->ev_copy[t], j->cs));
-            CK(cudaStreamWaitEvent(s, j->ev_copy[t], 0));
+            if (b > 0 || !b0_resident) {
+                CK(cudaStreamWaitEvent(j->cs, j->ev_done[t], 0));
+                CK(cudaMemcpyAsync(bbuf[t], reads + (h_off[r0] - off0), nb, cudaMemcpyHostToDevice, j->cs));
+                CK(cudaMemcpyAsync(bofs[t], h_off + r0, (r1 - r0 + 1) * 8, cudaMemcpyHostToDevice, j->cs));
+                CK(cudaEventRecord(j->ev_copy[t], j->cs));
+                CK(cudaStreamWaitEvent(s, j->ev_copy[t], 0));
+            }
             P1Args ab = a;
             ab.reads = bbuf[t];
             ab.offsets = bofs[t];
@@ -541,6 +565,128 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         return nl;
     };
     if (host_reads) j->make_copy_stream();
+    if (sampled) {
+        // ---- sample pass: histogram of every step-th segment (device reads) or of the first
+        //      batch's every step-th segment (host reads)
+        const uint32_t step = host_reads ? 4 : 32;
+        a.seg_step = step;
+        const int nls = run_p1(P1_MODE_HIST, 1);
+        a.seg_step = 1;
+        j->launches += nls;
+        const uint64_t seg_total = p1_num_tiles(n_bases);
+        const uint64_t seg_in = host_reads ? p1_num_tiles(h_off[batches[0].second] - h_off[batches[0].first]) : n_tiles;
+        const uint64_t seg_sampled = std::max<uint64_t>(1, (seg_in + step - 1) / step);
+        const double F = (double)seg_total / (double)seg_sampled;
+        const uint32_t fl = (uint32_t)std::ceil(F);
+        CK(launch_scale_hist(hist_w, hist_r, ns, seg_total, seg_sampled, 4 * fl, fl, s));
+        j->stage_end(nls + 1);
+        PlanCtx& c = j->ctx;
+        c.ns = ns;
+        c.hist_w = hist_w;
+        c.hist_r = hist_r;
+        c.gstats = gstats;
+        c.check_p1 = false;
+        plan_phase(j, c);  // the plan of the estimates
+        c.check_p1 = true;
+        if (c.ev_plan) {
+            CK(cudaEventDestroy(c.ev_plan));
+            c.ev_plan = nullptr;
+        }
+        c.tables_pending = false;
+        PlanArgs& pa = c.pa;
+        const uint64_t n_bins = c.n_bins;
+        const int RWs = record_words(k);
+        // ---- bin capacities: estimate + 6 standard deviations + 64 records; offsets = their scan
+        uint32_t* bin_cap = ar.get<uint32_t>(n_bins + 1);
+        uint64_t* cap64 = ar.get<uint64_t>(n_bins + 1);
+        uint64_t* cap_scan = ar.get<uint64_t>(n_bins + 2);
+        void* ctemp = ar.alloc(scan_temp_bytes(n_bins + 1));
+        CK(launch_bin_caps(pa.bin_nrec, n_bins, F, 6.0, 64, bin_cap, cap64, cap_scan, ctemp, s));
+        unsigned long long* hs = j->host_small;
+        CK(cudaMemcpyAsync(&hs[3], cap_scan + n_bins, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(pa.bin_rec_off, cap_scan, n_bins * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t total_cap = hs[3];
+        uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(total_cap * RWs * 4));
+        uint32_t* bin_fill = ar.get<uint32_t>(n_bins);
+        // ---- pass 1: every record straight into its bin, exact histograms alongside
+        j->stage_begin(KMC_STAGE_SIGNATURE);
+        CK(cudaMemsetAsync(bin_fill, 0, n_bins * 4, s));
+        CK(cudaMemsetAsync(hist_w, 0, ns * 8, s));
+        CK(cudaMemsetAsync(hist_r, 0, ns * 4, s));
+        CK(cudaMemsetAsync(gstats, 0, GS_N * 8, s));
+        uint4* sig_dest = ar.get<uint4>(ns);
+        CK(launch_sig_dest(pa.sig2bin, bin_cap, pa.bin_rec_off, ns, sig_dest, s));
+        a.sig2bin = pa.sig2bin;
+        a.bin_rec_off = pa.bin_rec_off;
+        a.bin_fill = bin_fill;
+        a.bins = bins;
+        a.sig_dest = sig_dest;
+        a.scatter_hist = 1;
+        b0_resident = host_reads;
+        int nl = run_p1(P1_MODE_SCATTER);
+        b0_resident = false;
+        a.sig_dest = nullptr;
+        CK(cudaMemcpyAsync(&hs[4], gstats + GS_P1_OVF, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        j->launches += nl;
+        j->stage_end(nl);
+        ar.release(ctemp);
+        ar.release(cap64);
+        ar.release(cap_scan);
+        if (hs[4] == 0) {
+            // ---- exact per-bin tables on the sampled plan
+            j->stage_begin(KMC_STAGE_PLAN);
+            int pl = 0;
+            CK(launch_exact_tables(pa, n_bins, s, &pl));
+            j->launches += pl;
+            j->stage_end(pl);
+            CK(cudaMemcpyAsync(&hs[1], pa.win_scan + ns, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&hs[2], pa.rec_scan + ns, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            c.n_windows = hs[1];
+            c.n_records = hs[2];
+            j->st.n_windows = c.n_windows;
+            j->st.n_superkmers = hs[16 + GS_SUPERKMERS];
+            j->st.n_records = c.n_records;
+            j->st.n_invalid_bases = hs[16 + GS_INVALID];
+            j->st.n_signatures_used = hs[16 + GS_SIGS_USED];
+            j->st.max_signature_windows = hs[16 + GS_MAX_SIG];
+            if (hs[16 + GS_WINDOWS] != c.n_windows || hs[16 + GS_RECORDS] != c.n_records) {
+                set_err("sampled distribution: histogram totals disagree with pass-1 counters");
+                throw Fail{KMC_ERR_INTERNAL};
+            }
+            if (c.n_windows > 0) {
+                c.tables_pending = true;
+                CK(cudaEventCreateWithFlags(&c.ev_plan, cudaEventDisableTiming));
+                CK(cudaEventRecord(c.ev_plan, s));
+            }
+        } else {
+            // ---- a bin overflowed its sampled capacity: plan again from the exact histograms
+            //      of this pass and scatter again with exact offsets
+            j->st.n_distribute_reruns += 1;
+            ar.release(bins);
+            plan_phase(j, c);
+            bins = reinterpret_cast<uint32_t*>(ar.alloc(std::max<uint64_t>(c.n_records, 1) * RWs * 4));
+            j->stage_begin(KMC_STAGE_SCATTER);
+            if (c.n_bins > n_bins) bin_fill = ar.get<uint32_t>(c.n_bins);
+            CK(cudaMemsetAsync(bin_fill, 0, std::max<uint64_t>(c.n_bins, 1) * 4, s));
+            a.sig2bin = c.pa.sig2bin;
+            a.bin_rec_off = c.pa.bin_rec_off;
+            a.bin_fill = bin_fill;
+            a.bins = bins;
+            a.sig_dest = nullptr;
+            a.scatter_hist = 0;
+            nl = run_p1(P1_MODE_SCATTER);
+            j->launches += nl;
+            j->stage_end(nl);
+        }
+        c.bins_ready = bins;
+        c.a = a;
+        count_phase(j, c);
+        return;
+    }
     const int nl1 = run_p1(P1_MODE_HIST);
     j->launches += nl1;
     j->stage_end(nl1);
@@ -1125,12 +1271,15 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         return;
     }
     // ---- S5: records into bins -- a copy from pass 1's temporary stream, or (if the stream
-    //      overflowed its estimate) pass 2 = S1-S3 recomputed + scatter
-    uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4));
+    //      overflowed its estimate) pass 2 = S1-S3 recomputed + scatter; nothing when the
+    //      sampled distribution has written them already
+    uint32_t* bins = c.bins_ready ? c.bins_ready : reinterpret_cast<uint32_t*>(ar.alloc(n_records * RW * 4));
     const uint64_t tmp_n = c.tmp_n;
     j->stage_begin(KMC_STAGE_SCATTER);
     int s5_launches = 0;
-    if (tmp_recs && tmp_n <= tmp_cap) {
+    if (c.bins_ready) {
+        // (pass 1 wrote the bins)
+    } else if (tmp_recs && tmp_n <= tmp_cap) {
         // MSD passes of <= 8 bits over the bin id; the last one writes the bins
         int B = 1;
         while ((1ull << B) < n_bins) ++B;
@@ -1188,7 +1337,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
         c.a.bin_rec_off = pa.bin_rec_off;
         c.a.bin_fill = bin_fill;
         c.a.bins = bins;
-        s5_launches = c.run_p1(P1_MODE_SCATTER) - 1;
+        s5_launches = c.run_p1(P1_MODE_SCATTER);
     }
     j->launches += s5_launches;
     j->stage_end(s5_launches);

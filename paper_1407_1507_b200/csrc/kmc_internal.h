@@ -25,7 +25,8 @@ enum {
     GS_KX = 13,            // (k,x)-mers sorted (kx path)
     GS_KX_WIN = 14,        // windows of the bins counted through (k,x)-mers
     GS_SUB_OVF = 15,       // sub-signature digits whose table overflowed (counted in rounds)
-    GS_N = 16
+    GS_P1_OVF = 16,        // records beyond their bin's sampled capacity (scatter pass)
+    GS_N = 24
 };
 
 // ------------------------------------------------------------ phase 1 (distribution)
@@ -51,6 +52,10 @@ struct P1Args {
     uint32_t* bin_fill;
     uint32_t* bins;
     uint32_t bin_lo, bin_hi;  // pass 2 writes only the records of bins [bin_lo, bin_hi)
+    const uint4* sig_dest;    // pass 2 (sampled plan): per signature {bin, capacity, first slot lo, hi};
+                              // records beyond the capacity are dropped and counted in GS_P1_OVF
+    int scatter_hist;         // pass 2 also accumulates hist_w / hist_r (sampled plan)
+    uint32_t seg_step;        // 0/1: every segment; s > 1: every s-th segment (the sample pass)
     // pass 1: temporary record stream (nullptr = not used)
     uint32_t* tmp_recs;
     uint32_t* tmp_sig;
@@ -134,6 +139,21 @@ struct PlanArgs {
 };
 size_t plan_temp_bytes(uint64_t ns);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t s, int* n_launches);
+// Sampled plan (the paper's sampling): hist = ceil(hist * num / den) + floor (both
+// arrays, in place), so every signature gets room even if the sample missed it.
+cudaError_t launch_scale_hist(unsigned long long* hist_w, uint32_t* hist_r, uint64_t ns, uint64_t num, uint64_t den,
+                              uint32_t floor_w, uint32_t floor_r, cudaStream_t s);
+// bin_cap[b] = est + z * sqrt(F * est) + margin records (est = the sampled plan's bin_nrec; F =
+// num / den); out_scan (n_bins + 1 uint64) = exclusive scan of bin_cap (temp: scan_temp_bytes)
+// sig_dest[s] = {sig2bin[s], bin_cap[bin], bin_rec_off[bin] (lo, hi)} for s < ns
+cudaError_t launch_sig_dest(const uint32_t* sig2bin, const uint32_t* bin_cap, const uint64_t* bin_rec_off, uint64_t ns,
+                            uint4* sig_dest, cudaStream_t s);
+cudaError_t launch_bin_caps(const uint64_t* bin_nrec, uint64_t n_bins, double F, double z, uint32_t margin,
+                            uint32_t* bin_cap, uint64_t* bin_cap_u64, uint64_t* out_scan, void* temp, cudaStream_t s);
+// Exact per-bin tables from exact histograms and an existing bin plan (bin_first): scans of
+// hist_w / hist_r into win_scan / rec_scan, bin_w / bin_nrec (bin_rec_off untouched), and the
+// histogram statistics (GS_SIGS_USED, GS_MAX_SIG)
+cudaError_t launch_exact_tables(const PlanArgs& a, uint64_t n_bins, cudaStream_t s, int* n_launches);
 
 // ------------------------------------------------------------ phase 2 (sorting)
 struct SmallArgs {
