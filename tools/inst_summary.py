@@ -1,6 +1,6 @@
 """Warp instructions per kmc_count call from an ncu launch list that carries
 smsp__inst_executed.sum (one row per launch and metric), averaged over the calls in the list
-(a call = one k_sig<> launch).  usage: python tools/inst_summary.py LAUNCHES.csv [n_windows]"""
+(a call = one k_tile_reads launch).  usage: python tools/inst_summary.py LAUNCHES.csv [n_windows]"""
 import collections
 import csv
 import sys
@@ -15,7 +15,7 @@ for r in rows[1:]:
         continue
     name = r[ki].split("(")[0].replace("void ", "").replace("kmc::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
     inst[name] += float(r[vi].replace(",", ""))
-    calls += name.startswith("k_sig<")
+    calls += name.startswith("k_tile_reads")
 n_windows = float(sys.argv[2]) if len(sys.argv) > 2 else 0.0
 tot = sum(inst.values()) / calls
 peak = 148 * 4 * 1.965e9
