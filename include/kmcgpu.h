@@ -156,7 +156,7 @@ typedef struct {
                                   sample of the reads and pass 1 writes every record
                                   straight into its bin (no record stream, no S5 copy) */
     uint32_t input_batch_mb;   /* host-resident reads are streamed through pass 1 in read-aligned
-                                  batches of this many MiB (0 = default 1024), double-buffered so
+                                  batches of this many MiB (0 = default 256), double-buffered so
                                   the H2D copy of batch i+1 overlaps pass 1 on batch i */
     uint32_t large_group_mkeys;/* large bins are split/sorted in groups of at most this many Mi
                                   keys (0 = auto: as many as fit in free device memory) */

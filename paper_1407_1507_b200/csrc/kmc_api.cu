@@ -479,8 +479,8 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         j->ctx.multipass = j->opt.pass_mb > 0 || est > 0.7 * (double)(fr + cache_bytes());
     }
     // The paper's sampled distribution: the bin plan comes from a sample of the
-    // reads (every 32nd pass-1 segment; with host-resident reads every 4th segment of the first
-    // batch), bins get the sampled record count + 6 standard deviations of the estimate + a
+    // reads (every 32nd pass-1 segment; with host-resident reads segments of the first batch,
+    // ~1/16 of all), bins get the sampled record count + 6 standard deviations of the estimate + a
     // margin, and pass 1 then writes every record straight into its bin while it counts the
     // exact histograms -- no record stream, no S5 re-sort.  A record beyond its bin's capacity
     // (a sample far off) makes the call plan again from the exact histograms and repeat the
@@ -504,7 +504,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     uint64_t* bofs[2] = {nullptr, nullptr};
     uint64_t* btile[2] = {nullptr, nullptr};
     if (host_reads) {
-        const uint64_t batch_bytes = (uint64_t)(j->opt.input_batch_mb ? j->opt.input_batch_mb : 1024) << 20;
+        const uint64_t batch_bytes = (uint64_t)(j->opt.input_batch_mb ? j->opt.input_batch_mb : 256) << 20;
         uint64_t max_b = 0, max_r = 0;
         for (uint64_t r0 = 0; r0 < n_reads;) {
             const uint64_t lim = h_off[r0] + batch_bytes;
@@ -522,10 +522,22 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         }
         j->st.n_input_batches = batches.size();
     }
-    // max_batches: stop after that many batches (the sample pass: the first one); b0_resident:
-    // batch 0 is still in its device slot from the previous pass (no copy)
-    bool b0_resident = false, tiles_ready = false;
-    auto run_p1 = [&](int mode, size_t max_batches = ~(size_t)0) -> int {
+    // host reads: slot_batch[t] = the batch whose reads are in device slot t (-1: none); a pass
+    // with keep_slots set reuses them (the sampled distribution's scatter pass reuses the
+    // first two batches its sample pass copied), any other pass copies every batch
+    bool tiles_ready = false, keep_slots = false;
+    int64_t slot_batch[2] = {-1, -1};
+    auto copy_batch = [&](size_t b) {
+        const int t = (int)(b & 1);
+        const uint64_t r0 = batches[b].first, r1 = batches[b].second;
+        CK(cudaStreamWaitEvent(j->cs, j->ev_done[t], 0));
+        CK(cudaMemcpyAsync(bbuf[t], reads + (h_off[r0] - off0), h_off[r1] - h_off[r0], cudaMemcpyHostToDevice, j->cs));
+        CK(cudaMemcpyAsync(bofs[t], h_off + r0, (r1 - r0 + 1) * 8, cudaMemcpyHostToDevice, j->cs));
+        CK(cudaEventRecord(j->ev_copy[t], j->cs));
+        slot_batch[t] = (int64_t)b;
+    };
+    // max_batches: stop after that many batches; prefetch: then copy the next batch already
+    auto run_p1 = [&](int mode, size_t max_batches = ~(size_t)0, bool prefetch = false) -> int {
         if (!host_reads) {
             int nl = 1;
             if (!tiles_ready) {  // the segment -> first read table of device-resident reads is kept
@@ -536,18 +548,16 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             CK(launch_p1(mode, a, n_tiles, s));
             return nl;
         }
+        if (!keep_slots) slot_batch[0] = slot_batch[1] = -1;
+        keep_slots = false;
         int nl = 0;
-        for (size_t b = 0; b < batches.size() && b < max_batches; ++b) {
+        size_t b = 0;
+        for (; b < batches.size() && b < max_batches; ++b) {
             const int t = (int)(b & 1);
             const uint64_t r0 = batches[b].first, r1 = batches[b].second;
             const uint64_t nb = h_off[r1] - h_off[r0];
-            if (b > 0 || !b0_resident) {
-                CK(cudaStreamWaitEvent(j->cs, j->ev_done[t], 0));
-                CK(cudaMemcpyAsync(bbuf[t], reads + (h_off[r0] - off0), nb, cudaMemcpyHostToDevice, j->cs));
-                CK(cudaMemcpyAsync(bofs[t], h_off + r0, (r1 - r0 + 1) * 8, cudaMemcpyHostToDevice, j->cs));
-                CK(cudaEventRecord(j->ev_copy[t], j->cs));
-                CK(cudaStreamWaitEvent(s, j->ev_copy[t], 0));
-            }
+            if (slot_batch[t] != (int64_t)b) copy_batch(b);
+            CK(cudaStreamWaitEvent(s, j->ev_copy[t], 0));
             P1Args ab = a;
             ab.reads = bbuf[t];
             ab.offsets = bofs[t];
@@ -561,6 +571,9 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             CK(launch_p1(mode, ab, nt, s));
             CK(cudaEventRecord(j->ev_done[t], s));
             nl += 2;
+            if (b + 1 < batches.size() && slot_batch[(b + 1) & 1] != (int64_t)(b + 1) &&
+                (b + 1 < max_batches || prefetch))
+                copy_batch(b + 1);  // the next batch's copy overlaps this batch's pass 1
         }
         return nl;
     };
@@ -568,9 +581,15 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     if (sampled) {
         // ---- sample pass: histogram of every step-th segment (device reads) or of the first
         //      batch's every step-th segment (host reads)
-        const uint32_t step = host_reads ? 4 : 32;
+        // device reads: every 32nd segment; host reads: segments of the first batch, about one
+        // in 16 of all segments (every one when the batch is <= 1/16 of the input)
+        uint32_t step = 32;
+        if (host_reads) {
+            const uint64_t seg0 = p1_num_tiles(h_off[batches[0].second] - h_off[batches[0].first]);
+            step = (uint32_t)std::max<uint64_t>(1, 16 * seg0 / std::max<uint64_t>(1, p1_num_tiles(n_bases)));
+        }
         a.seg_step = step;
-        const int nls = run_p1(P1_MODE_HIST, 1);
+        const int nls = run_p1(P1_MODE_HIST, 1, true);  // (the second batch is copied meanwhile)
         a.seg_step = 1;
         j->launches += nls;
         const uint64_t seg_total = p1_num_tiles(n_bases);
@@ -623,9 +642,8 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         a.bins = bins;
         a.sig_dest = sig_dest;
         a.scatter_hist = 1;
-        b0_resident = host_reads;
+        keep_slots = true;
         int nl = run_p1(P1_MODE_SCATTER);
-        b0_resident = false;
         a.sig_dest = nullptr;
         CK(cudaMemcpyAsync(&hs[4], gstats + GS_P1_OVF, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
