@@ -196,6 +196,34 @@ bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// Host-resident inputs of concurrent calls cross the PCIe link one pass after another: a
+// call's copy stream waits for the previous call's last input copy (an event per device).
+// Sharing the link would not move the inputs faster; one after another, a call's device
+// stages and output copy overlap the next call's input copy (the link is full duplex).
+std::mutex g_h2d_mu;
+cudaEvent_t g_h2d_ev[64] = {};
+struct H2DChain {
+    std::unique_lock<std::mutex> lk;
+    int dev = 0;
+    bool on = false;
+    void begin(cudaStream_t cs) {
+        lk = std::unique_lock<std::mutex>(g_h2d_mu);
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+            lk.unlock();
+            return;
+        }
+        if (g_h2d_ev[dev]) CK(cudaStreamWaitEvent(cs, g_h2d_ev[dev], 0));
+        on = true;
+    }
+    void end(cudaStream_t cs) {
+        if (!on) return;
+        on = false;
+        if (!g_h2d_ev[dev]) CK(cudaEventCreateWithFlags(&g_h2d_ev[dev], cudaEventDisableTiming));
+        CK(cudaEventRecord(g_h2d_ev[dev], cs));
+        lk.unlock();
+    }
+};
+
 std::mutex g_pin_mu;
 std::vector<unsigned long long*> g_pin_free;
 unsigned long long* pin_acquire() {
@@ -231,6 +259,10 @@ struct StageEv {
 // sharded entry points (kmc_shard_*) can stop between them for the caller's exchanges.
 // inputs of at least this many Mi bases take the sampled distribution by default
 constexpr uint32_t SAMPLE_MIN_MBASES = 64;
+// device slots for batches of host-resident reads: the copy stream runs up to this many
+// batches ahead of pass 1 (2 GiB at the default 256 MiB batches), so the input copy keeps
+// going while the device is busy with another call's counting stages
+constexpr int IN_SLOTS = 8;
 
 struct PlanCtx {
     PlanArgs pa{};
@@ -281,12 +313,12 @@ struct kmc_job {
     uint32_t* recv_recs = nullptr;
     uint32_t* recv_sigs = nullptr;
     uint64_t n_recv = 0;
-    cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copy[IN_SLOTS] = {}, ev_done[IN_SLOTS] = {};
 
     void make_copy_stream() {
         if (cs) return;
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t < IN_SLOTS; ++t) {
             CK(cudaEventCreateWithFlags(&ev_copy[t], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ev_done[t], cudaEventDisableTiming));
             CK(cudaEventRecord(ev_done[t], s));
@@ -328,7 +360,7 @@ struct kmc_job {
         if (ctx.ev_plan) cudaEventDestroy(ctx.ev_plan);
         if (cs) {
             cudaStreamSynchronize(cs);
-            for (int t = 0; t < 2; ++t) {
+            for (int t = 0; t < IN_SLOTS; ++t) {
                 cudaEventDestroy(ev_copy[t]);
                 cudaEventDestroy(ev_done[t]);
             }
@@ -498,11 +530,12 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     a.tmp_sig = tmp_sig;
     a.tmp_cap = tmp_cap;
     // batches of host-resident reads: [r0, r1) with at most batch_bytes bases (one read may
-    // exceed it alone); two device slots, H2D on a copy stream overlapping pass 1
+    // exceed it alone); up to IN_SLOTS device slots, H2D on a copy stream ahead of pass 1
     std::vector<std::pair<uint64_t, uint64_t>> batches;
-    uint8_t* bbuf[2] = {nullptr, nullptr};
-    uint64_t* bofs[2] = {nullptr, nullptr};
-    uint64_t* btile[2] = {nullptr, nullptr};
+    uint8_t* bbuf[IN_SLOTS] = {};
+    uint64_t* bofs[IN_SLOTS] = {};
+    uint64_t* btile[IN_SLOTS] = {};
+    int NS = 1;
     if (host_reads) {
         const uint64_t batch_bytes = (uint64_t)(j->opt.input_batch_mb ? j->opt.input_batch_mb : 256) << 20;
         uint64_t max_b = 0, max_r = 0;
@@ -515,8 +548,14 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             max_r = std::max(max_r, r1 - r0);
             r0 = r1;
         }
-        for (int t = 0; t < 2 && t < (int)batches.size(); ++t) {
-            bbuf[t] = ar.get<uint8_t>(max_b + 16);
+        // slots: IN_SLOTS, fewer for few batches, and at least 2 when memory is short
+        NS = (int)std::min<size_t>(IN_SLOTS, std::max<size_t>(batches.size(), 1));
+        for (int t = 0; t < NS; ++t) {
+            bbuf[t] = reinterpret_cast<uint8_t*>(t < 2 ? ar.alloc(max_b + 16) : ar.try_alloc(max_b + 16));
+            if (!bbuf[t]) {
+                NS = t;
+                break;
+            }
             bofs[t] = ar.get<uint64_t>(max_r + 1);
             btile[t] = ar.get<uint64_t>(p1_num_tiles(max_b) + 1);
         }
@@ -524,11 +563,13 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     }
     // host reads: slot_batch[t] = the batch whose reads are in device slot t (-1: none); a pass
     // with keep_slots set reuses them (the sampled distribution's scatter pass reuses the
-    // first two batches its sample pass copied), any other pass copies every batch
+    // first batch its sample pass copied), any other pass copies every batch
     bool tiles_ready = false, keep_slots = false;
-    int64_t slot_batch[2] = {-1, -1};
+    int64_t slot_batch[IN_SLOTS];
+    for (int t = 0; t < IN_SLOTS; ++t) slot_batch[t] = -1;
     auto copy_batch = [&](size_t b) {
-        const int t = (int)(b & 1);
+        const int t = (int)(b % NS);
+        if (slot_batch[t] == (int64_t)b) return;
         const uint64_t r0 = batches[b].first, r1 = batches[b].second;
         CK(cudaStreamWaitEvent(j->cs, j->ev_done[t], 0));
         CK(cudaMemcpyAsync(bbuf[t], reads + (h_off[r0] - off0), h_off[r1] - h_off[r0], cudaMemcpyHostToDevice, j->cs));
@@ -536,8 +577,8 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         CK(cudaEventRecord(j->ev_copy[t], j->cs));
         slot_batch[t] = (int64_t)b;
     };
-    // max_batches: stop after that many batches; prefetch: then copy the next batch already
-    auto run_p1 = [&](int mode, size_t max_batches = ~(size_t)0, bool prefetch = false) -> int {
+    // max_batches: stop after that many batches (the sample pass: the first one)
+    auto run_p1 = [&](int mode, size_t max_batches = ~(size_t)0) -> int {
         if (!host_reads) {
             int nl = 1;
             if (!tiles_ready) {  // the segment -> first read table of device-resident reads is kept
@@ -548,15 +589,17 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             CK(launch_p1(mode, a, n_tiles, s));
             return nl;
         }
-        if (!keep_slots) slot_batch[0] = slot_batch[1] = -1;
+        if (!keep_slots)
+            for (int t = 0; t < IN_SLOTS; ++t) slot_batch[t] = -1;
         keep_slots = false;
+        const size_t nbt = batches.size(), lim = std::min(nbt, max_batches);
+        for (size_t q = 0; q < (size_t)NS && q < lim; ++q) copy_batch(q);
         int nl = 0;
-        size_t b = 0;
-        for (; b < batches.size() && b < max_batches; ++b) {
-            const int t = (int)(b & 1);
+        for (size_t b = 0; b < lim; ++b) {
+            const int t = (int)(b % NS);
             const uint64_t r0 = batches[b].first, r1 = batches[b].second;
             const uint64_t nb = h_off[r1] - h_off[r0];
-            if (slot_batch[t] != (int64_t)b) copy_batch(b);
+            copy_batch(b);
             CK(cudaStreamWaitEvent(s, j->ev_copy[t], 0));
             P1Args ab = a;
             ab.reads = bbuf[t];
@@ -571,13 +614,14 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             CK(launch_p1(mode, ab, nt, s));
             CK(cudaEventRecord(j->ev_done[t], s));
             nl += 2;
-            if (b + 1 < batches.size() && slot_batch[(b + 1) & 1] != (int64_t)(b + 1) &&
-                (b + 1 < max_batches || prefetch))
-                copy_batch(b + 1);  // the next batch's copy overlaps this batch's pass 1
+            // the batch NS ahead takes this slot once this batch's pass 1 is done
+            if (b + NS < lim) copy_batch(b + NS);
         }
         return nl;
     };
     if (host_reads) j->make_copy_stream();
+    H2DChain chain;
+    if (host_reads && !j->ctx.multipass) chain.begin(j->cs);
     if (sampled) {
         // ---- sample pass: histogram of every step-th segment (device reads) or of the first
         //      batch's every step-th segment (host reads)
@@ -589,7 +633,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             step = (uint32_t)std::max<uint64_t>(1, 16 * seg0 / std::max<uint64_t>(1, p1_num_tiles(n_bases)));
         }
         a.seg_step = step;
-        const int nls = run_p1(P1_MODE_HIST, 1, true);  // (the second batch is copied meanwhile)
+        const int nls = run_p1(P1_MODE_HIST, 1);
         a.seg_step = 1;
         j->launches += nls;
         const uint64_t seg_total = p1_num_tiles(n_bases);
@@ -642,7 +686,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         a.bins = bins;
         a.sig_dest = sig_dest;
         a.scatter_hist = 1;
-        keep_slots = true;
+        keep_slots = true;  // batch 0 is still in its slot
         int nl = run_p1(P1_MODE_SCATTER);
         a.sig_dest = nullptr;
         CK(cudaMemcpyAsync(&hs[4], gstats + GS_P1_OVF, 8, cudaMemcpyDeviceToHost, s));
@@ -700,12 +744,14 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             j->launches += nl;
             j->stage_end(nl);
         }
+        chain.end(j->cs);
         c.bins_ready = bins;
         c.a = a;
         count_phase(j, c);
         return;
     }
     const int nl1 = run_p1(P1_MODE_HIST);
+    chain.end(j->cs);
     j->launches += nl1;
     j->stage_end(nl1);
 
