@@ -173,6 +173,20 @@ def run_oracle_sample(w, n_reads_sample: int, threads: int):
 
 
 
+
+def pipelined_only(args):
+    """--e2e-pipelined-only: the two-stream e2e measurement alone, one JSON line."""
+    import torch
+    import paper_1407_1507_b200 as kmc
+    torch.cuda.set_device(0)
+    kmc.load()
+    w = synth.make(args.config, scale=args.scale, n_threads=os.cpu_count() or 8)
+    reads_h = torch.from_numpy(w.reads).pin_memory()
+    offs_h = torch.from_numpy(w.offsets.view(np.uint64)).pin_memory()
+    r = e2e_pipelined(kmc, reads_h, offs_h, w.k, w.p, w.cutoff_min, w.cutoff_max, args.count_path,
+                      max(1, min(args.steps, 3)), w.n_bases)
+    print(json.dumps(r))
+
 def e2e_pipelined(kmc, reads_h, offs_h, k, p, ci, cx, count_path, e_steps, n_bases):
     """The e2e call from two host threads on two streams: one call's device stages and output
     copy overlap the next call's input copy (PCIe is full duplex; the library lets the input
@@ -250,6 +264,8 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-e2e-pipelined", action="store_true")
+    ap.add_argument("--e2e-pipelined-only", action="store_true",
+                    help="(internal) run only the two-stream e2e measurement and print its JSON")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-reads", type=int, default=3_000_000)
@@ -263,6 +279,8 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args, world, rank, cfg)
+    if args.e2e_pipelined_only:
+        return pipelined_only(args)
 
     import torch
     import torch.distributed as dist
@@ -391,8 +409,17 @@ def main():
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(w.reads.nbytes + w.offsets.nbytes),
                "d2h_bytes_per_step": int(n_out * ((8 if k <= 32 else 16) + 4))}
         if world == 1 and not args.no_e2e_pipelined:
+            # in a process of its own (its own CUDA context), after this one's scratch is returned:
+            # whatever happens there cannot touch this run's numbers
+            kmc.empty_cache()
+            torch.cuda.empty_cache()
             try:
-                e2e["pipelined"] = e2e_pipelined(kmc, reads_h, offs_h, k, p, ci, cx, args.count_path, e_steps, n_bases)
+                cmd = [sys.executable, os.path.abspath(__file__), "--e2e-pipelined-only", "--config", args.config,
+                       "--scale", str(args.scale), "--steps", str(e_steps), "--count-path", str(args.count_path)]
+                pr = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+                line = [l_ for l_ in pr.stdout.splitlines() if l_.startswith("{")]
+                e2e["pipelined"] = json.loads(line[-1]) if pr.returncode == 0 and line else \
+                    {"error": f"rc {pr.returncode}: {pr.stderr.strip()[-300:]}"}
             except Exception as ex:  # the single-call e2e above stands; the failure is reported
                 e2e["pipelined"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 

@@ -8,6 +8,7 @@ w = synth.make("C4", scale=float(sys.argv[1]) if len(sys.argv) > 1 else 1.0)
 rh = torch.from_numpy(w.reads).pin_memory(); oh = torch.from_numpy(w.offsets.view(np.uint64)).pin_memory()
 if os.environ.get("KMC_TORCH_ALLOC"): kmc.use_torch_allocator(True)
 OPTS = eval(os.environ.get("KMC_OPTS", "dict()"))
+hold = torch.empty(int(os.environ.get("KMC_HOLD", "0")) * (20 << 30), dtype=torch.uint8, device="cuda")
 streams = [torch.cuda.Stream(), torch.cuda.Stream()]
 T0 = time.perf_counter(); log = []
 w2 = synth.make("C4", scale=0.1) if os.environ.get("SMALL2") else w
@@ -15,7 +16,7 @@ rh2 = torch.from_numpy(w2.reads).pin_memory(); oh2 = torch.from_numpy(w2.offsets
 def call(i, tag):
     t = time.perf_counter()
     R, O = (rh2, oh2) if i == 1 else (rh, oh)
-    r = kmc.count(R, O, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", stream=streams[i], **OPTS)
+    r = kmc.count(R, O, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device=os.environ.get("OUTDEV", "cpu"), stream=streams[i], **OPTS)
     log.append((tag, i, round((t - T0) * 1e3, 1), round((time.perf_counter() - T0) * 1e3, 1)))
     del r
 for i in range(2): call(i, "warm")
