@@ -641,7 +641,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         const uint64_t seg_sampled = std::max<uint64_t>(1, (seg_in + step - 1) / step);
         const double F = (double)seg_total / (double)seg_sampled;
         const uint32_t fl = (uint32_t)std::ceil(F);
-        CK(launch_scale_hist(hist_w, hist_r, ns, seg_total, seg_sampled, 4 * fl, fl, s));
+        CK(launch_scale_hist(hist_w, hist_r, ns, seg_total, seg_sampled, fl, fl, s));
         j->stage_end(nls + 1);
         PlanCtx& c = j->ctx;
         c.ns = ns;
