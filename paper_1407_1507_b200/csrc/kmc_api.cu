@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -194,6 +195,15 @@ bool is_device_ptr(const void* p) {
         return false;
     }
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// KMC_HOST_TRACE=1: host timestamps of the call's phases on stderr (diagnostics)
+void htrace(const char* what) {
+    static const bool on = getenv("KMC_HOST_TRACE") != nullptr;
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[kmc %8.3f ms] %s\n", std::chrono::duration<double, std::milli>(t - t0).count(), what);
 }
 
 // Host-resident inputs of concurrent calls cross the PCIe link one pass after another: a
@@ -689,6 +699,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         keep_slots = true;  // batch 0 is still in its slot
         int nl = run_p1(P1_MODE_SCATTER);
         a.sig_dest = nullptr;
+        htrace("scatter pass enqueued");
         CK(cudaMemcpyAsync(&hs[4], gstats + GS_P1_OVF, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         j->launches += nl;
@@ -747,6 +758,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         chain.end(j->cs);
         c.bins_ready = bins;
         c.a = a;
+        htrace("sampled distribution done");
         count_phase(j, c);
         return;
     }
@@ -849,19 +861,23 @@ void plan_phase(kmc_job* j, PlanCtx& c) {
 // plan is done, so that the caller can enqueue device work (S5) before waiting for them.
 void fetch_tables(kmc_job* j, PlanCtx& c) {
     if (!c.tables_pending) return;
+    htrace("fetch_tables");
     c.tables_pending = false;
     const uint64_t n_bins = c.n_bins;
     c.bw.assign(n_bins, 0);
     c.bn.assign(n_bins, 0);
     c.bo.assign(n_bins, 0);
-    j->make_copy_stream();
-    CK(cudaStreamWaitEvent(j->cs, c.ev_plan, 0));
+    // on the copy stream when there is one (host reads; or S5 is still running), else on the
+    // job's stream (creating a stream for three small copies costs more than it saves)
+    cudaStream_t fs = j->cs ? j->cs : j->s;
+    if (fs != j->s) CK(cudaStreamWaitEvent(fs, c.ev_plan, 0));
     cudaEventDestroy(c.ev_plan);
     c.ev_plan = nullptr;
-    CK(cudaMemcpyAsync(c.bw.data(), c.pa.bin_w, n_bins * 8, cudaMemcpyDeviceToHost, j->cs));
-    CK(cudaMemcpyAsync(c.bn.data(), c.pa.bin_nrec, n_bins * 8, cudaMemcpyDeviceToHost, j->cs));
-    CK(cudaMemcpyAsync(c.bo.data(), c.pa.bin_rec_off, n_bins * 8, cudaMemcpyDeviceToHost, j->cs));
-    CK(cudaStreamSynchronize(j->cs));
+    CK(cudaMemcpyAsync(c.bw.data(), c.pa.bin_w, n_bins * 8, cudaMemcpyDeviceToHost, fs));
+    CK(cudaMemcpyAsync(c.bn.data(), c.pa.bin_nrec, n_bins * 8, cudaMemcpyDeviceToHost, fs));
+    CK(cudaMemcpyAsync(c.bo.data(), c.pa.bin_rec_off, n_bins * 8, cudaMemcpyDeviceToHost, fs));
+    CK(cudaStreamSynchronize(fs));
+    htrace("tables fetched");
 }
 
 // Large bins of the default path for k <= 32 (k_split1.cu): one sized split pass puts every
@@ -873,6 +889,7 @@ void fetch_tables(kmc_job* j, PlanCtx& c) {
 template <class DR>
 void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vector<uint64_t>& large_ids, int kcap,
                   DR&& distinct_ratio) {
+    htrace("large_split1");
     (void)distinct_ratio;
     const int k = j->k;
     Arena& ar = j->arena;
@@ -999,6 +1016,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             CK(cudaMemsetAsync(cur, 0, dbase * 4, s));
             CK(cudaMemsetAsync(ctr, 0, 40, s));
             CK(launch_make_pieces(d_lbins, d_pp, gn, rpp, d_pieces, s));
+            htrace("split1 launch");
             CK(launch_split1(bins, d_pieces, n_pieces, d_sbins, k, !j->opt.non_canonical, cur, (uint64_t*)lkeys, ovf,
                              ctr + 3, ovf_cap, 2 * n_sms(), s));
             CK(launch_split1_chunks(d_sbins, gn, cur, 0xFFFFFFFFu, chunks, over, ovd, ctr, s));
@@ -1017,6 +1035,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             ovf_cap = n_ovk + (n_ovk >> 3) + 1024;
             ovf = ar.get<uint64_t>(ovf_cap);
         }
+        htrace("split1 done");
         j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
         CK(launch_chunk_hash(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, tovf,
                              ctr + 4, n_sms(), s));
@@ -1025,6 +1044,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
         CK(cudaMemcpyAsync(&hs[52], ctr + 4, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         const uint64_t n_tovf = hs[52];
+        htrace("chunk_hash done");
         j->st.n_overflow_chunks += n_tovf;
         if (n_over + n_ovd + n_ovk + n_tovf == 0) continue;
         int fl = 0;
@@ -1062,6 +1082,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
         }
         j->launches += fl;
         j->stage_end(fl);
+        htrace("fallback enqueued");
     }
     ar.release(lkeys);
     ar.release(ovf);
@@ -1496,6 +1517,7 @@ void count_multipass(kmc_job* j, PlanCtx& c) {
 // S6-S8 of the bins [b_lo, b_hi) (records in `bins`, addressed by global record index) into
 // the survivor buffer, grown to hold every survivor possible so far.
 void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t b_hi) {
+    htrace("count_bins");
     const int k = j->k, kw = j->key_words;
     const size_t ksz = kw == 1 ? 8 : 16;
     Arena& ar = j->arena;
@@ -1524,7 +1546,17 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
             large_ids.push_back(b);
         }
     }
-    std::sort(small.begin(), small.end(), [&](uint32_t x, uint32_t y) { return bw[x] > bw[y] || (bw[x] == bw[y] && x < y); });
+    htrace("classified");
+    {  // small bins by windows, largest first (ties by bin id): a counting sort, windows <= cap
+        uint64_t wmax = 0;
+        for (uint32_t b : small) wmax = std::max(wmax, bw[b]);
+        std::vector<uint32_t> start(wmax + 2, 0), sorted(small.size());
+        for (uint32_t b : small) ++start[wmax - bw[b] + 1];
+        for (uint64_t v = 1; v <= wmax + 1; ++v) start[v] += start[v - 1];
+        for (uint32_t b : small) sorted[start[wmax - bw[b]]++] = b;
+        small.swap(sorted);
+    }
+    htrace("sorted");
     j->st.n_large_bins += n_large;
     j->st.large_windows += large_windows;
     j->st.max_bin_windows = std::max<uint64_t>(j->st.max_bin_windows, max_bin);
@@ -1996,6 +2028,7 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
 }
 
 void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
+    htrace("finish");
     const int kw = j->key_words;
     const size_t ksz = kw == 1 ? 8 : 16;
     Arena& ar = j->arena;
@@ -2026,7 +2059,9 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     j->stage_begin(KMC_STAGE_ORDER);
     void* seg_k = nullptr;
     uint32_t* seg_v = nullptr;
+    htrace("order launch");
     CK(launch_order(kw, j->surv_keys, j->surv_counts, n, j->k, ok, oc, os, s, &sl, &over, &seg_k, &seg_v));
+    htrace("order enqueued");
     if (!over.empty()) {
         // oversize buckets (more survivors than one chunk): gathered into one array, sorted
         // together by the device LSD (they are disjoint, ascending key ranges, so the sorted
