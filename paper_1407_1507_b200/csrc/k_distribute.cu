@@ -81,24 +81,43 @@ __device__ __forceinline__ void encode16(const uint32_t (&wd)[4], uint32_t& pack
     }
 }
 
-// Lane w holds word w of a bitmask X (LSB-first; lanes past the mask hold 0).  Returns word
-// w of "X shifted down by s" (bit x <- bit x + s), 0 <= s < 64, via the next two lanes.
+// Lane w holds word w of a bitmask X (LSB-first; lanes past the mask hold 0, and the mask
+// has at most 30 words, so the lanes a shuffle wraps around to hold 0 too).  Word w of "X
+// shifted down by s" (bit x <- bit x + s): a compile-time s < 32 needs the next lane only,
+// a run-time s < 64 the next two.
+static_assert(NMW <= 30, "the wrapped lanes of a shuffle-down by 1 or 2 hold no mask word");
+template <int SH>
+__device__ __forceinline__ uint32_t shr_words_c(uint32_t x) {
+    static_assert(SH > 0 && SH < 32, "one-lane shift");
+    return __funnelshift_r(x, __shfl_down_sync(0xffffffffu, x, 1), SH);
+}
 __device__ __forceinline__ uint32_t shr_words(uint32_t x, int s) {
     const uint32_t x1 = __shfl_down_sync(0xffffffffu, x, 1), x2 = __shfl_down_sync(0xffffffffu, x, 2);
-    const int lane = threadIdx.x & 31;
-    const uint32_t n1 = lane < 31 ? x1 : 0u, n2 = lane < 30 ? x2 : 0u;
-    return s < 32 ? __funnelshift_r(x, n1, s) : __funnelshift_r(n1, n2, s - 32);
+    return s < 32 ? __funnelshift_r(x, x1, s) : __funnelshift_r(x1, x2, s - 32);
 }
-// Word w (lane w) of R_L: bit x = AND of G over positions [x, x + L) (L <= 63), by doubling.
-__device__ __forceinline__ uint32_t run_and(uint32_t g, int L) {
-    if (L == 0) return 0xFFFFFFFFu;
-    uint32_t r = g;
-    int a = 1;
-    while (2 * a <= L) {
-        r &= shr_words(r, a);
-        a *= 2;
-    }
-    return a == L ? r : (r & shr_words(r, L - a));
+// Bit x of word w (lane w) of R_L = AND of G over positions [x, x + L), for two run lengths at
+// once (L1, L2 <= 63), from one doubling chain R_1, R_2, R_4, .. (R_2a = R_a & R_a >> a):
+// R_L = R_a & (R_a >> (L - a)) for the largest power of two a <= L.
+__device__ __forceinline__ void run_and2(uint32_t g, int L1, int L2, uint32_t& o1, uint32_t& o2) {
+    const int need = max(L1, L2);
+    uint32_t r[6];
+    r[0] = g;
+    r[1] = r[0] & shr_words_c<1>(r[0]);
+    r[2] = r[1] & shr_words_c<2>(r[1]);
+    r[3] = r[2] & shr_words_c<4>(r[2]);
+    r[4] = need >= 16 ? r[3] & shr_words_c<8>(r[3]) : 0u;
+    r[5] = need >= 32 ? r[4] & shr_words_c<16>(r[4]) : 0u;
+    auto pick = [&](int i) {  // r[i] without dynamic register indexing
+        return i == 0 ? r[0] : i == 1 ? r[1] : i == 2 ? r[2] : i == 3 ? r[3] : i == 4 ? r[4] : r[5];
+    };
+    auto run = [&](int L) -> uint32_t {
+        if (L == 0) return 0xFFFFFFFFu;
+        const int i = 31 - __clz(L), a = 1 << i;
+        const uint32_t ra = pick(i);
+        return a == L ? ra : (ra & shr_words(ra, L - a));
+    };
+    o1 = run(L1);
+    o2 = run(L2);
 }
 
 __device__ __forceinline__ uint32_t rev2_32(uint32_t x) {  // reverse the order of the 2-bit groups
@@ -243,8 +262,10 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
         {
             const uint32_t g = lane < NMW ? ~S.bad[lane] : 0u;
             const uint32_t iv = lane < NMW ? S.inv[lane] : 0xFFFFFFFFu;
-            const uint32_t vw = ~iv & shr_words(run_and(g, k - 1), 1);
-            const uint32_t vp = ~iv & shr_words(run_and(g, p - 1), 1);
+            uint32_t rw, rp;
+            run_and2(g, k - 1, p - 1, rw, rp);
+            const uint32_t vw = ~iv & shr_words_c<1>(rw);
+            const uint32_t vp = ~iv & shr_words_c<1>(rp);
             if (lane < NMW) {
                 S.vwin[lane] = vw;
                 S.vpm[lane] = vp;
