@@ -142,23 +142,24 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         for (uint32_t w = tid; w < T; w += S1_NT) for_unit_keys(w, [&](uint64_t key) { atomicAdd(&h[s1_digit(key, nd)], 1u); });
         __syncthreads();
         // ---- R: one reservation per digit in its region (+ overflow beyond it); stage offsets
+        // (the reservation's round trip overlaps the stage-offset scan, which needs only c)
         uint32_t c = 0, g = 0;
         if ((uint32_t)tid < nd) {
             c = h[tid];
             h[tid] = 0;  // ready for the next piece
-            if (c) {
-                g = atomicAdd(&cur[sb.dbase + tid], c);
-                if (g + c > sb.rc) {
-                    const uint32_t lo = g > sb.rc ? g : sb.rc;
-                    ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + c - lo));
-                }
-            }
-            gst[tid] = g;
+            if (c) g = atomicAdd(&cur[sb.dbase + tid], c);
         }
         uint32_t npk;
         const uint32_t cp = (uint32_t)tid < nd ? c + 1 : 0u;  // one spare slot per digit (parity)
         const uint32_t P = block_excl_sum1<S1_NT, uint32_t>(cp, wsumB, &npk);
-        if ((uint32_t)tid < nd) lof[tid] = lc[tid] = P + ((P ^ g) & 1u);
+        if ((uint32_t)tid < nd) {
+            if (c && g + c > sb.rc) {
+                const uint32_t lo = g > sb.rc ? g : sb.rc;
+                ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + c - lo));
+            }
+            gst[tid] = g;
+            lof[tid] = lc[tid] = P + ((P ^ g) & 1u);
+        }
         __syncthreads();
         const bool staged = npk <= (uint32_t)S1_STAGE;
         uint64_t* region = keys + sb.key_base;
