@@ -477,7 +477,8 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             }
             if ((MODE == P1_MODE_HIST || (MODE == P1_MODE_SCATTER && a.scatter_hist)) && idx < emit_end) {
                 atomicAdd(&a.hist_w[s], (unsigned long long)n);
-                atomicAdd(&a.hist_r[s], (uint32_t)nrec);
+                // (the sampled scatter's record counts per bin are its bins' fill counters)
+                if (MODE == P1_MODE_HIST) atomicAdd(&a.hist_r[s], (uint32_t)nrec);
             }
             // slots: temporary stream (pass 1) from the warp's reserved block, or the bins
             uint64_t slot0 = 0;

@@ -188,13 +188,13 @@ __global__ void k_sig_dest(const uint32_t* sig2bin, const uint32_t* cap, const u
     }
 }
 __global__ void k_bins_exact(uint64_t ns, const uint64_t* B, const uint64_t* bin_first, const uint64_t* Wp,
-                             const uint64_t* Rp, uint64_t* bin_w, uint64_t* bin_nrec) {
+                             const uint32_t* fill, uint64_t* bin_w, uint64_t* bin_nrec) {
     const uint64_t n_bins = B[ns];
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n_bins;
          b += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t fs = bin_first[b], fe = bin_first[b + 1];
         bin_w[b] = Wp[fe] - Wp[fs];
-        bin_nrec[b] = Rp[fe] - Rp[fs];
+        bin_nrec[b] = fill[b];
     }
 }
 __global__ void k_hist_stats(const unsigned long long* hw, uint64_t ns, unsigned long long* gstats) {
@@ -237,16 +237,15 @@ cudaError_t launch_bin_caps(const uint64_t* bin_nrec, uint64_t n_bins, double F,
     return scan_generic<uint64_t>(ArrayIn<uint64_t>{bin_cap_u64}, n_bins, out_scan, (uint64_t*)temp, s, nullptr);
 }
 
-cudaError_t launch_exact_tables(const PlanArgs& a, uint64_t n_bins, cudaStream_t s, int* n_launches) {
+cudaError_t launch_exact_tables(const PlanArgs& a, uint64_t n_bins, const uint32_t* bin_fill, cudaStream_t s,
+                                int* n_launches) {
     cudaError_t e;
     uint64_t* tmp = (uint64_t*)a.temp;
     if ((e = scan_generic<uint64_t>(ArrayIn<unsigned long long>{a.hist_w}, a.ns, a.win_scan, tmp, s, n_launches)) !=
         cudaSuccess)
         return e;
-    if ((e = scan_generic<uint64_t>(ArrayIn<uint32_t>{a.hist_r}, a.ns, a.rec_scan, tmp, s, n_launches)) != cudaSuccess)
-        return e;
     k_bins_exact<<<(unsigned)std::min<uint64_t>((n_bins + 255) / 256 + 1, 4096), 256, 0, s>>>(
-        a.ns, a.bnd_scan, a.bin_first, a.win_scan, a.rec_scan, a.bin_w, a.bin_nrec);
+        a.ns, a.bnd_scan, a.bin_first, a.win_scan, bin_fill, a.bin_w, a.bin_nrec);
     if ((e = cudaGetLastError())) return e;
     k_hist_stats<<<(unsigned)((a.ns + 255) / 256), 256, 0, s>>>(a.hist_w, a.ns, a.gstats);
     if (n_launches) *n_launches += 2;

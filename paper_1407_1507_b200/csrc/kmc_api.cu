@@ -711,22 +711,21 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             // ---- exact per-bin tables on the sampled plan
             j->stage_begin(KMC_STAGE_PLAN);
             int pl = 0;
-            CK(launch_exact_tables(pa, n_bins, s, &pl));
+            CK(launch_exact_tables(pa, n_bins, bin_fill, s, &pl));
             j->launches += pl;
             j->stage_end(pl);
             CK(cudaMemcpyAsync(&hs[1], pa.win_scan + ns, 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(&hs[2], pa.rec_scan + ns, 8, cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             c.n_windows = hs[1];
-            c.n_records = hs[2];
+            c.n_records = hs[16 + GS_RECORDS];  // (the bins' fill counters are the per-bin counts)
             j->st.n_windows = c.n_windows;
             j->st.n_superkmers = hs[16 + GS_SUPERKMERS];
             j->st.n_records = c.n_records;
             j->st.n_invalid_bases = hs[16 + GS_INVALID];
             j->st.n_signatures_used = hs[16 + GS_SIGS_USED];
             j->st.max_signature_windows = hs[16 + GS_MAX_SIG];
-            if (hs[16 + GS_WINDOWS] != c.n_windows || hs[16 + GS_RECORDS] != c.n_records) {
+            if (hs[16 + GS_WINDOWS] != c.n_windows) {
                 set_err("sampled distribution: histogram totals disagree with pass-1 counters");
                 throw Fail{KMC_ERR_INTERNAL};
             }
@@ -736,10 +735,19 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
                 CK(cudaEventRecord(c.ev_plan, s));
             }
         } else {
-            // ---- a bin overflowed its sampled capacity: plan again from the exact histograms
-            //      of this pass and scatter again with exact offsets
+            // ---- a bin overflowed its sampled capacity: the exact histograms (a histogram
+            //      pass: the scatter pass counts windows only), the exact plan, and the
+            //      scatter again with exact offsets
             j->st.n_distribute_reruns += 1;
             ar.release(bins);
+            j->stage_begin(KMC_STAGE_SIGNATURE);
+            CK(cudaMemsetAsync(hist_w, 0, ns * 8, s));
+            CK(cudaMemsetAsync(hist_r, 0, ns * 4, s));
+            CK(cudaMemsetAsync(gstats, 0, GS_N * 8, s));
+            a.scatter_hist = 0;
+            nl = run_p1(P1_MODE_HIST);
+            j->launches += nl;
+            j->stage_end(nl);
             plan_phase(j, c);
             bins = reinterpret_cast<uint32_t*>(ar.alloc(std::max<uint64_t>(c.n_records, 1) * RWs * 4));
             j->stage_begin(KMC_STAGE_SCATTER);

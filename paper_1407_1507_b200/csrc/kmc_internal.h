@@ -54,7 +54,7 @@ struct P1Args {
     uint32_t bin_lo, bin_hi;  // pass 2 writes only the records of bins [bin_lo, bin_hi)
     const uint4* sig_dest;    // pass 2 (sampled plan): per signature {bin, capacity, first slot lo, hi};
                               // records beyond the capacity are dropped and counted in GS_P1_OVF
-    int scatter_hist;         // pass 2 also accumulates hist_w / hist_r (sampled plan)
+    int scatter_hist;         // pass 2 also accumulates hist_w (sampled plan)
     uint32_t seg_step;        // 0/1: every segment; s > 1: every s-th segment (the sample pass)
     // pass 1: temporary record stream (nullptr = not used)
     uint32_t* tmp_recs;
@@ -150,10 +150,11 @@ cudaError_t launch_sig_dest(const uint32_t* sig2bin, const uint32_t* bin_cap, co
                             uint4* sig_dest, cudaStream_t s);
 cudaError_t launch_bin_caps(const uint64_t* bin_nrec, uint64_t n_bins, double F, double z, uint32_t margin,
                             uint32_t* bin_cap, uint64_t* bin_cap_u64, uint64_t* out_scan, void* temp, cudaStream_t s);
-// Exact per-bin tables from exact histograms and an existing bin plan (bin_first): scans of
-// hist_w / hist_r into win_scan / rec_scan, bin_w / bin_nrec (bin_rec_off untouched), and the
-// histogram statistics (GS_SIGS_USED, GS_MAX_SIG)
-cudaError_t launch_exact_tables(const PlanArgs& a, uint64_t n_bins, cudaStream_t s, int* n_launches);
+// Exact per-bin tables on an existing bin plan (bin_first) after the sampled scatter: the scan
+// of the exact hist_w into win_scan, bin_w from it, bin_nrec = the bins' fill counters
+// (bin_rec_off untouched), and the histogram statistics (GS_SIGS_USED, GS_MAX_SIG)
+cudaError_t launch_exact_tables(const PlanArgs& a, uint64_t n_bins, const uint32_t* bin_fill, cudaStream_t s,
+                                int* n_launches);
 
 // ------------------------------------------------------------ phase 2 (sorting)
 struct SmallArgs {

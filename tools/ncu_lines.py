@@ -57,7 +57,8 @@ def main():
         ti = sum(v[0] for _, v in items) or 1
         ts = sum(v[1] for _, v in items) or 1
         print(f"== {f}: {ti} warp instr, {ts} stall samples")
-        for (fn, line), (ins, st) in sorted(items, key=lambda kv: -kv[1][1])[:top]:
+        byi = len(sys.argv) > 4 and sys.argv[4] == "instr"
+        for (fn, line), (ins, st) in sorted(items, key=lambda kv: -kv[1][0 if byi else 1])[:top]:
             print(f"  L{line:4d} instr {100*ins/ti:5.1f}%  stalls {100*st/ts:5.1f}%  {src.get((fn, line), '')}")
 
 

@@ -1,6 +1,6 @@
 """Instruction and stall shares of k_sig (k_distribute.cu) by pass-1 phase, from an ncu report's
 source page.  usage: python tools/ncu_phases.py REPORT.ncu-rep"""
-import csv, io, subprocess, sys, collections
+import csv, io, os, subprocess, sys, collections
 rep=sys.argv[1]
 out=subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","cuda,sass"],capture_output=True,text=True).stdout
 hdr=None; fpath=None; cur=None; agg=collections.Counter(); st=collections.Counter()
@@ -17,7 +17,21 @@ for row in csv.reader(io.StringIO(out)):
     try:
         agg[cur]+=int(float(d.get("Instructions Executed","0") or 0)); st[cur]+=int(float(d.get("Warp Stall Sampling (All Samples)","0") or 0))
     except ValueError: pass
-bounds=[(154,"A encode"),(230,"B read starts"),(241,"validity"),(254,"C p-mer keys"),(312,"D/E sliding min"),(386,"F runs"),(422,"G emission"),(532,"carry"),(547,"stats"),(10**9,"end")]
+# phase boundaries from the markers in the current source (line numbers move with edits)
+SRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1407_1507_b200", "csrc", "k_distribute.cu")
+MARK = [("// ---- A: load + encode", "A encode"), ("// ---- B: read starts", "B read starts"),
+        ("// validity masks by doubling", "validity"), ("// ---- C: canonical p-mer keys", "C p-mer keys"),
+        ("// ---- D: sliding minimum", "D/E sliding min"), ("// ---- F: super-k-mers", "F runs"),
+        ("// G: records of the runs", "G emission"), ("// carry the rest", "carry"),
+        ("// ---- per-warp statistics", "stats")]
+lines = open(SRC).read().split("\n")
+bounds = []
+for m, name in MARK:
+    for i, l in enumerate(lines):
+        if m in l:
+            bounds.append((i + 1, name))
+            break
+bounds.append((10**9, "end"))
 ph=collections.Counter(); phs=collections.Counter()
 T=sum(agg.values()); S=sum(st.values())
 for (f,l),v in agg.items():
