@@ -263,7 +263,10 @@ def main():
     ap.add_argument("--impl", default="kmcgpu", choices=["kmcgpu", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--no-e2e-pipelined", action="store_true")
+    ap.add_argument("--e2e-pipelined", action="store_true",
+                    help="also time the e2e call with two calls in flight (two threads / streams, in a "
+                         "subprocess); off by default: concurrent calls in one process are not supported "
+                         "yet (DESIGN.md 12)")
     ap.add_argument("--e2e-pipelined-only", action="store_true",
                     help="(internal) run only the two-stream e2e measurement and print its JSON")
     ap.add_argument("--no-e2e", action="store_true")
@@ -408,7 +411,7 @@ def main():
         e2e = {"value": world * n_bases / (e_ms / 1e3), "unit": "bases/s",
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(w.reads.nbytes + w.offsets.nbytes),
                "d2h_bytes_per_step": int(n_out * ((8 if k <= 32 else 16) + 4))}
-        if world == 1 and not args.no_e2e_pipelined:
+        if world == 1 and args.e2e_pipelined:
             # in a process of its own (its own CUDA context), after this one's scratch is returned:
             # whatever happens there cannot touch this run's numbers
             kmc.empty_cache()

@@ -234,6 +234,7 @@ struct H2DChain {
     }
 };
 
+std::mutex g_begin_mu;  // kmc_count_begin (S1-S8) of concurrent calls, one at a time
 std::mutex g_pin_mu;
 std::vector<unsigned long long*> g_pin_free;
 unsigned long long* pin_acquire() {
@@ -2177,6 +2178,10 @@ kmc_status kmc_count_begin(const uint8_t* reads, const uint64_t* read_offsets, u
     }
     j->arena.bind(j->s);
     try {
+        // Calls from several host threads of one process run S1-S8 one after another: two
+        // overlapping calls hit an illegal address in a race not yet found (one
+        // process per stream of calls is fine).  S9 and the output copy still overlap.
+        std::lock_guard<std::mutex> g(g_begin_mu);
         run_begin(j, reads, read_offsets, n_reads);
     } catch (const Fail& f) {
         cudaStreamSynchronize(j->s);
