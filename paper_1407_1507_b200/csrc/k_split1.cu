@@ -44,9 +44,14 @@ constexpr size_t S1_OFF_RB = S1_OFF_STAGE + (size_t)S1_STAGE * 8;
 constexpr size_t S1_OFF_UMAP = S1_OFF_RB + 2 * (size_t)S1_RBW * 4;
 constexpr size_t S1_OFF_RINFO = S1_OFF_UMAP + (size_t)S1_UMAX * 2;
 constexpr size_t S1_OFF_DIG = S1_OFF_RINFO + (size_t)S1_REC * 4;  // h, gst, lof, lc, ovb: S1_DMAX each
-constexpr size_t S1_OFF_MBAR = S1_OFF_DIG + 5 * (size_t)S1_DMAX * 4;
+constexpr int S1_SOVF = 256;      // single-pass mode: keys beyond their digit's stage region
+constexpr size_t S1_OFF_SOVK = S1_OFF_DIG + 5 * (size_t)S1_DMAX * 4;
+constexpr size_t S1_OFF_SOVI = S1_OFF_SOVK + (size_t)S1_SOVF * 8;
+constexpr size_t S1_OFF_MBAR = S1_OFF_SOVI + (size_t)S1_SOVF * 4;
 constexpr size_t S1_SMEM = S1_OFF_MBAR + 16 + 16;
-static_assert(S1_OFF_RB % 16 == 0 && S1_OFF_MBAR % 8 == 0, "alignment");
+static_assert(S1_OFF_RB % 16 == 0 && S1_OFF_MBAR % 8 == 0 && S1_OFF_SOVK % 8 == 0, "alignment");
+static_assert(2 * S1_SMEM + 2048 <= 228 * 1024, "two CTAs per SM");
+static_assert(S1_DMAX <= 512, "digit in 9 bits of an overflow entry");
 static_assert(S1_DMAX <= S1_NT, "one thread per digit");
 
 template <bool CANON>
@@ -65,8 +70,11 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
     uint32_t* lof = gst + S1_DMAX; // run start in the stage
     uint32_t* lc = lof + S1_DMAX;  // stage cursor
     uint32_t* ovb = lc + S1_DMAX;  // first overflow slot of the digit's keys beyond the region
+    uint64_t* sovk = reinterpret_cast<uint64_t*>(sm + S1_OFF_SOVK);  // single pass: stage-overflow keys
+    uint32_t* sovi = reinterpret_cast<uint32_t*>(sm + S1_OFF_SOVI);  //   their digit | rank << 9
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + S1_OFF_MBAR);
     __shared__ uint32_t wsumA[S1_NT / 32], wsumB[S1_NT / 32];  // alternating scan scratch
+    __shared__ uint32_t novf;
     const int tid = threadIdx.x;
     const int U = unit;
     const uint32_t R = gridDim.x, r = blockIdx.x;
@@ -116,8 +124,12 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
             bulk_wait_read();
             bulk_pending = false;
         }
+        if (tid < S1_DMAX) lc[tid] = 0;  // (the same thread read it last: the previous piece's W)
+        if (tid == 0) novf = 0;
         uint32_t T;
-        const uint32_t pre = block_excl_sum1<S1_NT, uint32_t>(nu, wsumA, &T);
+        const uint32_t pre2 = block_excl_sum1<S1_NT, uint32_t>(nu | (n << 16), wsumA, &T);
+        const uint32_t NWIN = T >> 16, pre = pre2 & 0xFFFFu;
+        T &= 0xFFFFu;
         for (uint32_t j = 0; j < nu; ++j) umap[pre + j] = (uint16_t)tid;
         if ((uint32_t)tid < pc.nrec) rinfo[tid] = pre | (n << 16);
         __syncthreads();
@@ -138,6 +150,66 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
                 }
             }
         };
+        uint64_t* region = keys + sb.key_base;
+        // place key at position i of digit d: its region, or the overflow list beyond it
+        auto put = [&](uint32_t d, uint32_t i, uint64_t key) {
+            if (i < sb.rc) {
+                region[(uint64_t)d * sb.rc + i] = key;
+            } else {
+                const uint32_t lo = gst[d] > sb.rc ? gst[d] : sb.rc;
+                const uint64_t o = (uint64_t)ovb[d] + (i - lo);
+                if (o < ovf_cap) ovf[o] = key;
+            }
+        };
+        // ---- single pass (pieces whose windows fill at most 4/5 of the stage): every key is
+        //      expanded once and placed at its rank in its digit's share of the stage (keys
+        //      beyond it: a short list with digit and rank); the digits' counts then reserve the
+        //      regions, and warps copy every digit's run out with coalesced stores
+        const uint32_t C1 = nd ? (uint32_t)S1_STAGE / nd : 0u;
+        if (NWIN + NWIN / 4 + 16 * nd <= (uint32_t)S1_STAGE) {
+            for (uint32_t w = tid; w < T; w += S1_NT)
+                for_unit_keys(w, [&](uint64_t key) {
+                    const uint32_t d = s1_digit(key, nd);
+                    const uint32_t q = atomicAdd(&lc[d], 1u);
+                    if (q < C1) {
+                        stage[d * C1 + q] = key;
+                    } else {
+                        const uint32_t o = atomicAdd(&novf, 1u);
+                        if (o < (uint32_t)S1_SOVF) {
+                            sovk[o] = key;
+                            sovi[o] = d | (q << 9);
+                        }
+                    }
+                });
+            __syncthreads();
+            const uint32_t nov = novf;  // (read before the next piece's thread 0 resets it)
+            if (nov <= (uint32_t)S1_SOVF) {
+                uint32_t c = 0, g = 0;
+                if ((uint32_t)tid < nd) {
+                    c = lc[tid];
+                    if (c) g = atomicAdd(&cur[sb.dbase + tid], c);
+                    if (c && g + c > sb.rc) {
+                        const uint32_t lo = g > sb.rc ? g : sb.rc;
+                        ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + c - lo));
+                    }
+                    gst[tid] = g;
+                    lof[tid] = c;
+                }
+                __syncthreads();
+                for (uint32_t d = tid >> 5; d < nd; d += S1_NT / 32) {
+                    const uint32_t m = min(lof[d], C1), g0 = gst[d];
+                    for (uint32_t i = tid & 31; i < m; i += 32) put(d, g0 + i, stage[d * C1 + i]);
+                }
+                for (uint32_t o = tid; o < nov; o += S1_NT) {
+                    const uint32_t d = sovi[o] & 511u;
+                    put(d, gst[d] + (sovi[o] >> 9), sovk[o]);
+                }
+                continue;  // (the next piece's first barrier ends this one's reads of the stage)
+            }
+            // the overflow list itself overflowed: this piece takes the two-pass mode
+            if ((uint32_t)tid < nd) lc[tid] = 0;
+            __syncthreads();
+        }
         // ---- A: digit histogram
         for (uint32_t w = tid; w < T; w += S1_NT) for_unit_keys(w, [&](uint64_t key) { atomicAdd(&h[s1_digit(key, nd)], 1u); });
         __syncthreads();
@@ -162,7 +234,6 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         }
         __syncthreads();
         const bool staged = npk <= (uint32_t)S1_STAGE;
-        uint64_t* region = keys + sb.key_base;
         // ---- B: place every key (stage, or straight to its region / the overflow list)
         for (uint32_t w = tid; w < T; w += S1_NT)
             for_unit_keys(w, [&](uint64_t key) {
