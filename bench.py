@@ -411,6 +411,19 @@ def main():
         e2e = {"value": world * n_bases / (e_ms / 1e3), "unit": "bases/s",
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(w.reads.nbytes + w.offsets.nbytes),
                "d2h_bytes_per_step": int(n_out * ((8 if k <= 32 else 16) + 4))}
+        # context: the link itself -- one plain copy of the same pinned reads and offsets
+        scratch = torch.empty(w.reads.nbytes + w.offsets.nbytes, dtype=torch.uint8, device="cuda")
+        l0 = torch.cuda.Event(enable_timing=True)
+        l1 = torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        scratch[:w.reads.nbytes].copy_(reads_h, non_blocking=True)
+        scratch[w.reads.nbytes:].copy_(offs_h.view(torch.uint8), non_blocking=True)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        link_ms = l0.elapsed_time(l1)
+        e2e["link_h2d"] = {"ms": round(link_ms, 2), "gbs": round(e2e["h2d_bytes_per_step"] / (link_ms / 1e3) / 1e9, 1),
+                           "note": "one plain copy of the same pinned inputs; the e2e step cannot be faster"}
+        del scratch
         if world == 1 and args.e2e_pipelined:
             # in a process of its own (its own CUDA context), after this one's scratch is returned:
             # whatever happens there cannot touch this run's numbers
