@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(RLE_NT) k_rle(const K* __restrict__ keys, uint
         if (i >= n) continue;
         const K key = keys[i];
         if (i > 0 && key_eq(keys[i - 1], key)) continue;
+        if (key_eq(key, key_empty<K>())) continue;  // pads of the one-pass split (never a k-mer)
         // galloping search for the end of the run
         uint64_t lo = i, hi, step = 1;
         for (;;) {
@@ -1047,7 +1048,8 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 const uint32_t i = t + (u0 + u) * CH_NT;
-                if (i < ch.n) ok &= table_insert_bounded<K>(T, C, lg, cur[u]);
+                // (the one-pass split pads odd runs with EMPTY keys: skipped)
+                if (i < ch.n && !key_eq(cur[u], E)) ok &= table_insert_bounded<K>(T, C, lg, cur[u]);
             }
 #pragma unroll
             for (int u = 0; u < UNR; ++u) cur[u] = nxt[u];

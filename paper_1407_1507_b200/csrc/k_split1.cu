@@ -164,8 +164,10 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         // ---- single pass (pieces whose windows fill at most 4/5 of the stage): every key is
         //      expanded once and placed at its rank in its digit's share of the stage (keys
         //      beyond it: a short list with digit and rank); the digits' counts then reserve the
-        //      regions, and warps copy every digit's run out with coalesced stores
-        const uint32_t C1 = nd ? (uint32_t)S1_STAGE / nd : 0u;
+        //      regions -- always an even number of slots, the odd one out an EMPTY key that the
+        //      counting skips, so every run starts 16-byte aligned -- and every digit's run leaves
+        //      by one TMA bulk copy issued by its thread while the other threads move on
+        const uint32_t C1 = nd ? ((uint32_t)S1_STAGE / nd) & ~1u : 0u;
         if (NWIN + NWIN / 4 + 16 * nd <= (uint32_t)S1_STAGE) {
             for (uint32_t w = tid; w < T; w += S1_NT)
                 for_unit_keys(w, [&](uint64_t key) {
@@ -181,30 +183,45 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
                         }
                     }
                 });
+            fence_proxy_async_smem();  // stage writes -> the bulk copies
             __syncthreads();
             const uint32_t nov = novf;  // (read before the next piece's thread 0 resets it)
             if (nov <= (uint32_t)S1_SOVF) {
-                uint32_t c = 0, g = 0;
                 if ((uint32_t)tid < nd) {
-                    c = lc[tid];
-                    if (c) g = atomicAdd(&cur[sb.dbase + tid], c);
-                    if (c && g + c > sb.rc) {
+                    const uint32_t c = lc[tid], ce = c + (c & 1u);
+                    uint32_t g = 0;
+                    if (c) g = atomicAdd(&cur[sb.dbase + tid], ce);
+                    if (c && g + ce > sb.rc) {
                         const uint32_t lo = g > sb.rc ? g : sb.rc;
-                        ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + c - lo));
+                        ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + ce - lo));
                     }
                     gst[tid] = g;
                     lof[tid] = c;
+                    if (c) {
+                        // the stage part (+ the pad slot when the run ends inside it), even-sized
+                        uint32_t sn = c < C1 ? ce : C1;
+                        if ((c & 1u) && c < C1) {
+                            stage[tid * C1 + c] = ~0ull;
+                            fence_proxy_async_smem();
+                        }
+                        const uint32_t in_reg = g >= sb.rc ? 0u : min(sn, sb.rc - g);  // even: g, rc even
+                        if (in_reg) {
+                            tma_store_1d(region + (uint64_t)tid * sb.rc + g, stage + tid * C1, in_reg * 8u);
+                            bulk_commit();
+                            bulk_pending = true;
+                        }
+                        for (uint32_t i = in_reg; i < sn; ++i) put(tid, g + i, stage[tid * C1 + i]);
+                        if ((c & 1u) && c >= C1) put(tid, g + c, ~0ull);  // the pad after the overflow part
+                    }
                 }
-                __syncthreads();
-                for (uint32_t d = tid >> 5; d < nd; d += S1_NT / 32) {
-                    const uint32_t m = min(lof[d], C1), g0 = gst[d];
-                    for (uint32_t i = tid & 31; i < m; i += 32) put(d, g0 + i, stage[d * C1 + i]);
+                if (nov) {
+                    __syncthreads();  // gst / ovb of every digit for the overflow entries
+                    for (uint32_t o = tid; o < nov; o += S1_NT) {
+                        const uint32_t d = sovi[o] & 511u;
+                        put(d, gst[d] + (sovi[o] >> 9), sovk[o]);
+                    }
                 }
-                for (uint32_t o = tid; o < nov; o += S1_NT) {
-                    const uint32_t d = sovi[o] & 511u;
-                    put(d, gst[d] + (sovi[o] >> 9), sovk[o]);
-                }
-                continue;  // (the next piece's first barrier ends this one's reads of the stage)
+                continue;  // (the next piece waits for its bulk copies before writing the stage)
             }
             // the overflow list itself overflowed: this piece takes the two-pass mode
             if ((uint32_t)tid < nd) lc[tid] = 0;
@@ -219,15 +236,15 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         if ((uint32_t)tid < nd) {
             c = h[tid];
             h[tid] = 0;  // ready for the next piece
-            if (c) g = atomicAdd(&cur[sb.dbase + tid], c);
+            if (c) g = atomicAdd(&cur[sb.dbase + tid], c + (c & 1u));  // even: see the single pass
         }
         uint32_t npk;
         const uint32_t cp = (uint32_t)tid < nd ? c + 1 : 0u;  // one spare slot per digit (parity)
         const uint32_t P = block_excl_sum1<S1_NT, uint32_t>(cp, wsumB, &npk);
         if ((uint32_t)tid < nd) {
-            if (c && g + c > sb.rc) {
+            if (c && g + c + (c & 1u) > sb.rc) {
                 const uint32_t lo = g > sb.rc ? g : sb.rc;
-                ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + c - lo));
+                ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + c + (c & 1u) - lo));
             }
             gst[tid] = g;
             lof[tid] = lc[tid] = P + ((P ^ g) & 1u);
@@ -276,6 +293,7 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
                 if (o < ovf_cap) ovf[o] = stage[s0 + e];
             }
         }
+        if ((uint32_t)tid < nd && (c & 1u)) put(tid, g + c, ~0ull);  // the pad slot of an odd run
     }
     if (bulk_pending) bulk_wait_all();
 }
