@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
     bool bulk_pending = false;
     uint32_t cur_bin = 0xFFFFFFFFu;
     S1Bin sb{};
+    uint32_t C1 = 0;  // single pass: stage slots of a digit (even), per bin
+    const uint32_t umagic = (65536u + (uint32_t)U - 1) / (uint32_t)U;  // (x / U) = (x * umagic) >> 16, x < 64
     Piece pnext = pieces[p0];
     for (uint64_t p = p0; p < p1; ++p) {
         const uint32_t it = (uint32_t)(p - p0);
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         if (pc.lbin != cur_bin) {
             cur_bin = pc.lbin;
             sb = sbins[cur_bin];
+            C1 = sb.nd ? ((uint32_t)S1_STAGE / sb.nd) & ~1u : 0u;
         }
         const uint32_t nd = sb.nd;
         mbar_wait(mbar + b, (it >> 1) & 1);
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         uint32_t n = 0, nu = 0;
         if ((uint32_t)tid < pc.nrec) {
             n = rec_nwin(Rp + tid * 4);
-            nu = (n + U - 1) / U;
+            nu = ((n + U - 1) * umagic) >> 16;
         }
         if (bulk_pending) {  // the previous piece's stage has been read by its bulk copies
             bulk_wait_read();
@@ -167,7 +170,6 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         //      regions -- always an even number of slots, the odd one out an EMPTY key that the
         //      counting skips, so every run starts 16-byte aligned -- and every digit's run leaves
         //      by one TMA bulk copy issued by its thread while the other threads move on
-        const uint32_t C1 = nd ? ((uint32_t)S1_STAGE / nd) & ~1u : 0u;
         if (NWIN + NWIN / 4 + 16 * nd <= (uint32_t)S1_STAGE) {
             for (uint32_t w = tid; w < T; w += S1_NT)
                 for_unit_keys(w, [&](uint64_t key) {
