@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         //      regions -- always an even number of slots, the odd one out an EMPTY key that the
         //      counting skips, so every run starts 16-byte aligned -- and every digit's run leaves
         //      by one TMA bulk copy issued by its thread while the other threads move on
-        if (NWIN + NWIN / 4 + 16 * nd <= (uint32_t)S1_STAGE) {
+        if (NWIN + NWIN / 8 + 16 * nd <= (uint32_t)S1_STAGE) {
             for (uint32_t w = tid; w < T; w += S1_NT)
                 for_unit_keys(w, [&](uint64_t key) {
                     const uint32_t d = s1_digit(key, nd);
