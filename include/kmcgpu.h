@@ -132,6 +132,7 @@ typedef struct {
     uint64_t n_passes;         /* passes over bin ranges (host-resident reads beyond HBM); 1 = one pass */
     uint64_t n_distribute_reruns; /* sampled distribution: 1 if a bin overflowed its sampled capacity
                                   and pass 1 was repeated on the exact plan */
+    uint64_t n_presplit_bins;  /* large bins split batch by batch during pass 1 (presplit) */
     float stage_ms[KMC_N_STAGES];   /* per-stage device time (profile != 0), else 0 */
     uint32_t stage_launches[KMC_N_STAGES];
 } kmc_stats;
@@ -195,6 +196,11 @@ typedef struct {
     uint32_t split_tight;      /* testing (one-pass split): 1 = digit regions without slack
                                   (ceil(W / nd) + 2 slots), so digits overflow into the overflow
                                   list and the fallback is exercised */
+    uint32_t presplit;         /* sampled distribution, one-pass split path (k <= 32): the large
+                                  bins of the sampled plan are split into their digit regions batch
+                                  by batch while pass 1 runs (host-resident reads: under the input
+                                  copy).  0 (default): for host-resident reads; 1: always; 2: never.
+                                  Same output. */
 } kmc_options;
 
 /* Allocator hook: alloc(bytes, stream, ctx) -> device pointer or NULL; free(ptr, stream, ctx).

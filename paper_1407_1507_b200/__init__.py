@@ -37,7 +37,7 @@ class _Stats(ctypes.Structure):
         "n_below_min", "n_above_max", "n_out", "n_launches", "n_input_batches", "n_large_groups",
         "chunk_capacity", "n_overflow_chunks", "n_order_oversize", "max_signature_windows", "n_small_sorted",
         "n_cluster_items", "n_single_items", "n_spilled_keys", "cluster_size", "cluster_ctas",
-        "n_split_overflow", "n_kxmers", "kx_windows", "n_passes", "n_distribute_reruns")] + [
+        "n_split_overflow", "n_kxmers", "kx_windows", "n_passes", "n_distribute_reruns", "n_presplit_bins")] + [
         ("stage_ms", ctypes.c_float * len(STAGES)), ("stage_launches", ctypes.c_uint32 * len(STAGES))]
 
     def to_dict(self) -> dict:
@@ -55,7 +55,7 @@ class _Options(ctypes.Structure):
                 ("chunk_capacity", ctypes.c_uint32), ("non_canonical", ctypes.c_uint32),
                 ("plain_minimizers", ctypes.c_uint32), ("cluster_size", ctypes.c_uint32),
                 ("table_keys", ctypes.c_uint32), ("kx", ctypes.c_uint32), ("spill_keys", ctypes.c_uint32),
-                ("pass_mb", ctypes.c_uint32), ("split_tight", ctypes.c_uint32)]
+                ("pass_mb", ctypes.c_uint32), ("split_tight", ctypes.c_uint32), ("presplit", ctypes.c_uint32)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
@@ -182,8 +182,9 @@ class Result:
 
 def _options(profile, small_bin_capacity, force_large, large_path=0, distribute_path=0, input_batch_mb=0,
              large_group_mkeys=0, count_path=0, chunk_capacity=0, canonical=True, plain_minimizers=False,
-             cluster_size=0, table_keys=0, spill_keys=0, kx=0, split_tight=False, pass_mb=0):
+             cluster_size=0, table_keys=0, spill_keys=0, kx=0, split_tight=False, pass_mb=0, presplit=0):
     o = _Options()
+    o.presplit = int(presplit)
     o.pass_mb = int(pass_mb)
     o.split_tight = int(bool(split_tight))
     o.kx = int(kx)
@@ -209,7 +210,8 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
           large_path: int = 0, distribute_path: int = 0, input_batch_mb: int = 0, large_group_mkeys: int = 0,
           count_path: int = 0, chunk_capacity: int = 0, out_device: str | None = None,
           canonical: bool = True, plain_minimizers: bool = False, cluster_size: int = 0, table_keys: int = 0,
-          spill_keys: int = 0, kx: int = 0, split_tight: bool = False, pass_mb: int = 0) -> Result:
+          spill_keys: int = 0, kx: int = 0, split_tight: bool = False, pass_mb: int = 0,
+          presplit: int = 0) -> Result:
     """Count canonical k-mers (KMC 2 hot path on the GPU); canonical=False counts them as
     they occur in the reads (KMC's -b).
 
@@ -226,7 +228,7 @@ def count(reads, offsets, k: int, p: int, cutoff_min: int = 2, cutoff_max: int =
         raise ValueError("offsets must have n_reads + 1 entries")
     opt = _options(profile, small_bin_capacity, force_large, large_path, distribute_path, input_batch_mb,
                    large_group_mkeys, count_path, chunk_capacity, canonical, plain_minimizers, cluster_size,
-                   table_keys, spill_keys, kx, split_tight, pass_mb)
+                   table_keys, spill_keys, kx, split_tight, pass_mb, presplit)
     job = ctypes.c_void_p()
     n_out = ctypes.c_uint64()
     sh = _stream_handle(stream)

@@ -460,15 +460,20 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
             uint32_t s = INV;
             int v = 0, n = 0, nrec = 0;
             const uint32_t* pkb = PK;
+            uint4 dd = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
             if (idx < emit_end) {
                 if (idx < npend) {
                     v = (int)S.pv[idx];
                     s = S.ps[idx];
                     n = (int)S.pn[idx];
                     pkb = PKprev;
+                    if (MODE == P1_MODE_SCATTER && a.sig_dest) dd = a.sig_dest[s];
                 } else {
                     v = (int)list[idx - npend];
                     s = lsig[idx - npend];
+                    // the run's (bin, capacity, first slot) load is issued before the walk
+                    // over the end marks, which hides its L2 latency
+                    if (MODE == P1_MODE_SCATTER && a.sig_dest) dd = a.sig_dest[s];
                     n = run_windows(v);
                 }
                 nrec = (int)(((uint32_t)(n + maxw - 1) * maxw_magic) >> 20);  // exact: (n+maxw)*maxw < 2^20
@@ -504,7 +509,6 @@ __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
                 uint64_t bbase = 0;
                 if (MODE == P1_MODE_SCATTER) {
                     if (a.sig_dest) {  // (bin, capacity, first slot) in one load
-                        const uint4 dd = a.sig_dest[s];
                         bin = dd.x;
                         cap = dd.y;
                         bbase = ((uint64_t)dd.w << 32) | dd.z;

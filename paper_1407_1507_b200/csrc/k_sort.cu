@@ -1026,7 +1026,7 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             const uint32_t i = t + (u0 + u) * CH_NT;
-            if (i < ch.n) buf[u] = ld_stream(keys + ch.begin + i);
+            if (i < ch.n) buf[u] = ld_stream(keys + ch.begin + i + (i >= (ch.pad & 0xFFFFu) ? ch.pad >> 16 : 0u));
         }
     };
     uint32_t uniq = 0, below = 0, above = 0;

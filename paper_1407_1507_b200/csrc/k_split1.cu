@@ -43,23 +43,26 @@ constexpr size_t S1_OFF_STAGE = 0;
 constexpr size_t S1_OFF_RB = S1_OFF_STAGE + (size_t)S1_STAGE * 8;
 constexpr size_t S1_OFF_UMAP = S1_OFF_RB + 2 * (size_t)S1_RBW * 4;
 constexpr size_t S1_OFF_RINFO = S1_OFF_UMAP + (size_t)S1_UMAX * 2;
-constexpr size_t S1_OFF_DIG = S1_OFF_RINFO + (size_t)S1_REC * 4;  // h, gst, lof, lc, ovb: S1_DMAX each
+constexpr size_t S1_OFF_DIG = S1_OFF_RINFO + (size_t)S1_REC * 4;  // h, gst, lof, lc, ovb (+ lim): S1_DMAX each
 constexpr int S1_SOVF = 256;      // single-pass mode: keys beyond their digit's stage region
-constexpr size_t S1_OFF_SOVK = S1_OFF_DIG + 5 * (size_t)S1_DMAX * 4;
-constexpr size_t S1_OFF_SOVI = S1_OFF_SOVK + (size_t)S1_SOVF * 8;
-constexpr size_t S1_OFF_MBAR = S1_OFF_SOVI + (size_t)S1_SOVF * 4;
-constexpr size_t S1_SMEM = S1_OFF_MBAR + 16 + 16;
-static_assert(S1_OFF_RB % 16 == 0 && S1_OFF_MBAR % 8 == 0 && S1_OFF_SOVK % 8 == 0, "alignment");
-static_assert(2 * S1_SMEM + 2048 <= 228 * 1024, "two CTAs per SM");
+template <bool PAIRED> struct S1Lay {  // the paired layout keeps one more per-digit array (lim)
+    static constexpr size_t SOVK = S1_OFF_DIG + (PAIRED ? 6 : 5) * (size_t)S1_DMAX * 4;
+    static constexpr size_t SOVI = SOVK + (size_t)S1_SOVF * 8;
+    static constexpr size_t MBAR = SOVI + (size_t)S1_SOVF * 4;
+    static constexpr size_t SMEM = MBAR + 16 + 16;
+    static_assert(S1_OFF_RB % 16 == 0 && MBAR % 8 == 0 && SOVK % 8 == 0, "alignment");
+    static_assert(2 * SMEM + 2048 <= 228 * 1024, "two CTAs per SM");
+};
 static_assert(S1_DMAX <= 512, "digit in 9 bits of an overflow entry");
 static_assert(S1_DMAX <= S1_NT, "one thread per digit");
 
-template <bool CANON>
+template <bool CANON, bool PAIRED>
 __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict__ bins, const Piece* __restrict__ pieces,
                                                      uint64_t n_pieces, const S1Bin* __restrict__ sbins, int k,
                                                      int unit, uint32_t* __restrict__ cur, uint64_t* __restrict__ keys,
                                                      uint64_t* __restrict__ ovf, unsigned long long* __restrict__ ovf_ctr,
-                                                     uint64_t ovf_cap) {
+                                                     uint64_t ovf_cap, const unsigned long long* __restrict__ n_pieces_dev,
+                                                     uint32_t* __restrict__ fail) {
     extern __shared__ __align__(128) uint8_t sm[];
     uint64_t* stage = reinterpret_cast<uint64_t*>(sm + S1_OFF_STAGE);
     uint32_t* RB = reinterpret_cast<uint32_t*>(sm + S1_OFF_RB);
@@ -70,14 +73,16 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
     uint32_t* lof = gst + S1_DMAX; // run start in the stage
     uint32_t* lc = lof + S1_DMAX;  // stage cursor
     uint32_t* ovb = lc + S1_DMAX;  // first overflow slot of the digit's keys beyond the region
-    uint64_t* sovk = reinterpret_cast<uint64_t*>(sm + S1_OFF_SOVK);  // single pass: stage-overflow keys
-    uint32_t* sovi = reinterpret_cast<uint32_t*>(sm + S1_OFF_SOVI);  //   their digit | rank << 9
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + S1_OFF_MBAR);
+    uint32_t* lim = ovb + S1_DMAX; // paired: positions of the digit below lim are in its region (this piece)
+    uint64_t* sovk = reinterpret_cast<uint64_t*>(sm + S1Lay<PAIRED>::SOVK);  // single pass: stage-overflow keys
+    uint32_t* sovi = reinterpret_cast<uint32_t*>(sm + S1Lay<PAIRED>::SOVI);  //   their digit | rank << 9
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + S1Lay<PAIRED>::MBAR);
     __shared__ uint32_t wsumA[S1_NT / 32], wsumB[S1_NT / 32];  // alternating scan scratch
     __shared__ uint32_t novf;
     const int tid = threadIdx.x;
     const int U = unit;
     const uint32_t R = gridDim.x, r = blockIdx.x;
+    if (n_pieces_dev) n_pieces = *n_pieces_dev;
     const uint64_t p0 = (uint64_t)r * n_pieces / R, p1 = (uint64_t)(r + 1) * n_pieces / R;
     if (p0 >= p1) return;
     for (int d = tid; d < S1_DMAX; d += S1_NT) h[d] = 0;
@@ -154,15 +159,56 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
             }
         };
         uint64_t* region = keys + sb.key_base;
+        constexpr bool paired = PAIRED;  // (every bin of a paired launch has S1_PAIRED)
+        // slot of position i (< rc) of digit d in the bin's regions (paired layout: odd digits
+        // fill their pair's slots downwards), and the first slot of positions [g, g + m)
+        auto slot = [&](uint32_t d, uint32_t i) -> uint64_t {
+            return (paired && (d & 1u)) ? (uint64_t)(d + 1) * sb.rc - 1 - i : (uint64_t)d * sb.rc + i;
+        };
+        auto run_dst = [&](uint32_t d, uint32_t g, uint32_t m) -> uint64_t {
+            return (paired && (d & 1u)) ? (uint64_t)(d + 1) * sb.rc - g - m : (uint64_t)d * sb.rc + g;
+        };
         // place key at position i of digit d: its region, or the overflow list beyond it
         auto put = [&](uint32_t d, uint32_t i, uint64_t key) {
-            if (i < sb.rc) {
-                region[(uint64_t)d * sb.rc + i] = key;
+            if constexpr (PAIRED) {
+                if (i < lim[d]) {
+                    region[slot(d, i)] = key;
+                } else {
+                    const uint64_t o = (uint64_t)ovb[d] + (i - lim[d]);
+                    if (o < ovf_cap) ovf[o] = key;
+                }
             } else {
-                const uint32_t lo = gst[d] > sb.rc ? gst[d] : sb.rc;
-                const uint64_t o = (uint64_t)ovb[d] + (i - lo);
-                if (o < ovf_cap) ovf[o] = key;
+                if (i < sb.rc) {
+                    region[(uint64_t)d * sb.rc + i] = key;
+                } else {
+                    const uint32_t lo = gst[d] > sb.rc ? gst[d] : sb.rc;
+                    const uint64_t o = (uint64_t)ovb[d] + (i - lo);
+                    if (o < ovf_cap) ovf[o] = key;
+                }
             }
+        };
+        // reserve ce (even) positions for digit d's run of this piece: g = the first, returns how
+        // many lie in the region (the rest go to the overflow list).  The digits of a pair share
+        // its 2 rc slots through one 64-bit counter (the even digit in the low word): a run fits
+        // while the two digits' counts stay within them; the first position of a digit that did
+        // not fit is recorded (fail) for the chunk listing.
+        auto reserve = [&](uint32_t d, uint32_t ce, uint32_t& g) -> uint32_t {
+            uint32_t ra;
+            if constexpr (PAIRED) {
+                const uint32_t hi = d & 1u;
+                const unsigned long long old = atomicAdd(
+                    reinterpret_cast<unsigned long long*>(cur + sb.dbase + (d & ~1u)), (unsigned long long)ce << (32 * hi));
+                g = (uint32_t)(old >> (32 * hi));
+                const uint32_t pn = (uint32_t)(old >> (32 * (hi ^ 1u)));
+                const uint32_t L = 2 * sb.rc > pn ? 2 * sb.rc - pn : 0u;
+                ra = g >= L ? 0u : min(ce, L - g);
+                if (ra < ce) atomicMin(&fail[sb.dbase + d], g + ra);
+            } else {
+                g = atomicAdd(&cur[sb.dbase + d], ce);
+                ra = g >= sb.rc ? 0u : min(ce, sb.rc - g);
+            }
+            if (ra < ce) ovb[d] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(ce - ra));
+            return ra;
         };
         // ---- single pass (pieces whose windows fill at most 4/5 of the stage): every key is
         //      expanded once and placed at its rank in its digit's share of the stage (keys
@@ -191,13 +237,10 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
             if (nov <= (uint32_t)S1_SOVF) {
                 if ((uint32_t)tid < nd) {
                     const uint32_t c = lc[tid], ce = c + (c & 1u);
-                    uint32_t g = 0;
-                    if (c) g = atomicAdd(&cur[sb.dbase + tid], ce);
-                    if (c && g + ce > sb.rc) {
-                        const uint32_t lo = g > sb.rc ? g : sb.rc;
-                        ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + ce - lo));
-                    }
+                    uint32_t g = 0, ra = 0;
+                    if (c) ra = reserve(tid, ce, g);
                     gst[tid] = g;
+                    if constexpr (PAIRED) lim[tid] = g + ra;
                     lof[tid] = c;
                     if (c) {
                         // the stage part (+ the pad slot when the run ends inside it), even-sized
@@ -206,9 +249,9 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
                             stage[tid * C1 + c] = ~0ull;
                             fence_proxy_async_smem();
                         }
-                        const uint32_t in_reg = g >= sb.rc ? 0u : min(sn, sb.rc - g);  // even: g, rc even
+                        const uint32_t in_reg = min(sn, ra);  // even: g, rc, ra even
                         if (in_reg) {
-                            tma_store_1d(region + (uint64_t)tid * sb.rc + g, stage + tid * C1, in_reg * 8u);
+                            tma_store_1d(region + run_dst(tid, g, in_reg), stage + tid * C1, in_reg * 8u);
                             bulk_commit();
                             bulk_pending = true;
                         }
@@ -234,21 +277,18 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         __syncthreads();
         // ---- R: one reservation per digit in its region (+ overflow beyond it); stage offsets
         // (the reservation's round trip overlaps the stage-offset scan, which needs only c)
-        uint32_t c = 0, g = 0;
+        uint32_t c = 0, g = 0, ra = 0;
         if ((uint32_t)tid < nd) {
             c = h[tid];
             h[tid] = 0;  // ready for the next piece
-            if (c) g = atomicAdd(&cur[sb.dbase + tid], c + (c & 1u));  // even: see the single pass
+            if (c) ra = reserve(tid, c + (c & 1u), g);  // even: see the single pass
         }
         uint32_t npk;
         const uint32_t cp = (uint32_t)tid < nd ? c + 1 : 0u;  // one spare slot per digit (parity)
         const uint32_t P = block_excl_sum1<S1_NT, uint32_t>(cp, wsumB, &npk);
         if ((uint32_t)tid < nd) {
-            if (c && g + c + (c & 1u) > sb.rc) {
-                const uint32_t lo = g > sb.rc ? g : sb.rc;
-                ovb[tid] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(g + c + (c & 1u) - lo));
-            }
             gst[tid] = g;
+            if constexpr (PAIRED) lim[tid] = g + ra;
             lof[tid] = lc[tid] = P + ((P ^ g) & 1u);
         }
         __syncthreads();
@@ -261,22 +301,19 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
                 if (staged) {
                     stage[q] = key;
                 } else {
-                    const uint32_t i = gst[d] + (q - lof[d]);
-                    if (i < sb.rc) {
-                        region[(uint64_t)d * sb.rc + i] = key;
-                    } else {
-                        const uint32_t lo = gst[d] > sb.rc ? gst[d] : sb.rc;
-                        const uint64_t o = (uint64_t)ovb[d] + (i - lo);
-                        if (o < ovf_cap) ovf[o] = key;
-                    }
+                    put(d, gst[d] + (q - lof[d]), key);
                 }
             });
         if (staged) fence_proxy_async_smem();  // stage writes -> the bulk copies
         __syncthreads();
         // ---- W: every digit's run leaves by one bulk copy (+ <= 2 single stores, + overflow)
-        if (staged && (uint32_t)tid < nd) {
+        if (staged && (uint32_t)tid < nd && paired && (tid & 1)) {
+            // (a downward run: single stores; the two-pass mode is rare)
             const uint32_t s0 = lof[tid], cn = lc[tid] - s0, g0 = gst[tid];
-            const uint32_t in_reg = g0 >= sb.rc ? 0u : min(cn, sb.rc - g0);
+            for (uint32_t e = 0; e < cn; ++e) put(tid, g0 + e, stage[s0 + e]);
+        } else if (staged && (uint32_t)tid < nd) {
+            const uint32_t s0 = lof[tid], cn = lc[tid] - s0, g0 = gst[tid];
+            const uint32_t in_reg = PAIRED ? min(cn, lim[tid] - g0) : (g0 >= sb.rc ? 0u : min(cn, sb.rc - g0));
             uint64_t* dst = region + (uint64_t)tid * sb.rc + g0;
             uint32_t i = 0;
             if (in_reg && (s0 & 1u)) {
@@ -305,8 +342,38 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
 // for the fallback (its other keys are in the overflow list).  One CTA per bin.
 __global__ void k_split1_chunks(const S1Bin* __restrict__ sbins, const uint32_t* __restrict__ cur, uint32_t hard_cap,
                                 Chunk* __restrict__ chunks, Chunk* __restrict__ over, Chunk* __restrict__ ovd,
-                                unsigned long long* __restrict__ ctr) {
+                                unsigned long long* __restrict__ ctr, uint32_t pair_cap,
+                                const uint32_t* __restrict__ fail) {
     const S1Bin sb = sbins[blockIdx.x];
+    if (sb.flags & S1_PAIRED) {
+        // pair e: slots [key_base + 2e rc, + 2 rc), digit 2e from the start, 2e + 1 from the end
+        const uint64_t rc2 = 2ull * sb.rc;
+        for (uint32_t e = threadIdx.x; 2 * e < sb.nd; e += blockDim.x) {
+            const uint32_t n0 = cur[sb.dbase + 2 * e], n1 = cur[sb.dbase + 2 * e + 1];
+            const uint64_t pb = sb.key_base + 2 * e * (uint64_t)sb.rc;
+            if ((uint64_t)n0 + n1 > rc2) {
+                // the pair overflowed: the region parts below each digit's first position that
+                // did not fit (its other keys are in the overflow list) go to the fallback
+                const uint32_t a = min(n0, fail[sb.dbase + 2 * e]), b = min(n1, fail[sb.dbase + 2 * e + 1]);
+                if (a) ovd[atomicAdd(&ctr[2], 1ull)] = Chunk{pb, a, 0};
+                if (b) ovd[atomicAdd(&ctr[2], 1ull)] = Chunk{pb + rc2 - b, b, 0};
+                continue;
+            }
+            const uint64_t gap = rc2 - n0 - n1;
+            if (n0 + n1 <= pair_cap && n0 + n1 <= hard_cap && n0 < 65536u && gap < 65536u) {
+                if (n0 + n1) chunks[atomicAdd(&ctr[0], 1ull)] = Chunk{pb, n0 + n1, n0 | (uint32_t)gap << 16};
+                continue;
+            }
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t n = h ? n1 : n0;
+                if (n == 0) continue;
+                const Chunk ch{h ? pb + rc2 - n : pb, n, 0};
+                if (n > hard_cap) over[atomicAdd(&ctr[1], 1ull)] = ch;
+                else chunks[atomicAdd(&ctr[0], 1ull)] = ch;
+            }
+        }
+        return;
+    }
     for (uint32_t d = threadIdx.x; d < sb.nd; d += blockDim.x) {
         const uint32_t n = cur[sb.dbase + d];
         if (n == 0) continue;
@@ -315,6 +382,42 @@ __global__ void k_split1_chunks(const S1Bin* __restrict__ sbins, const uint32_t*
         else if (n > hard_cap) over[atomicAdd(&ctr[1], 1ull)] = Chunk{base, n, 0};
         else chunks[atomicAdd(&ctr[0], 1ull)] = Chunk{base, n, 0};
     }
+}
+
+// Pieces of the records appended to the presplit bins since the last call (one CTA).
+constexpr int PP_NT = 1024;
+__global__ void __launch_bounds__(PP_NT) k_presplit_pieces(const uint32_t* __restrict__ bin_ids, uint32_t n_pb,
+                                                           const uint32_t* __restrict__ bin_fill,
+                                                           const uint32_t* __restrict__ bin_cap,
+                                                           const uint64_t* __restrict__ bin_rec_off,
+                                                           uint32_t* __restrict__ done, uint32_t rpp,
+                                                           Piece* __restrict__ pieces,
+                                                           unsigned long long* __restrict__ n_pieces) {
+    __shared__ uint32_t wsum[PP_NT / 32];
+    uint64_t base = 0;
+    for (uint32_t i0 = 0; i0 < n_pb; i0 += PP_NT) {
+        const uint32_t i = i0 + threadIdx.x;
+        uint32_t d0 = 0, f = 0, np = 0, b = 0;
+        if (i < n_pb) {
+            b = bin_ids[i];
+            f = min(bin_fill[b], bin_cap[b]);  // (a fill beyond the capacity: the call replans)
+            d0 = done[i];
+            np = f > d0 ? (f - d0 + rpp - 1) / rpp : 0u;
+        }
+        uint32_t tot;
+        const uint32_t pre = block_excl_sum1<PP_NT, uint32_t>(np, wsum, &tot);
+        if (np) {
+            const uint64_t ro = bin_rec_off[b];
+            for (uint32_t q = 0; q < np; ++q) {
+                const uint32_t r0 = d0 + q * rpp;
+                pieces[base + pre + q] = Piece{ro + r0, min(rpp, f - r0), i};
+            }
+            done[i] = f;
+        }
+        base += tot;
+        __syncthreads();  // (wsum is reused)
+    }
+    if (threadIdx.x == 0) *n_pieces = base;
 }
 
 }  // namespace
@@ -327,30 +430,44 @@ int split1_piece_records(int k) {
 
 cudaError_t launch_split1(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const S1Bin* sbins, int k,
                           int canonical, uint32_t* cur, uint64_t* keys, uint64_t* ovf, unsigned long long* ovf_ctr,
-                          uint64_t ovf_cap, int n_ctas, cudaStream_t s) {
-    if (n_pieces == 0) return cudaSuccess;
+                          uint64_t ovf_cap, int n_ctas, cudaStream_t s, const unsigned long long* n_pieces_dev,
+                          uint32_t* fail, bool paired) {
+    if (n_pieces == 0 && !n_pieces_dev) return cudaSuccess;
     if (k > 32) return cudaErrorInvalidValue;
     const int unit = std::min(S1_UNIT, 33 - k);
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(n_pieces, (uint64_t)n_ctas));
+    const unsigned grid =
+        n_pieces_dev ? (unsigned)n_ctas : (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(n_pieces, (uint64_t)n_ctas));
+    auto go = [&](auto kern, size_t smem) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e) return e;
+        kern<<<grid, S1_NT, smem, s>>>(bins, pieces, n_pieces, sbins, k, unit, cur, keys, ovf, ovf_ctr, ovf_cap,
+                                      n_pieces_dev, fail);
+        return cudaSuccess;
+    };
     cudaError_t e;
-    if (canonical) {
-        if ((e = cudaFuncSetAttribute(k_split1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S1_SMEM)))
-            return e;
-        k_split1<true><<<grid, S1_NT, S1_SMEM, s>>>(bins, pieces, n_pieces, sbins, k, unit, cur, keys, ovf, ovf_ctr,
-                                                    ovf_cap);
+    if (paired) {
+        if (!fail) return cudaErrorInvalidValue;
+        e = canonical ? go(k_split1<true, true>, S1Lay<true>::SMEM) : go(k_split1<false, true>, S1Lay<true>::SMEM);
     } else {
-        if ((e = cudaFuncSetAttribute(k_split1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S1_SMEM)))
-            return e;
-        k_split1<false><<<grid, S1_NT, S1_SMEM, s>>>(bins, pieces, n_pieces, sbins, k, unit, cur, keys, ovf, ovf_ctr,
-                                                     ovf_cap);
+        e = canonical ? go(k_split1<true, false>, S1Lay<false>::SMEM) : go(k_split1<false, false>, S1Lay<false>::SMEM);
     }
+    if (e) return e;
     return cudaGetLastError();
 }
 
 cudaError_t launch_split1_chunks(const S1Bin* sbins, uint64_t n_bins, const uint32_t* cur, uint32_t hard_cap,
-                                 Chunk* chunks, Chunk* over, Chunk* ovd, unsigned long long* ctr, cudaStream_t s) {
+                                 Chunk* chunks, Chunk* over, Chunk* ovd, unsigned long long* ctr, cudaStream_t s,
+                                 uint32_t pair_cap, const uint32_t* fail) {
     if (n_bins == 0) return cudaSuccess;
-    k_split1_chunks<<<(unsigned)n_bins, 256, 0, s>>>(sbins, cur, hard_cap, chunks, over, ovd, ctr);
+    k_split1_chunks<<<(unsigned)n_bins, 256, 0, s>>>(sbins, cur, hard_cap, chunks, over, ovd, ctr, pair_cap, fail);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_presplit_pieces(const uint32_t* bin_ids, uint32_t n_pb, const uint32_t* bin_fill,
+                                   const uint32_t* bin_cap, const uint64_t* bin_rec_off, uint32_t* done, uint32_t rpp,
+                                   Piece* pieces, unsigned long long* n_pieces, cudaStream_t s) {
+    if (rpp == 0) return cudaErrorInvalidValue;
+    k_presplit_pieces<<<1, PP_NT, 0, s>>>(bin_ids, n_pb, bin_fill, bin_cap, bin_rec_off, done, rpp, pieces, n_pieces);
     return cudaGetLastError();
 }
 

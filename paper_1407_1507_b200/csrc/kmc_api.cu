@@ -275,6 +275,31 @@ constexpr uint32_t SAMPLE_MIN_MBASES = 64;
 // going while the device is busy with another call's counting stages
 constexpr int IN_SLOTS = 8;
 
+// Large bins of the sampled plan split into their digit regions batch by batch while pass 1
+// writes their records (k_split1 on the records appended since the previous batch), so that
+// with host-resident reads the split runs under the input copy (kmc_options.presplit).
+struct PreSplit {
+    bool active = false;
+    std::vector<uint64_t> ids;  // bin ids
+    std::vector<S1Bin> sb;      // their split tables (paired layout)
+    std::vector<int32_t> index; // bin id -> index in ids (-1: not presplit)
+    uint32_t* d_ids = nullptr;
+    S1Bin* d_sbins = nullptr;
+    uint32_t* done = nullptr;   // records already split, per presplit bin
+    uint32_t* cur = nullptr;    // per (bin, digit) key counts
+    uint32_t* fail = nullptr;   // per (bin, digit) first position beyond the pair's slots
+    uint64_t* keys = nullptr;   // the digit regions
+    uint64_t* ovf = nullptr;    // keys beyond their region
+    uint64_t ovf_cap = 0;
+    unsigned long long* ctr = nullptr;  // [3] overflow keys, [5] pieces of the last batch
+    Piece* pieces = nullptr;
+    uint64_t n_digits = 0;
+    const uint32_t* bin_fill = nullptr;
+    const uint32_t* bin_cap = nullptr;
+    const uint64_t* bin_rec_off = nullptr;
+    uint32_t rpp = 0;
+};
+
 struct PlanCtx {
     PlanArgs pa{};
     uint64_t ns = 0, n_bins = 0, n_windows = 0, n_records = 0;
@@ -295,6 +320,7 @@ struct PlanCtx {
     std::vector<uint32_t> owner;
     bool multipass = false;  // host reads beyond HBM: passes over ranges of bins (f2)
     uint32_t* bins_ready = nullptr;  // sampled distribution: pass 1 wrote the records into their bins
+    PreSplit pre;
 };
 
 struct kmc_job {
@@ -423,6 +449,10 @@ void count_phase(kmc_job* j, PlanCtx& c);
 void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t b_hi);
 void count_multipass(kmc_job* j, PlanCtx& c);
 void release_plan_scratch(kmc_job* j, PlanCtx& c);
+void presplit_setup(kmc_job* j, PlanCtx& c, const std::vector<uint64_t>& bw, const std::vector<uint64_t>& bn,
+                    const uint32_t* bin_cap, const uint32_t* bin_fill, uint64_t total_cap);
+int presplit_batch(kmc_job* j, PlanCtx& c, const uint32_t* bins);
+void presplit_release(kmc_job* j, PreSplit& pre);
 
 void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64_t n_reads) {
     const int k = j->k, p = j->p, kw = j->key_words;
@@ -588,6 +618,8 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         CK(cudaEventRecord(j->ev_copy[t], j->cs));
         slot_batch[t] = (int64_t)b;
     };
+    // after every pass-1 launch of a scatter pass (the presplit of the new records)
+    std::function<int()> p1_hook;
     // max_batches: stop after that many batches (the sample pass: the first one)
     auto run_p1 = [&](int mode, size_t max_batches = ~(size_t)0) -> int {
         if (!host_reads) {
@@ -598,6 +630,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
                 ++nl;
             }
             CK(launch_p1(mode, a, n_tiles, s));
+            if (mode == P1_MODE_SCATTER && p1_hook) nl += p1_hook();
             return nl;
         }
         if (!keep_slots)
@@ -625,6 +658,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             CK(launch_p1(mode, ab, nt, s));
             CK(cudaEventRecord(j->ev_done[t], s));
             nl += 2;
+            if (mode == P1_MODE_SCATTER && p1_hook) nl += p1_hook();  // (after the slot is released)
             // the batch NS ahead takes this slot once this batch's pass 1 is done
             if (b + NS < lim) copy_batch(b + NS);
         }
@@ -679,6 +713,16 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         unsigned long long* hs = j->host_small;
         CK(cudaMemcpyAsync(&hs[3], cap_scan + n_bins, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(pa.bin_rec_off, cap_scan, n_bins * 8, cudaMemcpyDeviceToDevice, s));
+        // presplit: the estimated per-bin windows and records pick its bins
+        const bool presplit = j->opt.presplit != 2 && (j->opt.presplit == 1 || host_reads) && kw == 1 && k <= 32 &&
+                              j->opt.large_path == 0 && j->opt.count_path != 1;
+        std::vector<uint64_t> bw_est, bn_est;
+        if (presplit) {
+            bw_est.resize(n_bins);
+            bn_est.resize(n_bins);
+            CK(cudaMemcpyAsync(bw_est.data(), pa.bin_w, n_bins * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(bn_est.data(), pa.bin_nrec, n_bins * 8, cudaMemcpyDeviceToHost, s));
+        }
         CK(cudaStreamSynchronize(s));
         const uint64_t total_cap = hs[3];
         uint32_t* bins = reinterpret_cast<uint32_t*>(ar.alloc(total_cap * RWs * 4));
@@ -698,7 +742,12 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         a.sig_dest = sig_dest;
         a.scatter_hist = 1;
         keep_slots = true;  // batch 0 is still in its slot
+        if (presplit) {
+            presplit_setup(j, c, bw_est, bn_est, bin_cap, bin_fill, total_cap);
+            if (c.pre.active) p1_hook = [&]() { return presplit_batch(j, c, bins); };
+        }
         int nl = run_p1(P1_MODE_SCATTER);
+        p1_hook = nullptr;
         a.sig_dest = nullptr;
         htrace("scatter pass enqueued");
         CK(cudaMemcpyAsync(&hs[4], gstats + GS_P1_OVF, 8, cudaMemcpyDeviceToHost, s));
@@ -740,6 +789,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             //      pass: the scatter pass counts windows only), the exact plan, and the
             //      scatter again with exact offsets
             j->st.n_distribute_reruns += 1;
+            presplit_release(j, c.pre);
             ar.release(bins);
             j->stage_begin(KMC_STAGE_SIGNATURE);
             CK(cudaMemsetAsync(hist_w, 0, ns * 8, s));
@@ -889,6 +939,90 @@ void fetch_tables(kmc_job* j, PlanCtx& c) {
     htrace("tables fetched");
 }
 
+// ---- presplit (kmc_options.presplit): the large bins of the sampled plan -- estimated cost
+//      above twice the small-bin capacity -- get their digit regions before pass 1 writes the
+//      records (paired layout, digits of about 3/4 of a hash table each: a pair is one chunk
+//      when the measured distinct ratio lets it fit the table), and every batch's new records
+//      of those bins are split right after the batch's pass 1.
+void presplit_setup(kmc_job* j, PlanCtx& c, const std::vector<uint64_t>& bw, const std::vector<uint64_t>& bn,
+                    const uint32_t* bin_cap, const uint32_t* bin_fill, uint64_t total_cap) {
+    PreSplit& pre = c.pre;
+    Arena& ar = j->arena;
+    cudaStream_t s = j->s;
+    const int k = j->k;
+    const uint64_t lim = 2ull * (uint64_t)c.cap;
+    const double kf = (double)chunk_hash_cap(k) * 3 / 4;
+    pre.ids.clear();
+    pre.sb.clear();
+    uint64_t key_base = 0, dbase = 0;
+    for (uint64_t b = 0; b < c.n_bins; ++b) {
+        const uint64_t cost = std::max<uint64_t>(bw[b], bn[b] * c.pa.recw);
+        if (cost <= lim) continue;
+        uint64_t d = 2 * (uint64_t)std::ceil((double)bw[b] / (2 * kf));
+        d = std::min<uint64_t>(std::max<uint64_t>(d, 2), (uint64_t)S1_DMAX);
+        uint64_t r = (uint64_t)std::ceil((double)bw[b] / (double)d * 1.25) + 256;
+        r = std::min<uint64_t>((r + 1) & ~1ull, 0x7FFFFFFEull);
+        pre.ids.push_back(b);
+        pre.sb.push_back(S1Bin{key_base, (uint32_t)d, (uint32_t)r, (uint32_t)dbase, S1_PAIRED});
+        key_base += d * r;
+        dbase += d;
+    }
+    if (pre.ids.empty() || pre.ids.size() >= (1ull << 31)) return;
+    pre.keys = reinterpret_cast<uint64_t*>(ar.try_alloc(key_base * 8 + chunk_key_slack_bytes()));
+    if (!pre.keys) {  // no room next to the bins: the split after pass 1
+        pre.ids.clear();
+        pre.sb.clear();
+        return;
+    }
+    const size_t n = pre.ids.size();
+    pre.n_digits = dbase;
+    pre.index.assign(c.n_bins, -1);
+    std::vector<uint32_t> ids32(n);
+    for (size_t i = 0; i < n; ++i) {
+        pre.index[pre.ids[i]] = (int32_t)i;
+        ids32[i] = (uint32_t)pre.ids[i];
+    }
+    pre.rpp = (uint32_t)split1_piece_records(k);
+    pre.d_ids = ar.get<uint32_t>(n);
+    pre.d_sbins = ar.get<S1Bin>(n);
+    pre.done = ar.get<uint32_t>(n);
+    pre.cur = ar.get<uint32_t>(dbase);
+    pre.fail = ar.get<uint32_t>(dbase);
+    pre.ovf_cap = std::max<uint64_t>(1u << 20, key_base / 32);
+    pre.ovf = ar.get<uint64_t>(pre.ovf_cap);
+    pre.ctr = ar.get<unsigned long long>(8);
+    pre.pieces = ar.get<Piece>(total_cap / pre.rpp + 2 * n + 1);  // >= the pieces of any batch
+    // (pageable sources: the copies are staged before the calls return)
+    CK(cudaMemcpyAsync(pre.d_ids, ids32.data(), n * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(pre.d_sbins, pre.sb.data(), n * sizeof(S1Bin), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(pre.done, 0, n * 4, s));
+    CK(cudaMemsetAsync(pre.cur, 0, dbase * 4, s));
+    CK(cudaMemsetAsync(pre.fail, 0xFF, dbase * 4, s));
+    CK(cudaMemsetAsync(pre.ctr, 0, 64, s));
+    pre.bin_fill = bin_fill;
+    pre.bin_cap = bin_cap;
+    pre.bin_rec_off = c.pa.bin_rec_off;
+    pre.active = true;
+}
+
+int presplit_batch(kmc_job* j, PlanCtx& c, const uint32_t* bins) {
+    PreSplit& pre = c.pre;
+    cudaStream_t s = j->s;
+    CK(launch_presplit_pieces(pre.d_ids, (uint32_t)pre.ids.size(), pre.bin_fill, pre.bin_cap, pre.bin_rec_off,
+                              pre.done, pre.rpp, pre.pieces, pre.ctr + 5, s));
+    CK(launch_split1(bins, pre.pieces, 0, pre.d_sbins, j->k, !j->opt.non_canonical, pre.cur, pre.keys, pre.ovf,
+                     pre.ctr + 3, pre.ovf_cap, 2 * n_sms(), s, pre.ctr + 5, pre.fail, true));
+    return 2;
+}
+
+void presplit_release(kmc_job* j, PreSplit& pre) {
+    Arena& ar = j->arena;
+    for (void* q : {(void*)pre.keys, (void*)pre.d_ids, (void*)pre.d_sbins, (void*)pre.done, (void*)pre.cur,
+                    (void*)pre.fail, (void*)pre.ovf, (void*)pre.ctr, (void*)pre.pieces})
+        ar.release(q);
+    pre = PreSplit{};
+}
+
 // Large bins of the default path for k <= 32 (k_split1.cu): one sized split pass puts every
 // key of a bin into the region of its hashed digit (a bin of W windows: nd ~ W / (0.8 kcap)
 // digits of rc ~ 1.05 W / nd slots), then every digit that fits its region is one chunk of the
@@ -900,6 +1034,20 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
                   DR&& distinct_ratio) {
     htrace("large_split1");
     (void)distinct_ratio;
+    PreSplit& pre = c.pre;
+    // presplit bins that the exact plan made large are counted from their regions; the
+    // others take the split below
+    std::vector<uint64_t> rest_ids;
+    std::vector<uint8_t> pre_used;
+    if (pre.active) {
+        pre_used.assign(pre.ids.size(), 0);
+        for (const uint64_t b : large_ids) {
+            const int32_t x = pre.index[b];
+            if (x >= 0) pre_used[(size_t)x] = 1;
+            else rest_ids.push_back(b);
+        }
+    }
+    const std::vector<uint64_t>& ids = pre.active ? rest_ids : large_ids;
     const int k = j->k;
     Arena& ar = j->arena;
     cudaStream_t s = j->s;
@@ -914,11 +1062,143 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
     // overflow 6.0 M .. 0.4 M keys; bigger digits absorb pile-ups and need fewer reservations.
     const double target = std::max(1.0, (double)kcap);
     const uint32_t rpp = (uint32_t)split1_piece_records(k);
-    const size_t nl = large_ids.size();
+    RadixScratch rs{};
+    uint64_t rs_cap = 0;
+    auto sort_rle = [&](uint64_t* keys, uint64_t n, int& nlaunch) {
+        if (n == 0) return;
+        if (n > rs_cap) {
+            ar.release(rs.keys_alt);
+            ar.release(rs.tile_hist);
+            ar.release(rs.tile_off);
+            ar.release(rs.scan_temp);
+            rs.keys_alt = ar.alloc(n * 8);
+            rs.tile_hist = ar.get<uint32_t>(radix_status_words(n, 1));
+            rs.tile_off = ar.get<uint32_t>(radix_aux_words());
+            rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n, 1));
+            if (!rs.red) rs.red = ar.get<unsigned long long>(4);
+            rs.red_host = hs + 40;
+            rs_cap = n;
+        }
+        void* sorted = nullptr;
+        uint32_t* dummy = nullptr;
+        CK(device_radix_sort(1, keys, nullptr, n, 2 * k, rs, s, &sorted, &dummy, &nlaunch));
+        CK(launch_rle(1, sorted, n, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
+        nlaunch += 1;
+    };
+    // S7-S8 of a split group: its chunks by the SMEM hash count; overflowed digits (region
+    // parts + the overflow list) and chunks that overflowed the table by the device radix sort
+    auto count_group = [&](uint64_t* lkeys, uint64_t* ovf, uint64_t ovf_cap, Chunk* chunks, Chunk* over, Chunk* ovd,
+                           Chunk* tovf, unsigned long long* ctr, uint64_t n_chunks, uint64_t n_over, uint64_t n_ovd,
+                           uint64_t n_ovk) {
+        j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
+        CK(launch_chunk_hash(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, tovf,
+                             ctr + 4, n_sms(), s));
+        j->launches += 1;
+        j->stage_end(1);
+        CK(cudaMemcpyAsync(&hs[52], ctr + 4, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t n_tovf = hs[52];
+        htrace("chunk_hash done");
+        j->st.n_overflow_chunks += n_tovf;
+        if (n_over + n_ovd + n_ovk + n_tovf == 0) return;
+        int fl = 0;
+        j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
+        if (n_ovd + n_ovk > 0) {
+            // overflowed digits: their region parts join their excess keys in the overflow list
+            std::vector<Chunk> od(n_ovd);
+            if (n_ovd) {
+                CK(cudaMemcpyAsync(od.data(), ovd, n_ovd * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+            }
+            uint64_t need = n_ovk;
+            for (const Chunk& x : od) need += x.n;
+            j->st.n_split_overflow += need;
+            uint64_t* all = ovf;
+            if (need > ovf_cap) {
+                all = ar.get<uint64_t>(need);
+                if (n_ovk) CK(cudaMemcpyAsync(all, ovf, n_ovk * 8, cudaMemcpyDeviceToDevice, s));
+            }
+            uint64_t o = n_ovk;
+            for (const Chunk& x : od) {
+                CK(cudaMemcpyAsync(all + o, lkeys + x.begin, (size_t)x.n * 8, cudaMemcpyDeviceToDevice, s));
+                o += x.n;
+            }
+            sort_rle(all, need, fl);
+            if (all != ovf) ar.release(all);
+        }
+        if (n_over + n_tovf > 0) {
+            std::vector<Chunk> ov(n_over + n_tovf);
+            if (n_over) CK(cudaMemcpyAsync(ov.data(), over, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+            if (n_tovf)
+                CK(cudaMemcpyAsync(ov.data() + n_over, tovf, n_tovf * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (const Chunk& x : ov) {
+                if (x.pad) {  // a pair of digits: two segments (disjoint keys)
+                    const uint32_t n0 = x.pad & 0xFFFFu, gap = x.pad >> 16;
+                    sort_rle(lkeys + x.begin, n0, fl);
+                    sort_rle(lkeys + x.begin + n0 + gap, x.n - n0, fl);
+                } else {
+                    sort_rle(lkeys + x.begin, x.n, fl);
+                }
+            }
+        }
+        j->launches += fl;
+        j->stage_end(fl);
+        htrace("fallback enqueued");
+    };
+    // ---- the presplit group: its regions are filled; list the chunks (a pair of digits that
+    //      fits the table together is one chunk) and count them
+    if (pre.active) {
+        size_t used = 0;
+        for (uint8_t u : pre_used) used += u;
+        if (used) {
+            const size_t n = pre.ids.size();
+            std::vector<S1Bin> sbl = pre.sb;
+            for (size_t i = 0; i < n; ++i)
+                if (!pre_used[i]) sbl[i].nd = 0;  // small after all: counted from its records
+            CK(cudaMemcpyAsync(pre.d_sbins, sbl.data(), n * sizeof(S1Bin), cudaMemcpyHostToDevice, s));
+            const uint64_t nd_all = std::max<uint64_t>(pre.n_digits, 1);
+            Chunk* pch = ar.get<Chunk>(nd_all);
+            Chunk* pov = ar.get<Chunk>(nd_all);
+            Chunk* povd = ar.get<Chunk>(nd_all);
+            Chunk* ptovf = ar.get<Chunk>(nd_all);
+            j->stage_begin(KMC_STAGE_LARGE_SCATTER);
+            CK(launch_split1_chunks(pre.d_sbins, n, pre.cur, 0xFFFFFFFFu, pch, pov, povd, pre.ctr, s, (uint32_t)kcap,
+                                    pre.fail));
+            j->launches += 1;
+            j->stage_end(1);
+            CK(cudaMemcpyAsync(&hs[48], pre.ctr, 32, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (hs[51] <= pre.ovf_cap) {
+                j->st.n_presplit_bins += used;
+                j->st.n_large_groups += 1;
+                count_group(pre.keys, pre.ovf, pre.ovf_cap, pch, pov, povd, ptovf, pre.ctr, hs[48], hs[49], hs[50],
+                            hs[51]);
+            } else {
+                // the overflow list overflowed during the presplit: split these bins again
+                for (size_t i = 0; i < n; ++i)
+                    if (pre_used[i]) rest_ids.push_back(pre.ids[i]);
+                std::sort(rest_ids.begin(), rest_ids.end());
+            }
+            ar.release(pch);
+            ar.release(pov);
+            ar.release(povd);
+            ar.release(ptovf);
+        }
+        presplit_release(j, pre);
+    }
+    if (ids.empty()) {
+        ar.release(rs.keys_alt);
+        ar.release(rs.tile_hist);
+        ar.release(rs.tile_off);
+        ar.release(rs.scan_temp);
+        return;
+    }
+    const size_t nl = ids.size();
     std::vector<uint32_t> nd(nl), rc(nl);
     uint64_t total = 0;
     for (size_t i = 0; i < nl; ++i) {
-        const uint64_t b = large_ids[i];
+        const uint64_t b = ids[i];
         uint64_t d = (uint64_t)std::ceil((double)bw[b] / target);
         d = std::min<uint64_t>(std::max<uint64_t>(d, 1), (uint64_t)S1_DMAX);
         uint64_t r = j->opt.split_tight ? (bw[b] + d - 1) / d + 2
@@ -950,7 +1230,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             if (i1 > i0 && gk + need > budget) break;
             gk += need;
             gd += nd[i1];
-            gp += (bn[large_ids[i1]] + rpp - 1) / rpp;
+            gp += (bn[ids[i1]] + rpp - 1) / rpp;
             ++i1;
         }
         groups.push_back({i0, i1});
@@ -974,29 +1254,6 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
     if (!lkeys) lkeys = ar.alloc(max_gk * 8 + chunk_key_slack_bytes());
     uint64_t ovf_cap = std::max<uint64_t>(1u << 20, max_gk / 32);
     uint64_t* ovf = ar.get<uint64_t>(ovf_cap);
-    RadixScratch rs{};
-    uint64_t rs_cap = 0;
-    auto sort_rle = [&](uint64_t* keys, uint64_t n, int& nlaunch) {
-        if (n == 0) return;
-        if (n > rs_cap) {
-            ar.release(rs.keys_alt);
-            ar.release(rs.tile_hist);
-            ar.release(rs.tile_off);
-            ar.release(rs.scan_temp);
-            rs.keys_alt = ar.alloc(n * 8);
-            rs.tile_hist = ar.get<uint32_t>(radix_status_words(n, 1));
-            rs.tile_off = ar.get<uint32_t>(radix_aux_words());
-            rs.scan_temp = ar.alloc(radix_scan_temp_bytes(n, 1));
-            if (!rs.red) rs.red = ar.get<unsigned long long>(4);
-            rs.red_host = hs + 40;
-            rs_cap = n;
-        }
-        void* sorted = nullptr;
-        uint32_t* dummy = nullptr;
-        CK(device_radix_sort(1, keys, nullptr, n, 2 * k, rs, s, &sorted, &dummy, &nlaunch));
-        CK(launch_rle(1, sorted, n, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, s));
-        nlaunch += 1;
-    };
     static thread_local std::vector<LargeBin> lbins;
     static thread_local std::vector<S1Bin> sbins;
     static thread_local std::vector<uint64_t> pp;
@@ -1008,7 +1265,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
         uint64_t key_base = 0, dbase = 0;
         for (size_t i = 0; i < gn; ++i) {
             const size_t li = g.first + i;
-            const uint64_t b = large_ids[li];
+            const uint64_t b = ids[li];
             lbins[i] = LargeBin{0, 0, bo[b], 0, (uint32_t)bw[b], 0, (uint32_t)bn[b], 0, 0, 0};
             sbins[i] = S1Bin{key_base, nd[li], rc[li], (uint32_t)dbase, 0};
             key_base += (uint64_t)nd[li] * rc[li];
@@ -1045,53 +1302,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             ovf = ar.get<uint64_t>(ovf_cap);
         }
         htrace("split1 done");
-        j->stage_begin(KMC_STAGE_LARGE_CHUNKS);
-        CK(launch_chunk_hash(lkeys, chunks, n_chunks, k, j->ci, j->cx, j->surv_keys, j->surv_counts, gstats, tovf,
-                             ctr + 4, n_sms(), s));
-        j->launches += 1;
-        j->stage_end(1);
-        CK(cudaMemcpyAsync(&hs[52], ctr + 4, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        const uint64_t n_tovf = hs[52];
-        htrace("chunk_hash done");
-        j->st.n_overflow_chunks += n_tovf;
-        if (n_over + n_ovd + n_ovk + n_tovf == 0) continue;
-        int fl = 0;
-        j->stage_begin(KMC_STAGE_LARGE_FALLBACK);
-        if (n_ovd + n_ovk > 0) {
-            // overflowed digits: their region parts join their excess keys in the overflow list
-            std::vector<Chunk> od(n_ovd);
-            if (n_ovd) {
-                CK(cudaMemcpyAsync(od.data(), ovd, n_ovd * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
-                CK(cudaStreamSynchronize(s));
-            }
-            uint64_t need = n_ovk;
-            for (const Chunk& x : od) need += x.n;
-            j->st.n_split_overflow += need;
-            uint64_t* all = ovf;
-            if (need > ovf_cap) {
-                all = ar.get<uint64_t>(need);
-                if (n_ovk) CK(cudaMemcpyAsync(all, ovf, n_ovk * 8, cudaMemcpyDeviceToDevice, s));
-            }
-            uint64_t o = n_ovk;
-            for (const Chunk& x : od) {
-                CK(cudaMemcpyAsync(all + o, (uint64_t*)lkeys + x.begin, (size_t)x.n * 8, cudaMemcpyDeviceToDevice, s));
-                o += x.n;
-            }
-            sort_rle(all, need, fl);
-            if (all != ovf) ar.release(all);
-        }
-        if (n_over + n_tovf > 0) {
-            std::vector<Chunk> ov(n_over + n_tovf);
-            if (n_over) CK(cudaMemcpyAsync(ov.data(), over, n_over * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
-            if (n_tovf)
-                CK(cudaMemcpyAsync(ov.data() + n_over, tovf, n_tovf * sizeof(Chunk), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            for (const Chunk& x : ov) sort_rle((uint64_t*)lkeys + x.begin, x.n, fl);
-        }
-        j->launches += fl;
-        j->stage_end(fl);
-        htrace("fallback enqueued");
+        count_group((uint64_t*)lkeys, ovf, ovf_cap, chunks, over, ovd, tovf, ctr, n_chunks, n_over, n_ovd, n_ovk);
     }
     ar.release(lkeys);
     ar.release(ovf);
@@ -1442,6 +1653,7 @@ void count_phase(kmc_job* j, PlanCtx& c) {
     // the per-bin tables were copied to the host while S5 runs on the device
     fetch_tables(j, c);
     count_bins(j, c, bins, 0, n_bins);
+    presplit_release(j, c.pre);
     ar.release(bins);
 }
 

@@ -207,6 +207,8 @@ cudaError_t launch_make_pieces(const LargeBin* lbins, const uint64_t* piece_pref
 struct Chunk {
     uint64_t begin;  // into the large key array
     uint32_t n;
+    // k_chunk_hash: 0, or a two-segment chunk (a pair of split digits counted together),
+    // n0 | gap << 16: key i is at begin + i for i < n0, else at begin + i + gap
     uint32_t pad;
 };
 int msd_digit_bits(uint64_t bin_windows, int k, int cap);
@@ -251,20 +253,39 @@ cudaError_t launch_large_expand(const uint32_t* bins, const Piece* pieces, uint6
 
 // One-pass sized split of the large bins (k_split1.cu, k <= 32): bin b gets nd digits
 // (digit = (hash(key) * nd) >> 32), digit d owns key slots [key_base + d * rc, + rc).
+// Paired layout (flags & S1_PAIRED, nd even; needs fail[], UINT_MAX-initialised per digit):
+// digits 2e and 2e + 1 share the slots [key_base + 2e rc, + 2 rc), the even one filling them
+// upwards from the start, the odd one downwards from the end (their counts are one 64-bit
+// word of cur, the even digit low), so that a pair overflows only when both together exceed
+// 2 rc, and a pair is one chunk with one gap when it fits the table.
 constexpr int S1_DMAX = 512;
+constexpr uint32_t S1_PAIRED = 1;
 struct S1Bin {
     uint64_t key_base;
-    uint32_t nd, rc, dbase, pad;
+    uint32_t nd, rc, dbase, flags;
 };
 int split1_piece_records(int k);
 // cur: per-digit key counts (zeroed; may exceed rc: overflow); ovf_ctr: keys beyond their
 // region (written to ovf while below ovf_cap)
+// n_pieces_dev (optional): the piece count in device memory (pieces built on the device);
+// n_pieces is then unused
 cudaError_t launch_split1(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const S1Bin* sbins, int k,
                           int canonical, uint32_t* cur, uint64_t* keys, uint64_t* ovf, unsigned long long* ovf_ctr,
-                          uint64_t ovf_cap, int n_ctas, cudaStream_t s);
-// ctr[0] chunks, ctr[1] oversize (> hard_cap), ctr[2] overflowed digits (region parts in ovd)
+                          uint64_t ovf_cap, int n_ctas, cudaStream_t s,
+                          const unsigned long long* n_pieces_dev = nullptr, uint32_t* fail = nullptr,
+                          bool paired = false);
+// ctr[0] chunks, ctr[1] oversize (> hard_cap), ctr[2] overflowed digits (region parts in ovd).
+// Paired bins: a pair whose digits fit their regions and hold <= pair_cap keys together is one
+// two-segment chunk.  Bins with nd = 0 are skipped.
 cudaError_t launch_split1_chunks(const S1Bin* sbins, uint64_t n_bins, const uint32_t* cur, uint32_t hard_cap,
-                                 Chunk* chunks, Chunk* over, Chunk* ovd, unsigned long long* ctr, cudaStream_t s);
+                                 Chunk* chunks, Chunk* over, Chunk* ovd, unsigned long long* ctr, cudaStream_t s,
+                                 uint32_t pair_cap = 0, const uint32_t* fail = nullptr);
+// Pieces of the records that pass 1 appended to the presplit bins since the last call
+// (done[i]: records already split; fill: the bins' fill counters, capped by cap): at most
+// rpp records each, written to pieces[0, *n_pieces).  One CTA.
+cudaError_t launch_presplit_pieces(const uint32_t* bin_ids, uint32_t n_pb, const uint32_t* bin_fill,
+                                   const uint32_t* bin_cap, const uint64_t* bin_rec_off, uint32_t* done, uint32_t rpp,
+                                   Piece* pieces, unsigned long long* n_pieces, cudaStream_t s);
 
 // S6-S8 of the large bins through sub-signatures (k_subsplit.cu, large_path 4, SS_KMIN <= k <=
 // SS_KMAX): bin b gets nd digits, digit = hash of the window's sub-signature (the minimum

@@ -74,3 +74,51 @@ def test_sampled_edge_inputs(gpu):
         keys, counts, st = gpu_count(gpu, w, distribute_path=2)
         ref = oracle.count(w.reads, w.offsets, k, 1, 10**9)
         assert np.array_equal(keys, ref.keys) and np.array_equal(counts, ref.counts)
+
+
+# presplit (kmc_options.presplit): the sampled plan's large bins are split into their digit
+# regions batch by batch during pass 1 (paired digit layout, pairs counted as one two-segment
+# chunk when they fit the table); same bytes as the oracle on every route through it
+@pytest.mark.parametrize("opts", [dict(), dict(small_bin_capacity=256), dict(canonical=False),
+                                  dict(force_large=True), dict(split_tight=True), dict(chunk_capacity=40000),
+                                  dict(small_bin_capacity=256, split_tight=True, canonical=False)])
+def test_presplit_device_reads(gpu, opts):
+    w = synth.make("C4", scale=0.004)
+    opts = dict(dict(small_bin_capacity=512), **opts)
+    keys, counts, st = gpu_count(gpu, w, distribute_path=2, presplit=1, **opts)
+    ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max, canonical=opts.get("canonical", True))
+    assert st["n_presplit_bins"] > 0
+    assert np.array_equal(keys, ref.keys) and np.array_equal(counts, ref.counts)
+    if opts.get("split_tight"):
+        assert st["n_split_overflow"] > 0
+
+
+@pytest.mark.parametrize("batch_mb,opts", [(2, dict()), (1, dict(small_bin_capacity=256)), (3, dict(split_tight=True)),
+                                           (2, dict(presplit=2))])
+def test_presplit_host_batches(gpu, batch_mb, opts):
+    # host-resident reads take the presplit by default: the split of every batch's new records
+    w = synth.make("C4", scale=0.005)
+    opts = dict(dict(small_bin_capacity=512), **opts)
+    rh = torch.from_numpy(w.reads).pin_memory()
+    oh = torch.from_numpy(w.offsets.view(np.uint64))
+    res = gpu.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu", input_batch_mb=batch_mb,
+                    distribute_path=2, **opts)
+    ref = oracle.count(w.reads, w.offsets, w.k, w.cutoff_min, w.cutoff_max)
+    assert res.stats["n_input_batches"] >= 4
+    assert (res.stats["n_presplit_bins"] > 0) == (opts.get("presplit", 0) != 2)
+    assert np.array_equal(res.kmers.numpy(), ref.keys) and np.array_equal(res.counts.numpy(), ref.counts)
+
+
+def test_presplit_rerun(gpu):
+    # a sample that misses part of the input overflows a bin: the presplit is dropped with the
+    # rest of the sampled plan and the call replans
+    first = [s.decode() for s in synth.random_reads(41, 20000, 100, 100, alphabet=b"ACGT")]
+    rest = [s.decode() for s in synth.random_reads(42, 5, 150, 150, alphabet=b"ACGT")] * 3000
+    w = synth.from_strings(first + rest, 28, 9, 1)
+    rh = torch.from_numpy(w.reads).pin_memory()
+    oh = torch.from_numpy(w.offsets.view(np.uint64))
+    res = gpu.count(rh, oh, w.k, w.p, 1, 10**9, out_device="cpu", input_batch_mb=1, distribute_path=2,
+                    small_bin_capacity=256)
+    ref = oracle.count(w.reads, w.offsets, w.k, 1, 10**9)
+    assert res.stats["n_distribute_reruns"] == 1
+    assert np.array_equal(res.kmers.numpy(), ref.keys) and np.array_equal(res.counts.numpy(), ref.counts)
