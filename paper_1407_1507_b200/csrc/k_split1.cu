@@ -308,9 +308,20 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         __syncthreads();
         // ---- W: every digit's run leaves by one bulk copy (+ <= 2 single stores, + overflow)
         if (staged && (uint32_t)tid < nd && paired && (tid & 1)) {
-            // (a downward run: single stores; the two-pass mode is rare)
+            // a downward run: positions [g0, g0 + in_reg) take the slots [E - in_reg, E) below
+            // E = (d + 1) rc - g0 (even; s0 is even as g0 is) -- one bulk copy of an even
+            // number of keys to an even slot, the odd one out stored alone
             const uint32_t s0 = lof[tid], cn = lc[tid] - s0, g0 = gst[tid];
-            for (uint32_t e = 0; e < cn; ++e) put(tid, g0 + e, stage[s0 + e]);
+            const uint32_t in_reg = min(cn, lim[tid] - g0);
+            const uint64_t E = (uint64_t)(tid + 1) * sb.rc - g0;
+            const uint32_t m = in_reg & ~1u;
+            if (in_reg & 1u) region[E - in_reg] = stage[s0 + m];
+            if (m) {
+                tma_store_1d(region + E - m, stage + s0, m * 8u);
+                bulk_commit();
+                bulk_pending = true;
+            }
+            for (uint32_t e = in_reg; e < cn; ++e) put(tid, g0 + e, stage[s0 + e]);
         } else if (staged && (uint32_t)tid < nd) {
             const uint32_t s0 = lof[tid], cn = lc[tid] - s0, g0 = gst[tid];
             const uint32_t in_reg = PAIRED ? min(cn, lim[tid] - g0) : (g0 >= sb.rc ? 0u : min(cn, sb.rc - g0));

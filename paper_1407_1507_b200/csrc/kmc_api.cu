@@ -960,7 +960,8 @@ void presplit_setup(kmc_job* j, PlanCtx& c, const std::vector<uint64_t>& bw, con
         if (cost <= lim) continue;
         uint64_t d = 2 * (uint64_t)std::ceil((double)bw[b] / (2 * kf));
         d = std::min<uint64_t>(std::max<uint64_t>(d, 2), (uint64_t)S1_DMAX);
-        uint64_t r = (uint64_t)std::ceil((double)bw[b] / (double)d * 1.25) + 256;
+        // (more slack than the split after pass 1: the window count is an estimate)
+        uint64_t r = (uint64_t)std::ceil((double)bw[b] / (double)d * 1.4) + 512;
         r = std::min<uint64_t>((r + 1) & ~1ull, 0x7FFFFFFEull);
         pre.ids.push_back(b);
         pre.sb.push_back(S1Bin{key_base, (uint32_t)d, (uint32_t)r, (uint32_t)dbase, S1_PAIRED});

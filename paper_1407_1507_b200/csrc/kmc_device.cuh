@@ -330,6 +330,21 @@ __device__ __forceinline__ bool table_insert_bounded(K* T, uint32_t* C, int lg, 
     }
     return false;
 }
+// The same for a table of TS slots (any TS): slot = the 32-bit hash scaled to [0, TS).
+template <class K>
+__device__ __forceinline__ bool table_insert_ts(K* T, uint32_t* C, uint32_t TS, const K& key) {
+    const K E = key_empty<K>();
+    uint32_t s = (uint32_t)(((uint64_t)slot_hash(key, 32) * TS) >> 32);
+    for (int pr = 0; pr < PROBE_MAX; ++pr) {
+        const K old = smem_cas_empty(&T[s], key);
+        if (key_eq(old, E) || key_eq(old, key)) {
+            atomicAdd(&C[s], 1u);
+            return true;
+        }
+        s = s + 1 == TS ? 0u : s + 1;
+    }
+    return false;
+}
 
 // ---------------------------------------------------------------- warp / block helpers
 __device__ __forceinline__ uint32_t lanemask_lt() {
