@@ -581,7 +581,12 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         const uint64_t batch_bytes = (uint64_t)(j->opt.input_batch_mb ? j->opt.input_batch_mb : 256) << 20;
         uint64_t max_b = 0, max_r = 0;
         for (uint64_t r0 = 0; r0 < n_reads;) {
-            const uint64_t lim = h_off[r0] + batch_bytes;
+            // the last two batches' worth of bases in halving batches (down to 1/8 of one):
+            // what pass 1 still has to do after the input copy ends is the last batch's work
+            const uint64_t left = h_off[n_reads] - h_off[r0];
+            uint64_t bb = batch_bytes;
+            if (left <= 2 * batch_bytes) bb = std::max(left / 2, batch_bytes / 8);
+            const uint64_t lim = h_off[r0] + bb;
             uint64_t r1 = (uint64_t)(std::upper_bound(h_off + r0 + 1, h_off + n_reads + 1, lim) - h_off) - 1;
             if (r1 <= r0) r1 = r0 + 1;
             batches.push_back({r0, r1});
