@@ -186,28 +186,34 @@ __global__ void __launch_bounds__(OC_NT, 2) k_order_chunk_sort(const K* __restri
 // the chunk capacity (CTA radix sort), and above it (oversize, device LSD).  Lists are
 // appended with one atomic per CTA and list; their order is irrelevant.
 constexpr int WS_NT = 256;
+constexpr uint64_t ORD_GROUPS = 8;  // S9's final sorts in this many bucket groups (copy overlap)
 
+// Buckets [b0, b1) of nbk (a group of consecutive buckets: runs of small buckets stop at b1);
+// the group's warp-sort lists in wl[0, 2 (b1 - b0)), its CTA chunks in big[0, b1 - b0), its
+// class counters in counters[0..4]; oversize buckets of every group share one list (over_ctr).
 __global__ void __launch_bounds__(WS_NT) k_ord_classify(const uint32_t* __restrict__ cnt,
                                                         const uint32_t* __restrict__ start, uint64_t nbk,
                                                         uint32_t n, uint32_t cap, uint2* __restrict__ wl,
                                                         Chunk* __restrict__ big, Chunk* __restrict__ over,
-                                                        unsigned long long* __restrict__ counters) {
+                                                        unsigned long long* __restrict__ counters, uint64_t b0,
+                                                        uint64_t b1, unsigned long long* __restrict__ over_ctr) {
+    const uint64_t wn = b1 - b0;
     __shared__ unsigned long long wsum64[WS_NT / 32 + 1];
     __shared__ unsigned long long base[6];
-    const uint64_t d = (uint64_t)blockIdx.x * WS_NT + threadIdx.x;
+    const uint64_t d = b0 + (uint64_t)blockIdx.x * WS_NT + threadIdx.x;
     int cls = -1;  // 0/1/2/3: warp sort of 32/64/128/256 items, 4: CTA sort, 5: oversize
     uint32_t st = 0, sz = 0;
-    if (d < nbk) {
+    if (d < b1) {
         const uint32_t c = cnt[d];
         st = start[d];
         if (c > 32) {
             sz = c;
             cls = c <= 64 ? 1 : c <= 128 ? 2 : c <= 256 ? 3 : c <= cap ? 4 : 5;
         } else {
-            const bool lead = d == 0 || cnt[d - 1] > 32 || (start[d - 1] >> 5) != (st >> 5);
+            const bool lead = d == b0 || cnt[d - 1] > 32 || (start[d - 1] >> 5) != (st >> 5);
             if (lead) {
                 uint64_t e = d + 1;
-                while (e < nbk && cnt[e] <= 32 && (start[e] >> 5) == (st >> 5)) ++e;
+                while (e < b1 && cnt[e] <= 32 && (start[e] >> 5) == (st >> 5)) ++e;
                 sz = (e < nbk ? start[e] : n) - st;
                 if (sz) cls = sz <= 32 ? 0 : 1;
             }
@@ -219,7 +225,8 @@ __global__ void __launch_bounds__(WS_NT) k_ord_classify(const uint32_t* __restri
         block_excl_sum<WS_NT, unsigned long long>(cls >= 0 ? 1ull << (10 * cls) : 0ull, wsum64, &tot);
     if (threadIdx.x < 6) {
         const uint32_t t = (uint32_t)(tot >> (10 * threadIdx.x)) & 1023u;
-        base[threadIdx.x] = t ? atomicAdd(&counters[threadIdx.x], (unsigned long long)t) : 0ull;
+        unsigned long long* ctr = threadIdx.x == 5 ? over_ctr : &counters[threadIdx.x];
+        base[threadIdx.x] = t ? atomicAdd(ctr, (unsigned long long)t) : 0ull;
     }
     __syncthreads();
     if (cls >= 0) {
@@ -228,9 +235,9 @@ __global__ void __launch_bounds__(WS_NT) k_ord_classify(const uint32_t* __restri
         // warp-sort lists in 2 nbk slots: sizes <= 32 / <= 64 from both ends of the first half
         // (together at most one item per bucket), <= 128 / <= 256 from both ends of the second
         if (cls == 0) wl[q] = make_uint2(st, sz);
-        else if (cls == 1) wl[nbk - 1 - q] = make_uint2(st, sz);
-        else if (cls == 2) wl[nbk + q] = make_uint2(st, sz);
-        else if (cls == 3) wl[2 * nbk - 1 - q] = make_uint2(st, sz);
+        else if (cls == 1) wl[wn - 1 - q] = make_uint2(st, sz);
+        else if (cls == 2) wl[wn + q] = make_uint2(st, sz);
+        else if (cls == 3) wl[2 * wn - 1 - q] = make_uint2(st, sz);
         else if (cls == 4) big[q] = ch;
         else over[q] = ch;
     }
@@ -349,7 +356,7 @@ int order_levels(uint64_t n, int k, int cap, int* D) {
 template <class K>
 cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uint32_t* out_vals,
                     const OrderScratch& os, cudaStream_t s, int* launches, std::vector<OrderSegment>* oversize,
-                    void** seg_keys, uint32_t** seg_vals) {
+                    void** seg_keys, uint32_t** seg_vals, const OrderRangeFn* range_done) {
     constexpr uint64_t TI = OrderTile<K>::v;
     const int twok = 2 * k;
     int D[4];
@@ -398,44 +405,89 @@ cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uin
     const Chunk* over_list = os.oversize;
     const size_t sm = order_smem<K>();
     if ((e = cudaFuncSetAttribute(k_order_chunk_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
+    oversize->clear();
     if constexpr (sizeof(K) == 8) {
         // lists in buffers the MSD passes are done with: the warp-sort lists {begin, n} in
         // os.chunks (2 nbk uint2: 64-item sorts from the front of the first half, 128 / 256
         // from both ends of the second), CTA chunks in os.oversize, oversize buckets (at
-        // most n / cap + 1 of them) in os.cursor
+        // most n / cap + 1 of them) in os.cursor.  With range_done, the buckets are taken in
+        // G groups of consecutive buckets, so that the caller can copy a group's output
+        // while the next one is sorted.
         uint2* wlist = reinterpret_cast<uint2*>(os.chunks);
         Chunk* big = os.oversize;
         Chunk* over = reinterpret_cast<Chunk*>(os.cursor);
         static_assert(sizeof(Chunk) == 2 * sizeof(uint2), "two list entries per chunk slot");
-        k_ord_classify<<<(unsigned)((nbk + WS_NT - 1) / WS_NT), WS_NT, 0, s>>>(
-            os.hist, os.start, nbk, (uint32_t)n, OrderCap<K>::v, wlist, big, over, os.counters);
-        chunk_list = big;
-        over_list = over;
-        if ((e = cudaGetLastError())) return e;
-        if ((e = cudaMemcpyAsync(os.host, os.counters, 48, cudaMemcpyDeviceToHost, s))) return e;
-        if ((e = cudaStreamSynchronize(s))) return e;
-        const uint64_t nw[4] = {os.host[0], os.host[1], os.host[2], os.host[3]};
-        n_chunks = os.host[4];
-        n_over = os.host[5];
-        constexpr int WPB = WS_NT / 32;
-        const uint2* wl[4] = {wlist, wlist + nbk - 1, wlist + nbk, wlist + 2 * nbk - 1};
-        const int dir[4] = {1, -1, 1, -1};
-        const bool pack = twok <= 56;
-        for (int q = 0; q < 4; ++q) {
-            if (!nw[q]) continue;
-            const unsigned g = (unsigned)((nw[q] + WPB - 1) / WPB);
-#define KMC_WSORT(R)                                                                                          \
-    (pack ? k_ord_wsort<R, true><<<g, WS_NT, 0, s>>>(ck, cv, wl[q], nw[q], dir[q], out_keys, out_vals)          \
-          : k_ord_wsort<R, false><<<g, WS_NT, 0, s>>>(ck, cv, wl[q], nw[q], dir[q], out_keys, out_vals))
-            if (q == 0) KMC_WSORT(1);
-            if (q == 1) KMC_WSORT(2);
-            if (q == 2) KMC_WSORT(4);
-            if (q == 3) KMC_WSORT(8);
-#undef KMC_WSORT
+        // every group is classified first (its lists in its own slice of the buffers, one
+        // read-back for all), then the groups' sorts are launched in order: the caller's copy
+        // of a group can start while the next group sorts, with no read-back behind it
+        const uint64_t G = range_done ? std::min<uint64_t>(ORD_GROUPS, nbk) : 1;
+        unsigned long long* over_ctr = os.counters + 8 * ORD_GROUPS;
+        if ((e = cudaMemsetAsync(os.counters, 0, (8 * ORD_GROUPS + 1) * 8, s))) return e;
+        std::vector<uint64_t> bb(G + 1);
+        for (uint64_t g = 0; g <= G; ++g) bb[g] = g * nbk / G;
+        for (uint64_t g = 0; g < G; ++g) {
+            const uint64_t b0 = bb[g], b1 = bb[g + 1];
+            if (b1 <= b0) continue;
+            k_ord_classify<<<(unsigned)((b1 - b0 + WS_NT - 1) / WS_NT), WS_NT, 0, s>>>(
+                os.hist, os.start, nbk, (uint32_t)n, OrderCap<K>::v, wlist + 2 * b0, big + b0, over,
+                os.counters + 8 * g, b0, b1, over_ctr);
             *launches += 1;
         }
         if ((e = cudaGetLastError())) return e;
-        *launches += 1;
+        unsigned long long* H = os.host;  // [8 G counters][over count][G + 1 group starts]
+        if ((e = cudaMemcpyAsync(H, os.counters, (8 * ORD_GROUPS + 1) * 8, cudaMemcpyDeviceToHost, s))) return e;
+        uint32_t* hstart = reinterpret_cast<uint32_t*>(H + 8 * ORD_GROUPS + 1);
+        for (uint64_t g = 1; g < G; ++g)
+            if ((e = cudaMemcpyAsync(hstart + g, os.start + bb[g], 4, cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaStreamSynchronize(s))) return e;
+        const uint64_t nov = H[8 * ORD_GROUPS];
+        std::vector<Chunk> ovs(nov);
+        if (nov) {
+            if ((e = cudaMemcpyAsync(ovs.data(), over, nov * sizeof(Chunk), cudaMemcpyDeviceToHost, s))) return e;
+            if ((e = cudaStreamSynchronize(s))) return e;
+            for (auto& c : ovs) oversize->push_back(OrderSegment{c.begin, c.n});
+        }
+        std::vector<uint64_t> ist(G + 1);
+        ist[0] = 0;
+        ist[G] = n;
+        for (uint64_t g = 1; g < G; ++g) ist[g] = hstart[g];
+        constexpr int WPB = WS_NT / 32;
+        const int dir[4] = {1, -1, 1, -1};
+        const bool pack = twok <= 56;
+        for (uint64_t g = 0; g < G; ++g) {
+            const uint64_t b0 = bb[g], b1 = bb[g + 1], wn = b1 - b0;
+            if (wn == 0) continue;
+            const unsigned long long* c = H + 8 * g;
+            uint2* w = wlist + 2 * b0;
+            const uint2* wl[4] = {w, w + wn - 1, w + wn, w + 2 * wn - 1};
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t nw = c[q];
+                if (!nw) continue;
+                const unsigned gr = (unsigned)((nw + WPB - 1) / WPB);
+#define KMC_WSORT(R)                                                                                          \
+    (pack ? k_ord_wsort<R, true><<<gr, WS_NT, 0, s>>>(ck, cv, wl[q], nw, dir[q], out_keys, out_vals)            \
+          : k_ord_wsort<R, false><<<gr, WS_NT, 0, s>>>(ck, cv, wl[q], nw, dir[q], out_keys, out_vals))
+                if (q == 0) KMC_WSORT(1);
+                if (q == 1) KMC_WSORT(2);
+                if (q == 2) KMC_WSORT(4);
+                if (q == 3) KMC_WSORT(8);
+#undef KMC_WSORT
+                *launches += 1;
+            }
+            if (c[4]) {
+                k_order_chunk_sort<K><<<(unsigned)c[4], OC_NT, sm, s>>>(ck, cv, big + b0, twok, out_keys, out_vals);
+                *launches += 1;
+            }
+            if ((e = cudaGetLastError())) return e;
+            if (range_done) {
+                bool has_over = false;
+                for (auto& o : ovs) has_over |= o.begin >= ist[g] && o.begin < ist[g + 1];
+                (*range_done)(ist[g], ist[g + 1], !has_over);
+            }
+        }
+        *seg_keys = ck;
+        *seg_vals = cv;
+        return cudaSuccess;
     } else {
         GreedyArgs ga{};
         ga.cnt = os.hist;
@@ -456,7 +508,6 @@ cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uin
         k_order_chunk_sort<K><<<(unsigned)n_chunks, OC_NT, sm, s>>>(ck, cv, chunk_list, twok, out_keys, out_vals);
     if ((e = cudaGetLastError())) return e;
     *launches += n_chunks > 0;
-    oversize->clear();
     *seg_keys = ck;
     *seg_vals = cv;
     if (n_over) {
@@ -501,7 +552,8 @@ size_t order_scan_temp_bytes(uint64_t n_digits) { return scan_detail::scan_temp_
 
 cudaError_t launch_order(int key_words, void* keys, uint32_t* vals, uint64_t n, int k, void* out_keys,
                          uint32_t* out_vals, const OrderScratch& os, cudaStream_t s, int* launches,
-                         std::vector<OrderSegment>* oversize, void** seg_keys, uint32_t** seg_vals) {
+                         std::vector<OrderSegment>* oversize, void** seg_keys, uint32_t** seg_vals,
+                         const OrderRangeFn* range_done) {
     oversize->clear();
     *seg_keys = keys;
     *seg_vals = vals;
@@ -509,9 +561,9 @@ cudaError_t launch_order(int key_words, void* keys, uint32_t* vals, uint64_t n, 
     if (n >= (1ull << 32)) return cudaErrorInvalidValue;
     if (key_words == 1)
         return order_t<uint64_t>((uint64_t*)keys, vals, n, k, (uint64_t*)out_keys, out_vals, os, s, launches, oversize,
-                                 seg_keys, seg_vals);
+                                 seg_keys, seg_vals, range_done);
     return order_t<K128>((K128*)keys, vals, n, k, (K128*)out_keys, out_vals, os, s, launches, oversize, seg_keys,
-                         seg_vals);
+                         seg_vals, nullptr);
 }
 
 }  // namespace kmc

@@ -197,6 +197,16 @@ bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+bool is_pinned_host(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 // KMC_HOST_TRACE=1: host timestamps of the call's phases on stderr (diagnostics)
 void htrace(const char* what) {
     static const bool on = getenv("KMC_HOST_TRACE") != nullptr;
@@ -2273,7 +2283,7 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     os.cursor = ar.get<uint32_t>(nd);
     os.chunks = ar.get<Chunk>(nd);
     os.oversize = ar.get<Chunk>(nd);
-    os.counters = ar.get<unsigned long long>(8);
+    os.counters = ar.get<unsigned long long>(80);
     os.tiles = ar.get<OrdTile>(order_max_tiles(n, j->k));
     os.tprefix = ar.get<uint64_t>(order_prev_buckets(n, j->k) + 1);
     os.ttemp = ar.alloc(scan_temp_bytes(order_prev_buckets(n, j->k) + 1));
@@ -2286,8 +2296,30 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     j->stage_begin(KMC_STAGE_ORDER);
     void* seg_k = nullptr;
     uint32_t* seg_v = nullptr;
+    // host outputs in pinned memory: every group of S9's final sorts is copied out on the copy
+    // stream while the next group is sorted (groups holding an oversize bucket after its sort)
+    const bool overlap = !dev_out && is_pinned_host(out_kmers) && is_pinned_host(out_counts) && kw == 1;
+    std::vector<std::pair<uint64_t, uint64_t>> later;
+    std::vector<cudaEvent_t> gev;
+    OrderRangeFn range_done = [&](uint64_t lo, uint64_t hi, bool final) {
+        if (hi <= lo) return;
+        if (!final) {
+            later.push_back({lo, hi});
+            return;
+        }
+        cudaEvent_t ev = nullptr;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        gev.push_back(ev);
+        CK(cudaEventRecord(ev, s));
+        CK(cudaStreamWaitEvent(j->cs, ev, 0));
+        CK(cudaMemcpyAsync((uint8_t*)out_kmers + lo * ksz, (uint8_t*)ok + lo * ksz, (hi - lo) * ksz,
+                           cudaMemcpyDeviceToHost, j->cs));
+        CK(cudaMemcpyAsync(out_counts + lo, oc + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost, j->cs));
+    };
+    if (overlap) j->make_copy_stream();
     htrace("order launch");
-    CK(launch_order(kw, j->surv_keys, j->surv_counts, n, j->k, ok, oc, os, s, &sl, &over, &seg_k, &seg_v));
+    CK(launch_order(kw, j->surv_keys, j->surv_counts, n, j->k, ok, oc, os, s, &sl, &over, &seg_k, &seg_v,
+                    overlap ? &range_done : nullptr));
     htrace("order enqueued");
     if (!over.empty()) {
         // oversize buckets (more survivors than one chunk): gathered into one array, sorted
@@ -2326,7 +2358,22 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     }
     j->launches += sl;
     j->stage_end(sl);
-    if (!dev_out) {
+    if (overlap) {
+        // (the stage covers what is left of the copies once the sorts are done)
+        j->stage_begin(KMC_STAGE_OUTPUT);
+        for (auto& r : later) {
+            CK(cudaMemcpyAsync((uint8_t*)out_kmers + r.first * ksz, (uint8_t*)ok + r.first * ksz,
+                               (r.second - r.first) * ksz, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(out_counts + r.first, oc + r.first, (r.second - r.first) * 4, cudaMemcpyDeviceToHost, s));
+        }
+        cudaEvent_t done = nullptr;
+        CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        CK(cudaEventRecord(done, j->cs));
+        CK(cudaStreamWaitEvent(s, done, 0));  // the call's stream covers every copy
+        j->stage_end(0);
+        cudaEventDestroy(done);
+        for (cudaEvent_t e : gev) cudaEventDestroy(e);
+    } else if (!dev_out) {
         j->stage_begin(KMC_STAGE_OUTPUT);
         CK(cudaMemcpyAsync(out_kmers, ok, n * ksz, cudaMemcpyDefault, s));
         CK(cudaMemcpyAsync(out_counts, oc, n * 4, cudaMemcpyDefault, s));

@@ -1,6 +1,7 @@
 // kmc_internal.h -- host-side declarations shared by the kmcgpu translation units.
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -387,14 +388,14 @@ struct OrderScratch {
     uint32_t* cursor;       // [2^order_digit_bits] scatter cursors
     Chunk* chunks;          // [2^order_digit_bits]
     Chunk* oversize;        // [2^order_digit_bits]
-    unsigned long long* counters;  // [8]
+    unsigned long long* counters;  // [80]
     OrdTile* tiles;         // [order_max_tiles(n, k)]
     uint64_t* tprefix;      // [order_prev_buckets(n, k) + 1] tiles per bucket (device-built tiles)
     void* ttemp;            // scan_temp_bytes(order_prev_buckets(n, k) + 1)
     void* tmp_keys;         // [n] K
     uint32_t* tmp_vals;     // [n]
     void* scan_temp;        // order_scan_temp_bytes(2^(D1+D2) + 1)
-    unsigned long long* host;  // pinned, >= 2 entries
+    unsigned long long* host;  // pinned, >= 80 entries
 };
 struct OrderSegment {
     uint64_t begin, n;  // items of an oversize bucket in (*seg_keys, *seg_vals) after launch_order
@@ -407,8 +408,14 @@ size_t order_scan_temp_bytes(uint64_t n_digits);
 // Sorts (keys, vals) ascending into (out_keys, out_vals); keys/vals are used as scratch.
 // Buckets holding more than the chunk capacity are left, grouped, in (*seg_keys, *seg_vals)
 // and returned in *oversize for the caller to sort with device_radix_sort and copy out.
+// range_done (optional, 64-bit keys): the final sorts run in groups of consecutive buckets;
+// after each group's kernels are enqueued on s, range_done(lo, hi, final) names its output
+// items [lo, hi) -- final = false when the group holds an oversize bucket (its items are in
+// place only after the caller's oversize sort)
+using OrderRangeFn = std::function<void(uint64_t lo, uint64_t hi, bool final)>;
 cudaError_t launch_order(int key_words, void* keys, uint32_t* vals, uint64_t n, int k, void* out_keys,
                          uint32_t* out_vals, const OrderScratch& os, cudaStream_t s, int* launches,
-                         std::vector<OrderSegment>* oversize, void** seg_keys, uint32_t** seg_vals);
+                         std::vector<OrderSegment>* oversize, void** seg_keys, uint32_t** seg_vals,
+                         const OrderRangeFn* range_done = nullptr);
 
 }  // namespace kmc

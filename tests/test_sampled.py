@@ -122,3 +122,22 @@ def test_presplit_rerun(gpu):
     ref = oracle.count(w.reads, w.offsets, w.k, 1, 10**9)
     assert res.stats["n_distribute_reruns"] == 1
     assert np.array_equal(res.kmers.numpy(), ref.keys) and np.array_equal(res.counts.numpy(), ref.counts)
+
+
+@pytest.mark.parametrize("out_device", ["cpu", "cuda"])
+def test_order_oversize_buckets(gpu, out_device):
+    # survivors piling into one S9 bucket (a shared all-A prefix) beyond a CTA sort: the
+    # oversize path; with pinned host outputs the groups of S9's final sorts are copied out
+    # while the next group sorts, the group holding the oversize bucket after its sort
+    tails = [s.decode() for s in synth.random_reads(7, 30000, 88, 88, alphabet=b"ACGT")]
+    w = synth.from_strings(["A" * 12 + t for t in tails], 28, 9, 1)
+    rh = torch.from_numpy(w.reads)
+    oh = torch.from_numpy(w.offsets.view(np.uint64))
+    if out_device == "cuda":
+        rh, oh = rh.cuda(), oh.cuda()
+    else:
+        rh = rh.pin_memory()
+    res = gpu.count(rh, oh, w.k, w.p, 1, 10**9, out_device=out_device)
+    ref = oracle.count(w.reads, w.offsets, w.k, 1, 10**9)
+    assert res.stats["n_order_oversize"] > 0
+    assert np.array_equal(res.kmers.cpu().numpy(), ref.keys) and np.array_equal(res.counts.cpu().numpy(), ref.counts)
