@@ -1076,15 +1076,21 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
             __syncthreads();
             continue;
         }
+        // the thread's slots t + i CH_NT (i < TS / CH_NT: the same for the whole block): their
+        // counts stay in registers between the two passes
+        constexpr int SPT = TSMAX / CH_NT;
+        static_assert(TSMAX % CH_NT == 0, "whole rounds of slots");
+        uint32_t cv[SPT];
         uint32_t keep = 0;
-        for (int s = t; s < TS; s += CH_NT) {
-            const uint32_t c = C[s];
-            if (c) {
-                ++uniq;
-                if (c < ci) ++below;
-                else if (c > cx) ++above;
-                else ++keep;
-            }
+#pragma unroll
+        for (int i = 0; i < SPT; ++i) {
+            const uint32_t s = t + i * CH_NT;
+            cv[i] = s < TS ? C[s] : 0u;
+            const uint32_t c = cv[i];
+            uniq += c != 0;
+            below += c != 0 && c < ci;
+            above += c > cx;
+            keep += c != 0 && c >= ci && c <= cx;
         }
         // every warp reserves the output range of the survivors it counted (it writes the same
         // slots below): no barrier, and the atomic's round trip overlaps the other warps' work
@@ -1092,8 +1098,11 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
         unsigned long long o = 0;
         if (lane == 0 && keep) o = atomicAdd(&gstats[GS_SURV], (unsigned long long)keep);
         o = __shfl_sync(0xffffffffu, o, 0);
-        for (int s = t; s < TS; s += CH_NT) {  // TS is a multiple of 64: whole warps iterate
-            const uint32_t c = C[s];
+#pragma unroll
+        for (int i = 0; i < SPT; ++i) {
+            const uint32_t s = t + i * CH_NT;
+            if (s >= TS) break;  // (uniform)
+            const uint32_t c = cv[i];
             const bool kp = c >= ci && c <= cx && c != 0;
             const uint32_t bb = __ballot_sync(0xffffffffu, kp);
             if (kp) {
