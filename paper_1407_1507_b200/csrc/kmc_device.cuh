@@ -331,17 +331,23 @@ __device__ __forceinline__ bool table_insert_bounded(K* T, uint32_t* C, int lg, 
     return false;
 }
 // The same for a table of TS slots (any TS): slot = the 32-bit hash scaled to [0, TS).
+// Double hashing: the probe step is 1 + 6 j (j = the hash's low 7 bits; the slot comes from
+// its high bits).  The step is odd, so with TS = 1024 m its cycle has TS / gcd(step, m) >= 1024
+// slots, more than PROBE_MAX probes visit.
 template <class K>
 __device__ __forceinline__ bool table_insert_ts(K* T, uint32_t* C, uint32_t TS, const K& key) {
     const K E = key_empty<K>();
-    uint32_t s = (uint32_t)(((uint64_t)slot_hash(key, 32) * TS) >> 32);
+    const uint32_t h = slot_hash(key, 32);
+    uint32_t s = (uint32_t)(((uint64_t)h * TS) >> 32);
+    const uint32_t step = 1u + 6u * (h & 127u);
     for (int pr = 0; pr < PROBE_MAX; ++pr) {
         const K old = smem_cas_empty(&T[s], key);
         if (key_eq(old, E) || key_eq(old, key)) {
             atomicAdd(&C[s], 1u);
             return true;
         }
-        s = s + 1 == TS ? 0u : s + 1;
+        s += step;
+        if (s >= TS) s -= TS;
     }
     return false;
 }
