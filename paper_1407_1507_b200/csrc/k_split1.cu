@@ -102,6 +102,16 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
     bool bulk_pending = false;
     uint32_t cur_bin = 0xFFFFFFFFu;
     S1Bin sb{};
+    // A bin whose pieces all fall in this CTA's range is OWNED: thread d keeps digit d's cursor
+    // in a register (no global atomic -- and no round trip -- between a piece's expansion and
+    // its runs' bulk copies) and stores it when the bin ends.  Only the first and the last bin
+    // of the range can be shared with a neighbouring CTA (pieces of a bin are consecutive);
+    // those reserve with global atomics.  (Unpaired layout; the paired one always reserves.)
+    const uint32_t first_lbin = pieces[p0].lbin, last_lbin = pieces[p1 - 1].lbin;
+    const bool first_shared = p0 > 0 && pieces[p0 - 1].lbin == first_lbin;
+    const bool last_shared = p1 < n_pieces && pieces[p1].lbin == last_lbin;
+    bool owned = false;
+    uint32_t my_cur = 0;
     uint32_t C1 = 0;  // single pass: stage slots of a digit (even), per bin
     const uint32_t umagic = (65536u + (uint32_t)U - 1) / (uint32_t)U;  // (x / U) = (x * umagic) >> 16, x < 64
     Piece pnext = pieces[p0];
@@ -115,9 +125,12 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         const Piece pc = pnext;
         if (p + 1 < p1) pnext = pieces[p + 1];
         if (pc.lbin != cur_bin) {
+            if (!PAIRED && owned && (uint32_t)tid < sb.nd) cur[sb.dbase + tid] = my_cur;
             cur_bin = pc.lbin;
             sb = sbins[cur_bin];
             C1 = sb.nd ? ((uint32_t)S1_STAGE / sb.nd) & ~1u : 0u;
+            owned = !PAIRED && !(first_shared && cur_bin == first_lbin) && !(last_shared && cur_bin == last_lbin);
+            if (owned && (uint32_t)tid < sb.nd) my_cur = cur[sb.dbase + tid];
         }
         const uint32_t nd = sb.nd;
         mbar_wait(mbar + b, (it >> 1) & 1);
@@ -204,7 +217,12 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
                 ra = g >= L ? 0u : min(ce, L - g);
                 if (ra < ce) atomicMin(&fail[sb.dbase + d], g + ra);
             } else {
-                g = atomicAdd(&cur[sb.dbase + d], ce);
+                if (owned) {  // (d == this thread's digit)
+                    g = my_cur;
+                    my_cur += ce;
+                } else {
+                    g = atomicAdd(&cur[sb.dbase + d], ce);
+                }
                 ra = g >= sb.rc ? 0u : min(ce, sb.rc - g);
             }
             if (ra < ce) ovb[d] = (uint32_t)atomicAdd(ovf_ctr, (unsigned long long)(ce - ra));
@@ -345,6 +363,7 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         }
         if ((uint32_t)tid < nd && (c & 1u)) put(tid, g + c, ~0ull);  // the pad slot of an odd run
     }
+    if (!PAIRED && owned && (uint32_t)tid < sb.nd) cur[sb.dbase + tid] = my_cur;
     if (bulk_pending) bulk_wait_all();
 }
 
