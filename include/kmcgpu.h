@@ -221,7 +221,7 @@ void kmc_empty_cache(void);
 
 /* One-call form.  reads: n_bases bytes, read i = reads[offsets[i]-offsets[0] ..
  * offsets[i+1]-offsets[0]); read_offsets: n_reads+1 nondecreasing uint64 (offsets[0] may
- * be any value).  Requires 1 <= k <= 64, 1 <= p <= min(k, 12) (p = signature length,
+ * be any value).  Requires 1 <= k <= 64, 1 <= p <= min(k, 15) (p = signature length,
  * P:L1188 "-p"), cutoff_max >= max(cutoff_min, 1) (cutoff_min 0 is treated as 1).
  * Writes n_out pairs if out_capacity >= n_out, else returns KMC_ERR_OUT_CAPACITY with
  * stats->n_out = required.  A capacity that is always enough is

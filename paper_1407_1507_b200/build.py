@@ -21,7 +21,7 @@ HEADERS = ["kmc_device.cuh", "kmc_internal.h", "kmc_scan.cuh"]
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include")] + os.environ.get("KMC_NVCC_EXTRA", "").split()  # (experiments)
 
 
 def _newest_input() -> float:

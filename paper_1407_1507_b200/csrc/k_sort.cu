@@ -1009,7 +1009,10 @@ __global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ k
     // Keys stream straight from HBM into registers: thread t takes the chunk's keys
     // t, t + CH_NT, ...; UNR of them are in flight while the previous UNR are inserted, and
     // the next chunk's first UNR are issued before the table of the current one is scanned.
-    constexpr int TSMAX = HashCfg<K>::slots, UNR = 2;
+    #ifndef KMC_CH_UNR
+#define KMC_CH_UNR 2
+#endif
+    constexpr int TSMAX = HashCfg<K>::slots, UNR = KMC_CH_UNR;
     constexpr int NW = CH_NT / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     K* T = reinterpret_cast<K*>(smem);

@@ -427,8 +427,8 @@ kmc_status validate(int k, int p, uint32_t ci, uint32_t cx) {
         set_err("k=%d outside [1, 64]", k);
         return KMC_ERR_INVALID_ARG;
     }
-    if (p < 1 || p > 12 || p > k) {
-        set_err("p=%d outside [1, min(k, 12)] (k=%d)", p, k);
+    if (p < 1 || p > 15 || p > k) {  // 4^15 + 1 signature ids fit 32 bits
+        set_err("p=%d outside [1, min(k, 15)] (k=%d)", p, k);
         return KMC_ERR_INVALID_ARG;
     }
     if (ci == 0) ci = 1;
@@ -2935,8 +2935,8 @@ kmc_status kmc_debug_signatures_ex(const uint8_t* reads, const uint64_t* read_of
 }
 
 kmc_status kmc_debug_allowed(int p, uint8_t* out_allowed, void* stream) {
-    if (p < 1 || p > 12) {
-        set_err("p=%d outside [1, 12]", p);
+    if (p < 1 || p > 15) {
+        set_err("p=%d outside [1, 15]", p);
         return KMC_ERR_INVALID_ARG;
     }
     cudaStream_t s = (cudaStream_t)stream;

@@ -54,7 +54,7 @@ def test_invalid_args_rejected_before_device_work(lib_path):
     # k out of range -> KMC_ERR_INVALID_ARG (1) without touching the device
     st = lib.kmc_count(None, None, ctypes.c_uint64(0), 0, 7, 1, 10, None, None, ctypes.c_uint64(0), None, None)
     assert st == 1 and b"k=" in lib.kmc_last_error()
-    st = lib.kmc_count(None, None, ctypes.c_uint64(0), 25, 13, 1, 10, None, None, ctypes.c_uint64(0), None, None)
+    st = lib.kmc_count(None, None, ctypes.c_uint64(0), 25, 16, 1, 10, None, None, ctypes.c_uint64(0), None, None)
     assert st == 1
     st = lib.kmc_count(None, None, ctypes.c_uint64(0), 25, 7, 5, 4, None, None, ctypes.c_uint64(0), None, None)
     assert st == 1

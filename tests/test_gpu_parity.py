@@ -74,7 +74,8 @@ def test_signature_fig1_golden(gpu):
     assert got[:7].tolist() == sig and all(x == 0xFFFFFFFF for x in got[7:])
 
 
-@pytest.mark.parametrize("k,p", [(25, 7), (28, 9), (31, 9), (55, 11), (64, 12), (8, 8), (12, 3), (5, 1), (33, 5), (64, 1), (37, 1), (36, 1), (46, 10)])
+@pytest.mark.parametrize("k,p", [(25, 7), (28, 9), (31, 9), (55, 11), (64, 12), (8, 8), (12, 3), (5, 1), (33, 5), (64, 1), (37, 1), (36, 1), (46, 10),
+                                 (28, 13), (40, 14), (31, 15), (15, 15), (64, 15)])
 def test_signature_parity_random(gpu, k, p):
     seqs = synth.random_reads(k * 100 + p, 400, 0, 300, n_frac=0.01, lower_frac=0.02)
     _sig_case(gpu, synth.from_strings(seqs, k), k, p)
@@ -113,10 +114,16 @@ def test_forced_paths(gpu, opts):
         assert st["large_windows"] == st["n_windows"]
 
 
+@pytest.mark.parametrize("name,scale,p", [("C5", 0.005, 13), ("C5", 0.005, 15), ("C4", 0.001, 14), ("C4", 0.001, 15)])
+def test_long_signatures(gpu, name, scale, p):
+    # p up to 15 (4^15 + 1 signature ids in 32 bits); C4 at 0.001 takes the sampled plan
+    assert_same(gpu, synth.make(name, scale=scale), p=p)
+
+
 def test_p_invariance(gpu):
     w = synth.make("C2", scale=0.005)
     outs = []
-    for p in (3, 5, 7, 9, 11, 12):
+    for p in (3, 5, 7, 9, 11, 12, 13, 15):
         keys, counts, _ = gpu_count(gpu, w, p=p)
         outs.append((keys, counts))
     for keys, counts in outs[1:]:
@@ -307,7 +314,7 @@ def test_host_buffers_and_capacity(gpu):
 def test_invalid_args(gpu):
     w = synth.make("C1", scale=0.001)
     r, o = to_dev(w)
-    for k, p, ci, cx in ((0, 1, 1, 10), (65, 9, 1, 10), (25, 13, 1, 10), (5, 7, 1, 10), (25, 7, 5, 4)):
+    for k, p, ci, cx in ((0, 1, 1, 10), (65, 9, 1, 10), (25, 16, 1, 10), (12, 13, 1, 10), (5, 7, 1, 10), (25, 7, 5, 4)):
         with pytest.raises(gpu.KmcError) as ei:
             gpu.count(r, o, k, p, ci, cx)
         assert ei.value.status == gpu.KMC_ERR_INVALID_ARG
