@@ -310,6 +310,59 @@ struct PreSplit {
     uint32_t rpp = 0;
 };
 
+// A per-bin host table (windows, records or first record of every bin) in pinned memory from
+// a process-wide pool: the three tables reach the host by asynchronous copies and one
+// synchronisation (pageable destinations made every copy a synchronous staged transfer).
+std::mutex g_tab_mu;
+std::vector<std::pair<uint64_t*, size_t>> g_tab_free;  // (block, capacity in entries)
+struct HostTable {
+    uint64_t* p = nullptr;
+    size_t n = 0, cap = 0;
+    HostTable() = default;
+    HostTable(const HostTable&) = delete;
+    HostTable& operator=(const HostTable&) = delete;
+    ~HostTable() { release(); }
+    void release() {
+        if (!p) return;
+        std::lock_guard<std::mutex> g(g_tab_mu);
+        g_tab_free.emplace_back(p, cap);
+        p = nullptr;
+        n = cap = 0;
+    }
+    // n entries (contents undefined until written)
+    void resize(size_t m) {
+        if (m > cap) {
+            release();
+            {
+                std::lock_guard<std::mutex> g(g_tab_mu);
+                for (size_t i = 0; i < g_tab_free.size(); ++i)
+                    if (g_tab_free[i].second >= m) {
+                        p = g_tab_free[i].first;
+                        cap = g_tab_free[i].second;
+                        g_tab_free.erase(g_tab_free.begin() + (long)i);
+                        break;
+                    }
+            }
+            if (!p) {
+                const size_t c = m + m / 4 + 1024;
+                if (cudaMallocHost(&p, c * 8) != cudaSuccess) {
+                    cudaGetLastError();
+                    p = nullptr;
+                    set_err("cudaMallocHost of a %zu-entry bin table failed", c);
+                    throw Fail{KMC_ERR_ALLOC};
+                }
+                cap = c;
+            }
+        }
+        n = m;
+    }
+    uint64_t& operator[](size_t i) { return p[i]; }
+    const uint64_t& operator[](size_t i) const { return p[i]; }
+    uint64_t* data() { return p; }
+    const uint64_t* data() const { return p; }
+    size_t size() const { return n; }
+};
+
 struct PlanCtx {
     PlanArgs pa{};
     uint64_t ns = 0, n_bins = 0, n_windows = 0, n_records = 0;
@@ -321,7 +374,7 @@ struct PlanCtx {
     unsigned long long* gstats = nullptr;
     uint32_t* tmp_recs = nullptr;
     uint32_t* tmp_sig = nullptr;
-    std::vector<uint64_t> bw, bn, bo;  // per bin: windows, records, first record
+    HostTable bw, bn, bo;              // per bin: windows, records, first record (pinned)
     bool tables_pending = false;       // bw/bn/bo not yet copied to the host (fetch_tables)
     cudaEvent_t ev_plan = nullptr;     // recorded on the job stream right after the plan
     P1Args a{};
@@ -766,22 +819,32 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         a.sig_dest = nullptr;
         htrace("scatter pass enqueued");
         CK(cudaMemcpyAsync(&hs[4], gstats + GS_P1_OVF, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
         j->launches += nl;
         j->stage_end(nl);
+        // ---- the exact per-bin tables on the sampled plan and their copies to the host are
+        //      enqueued before the capacity check (a pass whose bins overflowed discards them
+        //      and replans): one synchronisation after pass 1 instead of three
+        j->stage_begin(KMC_STAGE_PLAN);
+        int pl = 0;
+        CK(launch_exact_tables(pa, n_bins, bin_fill, s, &pl));
+        j->launches += pl;
+        j->stage_end(pl);
+        CK(cudaMemcpyAsync(&hs[1], pa.win_scan + ns, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
+        const bool early_tables = !j->cs && n_bins > 0;
+        if (early_tables) {
+            c.bw.resize(n_bins);
+            c.bn.resize(n_bins);
+            c.bo.resize(n_bins);
+            CK(cudaMemcpyAsync(c.bw.data(), pa.bin_w, n_bins * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(c.bn.data(), pa.bin_nrec, n_bins * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(c.bo.data(), pa.bin_rec_off, n_bins * 8, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
         ar.release(ctemp);
         ar.release(cap64);
         ar.release(cap_scan);
         if (hs[4] == 0) {
-            // ---- exact per-bin tables on the sampled plan
-            j->stage_begin(KMC_STAGE_PLAN);
-            int pl = 0;
-            CK(launch_exact_tables(pa, n_bins, bin_fill, s, &pl));
-            j->launches += pl;
-            j->stage_end(pl);
-            CK(cudaMemcpyAsync(&hs[1], pa.win_scan + ns, 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(&hs[16], gstats, GS_N * 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
             c.n_windows = hs[1];
             c.n_records = hs[16 + GS_RECORDS];  // (the bins' fill counters are the per-bin counts)
             j->st.n_windows = c.n_windows;
@@ -794,7 +857,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
                 set_err("sampled distribution: histogram totals disagree with pass-1 counters");
                 throw Fail{KMC_ERR_INTERNAL};
             }
-            if (c.n_windows > 0) {
+            if (c.n_windows > 0 && !early_tables) {
                 c.tables_pending = true;
                 CK(cudaEventCreateWithFlags(&c.ev_plan, cudaEventDisableTiming));
                 CK(cudaEventRecord(c.ev_plan, s));
@@ -938,9 +1001,9 @@ void fetch_tables(kmc_job* j, PlanCtx& c) {
     htrace("fetch_tables");
     c.tables_pending = false;
     const uint64_t n_bins = c.n_bins;
-    c.bw.assign(n_bins, 0);
-    c.bn.assign(n_bins, 0);
-    c.bo.assign(n_bins, 0);
+    c.bw.resize(n_bins);
+    c.bn.resize(n_bins);
+    c.bo.resize(n_bins);
     // on the copy stream when there is one (host reads; or S5 is still running), else on the
     // job's stream (creating a stream for three small copies costs more than it saves)
     cudaStream_t fs = j->cs ? j->cs : j->s;
@@ -1069,9 +1132,9 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
     cudaStream_t s = j->s;
     unsigned long long* hs = j->host_small;
     unsigned long long* gstats = c.gstats;
-    const std::vector<uint64_t>& bw = c.bw;
-    const std::vector<uint64_t>& bn = c.bn;
-    const std::vector<uint64_t>& bo = c.bo;
+    const HostTable& bw = c.bw;
+    const HostTable& bn = c.bn;
+    const HostTable& bo = c.bo;
     // digit target = kcap keys; regions 1.25x the mean + 256 (hashed digits are near-uniform,
     // but a k-mer of multiplicity m moves m keys at once: repeat families skew them).  C4
     // (tools/stage_run.py, target / kcap 0.6 .. 1.1): 62.4, 60.8, 60.1, 60.0, 59.9 ms/step,
@@ -1341,9 +1404,9 @@ void large_subsplit(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vec
     cudaStream_t s = j->s;
     unsigned long long* hs = j->host_small;
     unsigned long long* gstats = c.gstats;
-    const std::vector<uint64_t>& bw = c.bw;
-    const std::vector<uint64_t>& bn = c.bn;
-    const std::vector<uint64_t>& bo = c.bo;
+    const HostTable& bw = c.bw;
+    const HostTable& bn = c.bn;
+    const HostTable& bo = c.bo;
     const double target = std::max(1.0, (double)kcap);
     const uint32_t rpp = (uint32_t)subsplit_piece_records(k);
     const size_t nl = large_ids.size();
@@ -1576,9 +1639,9 @@ void count_phase(kmc_job* j, PlanCtx& c) {
     unsigned long long* hs = j->host_small;
     unsigned long long* gstats = c.gstats;
     const uint64_t n_bins = c.n_bins, n_windows = c.n_windows, n_records = c.n_records;
-    const std::vector<uint64_t>& bw = c.bw;
-    const std::vector<uint64_t>& bn = c.bn;
-    const std::vector<uint64_t>& bo = c.bo;
+    const HostTable& bw = c.bw;
+    const HostTable& bn = c.bn;
+    const HostTable& bo = c.bo;
     uint32_t* tmp_recs = c.tmp_recs;
     uint32_t* tmp_sig = c.tmp_sig;
     const uint64_t tmp_cap = c.tmp_cap;
@@ -1699,8 +1762,8 @@ void count_multipass(kmc_job* j, PlanCtx& c) {
     PlanArgs& pa = c.pa;
     release_plan_scratch(j, c);
     fetch_tables(j, c);
-    const std::vector<uint64_t>& bn = c.bn;
-    const std::vector<uint64_t>& bo = c.bo;
+    const HostTable& bn = c.bn;
+    const HostTable& bo = c.bo;
     const uint64_t n_bins = c.n_bins;
     // records per pass: the option, else a share of the free device memory (bins 16-32 B,
     // survivors up to 12-20 B per window / ci, the large-bin key regions are grouped anyway)
@@ -1763,9 +1826,9 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
     PlanArgs& pa = c.pa;
     unsigned long long* hs = j->host_small;
     unsigned long long* gstats = c.gstats;
-    const std::vector<uint64_t>& bw = c.bw;
-    const std::vector<uint64_t>& bn = c.bn;
-    const std::vector<uint64_t>& bo = c.bo;
+    const HostTable& bw = c.bw;
+    const HostTable& bn = c.bn;
+    const HostTable& bo = c.bo;
     // ---- host: classify bins (small: one CTA in SMEM; large: multi-CTA path)
     std::vector<uint32_t> small;
     std::vector<uint64_t> large_ids;
