@@ -363,6 +363,20 @@ struct HostTable {
     size_t size() const { return n; }
 };
 
+// An array of T in the same pinned pool (host tables copied to the device asynchronously:
+// the caller keeps it unchanged until the copy has completed).
+template <class T> struct PinnedArr {
+    HostTable raw;
+    size_t n = 0;
+    void resize(size_t m) {
+        raw.resize((m * sizeof(T) + 7) / 8 + 1);
+        n = m;
+    }
+    T* data() { return reinterpret_cast<T*>(raw.data()); }
+    T& operator[](size_t i) { return data()[i]; }
+    size_t size() const { return n; }
+};
+
 struct PlanCtx {
     PlanArgs pa{};
     uint64_t ns = 0, n_bins = 0, n_windows = 0, n_records = 0;
@@ -1273,6 +1287,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
         ar.release(rs.scan_temp);
         return;
     }
+    htrace("split1 plan");
     const size_t nl = ids.size();
     std::vector<uint32_t> nd(nl), rc(nl);
     uint64_t total = 0;
@@ -1299,6 +1314,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             budget = std::max<uint64_t>((uint64_t)(fr / 2) / 9, 1u << 20);
         }
     }
+    htrace("split1 keys allocated");
     std::vector<std::pair<size_t, size_t>> groups;
     uint64_t max_gk = 0, max_gd = 0, max_gp = 0, max_gn = 0;
     for (size_t i0 = 0; i0 < nl;) {
@@ -1333,14 +1349,18 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
     if (!lkeys) lkeys = ar.alloc(max_gk * 8 + chunk_key_slack_bytes());
     uint64_t ovf_cap = std::max<uint64_t>(1u << 20, max_gk / 32);
     uint64_t* ovf = ar.get<uint64_t>(ovf_cap);
-    static thread_local std::vector<LargeBin> lbins;
-    static thread_local std::vector<S1Bin> sbins;
-    static thread_local std::vector<uint64_t> pp;
+    htrace("split1 buffers");
+    // pinned: the table copies below are asynchronous (a group's copies have completed when
+    // the next group rewrites the tables -- every group ends with a stream synchronisation)
+    PinnedArr<LargeBin> lbins;
+    PinnedArr<S1Bin> sbins;
+    PinnedArr<uint64_t> pp;
     for (const auto& g : groups) {
         const size_t gn = g.second - g.first;
         lbins.resize(gn);
         sbins.resize(gn);
-        pp.assign(gn + 1, 0);
+        pp.resize(gn + 1);
+        pp[0] = 0;
         uint64_t key_base = 0, dbase = 0;
         for (size_t i = 0; i < gn; ++i) {
             const size_t li = g.first + i;
@@ -1351,7 +1371,8 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             dbase += nd[li];
             pp[i + 1] = pp[i] + (bn[b] + rpp - 1) / rpp;
         }
-        const uint64_t n_pieces = pp.back();
+        const uint64_t n_pieces = pp[gn];
+        htrace("split1 tables");
         CK(cudaMemcpyAsync(d_lbins, lbins.data(), gn * sizeof(LargeBin), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d_sbins, sbins.data(), gn * sizeof(S1Bin), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d_pp, pp.data(), pp.size() * 8, cudaMemcpyHostToDevice, s));
@@ -1832,6 +1853,8 @@ void count_bins(kmc_job* j, PlanCtx& c, uint32_t* bins, uint64_t b_lo, uint64_t 
     // ---- host: classify bins (small: one CTA in SMEM; large: multi-CTA path)
     std::vector<uint32_t> small;
     std::vector<uint64_t> large_ids;
+    small.reserve(b_hi - b_lo);
+    large_ids.reserve(b_hi - b_lo);
     uint64_t large_windows = 0, n_large = 0, max_bin = 0, range_windows = 0;
     for (uint64_t b = b_lo; b < b_hi; ++b) {
         if (bw[b] == 0) continue;
