@@ -353,6 +353,162 @@ int order_levels(uint64_t n, int k, int cap, int* D) {
     return L;
 }
 
+// A few counters straight into pinned (mapped) host memory: a read-back that does not queue
+// on the device-to-host copy engine behind the output copies of the groups before it.
+__global__ void k_counters_to_host(const unsigned long long* __restrict__ src, unsigned long long* dst, int n) {
+    if ((int)threadIdx.x < n) dst[threadIdx.x] = src[threadIdx.x];
+}
+
+// Host outputs (range_done, 64-bit keys): S9 depth first.  The top level partitions all
+// survivors; then the top buckets are taken in ORD_GROUPS groups of about n / ORD_GROUPS
+// survivors each, and every group runs its lower levels, its classification and its final
+// sorts on its own item range (tiles from the top-level starts, offset to the range).  The
+// caller's copy of a group's output can start after one pass over all survivors plus the
+// first group's work, and runs while the later groups are sorted (breadth first, every
+// level over all survivors came before the first copy).
+cudaError_t order_groups64(uint64_t* keys, uint32_t* vals, uint64_t n, int k, const int* D, int L,
+                           uint64_t* out_keys, uint32_t* out_vals, const OrderScratch& os, cudaStream_t s,
+                           int* launches, std::vector<OrderSegment>* oversize, void** seg_keys,
+                           uint32_t** seg_vals, const OrderRangeFn& range_done) {
+    using K = uint64_t;
+    constexpr uint64_t TI = OrderTile<K>::v;
+    const int twok = 2 * k;
+    const int osm = (int)otile_smem<K>();
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_ord_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, osm))) return e;
+    const size_t sm = order_smem<K>();
+    if ((e = cudaFuncSetAttribute(k_order_chunk_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
+    // one MSD level over items [0, m) of (kin, vin) into (kout, vout): tiles of src's nbk
+    // buckets, digit = the D_l bits below top; leaves the level's counts / starts in hist / start
+    auto level = [&](const TileSrc& src, uint64_t nbk, uint64_t m, int top, int Dl, const K* kin,
+                     const uint32_t* vin, K* kout, uint32_t* vout) -> cudaError_t {
+        const uint64_t mt = m / TI + nbk;
+        cudaError_t e2;
+        if ((e2 = launch_make_tiles(src, nbk, (uint32_t)TI, mt, os.tprefix, os.ttemp,
+                                    reinterpret_cast<RecTile2*>(os.tiles), s)))
+            return e2;
+        const uint64_t* ntl = os.tprefix + nbk;
+        const uint64_t nd = nbk << Dl;
+        if ((e2 = cudaMemsetAsync(os.hist, 0, nd * 4, s))) return e2;
+        k_ord_hist<K><<<(unsigned)mt, OT_NT, 0, s>>>(kin, os.tiles, ntl, top, Dl, os.hist);
+        if ((e2 = cudaGetLastError())) return e2;
+        if ((e2 = scan_detail::scan_generic<uint32_t>(scan_detail::ArrayIn<uint32_t>{os.hist}, nd, os.start,
+                                                      (uint32_t*)os.scan_temp, s, launches)))
+            return e2;
+        if ((e2 = cudaMemcpyAsync(os.cursor, os.start, nd * 4, cudaMemcpyDeviceToDevice, s))) return e2;
+        k_ord_scatter<K><<<(unsigned)mt, OT_NT, osm, s>>>(kin, vin, os.tiles, ntl, top, Dl, os.cursor, kout, vout);
+        *launches += 5;
+        return cudaGetLastError();
+    };
+    K* ck = keys;
+    uint32_t* cv = vals;
+    K* ok = (K*)os.tmp_keys;
+    uint32_t* ov = os.tmp_vals;
+    if ((e = level(TileSrc{nullptr, 0, 0, 0, n}, 1, n, twok, D[0], ck, cv, ok, ov))) return e;
+    std::swap(ck, ok);
+    std::swap(cv, ov);
+    const uint64_t nb0 = 1ull << D[0];
+    if ((e = cudaMemcpyAsync(os.start0, os.start, nb0 * 4, cudaMemcpyDeviceToDevice, s))) return e;
+    std::vector<uint32_t> h0(nb0 + 1);
+    if ((e = cudaMemcpyAsync(h0.data(), os.start, nb0 * 4, cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    h0[nb0] = (uint32_t)n;
+    // the group of every top bucket: about n / G survivors each
+    const uint64_t G = std::min<uint64_t>(ORD_GROUPS, nb0);
+    std::vector<uint64_t> B(G + 1, nb0);
+    B[0] = 0;
+    for (uint64_t g = 1, b = 0; g < G; ++g) {
+        while (b < nb0 && (uint64_t)h0[b] < g * n / G) ++b;
+        B[g] = std::max(b, B[g - 1]);
+    }
+    // after level 0 and L - 1 levels per group, every group's items are in the same buffer
+    K* fk = (L - 1) % 2 == 0 ? ck : ok;
+    uint32_t* fv = (L - 1) % 2 == 0 ? cv : ov;
+    uint2* wlist = reinterpret_cast<uint2*>(os.chunks);
+    Chunk* big = os.oversize;
+    Chunk* over = reinterpret_cast<Chunk*>(os.cursor);
+    unsigned long long* H = os.host;
+    constexpr int WPB = WS_NT / 32;
+    const int dir[4] = {1, -1, 1, -1};
+    const bool pack = twok <= 56;
+    oversize->clear();
+    // the counters of every group's classification reach the host through mapped memory
+    // written by a kernel, waited for with an event: a copy would wait behind the output
+    // copies of the previous groups on the copy engine (and the next group behind it)
+    cudaEvent_t ev = nullptr;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return e;
+    struct EvGuard {
+        cudaEvent_t e;
+        ~EvGuard() { cudaEventDestroy(e); }
+    } ev_guard{ev};
+    for (uint64_t g = 0; g < G; ++g) {
+        const uint64_t b0 = B[g], b1 = B[g + 1];
+        if (b1 <= b0) continue;
+        const uint64_t s0 = h0[b0], s1 = h0[b1], m = s1 - s0;
+        if (m == 0) continue;
+        K* ak = ck + s0;
+        uint32_t* av = cv + s0;
+        K* bk = ok + s0;
+        uint32_t* bv = ov + s0;
+        uint64_t nbk = b1 - b0;
+        int top = twok - D[0];
+        for (int l = 1; l < L; ++l) {
+            const TileSrc src = l == 1 ? TileSrc{os.start0 + b0, 0, nbk, 0, m, s0} : TileSrc{os.start, 0, nbk, 0, m};
+            if ((e = level(src, nbk, m, top, D[l], ak, av, bk, bv))) return e;
+            std::swap(ak, bk);
+            std::swap(av, bv);
+            top -= D[l];
+            nbk <<= D[l];
+        }
+        // the group's final buckets [0, nbk): counts in hist, starts (from s0) in start
+        if ((e = cudaMemsetAsync(os.counters, 0, 9 * 8, s))) return e;
+        k_ord_classify<<<(unsigned)((nbk + WS_NT - 1) / WS_NT), WS_NT, 0, s>>>(
+            os.hist, os.start, nbk, (uint32_t)m, OrderCap<K>::v, wlist, big, over, os.counters, 0, nbk,
+            os.counters + 8);
+        *launches += 1;
+        if ((e = cudaGetLastError())) return e;
+        k_counters_to_host<<<1, 32, 0, s>>>(os.counters, H, 9);
+        *launches += 1;
+        if ((e = cudaGetLastError())) return e;
+        if ((e = cudaEventRecord(ev, s))) return e;
+        if ((e = cudaEventSynchronize(ev))) return e;
+        const uint64_t nov = *(volatile unsigned long long*)&H[8];
+        bool has_over = false;
+        if (nov) {
+            std::vector<Chunk> ovs(nov);
+            if ((e = cudaMemcpyAsync(ovs.data(), over, nov * sizeof(Chunk), cudaMemcpyDeviceToHost, s))) return e;
+            if ((e = cudaStreamSynchronize(s))) return e;
+            for (auto& c : ovs) oversize->push_back(OrderSegment{s0 + c.begin, c.n});
+            has_over = true;
+        }
+        const uint64_t wn = nbk;
+        const uint2* wl[4] = {wlist, wlist + wn - 1, wlist + wn, wlist + 2 * wn - 1};
+        for (int q = 0; q < 4; ++q) {
+            const uint64_t nw = H[q];
+            if (!nw) continue;
+            const unsigned gr = (unsigned)((nw + WPB - 1) / WPB);
+#define KMC_WSORT(R)                                                                                               \
+    (pack ? k_ord_wsort<R, true><<<gr, WS_NT, 0, s>>>(ak, av, wl[q], nw, dir[q], out_keys + s0, out_vals + s0)      \
+          : k_ord_wsort<R, false><<<gr, WS_NT, 0, s>>>(ak, av, wl[q], nw, dir[q], out_keys + s0, out_vals + s0))
+            if (q == 0) KMC_WSORT(1);
+            if (q == 1) KMC_WSORT(2);
+            if (q == 2) KMC_WSORT(4);
+            if (q == 3) KMC_WSORT(8);
+#undef KMC_WSORT
+            *launches += 1;
+        }
+        if (H[4]) {
+            k_order_chunk_sort<K><<<(unsigned)H[4], OC_NT, sm, s>>>(ak, av, big, twok, out_keys + s0, out_vals + s0);
+            *launches += 1;
+        }
+        if ((e = cudaGetLastError())) return e;
+        range_done(s0, s1, !has_over);
+    }
+    *seg_keys = fk;
+    *seg_vals = fv;
+    return cudaSuccess;
+}
+
 template <class K>
 cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uint32_t* out_vals,
                     const OrderScratch& os, cudaStream_t s, int* launches, std::vector<OrderSegment>* oversize,
@@ -361,6 +517,10 @@ cudaError_t order_t(K* keys, uint32_t* vals, uint64_t n, int k, K* out_keys, uin
     const int twok = 2 * k;
     int D[4];
     const int L = order_levels(n, k, OrderCap<K>::v, D);
+    if constexpr (sizeof(K) == 8)
+        if (range_done && L >= 2 && os.start0)
+            return order_groups64(keys, vals, n, k, D, L, out_keys, out_vals, os, s, launches, oversize, seg_keys,
+                                  seg_vals, *range_done);
     cudaError_t e;
     const int osm = (int)otile_smem<K>();
     if ((e = cudaFuncSetAttribute(k_ord_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, osm))) return e;

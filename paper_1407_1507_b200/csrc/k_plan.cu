@@ -86,7 +86,7 @@ __device__ __forceinline__ uint64_t tile_src_start(const TileSrc& t, uint64_t b)
     if (!t.base) return b == 0 ? 0 : t.total;
     const uint64_t i = b << t.sh;
     if (i >= t.nbase) return t.total;
-    return t.is64 ? reinterpret_cast<const uint64_t*>(t.base)[i] : reinterpret_cast<const uint32_t*>(t.base)[i];
+    return (t.is64 ? reinterpret_cast<const uint64_t*>(t.base)[i] : reinterpret_cast<const uint32_t*>(t.base)[i]) - t.off;
 }
 
 __global__ void k_tile_count(TileSrc t, uint64_t nb, uint32_t TI, uint64_t* __restrict__ cnt) {

@@ -2377,6 +2377,7 @@ void run_finish(kmc_job* j, uint64_t* out_kmers, uint32_t* out_counts) {
     os.tmp_vals = ar.get<uint32_t>(n);
     os.scan_temp = ar.alloc(order_scan_temp_bytes(nd + 1));
     os.host = j->host_small + 56;
+    os.start0 = ar.get<uint32_t>(257);
     std::vector<OrderSegment> over;
     int sl = 0;
     j->stage_begin(KMC_STAGE_ORDER);

@@ -93,6 +93,7 @@ struct TileSrc {
     uint64_t nbase;
     int sh;
     uint64_t total;
+    uint64_t off = 0;  // subtracted from the base entries (tiles of a sub-range; total is relative)
 };
 cudaError_t launch_make_tiles(const TileSrc& src, uint64_t nb, uint32_t TI, uint64_t max_tiles, uint64_t* prefix,
                               void* temp, RecTile2* tiles, cudaStream_t s);
@@ -396,6 +397,7 @@ struct OrderScratch {
     uint32_t* tmp_vals;     // [n]
     void* scan_temp;        // order_scan_temp_bytes(2^(D1+D2) + 1)
     unsigned long long* host;  // pinned, >= 80 entries
+    uint32_t* start0 = nullptr;  // [257] top-level bucket starts (host outputs: S9 by groups)
 };
 struct OrderSegment {
     uint64_t begin, n;  // items of an oversize bucket in (*seg_keys, *seg_vals) after launch_order

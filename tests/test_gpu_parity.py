@@ -577,6 +577,19 @@ def test_multipass_host_input(gpu, name, scale, opts):
         assert res.stats[f] == getattr(ref, f), f
 
 
+def test_full_c4_host_buffers_digest(gpu):
+    """The bench's end-to-end call: host-resident C4 reads in, pinned host outputs out (S9's
+    groups sorted depth first and copied while the next group sorts) -- the oracle's digest."""
+    w = synth.make("C4")
+    rh = torch.from_numpy(w.reads).pin_memory()
+    oh = torch.from_numpy(w.offsets.view(np.uint64)).pin_memory()
+    res = gpu.count(rh, oh, w.k, w.p, w.cutoff_min, w.cutoff_max, out_device="cpu")
+    g = GOLD["C4"]
+    assert res.kmers.is_pinned() and res.counts.is_pinned()
+    assert res.stats["n_out"] == g["n_out"] and res.stats["n_unique"] == g["n_unique"]
+    assert oracle.digest(res.kmers.numpy(), res.counts.numpy()) == g["sha256"]
+
+
 def test_multipass_full_c4_digest(gpu):
     """The whole C4 read set (4 G bases, host-resident) counted in forced passes of <= 1 GiB of
     records gives exactly the oracle's digest (tests/golden/full_configs.json)."""
