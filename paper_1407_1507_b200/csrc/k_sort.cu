@@ -945,6 +945,7 @@ __global__ void k_digit_totals(const LargeBin* __restrict__ lbins, const uint32_
 __global__ void k_make_pieces(const LargeBin* __restrict__ lbins, const uint64_t* __restrict__ piece_prefix,
                               uint32_t rpp, Piece* __restrict__ pieces) {
     const LargeBin lb = lbins[blockIdx.x];
+    if (rpp == 0) rpp = lb.nseg;  // per-bin records per piece (k_split1 pieces sized by windows)
     const uint64_t p0 = piece_prefix[blockIdx.x], np = piece_prefix[blockIdx.x + 1] - p0;
     for (uint64_t j = threadIdx.x; j < np; j += blockDim.x) {
         const uint64_t r = j * rpp;

@@ -28,10 +28,7 @@ namespace kmc {
 namespace {
 
 constexpr int S1_NT = 512;
-#ifndef KMC_S1_REC
-#define KMC_S1_REC 448  // C4: 512 -> 14.5 ms, 464 -> 12.1, 448 -> 11.2, 416 -> 11.5 (pieces past the single-pass stage)
-#endif
-constexpr int S1_REC = KMC_S1_REC;  // records per piece at most
+constexpr int S1_REC = 512;       // records per piece at most (the piece buffers)
 constexpr int S1_UMAX = 7680;     // units per piece (umap entries)
 constexpr int S1_STAGE = 8192;    // keys staged per piece (+ one spare slot per digit)
 constexpr int S1_RBW = S1_REC * 4 + 8;
@@ -459,6 +456,25 @@ int split1_piece_records(int k) {
     const int U = std::min(S1_UNIT, 33 - k);
     const int upr = (record_max_windows(k) + U - 1) / U;
     return std::min(S1_REC, S1_UMAX / upr);
+}
+
+// Pieces of one records-per-piece for every bin (the presplit, whose bins' windows per record
+// are only estimates): 448 records.  C4, one size for all bins: 512 -> 14.5 ms, 464 -> 12.1,
+// 448 -> 11.2, 416 -> 11.5 (large-bin records average ~14 windows: bigger pieces often exceed
+// the single-pass stage and take the two-pass mode).
+int split1_uniform_records(int k) { return std::min(448, split1_piece_records(k)); }
+
+// Records per piece of a bin of W windows in R records split into nd digits: pieces of about
+// fill x the windows the single-pass mode takes (NWIN + NWIN / 8 + 16 nd <= S1_STAGE).
+#ifndef KMC_S1_FILL
+#define KMC_S1_FILL 0.80
+#endif
+int split1_bin_records(int k, uint64_t W, uint64_t R, uint32_t nd) {
+    const int cap = split1_piece_records(k);
+    if (W == 0 || R == 0) return cap;
+    const double win = ((double)S1_STAGE - 16.0 * nd) / 1.125 * KMC_S1_FILL;
+    const double r = win * (double)R / (double)W;
+    return (int)std::max(32.0, std::min((double)cap, r));
 }
 
 cudaError_t launch_split1(const uint32_t* bins, const Piece* pieces, uint64_t n_pieces, const S1Bin* sbins, int k,

@@ -1075,7 +1075,7 @@ void presplit_setup(kmc_job* j, PlanCtx& c, const std::vector<uint64_t>& bw, con
         pre.index[pre.ids[i]] = (int32_t)i;
         ids32[i] = (uint32_t)pre.ids[i];
     }
-    pre.rpp = (uint32_t)split1_piece_records(k);
+    pre.rpp = (uint32_t)split1_uniform_records(k);
     pre.d_ids = ar.get<uint32_t>(n);
     pre.d_sbins = ar.get<S1Bin>(n);
     pre.done = ar.get<uint32_t>(n);
@@ -1154,7 +1154,6 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
     // (tools/stage_run.py, target / kcap 0.6 .. 1.1): 62.4, 60.8, 60.1, 60.0, 59.9 ms/step,
     // overflow 6.0 M .. 0.4 M keys; bigger digits absorb pile-ups and need fewer reservations.
     const double target = std::max(1.0, (double)kcap);
-    const uint32_t rpp = (uint32_t)split1_piece_records(k);
     RadixScratch rs{};
     uint64_t rs_cap = 0;
     auto sort_rle = [&](uint64_t* keys, uint64_t n, int& nlaunch) {
@@ -1289,7 +1288,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
     }
     htrace("split1 plan");
     const size_t nl = ids.size();
-    std::vector<uint32_t> nd(nl), rc(nl);
+    std::vector<uint32_t> nd(nl), rc(nl), rpb(nl);
     uint64_t total = 0;
     for (size_t i = 0; i < nl; ++i) {
         const uint64_t b = ids[i];
@@ -1300,6 +1299,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
         r = std::min<uint64_t>((r + 1) & ~1ull, 0x7FFFFFFEull);
         nd[i] = (uint32_t)d;
         rc[i] = (uint32_t)r;
+        rpb[i] = (uint32_t)split1_bin_records(k, bw[b], bn[b], (uint32_t)d);  // pieces sized by windows
         total += d * r;
     }
     // group budget in region keys: the option, else everything if the key buffer can be
@@ -1325,7 +1325,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             if (i1 > i0 && gk + need > budget) break;
             gk += need;
             gd += nd[i1];
-            gp += (bn[ids[i1]] + rpp - 1) / rpp;
+            gp += (bn[ids[i1]] + rpb[i1] - 1) / rpb[i1];
             ++i1;
         }
         groups.push_back({i0, i1});
@@ -1365,11 +1365,11 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
         for (size_t i = 0; i < gn; ++i) {
             const size_t li = g.first + i;
             const uint64_t b = ids[li];
-            lbins[i] = LargeBin{0, 0, bo[b], 0, (uint32_t)bw[b], 0, (uint32_t)bn[b], 0, 0, 0};
+            lbins[i] = LargeBin{0, 0, bo[b], 0, (uint32_t)bw[b], 0, (uint32_t)bn[b], 0, rpb[li], 0};
             sbins[i] = S1Bin{key_base, nd[li], rc[li], (uint32_t)dbase, 0};
             key_base += (uint64_t)nd[li] * rc[li];
             dbase += nd[li];
-            pp[i + 1] = pp[i] + (bn[b] + rpp - 1) / rpp;
+            pp[i + 1] = pp[i] + (bn[b] + rpb[li] - 1) / rpb[li];
         }
         const uint64_t n_pieces = pp[gn];
         htrace("split1 tables");
@@ -1381,7 +1381,7 @@ void large_split1(kmc_job* j, PlanCtx& c, const uint32_t* bins, const std::vecto
             j->stage_begin(KMC_STAGE_LARGE_SCATTER);
             CK(cudaMemsetAsync(cur, 0, dbase * 4, s));
             CK(cudaMemsetAsync(ctr, 0, 40, s));
-            CK(launch_make_pieces(d_lbins, d_pp, gn, rpp, d_pieces, s));
+            CK(launch_make_pieces(d_lbins, d_pp, gn, 0, d_pieces, s));  // (rpp 0: LargeBin.nseg per bin)
             htrace("split1 launch");
             CK(launch_split1(bins, d_pieces, n_pieces, d_sbins, k, !j->opt.non_canonical, cur, (uint64_t*)lkeys, ovf,
                              ctr + 3, ovf_cap, 2 * n_sms(), s));

@@ -267,6 +267,8 @@ struct S1Bin {
     uint32_t nd, rc, dbase, flags;
 };
 int split1_piece_records(int k);
+int split1_uniform_records(int k);  // the presplit's records per piece
+int split1_bin_records(int k, uint64_t W, uint64_t R, uint32_t nd);  // per bin, sized by windows
 // cur: per-digit key counts (zeroed; may exceed rc: overflow); ovf_ctr: keys beyond their
 // region (written to ovf while below ovf_cap)
 // n_pieces_dev (optional): the piece count in device memory (pieces built on the device);
