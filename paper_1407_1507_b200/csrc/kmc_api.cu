@@ -754,7 +754,10 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
         //      batch's every step-th segment (host reads)
         // device reads: every 32nd segment; host reads: segments of the first batch, about one
         // in 16 of all segments (every one when the batch is <= 1/16 of the input)
-        uint32_t step = 32;
+#ifndef KMC_SAMPLE_STEP
+#define KMC_SAMPLE_STEP 32
+#endif
+        uint32_t step = KMC_SAMPLE_STEP;
         if (host_reads) {
             const uint64_t seg0 = p1_num_tiles(h_off[batches[0].second] - h_off[batches[0].first]);
             step = (uint32_t)std::max<uint64_t>(1, 16 * seg0 / std::max<uint64_t>(1, p1_num_tiles(n_bases)));
