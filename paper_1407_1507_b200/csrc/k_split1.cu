@@ -141,10 +141,6 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
             n = rec_nwin(Rp + tid * 4);
             nu = ((n + U - 1) * umagic) >> 16;
         }
-        if (bulk_pending) {  // the previous piece's stage has been read by its bulk copies
-            bulk_wait_read();
-            bulk_pending = false;
-        }
         if (tid < S1_DMAX) lc[tid] = 0;  // (the same thread read it last: the previous piece's W)
         if (tid == 0) novf = 0;
         uint32_t T;
@@ -153,6 +149,12 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
         T &= 0xFFFFu;
         for (uint32_t j = 0; j < nu; ++j) umap[pre + j] = (uint16_t)tid;
         if ((uint32_t)tid < pc.nrec) rinfo[tid] = pre | (n << 16);
+        // the previous piece's bulk copies have read the stage before anyone writes it again:
+        // their issuers wait here, so the copies overlap the block scan and the unit map
+        if (bulk_pending) {
+            bulk_wait_read();
+            bulk_pending = false;
+        }
         __syncthreads();
         // expansion of unit w: keys of windows first .. first + cnt - 1 of its record
         auto for_unit_keys = [&](uint32_t w, auto&& fn) {
