@@ -32,7 +32,10 @@ constexpr int S1_REC = 512;       // records per piece at most (the piece buffer
 constexpr int S1_UMAX = 7680;     // units per piece (umap entries)
 constexpr int S1_STAGE = 8192;    // keys staged per piece (+ one spare slot per digit)
 constexpr int S1_RBW = S1_REC * 4 + 8;
-constexpr int S1_UNIT = 5;        // windows per expansion unit at most (k + unit - 1 <= 32 symbols)
+#ifndef KMC_S1_UNIT
+#define KMC_S1_UNIT 5
+#endif
+constexpr int S1_UNIT = KMC_S1_UNIT;  // windows per expansion unit at most (k + unit - 1 <= 32 symbols)
 
 __device__ __forceinline__ uint32_t s1_digit(uint64_t key, uint32_t nd) {
     const uint32_t h = (((uint32_t)(key >> 32) * 0x85EBCA6Bu) ^ (uint32_t)key) * 0x9E3779B1u;
