@@ -536,6 +536,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
     const size_t ksz = kw == 1 ? 8 : 16;
     Arena& ar = j->arena;
     cudaStream_t s = j->s;
+    htrace("run_begin");
     j->host_small = pin_acquire();
     if (!j->host_small) {
         set_err("pinned readback buffer allocation failed");
@@ -549,6 +550,7 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
                 (unsigned long long)offN);
         throw Fail{KMC_ERR_INVALID_ARG};
     }
+    htrace("extent read");
     const uint64_t n_bases = offN - off0;
     j->st.n_bases = n_bases;
     if (n_bases == 0 || (uint64_t)k > n_bases) {
@@ -763,7 +765,9 @@ void run_begin(kmc_job* j, const uint8_t* reads, const uint64_t* offsets, uint64
             step = (uint32_t)std::max<uint64_t>(1, 16 * seg0 / std::max<uint64_t>(1, p1_num_tiles(n_bases)));
         }
         a.seg_step = step;
+        htrace("sample pass");
         const int nls = run_p1(P1_MODE_HIST, 1);
+        htrace("sample pass enqueued");
         a.seg_step = 1;
         j->launches += nls;
         const uint64_t seg_total = p1_num_tiles(n_bases);
