@@ -394,7 +394,7 @@ def main():
         r = e2e_step()
         n_out = r.stats["n_out"]
         del r
-        e_steps = max(1, min(args.steps, 3))
+        e_steps = max(1, min(args.steps, 5))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
