@@ -991,18 +991,22 @@ __global__ void __launch_bounds__(SB_NT, 2) k_chunk_sort(const K* __restrict__ k
 // chunk_hash_cap() keys but the table only ~3/4 of its slots in distinct keys: a probe
 // sequence longer than PROBE_MAX marks the chunk "overflowed" -- its partial counts are
 // dropped and the chunk is listed for the device radix-sort fallback.
-constexpr int CH_NT = 1024;
+#ifndef KMC_CH_NT
+#define KMC_CH_NT 1024
+#endif
+constexpr int CH_NT = KMC_CH_NT;        // threads per CTA; 1024 / CH_NT CTAs per SM
+constexpr int CH_CPS = 1024 / CH_NT;
 template <class K> struct HashCfg;
 // slots: a multiple of CH_NT, as many as shared memory holds (the slot of a key: its 32-bit
 // hash scaled to the table, so any size works).  C4: 16384 -> 18432 slots, with chunks
 // planned for them, 52.6 -> 52.35 ms/step
-template <> struct HashCfg<uint64_t> { static constexpr int slots = 18432; };
-template <> struct HashCfg<K128> { static constexpr int slots = 11264; };
+template <> struct HashCfg<uint64_t> { static constexpr int slots = 18 * CH_NT; };
+template <> struct HashCfg<K128> { static constexpr int slots = 11 * CH_NT; };
 
 template <class K> constexpr size_t chunk_hash_smem() { return (size_t)HashCfg<K>::slots * (sizeof(K) + 4); }
 
 template <class K>
-__global__ void __launch_bounds__(CH_NT, 1) k_chunk_hash(const K* __restrict__ keys, const Chunk* __restrict__ chunks,
+__global__ void __launch_bounds__(CH_NT, CH_CPS) k_chunk_hash(const K* __restrict__ keys, const Chunk* __restrict__ chunks,
                                                          uint32_t n_chunks, uint32_t ci, uint32_t cx, K* sk,
                                                          uint32_t* sc, unsigned long long* gstats,
                                                          Chunk* __restrict__ overflow,
@@ -1141,7 +1145,7 @@ cudaError_t launch_chunk_hash(const void* keys, const Chunk* chunks, uint64_t n_
                               Chunk* overflow, unsigned long long* n_overflow, int n_sms, cudaStream_t s) {
     if (n_chunks == 0) return cudaSuccess;
     if (n_chunks >= (1ull << 32)) return cudaErrorInvalidValue;
-    const unsigned grid = (unsigned)std::min<uint64_t>(n_chunks, (uint64_t)std::max(1, n_sms));
+    const unsigned grid = (unsigned)std::min<uint64_t>(n_chunks, (uint64_t)std::max(1, n_sms) * CH_CPS);
     cudaError_t e;
     if (k <= 32) {
         const size_t sm = chunk_hash_smem<uint64_t>();
