@@ -548,7 +548,11 @@ def main():
                                    f"histogram + all-to-all of super-k-mer records by bin owner")
                    if world > 1 else "1 GPU",
                    "count_path": ["smem_hash", "smem_radix_sort"][args.count_path],
-                   "l2": "inputs (4 GB) larger than L2 (126 MB); no flush needed"},
+                   "l2": "inputs (4 GB) larger than L2 (126 MB); no flush needed",
+                   # N > 1: the NCCL process group every rank joined (torch.distributed, one
+                   # process per GPU) and the record exchange the run used
+                   **({"comm_backend": dist.get_backend(), "comm_nranks": dist.get_world_size(),
+                       "exchange": xmode["mode"]} if world > 1 else {})},
         "kmers_per_s": windows_all / (ms / 1e3),
         "stats": {x: last[x] for x in ("n_windows", "n_superkmers", "n_records", "n_bins", "n_large_bins",
                                       "max_bin_windows", "large_windows", "n_unique", "n_out", "n_cluster_items",
