@@ -140,6 +140,19 @@ __global__ void k_tile_reads(const uint64_t* __restrict__ offsets, uint64_t n_re
     tile_r_lo[t] = lo;
 }
 
+// The same table from the reads' side: read r (0 <= r <= n_reads + 1) is the first read of
+// every tile whose left edge e_t = t SEG - HL satisfies O[r-1] <= e_t < O[r] (O[r] = offsets[r]
+// - off0, O[-1] = -inf, O[n_reads + 1] = +inf): exactly the binary search's answer.
+__global__ void k_tile_reads_by_read(const uint64_t* __restrict__ offsets, uint64_t n_reads, uint64_t off0,
+                                     uint64_t n_tiles, uint64_t* __restrict__ tile_r_lo) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > n_reads + 1) return;
+    // first tile: ceil((O[r-1] + HL) / SEG) (0 for r = 0); end: ceil((O[r] + HL) / SEG)
+    const uint64_t t0 = r == 0 ? 0 : (offsets[r - 1] - off0 + HL + SEG - 1) / SEG;
+    const uint64_t t1 = r == n_reads + 1 ? n_tiles : (offsets[r] - off0 + HL + SEG - 1) / SEG;
+    for (uint64_t t = t0; t < t1 && t < n_tiles; ++t) tile_r_lo[t] = r;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
     extern __shared__ __align__(16) uint8_t p1_smem[];
@@ -758,6 +771,16 @@ uint64_t p1_num_tiles(uint64_t n_bases) { return (n_bases + SEG - 1) / SEG; }
 cudaError_t launch_tile_reads(const uint64_t* offsets, uint64_t n_reads, uint64_t off0, uint64_t n_tiles,
                               uint64_t* tile_r_lo, cudaStream_t s) {
     if (n_tiles == 0) return cudaSuccess;
+    if (n_reads + 2 < (1ull << 31) * 256ull && n_reads > 0) {
+        // by read: one coalesced pass over the offsets instead of a binary search per tile
+        // (C4: 0.25 ms); tiles are zeroed first so that offsets that break the nondecreasing
+        // contract leave every tile with a valid first read
+        cudaError_t e = cudaMemsetAsync(tile_r_lo, 0, n_tiles * 8, s);
+        if (e) return e;
+        k_tile_reads_by_read<<<(unsigned)((n_reads + 2 + 255) / 256), 256, 0, s>>>(offsets, n_reads, off0, n_tiles,
+                                                                                   tile_r_lo);
+        return cudaGetLastError();
+    }
     k_tile_reads<<<(unsigned)((n_tiles + 255) / 256), 256, 0, s>>>(offsets, n_reads, off0, n_tiles, tile_r_lo);
     return cudaGetLastError();
 }
