@@ -59,9 +59,10 @@ template <bool PAIRED> struct S1Lay {  // the paired layout keeps one more per-d
 static_assert(S1_DMAX <= 512, "digit in 9 bits of an overflow entry");
 static_assert(S1_DMAX <= S1_NT, "one thread per digit");
 
-template <bool CANON, bool PAIRED>
+// KC: k as a compile-time constant (0: the argument); the window extraction shifts by 2k
+template <bool CANON, bool PAIRED, int KC = 0>
 __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict__ bins, const Piece* __restrict__ pieces,
-                                                     uint64_t n_pieces, const S1Bin* __restrict__ sbins, int k,
+                                                     uint64_t n_pieces, const S1Bin* __restrict__ sbins, int k_arg,
                                                      int unit, uint32_t* __restrict__ cur, uint64_t* __restrict__ keys,
                                                      uint64_t* __restrict__ ovf, unsigned long long* __restrict__ ovf_ctr,
                                                      uint64_t ovf_cap, const unsigned long long* __restrict__ n_pieces_dev,
@@ -83,7 +84,8 @@ __global__ void __launch_bounds__(S1_NT, 2) k_split1(const uint32_t* __restrict_
     __shared__ uint32_t wsumA[S1_NT / 32], wsumB[S1_NT / 32];  // alternating scan scratch
     __shared__ uint32_t novf;
     const int tid = threadIdx.x;
-    const int U = unit;
+    const int k = KC ? KC : k_arg;
+    const int U = KC ? (S1_UNIT < 33 - KC ? S1_UNIT : 33 - KC) : unit;
     const uint32_t R = gridDim.x, r = blockIdx.x;
     if (n_pieces_dev) n_pieces = *n_pieces_dev;
     const uint64_t p0 = (uint64_t)r * n_pieces / R, p1 = (uint64_t)(r + 1) * n_pieces / R;
@@ -499,11 +501,27 @@ cudaError_t launch_split1(const uint32_t* bins, const Piece* pieces, uint64_t n_
         return cudaSuccess;
     };
     cudaError_t e;
+#ifndef KMC_S1_KSPEC
+#define KMC_S1_KSPEC 1
+#endif
+    // canonical splits of the k-mer lengths of the paper's configurations (25, 28, 31) get
+    // instances with k folded into the window extraction; other k at run time
+    const int kc = KMC_S1_KSPEC && canonical && (k == 25 || k == 28 || k == 31) ? k : 0;
     if (paired) {
         if (!fail) return cudaErrorInvalidValue;
-        e = canonical ? go(k_split1<true, true>, S1Lay<true>::SMEM) : go(k_split1<false, true>, S1Lay<true>::SMEM);
+        const size_t sm = S1Lay<true>::SMEM;
+        e = kc == 25   ? go(k_split1<true, true, 25>, sm)
+            : kc == 28 ? go(k_split1<true, true, 28>, sm)
+            : kc == 31 ? go(k_split1<true, true, 31>, sm)
+            : canonical ? go(k_split1<true, true>, sm)
+                        : go(k_split1<false, true>, sm);
     } else {
-        e = canonical ? go(k_split1<true, false>, S1Lay<false>::SMEM) : go(k_split1<false, false>, S1Lay<false>::SMEM);
+        const size_t sm = S1Lay<false>::SMEM;
+        e = kc == 25   ? go(k_split1<true, false, 25>, sm)
+            : kc == 28 ? go(k_split1<true, false, 28>, sm)
+            : kc == 31 ? go(k_split1<true, false, 31>, sm)
+            : canonical ? go(k_split1<true, false>, sm)
+                        : go(k_split1<false, false>, sm);
     }
     if (e) return e;
     return cudaGetLastError();
