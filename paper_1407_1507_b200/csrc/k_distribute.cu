@@ -155,14 +155,14 @@ __global__ void k_tile_reads_by_read(const uint64_t* __restrict__ offsets, uint6
 
 // PC: the signature length as a compile-time constant (0: a.p at run time).  The p-mer keys
 // (phase C) shift and mask by p; the instances for the common lengths fold those constants.
-template <int MODE, int PC = 0>
+template <int MODE, int PC = 0, int KC = 0>
 __global__ void __launch_bounds__(SG_NT, 4) k_sig(P1Args a, uint64_t n_segs) {
     extern __shared__ __align__(16) uint8_t p1_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpSmem& S = reinterpret_cast<WarpSmem*>(p1_smem)[warp];
     const uint32_t ltm = lanemask_lt();
     const int64_t nb = (int64_t)a.n_bases;
-    const int k = a.k, p = PC ? PC : a.p, W = k - p + 1;
+    const int k = KC ? KC : a.k, p = PC ? PC : a.p, W = k - p + 1;  // (KC: with PC, the window length folds too)
     const int RW = record_words(k), maxw = record_max_windows(k);
     const uint32_t maxw_magic = ((1u << 20) + maxw - 1) / maxw;  // ceil(2^20 / maxw)
     const uint32_t RES = 1u << (2 * p);
@@ -751,18 +751,18 @@ __global__ void k_debug_allowed(int p, uint8_t* out) {
         out[i] = sig_allowed((uint32_t)i, p) ? 1 : 0;
 }
 
-template <int MODE, int PC> cudaError_t launch_sig_p(const P1Args& a, uint64_t n_segs, cudaStream_t s) {
+template <int MODE, int PC, int KC = 0> cudaError_t launch_sig_p(const P1Args& a, uint64_t n_segs, cudaStream_t s) {
     const int sm = (int)(sizeof(WarpSmem) * SG_WARPS);
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_sig<MODE, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+    if ((e = cudaFuncSetAttribute(k_sig<MODE, PC, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
     int dev = 0, nsm = 148, per = 1;
     if ((e = cudaGetDevice(&dev))) return e;
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sig<MODE, PC>, SG_NT, sm))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sig<MODE, PC, KC>, SG_NT, sm))) return e;
     const uint64_t n_iter = a.seg_step > 1 ? (n_segs + a.seg_step - 1) / a.seg_step : n_segs;
     const uint64_t want = (n_iter + SG_WARPS - 1) / SG_WARPS;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)nsm * std::max(1, per)));
-    k_sig<MODE, PC><<<grid, SG_NT, sm, s>>>(a, n_segs);
+    k_sig<MODE, PC, KC><<<grid, SG_NT, sm, s>>>(a, n_segs);
     return cudaGetLastError();
 }
 template <int MODE> cudaError_t launch_sig_t(const P1Args& a, uint64_t n_segs, cudaStream_t s) {
@@ -770,6 +770,14 @@ template <int MODE> cudaError_t launch_sig_t(const P1Args& a, uint64_t n_segs, c
 #define KMC_SIG_PSPEC 1
 #endif
     if (KMC_SIG_PSPEC && MODE != P1_MODE_DEBUG) {
+        // the (k, p) pairs of the paper's configurations fold the window length as well
+#ifndef KMC_SIG_KSPEC
+#define KMC_SIG_KSPEC 1
+#endif
+        if (KMC_SIG_KSPEC && a.k == 25 && a.p == 7) return launch_sig_p<MODE, 7, 25>(a, n_segs, s);
+        if (KMC_SIG_KSPEC && a.k == 28 && a.p == 9) return launch_sig_p<MODE, 9, 28>(a, n_segs, s);
+        if (KMC_SIG_KSPEC && a.k == 31 && a.p == 9) return launch_sig_p<MODE, 9, 31>(a, n_segs, s);
+        if (KMC_SIG_KSPEC && a.k == 55 && a.p == 11) return launch_sig_p<MODE, 11, 55>(a, n_segs, s);
         switch (a.p) {  // the signature lengths of the paper's configurations (7, 9, 11)
             case 7: return launch_sig_p<MODE, 7>(a, n_segs, s);
             case 9: return launch_sig_p<MODE, 9>(a, n_segs, s);
