@@ -8,7 +8,7 @@ timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
   --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-sort-path > $OUT/ncu_bench.log 2>&1; echo "ncu list rc $?"
 # k_sig: the scatter pass (k_sig<1>), not the sample pass (k_sig<0>)
-timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:k_sig<\(int\)1>" -c 1 -f -o $OUT/full_k_sig \
+timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:k_sig<\(int\)1" -c 1 -f -o $OUT/full_k_sig \
   python tools/profile_run.py C4 1.0 1 > $OUT/full_k_sig.log 2>&1; echo "ncu k_sig rc $?"
 for kr in k_split1 k_chunk_hash; do
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:$kr -c 1 -f -o $OUT/full_$kr \
